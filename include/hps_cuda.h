@@ -1,0 +1,154 @@
+/* hps_cuda.h -- C-ABI of the B200-native HPS fast direct solver (libhps_b200.so).
+ *
+ * Drop-in boundary for the reference's HpsSolver<Real> DtN path
+ * (/root/reference/proj/include/hps/solver.hpp:40-117).  Plain C types only:
+ * host pointers, sizes and int status codes; no CUDA or torch types.  Each entry
+ * point names the reference interface it replaces.
+ *
+ * Conventions (identical to the reference):
+ *   - matrices are column-major (proj/include/hps/core.hpp:17);
+ *   - leaves are in depth-first order (proj/src/mesh.cpp:54-71), points of a leaf
+ *     in tensor order i1*p+i2 (3D (i1*p+i2)*p+i3) with axis node k at
+ *     cheb_lobatto_1d(p)[k], descending (proj/include/hps/spectral.hpp:36-37);
+ *   - boundary vectors are in the canonical section order of
+ *     HpsSolver::root_boundary_points (proj/src/solver.cpp:159-182);
+ *   - node ids follow build_uniform_tree's construction order (proj/src/mesh.cpp:113-118).
+ *   - solution arrays are leaf-major, point-minor (SPEC.md:438 dump order); with
+ *     nrhs > 1 the right-hand side index is outermost.
+ */
+#ifndef HPS_CUDA_H
+#define HPS_CUDA_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (hps::Error in the reference, proj/include/hps/core.hpp:27-35) */
+enum {
+  HPSG_OK = 0,
+  HPSG_ERR_INVALID = 1,        /* bad argument / unsupported configuration (reference: require()) */
+  HPSG_ERR_SINGULAR_LEAF = 2,  /* "local_solve_dtn: singular factorization (zero pivot at i)", local_solve.cpp:96-101 */
+  HPSG_ERR_SINGULAR_MERGE = 3, /* "merge_dtn: singular interface matrix D (pivot i)", merge.cpp:281-288 */
+  HPSG_ERR_NONFINITE = 4,      /* "discretize_operator: non-finite coefficient sample ...", local_solve.cpp:56-61 */
+  HPSG_ERR_OOM = 5,
+  HPSG_ERR_CUDA = 6,
+  HPSG_ERR_STATE = 7,          /* call order (e.g. solve before build) */
+  HPSG_ERR_NO_DEVICE = 8       /* no CUDA device: the product never falls back to the CPU */
+};
+
+/* coefficient / source field descriptors.  The reference takes
+ * std::function<Real(const Point&)> evaluated on the host per point
+ * (proj/include/hps/local_solve.hpp:17-23, solver.hpp:43-45); here a field is
+ * either a built-in closed form evaluated on the device, or host samples
+ * (HPSG_FIELD_SAMPLED, samples[leaf * p^dim + pt]) for arbitrary functions. */
+enum {
+  HPSG_FIELD_CONST = 0,          /* c0 */
+  HPSG_FIELD_BUMPS = 1,          /* c0 + c1 * sum_j exp(-c2 |x - z_j|^2) */
+  HPSG_FIELD_PLANE_SIN = 2,      /* c0 * sin(c1 x1 + c2 x2 + c3 x3 + c4) */
+  HPSG_FIELD_PLANE_COS = 3,      /* c0 * cos(c1 x1 + c2 x2 + c3 x3 + c4) */
+  HPSG_FIELD_BUMPS_SIN = 4,      /* c0 * sum_j exp(-c2 |x-z_j|^2) * sin(c3 x1 + c4 x2 + c5 x3 + c6) */
+  HPSG_FIELD_POISSON2D_SRC = 5,  /* source of make_manufactured_2d_dtn, proj/src/problems.cpp:62-66 */
+  HPSG_FIELD_SAMPLED = 6
+};
+typedef struct {
+  int kind;
+  int n_centers;
+  double c[8];
+  const double* centers; /* n_centers x 3 (host) */
+  const double* samples; /* n_leaves x p^dim (host), for HPSG_FIELD_SAMPLED */
+} hpsg_field;
+
+/* CoefficientField (proj/include/hps/local_solve.hpp:17-23) */
+enum { HPSG_ROLE_LAPLACIAN = 0, HPSG_ROLE_GRADIENT = 1, HPSG_ROLE_ZEROTH = 2, HPSG_ROLE_SECOND_ORDER = 3 };
+typedef struct {
+  int role;
+  int axis, axis2;
+  hpsg_field field;
+} hpsg_term;
+
+/* uniform quad/octree: build_uniform_tree(domain, L, dim, p), proj/src/mesh.cpp:90-121 */
+typedef struct {
+  int dim;        /* 2 or 3 */
+  int p;          /* Chebyshev points per axis; q = p - 2 Gauss points per panel */
+  int L;          /* depth (>= 1) */
+  double lo, hi;  /* domain [lo,hi]^dim */
+} hpsg_tree;
+
+typedef struct {
+  int literal_sign;     /* 1: reference convention v_i = -L_ii^-1 f_i (local_solve.cpp:137); 0: corrected (+) */
+  int root_implicit_S;  /* MergeOptions::implicit_S at the root (merge.hpp:104, solver.cpp:104) */
+  int device;           /* CUDA device ordinal */
+  int reserved;
+} hpsg_options;
+
+typedef struct {
+  int n_leaves;
+  long long n_points;          /* N = n_leaves * p^dim */
+  int root_bsize;              /* length of the root boundary vector */
+  int top_D_size;              /* HpsSolver::top_D_size (solver.cpp:321-324) */
+  int tree_depth;
+  double min_rcond;            /* min over leaves of min|u_ii|/max|u_ii| (local_solve.cpp:103-106) */
+  int ill_conditioned;         /* any_ill_conditioned (solver.hpp:92) */
+  double t_build_ms, t_leaf_ms, t_merge_ms, t_solve_ms;   /* last build / solve, CUDA events */
+  double build_flops;          /* counted algorithmic FLOPs of the build (SURVEY 8d formulas) */
+  double solve_bytes;          /* algorithmic HBM bytes of the last solve */
+  double device_bytes;         /* device memory held by the context */
+  int launches_build, launches_solve; /* kernels launched by the last build / solve */
+} hpsg_stats;
+
+typedef struct hpsg_ctx hpsg_ctx;
+
+/* HpsSolver<Real>(tree, Variant::dtn, eta, terms, source, opts), solver.hpp:43-45 */
+int hpsg_create(const hpsg_tree* tree, const hpsg_term* terms, int n_terms, const hpsg_field* source,
+                const hpsg_options* opts, hpsg_ctx** out);
+/* HpsSolver::build(), solver.hpp:48 / solver.cpp:144-151: leaf stage + all merge levels */
+int hpsg_build(hpsg_ctx* ctx);
+/* HpsSolver::solve(g_root, leaf_g_out), solver.hpp:64 / solver.cpp:238-252, for nrhs boundary
+ * vectors (g_root: nrhs x root_bsize).  u_out: nrhs x n_leaves x p^dim (host);
+ * leaf_g_out (optional): nrhs x n_leaves x (boundary Gauss points of a leaf). */
+int hpsg_solve(hpsg_ctx* ctx, const double* g_root, int nrhs, double* u_out, double* leaf_g_out);
+/* same with device pointers (no host copies); results are ready when the call returns */
+int hpsg_solve_device(hpsg_ctx* ctx, const double* d_g_root, int nrhs, double* d_u_out);
+/* HpsSolver::root_boundary_points(), solver.hpp:60 (root_bsize x 3) */
+int hpsg_root_boundary_points(hpsg_ctx* ctx, double* xyz);
+/* leaf_cheb_points over all leaves, mesh.hpp:73-74 (n_leaves x p^dim x 3) */
+int hpsg_leaf_points(hpsg_ctx* ctx, double* xyz);
+/* LeafSolution<Real> of leaf `ord` (local_solve.hpp:30-39): Y (p^d x nb), v (p^d), T (nb x nb), h (nb) */
+int hpsg_get_leaf(hpsg_ctx* ctx, int ord, double* Y, double* v, double* T, double* h);
+/* MergeArtifact sizes of an internal node (merge.hpp:58-64) */
+int hpsg_node_sizes(hpsg_ctx* ctx, int node_id, int* n_ext, int* n_int);
+/* MergeArtifact S_mat (n_int x n_ext), gtilde (n_int) and node_T/node_h (n_ext^2, n_ext) of a
+ * non-root internal node (solver.hpp:83-85).  Any pointer may be NULL. */
+int hpsg_get_node(hpsg_ctx* ctx, int node_id, double* S, double* gtilde, double* T, double* h);
+int hpsg_get_stats(hpsg_ctx* ctx, hpsg_stats* out);
+const char* hpsg_last_error(hpsg_ctx* ctx);
+void hpsg_destroy(hpsg_ctx* ctx);
+
+/* centers of the seeded Gaussian-bump fields: std::mt19937_64(seed) with
+ * uniform_real_distribution(-0.5, 0.5), as make_scattering / make_pb_spec draw them
+ * (proj/src/problems.cpp:126-141, :240-249).  out: n x 3 (z = 0 in 2D). */
+void hpsg_bump_centers(unsigned long long seed, int n, int dim, double* out);
+
+/* library-level probes */
+int hpsg_device_count(void);
+const char* hpsg_build_info(void);
+
+/* Batched primitives on DEVICE pointers (column-major, strided batches; used by the
+ * kernel-level parity tests).  They replace the Eigen calls inside the hot path:
+ *   hpsg_dev_dgemm     : D = alpha*A*B + beta*C          (Eigen products, merge.cpp:294-295)
+ *   hpsg_dev_getrf_aug : PartialPivLU of M[:, :n] and M[:, n:n+m] <- A^-1 M[:, n:n+m]
+ *                        (local_solve.cpp:125-137, merge.cpp:280-292); ipiv 0-based,
+ *                        stats = (min|u_ii|, max|u_ii|, first zero pivot or -1) per matrix
+ *   hpsg_dev_getrs     : R <- A^-1 R with stored factors (MergeArtifact::apply_Dinv, merge.cpp:156-174) */
+int hpsg_dev_dgemm(int m, int n, int k, int batch, double alpha, const double* A, long long lda, long long sA,
+                   const double* B, long long ldb, long long sB, double beta, const double* C, long long ldc,
+                   long long sC, double* D, long long ldd, long long sD);
+int hpsg_dev_getrf_aug(int batch, int n, int m, double* M, long long ld, long long stride, int* ipiv,
+                       double* stats);
+int hpsg_dev_getrs(int batch, int n, int m, const double* LU, long long ld, long long stride, const int* ipiv,
+                   double* R, long long ldr, long long strideR);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HPS_CUDA_H */

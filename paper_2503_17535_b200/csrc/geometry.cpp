@@ -1,0 +1,447 @@
+// geometry.cpp -- host precompute for the B200 HPS solver (see geometry.hpp).
+#include "geometry.hpp"
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <functional>
+#include <stdexcept>
+
+namespace hpsg {
+
+std::string fmt(const char* f, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, f);
+  vsnprintf(buf, sizeof buf, f, ap);
+  va_end(ap);
+  return buf;
+}
+
+static const int kChildOffset[8][3] = {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {0, 1, 0},
+                                       {0, 0, 1}, {1, 0, 1}, {1, 1, 1}, {0, 1, 1}};
+
+// Chebyshev-Lobatto nodes, descending, antisymmetric by construction (spectral.cpp:14-26).
+std::vector<double> cheb_nodes(int p) {
+  const int n = p - 1;
+  std::vector<double> x(p);
+  for (int k = 0; k <= n / 2; ++k) {
+    const double v = std::sin(M_PI * (n - 2 * k) / (2.0 * n));
+    x[k] = v;
+    x[n - k] = -v;
+  }
+  if (n % 2 == 0) x[n / 2] = 0.0;
+  return x;
+}
+
+// Gauss-Legendre by Newton on the three-term recurrence (spectral.cpp:51-85).
+void gauss_rule(int q, std::vector<double>& xs, std::vector<double>& ws) {
+  xs.assign(q, 0.0);
+  ws.assign(q, 0.0);
+  for (int i = 0; i < (q + 1) / 2; ++i) {
+    double x = std::cos(M_PI * (i + 0.75) / (q + 0.5)), dp = 0.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = x;
+      for (int k = 2; k <= q; ++k) {
+        const double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      const double pq = q == 1 ? x : p1;
+      dp = q == 1 ? 1.0 : q * (x * pq - p0) / (x * x - 1.0);
+      const double dx = pq / dp;
+      x -= dx;
+      if (std::fabs(dx) < 1e-15) break;
+    }
+    if (q == 1) x = 0.0;
+    const double w = q == 1 ? 2.0 : 2.0 / ((1.0 - x * x) * dp * dp);
+    xs[i] = -x;
+    xs[q - 1 - i] = x;
+    ws[i] = ws[q - 1 - i] = w;
+  }
+  if (q % 2 == 1) xs[q / 2] = 0.0;
+}
+
+// Chebyshev differentiation with the negative-sum diagonal (spectral.cpp:87-103).
+HostMat cheb_diff(int p) {
+  const std::vector<double> x = cheb_nodes(p);
+  HostMat d(p, p);
+  for (int i = 0; i < p; ++i) {
+    const double ci = (i == 0 || i == p - 1) ? 2.0 : 1.0;
+    double sum = 0.0;
+    for (int j = 0; j < p; ++j) {
+      if (j == i) continue;
+      const double cj = (j == 0 || j == p - 1) ? 2.0 : 1.0;
+      d(i, j) = (ci / cj) * (((i + j) % 2 == 0) ? 1.0 : -1.0) / (x[i] - x[j]);
+      sum += d(i, j);
+    }
+    d(i, i) = -sum;
+  }
+  return d;
+}
+
+// Barycentric Lagrange interpolation src -> dst (spectral.cpp:105-137).
+HostMat bary_interp(const std::vector<double>& src, const std::vector<double>& dst) {
+  const int n = int(src.size()), m = int(dst.size());
+  std::vector<double> w(n);
+  for (int j = 0; j < n; ++j) {
+    double prod = 1.0;
+    for (int k = 0; k < n; ++k)
+      if (k != j) prod *= src[j] - src[k];
+    w[j] = 1.0 / prod;
+  }
+  HostMat out(m, n);
+  for (int i = 0; i < m; ++i) {
+    int hit = -1;
+    for (int j = 0; j < n && hit < 0; ++j)
+      if (dst[i] == src[j]) hit = j;
+    if (hit >= 0) {
+      out(i, hit) = 1.0;
+      continue;
+    }
+    double den = 0.0;
+    for (int j = 0; j < n; ++j) den += w[j] / (dst[i] - src[j]);
+    for (int j = 0; j < n; ++j) out(i, j) = (w[j] / (dst[i] - src[j])) / den;
+  }
+  return out;
+}
+
+static HostMat matmul(const HostMat& a, const HostMat& b) {
+  HostMat c(a.r, b.c);
+  for (int j = 0; j < b.c; ++j)
+    for (int k = 0; k < a.c; ++k) {
+      const double bk = b(k, j);
+      if (bk == 0.0) continue;
+      for (int i = 0; i < a.r; ++i) c(i, j) += a(i, k) * bk;
+    }
+  return c;
+}
+
+LeafOperators make_leaf_operators(int dim, int p, double side) {
+  if (dim != 2 && dim != 3) throw std::runtime_error("make_leaf_operators: dim must be 2 or 3");
+  if (p < 4) throw std::runtime_error("make_leaf_operators: p must be >= 4");
+  LeafOperators op;
+  op.dim = dim;
+  op.p = p;
+  op.q = p - 2;
+  op.side = side;
+  const int q = op.q;
+  op.n = dim == 2 ? p * p : p * p * p;
+  // interior / exterior tensor indices, increasing (spectral.cpp:139-160)
+  for (int idx = 0; idx < op.n; ++idx) {
+    int c[3] = {idx / p, idx % p, 0};
+    if (dim == 3) c[0] = idx / (p * p), c[1] = (idx / p) % p, c[2] = idx % p;
+    bool bnd = false;
+    for (int a = 0; a < dim; ++a) bnd = bnd || c[a] == 0 || c[a] == p - 1;
+    (bnd ? op.exterior : op.interior).push_back(idx);
+  }
+  op.ni = int(op.interior.size());
+  op.ne = int(op.exterior.size());
+  op.nb = dim == 2 ? 4 * q : 6 * q * q;
+
+  const std::vector<double> cn = cheb_nodes(p);
+  std::vector<double> gx, gw;
+  gauss_rule(q, gx, gw);
+  op.D = cheb_diff(p);
+  op.D2 = matmul(op.D, op.D);
+  const double ds = 2.0 / side;
+  const std::vector<double> cheb_up(cn.rbegin(), cn.rend());
+  const HostMat c2g = bary_interp(cheb_up, gx);  // q x p, ascending Chebyshev -> Gauss
+
+  op.P = HostMat(op.ne, op.nb);
+  op.Q = HostMat(op.nb, op.n);
+  if (dim == 2) {
+    // side s: normal axis, outward sign, Chebyshev node on the normal axis (spectral.cpp:172-188)
+    const int nax[4] = {1, 0, 1, 0};
+    const double sgn[4] = {-1, 1, 1, -1};
+    const int fixed[4] = {p - 1, 0, 0, p - 1};
+    for (int r = 0; r < op.ne; ++r) {
+      const int i1 = op.exterior[r] / p, i2 = op.exterior[r] % p;
+      int own[2], no = 0;
+      if (i2 == p - 1) own[no++] = 0;
+      if (i1 == 0) own[no++] = 1;
+      if (i2 == 0) own[no++] = 2;
+      if (i1 == p - 1) own[no++] = 3;
+      for (int o = 0; o < no; ++o) {
+        const int s = own[o];
+        const double t = nax[s] == 0 ? cn[i2] : cn[i1];
+        const HostMat row = bary_interp(gx, {t});
+        for (int j = 0; j < q; ++j) op.P(r, s * q + j) += (1.0 / no) * row(0, j);
+      }
+    }
+    for (int s = 0; s < 4; ++s) {
+      HostMat ns(p, op.n);
+      for (int r = 0; r < p; ++r) {
+        const int run = p - 1 - r;
+        for (int k = 0; k < p; ++k) {
+          const int col = nax[s] == 0 ? k * p + run : run * p + k;
+          ns(r, col) += sgn[s] * op.D(fixed[s], k);
+        }
+      }
+      const HostMat blk = matmul(c2g, ns);
+      for (int i = 0; i < q; ++i)
+        for (int j = 0; j < op.n; ++j) op.Q(s * q + i, j) = ds * blk(i, j);
+    }
+  } else {
+    auto face = [&](int f, int& axis, double& sg, int& fixed_node, int& ua, int& va) {
+      axis = f / 2;
+      sg = (f % 2 == 0) ? -1.0 : 1.0;
+      fixed_node = (f % 2 == 0) ? p - 1 : 0;
+      ua = axis == 0 ? 1 : 0;
+      va = axis == 2 ? 1 : 2;
+    };
+    for (int r = 0; r < op.ne; ++r) {
+      const int idx = op.exterior[r];
+      const int ijk[3] = {idx / (p * p), (idx / p) % p, idx % p};
+      int own[3], no = 0;
+      for (int a = 0; a < 3; ++a) {
+        if (ijk[a] == p - 1) own[no++] = 2 * a;
+        if (ijk[a] == 0) own[no++] = 2 * a + 1;
+      }
+      for (int o = 0; o < no; ++o) {
+        int axis, fx, ua, va;
+        double sg;
+        face(own[o], axis, sg, fx, ua, va);
+        const HostMat ru = bary_interp(gx, {cn[ijk[ua]]}), rv = bary_interp(gx, {cn[ijk[va]]});
+        for (int a = 0; a < q; ++a)
+          for (int b = 0; b < q; ++b) op.P(r, own[o] * q * q + a * q + b) += (1.0 / no) * ru(0, a) * rv(0, b);
+      }
+    }
+    HostMat fi(q * q, p * p);  // kron(c2g, c2g)
+    for (int a = 0; a < q; ++a)
+      for (int b = 0; b < q; ++b)
+        for (int i = 0; i < p; ++i)
+          for (int j = 0; j < p; ++j) fi(a * q + b, i * p + j) = c2g(a, i) * c2g(b, j);
+    for (int f = 0; f < 6; ++f) {
+      int axis, fx, ua, va;
+      double sg;
+      face(f, axis, sg, fx, ua, va);
+      HostMat nf(p * p, op.n);
+      for (int ru = 0; ru < p; ++ru)
+        for (int rv = 0; rv < p; ++rv)
+          for (int k = 0; k < p; ++k) {
+            int id[3];
+            id[axis] = k;
+            id[ua] = p - 1 - ru;
+            id[va] = p - 1 - rv;
+            nf(ru * p + rv, (id[0] * p + id[1]) * p + id[2]) += sg * op.D(fx, k);
+          }
+      const HostMat blk = matmul(fi, nf);
+      for (int i = 0; i < q * q; ++i)
+        for (int j = 0; j < op.n; ++j) op.Q(f * q * q + i, j) = ds * blk(i, j);
+    }
+  }
+  op.Qi = HostMat(op.nb, op.ni);
+  HostMat Qe(op.nb, op.ne);
+  for (int i = 0; i < op.nb; ++i) {
+    for (int j = 0; j < op.ni; ++j) op.Qi(i, j) = op.Q(i, op.interior[j]);
+    for (int j = 0; j < op.ne; ++j) Qe(i, j) = op.Q(i, op.exterior[j]);
+  }
+  op.QeP = matmul(Qe, op.P);
+  return op;
+}
+
+long long UniformTree::level_first_id(int d) const {
+  long long id = 0, cnt = 1;
+  for (int k = 0; k < d; ++k) id += cnt, cnt *= nchild;
+  return id;
+}
+long long UniformTree::level_count(int d) const {
+  long long c = 1;
+  for (int k = 0; k < d; ++k) c *= nchild;
+  return c;
+}
+
+UniformTree make_uniform_tree(int dim, int p, int L, double lo, double hi) {
+  if (!(hi > lo)) throw std::runtime_error("build_uniform_tree: empty domain");
+  UniformTree t;
+  t.dim = dim;
+  t.p = p;
+  t.q = p - 2;
+  t.L = L;
+  t.lo = lo;
+  t.hi = hi;
+  t.nchild = dim == 2 ? 4 : 8;
+  t.nface = 2 * dim;
+  const long long nl = t.level_count(L);
+  t.leaf_lo.assign(size_t(nl) * 6, 0.0);  // lo[3], hi[3] per leaf
+  for (long long o = 0; o < nl; ++o) {
+    double blo[3] = {lo, lo, dim == 3 ? lo : 0.0}, bhi[3] = {hi, hi, dim == 3 ? hi : 0.0};
+    long long div = nl;
+    for (int l = 0; l < L; ++l) {
+      div /= t.nchild;
+      const int c = int((o / div) % t.nchild);
+      for (int k = 0; k < dim; ++k) {
+        const double mid = 0.5 * (blo[k] + bhi[k]);  // repeated midpoint split, as mesh.cpp:31-43
+        if (kChildOffset[c][k])
+          blo[k] = mid;
+        else
+          bhi[k] = mid;
+      }
+    }
+    for (int k = 0; k < 3; ++k) t.leaf_lo[size_t(o) * 6 + k] = blo[k], t.leaf_lo[size_t(o) * 6 + 3 + k] = bhi[k];
+  }
+  t.leaf_side = (hi - lo) / double(1LL << L);
+  return t;
+}
+
+namespace {
+struct Iface {
+  int clo, flo, chi, fhi;
+};
+const std::vector<Iface>& ifaces(int dim) {
+  // proj/src/merge.cpp:20-33
+  static const std::vector<Iface> i2 = {{0, 1, 1, 3}, {1, 2, 2, 0}, {3, 1, 2, 3}, {0, 2, 3, 0}};
+  static const std::vector<Iface> i3 = {{0, 1, 1, 0}, {1, 3, 2, 2}, {3, 1, 2, 0}, {0, 3, 3, 2},
+                                        {4, 1, 5, 0}, {5, 3, 6, 2}, {7, 1, 6, 0}, {4, 3, 7, 2},
+                                        {0, 5, 4, 4}, {1, 5, 5, 4}, {2, 5, 6, 4}, {3, 5, 7, 4}};
+  return dim == 2 ? i2 : i3;
+}
+// exterior position (parent face, quadrant) of a child face, or -1 (merge.cpp:41-56)
+int ext_qpos(int dim, int c, int f) {
+  const int* off = kChildOffset[c];
+  if (dim == 2) {
+    const int axis = (f == 1 || f == 3) ? 0 : 1, high = (f == 1 || f == 2) ? 1 : 0;
+    if (off[axis] != high) return -1;
+    return off[axis == 0 ? 1 : 0];
+  }
+  const int axis = f / 2, high = f % 2;
+  if (off[axis] != high) return -1;
+  const int ua = axis == 0 ? 1 : 0, va = axis == 2 ? 1 : 2;
+  return off[ua] * 2 + off[va];
+}
+}  // namespace
+
+MergeTables make_merge_tables(int dim, int s) {
+  MergeTables m;
+  m.dim = dim;
+  m.s = s;
+  m.nchild = dim == 2 ? 4 : 8;
+  m.nface = 2 * dim;
+  const int nquad = dim == 2 ? 2 : 4;
+  const auto& ifs = ifaces(dim);
+  m.NI = int(ifs.size());
+  m.NE = m.nface * nquad;
+  m.sec.assign(m.nchild * m.nface, 0);
+  for (int c = 0; c < m.nchild; ++c)
+    for (int f = 0; f < m.nface; ++f) {
+      const int qp = ext_qpos(dim, c, f);
+      if (qp >= 0) {
+        m.sec[c * m.nface + f] = f * nquad + qp;
+      } else {
+        int t = -1;
+        for (int k = 0; k < m.NI; ++k)
+          if ((ifs[k].clo == c && ifs[k].flo == f) || (ifs[k].chi == c && ifs[k].fhi == f)) t = k;
+        if (t < 0) throw std::runtime_error("make_merge_tables: unmatched face");
+        m.sec[c * m.nface + f] = -t - 1;
+      }
+    }
+  const int mdc = m.NI + 1 + m.NE, ahc = 1 + m.NE;
+  m.md_src.assign(m.NI * mdc * 2, -1);
+  m.b_src.assign(m.NE * m.NI * 2, -1);
+  m.ah_src.assign(m.NE * ahc * 2, -1);
+  auto add = [](std::vector<int>& tab, int slot, int code) {
+    if (tab[2 * slot] < 0)
+      tab[2 * slot] = code;
+    else if (tab[2 * slot + 1] < 0)
+      tab[2 * slot + 1] = code;
+    else
+      throw std::runtime_error("make_merge_tables: more than two contributions");
+  };
+  // MD = [D | h_int | C] (rows: interfaces), B (ext x int), AH = [h_ext | A]
+  for (int c = 0; c < m.nchild; ++c)
+    for (int rf = 0; rf < m.nface; ++rf) {
+      const int rs = m.sec[c * m.nface + rf];
+      for (int cf = -1; cf < m.nface; ++cf) {
+        const int code = c * 64 + rf * 8 + (cf + 1);
+        if (cf < 0) {
+          if (rs >= 0)
+            add(m.ah_src, rs * ahc + 0, code);
+          else
+            add(m.md_src, (-rs - 1) * mdc + m.NI, code);
+          continue;
+        }
+        const int cs = m.sec[c * m.nface + cf];
+        if (rs >= 0 && cs >= 0)
+          add(m.ah_src, rs * ahc + 1 + cs, code);
+        else if (rs >= 0)
+          add(m.b_src, rs * m.NI + (-cs - 1), code);
+        else if (cs >= 0)
+          add(m.md_src, (-rs - 1) * mdc + m.NI + 1 + cs, code);
+        else
+          add(m.md_src, (-rs - 1) * mdc + (-cs - 1), code);
+      }
+    }
+  m.down.assign(m.nchild * m.nface, 0);
+  for (int c = 0; c < m.nchild; ++c)
+    for (int f = 0; f < m.nface; ++f) {
+      const int sc = m.sec[c * m.nface + f];
+      m.down[c * m.nface + f] = sc >= 0 ? sc * s : -((-sc - 1) * s) - 1;
+    }
+  return m;
+}
+
+namespace {
+// proj/src/layout.cpp:89-119 for uniform layouts of depth `levels`
+void collect(double lo[3], double hi[3], int dim, int face, int levels, int q, const std::vector<double>& gx,
+             std::vector<double>& out) {
+  if (levels == 0) {
+    auto map1 = [&](double t, int k) { return 0.5 * (lo[k] + hi[k]) + 0.5 * (hi[k] - lo[k]) * t; };
+    if (dim == 2) {
+      for (int i = 0; i < q; ++i) {
+        double x[3] = {0, 0, 0};
+        switch (face) {
+          case 0: x[0] = map1(gx[i], 0); x[1] = lo[1]; break;
+          case 1: x[0] = hi[0]; x[1] = map1(gx[i], 1); break;
+          case 2: x[0] = map1(gx[i], 0); x[1] = hi[1]; break;
+          default: x[0] = lo[0]; x[1] = map1(gx[i], 1); break;
+        }
+        out.insert(out.end(), x, x + 3);
+      }
+    } else {
+      const int axis = face / 2, ua = axis == 0 ? 1 : 0, va = axis == 2 ? 1 : 2;
+      const double fixed = face % 2 == 0 ? lo[axis] : hi[axis];
+      for (int iu = 0; iu < q; ++iu)
+        for (int iv = 0; iv < q; ++iv) {
+          double x[3];
+          x[axis] = fixed;
+          x[ua] = map1(gx[iu], ua);
+          x[va] = map1(gx[iv], va);
+          out.insert(out.end(), x, x + 3);
+        }
+    }
+    return;
+  }
+  double mid[3];
+  for (int k = 0; k < 3; ++k) mid[k] = 0.5 * (lo[k] + hi[k]);
+  if (dim == 2) {
+    const int axis = (face == 0 || face == 2) ? 0 : 1;
+    for (int h = 0; h < 2; ++h) {
+      double sl[3] = {lo[0], lo[1], lo[2]}, sh[3] = {hi[0], hi[1], hi[2]};
+      (h ? sl : sh)[axis] = mid[axis];
+      collect(sl, sh, dim, face, levels - 1, q, gx, out);
+    }
+  } else {
+    const int fa = face / 2, ua = fa == 0 ? 1 : 0, va = fa == 2 ? 1 : 2;
+    for (int hu = 0; hu < 2; ++hu)
+      for (int hv = 0; hv < 2; ++hv) {
+        double sl[3] = {lo[0], lo[1], lo[2]}, sh[3] = {hi[0], hi[1], hi[2]};
+        (hu ? sl : sh)[ua] = mid[ua];
+        (hv ? sl : sh)[va] = mid[va];
+        collect(sl, sh, dim, face, levels - 1, q, gx, out);
+      }
+  }
+}
+}  // namespace
+
+std::vector<double> root_boundary_points(const UniformTree& t) {
+  std::vector<double> gx, gw, out;
+  gauss_rule(t.q, gx, gw);
+  for (int f = 0; f < t.nface; ++f) {
+    double lo[3] = {t.lo, t.lo, t.dim == 3 ? t.lo : 0.0}, hi[3] = {t.hi, t.hi, t.dim == 3 ? t.hi : 0.0};
+    collect(lo, hi, t.dim, f, t.L, t.q, gx, out);
+  }
+  return out;
+}
+
+}  // namespace hpsg

@@ -1,0 +1,92 @@
+// geometry.hpp -- host-side precompute for the B200 HPS solver (product code).
+//
+// Everything here is small and computed once per solver on the host, then
+// uploaded: the spectral leaf operators (reference: proj/src/spectral.cpp
+// cheb_lobatto_1d :14-26, gauss_legendre_1d :51-85, cheb_diff_matrix :87-103,
+// barycentric_interp_matrix :105-137, leaf_index_sets :139-160,
+// assemble_dtn_ops_2d :260-310, assemble_dtn_ops_3d :370-436), the uniform
+// quad/octree in DFS leaf order (proj/src/mesh.cpp:27-121), the index tables of
+// the 4->1 / 8->1 merges (proj/src/merge.cpp:20-152, :302-320) and the root
+// boundary ordering (proj/src/layout.cpp:89-126).  Matrices are column-major.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace hpsg {
+
+struct HostMat {
+  int r = 0, c = 0;
+  std::vector<double> a;
+  HostMat() = default;
+  HostMat(int rr, int cc) : r(rr), c(cc), a(size_t(rr) * cc, 0.0) {}
+  double& operator()(int i, int j) { return a[size_t(j) * r + i]; }
+  double operator()(int i, int j) const { return a[size_t(j) * r + i]; }
+};
+
+std::vector<double> cheb_nodes(int p);                 // descending from +1
+void gauss_rule(int q, std::vector<double>& x, std::vector<double>& w);  // ascending
+HostMat cheb_diff(int p);
+HostMat bary_interp(const std::vector<double>& src, const std::vector<double>& dst);
+
+struct LeafOperators {
+  int dim = 2, p = 0, q = 0;
+  int n = 0, ni = 0, ne = 0, nb = 0;  // p^d, (p-2)^d, n-ni, boundary Gauss points
+  double side = 0.0;
+  std::vector<int> interior, exterior;  // tensor indices, increasing
+  HostMat P;   // ne x nb
+  HostMat Q;   // nb x n
+  HostMat Qi;  // nb x ni  (Q restricted to interior columns)
+  HostMat QeP; // nb x nb  (Q restricted to exterior columns, times P)
+  HostMat D, D2;  // p x p reference-element first/second derivative
+};
+LeafOperators make_leaf_operators(int dim, int p, double side);
+
+// Uniform tree of depth L on [lo,hi]^dim.  Node ids follow the reference's
+// construction order (breadth-first by level; proj/src/mesh.cpp:113-118); for a
+// uniform tree the level order of tree.levels[d] (DFS) coincides with id order,
+// and children of level-d node i are level-(d+1) nodes nchild*i + c.
+struct UniformTree {
+  int dim = 2, p = 0, q = 0, L = 0, nchild = 4, nface = 4;
+  double lo = -1, hi = 1;
+  long long level_first_id(int d) const;   // id of the first node at depth d
+  long long level_count(int d) const;      // nchild^d
+  int n_leaves() const { return int(level_count(L)); }
+  // leaf lower corners in DFS order (n_leaves x 3) and side length
+  std::vector<double> leaf_lo;
+  double leaf_side = 0;
+};
+UniformTree make_uniform_tree(int dim, int p, int L, double lo, double hi);
+
+// Merge of one level (all nodes at depth d of a uniform tree share it).
+// Child boundary layout: faces in reference order, s points per face section.
+// Parent exterior: faces in order, each split into nquad child sections
+// (qpos order of proj/src/merge.cpp:41-56); interface sections in the order of
+// proj/src/merge.cpp:20-33.  All sections hold s points.
+struct MergeTables {
+  int dim = 2, s = 0, nchild = 4, nface = 4, NI = 4, NE = 8;
+  int n_int() const { return NI * s; }
+  int n_ext() const { return NE * s; }
+  int child_nb() const { return nface * s; }
+  // per (child, face): ext section id (>=0) or -(interface id)-1
+  std::vector<int> sec;  // nchild*nface
+  // gather sources: for each destination block, up to 2 (child, rface, cface);
+  // cface == -1 means the outgoing-data (h) column.  Encoded child*64 + rf*8 + (cf+1), -1 = none.
+  std::vector<int> md_src;  // NI x (NI + 1 + NE) x 2
+  std::vector<int> b_src;   // NE x NI x 2
+  std::vector<int> ah_src;  // NE x (1 + NE) x 2
+  // downward scatter per (child, face): >=0 : offset into parent g (ext), <0: -(offset into g_int)-1
+  std::vector<int> down;    // nchild*nface
+};
+MergeTables make_merge_tables(int dim, int s);
+
+// Root boundary points in the reference's canonical section order
+// (HpsSolver::root_boundary_points, proj/src/solver.cpp:159-182).
+std::vector<double> root_boundary_points(const UniformTree& t);  // nb_root x 3
+
+// Reference-style problem error string helpers
+std::string fmt(const char* f, ...);
+
+}  // namespace hpsg

@@ -1,0 +1,102 @@
+// hps_kernels.cuh -- HPS-specific device kernels (leaf assembly, merge gather,
+// downward scatter, leaf output).  The dense FP64 work (LU, TRSM, GEMM) lives
+// in lu.cu / gemm.cu; these kernels move and build the operands around it.
+#pragma once
+
+#include "common.cuh"
+
+namespace hpsk {
+
+constexpr int kMaxTerms = 6;
+
+struct DevField {
+  int kind;
+  int n_centers;
+  double c[8];
+  const double* centers;  // device, n_centers x 3
+  const double* samples;  // device, n_leaves x npts
+};
+struct DevTerm {
+  int role, axis, axis2;
+  DevField f;
+};
+
+// ---- stage 1: leaf operator assembly -------------------------------------
+// Reference: discretize_operator (proj/src/local_solve.cpp:44-86) restricted to
+// the interior rows, plus the source sampling of HpsSolver::build_leaf
+// (proj/src/solver.cpp:49-57).  Never materializes the full n x n operator.
+struct LeafAsmArgs {
+  int dim, p, n, ni, ne, nb, nterms;
+  double scale;         // 2/side
+  double fsign;         // -1 literal (v = -L^-1 f, local_solve.cpp:137), +1 corrected
+  DevTerm terms[kMaxTerms];
+  DevField source;
+  int has_source;
+  const double* leaf_box;  // 6 per leaf (lo[3], hi[3]) in DFS order
+  const double* cheb;      // p
+  const double* D;         // p x p col-major
+  const double* D2;        // p x p col-major
+  const int* interior;     // ni tensor indices
+  const int* exterior;     // ne
+  double* M;               // per leaf: ni x (ni + 1 + nb): [L_ii | sgn*f_i | (filled by GEMM)]
+  long long strideM;
+  double* E;               // per leaf: ni x ne  (L_ie)
+  long long strideE;
+  int* bad_point;          // per leaf: first non-finite sample point index (or INT_MAX)
+};
+void launch_leaf_assemble(const LeafAsmArgs& a, int n_leaves, cudaStream_t st);
+
+// ---- stage 2: merge operand gather ------------------------------------------
+// Reference block assembly, proj/src/merge.cpp:226-278: child DtN blocks summed
+// into [D | h_int | C], B and [h_ext | A] by destination-driven gathers (no atomics).
+struct GatherArgs {
+  int s, nchild, child_nb;
+  const double* child_HT;   // per child: child_nb x (1 + child_nb), [h | T]
+  long long child_stride;
+  const int* src;           // destination table (2 codes per section block)
+  int kind;                 // 0: MD = [D | h_int | C], 1: B, 2: AH = [h_ext | A]
+  int NI, NE;
+  int nrows, ncols;
+  double* dst;
+  long long ld, stride;
+};
+void launch_gather(const GatherArgs& a, int n_nodes, cudaStream_t st);
+
+// ---- stage 3: downward pass scatter ------------------------------------------
+// Reference propagate() child gather, proj/src/solver.cpp:210-224: builds each
+// child's [1; g] column(s) from the parent's g_ext and the interface values g_int.
+struct ScatterArgs {
+  int nchild, nface, s, nrhs;
+  const int* down;          // nchild*nface
+  const double* Gp;         // parent: (1 + nbp) x nrhs per node
+  long long ldGp, strideGp;
+  const double* GI;         // parent interface values: n_int x nrhs per node
+  long long ldGI, strideGI;
+  double* Gc;               // children: (1 + nchild_b) x nrhs per child
+  long long ldGc, strideGc;
+};
+void launch_scatter(const ScatterArgs& a, int n_parents, cudaStream_t st);
+
+// GI <- -(GI + xh) (implicit root: g_int = -(x_h + D^-1 C g), solver.cpp:204-206)
+void launch_neg_add(double* GI, const double* xh, int n, int nrhs, long long ld, cudaStream_t st);
+
+// Leaf output in tensor order: u[rhs][leaf][idx] from the interior block
+// Ui (ni x nrhs per leaf) and the exterior block Ue (ne x nrhs per leaf).
+struct LeafOutArgs {
+  int ni, ne, npts, nrhs, n_leaves;
+  const int* interior;
+  const int* exterior;
+  const double* Ui;
+  long long ldUi, strideUi;
+  const double* Ue;
+  long long ldUe, strideUe;
+  double* u;
+};
+void launch_leaf_output(const LeafOutArgs& a, cudaStream_t st);
+
+// Fill a batch of (1 + nb) x nrhs columns with [1; g]: from a dense g (nb x nrhs, ld nb).
+void launch_pack_root(double* G, const double* g, int nb, int nrhs, cudaStream_t st);
+// Extract leaf boundary data (without the leading 1) for leaf_g_out.
+void launch_unpack_leaf_g(double* out, const double* G, int nb, int nrhs, int n_leaves, cudaStream_t st);
+
+}  // namespace hpsk

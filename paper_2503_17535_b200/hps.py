@@ -1,0 +1,291 @@
+"""Python host mirror of the reference HpsSolver<Real> API over the B200 C-ABI.
+
+The reference API (/root/reference/proj/include/hps/solver.hpp:40-117) is C++:
+HpsSolver(tree, variant, eta, terms, source, opts); build(); solve(g_root).
+This module binds the same surface to libhps_b200.so (include/hps_cuda.h)
+with ctypes, so tests and bench.py drive exactly the entry points a C/C++
+caller would.  There is no CPU fallback: without the shared library or a
+CUDA device every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libhps_b200.so")
+
+# status codes (include/hps_cuda.h)
+HPSG_OK, HPSG_ERR_INVALID, HPSG_ERR_SINGULAR_LEAF, HPSG_ERR_SINGULAR_MERGE, HPSG_ERR_NONFINITE, HPSG_ERR_OOM, \
+    HPSG_ERR_CUDA, HPSG_ERR_STATE, HPSG_ERR_NO_DEVICE = range(9)
+
+FIELD_CONST, FIELD_BUMPS, FIELD_PLANE_SIN, FIELD_PLANE_COS, FIELD_BUMPS_SIN, FIELD_POISSON2D_SRC, FIELD_SAMPLED = \
+    range(7)
+ROLE_LAPLACIAN, ROLE_GRADIENT, ROLE_ZEROTH, ROLE_SECOND_ORDER = range(4)
+
+
+class HpsError(RuntimeError):
+    """hps::Error (proj/include/hps/core.hpp:27-29) raised from a C-ABI status."""
+
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+class _Field(C.Structure):
+    _fields_ = [("kind", C.c_int), ("n_centers", C.c_int), ("c", C.c_double * 8),
+                ("centers", C.POINTER(C.c_double)), ("samples", C.POINTER(C.c_double))]
+
+
+class _Term(C.Structure):
+    _fields_ = [("role", C.c_int), ("axis", C.c_int), ("axis2", C.c_int), ("field", _Field)]
+
+
+class _Tree(C.Structure):
+    _fields_ = [("dim", C.c_int), ("p", C.c_int), ("L", C.c_int), ("lo", C.c_double), ("hi", C.c_double)]
+
+
+class _Options(C.Structure):
+    _fields_ = [("literal_sign", C.c_int), ("root_implicit_S", C.c_int), ("device", C.c_int), ("reserved", C.c_int)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("n_leaves", C.c_int), ("n_points", C.c_longlong), ("root_bsize", C.c_int), ("top_D_size", C.c_int),
+                ("tree_depth", C.c_int), ("min_rcond", C.c_double), ("ill_conditioned", C.c_int),
+                ("t_build_ms", C.c_double), ("t_leaf_ms", C.c_double), ("t_merge_ms", C.c_double),
+                ("t_solve_ms", C.c_double), ("build_flops", C.c_double), ("solve_bytes", C.c_double),
+                ("device_bytes", C.c_double), ("launches_build", C.c_int), ("launches_solve", C.c_int)]
+
+
+_lib = None
+
+
+def build_library():
+    subprocess.run(["make", "-s", "-C", HERE, "-j8"], check=True)
+
+
+def lib():
+    """Load libhps_b200.so (fails loudly; the product has no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise HpsError(HPSG_ERR_STATE, f"{LIB_PATH} not built: run __graft_entry__.build() or make -C {HERE}")
+        L = C.CDLL(LIB_PATH)
+        vp, dp = C.c_void_p, C.POINTER(C.c_double)
+        L.hpsg_create.argtypes = [C.POINTER(_Tree), C.POINTER(_Term), C.c_int, C.POINTER(_Field), C.POINTER(_Options),
+                                  C.POINTER(vp)]
+        L.hpsg_build.argtypes = [vp]
+        L.hpsg_solve.argtypes = [vp, dp, C.c_int, dp, dp]
+        L.hpsg_solve_device.argtypes = [vp, C.c_void_p, C.c_int, C.c_void_p]
+        L.hpsg_root_boundary_points.argtypes = [vp, dp]
+        L.hpsg_leaf_points.argtypes = [vp, dp]
+        L.hpsg_get_leaf.argtypes = [vp, C.c_int, dp, dp, dp, dp]
+        L.hpsg_node_sizes.argtypes = [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.hpsg_get_node.argtypes = [vp, C.c_int, dp, dp, dp, dp]
+        L.hpsg_get_stats.argtypes = [vp, C.POINTER(_Stats)]
+        L.hpsg_last_error.argtypes = [vp]
+        L.hpsg_last_error.restype = C.c_char_p
+        L.hpsg_destroy.argtypes = [vp]
+        L.hpsg_build_info.restype = C.c_char_p
+        L.hpsg_bump_centers.argtypes = [C.c_ulonglong, C.c_int, C.c_int, dp]
+        _lib = L
+    return _lib
+
+
+def _dp(a):
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+# ----------------------------------------------------------------------------- problem description
+@dataclass
+class Field:
+    """Coefficient/source field: a device-evaluated closed form or host samples.
+
+    Mirrors the reference's std::function<Real(const Point&)> fields
+    (proj/include/hps/local_solve.hpp:17-23) -- see include/hps_cuda.h HPSG_FIELD_*.
+    """
+    kind: int
+    c: tuple = ()
+    centers: np.ndarray | None = None
+    samples: np.ndarray | None = None
+
+    def to_c(self, keep):
+        f = _Field()
+        f.kind = self.kind
+        for i, v in enumerate(self.c):
+            f.c[i] = float(v)
+        if self.centers is not None:
+            cen = np.ascontiguousarray(self.centers, dtype=np.float64).reshape(-1, 3)
+            keep.append(cen)
+            f.n_centers = cen.shape[0]
+            f.centers = _dp(cen)
+        if self.samples is not None:
+            smp = np.ascontiguousarray(self.samples, dtype=np.float64)
+            keep.append(smp)
+            f.samples = _dp(smp)
+        return f
+
+    @staticmethod
+    def const(v):
+        return Field(FIELD_CONST, (v,))
+
+
+@dataclass
+class Term:
+    """CoefficientField (role, axis, axis2, field), proj/include/hps/local_solve.hpp:17-23."""
+    role: int
+    field: Field
+    axis: int = -1
+    axis2: int = -1
+
+
+@dataclass
+class UniformTree:
+    """build_uniform_tree(domain=[lo,hi]^dim, L, dim, p), proj/src/mesh.cpp:90-121."""
+    dim: int
+    p: int
+    L: int
+    lo: float = -1.0
+    hi: float = 1.0
+
+    @property
+    def q(self):
+        return self.p - 2
+
+    @property
+    def n_leaves(self):
+        return (4 if self.dim == 2 else 8) ** self.L
+
+    @property
+    def total_points(self):
+        return self.n_leaves * self.p ** self.dim
+
+    @property
+    def leaf_boundary_size(self):
+        return 2 * self.dim * self.q ** (self.dim - 1)
+
+    @property
+    def root_boundary_size(self):
+        return 4 * self.q * 2 ** self.L if self.dim == 2 else 6 * self.q ** 2 * 4 ** self.L
+
+
+def build_uniform_tree(lo, hi, L, dim, p):
+    return UniformTree(dim=dim, p=p, L=L, lo=lo, hi=hi)
+
+
+def bump_centers(seed, n=10, dim=2):
+    """std::mt19937_64(seed) + uniform_real_distribution(-0.5,0.5) (proj/src/problems.cpp:126-141)."""
+    out = np.zeros(3 * n)
+    lib().hpsg_bump_centers(seed, n, dim, _dp(out))
+    return out.reshape(n, 3)
+
+
+# ----------------------------------------------------------------------------- solver
+class HpsSolver:
+    """HpsSolver<Real> (DtN variant) on one B200, via libhps_b200.so.
+
+    literal_sign=True reproduces the reference's v_i = -L_ii^-1 f_i
+    (proj/src/local_solve.cpp:137); False uses the corrected +L_ii^-1 f_i.
+    """
+
+    def __init__(self, tree: UniformTree, terms, source: Field | None = None, literal_sign=True,
+                 root_implicit_S=False, device=0):
+        L = lib()
+        self.tree = tree
+        keep = []
+        arr = (_Term * max(1, len(terms)))()
+        for i, t in enumerate(terms):
+            arr[i].role, arr[i].axis, arr[i].axis2 = t.role, t.axis, t.axis2
+            arr[i].field = t.field.to_c(keep)
+        src = source.to_c(keep) if source is not None else None
+        tr = _Tree(tree.dim, tree.p, tree.L, tree.lo, tree.hi)
+        op = _Options(int(literal_sign), int(root_implicit_S), device, 0)
+        h = C.c_void_p()
+        rc = L.hpsg_create(C.byref(tr), arr, len(terms), C.byref(src) if src is not None else None, C.byref(op),
+                           C.byref(h))
+        self._h = h
+        if rc != HPSG_OK:
+            msg = L.hpsg_last_error(h).decode() if h.value else "no CUDA device"
+            self.close()
+            raise HpsError(rc, f"hpsg_create: {msg}")
+        self.root_implicit_S = root_implicit_S
+        self.npts = tree.p ** tree.dim
+        self.nb_root = tree.root_boundary_size
+
+    def _check(self, rc, what):
+        if rc != HPSG_OK:
+            raise HpsError(rc, f"{what}: {lib().hpsg_last_error(self._h).decode()}")
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().hpsg_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def build(self):
+        self._check(lib().hpsg_build(self._h), "build")
+
+    def root_boundary_points(self):
+        out = np.zeros((self.nb_root, 3))
+        self._check(lib().hpsg_root_boundary_points(self._h, _dp(out)), "root_boundary_points")
+        return out
+
+    def leaf_points(self):
+        out = np.zeros((self.tree.n_leaves, self.npts, 3))
+        self._check(lib().hpsg_leaf_points(self._h, _dp(out)), "leaf_points")
+        return out
+
+    def solve(self, g_root, want_leaf_g=False):
+        """g_root: (nb,) or (nrhs, nb) host array -> u: (n_leaves, p^d) or (nrhs, n_leaves, p^d)."""
+        g = np.ascontiguousarray(g_root, dtype=np.float64)
+        single = g.ndim == 1
+        g2 = g.reshape(1, -1) if single else g
+        nrhs = g2.shape[0]
+        assert g2.shape[1] == self.nb_root
+        u = np.empty((nrhs, self.tree.n_leaves, self.npts))
+        lg = np.empty((nrhs, self.tree.n_leaves, self.tree.leaf_boundary_size)) if want_leaf_g else None
+        self._check(lib().hpsg_solve(self._h, _dp(g2), nrhs, _dp(u), _dp(lg)), "solve")
+        if single:
+            u = u[0]
+            lg = lg[0] if lg is not None else None
+        return (u, lg) if want_leaf_g else u
+
+    def solve_device(self, d_g_ptr, nrhs, d_u_ptr):
+        """Zero-copy solve on device pointers (e.g. torch.Tensor.data_ptr())."""
+        self._check(lib().hpsg_solve_device(self._h, C.c_void_p(d_g_ptr), nrhs, C.c_void_p(d_u_ptr)), "solve")
+
+    def get_leaf(self, ord_):
+        n, nb = self.npts, self.tree.leaf_boundary_size
+        Y, v, T, h = np.zeros(n * nb), np.zeros(n), np.zeros(nb * nb), np.zeros(nb)
+        self._check(lib().hpsg_get_leaf(self._h, ord_, _dp(Y), _dp(v), _dp(T), _dp(h)), "get_leaf")
+        return Y.reshape(n, nb, order="F"), v, T.reshape(nb, nb, order="F"), h
+
+    def node_sizes(self, node_id):
+        a, b = C.c_int(), C.c_int()
+        self._check(lib().hpsg_node_sizes(self._h, node_id, C.byref(a), C.byref(b)), "node_sizes")
+        return a.value, b.value
+
+    def get_node(self, node_id):
+        ne, ni = self.node_sizes(node_id)
+        want_S = not (node_id == 0 and self.root_implicit_S)
+        S = np.zeros(ni * ne) if want_S else None
+        gt = np.zeros(ni)
+        T = np.zeros(ne * ne) if node_id != 0 else None
+        h = np.zeros(ne) if node_id != 0 else None
+        self._check(lib().hpsg_get_node(self._h, node_id, _dp(S), _dp(gt), _dp(T), _dp(h)), "get_node")
+        return (S.reshape(ni, ne, order="F") if S is not None else None, gt,
+                T.reshape(ne, ne, order="F") if T is not None else None, h)
+
+    def stats(self):
+        s = _Stats()
+        self._check(lib().hpsg_get_stats(self._h, C.byref(s)), "stats")
+        return {k: getattr(s, k) for k, _ in _Stats._fields_}

@@ -1,0 +1,86 @@
+"""Problem catalog for the B200 HPS solver (mirrors proj/src/problems.cpp).
+
+Each problem is a ProblemSpec-like record: operator terms and source as device
+field descriptors (hps.Field), Dirichlet boundary data and, where manufactured,
+the exact solution as numpy callables on (..., 3) point arrays.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+
+from .hps import (FIELD_BUMPS, FIELD_BUMPS_SIN, FIELD_CONST, FIELD_PLANE_COS, FIELD_PLANE_SIN, FIELD_POISSON2D_SRC,
+                  ROLE_GRADIENT, ROLE_LAPLACIAN, ROLE_ZEROTH, Field, Term, bump_centers)
+
+
+@dataclass
+class Problem:
+    name: str
+    dim: int
+    lo: float
+    hi: float
+    terms: list
+    source: Field | None
+    boundary: Callable  # x (...,3) -> values
+    exact: Callable | None = None
+
+
+def poisson2d() -> Problem:
+    """make_manufactured_2d_dtn, proj/src/problems.cpp:40-74:
+    Delta u - cos(5 x2) d1 u + sin(5 x2) d2 u = f, u = e^{5x1} sin 5x2 + sin(10 pi x1) sin(pi x2)."""
+    def u(x):
+        return np.exp(5 * x[..., 0]) * np.sin(5 * x[..., 1]) + np.sin(10 * np.pi * x[..., 0]) * np.sin(np.pi * x[..., 1])
+
+    terms = [Term(ROLE_LAPLACIAN, Field(FIELD_CONST, (1.0,))),
+             Term(ROLE_GRADIENT, Field(FIELD_PLANE_COS, (-1.0, 0.0, 5.0, 0.0, 0.0)), axis=0),
+             Term(ROLE_GRADIENT, Field(FIELD_PLANE_SIN, (1.0, 0.0, 5.0, 0.0, 0.0)), axis=1)]
+    return Problem("poisson2d", 2, -1.0, 1.0, terms, Field(FIELD_POISSON2D_SRC), u, u)
+
+
+def helmholtz_bumps(k=20.0, seed=7, n_bumps=10, alpha=50.0, phase=0.3) -> Problem:
+    """Headline config 2 (BASELINE.json configs[1]): variable-coefficient Helmholtz on [-1,1]^2,
+
+        Delta u + k^2 (1 + q(x)) u = f,   q = sum_j exp(-alpha |x - z_j|^2),
+
+    q is the seeded random-bump potential of make_scattering (proj/src/problems.cpp:126-141,
+    centers from std::mt19937_64(seed)).  Manufactured from the plane wave
+    u = sin(k x1 + phase): f = k^2 q u, Dirichlet data u on the boundary.
+    """
+    z = bump_centers(seed, n_bumps, 2)
+    k2 = k * k
+    terms = [Term(ROLE_LAPLACIAN, Field(FIELD_CONST, (1.0,))),
+             Term(ROLE_ZEROTH, Field(FIELD_BUMPS, (k2, k2, alpha), centers=z))]
+    src = Field(FIELD_BUMPS_SIN, (k2, 0.0, alpha, k, 0.0, 0.0, phase), centers=z)
+
+    def u(x):
+        return np.sin(k * x[..., 0] + phase)
+
+    return Problem(f"helmholtz_bumps(k={k:g},seed={seed})", 2, -1.0, 1.0, terms, src, u, u)
+
+
+def laplace_poly2d() -> Problem:
+    """Harmonic polynomial u = x^3 - 3 x y^2 + x y (f = 0): HPS is exact up to roundoff."""
+    def u(x):
+        return x[..., 0] ** 3 - 3 * x[..., 0] * x[..., 1] ** 2 + x[..., 0] * x[..., 1]
+
+    return Problem("laplace_poly2d", 2, -1.0, 1.0, [Term(ROLE_LAPLACIAN, Field(FIELD_CONST, (1.0,)))], None, u, u)
+
+
+def poisson3d_const(kx=1.0) -> Problem:
+    """3D smoke problem: Delta u = f with u = sin(kx x1) e^{x2} cos(x3)... kept simple: harmonic
+    u = e^{x1} cos(x2) + x3^2 - x1^2 (f = 0)."""
+    def u(x):
+        return np.exp(x[..., 0]) * np.cos(x[..., 1]) + x[..., 2] ** 2 - x[..., 0] ** 2
+
+    return Problem("laplace3d", 3, 0.0, 1.0, [Term(ROLE_LAPLACIAN, Field(FIELD_CONST, (1.0,)))], None, u, u)
+
+
+CATALOG = {"poisson2d": poisson2d, "helmholtz_bumps": helmholtz_bumps, "laplace_poly2d": laplace_poly2d,
+           "laplace3d": poisson3d_const}
+
+
+def rel_linf(u, ref):
+    """error_report rel L-inf (proj/src/problems.cpp:270-293)."""
+    return float(np.abs(u - ref).max() / np.abs(ref).max())
