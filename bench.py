@@ -1,0 +1,285 @@
+#!/usr/bin/env python
+"""HPS build+solve benchmark (BASELINE.json metric) on B200.
+
+Workload (BASELINE.json configs[1]): 2D variable-coefficient Helmholtz
+Delta u + k^2 (1 + q(x)) u = f on [-1,1]^2, DtN HPS, p = 16, uniform quadtree
+L = 8 (65,536 leaves, N = 16,777,216 DOF), q = 10 seeded Gaussian bumps,
+manufactured plane-wave solution (synthetic data, k = 20).
+
+One step = one full build (leaf stage + all merge levels) + one solve (downward
+pass + leaf reconstruction) through the C-ABI (libhps_b200.so).  `value` is
+DOF/s with the problem descriptor and the root boundary data resident on the
+device; `e2e` is the same step through hpsg_solve with HOST buffers (boundary
+data H2D, the whole solution field D2H inside the timed region).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+--impl reference times the reference algorithm on the host cores: the C++
+restatement in oracle/ (the reference itself needs Eigen, absent here), with
+all host threads.  Under torchrun (N>1) every rank runs an independent replica
+(weak scaling; the subtree-sharded multi-GPU build is not in this round).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "HPS build+solve seconds & DOF/s (2D p=16 L=8) at 1/2/4/8 B200; rel err vs oracle"
+# PAPER.md:629 / :1755 -- H100 JAX, subtree recomputation, p=16 L=8: 4.02 s (N = 16,777,216)
+PAPER_H100_DOFS = 16777216 / 4.02
+FP64_PEAK_TFLOPS = 37.155     # profiles/r01_fp64_peak.json (DMMA microbench; MEASURED_PEAKS.json has no FP64 entry)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index=0):
+        self.samples, self.proc, self.gpu = [], None, gpu_index
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[4 + i].strip() == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "n_samples": len(self.samples)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2503_17535_b200 as H
+    from paper_2503_17535_b200 import problems as PR
+
+    prob = PR.helmholtz_bumps(k=args.k, seed=args.seed)
+    tree = H.build_uniform_tree(prob.lo, prob.hi, args.L, 2, args.p)
+    N = tree.total_points
+    solver = H.HpsSolver(tree, prob.terms, prob.source, literal_sign=False, root_implicit_S=not args.explicit_root,
+                         device=local)
+    stream = torch.cuda.current_stream()
+    solver.set_stream(stream.cuda_stream)
+
+    g_host = prob.boundary(solver.root_boundary_points())
+    g_dev = torch.tensor(g_host, device="cuda")
+    u_dev = torch.empty((tree.n_leaves, tree.p ** 2), dtype=torch.float64, device="cuda")
+    g_pin = torch.tensor(g_host).pin_memory()
+    u_pin = torch.empty((tree.n_leaves, tree.p ** 2), dtype=torch.float64).pin_memory()
+
+    def step_device():
+        solver.build()
+        solver.solve_device(g_dev.data_ptr(), 1, u_dev.data_ptr())
+
+    def step_e2e():
+        solver.build()
+        H.lib().hpsg_solve(solver._h, H.hps._dp(g_pin.numpy()), 1, H.hps._dp(u_pin.numpy()), None)
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+    st = solver.stats()
+    launches_per_step = st["launches_build"] + st["launches_solve"]
+
+    def timed(fn, K):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        builds, solves = [], []
+        for _ in range(K):
+            fn()
+            s = solver.stats()
+            builds.append(s["t_build_ms"])
+            solves.append(s["t_solve_ms"])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / K
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        return ms, float(np.mean(builds)), float(np.mean(solves))
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms, t_build, t_solve = timed(step_device, args.steps)
+    clk = clocks.stop()
+    u_gpu = u_dev.cpu().numpy()
+    ms_e2e = ms
+    if not args.profile:
+        ms_e2e, _, _ = timed(step_e2e, max(1, args.steps // 2))
+    st = solver.stats()
+
+    err_exact = PR.rel_linf(u_gpu, prob.exact(solver.leaf_points()))
+    peaks = load_peaks()
+    flops = st["build_flops"]
+    value = N * world / (ms / 1e3)
+    out = {
+        "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": value / world / PAPER_H100_DOFS,
+        "vs_baseline_ref": "per-GPU DOF/s / 4.17e6 DOF/s (PAPER.md:629, H100 JAX subtree recompute, p=16 L=8, 4.02 s)",
+        "dtype": "f64", "data": "synthetic (seeded bump potential, manufactured plane wave; coefficients evaluated on device)",
+        "config": {"workload": f"2D variable-coefficient Helmholtz DtN HPS, p={args.p}, L={args.L} uniform quadtree, "
+                               f"N={N} DOF (BASELINE configs[1])", "k": args.k, "seed": args.seed,
+                   "root": "explicit S" if args.explicit_root else "implicit S (MergeOptions::implicit_S)",
+                   "sign": "corrected (v=+L^-1 f); literal differs only in the sign of f",
+                   "l2": "inputs larger than L2 (each step streams > 40 GB of leaf/merge operands)",
+                   "parallelism": f"{world} independent replica(s)"},
+        "stages_ms": {"build": t_build, "leaf": st["t_leaf_ms"], "merge": st["t_merge_ms"], "solve": t_solve},
+        "roofline": {"bound": "tensor", "kernel": "build (batched DMMA LU/TRSM/GEMM pipeline)",
+                     "achieved": flops / (t_build / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": flops / (t_build / 1e3) / 1e12 / FP64_PEAK_TFLOPS, "traffic": None,
+                     "algorithmic_flops": flops,
+                     "peak_source": "FP64 DMMA microbench profiles/r01_fp64_peak.json (of measured)"},
+        "solve_roofline": {"bound": "hbm", "achieved": st["solve_bytes"] / (t_solve / 1e3) / 1e9,
+                           "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                           "frac": st["solve_bytes"] / (t_solve / 1e3) / 1e9 / peaks.get("hbm_gbs", 6532.5),
+                           "algorithmic_bytes": st["solve_bytes"]},
+        "e2e": {"value": N * world / (ms_e2e / 1e3), "unit": "DOF/s", "ms_per_step": ms_e2e,
+                "h2d_bytes_per_step": int(g_host.nbytes), "d2h_bytes_per_step": int(u_pin.numpy().nbytes)},
+        "gpu_launches": int(launches_per_step * args.steps),
+        "accuracy": {"rel_linf_vs_exact": err_exact, "min_leaf_rcond": st["min_rcond"]},
+        "clocks": clk,
+        "device_gb": st["device_bytes"] / 1e9,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"], par = cpu_baseline(args, prob, u_gpu)
+        out["accuracy"].update(par)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def cpu_baseline(args, prob, u_gpu=None):
+    """Oracle (C++ restatement of the reference) on the host cores: full workload, one run."""
+    from oracle import oracle as O
+    from tests.oracle_problems import oracle_solver
+    threads = os.cpu_count()
+    O.set_threads(threads)
+    s = oracle_solver(prob, args.p, args.cpu_L, literal=False, root_implicit=not args.explicit_root, parallel=True)
+    t0 = time.perf_counter()
+    s.build()
+    t1 = time.perf_counter()
+    g = prob.boundary(s.root_points())
+    u = s.solve(g)
+    t2 = time.perf_counter()
+    N = s.n_leaves * s.npts
+    res = {"value": N / (t2 - t0), "unit": "DOF/s", "cores": threads, "kind": "port",
+           "sample": f"full workload at L={args.cpu_L} (N={N}), one build+solve, OpenMP over leaves/merges "
+                     f"+ threaded OpenBLAS; build {t1 - t0:.2f} s, solve {t2 - t1:.2f} s"}
+    par = {}
+    if u_gpu is not None and args.cpu_L == args.L:
+        par["rel_linf_vs_oracle"] = float(np.abs(u_gpu - u).max() / np.abs(u).max())
+    return res, par
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    from paper_2503_17535_b200 import problems as PR
+    prob = PR.helmholtz_bumps(k=args.k, seed=args.seed)
+    times = []
+    res = None
+    for i in range(args.warmup + args.steps):
+        res, _ = cpu_baseline(args, prob)
+        if i >= args.warmup:
+            times.append(res["value"])
+    value = float(np.median(times))
+    N = (4 ** args.cpu_L) * args.p ** 2
+    out = {"metric": METRIC, "impl": "reference", "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": N / value * 1e3, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"2D variable-coefficient Helmholtz DtN HPS, p={args.p}, L={args.cpu_L}, N={N} DOF "
+                                  "(BASELINE configs[1])", "k": args.k, "seed": args.seed},
+           "cpu_baseline": dict(res, value=value),
+           "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--L", type=int, default=8)
+    ap.add_argument("--p", type=int, default=16)
+    ap.add_argument("--k", type=float, default=20.0)
+    ap.add_argument("--seed", type=int, default=7)
+    ap.add_argument("--cpu-L", type=int, default=None, help="tree depth of the CPU baseline run (default: --L)")
+    ap.add_argument("--explicit-root", action="store_true", help="form S at the root (reference 2D default)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="one untimed-warmup-free step for ncu launch lists")
+    args = ap.parse_args()
+    if args.profile:
+        args.steps, args.warmup, args.no_cpu_baseline = 1, 0, True
+    if args.cpu_L is None:
+        args.cpu_L = args.L
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

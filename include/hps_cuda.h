@@ -121,6 +121,9 @@ int hpsg_node_sizes(hpsg_ctx* ctx, int node_id, int* n_ext, int* n_int);
  * non-root internal node (solver.hpp:83-85).  Any pointer may be NULL. */
 int hpsg_get_node(hpsg_ctx* ctx, int node_id, double* S, double* gtilde, double* T, double* h);
 int hpsg_get_stats(hpsg_ctx* ctx, hpsg_stats* out);
+/* run all later work of ctx on a caller-owned cudaStream_t (passed as void*; NULL = legacy
+ * default stream) so callers can order and time it with their own events */
+int hpsg_set_stream(hpsg_ctx* ctx, void* stream);
 const char* hpsg_last_error(hpsg_ctx* ctx);
 void hpsg_destroy(hpsg_ctx* ctx);
 

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <omp.h>
 #include <sstream>
 
 namespace hpso {
@@ -1122,7 +1123,11 @@ void Solver::build() {
   using clk = std::chrono::steady_clock;
   auto t0 = clk::now();
   const int nl = tree_->n_leaves();
+  // "parallel oracle": OpenMP across independent leaves/merges with single-threaded BLAS
+  // inside; levels with fewer nodes than threads run serially with threaded BLAS.
+  const int nthr = omp_get_max_threads();
   if (opts_.parallel) {
+    set_blas_threads(1);
     std::string err;
 #pragma omp parallel for schedule(dynamic, 4)
     for (int i = 0; i < nl; ++i) {
@@ -1142,7 +1147,8 @@ void Solver::build() {
   for (int depth = tree_->max_depth() - 1; depth >= 0; --depth) {
     const auto& lev = tree_->levels[depth];
     const int cnt = int(lev.size());
-    if (opts_.parallel && cnt > 1) {
+    if (opts_.parallel && cnt >= nthr) {
+      set_blas_threads(1);
       std::string err;
 #pragma omp parallel for schedule(dynamic, 1)
       for (int i = 0; i < cnt; ++i) {
@@ -1156,10 +1162,12 @@ void Solver::build() {
       }
       if (!err.empty()) fail(err);
     } else {
+      set_blas_threads(nthr);
       for (int id : lev)
         if (!tree_->nodes[id].is_leaf()) merge_internal(id);
     }
   }
+  set_blas_threads(nthr);
   auto t2 = clk::now();
   t_leaf = std::chrono::duration<double>(t1 - t0).count();
   t_merge = std::chrono::duration<double>(t2 - t1).count();

@@ -101,6 +101,7 @@ struct hpsg_ctx {
   std::string err;
   int dev = 0;
   cudaStream_t st = nullptr;
+  bool own_stream = true;
   cudaEvent_t ev[8] = {};
   hpsg_tree tree{};
   hpsg_options opts{};
@@ -904,6 +905,16 @@ int hpsg_get_node(hpsg_ctx* c, int id, double* S, double* gtilde, double* Tm, do
   });
 }
 
+int hpsg_set_stream(hpsg_ctx* c, void* stream) {
+  if (!c) return HPSG_ERR_INVALID;
+  return guarded(c, [&] {
+    ck(cudaStreamSynchronize(c->st), "set_stream sync");
+    if (c->own_stream) ck(cudaStreamDestroy(c->st), "stream destroy");
+    c->st = static_cast<cudaStream_t>(stream);
+    c->own_stream = false;
+  });
+}
+
 int hpsg_get_stats(hpsg_ctx* c, hpsg_stats* out) {
   if (!c || !out) return HPSG_ERR_INVALID;
   *out = c->stats;
@@ -920,7 +931,7 @@ void hpsg_destroy(hpsg_ctx* c) {
     hpsg_ctx* tmp = c;
     for (auto& e : tmp->ev)
       if (e) cudaEventDestroy(e);
-    cudaStream_t st = tmp->st;
+    cudaStream_t st = tmp->own_stream ? tmp->st : nullptr;
     delete tmp;  // frees device buffers
     if (st) cudaStreamDestroy(st);
   }

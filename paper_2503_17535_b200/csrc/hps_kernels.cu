@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const GatherArgs
   const int nslots = a.kind == 0 ? a.NI + 1 + a.NE : (a.kind == 1 ? a.NI : 1 + a.NE);
   double* dst = a.dst + node * a.stride;
   const double* ch0 = a.child_HT + node * a.nchild * a.child_stride;
-  const long long base = (long long)blockIdx.y * kGatherThreads * kGatherPerThread;
+  for (long long base = (long long)blockIdx.y * kGatherThreads * kGatherPerThread; base < total;
+       base += (long long)gridDim.y * kGatherThreads * kGatherPerThread)
 #pragma unroll
   for (int it = 0; it < kGatherPerThread; ++it) {
     const long long e = base + it * kGatherThreads + threadIdx.x;
@@ -289,7 +290,7 @@ void launch_leaf_assemble(const LeafAsmArgs& a, int n_leaves, cudaStream_t st) {
 void launch_gather(const GatherArgs& a, int n_nodes, cudaStream_t st) {
   const long long total = (long long)a.nrows * a.ncols;
   const long long per = kGatherThreads * kGatherPerThread;
-  dim3 grid(n_nodes, (unsigned)((total + per - 1) / per));
+  dim3 grid(n_nodes, (unsigned)std::min<long long>((total + per - 1) / per, 65535));
   gather_kernel<<<grid, kGatherThreads, 0, st>>>(a);
 }
 

@@ -182,6 +182,7 @@ struct SwapTrsmArgs {
   const int* ipiv;
   int n, j0, nb;
   int nseg;
+  int do_swaps;  // 0 when the rows were already permuted (bgetrs)
   Seg seg[3];
 };
 
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(kColThreads) swap_trsm_kernel(const SwapTrsmAr
   if (s >= a.nseg) return;
   const Seg sg = a.seg[s];
   double* x = sg.base + b * sg.stride + (long long)col * sg.ld;
-  for (int jj = 0; jj < nb; ++jj) {
+  for (int jj = 0; jj < (a.do_swaps ? nb : 0); ++jj) {
     const int r1 = a.j0 + jj, r2 = piv[jj];
     if (r2 != r1) {
       const double t = x[r1];
@@ -273,6 +274,36 @@ __global__ void __launch_bounds__(kColThreads) trsm_upper_kernel(const TrsmUArgs
     if (jj < nb) x[jj] = v[jj];
 }
 
+// Apply the complete pivot sequence of a factorization to R (LAPACK laswp), via the
+// composite permutation built in shared memory: R[i, :] <- R[perm[i], :].
+__global__ void laswp_perm_kernel(const int* ipiv, int n, double* R, long long ldR, long long strideR, int ncols,
+                                  int cols_per_cta) {
+  extern __shared__ __align__(16) double sbuf[];
+  int* perm = reinterpret_cast<int*>(sbuf + n);
+  const long long b = blockIdx.x;
+  const int* pv = ipiv + b * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = i;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < n; ++i) {
+      const int j = pv[i];
+      if (j != i) {
+        const int t = perm[i];
+        perm[i] = perm[j];
+        perm[j] = t;
+      }
+    }
+  __syncthreads();
+  const int c0 = blockIdx.y * cols_per_cta, c1 = min(ncols, c0 + cols_per_cta);
+  for (int c = c0; c < c1; ++c) {
+    double* x = R + b * strideR + (long long)c * ldR;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sbuf[i] = x[perm[i]];
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = sbuf[i];
+    __syncthreads();
+  }
+}
+
 __global__ void stats_init_kernel(double* s, int batch) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < batch) {
@@ -325,8 +356,9 @@ cudaError_t launch_panel(int batch, int n, int j0, int nb, BatchedMat M, int* ip
 }
 
 cudaError_t launch_swap_trsm(int batch, int n, int j0, int nb, const double* L, long long ldL, long long strideL,
-                             const int* ipiv, const Seg* segs, int nseg, cudaStream_t st) {
+                             const int* ipiv, const Seg* segs, int nseg, cudaStream_t st, int do_swaps = 1) {
   SwapTrsmArgs a{};
+  a.do_swaps = do_swaps;
   a.L = L;
   a.ldL = ldL;
   a.strideL = strideL;
@@ -440,10 +472,23 @@ cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double*
 cudaError_t bgetrs(int batch, int n, int m, BatchedMat LU, const int* ipiv, BatchedMat R, cudaStream_t st) {
   if (batch <= 0 || n <= 0 || m <= 0) return cudaSuccess;
   cudaError_t e;
+  {
+    const int cpc = 8;
+    const size_t smem = (size_t)n * 12;
+    static size_t smem_set = 0;
+    if (smem > smem_set && smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(laswp_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      smem_set = smem;
+    }
+    laswp_perm_kernel<<<dim3(batch, (m + cpc - 1) / cpc), 256, smem, st>>>(ipiv, n, R.p, R.ld, R.stride, m, cpc);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   for (int j0 = 0; j0 < n; j0 += kLuNB) {
     const int nb = std::min(kLuNB, n - j0);
     Seg seg{R.p, R.ld, R.stride, m, 1};
-    e = launch_swap_trsm(batch, n, j0, nb, LU.p, LU.ld, LU.stride, ipiv, &seg, 1, st);
+    e = launch_swap_trsm(batch, n, j0, nb, LU.p, LU.ld, LU.stride, ipiv, &seg, 1, st, /*do_swaps=*/0);
     if (e != cudaSuccess) return e;
     const int rows = n - j0 - nb;
     if (rows > 0) {

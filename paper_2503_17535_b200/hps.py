@@ -87,6 +87,7 @@ def lib():
         L.hpsg_node_sizes.argtypes = [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.hpsg_get_node.argtypes = [vp, C.c_int, dp, dp, dp, dp]
         L.hpsg_get_stats.argtypes = [vp, C.POINTER(_Stats)]
+        L.hpsg_set_stream.argtypes = [vp, C.c_void_p]
         L.hpsg_last_error.argtypes = [vp]
         L.hpsg_last_error.restype = C.c_char_p
         L.hpsg_destroy.argtypes = [vp]
@@ -284,6 +285,10 @@ class HpsSolver:
         self._check(lib().hpsg_get_node(self._h, node_id, _dp(S), _dp(gt), _dp(T), _dp(h)), "get_node")
         return (S.reshape(ni, ne, order="F") if S is not None else None, gt,
                 T.reshape(ne, ne, order="F") if T is not None else None, h)
+
+    def set_stream(self, stream_handle):
+        """Run on a caller-owned cudaStream_t (int handle, e.g. torch.cuda.current_stream().cuda_stream)."""
+        self._check(lib().hpsg_set_stream(self._h, C.c_void_p(stream_handle)), "set_stream")
 
     def stats(self):
         s = _Stats()

@@ -68,11 +68,11 @@ def laplace_poly2d() -> Problem:
     return Problem("laplace_poly2d", 2, -1.0, 1.0, [Term(ROLE_LAPLACIAN, Field(FIELD_CONST, (1.0,)))], None, u, u)
 
 
-def poisson3d_const(kx=1.0) -> Problem:
-    """3D smoke problem: Delta u = f with u = sin(kx x1) e^{x2} cos(x3)... kept simple: harmonic
-    u = e^{x1} cos(x2) + x3^2 - x1^2 (f = 0)."""
+def poisson3d_const() -> Problem:
+    """3D Laplace with the harmonic cubic u = x^3 - 3 x y^2 + z^2 - x^2 + x y z on [0,1]^3 (exact for q >= 4)."""
     def u(x):
-        return np.exp(x[..., 0]) * np.cos(x[..., 1]) + x[..., 2] ** 2 - x[..., 0] ** 2
+        X, Y, Z = x[..., 0], x[..., 1], x[..., 2]
+        return X ** 3 - 3 * X * Y ** 2 + Z ** 2 - X ** 2 + X * Y * Z
 
     return Problem("laplace3d", 3, 0.0, 1.0, [Term(ROLE_LAPLACIAN, Field(FIELD_CONST, (1.0,)))], None, u, u)
 
