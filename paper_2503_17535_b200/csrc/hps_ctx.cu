@@ -159,14 +159,7 @@ void gemm(hpsg_ctx* c, const GemmArgs& g) {
   ++c->launches;
 }
 
-// launches issued by bgetrf_aug / bgetrs (for the gpu_launches claim)
-int lu_launches(int n, int m, bool factor) {
-  const int np = (n + hpsk::kLuNB - 1) / hpsk::kLuNB;
-  int l = factor ? 1 : 0;  // stats init
-  for (int j = 0; j < np; ++j) l += (factor ? 1 : 0) + 1 + ((j + 1) * hpsk::kLuNB < n ? 1 : 0);
-  if (m > 0) l += np + (np - 1);
-  return l;
-}
+int lu_launches(int n, int m, bool factor) { return hpsk::lu_launch_count(n, m, factor); }
 
 hpsk::DevField make_dev_field(hpsg_ctx* c, const hpsg_field& f, bool is_source) {
   hpsk::DevField d{};

@@ -378,41 +378,66 @@ cudaError_t launch_swap_trsm(int batch, int n, int j0, int nb, const double* L, 
   return cudaGetLastError();
 }
 
+// Two-level blocking: 32-column panels (GEPP in shared memory) inside 256-column
+// outer blocks, so the bulk of every factorization and solve is one DMMA GEMM
+// with k = 256 per outer block instead of a k = 32 update per panel (the
+// trailing matrix is streamed from HBM 8x less often).
+constexpr int kOuterNB = 256;
+
+// C[rows, cols] += alpha * A[rows, k] * B[k, cols] on sub-blocks of strided batches.
+cudaError_t gemm_sub(int batch, int rows, int cols, int k, double alpha, const double* A, long long lda, long long sA,
+                     const double* B, long long ldb, long long sB, double* C, long long ldc, long long sC,
+                     cudaStream_t st) {
+  if (rows <= 0 || cols <= 0 || k <= 0) return cudaSuccess;
+  GemmArgs g;
+  g.m = rows;
+  g.n = cols;
+  g.k = k;
+  g.batch = batch;
+  g.A = A;
+  g.lda = lda;
+  g.sA = sA;
+  g.B = B;
+  g.ldb = ldb;
+  g.sB = sB;
+  g.C = C;
+  g.ldc = ldc;
+  g.sC = sC;
+  g.D = C;
+  g.ldd = ldc;
+  g.sD = sC;
+  g.alpha = alpha;
+  g.beta = 1.0;
+  return launch_dgemm(g, st);
+}
+
+#define HPS_TRY(x)                      \
+  do {                                  \
+    cudaError_t e_ = (x);               \
+    if (e_ != cudaSuccess) return e_;   \
+  } while (0)
+
 // Blocked back substitution R <- U^-1 R, U = upper triangle of LU (n x n).
 cudaError_t back_subst(int batch, int n, int m, const double* U, long long ldU, long long strideU, double* R,
                        long long ldR, long long strideR, cudaStream_t st) {
   if (m <= 0) return cudaSuccess;
-  const int nblk = (n + kLuNB - 1) / kLuNB;
-  for (int jb = nblk - 1; jb >= 0; --jb) {
-    const int r0 = jb * kLuNB, nb = std::min(kLuNB, n - r0);
-    TrsmUArgs t{U, ldU, strideU, r0, nb, R, ldR, strideR, m};
-    dim3 grid(batch, (m + kColThreads - 1) / kColThreads);
-    trsm_upper_kernel<<<grid, kColThreads, 0, st>>>(t);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    if (r0 > 0) {
-      GemmArgs g;
-      g.m = r0;
-      g.n = m;
-      g.k = nb;
-      g.batch = batch;
-      g.A = U + (long long)r0 * ldU;
-      g.lda = ldU;
-      g.sA = strideU;
-      g.B = R + r0;
-      g.ldb = ldR;
-      g.sB = strideR;
-      g.C = R;
-      g.ldc = ldR;
-      g.sC = strideR;
-      g.D = R;
-      g.ldd = ldR;
-      g.sD = strideR;
-      g.alpha = -1.0;
-      g.beta = 1.0;
-      e = launch_dgemm(g, st);
-      if (e != cudaSuccess) return e;
+  const int nouter = (n + kOuterNB - 1) / kOuterNB;
+  for (int ob = nouter - 1; ob >= 0; --ob) {
+    const int r0 = ob * kOuterNB, r1 = std::min(n, r0 + kOuterNB);
+    const int nsub = (r1 - r0 + kLuNB - 1) / kLuNB;
+    for (int sb = nsub - 1; sb >= 0; --sb) {
+      const int s0 = r0 + sb * kLuNB, nb = std::min(kLuNB, r1 - s0);
+      TrsmUArgs t{U, ldU, strideU, s0, nb, R, ldR, strideR, m};
+      dim3 grid(batch, (m + kColThreads - 1) / kColThreads);
+      trsm_upper_kernel<<<grid, kColThreads, 0, st>>>(t);
+      HPS_TRY(cudaGetLastError());
+      // rows of this outer block above the sub-block
+      HPS_TRY(gemm_sub(batch, s0 - r0, m, nb, -1.0, U + (long long)s0 * ldU + r0, ldU, strideU, R + s0, ldR, strideR,
+                       R + r0, ldR, strideR, st));
     }
+    // everything above the outer block, k = outer block width
+    HPS_TRY(gemm_sub(batch, r0, m, r1 - r0, -1.0, U + (long long)r0 * ldU, ldU, strideU, R + r0, ldR, strideR, R, ldR,
+                     strideR, st));
   }
   return cudaSuccess;
 }
@@ -430,92 +455,88 @@ cudaError_t lu_stats_init(double* stats, int batch, cudaStream_t st) {
 cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double* stats, cudaStream_t st) {
   if (batch <= 0 || n <= 0) return cudaSuccess;
   if (n > bgetrf_max_n()) return cudaErrorInvalidValue;
-  cudaError_t e;
-  for (int j0 = 0; j0 < n; j0 += kLuNB) {
-    const int nb = std::min(kLuNB, n - j0);
-    e = launch_panel(batch, n, j0, nb, M, ipiv, stats, st);
-    if (e != cudaSuccess) return e;
-    Seg segs[2];
-    segs[0] = Seg{M.p, M.ld, M.stride, j0, 0};                                   // L columns: swaps only
-    segs[1] = Seg{M.p + (long long)(j0 + nb) * M.ld, M.ld, M.stride, n + m - j0 - nb, 1};  // U12 | RHS
-    e = launch_swap_trsm(batch, n, j0, nb, M.p, M.ld, M.stride, ipiv, segs, 2, st);
-    if (e != cudaSuccess) return e;
-    const int rows = n - j0 - nb, cols = n + m - j0 - nb;
-    if (rows > 0 && cols > 0) {
-      GemmArgs g;
-      g.m = rows;
-      g.n = cols;
-      g.k = nb;
-      g.batch = batch;
-      g.A = M.p + (long long)j0 * M.ld + j0 + nb;
-      g.lda = M.ld;
-      g.sA = M.stride;
-      g.B = M.p + (long long)(j0 + nb) * M.ld + j0;
-      g.ldb = M.ld;
-      g.sB = M.stride;
-      double* C = M.p + (long long)(j0 + nb) * M.ld + j0 + nb;
-      g.C = C;
-      g.ldc = M.ld;
-      g.sC = M.stride;
-      g.D = C;
-      g.ldd = M.ld;
-      g.sD = M.stride;
-      g.alpha = -1.0;
-      g.beta = 1.0;
-      e = launch_dgemm(g, st);
-      if (e != cudaSuccess) return e;
+  const long long ld = M.ld, sM = M.stride;
+  double* A = M.p;
+  auto at = [&](int r, int c) { return A + (long long)c * ld + r; };
+  const int ncol = n + m;
+  for (int J = 0; J < n; J += kOuterNB) {
+    const int Jend = std::min(n, J + kOuterNB);
+    // (1) factor the outer panel columns [J, Jend); the row swaps go to every column at once,
+    //     while columns right of the outer panel are otherwise left untouched
+    for (int j0 = J; j0 < Jend; j0 += kLuNB) {
+      const int nb = std::min(kLuNB, Jend - j0);
+      HPS_TRY(launch_panel(batch, n, j0, nb, M, ipiv, stats, st));
+      Seg segs[3];
+      segs[0] = Seg{A, ld, sM, j0, 0};                              // factored L columns: swaps only
+      segs[1] = Seg{at(0, j0 + nb), ld, sM, Jend - j0 - nb, 1};      // rest of the outer panel: swaps + L11^-1
+      segs[2] = Seg{at(0, Jend), ld, sM, ncol - Jend, 0};            // right of the outer panel: swaps only
+      HPS_TRY(launch_swap_trsm(batch, n, j0, nb, A, ld, sM, ipiv, segs, 3, st));
+      HPS_TRY(gemm_sub(batch, n - j0 - nb, Jend - j0 - nb, nb, -1.0, at(j0 + nb, j0), ld, sM, at(j0, j0 + nb), ld, sM,
+                       at(j0 + nb, j0 + nb), ld, sM, st));
     }
+    // (2) U12 = L11^-1 A12 over the outer block's row slab (blocked forward substitution)
+    for (int j0 = J; j0 < Jend && Jend < ncol; j0 += kLuNB) {
+      const int nb = std::min(kLuNB, Jend - j0);
+      Seg seg{at(0, Jend), ld, sM, ncol - Jend, 1};
+      HPS_TRY(launch_swap_trsm(batch, n, j0, nb, A, ld, sM, ipiv, &seg, 1, st, /*do_swaps=*/0));
+      HPS_TRY(gemm_sub(batch, Jend - j0 - nb, ncol - Jend, nb, -1.0, at(j0 + nb, j0), ld, sM, at(j0, Jend), ld, sM,
+                       at(j0 + nb, Jend), ld, sM, st));
+    }
+    // delayed trailing update with k = outer block width
+    HPS_TRY(gemm_sub(batch, n - Jend, ncol - Jend, Jend - J, -1.0, at(Jend, J), ld, sM, at(J, Jend), ld, sM,
+                     at(Jend, Jend), ld, sM, st));
   }
-  return back_subst(batch, n, m, M.p, M.ld, M.stride, M.p + (long long)n * M.ld, M.ld, M.stride, st);
+  return back_subst(batch, n, m, A, ld, sM, at(0, n), ld, sM, st);
 }
 
 cudaError_t bgetrs(int batch, int n, int m, BatchedMat LU, const int* ipiv, BatchedMat R, cudaStream_t st) {
   if (batch <= 0 || n <= 0 || m <= 0) return cudaSuccess;
-  cudaError_t e;
   {
     const int cpc = 8;
     const size_t smem = (size_t)n * 12;
     static size_t smem_set = 0;
     if (smem > smem_set && smem > 48 * 1024) {
-      e = cudaFuncSetAttribute(laswp_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
+      HPS_TRY(cudaFuncSetAttribute(laswp_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       smem_set = smem;
     }
     laswp_perm_kernel<<<dim3(batch, (m + cpc - 1) / cpc), 256, smem, st>>>(ipiv, n, R.p, R.ld, R.stride, m, cpc);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    HPS_TRY(cudaGetLastError());
   }
-  for (int j0 = 0; j0 < n; j0 += kLuNB) {
-    const int nb = std::min(kLuNB, n - j0);
-    Seg seg{R.p, R.ld, R.stride, m, 1};
-    e = launch_swap_trsm(batch, n, j0, nb, LU.p, LU.ld, LU.stride, ipiv, &seg, 1, st, /*do_swaps=*/0);
-    if (e != cudaSuccess) return e;
-    const int rows = n - j0 - nb;
-    if (rows > 0) {
-      GemmArgs g;
-      g.m = rows;
-      g.n = m;
-      g.k = nb;
-      g.batch = batch;
-      g.A = LU.p + (long long)j0 * LU.ld + j0 + nb;
-      g.lda = LU.ld;
-      g.sA = LU.stride;
-      g.B = R.p + j0;
-      g.ldb = R.ld;
-      g.sB = R.stride;
-      g.C = R.p + j0 + nb;
-      g.ldc = R.ld;
-      g.sC = R.stride;
-      g.D = R.p + j0 + nb;
-      g.ldd = R.ld;
-      g.sD = R.stride;
-      g.alpha = -1.0;
-      g.beta = 1.0;
-      e = launch_dgemm(g, st);
-      if (e != cudaSuccess) return e;
+  const double* L = LU.p;
+  for (int J = 0; J < n; J += kOuterNB) {
+    const int Jend = std::min(n, J + kOuterNB);
+    for (int j0 = J; j0 < Jend; j0 += kLuNB) {
+      const int nb = std::min(kLuNB, Jend - j0);
+      Seg seg{R.p, R.ld, R.stride, m, 1};
+      HPS_TRY(launch_swap_trsm(batch, n, j0, nb, L, LU.ld, LU.stride, ipiv, &seg, 1, st, /*do_swaps=*/0));
+      HPS_TRY(gemm_sub(batch, Jend - j0 - nb, m, nb, -1.0, L + (long long)j0 * LU.ld + j0 + nb, LU.ld, LU.stride,
+                       R.p + j0, R.ld, R.stride, R.p + j0 + nb, R.ld, R.stride, st));
     }
+    HPS_TRY(gemm_sub(batch, n - Jend, m, Jend - J, -1.0, L + (long long)J * LU.ld + Jend, LU.ld, LU.stride, R.p + J,
+                     R.ld, R.stride, R.p + Jend, R.ld, R.stride, st));
   }
   return back_subst(batch, n, m, LU.p, LU.ld, LU.stride, R.p, R.ld, R.stride, st);
+}
+
+int lu_launch_count(int n, int m, bool factor) {
+  // mirrors bgetrf_aug / bgetrs above (upper bound; zero-size GEMMs are skipped)
+  int l = 1;  // stats init | laswp
+  for (int J = 0; J < n; J += kOuterNB) {
+    const int Jend = std::min(n, J + kOuterNB);
+    for (int j0 = J; j0 < Jend; j0 += kLuNB) {
+      const int nb = std::min(kLuNB, Jend - j0);
+      if (factor) l += 2 + (Jend - j0 - nb > 0 ? 1 : 0);
+      if (!factor || Jend < n + m) l += 1 + (Jend - j0 - nb > 0 ? 1 : 0);
+    }
+    if (Jend < n) l += 1;
+  }
+  if (m > 0)
+    for (int r0 = 0; r0 < n; r0 += kOuterNB) {
+      const int r1 = std::min(n, r0 + kOuterNB);
+      for (int s0 = r0; s0 < r1; s0 += kLuNB) l += 1 + (s0 > r0 ? 1 : 0);
+      if (r0 > 0) l += 1;
+    }
+  return l;
 }
 
 }  // namespace hpsk

@@ -42,4 +42,7 @@ cudaError_t bgetrs(int batch, int n, int m, BatchedMat LU, const int* ipiv, Batc
 // Largest n the panel kernel can handle (cluster limit x rows per CTA).
 int bgetrf_max_n();
 
+// kernel launches issued by bgetrf_aug (factor=true) / bgetrs (factor=false)
+int lu_launch_count(int n, int m, bool factor);
+
 }  // namespace hpsk
