@@ -1,4 +1,6 @@
 // gemm.cu -- tile-shape dispatch for the strided-batched DMMA DGEMM (gemm.cuh).
+#include <cstdlib>
+
 #include "gemm.cuh"
 
 namespace hpsk {
@@ -24,18 +26,50 @@ cudaError_t run(const GemmArgs& a, cudaStream_t st) {
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 }  // namespace
 
+// Tile configurations (CTA tile BMxBN, k-step BK, warp tile WMxWN, pipeline stages).
+// HPS_GEMM_CFG (env, developer knob) forces one config for the tuning sweep in tools/gemm_bench.py.
+static int forced_cfg() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("HPS_GEMM_CFG");
+    v = e ? atoi(e) : -1;
+  }
+  return v;
+}
+
+template <bool V>
+static cudaError_t run_cfg(int cfg, const GemmArgs& a, cudaStream_t st) {
+  switch (cfg) {
+    case 0: return run<128, 128, 16, 32, 64, 3, V>(a, st);   // 8 warps, 64 acc/thread
+    case 1: return run<128, 128, 16, 32, 32, 3, V>(a, st);   // 16 warps, 32 acc/thread
+    case 2: return run<128, 128, 32, 32, 32, 3, V>(a, st);   // 16 warps, BK=32
+    case 3: return run<128, 128, 16, 32, 32, 4, V>(a, st);   // 16 warps, 4 stages
+    case 4: return run<64, 64, 16, 32, 32, 3, V>(a, st);     // 4 warps
+    case 5: return run<64, 64, 16, 16, 32, 3, V>(a, st);     // 8 warps
+    case 6: return run<128, 64, 16, 32, 32, 3, V>(a, st);    // 8 warps
+    case 7: return run<64, 128, 16, 32, 32, 3, V>(a, st);    // 8 warps
+    case 8: return run<64, 64, 32, 16, 32, 3, V>(a, st);     // 8 warps, BK=32
+    case 9: return run<64, 64, 16, 32, 32, 4, V>(a, st);     // 4 warps, 4 stages
+    case 10: return run<64, 64, 32, 32, 32, 2, V>(a, st);    // 4 warps, BK=32, 2 stages
+    case 11: return run<64, 32, 16, 32, 32, 3, V>(a, st);    // 2 warps
+    case 12: return run<32, 64, 16, 32, 32, 3, V>(a, st);    // 2 warps
+    case 13: return run<64, 64, 16, 32, 16, 3, V>(a, st);    // 8 warps of 32x16
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st) {
   if (a.m <= 0 || a.n <= 0 || a.batch <= 0) return cudaSuccess;
   // k <= 0 runs zero k-tiles: D = beta*C
   const bool vec = aligned16(a.A) && aligned16(a.B) && (a.lda % 2 == 0) && (a.ldb % 2 == 0) &&
                    (a.sA % 2 == 0) && (a.sB % 2 == 0);
-  const long long work_tiles_big = (long long)((a.m + 127) / 128) * ((a.n + 127) / 128) * a.batch;
-  // Large single/few-matrix products: 128x128 CTA tile, 8 warps of 32x64.
-  if (a.m >= 256 && a.n >= 256 && work_tiles_big >= 148) {
-    return vec ? run<128, 128, 16, 32, 64, 3, true>(a, st) : run<128, 128, 16, 32, 64, 3, false>(a, st);
+  int cfg = forced_cfg();
+  if (cfg < 0) {
+    const long long work_tiles_big = (long long)((a.m + 127) / 128) * ((a.n + 127) / 128) * a.batch;
+    cfg = 4;
+    (void)work_tiles_big;
   }
-  // Everything else (batched small/medium matrices): 64x64 CTA tile, 4 warps of 32x32.
-  return vec ? run<64, 64, 16, 32, 32, 3, true>(a, st) : run<64, 64, 16, 32, 32, 3, false>(a, st);
+  return vec ? run_cfg<true>(cfg, a, st) : run_cfg<false>(cfg, a, st);
 }
 
 }  // namespace hpsk

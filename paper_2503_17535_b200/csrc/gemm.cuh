@@ -40,6 +40,8 @@ struct GemmCfg {
   static constexpr int kStageB = BN * kLdB;
   static constexpr int kSmemBytes = STAGES * (kStageA + kStageB) * 8;
   static constexpr int TM = WM / 8, TN = WN / 8;  // DMMA tiles per warp
+  // two CTAs per SM when the register budget allows (<= 128 regs/thread at 256 threads)
+  static constexpr int kMinBlocks = (kThreads >= 256) ? 1 : 4;
   static_assert(BM % WM == 0 && BN % WN == 0 && WM % 8 == 0 && WN % 8 == 0, "tile shape");
   static_assert(BK % 16 == 0 || BK == 8, "BK");
 };
@@ -82,7 +84,8 @@ HPS_DEV void gemm_load_stage(double* sA, double* sB, const double* A, long long 
 }
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool VEC>
-__global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, STAGES, VEC>::kThreads)
+__global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, STAGES, VEC>::kThreads,
+                                  GemmCfg<BM, BN, BK, WM, WN, STAGES, VEC>::kMinBlocks)
     dgemm_dmma_kernel(const GemmArgs p) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES, VEC>;
   extern __shared__ __align__(16) double smem[];
@@ -128,17 +131,27 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, STAGES, VEC>::kThr
 
     const double* a_s = sA + (kt % STAGES) * Cfg::kStageA;
     const double* b_s = sB + (kt % STAGES) * Cfg::kStageB;
+    // register double-buffered fragments: loads of k-slice kk+4 overlap the DMMAs of kk
+    const double* a_w = a_s + t4 * Cfg::kLdA + wm * WM + g;
+    const double* b_w = b_s + (wn * WN + g) * Cfg::kLdB + t4;
+    double af[2][Cfg::TM], bf[2][Cfg::TN];
+#pragma unroll
+    for (int i = 0; i < Cfg::TM; ++i) af[0][i] = a_w[i * 8];
+#pragma unroll
+    for (int j = 0; j < Cfg::TN; ++j) bf[0][j] = b_w[j * 8 * Cfg::kLdB];
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[Cfg::TM], bf[Cfg::TN];
+      const int cur = (kk / 4) & 1;
+      if (kk + 4 < BK) {
 #pragma unroll
-      for (int i = 0; i < Cfg::TM; ++i) af[i] = a_s[(kk + t4) * Cfg::kLdA + wm * WM + i * 8 + g];
+        for (int i = 0; i < Cfg::TM; ++i) af[cur ^ 1][i] = a_w[(kk + 4) * Cfg::kLdA + i * 8];
 #pragma unroll
-      for (int j = 0; j < Cfg::TN; ++j) bf[j] = b_s[(wn * WN + j * 8 + g) * Cfg::kLdB + kk + t4];
+        for (int j = 0; j < Cfg::TN; ++j) bf[cur ^ 1][j] = b_w[j * 8 * Cfg::kLdB + kk + 4];
+      }
 #pragma unroll
       for (int i = 0; i < Cfg::TM; ++i)
 #pragma unroll
-        for (int j = 0; j < Cfg::TN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < Cfg::TN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
     }
   }
   cp_async_wait<0>();
