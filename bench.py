@@ -182,7 +182,8 @@ def run_b200(args):
                    "sign": "corrected (v=+L^-1 f); literal differs only in the sign of f",
                    "l2": "inputs larger than L2 (each step streams > 40 GB of leaf/merge operands)",
                    "parallelism": f"{world} independent replica(s)"},
-        "stages_ms": {"build": t_build, "leaf": st["t_leaf_ms"], "merge": st["t_merge_ms"], "solve": t_solve},
+        "stages_ms": {"build": t_build, "leaf": st["t_leaf_ms"], "merge": st["t_merge_ms"], "solve": t_solve,
+                      "merge_by_depth": [round(x, 3) for x in st["t_level_ms"]]},
         "roofline": {"bound": "tensor", "kernel": "build (batched DMMA LU/TRSM/GEMM pipeline)",
                      "achieved": flops / (t_build / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": flops / (t_build / 1e3) / 1e12 / FP64_PEAK_TFLOPS, "traffic": None,

@@ -94,6 +94,8 @@ typedef struct {
   double solve_bytes;          /* algorithmic HBM bytes of the last solve */
   double device_bytes;         /* device memory held by the context */
   int launches_build, launches_solve; /* kernels launched by the last build / solve */
+  int n_levels;                /* = tree depth L */
+  double t_level_ms[24];       /* merge time of depth d (CUDA events), d = 0 .. L-1 */
 } hpsg_stats;
 
 typedef struct hpsg_ctx hpsg_ctx;

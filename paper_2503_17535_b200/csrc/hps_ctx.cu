@@ -103,6 +103,7 @@ struct hpsg_ctx {
   cudaStream_t st = nullptr;
   bool own_stream = true;
   cudaEvent_t ev[8] = {};
+  cudaEvent_t lev_ev[25] = {};  // merge level boundaries
   hpsg_tree tree{};
   hpsg_options opts{};
   hpsg::UniformTree T;
@@ -118,6 +119,11 @@ struct hpsg_ctx {
   DevBuf leaf_box, cheb, Dm, D2m, interior, exterior, P, Qi, ZQeP;
   // leaf stage
   DevBuf leafM, leafE, leafPiv, leafStats, leafBad, leafHT;
+  DevBuf leafYv, leafScratch;  // fused leaf path
+  bool fused = false;
+  int fused_grid = 0;
+  double* yv = nullptr;        // [v_i | Y_i] of leaf 0 (ni x (1+nb), ld ni)
+  long long yv_stride = 0;
   // merges
   std::vector<Level> lv;  // index d = 0..L-1
   DevBuf Bscratch;
@@ -268,9 +274,24 @@ void alloc_build(hpsg_ctx* c) {
   const hpsg::LeafOperators& o = c->ops;
   const long long nl = c->T.n_leaves();
   size_t* tot = &c->dev_bytes;
-  c->leafM.alloc(size_t(nl) * c->strideLeafM() * 8, tot);
-  c->leafE.alloc(size_t(nl) * o.ni * o.ne * 8, tot);
-  c->leafPiv.alloc(size_t(nl) * o.ni * 4, tot);
+  const char* path = getenv("HPS_LEAF_PATH");  // developer knob: "batched" forces the multi-launch path
+  c->fused = hpsk::leaf_fused_supported(o.ni, o.nb) && !(path && std::string(path) == "batched");
+  if (c->fused) {
+    int nsm = 0;
+    ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->opts.device), "sm count");
+    c->fused_grid = int(std::min<long long>(nl, nsm));
+    const long long per = hpsk::leaf_fused_scratch_per_cta(o.ni, o.ne, o.nb);
+    c->leafScratch.alloc(size_t(c->fused_grid) * per * 8, tot);
+    c->leafYv.alloc(size_t(nl) * o.ni * (1 + o.nb) * 8, tot);
+    c->yv = c->leafYv.d();
+    c->yv_stride = (long long)o.ni * (1 + o.nb);
+  } else {
+    c->leafM.alloc(size_t(nl) * c->strideLeafM() * 8, tot);
+    c->leafE.alloc(size_t(nl) * o.ni * o.ne * 8, tot);
+    c->leafPiv.alloc(size_t(nl) * o.ni * 4, tot);
+    c->yv = c->leafM.d() + (long long)o.ni * o.ni;
+    c->yv_stride = c->strideLeafM();
+  }
   c->leafStats.alloc(size_t(nl) * 3 * 8, tot);
   c->leafBad.alloc(size_t(nl) * 4, tot);
   c->leafHT.alloc(size_t(nl) * c->strideLeafHT() * 8, tot);
@@ -367,6 +388,24 @@ void run_leaf_stage(hpsg_ctx* c) {
   a.E = c->leafE.d();
   a.strideE = (long long)o.ni * o.ne;
   a.bad_point = c->leafBad.i();
+  if (c->fused) {
+    hpsk::LeafFusedArgs f{};
+    f.a = a;
+    f.P = c->P.d();
+    f.Qi = c->Qi.d();
+    f.ZQeP = c->ZQeP.d();
+    f.scratch = c->leafScratch.d();
+    f.scratch_stride = hpsk::leaf_fused_scratch_per_cta(o.ni, o.ne, o.nb);
+    f.Yv = c->leafYv.d();
+    f.strideYv = c->yv_stride;
+    f.HT = c->leafHT.d();
+    f.strideHT = c->strideLeafHT();
+    f.stats = c->leafStats.d();
+    f.n_leaves = nl;
+    ck(hpsk::launch_leaf_fused(f, c->fused_grid, c->st), "leaf_fused");
+    ++c->launches;
+    return;
+  }
   hpsk::launch_leaf_assemble(a, nl, c->st);
   ck(cudaGetLastError(), "leaf_assemble");
   ++c->launches;
@@ -592,9 +631,9 @@ void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_
   g.n = nrhs;
   g.k = 1 + o.nb;
   g.batch = nl;
-  g.A = c->leafM.d() + (long long)o.ni * o.ni;
+  g.A = c->yv;
   g.lda = o.ni;
-  g.sA = c->strideLeafM();
+  g.sA = c->yv_stride;
   g.B = c->G[Lh]->d();
   g.ldb = ldGL;
   g.sB = sGL;
@@ -694,6 +733,7 @@ int hpsg_create(const hpsg_tree* tree, const hpsg_term* terms, int n_terms, cons
     ck(cudaSetDevice(c->opts.device), "cudaSetDevice");
     ck(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking), "stream");
     for (auto& e : c->ev) ck(cudaEventCreate(&e), "event");
+    for (auto& e : c->lev_ev) ck(cudaEventCreate(&e), "event");
     if (n_terms < 0 || n_terms > hpsk::kMaxTerms)
       throw HpsError{HPSG_ERR_INVALID, hpsg::fmt("hpsg_create: 0..%d operator terms supported", hpsk::kMaxTerms)};
     setup(c.get());
@@ -737,7 +777,11 @@ int hpsg_build(hpsg_ctx* c) {
     ck(cudaEventRecord(c->ev[1], c->st), "ev");
     check_leaf_errors(c);
     ck(cudaEventRecord(c->ev[2], c->st), "ev");
-    for (int d = c->tree.L - 1; d >= 0; --d) run_merge_level(c, d);
+    for (int d = c->tree.L - 1; d >= 0; --d) {
+      ck(cudaEventRecord(c->lev_ev[d + 1], c->st), "ev");
+      run_merge_level(c, d);
+    }
+    ck(cudaEventRecord(c->lev_ev[0], c->st), "ev");
     ck(cudaEventRecord(c->ev[3], c->st), "ev");
     check_merge_errors(c);
     float a = 0, b = 0;
@@ -746,6 +790,12 @@ int hpsg_build(hpsg_ctx* c) {
     c->stats.t_leaf_ms = a;
     c->stats.t_merge_ms = b;
     c->stats.t_build_ms = a + b;
+    c->stats.n_levels = std::min(c->tree.L, 24);
+    for (int d = 0; d < c->stats.n_levels; ++d) {
+      float t = 0;
+      ck(cudaEventElapsedTime(&t, c->lev_ev[d + 1], c->lev_ev[d]), "elapsed");
+      c->stats.t_level_ms[d] = t;
+    }
     c->stats.build_flops = counted_build_flops(c);
     c->stats.launches_build = c->launches;
     c->built = true;
@@ -833,7 +883,7 @@ int hpsg_get_leaf(hpsg_ctx* c, int ord, double* Y, double* v, double* Tm, double
   return guarded(c, [&] {
     const hpsg::LeafOperators& o = c->ops;
     std::vector<double> yv(size_t(o.ni) * (1 + o.nb)), ht(size_t(o.nb) * (1 + o.nb));
-    ck(cudaMemcpy(yv.data(), c->leafM.d() + ord * c->strideLeafM() + (long long)o.ni * o.ni, yv.size() * 8,
+    ck(cudaMemcpy(yv.data(), c->yv + ord * c->yv_stride, yv.size() * 8,
                   cudaMemcpyDeviceToHost),
        "leaf D2H");
     ck(cudaMemcpy(ht.data(), c->leafHT.d() + ord * c->strideLeafHT(), ht.size() * 8, cudaMemcpyDeviceToHost),
@@ -923,6 +973,8 @@ void hpsg_destroy(hpsg_ctx* c) {
   {
     hpsg_ctx* tmp = c;
     for (auto& e : tmp->ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : tmp->lev_ev)
       if (e) cudaEventDestroy(e);
     cudaStream_t st = tmp->own_stream ? tmp->st : nullptr;
     delete tmp;  // frees device buffers

@@ -2,153 +2,19 @@
 #include <climits>
 
 #include "hps_kernels.cuh"
+#include "leaf_common.cuh"
 
 namespace hpsk {
 
 namespace {
 
 constexpr int kAsmThreads = 256;
-constexpr int kMaxPts = 512;  // p^d <= 512 (2D p <= 22, 3D p <= 8)
-constexpr int kMaxP = 24;
-
-__device__ double bumps(const DevField& f, const double* x, int dim) {
-  double s = 0.0;
-  for (int j = 0; j < f.n_centers; ++j) {
-    double r2 = 0.0;
-    for (int k = 0; k < dim; ++k) {
-      const double d = x[k] - f.centers[3 * j + k];
-      r2 += d * d;
-    }
-    s += exp(-f.c[2] * r2);
-  }
-  return s;
-}
-
-// Device evaluation of the built-in fields (hps_cuda.h HPSG_FIELD_*).
-__device__ double eval_field(const DevField& f, const double* x, int dim, long long leaf, int pt, int npts) {
-  const double* c = f.c;
-  switch (f.kind) {
-    case 0: return c[0];
-    case 1: return c[0] + c[1] * bumps(f, x, dim);
-    case 2: return c[0] * sin(c[1] * x[0] + c[2] * x[1] + c[3] * x[2] + c[4]);
-    case 3: return c[0] * cos(c[1] * x[0] + c[2] * x[1] + c[3] * x[2] + c[4]);
-    case 4: return c[0] * bumps(f, x, dim) * sin(c[3] * x[0] + c[4] * x[1] + c[5] * x[2] + c[6]);
-    case 5: {  // proj/src/problems.cpp:50-66
-      const double X = x[0], Y = x[1];
-      const double ux = 5.0 * exp(5.0 * X) * sin(5.0 * Y) + 10.0 * M_PI * cos(10.0 * M_PI * X) * sin(M_PI * Y);
-      const double uy = 5.0 * exp(5.0 * X) * cos(5.0 * Y) + M_PI * sin(10.0 * M_PI * X) * cos(M_PI * Y);
-      const double lap = -101.0 * M_PI * M_PI * sin(10.0 * M_PI * X) * sin(M_PI * Y);
-      return lap - cos(5.0 * Y) * ux + sin(5.0 * Y) * uy;
-    }
-    case 6: return f.samples[leaf * npts + pt];
-    default: return __longlong_as_double(0x7ff8000000000000ULL);
-  }
-}
-
-__device__ __forceinline__ void decode(int idx, int p, int dim, int* c) {
-  if (dim == 2) {
-    c[0] = idx / p;
-    c[1] = idx % p;
-    c[2] = 0;
-  } else {
-    c[0] = idx / (p * p);
-    c[1] = (idx / p) % p;
-    c[2] = idx % p;
-  }
-}
 
 __global__ void __launch_bounds__(kAsmThreads) leaf_assemble_kernel(const LeafAsmArgs a) {
-  __shared__ double coef[kMaxTerms][kMaxPts];
-  __shared__ double fsrc[kMaxPts];
-  __shared__ double sD[kMaxP * kMaxP], sD2[kMaxP * kMaxP];
-  __shared__ int bad;
+  __shared__ LeafAsmSmem s;
   const long long leaf = blockIdx.x;
-  const int tid = threadIdx.x, p = a.p, dim = a.dim, n = a.n;
-  if (tid == 0) bad = INT_MAX;
-  for (int e = tid; e < p * p; e += kAsmThreads) sD[e] = a.D[e], sD2[e] = a.D2[e];
-  const double* box = a.leaf_box + leaf * 6;
-  // leaf_cheb_points (proj/src/mesh.cpp:320-336): 0.5(lo+hi) + 0.5(hi-lo) t, no FMA contraction
-  for (int i = tid; i < n; i += kAsmThreads) {
-    int ci[3];
-    decode(i, p, dim, ci);
-    double x[3] = {0.0, 0.0, 0.0};
-    for (int k = 0; k < dim; ++k)
-      x[k] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(box[k], box[3 + k])),
-                       __dmul_rn(__dmul_rn(0.5, __dsub_rn(box[3 + k], box[k])), a.cheb[ci[k]]));
-    for (int t = 0; t < a.nterms; ++t) {
-      const double v = eval_field(a.terms[t].f, x, dim, leaf, i, n);
-      coef[t][i] = v;
-      if (!isfinite(v)) atomicMin(&bad, i);
-    }
-    fsrc[i] = a.has_source ? eval_field(a.source, x, dim, leaf, i, n) : 0.0;
-  }
-  __syncthreads();
-  if (tid == 0) a.bad_point[leaf] = bad;  // INT_MAX: all samples finite
-
-  const double s1 = a.scale, s2 = a.scale * a.scale;
-  double* M = a.M + leaf * a.strideM;
-  double* E = a.E + leaf * a.strideE;
-  const int ni = a.ni, ncol = ni + a.ne;
-  // L(ii, :) entry by entry; accumulation order = term order, axis order (local_solve.cpp:63-83)
-  for (int e = tid; e < ni * ncol; e += kAsmThreads) {
-    const int r = e % ni, cj = e / ni;
-    const int gi = a.interior[r];
-    const int gj = cj < ni ? a.interior[cj] : a.exterior[cj - ni];
-    int ii[3], jj[3];
-    decode(gi, p, dim, ii);
-    decode(gj, p, dim, jj);
-    bool same[3];
-    for (int k = 0; k < 3; ++k) same[k] = ii[k] == jj[k];
-    double val = 0.0;
-    for (int t = 0; t < a.nterms; ++t) {
-      const DevTerm& tm = a.terms[t];
-      const double c = coef[t][gi];
-      switch (tm.role) {
-        case 0:  // laplacian: c s^2 sum_a D2_a
-          for (int ax = 0; ax < dim; ++ax) {
-            bool ok = true;
-            for (int k = 0; k < dim; ++k)
-              if (k != ax && !same[k]) ok = false;
-            if (ok) val = __dadd_rn(val, __dmul_rn(s2, __dmul_rn(c, sD2[jj[ax] * p + ii[ax]])));
-          }
-          break;
-        case 1: {  // gradient: c s D_axis
-          const int ax = tm.axis;
-          bool ok = true;
-          for (int k = 0; k < dim; ++k)
-            if (k != ax && !same[k]) ok = false;
-          if (ok) val = __dadd_rn(val, __dmul_rn(s1, __dmul_rn(c, sD[jj[ax] * p + ii[ax]])));
-          break;
-        }
-        case 2:  // zeroth: diag(c)
-          if (gi == gj) val = __dadd_rn(val, c);
-          break;
-        default: {  // second_order
-          const int a1 = tm.axis, a2 = tm.axis2;
-          if (a1 == a2) {
-            bool ok = true;
-            for (int k = 0; k < dim; ++k)
-              if (k != a1 && !same[k]) ok = false;
-            if (ok) val = __dadd_rn(val, __dmul_rn(s2, __dmul_rn(c, sD2[jj[a1] * p + ii[a1]])));
-          } else {
-            bool ok = true;
-            for (int k = 0; k < dim; ++k)
-              if (k != a1 && k != a2 && !same[k]) ok = false;
-            if (ok) {
-              const double d = __dmul_rn(sD[jj[a1] * p + ii[a1]], sD[jj[a2] * p + ii[a2]]);
-              val = __dadd_rn(val, __dmul_rn(s2, __dmul_rn(c, d)));
-            }
-          }
-        }
-      }
-    }
-    if (cj < ni)
-      M[(long long)cj * ni + r] = val;
-    else
-      E[(long long)(cj - ni) * ni + r] = val;
-  }
-  // RHS column 0 of the augmented block: sgn * f(I_i)
-  for (int r = tid; r < ni; r += kAsmThreads) M[(long long)ni * ni + r] = a.fsign * fsrc[a.interior[r]];
+  leaf_assemble_block(a, leaf, a.M + leaf * a.strideM, a.ni, a.E + leaf * a.strideE, s);
+  if (threadIdx.x == 0) a.bad_point[leaf] = s.bad;  // INT_MAX: all samples finite
 }
 
 constexpr int kGatherThreads = 256;

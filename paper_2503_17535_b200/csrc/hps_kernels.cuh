@@ -46,6 +46,26 @@ struct LeafAsmArgs {
 };
 void launch_leaf_assemble(const LeafAsmArgs& a, int n_leaves, cudaStream_t st);
 
+// Fused stage 1 (leaf_fused.cu): assembly + -L_ie P + GEPP/solve + [h|T] per leaf in one
+// persistent kernel over an L2-resident per-CTA workspace.
+struct LeafFusedArgs {
+  LeafAsmArgs a;            // M/E fields unused; bad_point used
+  const double* P;          // ne x nb
+  const double* Qi;         // nb x ni
+  const double* ZQeP;       // nb x (1 + nb) = [0 | Q_e P]
+  double* scratch;          // per CTA: ni x (ni+1+nb) + ni x ne
+  long long scratch_stride;
+  double* Yv;               // per leaf: ni x (1 + nb) = [v_i | Y_i]
+  long long strideYv;
+  double* HT;               // per leaf: nb x (1 + nb) = [h | T]
+  long long strideHT;
+  double* stats;            // per leaf: min|u_ii|, max|u_ii|, first zero pivot (-1)
+  long long n_leaves;
+};
+bool leaf_fused_supported(int ni, int nb);
+long long leaf_fused_scratch_per_cta(int ni, int ne, int nb);
+cudaError_t launch_leaf_fused(const LeafFusedArgs& f, int grid, cudaStream_t st);
+
 // ---- stage 2: merge operand gather ------------------------------------------
 // Reference block assembly, proj/src/merge.cpp:226-278: child DtN blocks summed
 // into [D | h_int | C], B and [h_ext | A] by destination-driven gathers (no atomics).

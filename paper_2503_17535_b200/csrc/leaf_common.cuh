@@ -1,0 +1,210 @@
+// leaf_common.cuh -- device-side leaf operator assembly shared by the batched
+// (leaf_assemble_kernel) and fused (leaf_fused_kernel) leaf stages.
+//
+// Reference: discretize_operator (proj/src/local_solve.cpp:44-86) restricted to
+// the interior rows, and the source sampling of HpsSolver::build_leaf
+// (proj/src/solver.cpp:49-57).  Accumulation order per entry = term order, axis
+// order, with the reference's s^k * (c_i * op_ij) rounding (no FMA contraction).
+#pragma once
+
+#include <climits>
+
+#include "hps_kernels.cuh"
+
+namespace hpsk {
+
+constexpr int kLeafMaxPts = 512;  // p^d <= 512 (2D p <= 22, 3D p <= 8)
+constexpr int kLeafMaxP = 24;
+
+__device__ __forceinline__ double leaf_bumps(const DevField& f, const double* x, int dim) {
+  double s = 0.0;
+  for (int j = 0; j < f.n_centers; ++j) {
+    double r2 = 0.0;
+    for (int k = 0; k < dim; ++k) {
+      const double d = x[k] - f.centers[3 * j + k];
+      r2 += d * d;
+    }
+    s += exp(-f.c[2] * r2);
+  }
+  return s;
+}
+
+// Device evaluation of the built-in fields (hps_cuda.h HPSG_FIELD_*).
+__device__ __forceinline__ double eval_field(const DevField& f, const double* x, int dim, long long leaf, int pt,
+                                             int npts) {
+  const double* c = f.c;
+  switch (f.kind) {
+    case 0: return c[0];
+    case 1: return c[0] + c[1] * leaf_bumps(f, x, dim);
+    case 2: return c[0] * sin(c[1] * x[0] + c[2] * x[1] + c[3] * x[2] + c[4]);
+    case 3: return c[0] * cos(c[1] * x[0] + c[2] * x[1] + c[3] * x[2] + c[4]);
+    case 4: return c[0] * leaf_bumps(f, x, dim) * sin(c[3] * x[0] + c[4] * x[1] + c[5] * x[2] + c[6]);
+    case 5: {  // proj/src/problems.cpp:50-66
+      const double X = x[0], Y = x[1];
+      const double ux = 5.0 * exp(5.0 * X) * sin(5.0 * Y) + 10.0 * M_PI * cos(10.0 * M_PI * X) * sin(M_PI * Y);
+      const double uy = 5.0 * exp(5.0 * X) * cos(5.0 * Y) + M_PI * sin(10.0 * M_PI * X) * cos(M_PI * Y);
+      const double lap = -101.0 * M_PI * M_PI * sin(10.0 * M_PI * X) * sin(M_PI * Y);
+      return lap - cos(5.0 * Y) * ux + sin(5.0 * Y) * uy;
+    }
+    case 6: return f.samples[leaf * npts + pt];
+    default: return __longlong_as_double(0x7ff8000000000000ULL);
+  }
+}
+
+__device__ __forceinline__ void leaf_decode(int idx, int p, int dim, int* c) {
+  if (dim == 2) {
+    c[0] = idx / p;
+    c[1] = idx % p;
+    c[2] = 0;
+  } else {
+    c[0] = idx / (p * p);
+    c[1] = (idx / p) % p;
+    c[2] = idx % p;
+  }
+}
+
+struct LeafAsmSmem {
+  double coef[kMaxTerms][kLeafMaxPts];
+  double fsrc[kLeafMaxPts];
+  double D[kLeafMaxP * kLeafMaxP], D2[kLeafMaxP * kLeafMaxP];
+  int pos[kLeafMaxPts];  // tensor index -> interior position r (>= 0) or -(exterior position) - 1
+  int bad;
+};
+
+// Value of the operator entry L(gi, gj) accumulated in the reference order (term, then axis):
+// proj/src/local_solve.cpp:63-83, each contribution rounded as s^k * (c_i * op_ij).
+__device__ __forceinline__ double leaf_entry(const LeafAsmArgs& a, const LeafAsmSmem& s, int gi, const int* ii,
+                                             int gj, const int* jj) {
+  const int p = a.p, dim = a.dim;
+  const double s1 = a.scale, s2 = a.scale * a.scale;
+  bool same[3];
+  for (int k = 0; k < 3; ++k) same[k] = ii[k] == jj[k];
+  double val = 0.0;
+  for (int t = 0; t < a.nterms; ++t) {
+    const DevTerm& tm = a.terms[t];
+    const double c = s.coef[t][gi];
+    switch (tm.role) {
+      case 0:  // laplacian: c s^2 sum_a D2_a
+        for (int ax = 0; ax < dim; ++ax) {
+          bool ok = true;
+          for (int k = 0; k < dim; ++k)
+            if (k != ax && !same[k]) ok = false;
+          if (ok) val = __dadd_rn(val, __dmul_rn(s2, __dmul_rn(c, s.D2[jj[ax] * p + ii[ax]])));
+        }
+        break;
+      case 1: {  // gradient: c s D_axis
+        const int ax = tm.axis;
+        bool ok = true;
+        for (int k = 0; k < dim; ++k)
+          if (k != ax && !same[k]) ok = false;
+        if (ok) val = __dadd_rn(val, __dmul_rn(s1, __dmul_rn(c, s.D[jj[ax] * p + ii[ax]])));
+        break;
+      }
+      case 2:  // zeroth: diag(c)
+        if (gi == gj) val = __dadd_rn(val, c);
+        break;
+      default: {  // second_order
+        const int a1 = tm.axis, a2 = tm.axis2;
+        if (a1 == a2) {
+          bool ok = true;
+          for (int k = 0; k < dim; ++k)
+            if (k != a1 && !same[k]) ok = false;
+          if (ok) val = __dadd_rn(val, __dmul_rn(s2, __dmul_rn(c, s.D2[jj[a1] * p + ii[a1]])));
+        } else {
+          bool ok = true;
+          for (int k = 0; k < dim; ++k)
+            if (k != a1 && k != a2 && !same[k]) ok = false;
+          if (ok) {
+            const double d = __dmul_rn(s.D[jj[a1] * p + ii[a1]], s.D[jj[a2] * p + ii[a2]]);
+            val = __dadd_rn(val, __dmul_rn(s2, __dmul_rn(c, d)));
+          }
+        }
+      }
+    }
+  }
+  return val;
+}
+
+// One CTA assembles one leaf: M[:, 0:ni] = L(I_i, I_i), M[:, ni] = sgn * f(I_i) (ld = ldM),
+// E = L(I_i, I_e) (ld = ni).  Returns (via s.bad) the first non-finite coefficient point or INT_MAX.
+// Without mixed second-order terms the operator row of point i is supported on the dim grid
+// lines through i, so the block is zero-filled and only those (dim*(p-1)+1 per row) entries are
+// evaluated; otherwise every entry is evaluated.
+__device__ __forceinline__ void leaf_assemble_block(const LeafAsmArgs& a, long long leaf, double* M, long long ldM,
+                                                    double* E, LeafAsmSmem& s) {
+  const int tid = threadIdx.x, nthr = blockDim.x, p = a.p, dim = a.dim, n = a.n;
+  if (tid == 0) s.bad = INT_MAX;
+  for (int e = tid; e < p * p; e += nthr) s.D[e] = a.D[e], s.D2[e] = a.D2[e];
+  for (int r = tid; r < a.ni; r += nthr) s.pos[a.interior[r]] = r;
+  for (int r = tid; r < a.ne; r += nthr) s.pos[a.exterior[r]] = -r - 1;
+  const double* box = a.leaf_box + leaf * 6;
+  // leaf_cheb_points (proj/src/mesh.cpp:320-336): 0.5(lo+hi) + 0.5(hi-lo) t, no FMA contraction
+  for (int i = tid; i < n; i += nthr) {
+    int ci[3];
+    leaf_decode(i, p, dim, ci);
+    double x[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < dim; ++k)
+      x[k] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(box[k], box[3 + k])),
+                       __dmul_rn(__dmul_rn(0.5, __dsub_rn(box[3 + k], box[k])), a.cheb[ci[k]]));
+    for (int t = 0; t < a.nterms; ++t) {
+      const double v = eval_field(a.terms[t].f, x, dim, leaf, i, n);
+      s.coef[t][i] = v;
+      if (!isfinite(v)) atomicMin(&s.bad, i);
+    }
+    s.fsrc[i] = a.has_source ? eval_field(a.source, x, dim, leaf, i, n) : 0.0;
+  }
+  bool mixed = false;
+  for (int t = 0; t < a.nterms; ++t)
+    if (a.terms[t].role == 3 && a.terms[t].axis != a.terms[t].axis2) mixed = true;
+  const int ni = a.ni, ne = a.ne;
+  if (mixed) {
+    __syncthreads();
+    for (int e = tid; e < ni * (ni + ne); e += nthr) {
+      const int r = e % ni, cj = e / ni;
+      const int gi = a.interior[r], gj = cj < ni ? a.interior[cj] : a.exterior[cj - ni];
+      int ii[3], jj[3];
+      leaf_decode(gi, p, dim, ii);
+      leaf_decode(gj, p, dim, jj);
+      const double v = leaf_entry(a, s, gi, ii, gj, jj);
+      if (cj < ni)
+        M[(long long)cj * ldM + r] = v;
+      else
+        E[(long long)(cj - ni) * ni + r] = v;
+    }
+  } else {
+    // zero fill (coalesced, 16-byte stores where aligned)
+    if (ldM == ni && (ni % 2) == 0 && ((reinterpret_cast<uintptr_t>(M) & 15) == 0)) {
+      double2* m2 = reinterpret_cast<double2*>(M);
+      for (int e = tid; e < ni * ni / 2; e += nthr) m2[e] = make_double2(0.0, 0.0);
+    } else {
+      for (int e = tid; e < ni * ni; e += nthr) M[(long long)(e / ni) * ldM + e % ni] = 0.0;
+    }
+    for (int e = tid; e < ni * ne; e += nthr) E[e] = 0.0;
+    __syncthreads();
+    // entries on the grid lines through each interior point; the diagonal once
+    const int per_row = dim * (p - 1) + 1;
+    for (int e = tid; e < ni * per_row; e += nthr) {
+      const int r = e % ni, w = e / ni;
+      const int gi = a.interior[r];
+      int ii[3], jj[3];
+      leaf_decode(gi, p, dim, ii);
+      jj[0] = ii[0], jj[1] = ii[1], jj[2] = ii[2];
+      if (w > 0) {
+        const int ax = (w - 1) / (p - 1), k0 = (w - 1) % (p - 1);
+        jj[ax] = k0 < ii[ax] ? k0 : k0 + 1;  // skip the diagonal
+      }
+      const int gj = dim == 2 ? jj[0] * p + jj[1] : (jj[0] * p + jj[1]) * p + jj[2];
+      const double v = leaf_entry(a, s, gi, ii, gj, jj);
+      const int q = s.pos[gj];
+      if (q >= 0)
+        M[(long long)q * ldM + r] = v;
+      else
+        E[(long long)(-q - 1) * ni + r] = v;
+    }
+  }
+  // RHS column 0 of the augmented block: sgn * f(I_i)
+  for (int r = tid; r < ni; r += nthr) M[(long long)ni * ldM + r] = a.fsign * s.fsrc[a.interior[r]];
+  __syncthreads();
+}
+
+}  // namespace hpsk

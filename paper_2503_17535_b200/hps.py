@@ -58,7 +58,8 @@ class _Stats(C.Structure):
                 ("tree_depth", C.c_int), ("min_rcond", C.c_double), ("ill_conditioned", C.c_int),
                 ("t_build_ms", C.c_double), ("t_leaf_ms", C.c_double), ("t_merge_ms", C.c_double),
                 ("t_solve_ms", C.c_double), ("build_flops", C.c_double), ("solve_bytes", C.c_double),
-                ("device_bytes", C.c_double), ("launches_build", C.c_int), ("launches_solve", C.c_int)]
+                ("device_bytes", C.c_double), ("launches_build", C.c_int), ("launches_solve", C.c_int),
+                ("n_levels", C.c_int), ("t_level_ms", C.c_double * 24)]
 
 
 _lib = None
@@ -293,4 +294,6 @@ class HpsSolver:
     def stats(self):
         s = _Stats()
         self._check(lib().hpsg_get_stats(self._h, C.byref(s)), "stats")
-        return {k: getattr(s, k) for k, _ in _Stats._fields_}
+        out = {k: getattr(s, k) for k, _ in _Stats._fields_}
+        out["t_level_ms"] = list(s.t_level_ms)[:s.n_levels]
+        return out

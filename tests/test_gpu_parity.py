@@ -150,3 +150,17 @@ def test_errors():
     assert e.value.code == H.hps.HPSG_ERR_STATE
     with pytest.raises(H.HpsError):
         H.HpsSolver(H.build_uniform_tree(-1, 1, 2, 2, 3), [H.Term(H.ROLE_LAPLACIAN, H.Field.const(1.0))])
+
+
+@pytest.mark.parametrize("name,p,L", [("poisson2d", 16, 3), ("helmholtz_bumps", 16, 2), ("laplace3d", 6, 1)])
+def test_fused_leaf_path_equals_batched(name, p, L, monkeypatch):
+    """The persistent fused leaf kernel and the multi-launch batched leaf path agree."""
+    prob = PR.CATALOG[name]()
+    a = gpu_solver(prob, p, L)
+    monkeypatch.setenv("HPS_LEAF_PATH", "batched")
+    b = gpu_solver(prob, p, L)
+    g = prob.boundary(a.root_boundary_points())
+    assert rel(a.solve(g), b.solve(g)) < 1e-11
+    for o in (0, a.tree.n_leaves - 1):
+        for x, y in zip(a.get_leaf(o), b.get_leaf(o)):
+            assert rel(x, y) < 1e-11
