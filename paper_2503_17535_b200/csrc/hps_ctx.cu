@@ -275,11 +275,15 @@ void alloc_build(hpsg_ctx* c) {
   const long long nl = c->T.n_leaves();
   size_t* tot = &c->dev_bytes;
   const char* path = getenv("HPS_LEAF_PATH");  // developer knob: "batched" forces the multi-launch path
-  c->fused = hpsk::leaf_fused_supported(o.ni, o.nb) && !(path && std::string(path) == "batched");
+  bool mixed = false;
+  for (int i = 0; i < c->nterms; ++i)
+    if (c->terms[i].role == HPSG_ROLE_SECOND_ORDER && c->terms[i].axis != c->terms[i].axis2) mixed = true;
+  c->fused = hpsk::leaf_fused_supported(o.n, o.p, o.ni, o.nb, c->tree.dim, mixed) &&
+             !(path && std::string(path) == "batched");
   if (c->fused) {
     int nsm = 0;
     ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->opts.device), "sm count");
-    c->fused_grid = int(std::min<long long>(nl, nsm));
+    c->fused_grid = int(std::min<long long>(nl, (long long)nsm * hpsk::leaf_fused_ctas_per_sm()));
     const long long per = hpsk::leaf_fused_scratch_per_cta(o.ni, o.ne, o.nb);
     c->leafScratch.alloc(size_t(c->fused_grid) * per * 8, tot);
     c->leafYv.alloc(size_t(nl) * o.ni * (1 + o.nb) * 8, tot);

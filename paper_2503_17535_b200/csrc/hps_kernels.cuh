@@ -62,7 +62,8 @@ struct LeafFusedArgs {
   double* stats;            // per leaf: min|u_ii|, max|u_ii|, first zero pivot (-1)
   long long n_leaves;
 };
-bool leaf_fused_supported(int ni, int nb);
+bool leaf_fused_supported(int n, int p, int ni, int nb, int dim, bool mixed_terms);
+int leaf_fused_ctas_per_sm();
 long long leaf_fused_scratch_per_cta(int ni, int ne, int nb);
 cudaError_t launch_leaf_fused(const LeafFusedArgs& f, int grid, cudaStream_t st);
 

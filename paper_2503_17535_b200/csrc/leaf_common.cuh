@@ -63,17 +63,20 @@ __device__ __forceinline__ void leaf_decode(int idx, int p, int dim, int* c) {
   }
 }
 
-struct LeafAsmSmem {
-  double coef[kMaxTerms][kLeafMaxPts];
-  double fsrc[kLeafMaxPts];
-  double D[kLeafMaxP * kLeafMaxP], D2[kLeafMaxP * kLeafMaxP];
-  int pos[kLeafMaxPts];  // tensor index -> interior position r (>= 0) or -(exterior position) - 1
+template <int MAXPTS, int MAXP>
+struct LeafAsmSmemT {
+  double coef[kMaxTerms][MAXPTS];
+  double fsrc[MAXPTS];
+  double D[MAXP * MAXP], D2[MAXP * MAXP];
+  int pos[MAXPTS];  // tensor index -> interior position r (>= 0) or -(exterior position) - 1
   int bad;
 };
+using LeafAsmSmem = LeafAsmSmemT<kLeafMaxPts, kLeafMaxP>;
 
 // Value of the operator entry L(gi, gj) accumulated in the reference order (term, then axis):
 // proj/src/local_solve.cpp:63-83, each contribution rounded as s^k * (c_i * op_ij).
-__device__ __forceinline__ double leaf_entry(const LeafAsmArgs& a, const LeafAsmSmem& s, int gi, const int* ii,
+template <class SM>
+__device__ __forceinline__ double leaf_entry(const LeafAsmArgs& a, const SM& s, int gi, const int* ii,
                                              int gj, const int* jj) {
   const int p = a.p, dim = a.dim;
   const double s1 = a.scale, s2 = a.scale * a.scale;
@@ -130,8 +133,14 @@ __device__ __forceinline__ double leaf_entry(const LeafAsmArgs& a, const LeafAsm
 // Without mixed second-order terms the operator row of point i is supported on the dim grid
 // lines through i, so the block is zero-filled and only those (dim*(p-1)+1 per row) entries are
 // evaluated; otherwise every entry is evaluated.
+//
+// enz_idx/enz_val (optional, operators without mixed terms only): instead of writing the
+// exterior block E, record each interior row's 2*dim exterior line neighbours at slot
+// r*2*dim + 2*axis + (neighbour at node 0 ? 0 : 1) as (exterior position, value).
+template <class SM>
 __device__ __forceinline__ void leaf_assemble_block(const LeafAsmArgs& a, long long leaf, double* M, long long ldM,
-                                                    double* E, LeafAsmSmem& s) {
+                                                    double* E, SM& s, int* enz_idx = nullptr,
+                                                    double* enz_val = nullptr) {
   const int tid = threadIdx.x, nthr = blockDim.x, p = a.p, dim = a.dim, n = a.n;
   if (tid == 0) s.bad = INT_MAX;
   for (int e = tid; e < p * p; e += nthr) s.D[e] = a.D[e], s.D2[e] = a.D2[e];
@@ -179,7 +188,8 @@ __device__ __forceinline__ void leaf_assemble_block(const LeafAsmArgs& a, long l
     } else {
       for (int e = tid; e < ni * ni; e += nthr) M[(long long)(e / ni) * ldM + e % ni] = 0.0;
     }
-    for (int e = tid; e < ni * ne; e += nthr) E[e] = 0.0;
+    if (!enz_idx)
+      for (int e = tid; e < ni * ne; e += nthr) E[e] = 0.0;
     __syncthreads();
     // entries on the grid lines through each interior point; the diagonal once
     const int per_row = dim * (p - 1) + 1;
@@ -196,10 +206,16 @@ __device__ __forceinline__ void leaf_assemble_block(const LeafAsmArgs& a, long l
       const int gj = dim == 2 ? jj[0] * p + jj[1] : (jj[0] * p + jj[1]) * p + jj[2];
       const double v = leaf_entry(a, s, gi, ii, gj, jj);
       const int q = s.pos[gj];
-      if (q >= 0)
+      if (q >= 0) {
         M[(long long)q * ldM + r] = v;
-      else
+      } else if (enz_idx) {
+        const int ax = (w - 1) / (p - 1);
+        const int slot = r * 2 * dim + 2 * ax + (jj[ax] == 0 ? 0 : 1);
+        enz_idx[slot] = -q - 1;
+        enz_val[slot] = v;
+      } else {
         E[(long long)(-q - 1) * ni + r] = v;
+      }
     }
   }
   // RHS column 0 of the augmented block: sgn * f(I_i)

@@ -134,7 +134,7 @@ def test_sampled_field_equals_builtin():
     b = H.HpsSolver(tree, terms, prob.source)
     b.build()
     g = prob.boundary(a.root_boundary_points())
-    assert rel(b.solve(g), a.solve(g)) < 1e-12
+    assert rel(b.solve(g), a.solve(g)) < 1e-11  # 1-ulp coefficient differences, Helmholtz-conditioned
 
 
 def test_errors():
