@@ -28,6 +28,7 @@
 #include "geometry.hpp"
 #include "hps_kernels.cuh"
 #include "lu.cuh"
+#include "gemv.cuh"
 
 using hpsk::BatchedMat;
 using hpsk::GemmArgs;
@@ -130,7 +131,7 @@ struct hpsg_ctx {
   // solve workspace
   int ws_nrhs = 0;
   std::vector<std::unique_ptr<DevBuf>> G, GI;
-  DevBuf Ui, Ue, g_in, u_out, lg_out;
+  DevBuf Ui, Ue, g_in, u_out, lg_out, gemv_scratch;
   bool built = false;
   hpsg_stats stats{};
   int launches = 0;
@@ -166,6 +167,29 @@ void gemm(hpsg_ctx* c, const GemmArgs& g) {
 }
 
 int lu_launches(int n, int m, bool factor) { return hpsk::lu_launch_count(n, m, factor); }
+
+// Solve-time products: a streaming GEMV for up to 4 right-hand sides (HBM-bound), the DMMA
+// GEMM beyond that (multi-RHS solves become compute-bound, config 3).
+void matvecs(hpsg_ctx* c, const GemmArgs& g) {
+  if (g.n > 4) return gemm(c, g);
+  hpsk::GemvArgs v;
+  v.m = g.m;
+  v.k = g.k;
+  v.batch = g.batch;
+  v.nv = g.n;
+  v.A = g.A;
+  v.lda = g.lda;
+  v.sA = g.sA;
+  v.x = g.B;
+  v.ldx = g.ldb;
+  v.sx = g.sB;
+  v.y = g.D;
+  v.ldy = g.ldd;
+  v.sy = g.sD;
+  v.alpha = g.alpha;
+  v.beta = g.beta;
+  ck(hpsk::launch_gemv(v, c->gemv_scratch.d(), c->gemv_scratch.bytes / 8, c->st, &c->launches), "gemv");
+}
 
 hpsk::DevField make_dev_field(hpsg_ctx* c, const hpsg_field& f, bool is_source) {
   hpsk::DevField d{};
@@ -552,6 +576,7 @@ void ensure_solve_ws(hpsg_ctx* c, int nrhs) {
   const long long nl = c->T.n_leaves();
   c->Ui.alloc(size_t(nl) * c->ops.ni * nrhs * 8, tot);
   c->Ue.alloc(size_t(nl) * c->ops.ne * nrhs * 8, tot);
+  c->gemv_scratch.alloc(size_t(8) << 20, tot);  // split-k partial sums (64 MB)
   c->ws_nrhs = nrhs;
 }
 
@@ -581,7 +606,7 @@ void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_
       g.ldd = L.n_int;
       g.alpha = 1.0;
       g.beta = 0.0;
-      gemm(c, g);
+      matvecs(c, g);
       BatchedMat LU{L.MD.d(), L.n_int, L.strideMD()};
       BatchedMat R{c->GI[0]->d(), L.n_int, sGI};
       ck(hpsk::bgetrs(1, L.n_int, nrhs, LU, L.piv.i(), R, c->st), "root getrs");
@@ -606,7 +631,7 @@ void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_
       g.sD = sGI;
       g.alpha = -1.0;
       g.beta = 0.0;
-      gemm(c, g);
+      matvecs(c, g);
     }
     hpsk::ScatterArgs s{};
     s.nchild = L.mt.nchild;
@@ -644,7 +669,7 @@ void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_
   g.D = c->Ui.d();
   g.ldd = o.ni;
   g.sD = (long long)o.ni * nrhs;
-  gemm(c, g);
+  matvecs(c, g);
   GemmArgs e;
   e.m = o.ne;
   e.n = nrhs;
@@ -659,7 +684,7 @@ void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_
   e.D = c->Ue.d();
   e.ldd = o.ne;
   e.sD = (long long)o.ne * nrhs;
-  gemm(c, e);
+  matvecs(c, e);
   hpsk::LeafOutArgs lo{};
   lo.ni = o.ni;
   lo.ne = o.ne;

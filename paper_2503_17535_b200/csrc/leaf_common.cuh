@@ -146,6 +146,7 @@ __device__ __forceinline__ void leaf_assemble_block(const LeafAsmArgs& a, long l
   for (int e = tid; e < p * p; e += nthr) s.D[e] = a.D[e], s.D2[e] = a.D2[e];
   for (int r = tid; r < a.ni; r += nthr) s.pos[a.interior[r]] = r;
   for (int r = tid; r < a.ne; r += nthr) s.pos[a.exterior[r]] = -r - 1;
+  __syncthreads();  // s.bad initialised before any atomicMin
   const double* box = a.leaf_box + leaf * 6;
   // leaf_cheb_points (proj/src/mesh.cpp:320-336): 0.5(lo+hi) + 0.5(hi-lo) t, no FMA contraction
   for (int i = tid; i < n; i += nthr) {

@@ -1,6 +1,6 @@
 // leaf_fused.cu -- stage 1 (leaf-local solves) as ONE persistent kernel.
 //
-// One CTA (16 warps) per SM walks leaves blockIdx.x, +gridDim.x, ...  For every
+// Two CTAs (8 warps each) per SM walk leaves blockIdx.x, +gridDim.x, ...  For every
 // leaf it runs the whole reference local solve (proj/src/local_solve.cpp:111-143
 // with discretize_operator :44-86) on an L2-resident per-CTA workspace
 // W = [L_ii | sgn f_i | -L_ie P] (ni x (ni+1+nb)), keeping every DMMA operand in
@@ -28,21 +28,21 @@ namespace hpsk {
 
 namespace {
 
-constexpr int kFT = 512;          // threads per CTA
+constexpr int kFT = 256;          // threads per CTA (two CTAs per SM)
 constexpr int kFW = kFT / 32;     // warps
 constexpr int kNB = 32;           // panel width / k chunk
-constexpr int kMaxNI = 208;       // interior points (2D p <= 16, 3D p <= 7)
+constexpr int kMaxNI = 196;       // interior points (2D p <= 16)
 constexpr int kMaxCols = 256;     // ni + 1 + nb
-constexpr int kPLD = kMaxNI + 4;  // A-operand leading dim: (kPLD % 16) == 4 -> conflict-free fragments
+constexpr int kPLD = 196;         // A-operand leading dim: (kPLD % 16) == 4 -> conflict-free fragments
 constexpr int kBLD = kNB + 4;     // B-operand (k-major) leading dim, (36 % 16) == 4
-constexpr int kMaxNz = kMaxNI * 6;
+constexpr int kTileCols = 128;    // B-operand columns staged at a time
+constexpr int kMaxNz = kMaxNI * 4;
 
 struct FusedSmem {
   LeafAsmSmemT<256, 16> asmb;
-  double pan[kNB * kPLD];        // A operand: factored panel / U column block / Q_i chunk
-  double tile[kMaxCols * kBLD];  // B operand: U12 / X block / [v|Y] chunk; P during phase B
-  int nz_idx[kMaxNz];            // exterior line neighbours of each interior row
-  double nz_val[kMaxNz];
+  double pan[kNB * kPLD];         // A operand: factored panel / U column block / Q_i chunk;
+                                  // exterior-neighbour list during phases A-B
+  double tile[kTileCols * kBLD];  // B operand: U12 chunk / X block / [v|Y] chunk; P during phase B
   double urow[kNB];
   double cv[kFW];
   int cp[kFW], ct[kFW];
@@ -122,10 +122,14 @@ __device__ void panel_gepp_regs(FusedSmem& s, double* W, int ni, int j0, int pnb
       }
       if (lane == 0) s.cv[warp] = bv, s.cp[warp] = bp, s.ct[warp] = bt;
       __syncthreads();
-      bv = s.cv[0], bp = s.cp[0], bt = s.ct[0];
+      bv = s.cv[lane % kFW], bp = s.cp[lane % kFW], bt = s.ct[lane % kFW];
 #pragma unroll
-      for (int w = 1; w < kFW; ++w)
-        if (better(bv, bp, s.cv[w], s.cp[w])) bv = s.cv[w], bp = s.cp[w], bt = s.ct[w];
+      for (int o = kFW / 2; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int p2 = __shfl_xor_sync(0xffffffffu, bp, o);
+        const int t2 = __shfl_xor_sync(0xffffffffu, bt, o);
+        if (better(bv, bp, v2, p2)) bv = v2, bp = p2, bt = t2;
+      }
       if (tid == bt) {
 #pragma unroll
         for (int c = 0; c < kNB; ++c) s.urow[c] = v[c];
@@ -173,7 +177,7 @@ __device__ void panel_gepp_regs(FusedSmem& s, double* W, int ni, int j0, int pnb
 
 }  // namespace
 
-__global__ void __launch_bounds__(kFT, 1) leaf_fused_kernel(const LeafFusedArgs f) {
+__global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs f) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FusedSmem& s = *reinterpret_cast<FusedSmem*>(smem_raw);
   const LeafAsmArgs& a = f.a;
@@ -182,11 +186,13 @@ __global__ void __launch_bounds__(kFT, 1) leaf_fused_kernel(const LeafFusedArgs 
   const int g = lane >> 2, t4 = lane & 3;
   double* W = f.scratch + (long long)blockIdx.x * f.scratch_stride;  // ni x ncol, ld ni
   double* R = W + (long long)ni * ni;                                 // [sgn f | -L_ie P] -> [v | Y_i]
-  const bool p_in_smem = ne * nb <= kMaxCols * kBLD;
+  const bool p_in_smem = ne * nb <= kTileCols * kBLD;
 
   for (long long leaf = blockIdx.x; leaf < f.n_leaves; leaf += gridDim.x) {
     // ---- A. assembly (exterior neighbours into the shared list)
-    leaf_assemble_block(a, leaf, W, ni, nullptr, s.asmb, s.nz_idx, s.nz_val);
+    double* nz_val = s.pan;
+    int* nz_idx = reinterpret_cast<int*>(s.pan + kMaxNz);
+    leaf_assemble_block(a, leaf, W, ni, nullptr, s.asmb, nz_idx, nz_val);
     if (tid == 0) {
       a.bad_point[leaf] = s.asmb.bad;
       s.pmin = DBL_MAX;
@@ -203,7 +209,7 @@ __global__ void __launch_bounds__(kFT, 1) leaf_fused_kernel(const LeafFusedArgs 
       for (int e = tid; e < ni * nb; e += kFT) {
         const int r = e % ni, j = e / ni;
         double acc = 0.0;
-        for (int z = 0; z < nz; ++z) acc += s.nz_val[r * nz + z] * Pm[j * ne + s.nz_idx[r * nz + z]];
+        for (int z = 0; z < nz; ++z) acc += nz_val[r * nz + z] * Pm[j * ne + nz_idx[r * nz + z]];
         R[(long long)(1 + j) * ni + r] = -acc;
       }
     }
@@ -219,15 +225,17 @@ __global__ void __launch_bounds__(kFT, 1) leaf_fused_kernel(const LeafFusedArgs 
         if (nm > 0) {
           constexpr int kPer = 8;
           const int cols_per_chunk = (kFT * kPer) / nm;
-          for (int cc0 = 0; cc0 < ncol - pnb; cc0 += cols_per_chunk) {
-            const int total = min(cols_per_chunk, ncol - pnb - cc0) * nm;
+          // only columns right of the panel: the L columns left of it are dead (the
+          // factors are not kept on this path), so their row order does not matter
+          const int c_first = j0 + pnb, n_right = ncol - c_first;
+          for (int cc0 = 0; cc0 < n_right; cc0 += cols_per_chunk) {
+            const int total = min(cols_per_chunk, n_right - cc0) * nm;
             double vals[kPer];
 #pragma unroll
             for (int u = 0; u < kPer; ++u) {
               const int e = tid + u * kFT;
               if (e < total) {
-                const int cc = cc0 + e / nm, mv = e % nm;
-                const int c = cc < j0 ? cc : cc + pnb;
+                const int c = c_first + cc0 + e / nm, mv = e % nm;
                 vals[u] = W[(long long)c * ni + s.moved_src[mv]];
               }
             }
@@ -236,8 +244,7 @@ __global__ void __launch_bounds__(kFT, 1) leaf_fused_kernel(const LeafFusedArgs 
             for (int u = 0; u < kPer; ++u) {
               const int e = tid + u * kFT;
               if (e < total) {
-                const int cc = cc0 + e / nm, mv = e % nm;
-                const int c = cc < j0 ? cc : cc + pnb;
+                const int c = c_first + cc0 + e / nm, mv = e % nm;
                 W[(long long)c * ni + s.moved_dst[mv]] = vals[u];
               }
             }
@@ -260,15 +267,33 @@ __global__ void __launch_bounds__(kFT, 1) leaf_fused_kernel(const LeafFusedArgs 
           x[jj] = acc;
         }
 #pragma unroll
-        for (int jj = 0; jj < kNB; ++jj) {
+        for (int jj = 0; jj < kNB; ++jj)
           if (jj < pnb) col[jj] = x[jj];
-          s.tile[c * kBLD + jj] = jj < pnb ? x[jj] : 0.0;
-        }
       }
       __syncthreads();
-      if (rows > pnb && nrc > 0)
-        update_smem(rows - pnb, nrc, pnb, s.pan + pnb, kPLD, s.tile, kBLD, W + (long long)rc0 * ni + j0 + pnb, ni);
-      __syncthreads();
+      if (rows > pnb)
+        for (int cc0 = 0; cc0 < nrc; cc0 += kTileCols) {
+          const int ncc = min(kTileCols, nrc - cc0);
+          // stage U12[:, cc0:cc0+ncc] (k-major) -- 8 independent loads per thread per batch
+          for (int e0 = 0; e0 < ncc * kNB; e0 += 8 * kFT) {
+            double t[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int e = e0 + tid + u * kFT;
+              const int kk = e % kNB, c = e / kNB;
+              t[u] = (e < ncc * kNB && kk < pnb) ? W[(long long)(rc0 + cc0 + c) * ni + j0 + kk] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int e = e0 + tid + u * kFT;
+              if (e < ncc * kNB) s.tile[(e / kNB) * kBLD + e % kNB] = t[u];
+            }
+          }
+          __syncthreads();
+          update_smem(rows - pnb, ncc, pnb, s.pan + pnb, kPLD, s.tile, kBLD,
+                      W + (long long)(rc0 + cc0) * ni + j0 + pnb, ni);
+          __syncthreads();
+        }
     }
 
     // ---- D. back substitution on the 1+nb RHS columns
@@ -304,9 +329,18 @@ __global__ void __launch_bounds__(kFT, 1) leaf_fused_kernel(const LeafFusedArgs 
       __syncthreads();
       if (r0 > 0) {
         // stage the U column block U[0:r0, r0:r0+bnb] as the A operand
-        for (int e = tid; e < r0 * bnb; e += kFT) {
-          const int r = e % r0, c = e / r0;
-          s.pan[c * kPLD + r] = W[(long long)(r0 + c) * ni + r];
+        for (int e0 = 0; e0 < r0 * bnb; e0 += 8 * kFT) {
+          double t[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + tid + u * kFT;
+            t[u] = e < r0 * bnb ? W[(long long)(r0 + e / r0) * ni + e % r0] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + tid + u * kFT;
+            if (e < r0 * bnb) s.pan[(e / r0) * kPLD + e % r0] = t[u];
+          }
         }
         __syncthreads();
         update_smem(r0, nr, bnb, s.pan, kPLD, s.tile, kBLD, R, ni);
@@ -318,7 +352,7 @@ __global__ void __launch_bounds__(kFT, 1) leaf_fused_kernel(const LeafFusedArgs 
     //         k in shared chunks of 32 (A = Q_i chunk, B = [v|Y_i] chunk)
     {
       const int tmn = (nb + 7) / 8, tnn = (nr + 7) / 8, ntile = tmn * tnn;
-      constexpr int kMaxT = 4;  // 8x8 tiles per warp: ceil(7*8 / 16) = 4 for nb = 56
+      constexpr int kMaxT = 7;  // 8x8 tiles per warp: ceil(7*8 / 8) = 7 for nb = 56
       double acc[kMaxT][2];
 #pragma unroll
       for (int u = 0; u < kMaxT; ++u) acc[u][0] = acc[u][1] = 0.0;
@@ -378,12 +412,12 @@ __global__ void __launch_bounds__(kFT, 1) leaf_fused_kernel(const LeafFusedArgs 
 bool leaf_fused_supported(int n, int p, int ni, int nb, int dim, bool mixed_terms) {
   const int tmn = (nb + 7) / 8, tnn = (nb + 8) / 8;
   return !mixed_terms && n <= 256 && p <= 16 && ni <= kMaxNI && ni <= kFT && ni + 1 + nb <= kMaxCols &&
-         ni * 2 * dim <= kMaxNz && tmn * tnn <= 4 * kFW;
+         ni * 2 * dim <= kMaxNz && tmn * tnn <= 7 * kFW && 1 + nb <= kTileCols;
 }
 
 long long leaf_fused_scratch_per_cta(int ni, int ne, int nb) { return (long long)ni * (ni + 1 + nb); }
 
-int leaf_fused_ctas_per_sm() { return 1; }
+int leaf_fused_ctas_per_sm() { return 2; }
 
 cudaError_t launch_leaf_fused(const LeafFusedArgs& f, int grid, cudaStream_t st) {
   const size_t smem = sizeof(FusedSmem);

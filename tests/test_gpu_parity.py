@@ -156,6 +156,7 @@ def test_errors():
 def test_fused_leaf_path_equals_batched(name, p, L, monkeypatch):
     """The persistent fused leaf kernel and the multi-launch batched leaf path agree."""
     prob = PR.CATALOG[name]()
+    monkeypatch.setenv("HPS_LEAF_PATH", "fused")
     a = gpu_solver(prob, p, L)
     monkeypatch.setenv("HPS_LEAF_PATH", "batched")
     b = gpu_solver(prob, p, L)
