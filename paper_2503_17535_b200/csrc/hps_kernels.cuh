@@ -60,6 +60,7 @@ struct LeafFusedArgs {
   double* HT;               // per leaf: nb x (1 + nb) = [h | T]
   long long strideHT;
   double* stats;            // per leaf: min|u_ii|, max|u_ii|, first zero pivot (-1)
+  long long* prof;          // optional phase timestamps (clock64) of CTA 0: [leaf_iter][8]
   long long n_leaves;
 };
 bool leaf_fused_supported(int n, int p, int ni, int nb, int dim, bool mixed_terms);

@@ -188,7 +188,20 @@ __global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs 
   double* R = W + (long long)ni * ni;                                 // [sgn f | -L_ie P] -> [v | Y_i]
   const bool p_in_smem = ne * nb <= kTileCols * kBLD;
 
-  for (long long leaf = blockIdx.x; leaf < f.n_leaves; leaf += gridDim.x) {
+  int iter = 0;
+  auto stamp = [&](int k) {
+    if (f.prof && blockIdx.x == 0 && tid == 0 && iter < 4) f.prof[iter * 8 + k] = clock64();
+  };
+  long long sub_t0 = 0;
+  auto substamp = [&](int k) {  // accumulated sub-phases of the LU of leaf iteration 0 (slots 32..)
+    if (f.prof && blockIdx.x == 0 && tid == 0 && iter == 0) {
+      const long long t = clock64();
+      if (k > 0) f.prof[32 + k] += t - sub_t0;
+      sub_t0 = t;
+    }
+  };
+  for (long long leaf = blockIdx.x; leaf < f.n_leaves; leaf += gridDim.x, ++iter) {
+    stamp(0);
     // ---- A. assembly (exterior neighbours into the shared list)
     double* nz_val = s.pan;
     int* nz_idx = reinterpret_cast<int*>(s.pan + kMaxNz);
@@ -202,6 +215,7 @@ __global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs 
     if (p_in_smem)
       for (int e = tid; e < ne * nb; e += kFT) s.tile[e] = f.P[e];
     __syncthreads();
+    stamp(1);
     // ---- B. R[:, 1 + j] = -sum over the row's exterior neighbours of L_ie * P[e, j]
     {
       const double* Pm = p_in_smem ? s.tile : f.P;
@@ -215,10 +229,13 @@ __global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs 
     }
     __syncthreads();
 
+    stamp(2);
     // ---- C. blocked GEPP, RHS columns ride along
     for (int j0 = 0; j0 < ni; j0 += kNB) {
       const int pnb = min(kNB, ni - j0), rows = ni - j0;
+      substamp(0);
       panel_gepp_regs(s, W, ni, j0, pnb);
+      substamp(1);
       // row exchange of every other column; chunks end on column boundaries
       {
         const int nm = s.n_moved;
@@ -252,6 +269,7 @@ __global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs 
           }
         }
       }
+      substamp(2);
       // U12 = L11^-1 A12 for all columns right of the panel -> W and s.tile (k-major)
       const int rc0 = j0 + pnb, nrc = ncol - rc0;
       for (int c = tid; c < nrc; c += kFT) {
@@ -271,6 +289,7 @@ __global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs 
           if (jj < pnb) col[jj] = x[jj];
       }
       __syncthreads();
+      substamp(3);
       if (rows > pnb)
         for (int cc0 = 0; cc0 < nrc; cc0 += kTileCols) {
           const int ncc = min(kTileCols, nrc - cc0);
@@ -294,8 +313,10 @@ __global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs 
                       W + (long long)(rc0 + cc0) * ni + j0 + pnb, ni);
           __syncthreads();
         }
+      substamp(4);
     }
 
+    stamp(3);
     // ---- D. back substitution on the 1+nb RHS columns
     const int nblk = (ni + kNB - 1) / kNB;
     for (int jb = nblk - 1; jb >= 0; --jb) {
@@ -348,6 +369,7 @@ __global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs 
       __syncthreads();
     }
 
+    stamp(4);
     // ---- E. [h | T] = Q_i [v | Y_i] + [0 | Q_e P]: 8x8 output tiles over all warps,
     //         k in shared chunks of 32 (A = Q_i chunk, B = [v|Y_i] chunk)
     {
@@ -397,6 +419,7 @@ __global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs 
         }
       }
     }
+    stamp(5);
     // ---- outputs: [v | Y_i] for the solve, pivot statistics
     double* Yv = f.Yv + leaf * f.strideYv;
     for (int e = tid; e < ni * nr; e += kFT) Yv[e] = R[e];
