@@ -134,6 +134,13 @@ void hpsg_destroy(hpsg_ctx* ctx);
  * (proj/src/problems.cpp:126-141, :240-249).  out: n x 3 (z = 0 in 2D). */
 void hpsg_bump_centers(unsigned long long seed, int n, int dim, double* out);
 
+/* Host-only geometry (no device, no context): leaf_cheb_points of every leaf of the uniform
+ * tree in DFS order (n_leaves x p^dim x 3), so callers can sample std::function fields into
+ * HPSG_FIELD_SAMPLED arrays before hpsg_create (mesh.cpp:320-336, solver.cpp:49-57). */
+int hpsg_tree_leaf_points(const hpsg_tree* tree, double* xyz);
+/* Host-only: root boundary points in canonical section order (root_bsize x 3), no device needed */
+int hpsg_tree_root_points(const hpsg_tree* tree, double* xyz);
+
 /* library-level probes */
 int hpsg_device_count(void);
 const char* hpsg_build_info(void);

@@ -901,25 +901,50 @@ int hpsg_root_boundary_points(hpsg_ctx* c, double* xyz) {
   });
 }
 
+static void tree_leaf_points(const hpsg::UniformTree& T, double* xyz) {
+  const std::vector<double> cn = hpsg::cheb_nodes(T.p);
+  const int p = T.p, dim = T.dim, n = dim == 2 ? p * p : p * p * p;
+  for (int l = 0; l < T.n_leaves(); ++l) {
+    const double* b = &T.leaf_lo[size_t(l) * 6];
+    for (int i = 0; i < n; ++i) {
+      int ci[3] = {0, 0, 0};
+      if (dim == 2)
+        ci[0] = i / p, ci[1] = i % p;
+      else
+        ci[0] = i / (p * p), ci[1] = (i / p) % p, ci[2] = i % p;
+      double* x = xyz + (size_t(l) * n + i) * 3;
+      x[0] = x[1] = x[2] = 0.0;
+      for (int k = 0; k < dim; ++k) x[k] = 0.5 * (b[k] + b[3 + k]) + 0.5 * (b[3 + k] - b[k]) * cn[ci[k]];
+    }
+  }
+}
+
 int hpsg_leaf_points(hpsg_ctx* c, double* xyz) {
   if (!c || !xyz) return HPSG_ERR_INVALID;
-  return guarded(c, [&] {
-    const std::vector<double> cn = hpsg::cheb_nodes(c->tree.p);
-    const int p = c->tree.p, dim = c->tree.dim, n = c->ops.n;
-    for (int l = 0; l < c->T.n_leaves(); ++l) {
-      const double* b = &c->T.leaf_lo[size_t(l) * 6];
-      for (int i = 0; i < n; ++i) {
-        int ci[3] = {0, 0, 0};
-        if (dim == 2)
-          ci[0] = i / p, ci[1] = i % p;
-        else
-          ci[0] = i / (p * p), ci[1] = (i / p) % p, ci[2] = i % p;
-        double* x = xyz + (size_t(l) * n + i) * 3;
-        x[0] = x[1] = x[2] = 0.0;
-        for (int k = 0; k < dim; ++k) x[k] = 0.5 * (b[k] + b[3 + k]) + 0.5 * (b[3 + k] - b[k]) * cn[ci[k]];
-      }
-    }
-  });
+  return guarded(c, [&] { tree_leaf_points(c->T, xyz); });
+}
+
+int hpsg_tree_root_points(const hpsg_tree* t, double* xyz) {
+  if (!t || !xyz || (t->dim != 2 && t->dim != 3) || t->p < 4 || t->L < 0 || !(t->hi > t->lo))
+    return HPSG_ERR_INVALID;
+  try {
+    const std::vector<double> p = hpsg::root_boundary_points(hpsg::make_uniform_tree(t->dim, t->p, t->L, t->lo, t->hi));
+    std::memcpy(xyz, p.data(), p.size() * 8);
+  } catch (...) {
+    return HPSG_ERR_INVALID;
+  }
+  return HPSG_OK;
+}
+
+int hpsg_tree_leaf_points(const hpsg_tree* t, double* xyz) {
+  if (!t || !xyz || (t->dim != 2 && t->dim != 3) || t->p < 4 || t->L < 0 || !(t->hi > t->lo))
+    return HPSG_ERR_INVALID;
+  try {
+    tree_leaf_points(hpsg::make_uniform_tree(t->dim, t->p, t->L, t->lo, t->hi), xyz);
+  } catch (...) {
+    return HPSG_ERR_INVALID;
+  }
+  return HPSG_OK;
 }
 
 int hpsg_get_leaf(hpsg_ctx* c, int ord, double* Y, double* v, double* Tm, double* h) {

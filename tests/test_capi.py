@@ -1,0 +1,85 @@
+"""CPU-side checks of the C-ABI boundary (include/hps_cuda.h / libhps_b200.so):
+the library loads and exports every declared entry point, host-only geometry
+(orderings of leaf and root-boundary points) matches the oracle bit-for-bit, and
+the product fails loudly without a CUDA device (no CPU fallback)."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_2503_17535_b200 as H
+from paper_2503_17535_b200 import hps as HP
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "hps_cuda.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(hpsg_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = H.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    assert b"sm_100a" in lib.hpsg_build_info()
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", HP.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", HP.LIB_PATH], capture_output=True, text=True).stdout
+    assert "DMMA.8x8x4" in sass  # FP64 tensor-core path
+    assert "UCGABAR" in sass or "barrier.cluster" in sass or "CCTL" in sass or "MAPA" in sass  # cluster/DSMEM panel
+
+
+def _tree(dim, p, L, lo, hi):
+    return HP._Tree(dim, p, L, lo, hi)
+
+
+@pytest.mark.parametrize("dim,p,L,lo,hi", [(2, 16, 3, -1.0, 1.0), (2, 8, 2, 0.1, 0.225), (3, 6, 2, 0.0, 1.0)])
+def test_host_geometry_matches_oracle(oracle, dim, p, L, lo, hi):
+    from paper_2503_17535_b200 import problems as PR
+    from tests.oracle_problems import oracle_solver
+    lib = H.lib()
+    lib.hpsg_tree_leaf_points.argtypes = [C.POINTER(HP._Tree), C.POINTER(C.c_double)]
+    lib.hpsg_tree_root_points.argtypes = [C.POINTER(HP._Tree), C.POINTER(C.c_double)]
+    t = H.build_uniform_tree(lo, hi, L, dim, p)
+    tr = _tree(dim, p, L, lo, hi)
+    pts = np.zeros((t.n_leaves, p ** dim, 3))
+    assert lib.hpsg_tree_leaf_points(C.byref(tr), HP._dp(pts)) == 0
+    rp = np.zeros((t.root_boundary_size, 3))
+    assert lib.hpsg_tree_root_points(C.byref(tr), HP._dp(rp)) == 0
+    prob = PR.laplace_poly2d() if dim == 2 else PR.CATALOG["laplace3d"]()
+    prob.lo, prob.hi = lo, hi
+    o = oracle_solver(prob, p, L)
+    o.build()
+    assert np.array_equal(pts, o.leaf_points())
+    assert np.array_equal(rp, o.root_points())
+    info = oracle.tree_info(dim, L, p, [lo] * dim, [hi] * dim)
+    assert info["n_leaves"] == t.n_leaves and info["total_points"] == t.total_points
+
+
+def test_no_device_fails_loudly():
+    if H.lib().hpsg_device_count() > 0:
+        pytest.skip("a CUDA device is present")
+    with pytest.raises(H.HpsError) as e:
+        H.HpsSolver(H.build_uniform_tree(-1, 1, 2, 2, 8), [H.Term(H.ROLE_LAPLACIAN, H.Field.const(1.0))])
+    assert e.value.code == HP.HPSG_ERR_NO_DEVICE
+
+
+def test_cpp_dropin_example_builds_and_fails_loudly_without_device():
+    exe = os.path.join(ROOT, "examples", "solve_problem_b200")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "paper_2503_17535_b200"), "example"], check=True)
+    if H.lib().hpsg_device_count() > 0:
+        pytest.skip("a CUDA device is present (run by the gpu tests)")
+    r = subprocess.run([exe, "2", "8"], capture_output=True, text=True)
+    assert r.returncode == 1 and "no CUDA device" in r.stderr

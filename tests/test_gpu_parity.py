@@ -165,3 +165,20 @@ def test_fused_leaf_path_equals_batched(name, p, L, monkeypatch):
     for o in (0, a.tree.n_leaves - 1):
         for x, y in zip(a.get_leaf(o), b.get_leaf(o)):
             assert rel(x, y) < 1e-11
+
+
+def test_cpp_dropin_example_runs():
+    """examples/solve_problem_b200.cpp: the reference solve_problem() flow through the C++
+    drop-in header (std::function coefficients sampled on the host, SPEC.md:536 accuracy gate)."""
+    import json
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "examples", "solve_problem_b200")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-s", "-C", os.path.join(root, "paper_2503_17535_b200"), "example"], check=True)
+    r = subprocess.run([exe, "3", "16", "0"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    rep = json.loads(r.stdout)
+    assert rep["N"] == 16384 and rep["top_D"] == 4 * 14 * 4
+    assert rep["rel_linf"] < 1e-8
