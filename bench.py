@@ -4,7 +4,7 @@
 Workload (BASELINE.json configs[1]): 2D variable-coefficient Helmholtz
 Delta u + k^2 (1 + q(x)) u = f on [-1,1]^2, DtN HPS, p = 16, uniform quadtree
 L = 8 (65,536 leaves, N = 16,777,216 DOF), q = 10 seeded Gaussian bumps,
-manufactured plane-wave solution (synthetic data, k = 20).
+manufactured plane-wave solution (synthetic data, k = 30, away from box resonances).
 
 One step = one full build (leaf stage + all merge levels) + one solve (downward
 pass + leaf reconstruction) through the C-ABI (libhps_b200.so).  `value` is
@@ -265,7 +265,7 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--L", type=int, default=8)
     ap.add_argument("--p", type=int, default=16)
-    ap.add_argument("--k", type=float, default=20.0)
+    ap.add_argument("--k", type=float, default=30.0)
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--cpu-L", type=int, default=None, help="tree depth of the CPU baseline run (default: --L)")
     ap.add_argument("--explicit-root", action="store_true", help="form S at the root (reference 2D default)")

@@ -95,7 +95,14 @@ __device__ void update_smem(int m, int n, int k, const double* A, int lda, const
   }
 }
 
-__device__ __forceinline__ bool better(double v, int p, double v2, int p2) { return v2 > v || (v2 == v && p2 < p); }
+// Pivot order: inactive rows (p == INT_MAX) never win; NaN counts as +inf so a non-finite
+// column still yields an active pivot (reported as singular, never an out-of-range row).
+__device__ __forceinline__ bool better(double v, int p, double v2, int p2) {
+  if (p2 == INT_MAX) return false;
+  if (p == INT_MAX) return true;
+  const double a = isnan(v) ? INFINITY : v, b = isnan(v2) ? INFINITY : v2;
+  return b > a || (b == a && p2 < p);
+}
 
 // GEPP of panel columns [j0, j0+pnb) over rows [j0, ni) of W; one row per thread in registers.
 // Writes the factored panel to W and s.pan (final row order) and fills the moved-row list.

@@ -130,7 +130,8 @@ def test_sampled_field_equals_builtin():
     lp = a.leaf_points()
     z = prob.terms[1].field.centers
     q = sum(np.exp(-50.0 * ((lp[..., 0] - c[0]) ** 2 + (lp[..., 1] - c[1]) ** 2)) for c in z)
-    terms = [prob.terms[0], H.Term(H.ROLE_ZEROTH, H.Field(H.FIELD_SAMPLED, samples=400.0 * (1 + q)))]
+    k2 = prob.terms[1].field.c[0]
+    terms = [prob.terms[0], H.Term(H.ROLE_ZEROTH, H.Field(H.FIELD_SAMPLED, samples=k2 * (1 + q)))]
     b = H.HpsSolver(tree, terms, prob.source)
     b.build()
     g = prob.boundary(a.root_boundary_points())
