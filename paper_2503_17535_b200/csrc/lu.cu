@@ -31,16 +31,24 @@ HPS_DEV void argmax_merge(double& v, int& i, double v2, int i2) {
 }
 
 // One panel (rows j0..n-1, columns j0..j0+nb-1) of one matrix per cluster.
+// Per column: one cluster barrier.  Every CTA publishes its best candidate (value, row and
+// the whole candidate row) and, for the CTA owning row j, row j itself, into
+// double-buffered shared slots; after the barrier warp 0 of every CTA reduces the cs
+// candidates and pulls the pivot row (and row j for the pivot owner) through DSMEM.
+// Remote CTAs only ever read the published slots, so the local swap/elimination needs no
+// second barrier; slot reuse two columns later is ordered by the intervening barrier.
 __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelArgs a) {
   extern __shared__ __align__(16) double sm[];
-  double* pan = sm;                          // [nb][rpc]
-  double* urow = sm + (size_t)a.rpc * kLuNB; // pivot row (all nb cols)
-  double* jrow = urow + kLuNB;               // displaced row j
-  double* wv = jrow + kLuNB;                 // per-warp partial max
-  int* wi = reinterpret_cast<int*>(wv + kPanelThreads / 32);
-  double* cand_v = reinterpret_cast<double*>(wi + kPanelThreads / 32 + 2);  // 8-byte aligned slot
-  int* cand_i = reinterpret_cast<int*>(cand_v + 1);
-  int* s_piv = cand_i + 1;
+  double* pan = sm;                               // [nb][rpc]
+  double* cand_row = sm + (size_t)a.rpc * kLuNB;  // [2][kLuNB] published candidate row
+  double* jrow_pub = cand_row + 2 * kLuNB;        // [2][kLuNB] published row j
+  double* urow = jrow_pub + 2 * kLuNB;            // pivot row (local copy)
+  double* jrow = urow + kLuNB;                    // row j (pivot owner's copy)
+  double* wv = jrow + kLuNB;                      // per-warp partial max
+  double* cand_v = wv + kPanelThreads / 32;       // [2]
+  int* wi = reinterpret_cast<int*>(cand_v + 2);
+  int* cand_i = wi + kPanelThreads / 32;          // [2]
+  int* s_piv = cand_i + 2;
 
   const int cs = a.cs;
   const int rank = cs > 1 ? (int)cluster_ctarank() : 0;
@@ -62,6 +70,7 @@ __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelA
   int first_zero = -1;
 
   for (int j = 0; j < nb; ++j) {
+    const int buf = j & 1;
     // ---- local argmax over panel rows >= j
     double bv = -1.0;
     int bi = INT_MAX;
@@ -77,6 +86,7 @@ __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelA
     }
     if (lane == 0) wv[warp] = bv, wi[warp] = bi;
     __syncthreads();
+    const int own_j = j / a.rpc;
     if (warp == 0) {
       bv = lane < kPanelThreads / 32 ? wv[lane] : -1.0;
       bi = lane < kPanelThreads / 32 ? wi[lane] : INT_MAX;
@@ -86,45 +96,52 @@ __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelA
         const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
         argmax_merge(bv, bi, v2, i2);
       }
-      if (lane == 0) *cand_v = bv, *cand_i = bi;
-    }
-    if (cs > 1) {
-      cluster_sync();
-      if (warp == 0) {
-        bv = -1.0;
-        bi = INT_MAX;
-        if (lane < cs) {
-          bv = dsmem_ld_f64(dsmem_map(cand_v, lane));
-          bi = dsmem_ld_s32(dsmem_map(cand_i, lane));
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-          const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-          argmax_merge(bv, bi, v2, i2);
-        }
-        if (lane == 0) *s_piv = (bi == INT_MAX) ? j : bi;
-      }
-    } else {
-      if (tid == 0) *s_piv = (*cand_i == INT_MAX) ? j : *cand_i;
-    }
-    __syncthreads();
-    const int piv = *s_piv;
-    const int own_p = piv / a.rpc, own_j = j / a.rpc;
-
-    // ---- fetch pivot row (and displaced row j for the pivot owner)
-    for (int c = tid; c < nb; c += kPanelThreads) {
-      const double* src = &pan[c * a.rpc + (piv - own_p * a.rpc)];
-      urow[c] = (own_p == rank) ? *src : dsmem_ld_f64(dsmem_map(src, own_p));
-      if (own_p == rank && piv != j) {
-        const double* sj = &pan[c * a.rpc + (j - own_j * a.rpc)];
-        jrow[c] = (own_j == rank) ? *sj : dsmem_ld_f64(dsmem_map(sj, own_j));
+      // publish the candidate (value, row, whole row) and, if owned here, row j
+      if (lane == 0) cand_v[buf] = bv, cand_i[buf] = bi;
+      if (lane < nb) {
+        cand_row[buf * kLuNB + lane] = (bi != INT_MAX) ? pan[lane * a.rpc + (bi - r_begin)] : 0.0;
+        if (own_j == rank) jrow_pub[buf * kLuNB + lane] = pan[lane * a.rpc + (j - r_begin)];
       }
     }
     if (cs > 1)
       cluster_sync();
     else
       __syncthreads();
+    if (warp == 0) {
+      double gv = -1.0;
+      int gi = INT_MAX, gr = 0;
+      if (lane < cs) {
+        gv = cs > 1 ? dsmem_ld_f64(dsmem_map(&cand_v[buf], lane)) : cand_v[buf];
+        gi = cs > 1 ? dsmem_ld_s32(dsmem_map(&cand_i[buf], lane)) : cand_i[buf];
+        gr = lane;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, gv, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, gi, o);
+        const int r2 = __shfl_xor_sync(0xffffffffu, gr, o);
+        if (v2 > gv || (v2 == gv && i2 < gi)) gv = v2, gi = i2, gr = r2;
+      }
+      const int piv = (gi == INT_MAX) ? j : gi;
+      const int own_p = (gi == INT_MAX) ? own_j : gr;
+      if (lane == 0) *s_piv = piv;
+      if (lane < nb) {
+        const double* src = &cand_row[buf * kLuNB + lane];
+        if (gi == INT_MAX) {  // no candidate anywhere (cannot happen for rows >= nb): pivot = row j
+          const double* sj = &jrow_pub[buf * kLuNB + lane];
+          urow[lane] = (own_j == rank || cs == 1) ? *sj : dsmem_ld_f64(dsmem_map(sj, own_j));
+        } else {
+          urow[lane] = (own_p == rank || cs == 1) ? *src : dsmem_ld_f64(dsmem_map(src, own_p));
+        }
+        if (own_p == rank && piv != j) {
+          const double* sj = &jrow_pub[buf * kLuNB + lane];
+          jrow[lane] = (own_j == rank || cs == 1) ? *sj : dsmem_ld_f64(dsmem_map(sj, own_j));
+        }
+      }
+    }
+    __syncthreads();
+    const int piv = *s_piv;
+    const int own_p = piv / a.rpc;
     if (piv != j) {
       for (int c = tid; c < nb; c += kPanelThreads) {
         if (own_j == rank) pan[c * a.rpc + (j - r_begin)] = urow[c];
@@ -143,7 +160,7 @@ __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelA
     }
     if (rank == 0 && tid == 0) a.ipiv[b * a.n + a.j0 + j] = a.j0 + piv;
 
-    // ---- eliminate rows below j within this CTA's chunk
+    // ---- eliminate rows below j within this CTA's chunk (LAPACK scales by the reciprocal)
     if (apv > 0.0) {
       const double inv = 1.0 / pv;
       for (int r = tid; r < nr; r += kPanelThreads) {
@@ -167,7 +184,7 @@ __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelA
     s[1] = fmax(s[1], pmax);
     if (first_zero >= 0 && s[2] < 0) s[2] = first_zero;
   }
-  if (cs > 1) cluster_sync();  // keep smem alive until remote readers are done
+  if (cs > 1) cluster_sync();  // keep the published slots alive until remote readers are done
 }
 
 struct Seg {
@@ -326,7 +343,7 @@ cudaError_t launch_panel(int batch, int n, int j0, int nb, BatchedMat M, int* ip
   if (rpc > kMaxRowsPerCta) return cudaErrorInvalidValue;
   if (cs == 1) rpc = rows;
   PanelArgs pa{M.p, M.ld, M.stride, n, j0, nb, rpc, cs, ipiv, stats};
-  const size_t smem = (size_t)rpc * kLuNB * 8 + 2 * kLuNB * 8 + (kPanelThreads / 32) * 12 + 64;
+  const size_t smem = (size_t)rpc * kLuNB * 8 + 6 * kLuNB * 8 + (kPanelThreads / 32) * 12 + 128;
   static size_t smem_set = 0;
   if (smem > smem_set) {
     cudaError_t e = cudaFuncSetAttribute(panel_getrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
