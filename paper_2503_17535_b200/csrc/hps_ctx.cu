@@ -432,17 +432,23 @@ void run_leaf_stage(hpsg_ctx* c) {
     f.n_leaves = nl;
     if (getenv("HPS_LEAF_PROF")) {  // developer knob: per-phase clock64 stamps of CTA 0
       static DevBuf prof;
-      prof.alloc(48 * 8, nullptr);
-      ck(cudaMemsetAsync(prof.p, 0, 48 * 8, c->st), "memset");
+      const int np = 64 + c->fused_grid;
+      prof.alloc(np * 8, nullptr);
+      ck(cudaMemsetAsync(prof.p, 0, np * 8, c->st), "memset");
       f.prof = static_cast<long long*>(prof.p);
       ck(hpsk::launch_leaf_fused(f, c->fused_grid, c->st), "leaf_fused");
-      long long h[48];
-      ck(cudaMemcpyAsync(h, prof.p, sizeof h, cudaMemcpyDeviceToHost, c->st), "prof");
+      std::vector<long long> h(np);
+      ck(cudaMemcpyAsync(h.data(), prof.p, np * 8, cudaMemcpyDeviceToHost, c->st), "prof");
       ck(cudaStreamSynchronize(c->st), "prof sync");
+      std::vector<long long> per(h.begin() + 64, h.end());
+      std::sort(per.begin(), per.end());
+      fprintf(stderr, "leaf_fused per-CTA cycles: min %lld median %lld max %lld\n", per.front(), per[per.size() / 2],
+              per.back());
       for (int it = 0; it < 4; ++it)
         fprintf(stderr, "leaf_fused CTA0 leaf %d cycles: assemble %lld  -L_ieP %lld  LU %lld  backsub %lld  [h|T] %lld\n",
                 it, h[it * 8 + 1] - h[it * 8], h[it * 8 + 2] - h[it * 8 + 1], h[it * 8 + 3] - h[it * 8 + 2],
                 h[it * 8 + 4] - h[it * 8 + 3], h[it * 8 + 5] - h[it * 8 + 4]);
+      fprintf(stderr, "leaf_fused grid %d (%d CTAs/SM)\n", c->fused_grid, hpsk::leaf_fused_ctas_per_sm());
       fprintf(stderr, "leaf_fused LU leaf 0 sub-phases: gepp %lld exchange %lld trsm %lld update %lld\n", h[33], h[34],
               h[35], h[36]);
     }

@@ -37,6 +37,7 @@ constexpr int kPLD = 196;         // A-operand leading dim: (kPLD % 16) == 4 -> 
 constexpr int kBLD = kNB + 4;     // B-operand (k-major) leading dim, (36 % 16) == 4
 constexpr int kTileCols = 128;    // B-operand columns staged at a time
 constexpr int kMaxNz = kMaxNI * 4;
+constexpr int kRowsPerLane = (kMaxNI + 31) / 32;
 
 struct FusedSmem {
   LeafAsmSmemT<256, 16> asmb;
@@ -46,7 +47,9 @@ struct FusedSmem {
   double urow[kNB];
   double cv[kFW];
   int cp[kFW], ct[kFW];
-  int moved_dst[2 * kNB], moved_src[2 * kNB];
+  double rdiag[kNB];
+  int prow[kMaxNI];
+  int moved_dst[kMaxNI], moved_src[kMaxNI];
   int n_moved;
   double pmin, pmax;
   int first_zero;
@@ -95,54 +98,56 @@ __device__ void update_smem(int m, int n, int k, const double* A, int lda, const
   }
 }
 
-// Pivot order: inactive rows (p == INT_MAX) never win; NaN counts as +inf so a non-finite
-// column still yields an active pivot (reported as singular, never an out-of-range row).
-__device__ __forceinline__ bool better(double v, int p, double v2, int p2) {
-  if (p2 == INT_MAX) return false;
-  if (p == INT_MAX) return true;
-  const double a = isnan(v) ? INFINITY : v, b = isnan(v2) ? INFINITY : v2;
-  return b > a || (b == a && p2 < p);
-}
-
-// GEPP of panel columns [j0, j0+pnb) over rows [j0, ni) of W; one row per thread in registers.
-// Writes the factored panel to W and s.pan (final row order) and fills the moved-row list.
-__device__ void panel_gepp_regs(FusedSmem& s, double* W, int ni, int j0, int pnb) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// GEPP of panel columns [j0, j0+pnb) over rows [j0, ni) of W by ONE warp on the panel staged in
+// s.pan (rows physically exchanged; lane-strided rows, no CTA barrier per column).  Pivot = max
+// |a| with NaN ranked as +inf, ties -> lowest current row (the LAPACK/Eigen rule).  Writes the
+// factored panel back to W and fills the moved-row list for the other columns.
+__device__ void panel_gepp_warp(FusedSmem& s, double* W, int ni, int j0, int pnb) {
+  const int tid = threadIdx.x, lane = tid & 31;
   const int rows = ni - j0;
-  const bool own = tid < rows;
-  double v[kNB];
+  for (int e = tid; e < pnb * rows; e += kFT) {
+    const int c = e / rows, r = e - c * rows;
+    s.pan[c * kPLD + r] = W[(long long)(j0 + c) * ni + j0 + r];
+  }
+  for (int r = tid; r < rows; r += kFT) s.prow[r] = r;
+  __syncthreads();
+  if (tid < 32) {
+    for (int j = 0; j < pnb; ++j) {
+      double* pj = s.pan + j * kPLD;
+      double bv = -1.0;
+      int bp = INT_MAX;
+      {
+        double a[kRowsPerLane];
 #pragma unroll
-  for (int c = 0; c < kNB; ++c) v[c] = (own && c < pnb) ? W[(long long)(j0 + c) * ni + j0 + tid] : 0.0;
-  bool active = own;
-  int mypos = tid;
+        for (int q = 0; q < kRowsPerLane; ++q) {
+          const int r = j + lane + 32 * q;
+          a[q] = r < rows ? fabs(pj[r]) : -1.0;
+        }
 #pragma unroll
-  for (int j = 0; j < kNB; ++j) {
-    if (j < pnb) {
-      double bv = active ? fabs(v[j]) : -1.0;
-      int bp = active ? mypos : INT_MAX, bt = tid;
+        for (int q = 0; q < kRowsPerLane; ++q) {
+          const double av = isnan(a[q]) ? INFINITY : a[q];
+          if (av > bv) bv = av, bp = j + lane + 32 * q;
+        }
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
         const int p2 = __shfl_xor_sync(0xffffffffu, bp, o);
-        const int t2 = __shfl_xor_sync(0xffffffffu, bt, o);
-        if (better(bv, bp, v2, p2)) bv = v2, bp = p2, bt = t2;
+        if (v2 > bv || (v2 == bv && p2 < bp)) bv = v2, bp = p2;
       }
-      if (lane == 0) s.cv[warp] = bv, s.cp[warp] = bp, s.ct[warp] = bt;
-      __syncthreads();
-      bv = s.cv[lane % kFW], bp = s.cp[lane % kFW], bt = s.ct[lane % kFW];
-#pragma unroll
-      for (int o = kFW / 2; o > 0; o >>= 1) {
-        const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int p2 = __shfl_xor_sync(0xffffffffu, bp, o);
-        const int t2 = __shfl_xor_sync(0xffffffffu, bt, o);
-        if (better(bv, bp, v2, p2)) bv = v2, bp = p2, bt = t2;
+      if (bp != j) {
+        for (int c = lane; c < pnb; c += 32) {
+          const double t = s.pan[c * kPLD + j];
+          s.pan[c * kPLD + j] = s.pan[c * kPLD + bp];
+          s.pan[c * kPLD + bp] = t;
+        }
+        if (lane == 0) {
+          const int t = s.prow[j];
+          s.prow[j] = s.prow[bp];
+          s.prow[bp] = t;
+        }
       }
-      if (tid == bt) {
-#pragma unroll
-        for (int c = 0; c < kNB; ++c) s.urow[c] = v[c];
-        active = false;
-      }
-      if (tid == 0) {
+      if (lane == 0) {
         if (!(bv > 0.0) || !isfinite(bv)) {
           if (s.first_zero < 0) s.first_zero = j0 + j;
         } else {
@@ -150,35 +155,66 @@ __device__ void panel_gepp_regs(FusedSmem& s, double* W, int ni, int j0, int pnb
           s.pmax = fmax(s.pmax, bv);
         }
       }
-      if (tid == bt)
-        mypos = j;
-      else if (mypos == j)
-        mypos = bp;
-      __syncthreads();
-      const double pv = s.urow[j];
-      if (active && fabs(pv) > 0.0) {
-        const double l = v[j] / pv;
-        v[j] = l;
+      __syncwarp();
+      const double pv = pj[j];
+      if (fabs(pv) > 0.0) {
+        const double rinv = 1.0 / pv;
+        double l[kRowsPerLane];
 #pragma unroll
-        for (int c = j + 1; c < kNB; ++c) v[c] -= l * s.urow[c];
+        for (int q = 0; q < kRowsPerLane; ++q) {
+          const int r = j + 1 + lane + 32 * q;
+          l[q] = 0.0;
+          if (r < rows) {
+            l[q] = pj[r] * rinv;
+            pj[r] = l[q];
+          }
+        }
+        // rank-1 update, four columns at a time so 28 loads are in flight per lane
+        int c = j + 1;
+        for (; c + 4 <= pnb; c += 4) {
+          double u[4], a[4][kRowsPerLane];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) u[k] = s.pan[(c + k) * kPLD + j];
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int q = 0; q < kRowsPerLane; ++q) {
+              const int r = j + 1 + lane + 32 * q;
+              a[k][q] = r < rows ? s.pan[(c + k) * kPLD + r] : 0.0;
+            }
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int q = 0; q < kRowsPerLane; ++q) {
+              const int r = j + 1 + lane + 32 * q;
+              if (r < rows) s.pan[(c + k) * kPLD + r] = a[k][q] - l[q] * u[k];
+            }
+        }
+        for (; c < pnb; ++c) {
+          double* pc = s.pan + c * kPLD;
+          const double u = pc[j];
+#pragma unroll
+          for (int q = 0; q < kRowsPerLane; ++q) {
+            const int r = j + 1 + lane + 32 * q;
+            if (r < rows) pc[r] -= l[q] * u;
+          }
+        }
       }
+      __syncwarp();
     }
-  }
-  if (own) {
-#pragma unroll
-    for (int c = 0; c < kNB; ++c)
-      if (c < pnb) {
-        W[(long long)(j0 + c) * ni + j0 + mypos] = v[c];
-        s.pan[c * kPLD + mypos] = v[c];
-      }
   }
   if (tid == 0) s.n_moved = 0;
   __syncthreads();
-  if (own && mypos != tid) {
-    const int slot = atomicAdd(&s.n_moved, 1);
-    s.moved_dst[slot] = j0 + mypos;
-    s.moved_src[slot] = j0 + tid;
+  for (int e = tid; e < pnb * rows; e += kFT) {
+    const int c = e / rows, r = e - c * rows;
+    W[(long long)(j0 + c) * ni + j0 + r] = s.pan[c * kPLD + r];
   }
+  for (int r = tid; r < rows; r += kFT)
+    if (s.prow[r] != r) {
+      const int slot = atomicAdd(&s.n_moved, 1);
+      s.moved_dst[slot] = j0 + r;
+      s.moved_src[slot] = j0 + s.prow[r];
+    }
   __syncthreads();
 }
 
@@ -196,6 +232,7 @@ __global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs 
   const bool p_in_smem = ne * nb <= kTileCols * kBLD;
 
   int iter = 0;
+  const long long t_begin = clock64();
   auto stamp = [&](int k) {
     if (f.prof && blockIdx.x == 0 && tid == 0 && iter < 4) f.prof[iter * 8 + k] = clock64();
   };
@@ -241,7 +278,7 @@ __global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs 
     for (int j0 = 0; j0 < ni; j0 += kNB) {
       const int pnb = min(kNB, ni - j0), rows = ni - j0;
       substamp(0);
-      panel_gepp_regs(s, W, ni, j0, pnb);
+      panel_gepp_warp(s, W, ni, j0, pnb);
       substamp(1);
       // row exchange of every other column; chunks end on column boundaries
       {
@@ -285,12 +322,9 @@ __global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs 
 #pragma unroll
         for (int jj = 0; jj < kNB; ++jj) x[jj] = jj < pnb ? col[jj] : 0.0;
 #pragma unroll
-        for (int jj = 1; jj < kNB; ++jj) {
-          double acc = x[jj];
+        for (int ii = 0; ii < kNB - 1; ++ii)
 #pragma unroll
-          for (int ii = 0; ii < jj; ++ii) acc -= s.pan[ii * kPLD + jj] * x[ii];
-          x[jj] = acc;
-        }
+          for (int jj = ii + 1; jj < kNB; ++jj) x[jj] -= s.pan[ii * kPLD + jj] * x[ii];
 #pragma unroll
         for (int jj = 0; jj < kNB; ++jj)
           if (jj < pnb) col[jj] = x[jj];
@@ -330,7 +364,9 @@ __global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs 
       const int r0 = jb * kNB, bnb = min(kNB, ni - r0);
       for (int e = tid; e < bnb * bnb; e += kFT) {
         const int r = e % bnb, c = e / bnb;
-        s.pan[c * kPLD + r] = W[(long long)(r0 + c) * ni + r0 + r];
+        const double u = W[(long long)(r0 + c) * ni + r0 + r];
+        s.pan[c * kPLD + r] = u;
+        if (r == c) s.rdiag[r] = 1.0 / u;
       }
       __syncthreads();
       for (int c = tid; c < nr; c += kFT) {
@@ -341,11 +377,9 @@ __global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs 
 #pragma unroll
         for (int jj = kNB - 1; jj >= 0; --jj) {
           if (jj < bnb) {
-            double acc = x[jj];
+            x[jj] *= s.rdiag[jj];
 #pragma unroll
-            for (int ii = jj + 1; ii < kNB; ++ii)
-              if (ii < bnb) acc -= s.pan[ii * kPLD + jj] * x[ii];
-            x[jj] = acc / s.pan[jj * kPLD + jj];
+            for (int ii = 0; ii < jj; ++ii) x[ii] -= s.pan[jj * kPLD + ii] * x[jj];
           }
         }
 #pragma unroll
@@ -437,6 +471,7 @@ __global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs 
     }
     __syncthreads();
   }
+  if (f.prof && tid == 0) f.prof[64 + blockIdx.x] = clock64() - t_begin;
 }
 
 bool leaf_fused_supported(int n, int p, int ni, int nb, int dim, bool mixed_terms) {
@@ -447,7 +482,16 @@ bool leaf_fused_supported(int n, int p, int ni, int nb, int dim, bool mixed_term
 
 long long leaf_fused_scratch_per_cta(int ni, int ne, int nb) { return (long long)ni * (ni + 1 + nb); }
 
-int leaf_fused_ctas_per_sm() { return 2; }
+// resident CTAs per SM of the fused kernel at its shared-memory size (the persistent grid is
+// sized from this; the workspace footprint is grid * leaf_fused_scratch_per_cta)
+int leaf_fused_ctas_per_sm() {
+  const size_t smem = sizeof(FusedSmem);
+  if (cudaFuncSetAttribute(leaf_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, leaf_fused_kernel, kFT, smem) != cudaSuccess || n < 1) return 1;
+  return n;
+}
 
 cudaError_t launch_leaf_fused(const LeafFusedArgs& f, int grid, cudaStream_t st) {
   const size_t smem = sizeof(FusedSmem);

@@ -2,6 +2,8 @@
 #include <algorithm>
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
+#include <vector>
 
 #include "gemm.cuh"
 #include "lu.cuh"
@@ -459,6 +461,174 @@ cudaError_t back_subst(int batch, int n, int m, const double* U, long long ldU, 
   return cudaSuccess;
 }
 
+
+// ---- look-ahead driver (n > 512): the next outer panel is factored on a side stream
+// while the main stream runs the bulk of the current trailing update.  Row swaps that
+// would touch columns outside the panel being factored are deferred and applied once per
+// outer block from the block's composite permutation.
+
+// moved-row list (dst, src) of the composite permutation of one outer block's pivots
+__global__ void block_perm_kernel(const int* ipiv, int n, int J, int Jend, int* moved, int* nmoved) {
+  extern __shared__ int perm[];  // perm[i]: original row (relative to J) now at row J + i
+  __shared__ int cnt;
+  const long long b = blockIdx.x;
+  const int len = n - J;
+  for (int i = threadIdx.x; i < len; i += blockDim.x) perm[i] = i;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int j = J; j < Jend; ++j) {
+      const int p = ipiv[b * n + j];
+      if (p != j) {
+        const int t = perm[j - J];
+        perm[j - J] = perm[p - J];
+        perm[p - J] = t;
+      }
+    }
+  __syncthreads();
+  int* mv = moved + b * (4 * kOuterNB);
+  for (int i = threadIdx.x; i < len; i += blockDim.x)
+    if (perm[i] != i) {
+      const int s = atomicAdd(&cnt, 1);
+      mv[2 * s] = J + i;
+      mv[2 * s + 1] = J + perm[i];
+    }
+  __syncthreads();
+  if (threadIdx.x == 0) nmoved[b] = cnt;
+}
+
+// new[dst] = old[src] over the moved rows, one warp per column, columns [ca0,ca1) u [cb0,cb1)
+__global__ void apply_perm_kernel(double* M, long long ld, long long stride, const int* moved, const int* nmoved,
+                                  int ca0, int ca1, int cb0, int cb1) {
+  const long long b = blockIdx.x;
+  const int nm = nmoved[b];
+  const int* mv = moved + b * (4 * kOuterNB);
+  const int lane = threadIdx.x & 31;
+  const int na = ca1 - ca0, ntot = na + (cb1 - cb0);
+  for (int w = blockIdx.y * (blockDim.x / 32) + (threadIdx.x >> 5); w < ntot; w += gridDim.y * (blockDim.x / 32)) {
+    const int c = w < na ? ca0 + w : cb0 + (w - na);
+    double* col = M + b * stride + (long long)c * ld;
+    double v[2 * kOuterNB / 32];
+#pragma unroll
+    for (int u = 0; u < 2 * kOuterNB / 32; ++u) {
+      const int t = lane + 32 * u;
+      if (t < nm) v[u] = col[mv[2 * t + 1]];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 2 * kOuterNB / 32; ++u) {
+      const int t = lane + 32 * u;
+      if (t < nm) col[mv[2 * t]] = v[u];
+    }
+  }
+}
+
+struct LookAhead {
+  cudaStream_t ps = nullptr;
+  std::vector<cudaEvent_t> ev;
+  int* moved = nullptr;
+  int* nmoved = nullptr;
+  long long cap = 0;
+};
+LookAhead& lookahead() {
+  static LookAhead la;
+  return la;
+}
+cudaError_t lookahead_prepare(int batch, int nev) {
+  LookAhead& la = lookahead();
+  if (!la.ps) HPS_TRY(cudaStreamCreateWithFlags(&la.ps, cudaStreamNonBlocking));
+  while ((int)la.ev.size() < nev) {
+    cudaEvent_t e;
+    HPS_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    la.ev.push_back(e);
+  }
+  if (batch > la.cap) {
+    if (la.moved) cudaFree(la.moved);
+    if (la.nmoved) cudaFree(la.nmoved);
+    HPS_TRY(cudaMalloc(&la.moved, sizeof(int) * (size_t)batch * 4 * kOuterNB));
+    HPS_TRY(cudaMalloc(&la.nmoved, sizeof(int) * (size_t)batch));
+    la.cap = batch;
+  }
+  return cudaSuccess;
+}
+
+// inner loop of outer block [J, Jend): panels + in-block swaps/TRSM + in-block updates
+cudaError_t factor_outer_panel(int batch, int n, int J, int Jend, BatchedMat M, int* ipiv, double* stats,
+                               cudaStream_t s) {
+  const long long ld = M.ld, sM = M.stride;
+  double* A = M.p;
+  auto at = [&](int r, int c) { return A + (long long)c * ld + r; };
+  for (int j0 = J; j0 < Jend; j0 += kLuNB) {
+    const int nb = std::min(kLuNB, Jend - j0);
+    HPS_TRY(launch_panel(batch, n, j0, nb, M, ipiv, stats, s));
+    Seg segs[2];
+    segs[0] = Seg{at(0, J), ld, sM, j0 - J, 0};                  // in-block L columns: swaps only
+    segs[1] = Seg{at(0, j0 + nb), ld, sM, Jend - j0 - nb, 1};     // rest of the outer panel: swaps + L11^-1
+    HPS_TRY(launch_swap_trsm(batch, n, j0, nb, A, ld, sM, ipiv, segs, 2, s));
+    HPS_TRY(gemm_sub(batch, n - j0 - nb, Jend - j0 - nb, nb, -1.0, at(j0 + nb, j0), ld, sM, at(j0, j0 + nb), ld, sM,
+                     at(j0 + nb, j0 + nb), ld, sM, s));
+  }
+  return cudaSuccess;
+}
+
+cudaError_t bgetrf_aug_lookahead(int batch, int n, int m, BatchedMat M, int* ipiv, double* stats, cudaStream_t st) {
+  const int K = (n + kOuterNB - 1) / kOuterNB;
+  HPS_TRY(lookahead_prepare(batch, 2 * K + 2));
+  LookAhead& la = lookahead();
+  cudaEvent_t* evP = la.ev.data();      // panel k done (side stream)
+  cudaEvent_t* evA = la.ev.data() + K;  // next panel's columns updated (main stream)
+  cudaEvent_t evF = la.ev[2 * K];
+  const long long ld = M.ld, sM = M.stride;
+  double* A = M.p;
+  auto at = [&](int r, int c) { return A + (long long)c * ld + r; };
+  const int ncol = n + m;
+  static size_t perm_smem_set = 0;
+  const size_t perm_smem = (size_t)n * sizeof(int);
+  if (perm_smem > 48 * 1024 && perm_smem > perm_smem_set) {
+    HPS_TRY(cudaFuncSetAttribute(block_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)perm_smem));
+    perm_smem_set = perm_smem;
+  }
+  HPS_TRY(cudaEventRecord(evF, st));
+  HPS_TRY(cudaStreamWaitEvent(la.ps, evF, 0));
+  HPS_TRY(factor_outer_panel(batch, n, 0, std::min(n, kOuterNB), M, ipiv, stats, la.ps));
+  HPS_TRY(cudaEventRecord(evP[0], la.ps));
+  for (int k = 0; k < K; ++k) {
+    const int J = k * kOuterNB, Jend = std::min(n, J + kOuterNB);
+    HPS_TRY(cudaStreamWaitEvent(st, evP[k], 0));
+    // deferred swaps of block k for every column outside [J, Jend)
+    block_perm_kernel<<<batch, 256, (size_t)(n - J) * sizeof(int), st>>>(ipiv, n, J, Jend, la.moved, la.nmoved);
+    HPS_TRY(cudaGetLastError());
+    {
+      const int ncols = J + (ncol - Jend);
+      const int gy = std::max(1, std::min(65535, (ncols + 7) / 8));
+      apply_perm_kernel<<<dim3(batch, gy), 256, 0, st>>>(A, ld, sM, la.moved, la.nmoved, 0, J, Jend, ncol);
+      HPS_TRY(cudaGetLastError());
+    }
+    // U12 = L11^-1 A12 over the block's row slab
+    for (int j0 = J; j0 < Jend && Jend < ncol; j0 += kLuNB) {
+      const int nb = std::min(kLuNB, Jend - j0);
+      Seg seg{at(0, Jend), ld, sM, ncol - Jend, 1};
+      HPS_TRY(launch_swap_trsm(batch, n, j0, nb, A, ld, sM, ipiv, &seg, 1, st, /*do_swaps=*/0));
+      HPS_TRY(gemm_sub(batch, Jend - j0 - nb, ncol - Jend, nb, -1.0, at(j0 + nb, j0), ld, sM, at(j0, Jend), ld, sM,
+                       at(j0 + nb, Jend), ld, sM, st));
+    }
+    if (Jend < n) {
+      const int J2end = std::min(n, Jend + kOuterNB);
+      // (a) the next outer panel's columns first, then hand them to the side stream
+      HPS_TRY(gemm_sub(batch, n - Jend, J2end - Jend, Jend - J, -1.0, at(Jend, J), ld, sM, at(J, Jend), ld, sM,
+                       at(Jend, Jend), ld, sM, st));
+      HPS_TRY(cudaEventRecord(evA[k], st));
+      HPS_TRY(cudaStreamWaitEvent(la.ps, evA[k], 0));
+      HPS_TRY(factor_outer_panel(batch, n, Jend, J2end, M, ipiv, stats, la.ps));
+      HPS_TRY(cudaEventRecord(evP[k + 1], la.ps));
+      // (b) the rest of the trailing update, concurrently with that panel
+      HPS_TRY(gemm_sub(batch, n - Jend, ncol - J2end, Jend - J, -1.0, at(Jend, J), ld, sM, at(J, J2end), ld, sM,
+                       at(Jend, J2end), ld, sM, st));
+    }
+  }
+  return back_subst(batch, n, m, A, ld, sM, at(0, n), ld, sM, st);
+}
+
 }  // namespace
 
 int bgetrf_max_n() { return kMaxCluster * kMaxRowsPerCta; }
@@ -472,6 +642,7 @@ cudaError_t lu_stats_init(double* stats, int batch, cudaStream_t st) {
 cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double* stats, cudaStream_t st) {
   if (batch <= 0 || n <= 0) return cudaSuccess;
   if (n > bgetrf_max_n()) return cudaErrorInvalidValue;
+  if (n > 2 * kOuterNB && getenv("HPS_LU_LOOKAHEAD")) return bgetrf_aug_lookahead(batch, n, m, M, ipiv, stats, st);
   const long long ld = M.ld, sM = M.stride;
   double* A = M.p;
   auto at = [&](int r, int c) { return A + (long long)c * ld + r; };
