@@ -98,12 +98,103 @@ __device__ void update_smem(int m, int n, int k, const double* A, int lda, const
   }
 }
 
+// One warp factors the rows x pnb panel in s.pan.  Lane-strided rows r = j + 1 + lane + 32 q; the
+// slots past the last row are clamped onto it, so loads/stores need no predicates (the clamped
+// lanes recompute and store exactly the owner's value).
+template <int NQ>
+__device__ __forceinline__ void gepp_warp_body(FusedSmem& s, int rows, int pnb, int j0) {
+  const int lane = threadIdx.x & 31;
+  for (int j = 0; j < pnb; ++j) {
+    double* pj = s.pan + j * kPLD;
+    double bv = -1.0;
+    int bp = INT_MAX;
+    {
+      double a[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) a[q] = fabs(pj[min(j + lane + 32 * q, rows - 1)]);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const double av = isnan(a[q]) ? INFINITY : a[q];
+        if (j + lane + 32 * q < rows && av > bv) bv = av, bp = j + lane + 32 * q;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int p2 = __shfl_xor_sync(0xffffffffu, bp, o);
+      if (v2 > bv || (v2 == bv && p2 < bp)) bv = v2, bp = p2;
+    }
+    if (bp != j) {
+      if (lane < pnb) {
+        const double t = s.pan[lane * kPLD + j];
+        s.pan[lane * kPLD + j] = s.pan[lane * kPLD + bp];
+        s.pan[lane * kPLD + bp] = t;
+      }
+      if (lane == 0) {
+        const int t = s.prow[j];
+        s.prow[j] = s.prow[bp];
+        s.prow[bp] = t;
+      }
+    }
+    if (lane == 0) {
+      if (!(bv > 0.0) || !isfinite(bv)) {
+        if (s.first_zero < 0) s.first_zero = j0 + j;
+      } else {
+        s.pmin = fmin(s.pmin, bv);
+        s.pmax = fmax(s.pmax, bv);
+      }
+    }
+    __syncwarp();
+    const double pv = pj[j];
+    if (fabs(pv) > 0.0 && j + 1 < rows) {
+      const double rinv = 1.0 / pv;
+      int off[NQ];
+      double l[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) off[q] = min(j + 1 + lane + 32 * q, rows - 1);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) l[q] = pj[off[q]] * rinv;
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) pj[off[q]] = l[q];
+      // rank-1 update, four columns at a time (4*NQ loads in flight per lane)
+      int c = j + 1;
+      for (; c + 4 <= pnb; c += 4) {
+        const double* pc = s.pan + c * kPLD;
+        double u[4], a[4][NQ];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) u[k] = pc[k * kPLD + j];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) a[k][q] = pc[k * kPLD + off[q]];
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) s.pan[(c + k) * kPLD + off[q]] = a[k][q] - l[q] * u[k];
+      }
+      for (; c < pnb; ++c) {
+        double* pc = s.pan + c * kPLD;
+        const double u = pc[j];
+        double a[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) a[q] = pc[off[q]];
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) pc[off[q]] = a[q] - l[q] * u;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // GEPP of panel columns [j0, j0+pnb) over rows [j0, ni) of W by ONE warp on the panel staged in
 // s.pan (rows physically exchanged; lane-strided rows, no CTA barrier per column).  Pivot = max
 // |a| with NaN ranked as +inf, ties -> lowest current row (the LAPACK/Eigen rule).  Writes the
 // factored panel back to W and fills the moved-row list for the other columns.
 __device__ void panel_gepp_warp(FusedSmem& s, double* W, int ni, int j0, int pnb) {
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x;
   const int rows = ni - j0;
   for (int e = tid; e < pnb * rows; e += kFT) {
     const int c = e / rows, r = e - c * rows;
@@ -112,101 +203,21 @@ __device__ void panel_gepp_warp(FusedSmem& s, double* W, int ni, int j0, int pnb
   for (int r = tid; r < rows; r += kFT) s.prow[r] = r;
   __syncthreads();
   if (tid < 32) {
-    for (int j = 0; j < pnb; ++j) {
-      double* pj = s.pan + j * kPLD;
-      double bv = -1.0;
-      int bp = INT_MAX;
-      {
-        double a[kRowsPerLane];
-#pragma unroll
-        for (int q = 0; q < kRowsPerLane; ++q) {
-          const int r = j + lane + 32 * q;
-          a[q] = r < rows ? fabs(pj[r]) : -1.0;
-        }
-#pragma unroll
-        for (int q = 0; q < kRowsPerLane; ++q) {
-          const double av = isnan(a[q]) ? INFINITY : a[q];
-          if (av > bv) bv = av, bp = j + lane + 32 * q;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int p2 = __shfl_xor_sync(0xffffffffu, bp, o);
-        if (v2 > bv || (v2 == bv && p2 < bp)) bv = v2, bp = p2;
-      }
-      if (bp != j) {
-        for (int c = lane; c < pnb; c += 32) {
-          const double t = s.pan[c * kPLD + j];
-          s.pan[c * kPLD + j] = s.pan[c * kPLD + bp];
-          s.pan[c * kPLD + bp] = t;
-        }
-        if (lane == 0) {
-          const int t = s.prow[j];
-          s.prow[j] = s.prow[bp];
-          s.prow[bp] = t;
-        }
-      }
-      if (lane == 0) {
-        if (!(bv > 0.0) || !isfinite(bv)) {
-          if (s.first_zero < 0) s.first_zero = j0 + j;
-        } else {
-          s.pmin = fmin(s.pmin, bv);
-          s.pmax = fmax(s.pmax, bv);
-        }
-      }
-      __syncwarp();
-      const double pv = pj[j];
-      if (fabs(pv) > 0.0) {
-        const double rinv = 1.0 / pv;
-        double l[kRowsPerLane];
-#pragma unroll
-        for (int q = 0; q < kRowsPerLane; ++q) {
-          const int r = j + 1 + lane + 32 * q;
-          l[q] = 0.0;
-          if (r < rows) {
-            l[q] = pj[r] * rinv;
-            pj[r] = l[q];
-          }
-        }
-        // rank-1 update, four columns at a time so 28 loads are in flight per lane
-        int c = j + 1;
-        for (; c + 4 <= pnb; c += 4) {
-          double u[4], a[4][kRowsPerLane];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) u[k] = s.pan[(c + k) * kPLD + j];
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-#pragma unroll
-            for (int q = 0; q < kRowsPerLane; ++q) {
-              const int r = j + 1 + lane + 32 * q;
-              a[k][q] = r < rows ? s.pan[(c + k) * kPLD + r] : 0.0;
-            }
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-#pragma unroll
-            for (int q = 0; q < kRowsPerLane; ++q) {
-              const int r = j + 1 + lane + 32 * q;
-              if (r < rows) s.pan[(c + k) * kPLD + r] = a[k][q] - l[q] * u[k];
-            }
-        }
-        for (; c < pnb; ++c) {
-          double* pc = s.pan + c * kPLD;
-          const double u = pc[j];
-#pragma unroll
-          for (int q = 0; q < kRowsPerLane; ++q) {
-            const int r = j + 1 + lane + 32 * q;
-            if (r < rows) pc[r] -= l[q] * u;
-          }
-        }
-      }
-      __syncwarp();
+    switch ((rows + 31) / 32) {
+      case 1: gepp_warp_body<1>(s, rows, pnb, j0); break;
+      case 2: gepp_warp_body<2>(s, rows, pnb, j0); break;
+      case 3: gepp_warp_body<3>(s, rows, pnb, j0); break;
+      case 4: gepp_warp_body<4>(s, rows, pnb, j0); break;
+      case 5: gepp_warp_body<5>(s, rows, pnb, j0); break;
+      case 6: gepp_warp_body<6>(s, rows, pnb, j0); break;
+      default: gepp_warp_body<kRowsPerLane>(s, rows, pnb, j0); break;
     }
   }
   if (tid == 0) s.n_moved = 0;
   __syncthreads();
-  for (int e = tid; e < pnb * rows; e += kFT) {
-    const int c = e / rows, r = e - c * rows;
+  // only the U11 block goes back: L21 lives on in s.pan for the trailing update and is dead after
+  for (int e = tid; e < pnb * pnb; e += kFT) {
+    const int c = e / pnb, r = e - c * pnb;
     W[(long long)(j0 + c) * ni + j0 + r] = s.pan[c * kPLD + r];
   }
   for (int r = tid; r < rows; r += kFT)
