@@ -105,6 +105,34 @@ int hpsg_create(const hpsg_tree* tree, const hpsg_term* terms, int n_terms, cons
                 const hpsg_options* opts, hpsg_ctx** out);
 /* HpsSolver::build(), solver.hpp:48 / solver.cpp:144-151: leaf stage + all merge levels */
 int hpsg_build(hpsg_ctx* ctx);
+
+/* ---- subtree-sharded builds (the staged build_leaf/merge_internal API of
+ * solver.hpp:51-56 at subtree granularity).  A PART is the subtree rooted at node
+ * root_index (index within tree.levels[root_depth], = DFS order for uniform trees) cut at
+ * depth cut_depth: cut_depth == L -> its leaves are real leaves (leaf stage + merges);
+ * cut_depth < L -> its leaves are the depth-cut_depth nodes, whose [h|T] (n x (1+n),
+ * column-major, h first) are inputs.  Parts compose: the [h|T] a part produces at its root
+ * is exactly the input its parent part expects, and the boundary data a cut part's downward
+ * pass produces for its cut nodes is exactly the root data of the parts below. */
+typedef struct {
+  int root_depth;
+  long long root_index;
+  int cut_depth;
+} hpsg_part;
+int hpsg_create_part(const hpsg_tree* tree, const hpsg_part* part, const hpsg_term* terms, int n_terms,
+                     const hpsg_field* source, const hpsg_options* opts, hpsg_ctx** out);
+/* n_cut input nodes of cut_nb boundary points each (0 for a part with real leaves); root_nb =
+ * boundary points of the part root */
+int hpsg_part_sizes(hpsg_ctx* ctx, long long* n_cut, int* cut_nb, int* root_nb);
+/* [h|T] of the part root after hpsg_build (root_depth > 0): device-to-device into d_dst
+ * (root_nb x (1+root_nb)); MergeOutput::T/h, merge.hpp:58-66 */
+int hpsg_part_root_ht(hpsg_ctx* ctx, double* d_dst);
+/* input [h|T] of cut node k (0 <= k < n_cut, level order) from device memory; all must be set
+ * before hpsg_build */
+int hpsg_part_set_cut_ht(hpsg_ctx* ctx, long long k, const double* d_src);
+/* downward pass of a cut part (HpsSolver::propagate, solver.cpp:188-228): root boundary data
+ * (device, nrhs x root_nb) -> boundary data of every cut node (device, nrhs x n_cut x cut_nb) */
+int hpsg_part_solve_cut(hpsg_ctx* ctx, const double* d_g_root, int nrhs, double* d_g_cut);
 /* HpsSolver::solve(g_root, leaf_g_out), solver.hpp:64 / solver.cpp:238-252, for nrhs boundary
  * vectors (g_root: nrhs x root_bsize).  u_out: nrhs x n_leaves x p^dim (host);
  * leaf_g_out (optional): nrhs x n_leaves x (boundary Gauss points of a leaf). */

@@ -242,9 +242,12 @@ LeafOperators make_leaf_operators(int dim, int p, double side) {
 }
 
 long long UniformTree::level_first_id(int d) const {
+  // reference id of the first node at part depth d (breadth-first ids of the FULL tree, mesh.cpp:113-118)
   long long id = 0, cnt = 1;
-  for (int k = 0; k < d; ++k) id += cnt, cnt *= nchild;
-  return id;
+  for (int k = 0; k < root_depth + d; ++k) id += cnt, cnt *= nchild;
+  long long off = root_index;
+  for (int k = 0; k < d; ++k) off *= nchild;
+  return id + off;
 }
 long long UniformTree::level_count(int d) const {
   long long c = 1;
@@ -252,37 +255,67 @@ long long UniformTree::level_count(int d) const {
   return c;
 }
 
-UniformTree make_uniform_tree(int dim, int p, int L, double lo, double hi) {
+UniformTree make_part_tree(int dim, int p, int L_full, double lo, double hi, int root_depth, long long root_index,
+                           int cut_depth) {
   if (!(hi > lo)) throw std::runtime_error("build_uniform_tree: empty domain");
+  if (root_depth < 0 || cut_depth <= root_depth || cut_depth > L_full)
+    throw std::runtime_error("tree part: need 0 <= root_depth < cut_depth <= L");
   UniformTree t;
   t.dim = dim;
   t.p = p;
   t.q = p - 2;
-  t.L = L;
+  t.L = cut_depth - root_depth;
+  t.L_full = L_full;
+  t.root_depth = root_depth;
+  t.root_index = root_index;
+  t.cut = cut_depth < L_full;
   t.lo = lo;
   t.hi = hi;
   t.nchild = dim == 2 ? 4 : 8;
   t.nface = 2 * dim;
-  const long long nl = t.level_count(L);
-  t.leaf_lo.assign(size_t(nl) * 6, 0.0);  // lo[3], hi[3] per leaf
-  for (long long o = 0; o < nl; ++o) {
-    double blo[3] = {lo, lo, dim == 3 ? lo : 0.0}, bhi[3] = {hi, hi, dim == 3 ? hi : 0.0};
-    long long div = nl;
-    for (int l = 0; l < L; ++l) {
-      div /= t.nchild;
-      const int c = int((o / div) % t.nchild);
-      for (int k = 0; k < dim; ++k) {
-        const double mid = 0.5 * (blo[k] + bhi[k]);  // repeated midpoint split, as mesh.cpp:31-43
-        if (kChildOffset[c][k])
-          blo[k] = mid;
-        else
-          bhi[k] = mid;
-      }
+  if (root_index < 0 || root_index >= t.level_count(root_depth))
+    throw std::runtime_error("tree part: root index out of range");
+  // part root box: repeated midpoint splits along the path from the domain root (mesh.cpp:31-43)
+  double blo[3] = {lo, lo, dim == 3 ? lo : 0.0}, bhi[3] = {hi, hi, dim == 3 ? hi : 0.0};
+  long long div = t.level_count(root_depth);
+  for (int l = 0; l < root_depth; ++l) {
+    div /= t.nchild;
+    const int c = int((root_index / div) % t.nchild);
+    for (int k = 0; k < dim; ++k) {
+      const double mid = 0.5 * (blo[k] + bhi[k]);
+      if (kChildOffset[c][k])
+        blo[k] = mid;
+      else
+        bhi[k] = mid;
     }
-    for (int k = 0; k < 3; ++k) t.leaf_lo[size_t(o) * 6 + k] = blo[k], t.leaf_lo[size_t(o) * 6 + 3 + k] = bhi[k];
   }
-  t.leaf_side = (hi - lo) / double(1LL << L);
+  for (int k = 0; k < 3; ++k) t.rlo[k] = blo[k], t.rhi[k] = bhi[k];
+  if (!t.cut) {
+    const long long nl = t.level_count(t.L);
+    t.leaf_lo.assign(size_t(nl) * 6, 0.0);  // lo[3], hi[3] per leaf, DFS order within the part
+    for (long long o = 0; o < nl; ++o) {
+      double a[3] = {t.rlo[0], t.rlo[1], t.rlo[2]}, b[3] = {t.rhi[0], t.rhi[1], t.rhi[2]};
+      long long dv = nl;
+      for (int l = 0; l < t.L; ++l) {
+        dv /= t.nchild;
+        const int c = int((o / dv) % t.nchild);
+        for (int k = 0; k < dim; ++k) {
+          const double mid = 0.5 * (a[k] + b[k]);
+          if (kChildOffset[c][k])
+            a[k] = mid;
+          else
+            b[k] = mid;
+        }
+      }
+      for (int k = 0; k < 3; ++k) t.leaf_lo[size_t(o) * 6 + k] = a[k], t.leaf_lo[size_t(o) * 6 + 3 + k] = b[k];
+    }
+  }
+  t.leaf_side = (hi - lo) / double(1LL << L_full);
   return t;
+}
+
+UniformTree make_uniform_tree(int dim, int p, int L, double lo, double hi) {
+  return make_part_tree(dim, p, L, lo, hi, 0, 0, L);
 }
 
 namespace {
@@ -438,8 +471,8 @@ std::vector<double> root_boundary_points(const UniformTree& t) {
   std::vector<double> gx, gw, out;
   gauss_rule(t.q, gx, gw);
   for (int f = 0; f < t.nface; ++f) {
-    double lo[3] = {t.lo, t.lo, t.dim == 3 ? t.lo : 0.0}, hi[3] = {t.hi, t.hi, t.dim == 3 ? t.hi : 0.0};
-    collect(lo, hi, t.dim, f, t.L, t.q, gx, out);
+    double lo[3] = {t.rlo[0], t.rlo[1], t.rlo[2]}, hi[3] = {t.rhi[0], t.rhi[1], t.rhi[2]};
+    collect(lo, hi, t.dim, f, t.L_full - t.root_depth, t.q, gx, out);
   }
   return out;
 }

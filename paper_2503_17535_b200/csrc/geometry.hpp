@@ -48,17 +48,30 @@ LeafOperators make_leaf_operators(int dim, int p, double side);
 // construction order (breadth-first by level; proj/src/mesh.cpp:113-118); for a
 // uniform tree the level order of tree.levels[d] (DFS) coincides with id order,
 // and children of level-d node i are level-(d+1) nodes nchild*i + c.
+//
+// A tree PART (subtree-sharded builds) is the subtree of the full depth-L_full tree
+// rooted at node root_index (level order) of depth root_depth, cut at depth root_depth + L:
+// part depth d <-> full depth root_depth + d.  cut == false: the part's leaves are real leaves;
+// cut == true: they are internal nodes whose [h|T] are inputs.  The full tree is the part
+// (0, 0, L_full).
 struct UniformTree {
   int dim = 2, p = 0, q = 0, L = 0, nchild = 4, nface = 4;
   double lo = -1, hi = 1;
-  long long level_first_id(int d) const;   // id of the first node at depth d
+  int L_full = 0, root_depth = 0;
+  long long root_index = 0;
+  bool cut = false;
+  double rlo[3] = {0, 0, 0}, rhi[3] = {0, 0, 0};  // part root box
+  long long level_first_id(int d) const;   // reference id of the first node at part depth d
   long long level_count(int d) const;      // nchild^d
+  int face_shift(int d) const { return L_full - 1 - (root_depth + d); }  // child face = q 2^shift sections
   int n_leaves() const { return int(level_count(L)); }
   // leaf lower corners in DFS order (n_leaves x 3) and side length
   std::vector<double> leaf_lo;
   double leaf_side = 0;
 };
 UniformTree make_uniform_tree(int dim, int p, int L, double lo, double hi);
+UniformTree make_part_tree(int dim, int p, int L_full, double lo, double hi, int root_depth, long long root_index,
+                           int cut_depth);
 
 // Merge of one level (all nodes at depth d of a uniform tree share it).
 // Child boundary layout: faces in reference order, s points per face section.

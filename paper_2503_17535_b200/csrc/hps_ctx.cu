@@ -106,6 +106,7 @@ struct hpsg_ctx {
   cudaEvent_t ev[8] = {};
   cudaEvent_t lev_ev[25] = {};  // merge level boundaries
   hpsg_tree tree{};
+  hpsg_part part{};  // (0, 0, L) for the whole tree
   hpsg_options opts{};
   hpsg::UniformTree T;
   hpsg::LeafOperators ops;
@@ -133,11 +134,16 @@ struct hpsg_ctx {
   std::vector<std::unique_ptr<DevBuf>> G, GI;
   DevBuf Ui, Ue, g_in, u_out, lg_out, gemv_scratch;
   bool built = false;
+  std::vector<char> cut_set;  // cut part: which input [h|T] have been provided
   hpsg_stats stats{};
   int launches = 0;
 
   long long strideLeafM() const { return (long long)ops.ni * (ops.ni + 1 + ops.nb); }
-  long long strideLeafHT() const { return (long long)ops.nb * (1 + ops.nb); }
+  // [h|T] per part leaf: a real leaf (nb x (1+nb)) or, for a cut part, an input node
+  int leaf_nb() const { return T.cut ? lv[T.L - 1].child_nb : ops.nb; }
+  long long strideLeafHT() const { return (long long)leaf_nb() * (1 + leaf_nb()); }
+  // the merge at part depth d is the reference's root merge (no T/h, optional implicit S)
+  bool global_root(int d) const { return d == 0 && T.root_depth == 0; }
 };
 
 namespace {
@@ -225,12 +231,13 @@ double counted_build_flops(const hpsg_ctx* c) {
   // merge 2/3 n_int^3 + 2 n_int^2 n_ext + 2 n_ext n_int n_ext; root explicit 2/3 n_int^3 + 2 n_int^2 n_ext,
   // root implicit 2/3 n_int^3.
   const double ni = c->ops.ni, ne = c->ops.ne, nb = c->ops.nb, n = c->ops.n;
-  double f = c->T.n_leaves() *
-             (2.0 / 3.0 * ni * ni * ni + 2 * ni * ni * ne + 2 * ni * ne * nb + 2 * nb * n * nb + 2 * ni * ni + 2 * nb * n);
+  double f = c->T.cut ? 0.0
+                      : c->T.n_leaves() * (2.0 / 3.0 * ni * ni * ni + 2 * ni * ni * ne + 2 * ni * ne * nb +
+                                           2 * nb * n * nb + 2 * ni * ni + 2 * nb * n);
   for (const Level& L : c->lv) {
     const double a = L.n_int, e = L.n_ext;
     double per;
-    if (L.d > 0)
+    if (!c->global_root(L.d))
       per = 2.0 / 3.0 * a * a * a + 2 * a * a * e + 2 * e * a * e;
     else
       per = c->opts.root_implicit_S ? 2.0 / 3.0 * a * a * a : 2.0 / 3.0 * a * a * a + 2 * a * a * e;
@@ -247,7 +254,8 @@ void setup(hpsg_ctx* c) {
   if ((t.dim == 2 && t.p > 22) || (t.dim == 3 && t.p > 8))
     throw HpsError{HPSG_ERR_INVALID, "hpsg_create: p^dim > 512 not supported by the leaf kernel"};
   if (!(t.hi > t.lo)) throw HpsError{HPSG_ERR_INVALID, "build_uniform_tree: empty domain"};
-  c->T = hpsg::make_uniform_tree(t.dim, t.p, t.L, t.lo, t.hi);
+  c->T = hpsg::make_part_tree(t.dim, t.p, t.L, t.lo, t.hi, c->part.root_depth, c->part.root_index,
+                              c->part.cut_depth);
   c->ops = hpsg::make_leaf_operators(t.dim, t.p, c->T.leaf_side);
   const hpsg::LeafOperators& o = c->ops;
   const int nl = c->T.n_leaves();
@@ -267,12 +275,12 @@ void setup(hpsg_ctx* c) {
   upload(c->ZQeP, zq, &c->dev_bytes, st);
 
   // merge levels: child face size s_d = q * 2^(L-1-d) (2D) / q^2 * 4^(L-1-d) (3D)
-  c->lv.resize(t.L);
-  for (int d = t.L - 1; d >= 0; --d) {
+  c->lv.resize(c->T.L);
+  for (int d = c->T.L - 1; d >= 0; --d) {
     Level& L = c->lv[d];
     L.d = d;
     L.nodes = c->T.level_count(d);
-    const long long f = 1LL << (t.L - 1 - d);
+    const long long f = 1LL << c->T.face_shift(d);
     const int s = int(t.dim == 2 ? q * f : (long long)q * q * f * f);
     L.mt = hpsg::make_merge_tables(t.dim, s);
     L.n_int = L.mt.n_int();
@@ -286,8 +294,8 @@ void setup(hpsg_ctx* c) {
     upload(L.ah_src, L.mt.ah_src, &c->dev_bytes, st);
     upload(L.down, L.mt.down, &c->dev_bytes, st);
   }
-  c->stats.n_leaves = nl;
-  c->stats.n_points = (long long)nl * o.n;
+  c->stats.n_leaves = c->T.cut ? 0 : nl;
+  c->stats.n_points = c->T.cut ? 0 : (long long)nl * o.n;
   c->stats.root_bsize = c->lv[0].n_ext;
   c->stats.top_D_size = c->lv[0].n_int;
   c->stats.tree_depth = t.L;
@@ -304,7 +312,9 @@ void alloc_build(hpsg_ctx* c) {
     if (c->terms[i].role == HPSG_ROLE_SECOND_ORDER && c->terms[i].axis != c->terms[i].axis2) mixed = true;
   c->fused = hpsk::leaf_fused_supported(o.n, o.p, o.ni, o.nb, c->tree.dim, mixed) &&
              !(path && std::string(path) == "batched");
-  if (c->fused) {
+  if (c->T.cut) {
+    c->fused = false;  // no leaf stage: the part's leaves are input nodes
+  } else if (c->fused) {
     int nsm = 0;
     ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->opts.device), "sm count");
     c->fused_grid = int(std::min<long long>(nl, (long long)nsm * hpsk::leaf_fused_ctas_per_sm()));
@@ -320,15 +330,17 @@ void alloc_build(hpsg_ctx* c) {
     c->yv = c->leafM.d() + (long long)o.ni * o.ni;
     c->yv_stride = c->strideLeafM();
   }
-  c->leafStats.alloc(size_t(nl) * 3 * 8, tot);
-  c->leafBad.alloc(size_t(nl) * 4, tot);
+  if (!c->T.cut) {
+    c->leafStats.alloc(size_t(nl) * 3 * 8, tot);
+    c->leafBad.alloc(size_t(nl) * 4, tot);
+  }
   c->leafHT.alloc(size_t(nl) * c->strideLeafHT() * 8, tot);
   size_t bmax = 0;
   for (Level& L : c->lv) {
     L.MD.alloc(size_t(L.nodes) * L.strideMD() * 8, tot);
     L.piv.alloc(size_t(L.nodes) * L.n_int * 4, tot);
     L.stats.alloc(size_t(L.nodes) * 3 * 8, tot);
-    if (L.d > 0) {
+    if (!c->global_root(L.d)) {
       L.AH.alloc(size_t(L.nodes) * L.strideAH() * 8, tot);
       bmax = std::max(bmax, size_t(L.nodes) * L.n_ext * L.n_int * 8);
     }
@@ -343,7 +355,7 @@ void check_leaf_errors(hpsg_ctx* c) {
   std::vector<double> s(size_t(nl) * 3);
   ck(cudaMemcpyAsync(s.data(), c->leafStats.p, s.size() * 8, cudaMemcpyDeviceToHost, c->st), "stats D2H");
   ck(cudaStreamSynchronize(c->st), "leaf sync");
-  const long long leaf_id0 = c->T.level_first_id(c->tree.L);
+  const long long leaf_id0 = c->T.level_first_id(c->T.L);
   for (int i = 0; i < nl; ++i)
     if (bad[i] != INT_MAX) {
       const double* b = &c->T.leaf_lo[size_t(i) * 6];
@@ -508,10 +520,10 @@ void run_leaf_stage(hpsg_ctx* c) {
 
 void run_merge_level(hpsg_ctx* c, int d) {
   Level& L = c->lv[d];
-  const bool root = d == 0;
-  const double* child_HT = (d == c->tree.L - 1) ? c->leafHT.d() : c->lv[d + 1].AH.d();
+  const bool root = c->global_root(d);
+  const double* child_HT = (d == c->T.L - 1) ? c->leafHT.d() : c->lv[d + 1].AH.d();
   const long long child_stride =
-      (d == c->tree.L - 1) ? c->strideLeafHT() : c->lv[d + 1].strideAH();
+      (d == c->T.L - 1) ? c->strideLeafHT() : c->lv[d + 1].strideAH();
   hpsk::GatherArgs ga{};
   ga.s = L.mt.s;
   ga.nchild = L.mt.nchild;
@@ -583,13 +595,13 @@ void run_merge_level(hpsg_ctx* c, int d) {
 void ensure_solve_ws(hpsg_ctx* c, int nrhs) {
   if (c->ws_nrhs >= nrhs) return;
   size_t* tot = &c->dev_bytes;
-  const int Lh = c->tree.L;
+  const int Lh = c->T.L;
   c->G.resize(Lh + 1);
   c->GI.resize(Lh);
   for (int d = 0; d <= Lh; ++d) {
     if (!c->G[d]) c->G[d] = std::make_unique<DevBuf>();
     const long long nodes = c->T.level_count(d);
-    const long long nb = d < Lh ? c->lv[d].n_ext : c->ops.nb;
+    const long long nb = d < Lh ? c->lv[d].n_ext : c->leaf_nb();
     c->G[d]->alloc(size_t(nodes) * (1 + nb) * nrhs * 8, tot);
     if (d < Lh) {
       if (!c->GI[d]) c->GI[d] = std::make_unique<DevBuf>();
@@ -597,15 +609,17 @@ void ensure_solve_ws(hpsg_ctx* c, int nrhs) {
     }
   }
   const long long nl = c->T.n_leaves();
-  c->Ui.alloc(size_t(nl) * c->ops.ni * nrhs * 8, tot);
-  c->Ue.alloc(size_t(nl) * c->ops.ne * nrhs * 8, tot);
+  if (!c->T.cut) {
+    c->Ui.alloc(size_t(nl) * c->ops.ni * nrhs * 8, tot);
+    c->Ue.alloc(size_t(nl) * c->ops.ne * nrhs * 8, tot);
+  }
   c->gemv_scratch.alloc(size_t(8) << 20, tot);  // split-k partial sums (64 MB)
   c->ws_nrhs = nrhs;
 }
 
 // Downward pass + leaf reconstruction on device buffers.  d_g: root_bsize x nrhs; d_u: nrhs x n_leaves x npts.
 void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_leaf_g) {
-  const int Lh = c->tree.L;
+  const int Lh = c->T.L;
   ensure_solve_ws(c, nrhs);
   const int nb0 = c->lv[0].n_ext;
   hpsk::launch_pack_root(c->G[0]->d(), d_g, nb0, nrhs, c->st);
@@ -615,7 +629,7 @@ void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_
     const long long ldG = 1 + L.n_ext;
     const long long sG = ldG * nrhs;
     const long long sGI = (long long)L.n_int * nrhs;
-    if (d == 0 && c->opts.root_implicit_S) {
+    if (c->global_root(d) && c->opts.root_implicit_S) {
       // g_int = -(x_h + D^-1 C g)   (solver.cpp:204-206, merge.cpp:156-174)
       GemmArgs g;
       g.m = L.n_int;
@@ -673,6 +687,13 @@ void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_
     s.strideGc = (long long)(1 + L.child_nb) * nrhs;
     hpsk::launch_scatter(s, int(L.nodes), c->st);
     ++c->launches;
+  }
+  if (c->T.cut) {
+    // cut part: the boundary data of its input nodes is the result (nrhs x n_cut x cut_nb)
+    hpsk::launch_unpack_leaf_g(d_leaf_g, c->G[Lh]->d(), c->leaf_nb(), nrhs, c->T.n_leaves(), c->st);
+    ++c->launches;
+    ck(cudaGetLastError(), "solve kernels");
+    return;
   }
   // leaves: u_i = [v | Y_i][1; g],  u_e = P g   (solver.cpp:230-236)
   const hpsg::LeafOperators& o = c->ops;
@@ -737,9 +758,10 @@ double solve_bytes(const hpsg_ctx* c, int nrhs) {
   // plus write u (with the leaf block stored as interior rows only)
   double b = 0;
   for (const Level& L : c->lv) {
-    const double cols = (L.d == 0 && c->opts.root_implicit_S) ? L.n_ext + L.n_int : 1 + L.n_ext;
+    const double cols = (c->global_root(L.d) && c->opts.root_implicit_S) ? L.n_ext + L.n_int : 1 + L.n_ext;
     b += double(L.nodes) * L.n_int * cols * 8;
   }
+  if (c->T.cut) return b + double(c->T.n_leaves()) * c->leaf_nb() * 8 * nrhs;
   b += double(c->T.n_leaves()) * c->ops.ni * (1 + c->ops.nb) * 8;
   b += double(c->T.n_leaves()) * c->ops.n * 8 * nrhs;
   return b;
@@ -774,11 +796,19 @@ const char* hpsg_build_info(void) {
 
 int hpsg_create(const hpsg_tree* tree, const hpsg_term* terms, int n_terms, const hpsg_field* source,
                 const hpsg_options* opts, hpsg_ctx** out) {
-  if (!out || !tree) return HPSG_ERR_INVALID;
+  if (!tree) return HPSG_ERR_INVALID;
+  const hpsg_part whole{0, 0, tree->L};
+  return hpsg_create_part(tree, &whole, terms, n_terms, source, opts, out);
+}
+
+int hpsg_create_part(const hpsg_tree* tree, const hpsg_part* part, const hpsg_term* terms, int n_terms,
+                     const hpsg_field* source, const hpsg_options* opts, hpsg_ctx** out) {
+  if (!out || !tree || !part) return HPSG_ERR_INVALID;
   *out = nullptr;
   if (hpsg_device_count() <= 0) return HPSG_ERR_NO_DEVICE;
   auto c = std::make_unique<hpsg_ctx>();
   c->tree = *tree;
+  c->part = *part;
   if (opts) c->opts = *opts;
   else c->opts.literal_sign = 1;
   const int rc = guarded(c.get(), [&] {
@@ -808,6 +838,7 @@ int hpsg_create(const hpsg_tree* tree, const hpsg_term* terms, int n_terms, cons
       c->has_source = 1;
     }
     alloc_build(c.get());
+    c->cut_set.assign(c->T.cut ? size_t(c->T.n_leaves()) : 0, 0);
     ck(cudaStreamSynchronize(c->st), "create sync");
   });
   if (rc != HPSG_OK) {
@@ -824,12 +855,15 @@ int hpsg_build(hpsg_ctx* c) {
   return guarded(c, [&] {
     c->launches = 0;
     c->built = false;
+    for (size_t k = 0; k < c->cut_set.size(); ++k)
+      if (!c->cut_set[k])
+        throw HpsError{HPSG_ERR_STATE, hpsg::fmt("hpsg_build: input [h|T] of cut node %lld not set", (long long)k)};
     ck(cudaEventRecord(c->ev[0], c->st), "ev");
-    run_leaf_stage(c);
+    if (!c->T.cut) run_leaf_stage(c);
     ck(cudaEventRecord(c->ev[1], c->st), "ev");
-    check_leaf_errors(c);
+    if (!c->T.cut) check_leaf_errors(c);
     ck(cudaEventRecord(c->ev[2], c->st), "ev");
-    for (int d = c->tree.L - 1; d >= 0; --d) {
+    for (int d = c->T.L - 1; d >= 0; --d) {
       ck(cudaEventRecord(c->lev_ev[d + 1], c->st), "ev");
       run_merge_level(c, d);
     }
@@ -842,7 +876,7 @@ int hpsg_build(hpsg_ctx* c) {
     c->stats.t_leaf_ms = a;
     c->stats.t_merge_ms = b;
     c->stats.t_build_ms = a + b;
-    c->stats.n_levels = std::min(c->tree.L, 24);
+    c->stats.n_levels = std::min(c->T.L, 24);
     for (int d = 0; d < c->stats.n_levels; ++d) {
       float t = 0;
       ck(cudaEventElapsedTime(&t, c->lev_ev[d + 1], c->lev_ev[d]), "elapsed");
@@ -857,6 +891,7 @@ int hpsg_build(hpsg_ctx* c) {
 int hpsg_solve_device(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u) {
   if (!c || !d_g || !d_u || nrhs < 1) return HPSG_ERR_INVALID;
   if (!c->built) return fail(c, HPSG_ERR_STATE, "hpsg_solve: build() first");
+  if (c->T.cut) return fail(c, HPSG_ERR_STATE, "hpsg_solve: a cut part has no leaves (hpsg_part_solve_cut)");
   return guarded(c, [&] {
     c->launches = 0;
     ck(cudaEventRecord(c->ev[4], c->st), "ev");
@@ -874,6 +909,7 @@ int hpsg_solve_device(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u) {
 int hpsg_solve(hpsg_ctx* c, const double* g_root, int nrhs, double* u_out, double* leaf_g_out) {
   if (!c || !g_root || !u_out || nrhs < 1) return HPSG_ERR_INVALID;
   if (!c->built) return fail(c, HPSG_ERR_STATE, "hpsg_solve: build() first");
+  if (c->T.cut) return fail(c, HPSG_ERR_STATE, "hpsg_solve: a cut part has no leaves (hpsg_part_solve_cut)");
   return guarded(c, [&] {
     c->launches = 0;
     const size_t nbr = size_t(c->lv[0].n_ext) * nrhs;
@@ -956,6 +992,7 @@ int hpsg_tree_leaf_points(const hpsg_tree* t, double* xyz) {
 int hpsg_get_leaf(hpsg_ctx* c, int ord, double* Y, double* v, double* Tm, double* h) {
   if (!c) return HPSG_ERR_INVALID;
   if (!c->built) return fail(c, HPSG_ERR_STATE, "hpsg_get_leaf: build() first");
+  if (c->T.cut) return fail(c, HPSG_ERR_STATE, "hpsg_get_leaf: a cut part has no leaves");
   if (ord < 0 || ord >= c->T.n_leaves()) return fail(c, HPSG_ERR_INVALID, "hpsg_get_leaf: bad ordinal");
   return guarded(c, [&] {
     const hpsg::LeafOperators& o = c->ops;
@@ -1005,7 +1042,7 @@ int hpsg_get_node(hpsg_ctx* c, int id, double* S, double* gtilde, double* Tm, do
     }
     if (!Lp) throw HpsError{HPSG_ERR_INVALID, "hpsg_get_node: not an internal node"};
     const Level& L = *Lp;
-    const bool implicit = L.d == 0 && c->opts.root_implicit_S;
+    const bool implicit = c->global_root(L.d) && c->opts.root_implicit_S;
     std::vector<double> xs(size_t(L.n_int) * (1 + L.n_ext));
     ck(cudaMemcpy(xs.data(), L.MD.d() + idx * L.strideMD() + (long long)L.n_int * L.n_int,
                   (implicit ? L.n_int : xs.size()) * 8, cudaMemcpyDeviceToHost),
@@ -1016,12 +1053,63 @@ int hpsg_get_node(hpsg_ctx* c, int id, double* S, double* gtilde, double* Tm, do
       if (implicit) throw HpsError{HPSG_ERR_STATE, "hpsg_get_node: root S is implicit (root_implicit_S)"};
       for (size_t i = 0; i < size_t(L.n_int) * L.n_ext; ++i) S[i] = -xs[L.n_int + i];
     }
-    if ((Tm || h) && L.d > 0) {
+    if ((Tm || h) && !c->global_root(L.d)) {
       std::vector<double> ht(size_t(L.n_ext) * (1 + L.n_ext));
       ck(cudaMemcpy(ht.data(), L.AH.d() + idx * L.strideAH(), ht.size() * 8, cudaMemcpyDeviceToHost), "node D2H");
       if (Tm) std::memcpy(Tm, ht.data() + L.n_ext, size_t(L.n_ext) * L.n_ext * 8);
       if (h) std::memcpy(h, ht.data(), size_t(L.n_ext) * 8);
     }
+  });
+}
+
+int hpsg_part_sizes(hpsg_ctx* c, long long* n_cut, int* cut_nb, int* root_nb) {
+  if (!c) return HPSG_ERR_INVALID;
+  if (n_cut) *n_cut = c->T.cut ? c->T.n_leaves() : 0;
+  if (cut_nb) *cut_nb = c->T.cut ? c->leaf_nb() : 0;
+  if (root_nb) *root_nb = c->lv[0].n_ext;
+  return HPSG_OK;
+}
+
+int hpsg_part_root_ht(hpsg_ctx* c, double* d_dst) {
+  if (!c || !d_dst) return HPSG_ERR_INVALID;
+  if (!c->built) return fail(c, HPSG_ERR_STATE, "hpsg_part_root_ht: build() first");
+  if (c->global_root(0)) return fail(c, HPSG_ERR_STATE, "hpsg_part_root_ht: the tree root has no [h|T]");
+  return guarded(c, [&] {
+    const Level& L = c->lv[0];
+    ck(cudaMemcpyAsync(d_dst, L.AH.p, size_t(L.strideAH()) * 8, cudaMemcpyDeviceToDevice, c->st), "root HT D2D");
+    ck(cudaStreamSynchronize(c->st), "root HT sync");
+  });
+}
+
+int hpsg_part_set_cut_ht(hpsg_ctx* c, long long k, const double* d_src) {
+  if (!c || !d_src) return HPSG_ERR_INVALID;
+  if (!c->T.cut) return fail(c, HPSG_ERR_STATE, "hpsg_part_set_cut_ht: not a cut part");
+  if (k < 0 || k >= c->T.n_leaves()) return fail(c, HPSG_ERR_INVALID, "hpsg_part_set_cut_ht: bad cut node index");
+  return guarded(c, [&] {
+    const long long st = c->strideLeafHT();
+    ck(cudaMemcpyAsync(c->leafHT.d() + k * st, d_src, size_t(st) * 8, cudaMemcpyDeviceToDevice, c->st),
+       "cut HT D2D");
+    ck(cudaStreamSynchronize(c->st), "cut HT sync");
+    c->cut_set[size_t(k)] = 1;
+    c->built = false;
+  });
+}
+
+int hpsg_part_solve_cut(hpsg_ctx* c, const double* d_g_root, int nrhs, double* d_g_cut) {
+  if (!c || !d_g_root || !d_g_cut || nrhs < 1) return HPSG_ERR_INVALID;
+  if (!c->built) return fail(c, HPSG_ERR_STATE, "hpsg_part_solve_cut: build() first");
+  if (!c->T.cut) return fail(c, HPSG_ERR_STATE, "hpsg_part_solve_cut: the part has real leaves (hpsg_solve)");
+  return guarded(c, [&] {
+    c->launches = 0;
+    ck(cudaEventRecord(c->ev[4], c->st), "ev");
+    run_solve(c, d_g_root, nrhs, nullptr, d_g_cut);
+    ck(cudaEventRecord(c->ev[5], c->st), "ev");
+    ck(cudaEventSynchronize(c->ev[5]), "solve sync");
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]), "elapsed");
+    c->stats.t_solve_ms = ms;
+    c->stats.solve_bytes = solve_bytes(c, nrhs);
+    c->stats.launches_solve = c->launches;
   });
 }
 

@@ -49,6 +49,10 @@ class _Tree(C.Structure):
     _fields_ = [("dim", C.c_int), ("p", C.c_int), ("L", C.c_int), ("lo", C.c_double), ("hi", C.c_double)]
 
 
+class _Part(C.Structure):
+    _fields_ = [("root_depth", C.c_int), ("root_index", C.c_longlong), ("cut_depth", C.c_int)]
+
+
 class _Options(C.Structure):
     _fields_ = [("literal_sign", C.c_int), ("root_implicit_S", C.c_int), ("device", C.c_int), ("reserved", C.c_int)]
 
@@ -79,6 +83,12 @@ def lib():
         vp, dp = C.c_void_p, C.POINTER(C.c_double)
         L.hpsg_create.argtypes = [C.POINTER(_Tree), C.POINTER(_Term), C.c_int, C.POINTER(_Field), C.POINTER(_Options),
                                   C.POINTER(vp)]
+        L.hpsg_create_part.argtypes = [C.POINTER(_Tree), C.POINTER(_Part), C.POINTER(_Term), C.c_int,
+                                       C.POINTER(_Field), C.POINTER(_Options), C.POINTER(vp)]
+        L.hpsg_part_sizes.argtypes = [vp, C.POINTER(C.c_longlong), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.hpsg_part_root_ht.argtypes = [vp, C.c_void_p]
+        L.hpsg_part_set_cut_ht.argtypes = [vp, C.c_longlong, C.c_void_p]
+        L.hpsg_part_solve_cut.argtypes = [vp, C.c_void_p, C.c_int, C.c_void_p]
         L.hpsg_build.argtypes = [vp]
         L.hpsg_solve.argtypes = [vp, dp, C.c_int, dp, dp]
         L.hpsg_solve_device.argtypes = [vp, C.c_void_p, C.c_int, C.c_void_p]
@@ -192,10 +202,15 @@ class HpsSolver:
 
     literal_sign=True reproduces the reference's v_i = -L_ii^-1 f_i
     (proj/src/local_solve.cpp:137); False uses the corrected +L_ii^-1 f_i.
+
+    part=(root_depth, root_index, cut_depth) restricts the solver to a subtree PART of the tree
+    (include/hps_cuda.h hpsg_create_part; the subtree-sharded build of SURVEY 8e): its leaves are
+    the real leaves below the part root (cut_depth == L) or the depth-cut_depth nodes whose [h|T]
+    are inputs (cut_depth < L).
     """
 
     def __init__(self, tree: UniformTree, terms, source: Field | None = None, literal_sign=True,
-                 root_implicit_S=False, device=0):
+                 root_implicit_S=False, device=0, part=None):
         L = lib()
         self.tree = tree
         keep = []
@@ -206,9 +221,11 @@ class HpsSolver:
         src = source.to_c(keep) if source is not None else None
         tr = _Tree(tree.dim, tree.p, tree.L, tree.lo, tree.hi)
         op = _Options(int(literal_sign), int(root_implicit_S), device, 0)
+        self.part = tuple(part) if part is not None else (0, 0, tree.L)
+        pt = _Part(*self.part)
         h = C.c_void_p()
-        rc = L.hpsg_create(C.byref(tr), arr, len(terms), C.byref(src) if src is not None else None, C.byref(op),
-                           C.byref(h))
+        rc = L.hpsg_create_part(C.byref(tr), C.byref(pt), arr, len(terms), C.byref(src) if src is not None else None,
+                                C.byref(op), C.byref(h))
         self._h = h
         if rc != HPSG_OK:
             msg = L.hpsg_last_error(h).decode() if h.value else "no CUDA device"
@@ -216,7 +233,11 @@ class HpsSolver:
             raise HpsError(rc, f"hpsg_create: {msg}")
         self.root_implicit_S = root_implicit_S
         self.npts = tree.p ** tree.dim
-        self.nb_root = tree.root_boundary_size
+        nc, cnb, rnb = C.c_longlong(), C.c_int(), C.c_int()
+        self._check(L.hpsg_part_sizes(h, C.byref(nc), C.byref(cnb), C.byref(rnb)), "part_sizes")
+        self.n_cut, self.cut_nb, self.nb_root = nc.value, cnb.value, rnb.value
+        nchild = 4 if tree.dim == 2 else 8
+        self.n_leaves = 0 if self.n_cut else nchild ** (self.part[2] - self.part[0])
 
     def _check(self, rc, what):
         if rc != HPSG_OK:
@@ -242,7 +263,7 @@ class HpsSolver:
         return out
 
     def leaf_points(self):
-        out = np.zeros((self.tree.n_leaves, self.npts, 3))
+        out = np.zeros((self.n_leaves, self.npts, 3))
         self._check(lib().hpsg_leaf_points(self._h, _dp(out)), "leaf_points")
         return out
 
@@ -253,8 +274,8 @@ class HpsSolver:
         g2 = g.reshape(1, -1) if single else g
         nrhs = g2.shape[0]
         assert g2.shape[1] == self.nb_root
-        u = np.empty((nrhs, self.tree.n_leaves, self.npts))
-        lg = np.empty((nrhs, self.tree.n_leaves, self.tree.leaf_boundary_size)) if want_leaf_g else None
+        u = np.empty((nrhs, self.n_leaves, self.npts))
+        lg = np.empty((nrhs, self.n_leaves, self.tree.leaf_boundary_size)) if want_leaf_g else None
         self._check(lib().hpsg_solve(self._h, _dp(g2), nrhs, _dp(u), _dp(lg)), "solve")
         if single:
             u = u[0]
@@ -264,6 +285,20 @@ class HpsSolver:
     def solve_device(self, d_g_ptr, nrhs, d_u_ptr):
         """Zero-copy solve on device pointers (e.g. torch.Tensor.data_ptr())."""
         self._check(lib().hpsg_solve_device(self._h, C.c_void_p(d_g_ptr), nrhs, C.c_void_p(d_u_ptr)), "solve")
+
+    # ---- subtree parts (include/hps_cuda.h hpsg_part_*)
+    def root_ht_device(self, d_dst_ptr):
+        """[h|T] of the part root (nb_root x (1+nb_root), column-major) -> device buffer."""
+        self._check(lib().hpsg_part_root_ht(self._h, C.c_void_p(d_dst_ptr)), "part_root_ht")
+
+    def set_cut_ht_device(self, k, d_src_ptr):
+        """Input [h|T] (cut_nb x (1+cut_nb)) of cut node k from a device buffer."""
+        self._check(lib().hpsg_part_set_cut_ht(self._h, k, C.c_void_p(d_src_ptr)), "part_set_cut_ht")
+
+    def solve_cut_device(self, d_g_ptr, nrhs, d_out_ptr):
+        """Downward pass of a cut part: root data (nrhs x nb_root) -> cut-node data (nrhs x n_cut x cut_nb)."""
+        self._check(lib().hpsg_part_solve_cut(self._h, C.c_void_p(d_g_ptr), nrhs, C.c_void_p(d_out_ptr)),
+                    "part_solve_cut")
 
     def get_leaf(self, ord_):
         n, nb = self.npts, self.tree.leaf_boundary_size
