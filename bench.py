@@ -16,8 +16,13 @@ data H2D, the whole solution field D2H inside the timed region).
 
 --impl reference times the reference algorithm on the host cores: the C++
 restatement in oracle/ (the reference itself needs Eigen, absent here), with
-all host threads.  Under torchrun (N>1) every rank runs an independent replica
-(weak scaling; the subtree-sharded multi-GPU build is not in this round).
+all host threads.
+
+Under torchrun (N>1) the default is the north star's subtree-sharded run (strong scaling:
+ONE L=8 problem over N GPUs, paper_2503_17535_b200/sharded.py): each rank builds its
+subtrees, ships subtree-root [h|T] over NCCL to the owners of the few top merges, and the
+boundary data comes back down; `value` = N_DOF / (max over ranks of the step time).
+--mode replicas runs N independent full problems instead (weak scaling).
 """
 from __future__ import annotations
 
@@ -101,9 +106,15 @@ def run_b200(args):
     import torch.distributed as dist
 
     world, rank, local = dist_setup()
+    local %= max(1, torch.cuda.device_count())   # gloo functional runs: several ranks per GPU
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "gloo":   # one-GPU functional check of the sharded path (host-staged P2P)
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.mode == "sharded":
+            return run_sharded(args, world, rank, local)
     import paper_2503_17535_b200 as H
     from paper_2503_17535_b200 import problems as PR
 
@@ -210,6 +221,113 @@ def run_b200(args):
         print(json.dumps(out), flush=True)
 
 
+def run_sharded(args, world, rank, local):
+    """Subtree-sharded strong-scaling step on N GPUs of one node."""
+    import torch
+    import torch.distributed as dist
+    import paper_2503_17535_b200 as H
+    from paper_2503_17535_b200 import problems as PR
+    from paper_2503_17535_b200 import sharded as SH
+
+    dist.barrier()   # communicators up on every rank before the first (partial) point-to-point batch
+    prob = PR.helmholtz_bumps(k=args.k, seed=args.seed)
+    tree = H.build_uniform_tree(prob.lo, prob.hi, args.L, 2, args.p)
+    N = tree.total_points
+    plan = SH.make_plan(args.L, 2, world)
+    parts = SH.CudaParts(tree, prob.terms, prob.source, literal_sign=False,
+                         root_implicit_S=not args.explicit_root, device=local)
+    shard = SH.ShardedHps(plan, rank, parts)
+    stream = torch.cuda.current_stream()
+    g_host = prob.boundary(H.tree_root_points(tree)) if rank == 0 else None
+    g_dev = torch.tensor(g_host, device="cuda").reshape(1, -1) if rank == 0 else None
+    g_pin = torch.tensor(g_host).reshape(1, -1).pin_memory() if rank == 0 else None
+    all_parts = list(shard.sub.values()) + list(shard.top.values())
+    on_dev = dist.get_backend() == "nccl"
+
+    def reduce(vals, op):
+        t = torch.tensor(vals, dtype=torch.float64, device="cuda" if on_dev else "cpu")
+        dist.all_reduce(t, op=op)
+        return t.tolist()
+
+    def step_device():
+        return SH.run_dist(shard, g_dev, nrhs=1)
+
+    def step_e2e():
+        g = g_pin.to("cuda", non_blocking=True) if rank == 0 else None
+        u = SH.run_dist(shard, g, nrhs=1)
+        return {k: v.to("cpu") for k, v in u.items()}
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+
+    def timed(fn, K):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(K):
+            out = fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return reduce([e0.elapsed_time(e1) / K], dist.ReduceOp.MAX)[0], out
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms, u = timed(step_device, args.steps)
+    clk = clocks.stop()
+    ms_e2e = ms
+    if not args.profile:
+        ms_e2e, _ = timed(step_e2e, max(1, args.steps // 2))
+    # job-wide counters: counted FLOPs, launches, leaf/merge times of this rank's parts
+    loc = reduce([sum(p.stats()["build_flops"] for p in all_parts),
+                  sum(p.stats()["launches_build"] + p.stats()["launches_solve"] for p in all_parts),
+                  sum(p.stats()["t_build_ms"] for p in all_parts)], dist.ReduceOp.SUM)
+    # accuracy on this rank's leaves against the manufactured solution
+    err = 0.0
+    for k, part in shard.sub.items():
+        ex = prob.exact(part.s.leaf_points())
+        err = max(err, float(np.abs(u[k][0].cpu().numpy() - ex).max() / np.abs(ex).max()))
+    err = reduce([err], dist.ReduceOp.MAX)[0]
+    flops, launches = loc[0], int(loc[1])
+    value = N / (ms / 1e3)
+    up = 0
+    for d in range(plan.ds):
+        for i in range(plan.nchild ** d):
+            for c in range(plan.nchild):
+                if plan.owner(d + 1, plan.nchild * i + c) != plan.owner(d, i):
+                    nb = 4 * tree.q * 2 ** (args.L - 1 - d)   # boundary points of a depth-(d+1) node
+                    up += 8 * (1 + nb) * nb
+    out = {
+        "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": value / PAPER_H100_DOFS,
+        "vs_baseline_ref": "job DOF/s / 4.17e6 DOF/s (PAPER.md:629, 1x H100 JAX subtree recompute, p=16 L=8, 4.02 s)",
+        "dtype": "f64", "data": "synthetic (seeded bump potential, manufactured plane wave; coefficients evaluated on device)",
+        "config": {"workload": f"2D variable-coefficient Helmholtz DtN HPS, p={args.p}, L={args.L} uniform quadtree, "
+                               f"N={N} DOF (BASELINE configs[1])", "k": args.k, "seed": args.seed,
+                   "root": "explicit S" if args.explicit_root else "implicit S (MergeOptions::implicit_S)",
+                   "sign": "corrected (v=+L^-1 f); literal differs only in the sign of f",
+                   "l2": "inputs larger than L2 (each step streams > 40 GB of leaf/merge operands)",
+                   "parallelism": f"subtree-sharded over {world} GPUs: cut depth {plan.ds}, "
+                                  f"{plan.n_sub} subtrees, NCCL P2P of {up / 1e6:.0f} MB [h|T] up per build"},
+        "roofline": {"bound": "tensor", "kernel": "build (batched DMMA LU/TRSM/GEMM pipeline), whole job",
+                     "achieved": flops / (ms / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS * world, "unit": "TFLOP/s",
+                     "frac": flops / (ms / 1e3) / 1e12 / (FP64_PEAK_TFLOPS * world), "traffic": None,
+                     "algorithmic_flops": flops, "note": "counted build FLOPs over the whole build+solve step time"},
+        "e2e": {"value": N / (ms_e2e / 1e3), "unit": "DOF/s", "ms_per_step": ms_e2e,
+                "h2d_bytes_per_step": int(8 * tree.root_boundary_size),
+                "d2h_bytes_per_step": int(8 * N)},
+        "gpu_launches": launches * args.steps,
+        "accuracy": {"rel_linf_vs_exact": err},
+        "clocks": clk,
+    }
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
 def cpu_baseline(args, prob, u_gpu=None):
     """Oracle (C++ restatement of the reference) on the host cores: full workload, one run."""
     from oracle import oracle as O
@@ -263,6 +381,10 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo: host-staged transport, for functional runs of N ranks on one GPU")
+    ap.add_argument("--mode", choices=["sharded", "replicas"], default="sharded",
+                    help="N>1: subtree-sharded strong scaling (default) or independent replicas")
     ap.add_argument("--L", type=int, default=8)
     ap.add_argument("--p", type=int, default=16)
     ap.add_argument("--k", type=float, default=30.0)

@@ -104,6 +104,8 @@ def lib():
         L.hpsg_destroy.argtypes = [vp]
         L.hpsg_build_info.restype = C.c_char_p
         L.hpsg_bump_centers.argtypes = [C.c_ulonglong, C.c_int, C.c_int, dp]
+        L.hpsg_tree_root_points.argtypes = [C.POINTER(_Tree), dp]
+        L.hpsg_tree_leaf_points.argtypes = [C.POINTER(_Tree), dp]
         _lib = L
     return _lib
 
@@ -187,6 +189,16 @@ class UniformTree:
 
 def build_uniform_tree(lo, hi, L, dim, p):
     return UniformTree(dim=dim, p=p, L=L, lo=lo, hi=hi)
+
+
+def tree_root_points(tree: UniformTree):
+    """Root boundary points of a tree without a solver (hpsg_tree_root_points; solver.cpp:159-182)."""
+    out = np.zeros((tree.root_boundary_size, 3))
+    tr = _Tree(tree.dim, tree.p, tree.L, tree.lo, tree.hi)
+    rc = lib().hpsg_tree_root_points(C.byref(tr), _dp(out))
+    if rc != HPSG_OK:
+        raise HpsError(rc, "hpsg_tree_root_points: invalid tree")
+    return out
 
 
 def bump_centers(seed, n=10, dim=2):

@@ -78,7 +78,10 @@ class CudaParts:
         self.dev = torch.device("cuda", device)
 
     def make(self, root_depth, root_index, cut_depth):
-        return _CudaPart(self, root_depth, root_index, cut_depth)
+        part = _CudaPart(self, root_depth, root_index, cut_depth)
+        # one stream per rank: parts, torch collectives and CUDA-event timing share torch's stream
+        part.s.set_stream(torch.cuda.current_stream(self.dev).cuda_stream)
+        return part
 
 
 class _CudaPart:
@@ -231,15 +234,28 @@ def run_dist(shard: ShardedHps, g_root=None, nrhs=1, build=True, solve=True):
     import torch.distributed as dist
     p = shard.plan
 
+    # gloo has no device-memory point-to-point: stage through the host (CPU tests, one-GPU runs)
+    stage = dist.get_backend() == "gloo"
+
     def exchange(sends, recvs):
-        ops = []
+        ops, staged = [], []
         for peer, key, t in sorted(sends, key=lambda x: (x[0], x[1])):
-            ops.append(dist.P2POp(dist.isend, t.contiguous(), peer))
+            t = t.contiguous()
+            ops.append(dist.P2POp(dist.isend, t.cpu() if stage and t.is_cuda else t, peer))
         for peer, key, t in sorted(recvs, key=lambda x: (x[0], x[1])):
+            if stage and t.is_cuda:
+                h = torch.empty(t.shape, dtype=t.dtype)
+                staged.append((h, t))
+                t = h
             ops.append(dist.P2POp(dist.irecv, t, peer))
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
+            for h, t in staged:
+                t.copy_(h)
+            if any(t.is_cuda for _, _, t in recvs):
+                # the C-ABI parts read received buffers through plain device pointers
+                torch.cuda.current_stream().synchronize()
 
     if build:
         shard.build_local()
