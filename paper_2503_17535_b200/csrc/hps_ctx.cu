@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -92,6 +93,9 @@ struct Level {
   DevBuf MD, piv, stats;  // [D | h_int | C] -> [LU | x_h | X]
   DevBuf AH;              // [h | T] of the level's nodes (input of level d-1); unused at the root
   DevBuf md_src, b_src, ah_src, down;
+  // block-sparse Schur product: exterior section e only couples to the interfaces of its own
+  // child (B_{e,i} = 0 otherwise), as contiguous interface runs {e, first interface, count}
+  std::vector<std::array<int, 3>> schur_runs;
   long long strideMD() const { return (long long)n_int * (n_int + 1 + n_ext); }
   long long strideAH() const { return (long long)n_ext * (1 + n_ext); }
 };
@@ -173,6 +177,9 @@ void gemm(hpsg_ctx* c, const GemmArgs& g) {
 }
 
 int lu_launches(int n, int m, bool factor) { return hpsk::lu_launch_count(n, m, factor); }
+
+// block-sparse Schur products from this face size up (below it one dense GEMM launch is cheaper)
+constexpr int kSparseSchurMinS = 32;
 
 // Solve-time products: a streaming GEMV for up to 4 right-hand sides (HBM-bound), the DMMA
 // GEMM beyond that (multi-RHS solves become compute-bound, config 3).
@@ -289,6 +296,21 @@ void setup(hpsg_ctx* c) {
     if (L.n_int > hpsk::bgetrf_max_n())
       throw HpsError{HPSG_ERR_INVALID, hpsg::fmt("interface matrix of size %d exceeds the batched LU limit %d",
                                                  L.n_int, hpsk::bgetrf_max_n())};
+    for (int ch = 0; ch < L.mt.nchild; ++ch) {
+      std::vector<int> ext, itf;
+      for (int f = 0; f < L.mt.nface; ++f) {
+        const int v = L.mt.sec[ch * L.mt.nface + f];
+        (v >= 0 ? ext : itf).push_back(v >= 0 ? v : -v - 1);
+      }
+      std::sort(itf.begin(), itf.end());
+      for (int e : ext)
+        for (size_t a = 0; a < itf.size();) {
+          size_t b = a + 1;
+          while (b < itf.size() && itf[b] == itf[b - 1] + 1) ++b;
+          L.schur_runs.push_back({e, itf[a], int(b - a)});
+          a = b;
+        }
+    }
     upload(L.md_src, L.mt.md_src, &c->dev_bytes, st);
     upload(L.b_src, L.mt.b_src, &c->dev_bytes, st);
     upload(L.ah_src, L.mt.ah_src, &c->dev_bytes, st);
@@ -567,7 +589,34 @@ void run_merge_level(hpsg_ctx* c, int d) {
   BatchedMat M{L.MD.d(), L.n_int, L.strideMD()};
   ck(hpsk::bgetrf_aug(int(L.nodes), L.n_int, m, M, L.piv.i(), L.stats.d(), c->st), "merge bgetrf");
   c->launches += lu_launches(L.n_int, m, true);
-  if (!root) {
+  if (!root && L.mt.s >= kSparseSchurMinS && !getenv("HPS_DENSE_SCHUR")) {
+    // [h | T] = [h_ext | A] - B [x_h | X] over the nonzero blocks of B only: section e's rows get
+    // -B_{e,I} [x_h|X]_I for the runs I of interfaces of e's child (the other blocks of B are
+    // structurally zero, merge.cpp:226-278), i.e. half the dense product in 2D, a quarter in 3D
+    const int sz = L.mt.s;
+    for (const auto& r : L.schur_runs) {
+      GemmArgs g;
+      g.m = sz;
+      g.n = 1 + L.n_ext;
+      g.k = r[2] * sz;
+      g.batch = int(L.nodes);
+      g.A = c->Bscratch.d() + (long long)r[1] * sz * L.n_ext + (long long)r[0] * sz;
+      g.lda = L.n_ext;
+      g.sA = (long long)L.n_ext * L.n_int;
+      g.B = L.MD.d() + (long long)L.n_int * L.n_int + (long long)r[1] * sz;
+      g.ldb = L.n_int;
+      g.sB = L.strideMD();
+      g.C = L.AH.d() + (long long)r[0] * sz;
+      g.ldc = L.n_ext;
+      g.sC = L.strideAH();
+      g.D = L.AH.d() + (long long)r[0] * sz;
+      g.ldd = L.n_ext;
+      g.sD = L.strideAH();
+      g.alpha = -1.0;
+      g.beta = 1.0;
+      gemm(c, g);
+    }
+  } else if (!root) {
     // [h | T] = [h_ext | A] - B [x_h | X]   (merge.cpp:294-295 with gtilde = -x_h)
     GemmArgs g;
     g.m = L.n_ext;

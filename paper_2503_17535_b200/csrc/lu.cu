@@ -536,7 +536,12 @@ LookAhead& lookahead() {
 }
 cudaError_t lookahead_prepare(int batch, int nev) {
   LookAhead& la = lookahead();
-  if (!la.ps) HPS_TRY(cudaStreamCreateWithFlags(&la.ps, cudaStreamNonBlocking));
+  if (!la.ps) {
+    // the panel stream outranks the trailing GEMMs so its few CTAs are scheduled as SMs free up
+    int lo = 0, hi = 0;
+    HPS_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    HPS_TRY(cudaStreamCreateWithPriority(&la.ps, cudaStreamNonBlocking, hi));
+  }
   while ((int)la.ev.size() < nev) {
     cudaEvent_t e;
     HPS_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
