@@ -38,6 +38,7 @@ constexpr int kBLD = kNB + 4;     // B-operand (k-major) leading dim, (36 % 16) 
 constexpr int kTileCols = 128;    // B-operand columns staged at a time
 constexpr int kMaxNz = kMaxNI * 4;
 constexpr int kRowsPerLane = (kMaxNI + 31) / 32;
+constexpr int kSub = 8;           // sub-panel width factored by one warp inside a panel
 
 struct FusedSmem {
   LeafAsmSmemT<256, 16> asmb;
@@ -102,9 +103,9 @@ __device__ void update_smem(int m, int n, int k, const double* A, int lda, const
 // slots past the last row are clamped onto it, so loads/stores need no predicates (the clamped
 // lanes recompute and store exactly the owner's value).
 template <int NQ>
-__device__ __forceinline__ void gepp_warp_body(FusedSmem& s, int rows, int pnb, int j0) {
+__device__ __forceinline__ void gepp_warp_body(FusedSmem& s, int rows, int sb, int se, int pnb, int j0) {
   const int lane = threadIdx.x & 31;
-  for (int j = 0; j < pnb; ++j) {
+  for (int j = sb; j < se; ++j) {
     double* pj = s.pan + j * kPLD;
     double bv = -1.0;
     int bp = INT_MAX;
@@ -118,11 +119,15 @@ __device__ __forceinline__ void gepp_warp_body(FusedSmem& s, int rows, int pnb, 
         if (j + lane + 32 * q < rows && av > bv) bv = av, bp = j + lane + 32 * q;
       }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int p2 = __shfl_xor_sync(0xffffffffu, bp, o);
-      if (v2 > bv || (v2 == bv && p2 < bp)) bv = v2, bp = p2;
+    {
+      // warp argmax on the IEEE bits (non-negative doubles order as unsigned integers):
+      // max of the high words, max of the low words among those, then the lowest row
+      const unsigned long long key = bv >= 0.0 ? (unsigned long long)__double_as_longlong(bv) : 0ull;
+      const unsigned hi = unsigned(key >> 32), lo = unsigned(key);
+      const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+      const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+      bp = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? bp : INT_MAX);
+      bv = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
     }
     if (bp != j) {
       if (lane < pnb) {
@@ -159,7 +164,7 @@ __device__ __forceinline__ void gepp_warp_body(FusedSmem& s, int rows, int pnb, 
       for (int q = 0; q < NQ; ++q) pj[off[q]] = l[q];
       // rank-1 update, four columns at a time (4*NQ loads in flight per lane)
       int c = j + 1;
-      for (; c + 4 <= pnb; c += 4) {
+      for (; c + 4 <= se; c += 4) {
         const double* pc = s.pan + c * kPLD;
         double u[4], a[4][NQ];
 #pragma unroll
@@ -174,7 +179,7 @@ __device__ __forceinline__ void gepp_warp_body(FusedSmem& s, int rows, int pnb, 
 #pragma unroll
           for (int q = 0; q < NQ; ++q) s.pan[(c + k) * kPLD + off[q]] = a[k][q] - l[q] * u[k];
       }
-      for (; c < pnb; ++c) {
+      for (; c < se; ++c) {
         double* pc = s.pan + c * kPLD;
         const double u = pc[j];
         double a[NQ];
@@ -202,16 +207,67 @@ __device__ void panel_gepp_warp(FusedSmem& s, double* W, int ni, int j0, int pnb
   }
   for (int r = tid; r < rows; r += kFT) s.prow[r] = r;
   __syncthreads();
-  if (tid < 32) {
-    switch ((rows + 31) / 32) {
-      case 1: gepp_warp_body<1>(s, rows, pnb, j0); break;
-      case 2: gepp_warp_body<2>(s, rows, pnb, j0); break;
-      case 3: gepp_warp_body<3>(s, rows, pnb, j0); break;
-      case 4: gepp_warp_body<4>(s, rows, pnb, j0); break;
-      case 5: gepp_warp_body<5>(s, rows, pnb, j0); break;
-      case 6: gepp_warp_body<6>(s, rows, pnb, j0); break;
-      default: gepp_warp_body<kRowsPerLane>(s, rows, pnb, j0); break;
+  // kSub-column sub-panels: warp 0 factors one (swaps span the whole panel), then all warps apply
+  // its L11^-1 to the sub-panel's rows of the later panel columns and the k <= kSub DMMA update
+  const int nq = (rows + 31) / 32;
+  for (int sb = 0; sb < pnb; sb += kSub) {
+    const int se = min(sb + kSub, pnb);
+    if (tid < 32) {
+      switch (nq) {
+        case 1: gepp_warp_body<1>(s, rows, sb, se, pnb, j0); break;
+        case 2: gepp_warp_body<2>(s, rows, sb, se, pnb, j0); break;
+        case 3: gepp_warp_body<3>(s, rows, sb, se, pnb, j0); break;
+        case 4: gepp_warp_body<4>(s, rows, sb, se, pnb, j0); break;
+        case 5: gepp_warp_body<5>(s, rows, sb, se, pnb, j0); break;
+        case 6: gepp_warp_body<6>(s, rows, sb, se, pnb, j0); break;
+        default: gepp_warp_body<kRowsPerLane>(s, rows, sb, se, pnb, j0); break;
+      }
     }
+    __syncthreads();
+    if (se >= pnb) break;
+    // U12 rows [sb, se) of columns [se, pnb): unit-lower forward substitution
+    for (int c = se + tid; c < pnb; c += kFT) {
+      double* pc = s.pan + c * kPLD;
+      double x[kSub];
+#pragma unroll
+      for (int i = 0; i < kSub; ++i) x[i] = sb + i < se ? pc[sb + i] : 0.0;
+#pragma unroll
+      for (int k = 0; k < kSub - 1; ++k)
+#pragma unroll
+        for (int i = k + 1; i < kSub; ++i) x[i] -= s.pan[(sb + k) * kPLD + sb + i] * x[k];
+#pragma unroll
+      for (int i = 0; i < kSub; ++i)
+        if (sb + i < se) pc[sb + i] = x[i];
+    }
+    __syncthreads();
+    // rows [se, rows) x columns [se, pnb) -= L21 (k = se - sb) * U12: 8x8 DMMA tiles over all warps
+    {
+      const int lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+      const int tr = (rows - se + 7) / 8, tc = (pnb - se + 7) / 8;
+      for (int t = tid >> 5; t < tr * tc; t += kFW) {
+        const int r0 = se + (t % tr) * 8, c0 = se + (t / tr) * 8;
+        const int r = r0 + g;
+        double acc[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cc = c0 + 2 * t4 + h;
+          acc[h] = (r < rows && cc < pnb) ? s.pan[cc * kPLD + r] : 0.0;
+        }
+#pragma unroll
+        for (int kb = 0; kb < kSub; kb += 4) {
+          const int k = sb + kb + t4;
+          const double av = (k < se && r < rows) ? -s.pan[k * kPLD + r] : 0.0;
+          const double bv = (k < se && c0 + g < pnb) ? s.pan[(c0 + g) * kPLD + k] : 0.0;
+          dmma_8x8x4(acc[0], acc[1], av, bv);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cc = c0 + 2 * t4 + h;
+          if (r < rows && cc < pnb) s.pan[cc * kPLD + r] = acc[h];
+        }
+      }
+    }
+    __syncthreads();
   }
   if (tid == 0) s.n_moved = 0;
   __syncthreads();
