@@ -340,6 +340,8 @@ void alloc_build(hpsg_ctx* c) {
     int nsm = 0;
     ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->opts.device), "sm count");
     c->fused_grid = int(std::min<long long>(nl, (long long)nsm * hpsk::leaf_fused_ctas_per_sm()));
+    if (const char* gs = getenv("HPS_LEAF_GRID"))  // developer knob: persistent grid size (L2 footprint sweep)
+      c->fused_grid = std::max(1, std::min(c->fused_grid, atoi(gs)));
     const long long per = hpsk::leaf_fused_scratch_per_cta(o.ni, o.ne, o.nb);
     c->leafScratch.alloc(size_t(c->fused_grid) * per * 8, tot);
     c->leafYv.alloc(size_t(nl) * o.ni * (1 + o.nb) * 8, tot);

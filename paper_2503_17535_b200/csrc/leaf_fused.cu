@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs 
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int c = n0 + t4 * 2 + h;
-            if (r < nb && c < nr) HT[(long long)c * nb + r] = acc[u][h] + f.ZQeP[(long long)c * nb + r];
+            if (r < nb && c < nr) __stcs(&HT[(long long)c * nb + r], acc[u][h] + f.ZQeP[(long long)c * nb + r]);
           }
         }
       }
@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs 
     stamp(5);
     // ---- outputs: [v | Y_i] for the solve, pivot statistics
     double* Yv = f.Yv + leaf * f.strideYv;
-    for (int e = tid; e < ni * nr; e += kFT) Yv[e] = R[e];
+    for (int e = tid; e < ni * nr; e += kFT) __stcs(&Yv[e], R[e]);  // streamed: keep W resident in L2
     if (tid == 0 && f.stats) {
       f.stats[3 * leaf + 0] = s.pmin;
       f.stats[3 * leaf + 1] = s.pmax;
