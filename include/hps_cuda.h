@@ -48,7 +48,9 @@ enum {
   HPSG_FIELD_PLANE_COS = 3,      /* c0 * cos(c1 x1 + c2 x2 + c3 x3 + c4) */
   HPSG_FIELD_BUMPS_SIN = 4,      /* c0 * sum_j exp(-c2 |x-z_j|^2) * sin(c3 x1 + c4 x2 + c5 x3 + c6) */
   HPSG_FIELD_POISSON2D_SRC = 5,  /* source of make_manufactured_2d_dtn, proj/src/problems.cpp:62-66 */
-  HPSG_FIELD_SAMPLED = 6
+  HPSG_FIELD_SAMPLED = 6,
+  HPSG_FIELD_BUMPS_GRAD = 7,     /* d/dx_a of HPSG_FIELD_BUMPS: c1 * sum_j -2 c2 (x_a - z_ja) exp(-c2 |x - z_j|^2), a = c3 */
+  HPSG_FIELD_DIVGRAD_SRC = 8     /* div(eps grad u), eps = BUMPS(c0,c1,c2), u = prod_k sin(c3 x_k + c4) (3D config 4) */
 };
 typedef struct {
   int kind;

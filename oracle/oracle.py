@@ -19,7 +19,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
 
-FIELD_CONST, FIELD_BUMPS, FIELD_PLANE_SIN, FIELD_PLANE_COS, FIELD_BUMPS_SIN, FIELD_POISSON2D_SRC, FIELD_SAMPLED = range(7)
+FIELD_CONST, FIELD_BUMPS, FIELD_PLANE_SIN, FIELD_PLANE_COS, FIELD_BUMPS_SIN, FIELD_POISSON2D_SRC, FIELD_SAMPLED, \
+    FIELD_BUMPS_GRAD, FIELD_DIVGRAD_SRC = range(9)
 ROLE_LAPLACIAN, ROLE_GRADIENT, ROLE_ZEROTH, ROLE_SECOND_ORDER = range(4)
 
 

@@ -60,6 +60,42 @@ struct FieldEval {
         return lap - std::cos(5.0 * Y) * ux + std::sin(5.0 * Y) * uy;
       }
       case ORACLE_FIELD_SAMPLED: return samples[size_t(leaf) * npts + pt];
+      case ORACLE_FIELD_BUMPS_GRAD: {
+        const int a = int(c[3]);
+        double s = 0.0;
+        for (int j = 0; j < f.n_centers; ++j) {
+          double r2 = 0.0;
+          for (int k = 0; k < dim; ++k) {
+            const double d = x[k] - centers[3 * j + k];
+            r2 += d * d;
+          }
+          s += -2.0 * c[2] * (x[a] - centers[3 * j + a]) * std::exp(-c[2] * r2);
+        }
+        return c[1] * s;
+      }
+      case ORACLE_FIELD_DIVGRAD_SRC: {
+        double sn[3], cs[3], u = 1.0;
+        for (int k = 0; k < dim; ++k) sn[k] = std::sin(c[3] * x[k] + c[4]), cs[k] = std::cos(c[3] * x[k] + c[4]), u *= sn[k];
+        double eps = c[0], geps[3] = {0.0, 0.0, 0.0};
+        for (int j = 0; j < f.n_centers; ++j) {
+          double r2 = 0.0;
+          for (int k = 0; k < dim; ++k) {
+            const double d = x[k] - centers[3 * j + k];
+            r2 += d * d;
+          }
+          const double e = std::exp(-c[2] * r2);
+          eps += c[1] * e;
+          for (int k = 0; k < dim; ++k) geps[k] += c[1] * -2.0 * c[2] * (x[k] - centers[3 * j + k]) * e;
+        }
+        double f2 = -dim * c[3] * c[3] * u * eps;
+        for (int k = 0; k < dim; ++k) {
+          double du = c[3] * cs[k];
+          for (int l = 0; l < dim; ++l)
+            if (l != k) du *= sn[l];
+          f2 += geps[k] * du;
+        }
+        return f2;
+      }
       default: fail("oracle: unknown field kind " + std::to_string(f.kind));
     }
   }

@@ -23,7 +23,9 @@ enum {
   ORACLE_FIELD_PLANE_COS = 3,       /* c0 * cos(c1 x1 + c2 x2 + c3 x3 + c4) */
   ORACLE_FIELD_BUMPS_SIN = 4,       /* c0 * sum_j exp(-c2 |x-z_j|^2) * sin(c3 x1 + c4 x2 + c5 x3 + c6) */
   ORACLE_FIELD_POISSON2D_SRC = 5,   /* manufactured source of proj/src/problems.cpp:62-66 */
-  ORACLE_FIELD_SAMPLED = 6          /* samples[leaf * p^d + pt], leaf order */
+  ORACLE_FIELD_SAMPLED = 6,         /* samples[leaf * p^d + pt], leaf order */
+  ORACLE_FIELD_BUMPS_GRAD = 7,      /* d/dx_a of BUMPS (a = c3) */
+  ORACLE_FIELD_DIVGRAD_SRC = 8      /* div(eps grad u), eps = BUMPS, u = prod sin(c3 x_k + c4) */
 };
 
 typedef struct {

@@ -1,4 +1,5 @@
 // gemm.cu -- tile-shape dispatch for the strided-batched DMMA DGEMM (gemm.cuh).
+#include <algorithm>
 #include <cstdlib>
 
 #include "gemm.cuh"
@@ -16,9 +17,11 @@ cudaError_t run(const GemmArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  // tile index = blockIdx.z * gridDim.y + blockIdx.y (gridDim.y/z <= 65535; batch in x)
   const long long tiles = (long long)((a.m + BM - 1) / BM) * ((a.n + BN - 1) / BN);
-  if (tiles > 65535) return cudaErrorInvalidConfiguration;
-  dim3 grid(a.batch, (unsigned)tiles);
+  const unsigned ty = (unsigned)std::min<long long>(tiles, 65535), tz = (unsigned)((tiles + ty - 1) / ty);
+  if (tz > 65535) return cudaErrorInvalidConfiguration;
+  dim3 grid(a.batch, ty, tz);
   kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, st>>>(a);
   return cudaGetLastError();
 }

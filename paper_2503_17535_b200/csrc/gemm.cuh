@@ -93,7 +93,9 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, STAGES, VEC>::kThr
   double* sB = smem + STAGES * Cfg::kStageA;
 
   const int tiles_m = (p.m + BM - 1) / BM;
-  const int tm = blockIdx.y % tiles_m, tn = blockIdx.y / tiles_m;
+  const long long tile = (long long)blockIdx.z * gridDim.y + blockIdx.y;
+  if (tile >= (long long)tiles_m * ((p.n + BN - 1) / BN)) return;
+  const int tm = int(tile % tiles_m), tn = int(tile / tiles_m);
   const int m0 = tm * BM, n0 = tn * BN;
   const long long b = blockIdx.x;  // batch in x (gridDim.y/z are capped at 65535)
   const double* A = p.A + b * p.sA;

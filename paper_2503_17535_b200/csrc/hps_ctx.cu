@@ -209,11 +209,15 @@ hpsk::DevField make_dev_field(hpsg_ctx* c, const hpsg_field& f, bool is_source) 
   d.kind = f.kind;
   d.n_centers = f.n_centers;
   for (int i = 0; i < 8; ++i) d.c[i] = f.c[i];
-  if (f.kind < HPSG_FIELD_CONST || f.kind > HPSG_FIELD_SAMPLED)
+  if (f.kind < HPSG_FIELD_CONST || f.kind > HPSG_FIELD_DIVGRAD_SRC)
     throw HpsError{HPSG_ERR_INVALID, hpsg::fmt("unknown field kind %d", f.kind)};
   if (f.kind == HPSG_FIELD_POISSON2D_SRC && c->tree.dim != 2)
     throw HpsError{HPSG_ERR_INVALID, "HPSG_FIELD_POISSON2D_SRC is a 2D field"};
-  if ((f.kind == HPSG_FIELD_BUMPS || f.kind == HPSG_FIELD_BUMPS_SIN) && f.n_centers > 0) {
+  if (f.kind == HPSG_FIELD_BUMPS_GRAD && (f.c[3] < 0 || f.c[3] >= c->tree.dim || f.c[3] != double(int(f.c[3]))))
+    throw HpsError{HPSG_ERR_INVALID, "HPSG_FIELD_BUMPS_GRAD: c[3] must be an axis index"};
+  if ((f.kind == HPSG_FIELD_BUMPS || f.kind == HPSG_FIELD_BUMPS_SIN || f.kind == HPSG_FIELD_BUMPS_GRAD ||
+       f.kind == HPSG_FIELD_DIVGRAD_SRC) &&
+      f.n_centers > 0) {
     if (!f.centers) throw HpsError{HPSG_ERR_INVALID, "bump field without centers"};
     auto b = std::make_unique<DevBuf>();
     upload(*b, std::vector<double>(f.centers, f.centers + 3 * f.n_centers), &c->dev_bytes, c->st);

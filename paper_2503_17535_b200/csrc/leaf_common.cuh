@@ -47,6 +47,42 @@ __device__ __forceinline__ double eval_field(const DevField& f, const double* x,
       return lap - cos(5.0 * Y) * ux + sin(5.0 * Y) * uy;
     }
     case 6: return f.samples[leaf * npts + pt];
+    case 7: {  // d/dx_a of the bump field
+      const int ax = int(c[3]);
+      double s = 0.0;
+      for (int j = 0; j < f.n_centers; ++j) {
+        double r2 = 0.0;
+        for (int k = 0; k < dim; ++k) {
+          const double d = x[k] - f.centers[3 * j + k];
+          r2 += d * d;
+        }
+        s += -2.0 * c[2] * (x[ax] - f.centers[3 * j + ax]) * exp(-c[2] * r2);
+      }
+      return c[1] * s;
+    }
+    case 8: {  // div(eps grad u), eps = c0 + c1 sum exp(-c2 r^2), u = prod_k sin(c3 x_k + c4)
+      double sn[3], cs[3], u = 1.0;
+      for (int k = 0; k < dim; ++k) sn[k] = sin(c[3] * x[k] + c[4]), cs[k] = cos(c[3] * x[k] + c[4]), u *= sn[k];
+      double eps = c[0], geps[3] = {0.0, 0.0, 0.0};
+      for (int j = 0; j < f.n_centers; ++j) {
+        double r2 = 0.0;
+        for (int k = 0; k < dim; ++k) {
+          const double d = x[k] - f.centers[3 * j + k];
+          r2 += d * d;
+        }
+        const double e = exp(-c[2] * r2);
+        eps += c[1] * e;
+        for (int k = 0; k < dim; ++k) geps[k] += c[1] * -2.0 * c[2] * (x[k] - f.centers[3 * j + k]) * e;
+      }
+      double f2 = -dim * c[3] * c[3] * u * eps;
+      for (int k = 0; k < dim; ++k) {
+        double du = c[3] * cs[k];
+        for (int l = 0; l < dim; ++l)
+          if (l != k) du *= sn[l];
+        f2 += geps[k] * du;
+      }
+      return f2;
+    }
     default: return __longlong_as_double(0x7ff8000000000000ULL);
   }
 }

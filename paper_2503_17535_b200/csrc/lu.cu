@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -42,7 +43,7 @@ HPS_DEV void argmax_merge(double& v, int& i, double v2, int i2) {
 __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelArgs a) {
   extern __shared__ __align__(16) double sm[];
   double* pan = sm;                               // [nb][rpc]
-  double* cand_row = sm + (size_t)a.rpc * kLuNB;  // [2][kLuNB] published candidate row
+  double* cand_row = sm + (size_t)a.rpc * a.nb;   // [2][kLuNB] published candidate row
   double* jrow_pub = cand_row + 2 * kLuNB;        // [2][kLuNB] published row j
   double* urow = jrow_pub + 2 * kLuNB;            // pivot row (local copy)
   double* jrow = urow + kLuNB;                    // row j (pivot owner's copy)
@@ -295,6 +296,39 @@ __global__ void __launch_bounds__(kColThreads) trsm_upper_kernel(const TrsmUArgs
 
 // Apply the complete pivot sequence of a factorization to R (LAPACK laswp), via the
 // composite permutation built in shared memory: R[i, :] <- R[perm[i], :].
+// Large n (perm + column no longer fit one CTA's shared memory together): the composite
+// permutation goes to global memory first, then each column is gathered through shared memory.
+__global__ void build_perm_kernel(const int* ipiv, int n, int* perm_out) {
+  extern __shared__ int pm[];
+  const long long b = blockIdx.x;
+  const int* pv = ipiv + b * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) pm[i] = i;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < n; ++i) {
+      const int j = pv[i];
+      if (j != i) {
+        const int t = pm[i];
+        pm[i] = pm[j];
+        pm[j] = t;
+      }
+    }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) perm_out[b * n + i] = pm[i];
+}
+
+__global__ void apply_perm_cols_kernel(const int* perm, int n, double* R, long long ldR, long long strideR, int ncols) {
+  extern __shared__ __align__(16) double col[];
+  const long long b = blockIdx.x;
+  const int c = blockIdx.y;
+  if (c >= ncols) return;
+  double* x = R + b * strideR + (long long)c * ldR;
+  const int* pm = perm + b * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) col[i] = x[pm[i]];
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = col[i];
+}
+
 __global__ void laswp_perm_kernel(const int* ipiv, int n, double* R, long long ldR, long long strideR, int ncols,
                                   int cols_per_cta) {
   extern __shared__ __align__(16) double sbuf[];
@@ -342,10 +376,10 @@ cudaError_t launch_panel(int batch, int n, int j0, int nb, BatchedMat M, int* ip
   if (cs > kMaxCluster) cs = kMaxCluster;
   const int rows = n - j0;
   int rpc = (rows + cs - 1) / cs;
-  if (rpc > kMaxRowsPerCta) return cudaErrorInvalidValue;
+  if ((long long)rpc * nb > (long long)kMaxRowsPerCta * kLuNB) return cudaErrorInvalidValue;
   if (cs == 1) rpc = rows;
   PanelArgs pa{M.p, M.ld, M.stride, n, j0, nb, rpc, cs, ipiv, stats};
-  const size_t smem = (size_t)rpc * kLuNB * 8 + 6 * kLuNB * 8 + (kPanelThreads / 32) * 12 + 128;
+  const size_t smem = (size_t)rpc * nb * 8 + 6 * kLuNB * 8 + (kPanelThreads / 32) * 12 + 128;
   static size_t smem_set = 0;
   if (smem > smem_set) {
     cudaError_t e = cudaFuncSetAttribute(panel_getrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -403,6 +437,10 @@ cudaError_t launch_swap_trsm(int batch, int n, int j0, int nb, const double* L, 
 // trailing matrix is streamed from HBM 8x less often).
 constexpr int kOuterNB = 256;
 
+// GEPP panel width: 32 columns, or 16 when the panel of a matrix beyond 16 CTAs x 864 rows would
+// not fit the cluster's shared memory (2D L=9 / 3D L=4 roots, n up to 27,648)
+int panel_width(int n) { return n > kMaxCluster * kMaxRowsPerCta ? kLuNB / 2 : kLuNB; }
+
 // C[rows, cols] += alpha * A[rows, k] * B[k, cols] on sub-blocks of strided batches.
 cudaError_t gemm_sub(int batch, int rows, int cols, int k, double alpha, const double* A, long long lda, long long sA,
                      const double* B, long long ldb, long long sB, double* C, long long ldc, long long sC,
@@ -430,10 +468,13 @@ cudaError_t gemm_sub(int batch, int rows, int cols, int k, double alpha, const d
   return launch_dgemm(g, st);
 }
 
-#define HPS_TRY(x)                      \
-  do {                                  \
-    cudaError_t e_ = (x);               \
-    if (e_ != cudaSuccess) return e_;   \
+#define HPS_TRY(x)                                                                      \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess) {                                                            \
+      if (getenv("HPS_DEBUG")) fprintf(stderr, "lu.cu:%d %s -> %s\n", __LINE__, #x, cudaGetErrorString(e_)); \
+      return e_;                                                                        \
+    }                                                                                   \
   } while (0)
 
 // Blocked back substitution R <- U^-1 R, U = upper triangle of LU (n x n).
@@ -563,8 +604,9 @@ cudaError_t factor_outer_panel(int batch, int n, int J, int Jend, BatchedMat M, 
   const long long ld = M.ld, sM = M.stride;
   double* A = M.p;
   auto at = [&](int r, int c) { return A + (long long)c * ld + r; };
-  for (int j0 = J; j0 < Jend; j0 += kLuNB) {
-    const int nb = std::min(kLuNB, Jend - j0);
+  const int PW = panel_width(n);
+  for (int j0 = J; j0 < Jend; j0 += PW) {
+    const int nb = std::min(PW, Jend - j0);
     HPS_TRY(launch_panel(batch, n, j0, nb, M, ipiv, stats, s));
     Seg segs[2];
     segs[0] = Seg{at(0, J), ld, sM, j0 - J, 0};                  // in-block L columns: swaps only
@@ -636,7 +678,7 @@ cudaError_t bgetrf_aug_lookahead(int batch, int n, int m, BatchedMat M, int* ipi
 
 }  // namespace
 
-int bgetrf_max_n() { return kMaxCluster * kMaxRowsPerCta; }
+int bgetrf_max_n() { return kMaxCluster * kMaxRowsPerCta * (kLuNB / (kLuNB / 2)); }
 
 cudaError_t lu_stats_init(double* stats, int batch, cudaStream_t st) {
   if (!stats || batch <= 0) return cudaSuccess;
@@ -656,8 +698,8 @@ cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double*
     const int Jend = std::min(n, J + kOuterNB);
     // (1) factor the outer panel columns [J, Jend); the row swaps go to every column at once,
     //     while columns right of the outer panel are otherwise left untouched
-    for (int j0 = J; j0 < Jend; j0 += kLuNB) {
-      const int nb = std::min(kLuNB, Jend - j0);
+    for (int j0 = J; j0 < Jend; j0 += panel_width(n)) {
+      const int nb = std::min(panel_width(n), Jend - j0);
       HPS_TRY(launch_panel(batch, n, j0, nb, M, ipiv, stats, st));
       Seg segs[3];
       segs[0] = Seg{A, ld, sM, j0, 0};                              // factored L columns: swaps only
@@ -684,7 +726,7 @@ cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double*
 
 cudaError_t bgetrs(int batch, int n, int m, BatchedMat LU, const int* ipiv, BatchedMat R, cudaStream_t st) {
   if (batch <= 0 || n <= 0 || m <= 0) return cudaSuccess;
-  {
+  if ((size_t)n * 12 <= 200 * 1024) {
     const int cpc = 8;
     const size_t smem = (size_t)n * 12;
     static size_t smem_set = 0;
@@ -693,6 +735,26 @@ cudaError_t bgetrs(int batch, int n, int m, BatchedMat LU, const int* ipiv, Batc
       smem_set = smem;
     }
     laswp_perm_kernel<<<dim3(batch, (m + cpc - 1) / cpc), 256, smem, st>>>(ipiv, n, R.p, R.ld, R.stride, m, cpc);
+    HPS_TRY(cudaGetLastError());
+  } else {
+    static int* perm = nullptr;
+    static size_t perm_cap = 0;
+    const size_t need = (size_t)batch * n;
+    if (need > perm_cap) {
+      if (perm) cudaFree(perm);
+      HPS_TRY(cudaMalloc(&perm, need * sizeof(int)));
+      perm_cap = need;
+    }
+    static bool attr = false;
+    if (!attr) {
+      HPS_TRY(cudaFuncSetAttribute(build_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      HPS_TRY(cudaFuncSetAttribute(apply_perm_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      attr = true;
+    }
+    if ((size_t)n * 8 > 227 * 1024) return cudaErrorInvalidValue;
+    build_perm_kernel<<<batch, 256, (size_t)n * sizeof(int), st>>>(ipiv, n, perm);
+    HPS_TRY(cudaGetLastError());
+    apply_perm_cols_kernel<<<dim3(batch, m), 512, (size_t)n * 8, st>>>(perm, n, R.p, R.ld, R.stride, m);
     HPS_TRY(cudaGetLastError());
   }
   const double* L = LU.p;
@@ -716,9 +778,13 @@ int lu_launch_count(int n, int m, bool factor) {
   int l = 1;  // stats init | laswp
   for (int J = 0; J < n; J += kOuterNB) {
     const int Jend = std::min(n, J + kOuterNB);
+    if (factor)
+      for (int j0 = J; j0 < Jend; j0 += panel_width(n)) {
+        const int nb = std::min(panel_width(n), Jend - j0);
+        l += 2 + (Jend - j0 - nb > 0 ? 1 : 0);
+      }
     for (int j0 = J; j0 < Jend; j0 += kLuNB) {
       const int nb = std::min(kLuNB, Jend - j0);
-      if (factor) l += 2 + (Jend - j0 - nb > 0 ? 1 : 0);
       if (!factor || Jend < n + m) l += 1 + (Jend - j0 - nb > 0 ? 1 : 0);
     }
     if (Jend < n) l += 1;

@@ -23,8 +23,8 @@ LIB_PATH = os.path.join(HERE, "libhps_b200.so")
 HPSG_OK, HPSG_ERR_INVALID, HPSG_ERR_SINGULAR_LEAF, HPSG_ERR_SINGULAR_MERGE, HPSG_ERR_NONFINITE, HPSG_ERR_OOM, \
     HPSG_ERR_CUDA, HPSG_ERR_STATE, HPSG_ERR_NO_DEVICE = range(9)
 
-FIELD_CONST, FIELD_BUMPS, FIELD_PLANE_SIN, FIELD_PLANE_COS, FIELD_BUMPS_SIN, FIELD_POISSON2D_SRC, FIELD_SAMPLED = \
-    range(7)
+FIELD_CONST, FIELD_BUMPS, FIELD_PLANE_SIN, FIELD_PLANE_COS, FIELD_BUMPS_SIN, FIELD_POISSON2D_SRC, FIELD_SAMPLED, \
+    FIELD_BUMPS_GRAD, FIELD_DIVGRAD_SRC = range(9)
 ROLE_LAPLACIAN, ROLE_GRADIENT, ROLE_ZEROTH, ROLE_SECOND_ORDER = range(4)
 
 

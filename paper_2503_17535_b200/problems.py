@@ -11,7 +11,8 @@ from typing import Callable
 
 import numpy as np
 
-from .hps import (FIELD_BUMPS, FIELD_BUMPS_SIN, FIELD_CONST, FIELD_PLANE_COS, FIELD_PLANE_SIN, FIELD_POISSON2D_SRC,
+from .hps import (FIELD_BUMPS, FIELD_BUMPS_GRAD, FIELD_BUMPS_SIN, FIELD_CONST, FIELD_DIVGRAD_SRC, FIELD_PLANE_COS,
+                  FIELD_PLANE_SIN, FIELD_POISSON2D_SRC,
                   ROLE_GRADIENT, ROLE_LAPLACIAN, ROLE_ZEROTH, Field, Term, bump_centers)
 
 
@@ -81,8 +82,25 @@ def poisson3d_const() -> Problem:
     return Problem("laplace3d", 3, 0.0, 1.0, [Term(ROLE_LAPLACIAN, Field(FIELD_CONST, (1.0,)))], None, u, u)
 
 
+def poisson3d_var(seed=11, n_bumps=5, amp=0.5, alpha=4.0, omega=2.0, phase=0.5) -> Problem:
+    """BASELINE.json configs[3]: 3D variable-coefficient Poisson div(eps grad u) = f on [-1,1]^3
+    (roles laplacian = eps, gradient_a = d_a eps), eps = 1 + amp * sum_j exp(-alpha |x - z_j|^2)
+    with seeded centers (std::mt19937_64, proj/src/problems.cpp:126-141), manufactured
+    u = prod_k sin(omega x_k + phase)."""
+    z = bump_centers(seed, n_bumps, 3)
+    terms = [Term(ROLE_LAPLACIAN, Field(FIELD_BUMPS, (1.0, amp, alpha), centers=z))]
+    terms += [Term(ROLE_GRADIENT, Field(FIELD_BUMPS_GRAD, (0.0, amp, alpha, float(a)), centers=z), axis=a)
+              for a in range(3)]
+    src = Field(FIELD_DIVGRAD_SRC, (1.0, amp, alpha, omega, phase), centers=z)
+
+    def u(x):
+        return np.sin(omega * x[..., 0] + phase) * np.sin(omega * x[..., 1] + phase) * np.sin(omega * x[..., 2] + phase)
+
+    return Problem("poisson3d_var", 3, -1.0, 1.0, terms, src, u, u)
+
+
 CATALOG = {"poisson2d": poisson2d, "helmholtz_bumps": helmholtz_bumps, "laplace_poly2d": laplace_poly2d,
-           "laplace3d": poisson3d_const}
+           "laplace3d": poisson3d_const, "poisson3d_var": poisson3d_var}
 
 
 def rel_linf(u, ref):

@@ -97,3 +97,20 @@ def test_getrf_singular_reports_pivot():
     st = torch.zeros((1, 3), dtype=torch.float64, device="cuda")
     assert lib().hpsg_dev_getrf_aug(1, n, m, M.data_ptr(), n, n * (n + m), piv.data_ptr(), st.data_ptr()) == 0
     assert st[0, 2].item() == 7
+
+
+def test_getrf_aug_narrow_panels_large_n():
+    """n beyond 16 CTAs x 864 rows: 16-column GEPP panels (2D L=9 / 3D L=4 roots); residual check on device."""
+    import torch
+    n, m = 14400, 3
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
+    R = torch.randn((n, m), dtype=torch.float64, device="cuda", generator=g)
+    M = torch.cat([A, R], dim=1).t().contiguous()   # column-major [A | R]
+    piv = torch.zeros((1, n), dtype=torch.int32, device="cuda")
+    st = torch.zeros((1, 3), dtype=torch.float64, device="cuda")
+    assert lib().hpsg_dev_getrf_aug(1, n, m, M.data_ptr(), n, n * (n + m), piv.data_ptr(), st.data_ptr()) == 0
+    X = M[n:].t()
+    res = (A @ X - R).abs().max() / (A.abs().max() * X.abs().max() * n)
+    assert res < 1e-15, float(res)
+    assert st[0, 2].item() == -1
