@@ -211,6 +211,11 @@ def run_b200(args):
         "clocks": clk,
         "device_gb": st["device_bytes"] / 1e9,
     }
+    if world == 1 and not args.no_extras and not args.profile:
+        out["configs_extra"] = {"config3_multi_rhs": bench_multi_rhs(solver, tree, torch, args)}
+    del solver
+    if world == 1 and not args.no_extras and not args.profile:
+        out["configs_extra"]["config4_3d"] = bench_3d(torch)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"], par = cpu_baseline(args, prob, u_gpu)
         out["accuracy"].update(par)
@@ -219,6 +224,69 @@ def run_b200(args):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out), flush=True)
+
+
+def bench_multi_rhs(solver, tree, torch, args, nrhs=256, chunk=64):
+    """BASELINE configs[2]: 256 new boundary right-hand sides against the stored factorization
+    (downward pass + leaf reconstruction as DMMA GEMMs, chunks of 64 RHS)."""
+    gen = torch.Generator(device="cuda").manual_seed(args.seed)
+    G = torch.randn((nrhs, solver.nb_root), dtype=torch.float64, device="cuda", generator=gen)
+    U = torch.empty((chunk, tree.n_leaves, tree.p ** 2), dtype=torch.float64, device="cuda")
+    solver.solve_device(G[:chunk].data_ptr(), chunk, U.data_ptr())   # warm-up (workspace)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for c0 in range(0, nrhs, chunk):
+        solver.solve_device(G[c0:c0 + chunk].data_ptr(), chunk, U.data_ptr())
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    # linearity spot check: solve(2 g0 - g1) = 2 u0 - u1 on the last chunk
+    g2 = (2 * G[nrhs - chunk] - G[nrhs - chunk + 1]).reshape(1, -1).contiguous()
+    u2 = torch.empty((1, tree.n_leaves, tree.p ** 2), dtype=torch.float64, device="cuda")
+    solver.solve_device(g2.data_ptr(), 1, u2.data_ptr())
+    lin = float(((u2[0] - (2 * U[0] - U[1])).abs().max() / U[0].abs().max()).item())
+    st = solver.stats()   # of the single-RHS solve above: stored operator bytes + one u
+    flops_rhs = 2.0 * (st["solve_bytes"] - 8.0 * tree.total_points) / 8.0   # one FMA per stored operator entry
+    return {"workload": f"2D Helmholtz p={tree.p} L={tree.L}: {nrhs} boundary RHS (seeded N(0,1)) on one build, "
+                        f"chunks of {chunk}", "ms": ms, "ms_per_rhs": ms / nrhs,
+            "rhs_dof_per_s": nrhs * tree.total_points / (ms / 1e3), "flops_per_rhs": flops_rhs,
+            "achieved_tflops": flops_rhs * nrhs / (ms / 1e3) / 1e12, "linearity_rel": lin}
+
+
+def bench_3d(torch, L=4, p=8, steps=2):
+    """BASELINE configs[3]: 3D variable-coefficient Poisson div(eps grad u) = f, p=8, uniform
+    octree L=4 (N = 2,097,152; root D = 27,648), one GPU (the 8-GPU octant sharding is the
+    same sharded.py path with nchild = 8)."""
+    import paper_2503_17535_b200 as H
+    from paper_2503_17535_b200 import problems as PR
+    prob = PR.poisson3d_var()
+    tree = H.build_uniform_tree(prob.lo, prob.hi, L, 3, p)
+    s = H.HpsSolver(tree, prob.terms, prob.source, literal_sign=False, root_implicit_S=True)
+    g = torch.tensor(prob.boundary(s.root_boundary_points()), device="cuda")
+    u = torch.empty((tree.n_leaves, p ** 3), dtype=torch.float64, device="cuda")
+    s.build()
+    s.solve_device(g.data_ptr(), 1, u.data_ptr())
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        s.build()
+        s.solve_device(g.data_ptr(), 1, u.data_ptr())
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    st = s.stats()
+    err = PR.rel_linf(u.cpu().numpy(), prob.exact(s.leaf_points()))
+    out = {"workload": f"3D variable-coefficient Poisson, p={p}, L={L} uniform octree, N={tree.total_points} DOF "
+                       f"(BASELINE configs[3]), root D={st['top_D_size']} (implicit S)",
+           "ms_per_step": ms, "value": tree.total_points / (ms / 1e3), "unit": "DOF/s",
+           "build_ms": st["t_build_ms"], "solve_ms": st["t_solve_ms"],
+           "merge_by_depth_ms": [round(x, 2) for x in st["t_level_ms"]],
+           "counted_build_tflops": st["build_flops"] / st["t_build_ms"] / 1e9,
+           "rel_linf_vs_exact": err, "device_gb": st["device_bytes"] / 1e9}
+    s.close()
+    return out
 
 
 def run_sharded(args, world, rank, local):
@@ -392,6 +460,7 @@ def main():
     ap.add_argument("--cpu-L", type=int, default=None, help="tree depth of the CPU baseline run (default: --L)")
     ap.add_argument("--explicit-root", action="store_true", help="form S at the root (reference 2D default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the config 3 (256 RHS) and config 4 (3D) lines")
     ap.add_argument("--profile", action="store_true", help="one untimed-warmup-free step for ncu launch lists")
     args = ap.parse_args()
     if args.profile:

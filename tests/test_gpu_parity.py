@@ -183,3 +183,27 @@ def test_cpp_dropin_example_runs():
     rep = json.loads(r.stdout)
     assert rep["N"] == 16384 and rep["top_D"] == 4 * 14 * 4
     assert rep["rel_linf"] < 1e-8
+
+
+@pytest.mark.parametrize("p,L,literal", [(6, 2, True), (8, 2, False), (8, 3, False)])
+def test_3d_variable_poisson_parity(p, L, literal):
+    """BASELINE configs[3] operator (div(eps grad u), gradient terms from the bump-gradient field,
+    batched leaf path since ni > 196 at p = 8) against the oracle on identical inputs."""
+    prob = PR.poisson3d_var()
+    s = gpu_solver(prob, p, L, literal=literal, root_implicit=True)
+    o = oracle_solver(prob, p, L, literal=literal, root_implicit=True, parallel=True)
+    o.build()
+    g = prob.boundary(s.root_boundary_points())
+    assert rel(s.solve(g), o.solve(g)) < 1e-10
+    if not literal and p == 8:
+        assert PR.rel_linf(s.solve(g), prob.exact(s.leaf_points())) < (1e-5 if L == 2 else 1e-6)
+
+
+def test_lookahead_lu_matches_default(monkeypatch):
+    """The opt-in look-ahead LU driver (side-stream panels, deferred block swaps) gives the same merge."""
+    prob = PR.helmholtz_bumps()
+    a = gpu_solver(prob, 16, 5, root_implicit=True)       # root D = 1792 > 512: both drivers apply
+    monkeypatch.setenv("HPS_LU_LOOKAHEAD", "1")
+    b = gpu_solver(prob, 16, 5, root_implicit=True)
+    g = prob.boundary(a.root_boundary_points())
+    assert rel(b.solve(g), a.solve(g)) < 1e-12
