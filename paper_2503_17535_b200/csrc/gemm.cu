@@ -1,5 +1,6 @@
 // gemm.cu -- tile-shape dispatch for the strided-batched DMMA DGEMM (gemm.cuh).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "gemm.cuh"
@@ -63,6 +64,8 @@ static cudaError_t run_cfg(int cfg, const GemmArgs& a, cudaStream_t st) {
 
 cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st) {
   if (a.m <= 0 || a.n <= 0 || a.batch <= 0) return cudaSuccess;
+  static const bool log = getenv("HPS_GEMM_LOG") != nullptr;  // developer knob: shape trace for launch lists
+  if (log) fprintf(stderr, "GEMM %d %d %d %d\n", a.m, a.n, a.k, a.batch);
   // k <= 0 runs zero k-tiles: D = beta*C
   const bool vec = aligned16(a.A) && aligned16(a.B) && (a.lda % 2 == 0) && (a.ldb % 2 == 0) &&
                    (a.sA % 2 == 0) && (a.sB % 2 == 0);

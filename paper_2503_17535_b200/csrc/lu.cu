@@ -477,6 +477,174 @@ cudaError_t gemm_sub(int batch, int rows, int cols, int k, double alpha, const d
     }                                                                                   \
   } while (0)
 
+// ---- slab triangular solves on the tensor cores (n >= kSlabMinN) -------------------------
+// A 256-row slab solve X_slab <- T_slab^-1 X_slab (T unit-lower L or upper U of one outer
+// block) as ONE launch instead of 8 x (32-column TRSM + k=32 GEMM): the inverses of the
+// slab's 32x32 diagonal blocks are formed first (one warp per block), then every CTA keeps a
+// 32-column strip of X in shared memory and runs the blocked substitution with DMMA:
+// X_b = T_bb^-1 X_b, then X_i -= T_ib X_b for the remaining blocks i of the slab.
+constexpr int kSlabMinN = 512;
+constexpr int kSlabCW = 32;                 // strip width (4 warps x 8 columns)
+constexpr int kSlabLdX = kOuterNB + 4;      // 260 = 4 mod 16: conflict-free B fragments
+constexpr int kSlabChunk = 64;              // rows of T staged per update step
+constexpr int kSlabLdA = kSlabChunk + 4;    // 68
+constexpr int kSlabLdI = kLuNB + 4;         // 36
+
+struct SlabArgs {
+  const double* T;
+  long long ldT, strideT;
+  int r0, nbk;          // slab rows [r0, r0 + nbk), nbk <= kOuterNB; T_slab = T[r0.., r0..]
+  double* X;            // X[(c) * ldX + r0 + i] for c < ncols
+  long long ldX, strideX;
+  int ncols;
+  const double* Winv;   // [batch][kOuterNB / 32][32 x 32] diagonal-block inverses (column-major)
+};
+
+template <bool UPPER>
+__global__ void __launch_bounds__(32) diag_inv_kernel(const double* T, long long ld, long long stride, int r0,
+                                                      int nbk, double* Winv) {
+  __shared__ double D[kLuNB][kLuNB + 1];
+  const long long b = blockIdx.x;
+  const int blk = blockIdx.y, lane = threadIdx.x;
+  const int s0 = r0 + blk * kLuNB, nb = min(kLuNB, r0 + nbk - s0);
+  const double* Tb = T + b * stride;
+  for (int e = lane; e < kLuNB * kLuNB; e += 32) {
+    const int r = e % kLuNB, c = e / kLuNB;
+    D[r][c] = (r < nb && c < nb) ? Tb[(long long)(s0 + c) * ld + s0 + r] : (r == c ? 1.0 : 0.0);
+  }
+  __syncwarp();
+  double x[kLuNB];  // column `lane` of the inverse
+#pragma unroll
+  for (int i = 0; i < kLuNB; ++i) x[i] = i == lane ? 1.0 : 0.0;
+  if (!UPPER) {
+#pragma unroll
+    for (int k = 0; k < kLuNB - 1; ++k)
+#pragma unroll
+      for (int i = k + 1; i < kLuNB; ++i) x[i] -= D[i][k] * x[k];
+  } else {
+#pragma unroll
+    for (int k = kLuNB - 1; k >= 0; --k) {
+      x[k] /= D[k][k];
+#pragma unroll
+      for (int i = 0; i < k; ++i) x[i] -= D[i][k] * x[k];
+    }
+  }
+  double* out = Winv + (b * (kOuterNB / kLuNB) + blk) * (kLuNB * kLuNB) + lane * kLuNB;
+#pragma unroll
+  for (int i = 0; i < kLuNB; ++i) out[i] = x[i];
+}
+
+template <bool UPPER>
+__global__ void __launch_bounds__(128) slab_trsm_kernel(const SlabArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  double* xs = smem;                              // [kSlabCW][kSlabLdX]: X strip, k-major per column
+  double* as = xs + kSlabCW * kSlabLdX;           // [kLuNB][kSlabLdA]: T chunk (A operand, [k][m])
+  double* iv = as + kLuNB * kSlabLdA;             // [kLuNB][kSlabLdI]: T_bb^-1 (A operand, [k][m])
+  const long long b = blockIdx.x;
+  const int c0 = blockIdx.y * kSlabCW;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const double* T = a.T + b * a.strideT;
+  double* X = a.X + b * a.strideX;
+  const int nbk = a.nbk, nblk = (nbk + kLuNB - 1) / kLuNB;
+  for (int e = tid; e < kSlabCW * kOuterNB; e += blockDim.x) {
+    const int r = e % kOuterNB, c = e / kOuterNB;
+    xs[c * kSlabLdX + r] = (r < nbk && c0 + c < a.ncols) ? X[(long long)(c0 + c) * a.ldX + a.r0 + r] : 0.0;
+  }
+  const int wc = warp * 8;  // this warp's 8 columns of the strip
+  for (int step = 0; step < nblk; ++step) {
+    const int bk = UPPER ? nblk - 1 - step : step;
+    const int s0 = bk * kLuNB;  // slab-relative first row/column of the diagonal block
+    const double* inv = a.Winv + (b * (kOuterNB / kLuNB) + bk) * (kLuNB * kLuNB);
+    for (int e = tid; e < kLuNB * kLuNB; e += blockDim.x) iv[(e / kLuNB) * kSlabLdI + e % kLuNB] = inv[e];
+    __syncthreads();
+    {  // X_b <- T_bb^-1 X_b, in place (each warp reads and writes only its own columns)
+      double acc[kLuNB / 8][2];
+#pragma unroll
+      for (int mt = 0; mt < kLuNB / 8; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+#pragma unroll
+      for (int kb = 0; kb < kLuNB; kb += 4) {
+        const double bv = xs[(wc + g) * kSlabLdX + s0 + kb + t4];
+#pragma unroll
+        for (int mt = 0; mt < kLuNB / 8; ++mt) dmma_8x8x4(acc[mt][0], acc[mt][1], iv[(kb + t4) * kSlabLdI + mt * 8 + g], bv);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int mt = 0; mt < kLuNB / 8; ++mt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) xs[(wc + 2 * t4 + h) * kSlabLdX + s0 + mt * 8 + g] = acc[mt][h];
+    }
+    // X_i -= T_ib X_b over the rows still to be solved: below the block (L) or above it (U)
+    const int ra = UPPER ? 0 : s0 + kLuNB, rb = UPPER ? s0 : nbk;
+    for (int q0 = ra; q0 < rb; q0 += kSlabChunk) {
+      const int qn = min(kSlabChunk, rb - q0);
+      __syncthreads();  // previous chunk's A operand consumed; X_b visible
+      for (int e = tid; e < kLuNB * kSlabChunk; e += blockDim.x) {
+        const int mm = e % kSlabChunk, k = e / kSlabChunk;
+        as[k * kSlabLdA + mm] =
+            (mm < qn) ? -T[(long long)(a.r0 + s0 + k) * a.ldT + a.r0 + q0 + mm] : 0.0;
+      }
+      __syncthreads();
+      for (int mt = 0; mt < (qn + 7) / 8; ++mt) {
+        const int r = q0 + mt * 8 + g;
+        double c[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) c[h] = xs[(wc + 2 * t4 + h) * kSlabLdX + r];
+#pragma unroll
+        for (int kb = 0; kb < kLuNB; kb += 4)
+          dmma_8x8x4(c[0], c[1], as[(kb + t4) * kSlabLdA + mt * 8 + g], xs[(wc + g) * kSlabLdX + s0 + kb + t4]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) xs[(wc + 2 * t4 + h) * kSlabLdX + r] = c[h];
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < kSlabCW * kOuterNB; e += blockDim.x) {
+    const int r = e % kOuterNB, c = e / kOuterNB;
+    if (r < nbk && c0 + c < a.ncols) X[(long long)(c0 + c) * a.ldX + a.r0 + r] = xs[c * kSlabLdX + r];
+  }
+}
+
+double* slab_workspace(int batch) {
+  static double* w = nullptr;
+  static long long cap = 0;
+  const long long need = (long long)batch * (kOuterNB / kLuNB) * kLuNB * kLuNB;
+  if (need > cap) {
+    if (w) cudaFree(w);
+    w = nullptr;
+    if (cudaMalloc(&w, need * sizeof(double)) != cudaSuccess) return nullptr;
+    cap = need;
+  }
+  return w;
+}
+
+// X[r0:r0+nbk, 0:ncols] <- T_slab^-1 X[...] (unit-lower or upper slab of T), two launches
+template <bool UPPER>
+cudaError_t slab_trsm(int batch, const double* T, long long ldT, long long sT, int r0, int nbk, double* X,
+                      long long ldX, long long sX, int ncols, cudaStream_t st) {
+  if (ncols <= 0 || nbk <= 0) return cudaSuccess;
+  double* w = slab_workspace(batch);
+  if (!w) return cudaErrorMemoryAllocation;
+  const int nblk = (nbk + kLuNB - 1) / kLuNB;
+  diag_inv_kernel<UPPER><<<dim3(batch, nblk), 32, 0, st>>>(T, ldT, sT, r0, nbk, w);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t smem = (size_t)(kSlabCW * kSlabLdX + kLuNB * kSlabLdA + kLuNB * kSlabLdI) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(slab_trsm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(slab_trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  SlabArgs a{T, ldT, sT, r0, nbk, X, ldX, sX, ncols, w};
+  const long long strips = (ncols + kSlabCW - 1) / kSlabCW;
+  if (strips > 65535) return cudaErrorInvalidConfiguration;
+  slab_trsm_kernel<UPPER><<<dim3(batch, (unsigned)strips), 128, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 // Blocked back substitution R <- U^-1 R, U = upper triangle of LU (n x n).
 cudaError_t back_subst(int batch, int n, int m, const double* U, long long ldU, long long strideU, double* R,
                        long long ldR, long long strideR, cudaStream_t st) {
@@ -485,6 +653,12 @@ cudaError_t back_subst(int batch, int n, int m, const double* U, long long ldU, 
   for (int ob = nouter - 1; ob >= 0; --ob) {
     const int r0 = ob * kOuterNB, r1 = std::min(n, r0 + kOuterNB);
     const int nsub = (r1 - r0 + kLuNB - 1) / kLuNB;
+    if (n >= kSlabMinN && m >= kSlabCW && !getenv("HPS_NO_SLAB_TRSM")) {
+      HPS_TRY(slab_trsm<true>(batch, U, ldU, strideU, r0, r1 - r0, R, ldR, strideR, m, st));
+      HPS_TRY(gemm_sub(batch, r0, m, r1 - r0, -1.0, U + (long long)r0 * ldU, ldU, strideU, R + r0, ldR, strideR, R,
+                       ldR, strideR, st));
+      continue;
+    }
     for (int sb = nsub - 1; sb >= 0; --sb) {
       const int s0 = r0 + sb * kLuNB, nb = std::min(kLuNB, r1 - s0);
       TrsmUArgs t{U, ldU, strideU, s0, nb, R, ldR, strideR, m};
@@ -710,6 +884,9 @@ cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double*
                        at(j0 + nb, j0 + nb), ld, sM, st));
     }
     // (2) U12 = L11^-1 A12 over the outer block's row slab (blocked forward substitution)
+    if (n >= kSlabMinN && Jend < ncol && !getenv("HPS_NO_SLAB_TRSM")) {
+      HPS_TRY(slab_trsm<false>(batch, A, ld, sM, J, Jend - J, at(0, Jend), ld, sM, ncol - Jend, st));
+    } else
     for (int j0 = J; j0 < Jend && Jend < ncol; j0 += kLuNB) {
       const int nb = std::min(kLuNB, Jend - j0);
       Seg seg{at(0, Jend), ld, sM, ncol - Jend, 1};
@@ -760,6 +937,9 @@ cudaError_t bgetrs(int batch, int n, int m, BatchedMat LU, const int* ipiv, Batc
   const double* L = LU.p;
   for (int J = 0; J < n; J += kOuterNB) {
     const int Jend = std::min(n, J + kOuterNB);
+    if (n >= kSlabMinN && m >= kSlabCW && !getenv("HPS_NO_SLAB_TRSM")) {
+      HPS_TRY(slab_trsm<false>(batch, L, LU.ld, LU.stride, J, Jend - J, R.p, R.ld, R.stride, m, st));
+    } else
     for (int j0 = J; j0 < Jend; j0 += kLuNB) {
       const int nb = std::min(kLuNB, Jend - j0);
       Seg seg{R.p, R.ld, R.stride, m, 1};
