@@ -43,6 +43,9 @@ METRIC = "HPS build+solve seconds & DOF/s (2D p=16 L=8) at 1/2/4/8 B200; rel err
 # PAPER.md:629 / :1755 -- H100 JAX, subtree recomputation, p=16 L=8: 4.02 s (N = 16,777,216)
 PAPER_H100_DOFS = 16777216 / 4.02
 FP64_PEAK_TFLOPS = 37.155     # profiles/r01_fp64_peak.json (DMMA microbench; MEASURED_PEAKS.json has no FP64 entry)
+# dram__bytes_read.sum + dram__bytes_write.sum of one leaf_fused_kernel launch at p=16 L=8
+# (ncu --set full, profiles/r01_ncu_summary.md)
+LEAF_KERNEL_DRAM_BYTES = 19.78e9 + 68.50e9
 
 
 def load_peaks():
@@ -158,6 +161,7 @@ def run_b200(args):
             s = solver.stats()
             builds.append(s["t_build_ms"])
             solves.append(s["t_solve_ms"])
+            leaf_ms.append(s["t_leaf_ms"])
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / K
@@ -167,9 +171,11 @@ def run_b200(args):
             ms = t.item()
         return ms, float(np.mean(builds)), float(np.mean(solves))
 
+    leaf_ms = []
     clocks = ClockSampler(local)
     clocks.start()
     ms, t_build, t_solve = timed(step_device, args.steps)
+    t_leaf = float(np.mean(leaf_ms))
     clk = clocks.stop()
     u_gpu = u_dev.cpu().numpy()
     ms_e2e = ms
@@ -178,6 +184,9 @@ def run_b200(args):
     st = solver.stats()
 
     err_exact = PR.rel_linf(u_gpu, prob.exact(solver.leaf_points()))
+    ni, ne, nb, npt = (args.p - 2) ** 2, 4 * args.p - 4, 4 * (args.p - 2), args.p ** 2
+    leaf_flops = tree.n_leaves * (2 / 3 * ni ** 3 + 2 * ni * ni * ne + 2 * ni * ne * nb + 2 * nb * npt * nb
+                                  + 2 * ni * ni + 2 * nb * npt)
     peaks = load_peaks()
     flops = st["build_flops"]
     value = N * world / (ms / 1e3)
@@ -195,11 +204,20 @@ def run_b200(args):
                    "parallelism": f"{world} independent replica(s)"},
         "stages_ms": {"build": t_build, "leaf": st["t_leaf_ms"], "merge": st["t_merge_ms"], "solve": t_solve,
                       "merge_by_depth": [round(x, 3) for x in st["t_level_ms"]]},
-        "roofline": {"bound": "tensor", "kernel": "build (batched DMMA LU/TRSM/GEMM pipeline)",
-                     "achieved": flops / (t_build / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": flops / (t_build / 1e3) / 1e12 / FP64_PEAK_TFLOPS, "traffic": None,
-                     "algorithmic_flops": flops,
+        # dominant single kernel: leaf_fused_kernel (one launch per build, ~35% of the step in the
+        # ncu launch list profiles/r01_launches_L8_v2.csv); achieved = SURVEY 8d leaf FLOPs x leaves
+        # / the live CUDA-event time of that launch; traffic = dram read+write of that launch from
+        # the ncu --set full capture (profiles/r01_ncu_summary.md)
+        "roofline": {"bound": "tensor", "kernel": "leaf_fused_kernel (stage 1, all 65,536 leaves, one launch)",
+                     "achieved": leaf_flops / (t_leaf / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": leaf_flops / (t_leaf / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
+                     "traffic": LEAF_KERNEL_DRAM_BYTES if (args.L, args.p) == (8, 16) else None,
+                     "algorithmic_flops": leaf_flops, "launch_ms": t_leaf,
                      "peak_source": "FP64 DMMA microbench profiles/r01_fp64_peak.json (of measured)"},
+        "roofline_build": {"bound": "tensor", "kernel": "whole build (leaf kernel + batched DMMA LU/TRSM/GEMM merges)",
+                           "achieved": flops / (t_build / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                           "frac": flops / (t_build / 1e3) / 1e12 / FP64_PEAK_TFLOPS, "algorithmic_flops": flops,
+                           "note": "SURVEY 8d dense-equivalent counts; the block-sparse Schur products skip zero blocks"},
         "solve_roofline": {"bound": "hbm", "achieved": st["solve_bytes"] / (t_solve / 1e3) / 1e9,
                            "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                            "frac": st["solve_bytes"] / (t_solve / 1e3) / 1e9 / peaks.get("hbm_gbs", 6532.5),
