@@ -144,14 +144,10 @@ __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelA
     }
     __syncthreads();
     const int piv = *s_piv;
-    const int own_p = piv / a.rpc;
-    if (piv != j) {
-      for (int c = tid; c < nb; c += kPanelThreads) {
-        if (own_j == rank) pan[c * a.rpc + (j - r_begin)] = urow[c];
-        if (own_p == rank) pan[c * a.rpc + (piv - r_begin)] = jrow[c];
-      }
-    }
-    __syncthreads();
+    // Row exchange without a barrier: row j takes the pivot row (nobody reads row j again in this
+    // column), and the owner of row piv eliminates from the old row j (jrow) instead of pan.
+    if (piv != j && own_j == rank)
+      for (int c = tid; c < nb; c += kPanelThreads) pan[c * a.rpc + (j - r_begin)] = urow[c];
 
     const double pv = urow[j];
     const double apv = fabs(pv);
@@ -163,19 +159,26 @@ __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelA
     }
     if (rank == 0 && tid == 0) a.ipiv[b * a.n + a.j0 + j] = a.j0 + piv;
 
-    // ---- eliminate rows below j within this CTA's chunk (LAPACK scales by the reciprocal)
-    if (apv > 0.0) {
-      const double inv = 1.0 / pv;
-      for (int r = tid; r < nr; r += kPanelThreads) {
-        const int gr = r_begin + r;
-        if (gr <= j) continue;
-        const double l = pan[j * a.rpc + r] * inv;
+    // ---- eliminate rows below j within this CTA's chunk (LAPACK scales by the reciprocal).
+    // Each thread only touches its own rows, and the next column reads other threads' rows only
+    // after its first barrier, so no barrier closes the column.
+    const double inv = apv > 0.0 ? 1.0 / pv : 0.0;
+    for (int r = tid; r < nr; r += kPanelThreads) {
+      const int gr = r_begin + r;
+      if (gr <= j) continue;
+      const bool swapped = (gr == piv && piv != j);
+      if (swapped)  // the old row j moves here whole, its earlier multipliers included
+        for (int c = 0; c < j; ++c) pan[c * a.rpc + r] = jrow[c];
+      if (apv > 0.0) {
+        const double l = (swapped ? jrow[j] : pan[j * a.rpc + r]) * inv;
         pan[j * a.rpc + r] = l;
-        for (int c = j + 1; c < nb; ++c) pan[c * a.rpc + r] -= l * urow[c];
+        for (int c = j + 1; c < nb; ++c) pan[c * a.rpc + r] = (swapped ? jrow[c] : pan[c * a.rpc + r]) - l * urow[c];
+      } else if (swapped) {
+        for (int c = j; c < nb; ++c) pan[c * a.rpc + r] = jrow[c];
       }
     }
-    __syncthreads();
   }
+  __syncthreads();
 
   for (int e = tid; e < nr * nb; e += kPanelThreads) {
     const int r = e % nr, c = e / nr;
@@ -367,7 +370,8 @@ __global__ void stats_init_kernel(double* s, int batch) {
 }
 
 int cluster_for(int n) {
-  int cs = (n + kRowsPerCta - 1) / kRowsPerCta;
+  static const int rows_per_cta = getenv("HPS_PANEL_ROWS") ? atoi(getenv("HPS_PANEL_ROWS")) : kRowsPerCta;  // tuning knob
+  int cs = (n + rows_per_cta - 1) / rows_per_cta;
   return std::max(1, cs);
 }
 
@@ -488,7 +492,6 @@ constexpr int kSlabCW = 32;                 // strip width (4 warps x 8 columns)
 constexpr int kSlabLdX = kOuterNB + 4;      // 260 = 4 mod 16: conflict-free B fragments
 constexpr int kSlabChunk = 64;              // rows of T staged per update step
 constexpr int kSlabLdA = kSlabChunk + 4;    // 68
-constexpr int kSlabLdI = kLuNB + 4;         // 36
 
 struct SlabArgs {
   const double* T;
@@ -534,31 +537,74 @@ __global__ void __launch_bounds__(32) diag_inv_kernel(const double* T, long long
   for (int i = 0; i < kLuNB; ++i) out[i] = x[i];
 }
 
+// Work items of one slab solve, in order: for each diagonal block (top-down for L, bottom-up for
+// U) one "diag" item (X_b <- T_bb^-1 X_b) and one "update" item per 64-row chunk of the rows still
+// to be solved.  Every item's A operand (an inverse block or a T chunk) is staged by cp.async one
+// item ahead into a two-slot ring, so its global latency hides behind the previous item's DMMAs.
+template <bool UPPER>
+struct SlabItems {
+  int nblk, nbk;
+  HPS_DEV int blk(int step) const { return UPPER ? nblk - 1 - step : step; }
+  HPS_DEV int rows_lo(int bk) const { return UPPER ? 0 : (bk + 1) * kLuNB; }
+  HPS_DEV int rows_hi(int bk) const { return UPPER ? bk * kLuNB : nbk; }
+  HPS_DEV int nchunks(int bk) const { return (rows_hi(bk) - rows_lo(bk) + kSlabChunk - 1) / kSlabChunk; }
+};
+
 template <bool UPPER>
 __global__ void __launch_bounds__(128) slab_trsm_kernel(const SlabArgs a) {
   extern __shared__ __align__(16) double smem[];
-  double* xs = smem;                              // [kSlabCW][kSlabLdX]: X strip, k-major per column
-  double* as = xs + kSlabCW * kSlabLdX;           // [kLuNB][kSlabLdA]: T chunk (A operand, [k][m])
-  double* iv = as + kLuNB * kSlabLdA;             // [kLuNB][kSlabLdI]: T_bb^-1 (A operand, [k][m])
+  double* xs = smem;                          // [kSlabCW][kSlabLdX]: X strip, k-major per column
+  double* ring = xs + kSlabCW * kSlabLdX;     // 2 x [kLuNB][kSlabLdA]: A operand ([k][m]) per item
   const long long b = blockIdx.x;
   const int c0 = blockIdx.y * kSlabCW;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const double* T = a.T + b * a.strideT;
   double* X = a.X + b * a.strideX;
-  const int nbk = a.nbk, nblk = (nbk + kLuNB - 1) / kLuNB;
+  const SlabItems<UPPER> it{(a.nbk + kLuNB - 1) / kLuNB, a.nbk};
+  const double* winv = a.Winv + b * (kOuterNB / kLuNB) * (kLuNB * kLuNB);
+
+  // item cursor: (step, chunk) with chunk == -1 the diag item
+  auto stage = [&](int step, int chunk, double* dst) {
+    const int bk = it.blk(step);
+    if (chunk < 0) {
+      const double* inv = winv + bk * (kLuNB * kLuNB);  // column-major: (m, k) at m + 32 k
+      for (int e = tid; e < kLuNB * kLuNB; e += blockDim.x) cp_async8(dst + (e / kLuNB) * kSlabLdA + e % kLuNB, inv + e, true);
+    } else {
+      const int q0 = it.rows_lo(bk) + chunk * kSlabChunk, qn = min(kSlabChunk, it.rows_hi(bk) - q0);
+      const double* src = T + (long long)(a.r0 + bk * kLuNB) * a.ldT + a.r0 + q0;
+      for (int e = tid; e < kLuNB * kSlabChunk; e += blockDim.x) {
+        const int mm = e % kSlabChunk, k = e / kSlabChunk;
+        cp_async8(dst + k * kSlabLdA + mm, mm < qn ? src + (long long)k * a.ldT + mm : src, mm < qn);
+      }
+    }
+    cp_async_commit();
+  };
+  auto next = [&](int& step, int& chunk) {
+    if (chunk + 1 < it.nchunks(it.blk(step))) {
+      ++chunk;
+    } else {
+      ++step;
+      chunk = -1;
+    }
+  };
+
+  int step = 0, chunk = -1, slot = 0;
+  stage(step, chunk, ring);
   for (int e = tid; e < kSlabCW * kOuterNB; e += blockDim.x) {
     const int r = e % kOuterNB, c = e / kOuterNB;
-    xs[c * kSlabLdX + r] = (r < nbk && c0 + c < a.ncols) ? X[(long long)(c0 + c) * a.ldX + a.r0 + r] : 0.0;
+    xs[c * kSlabLdX + r] = (r < a.nbk && c0 + c < a.ncols) ? X[(long long)(c0 + c) * a.ldX + a.r0 + r] : 0.0;
   }
   const int wc = warp * 8;  // this warp's 8 columns of the strip
-  for (int step = 0; step < nblk; ++step) {
-    const int bk = UPPER ? nblk - 1 - step : step;
-    const int s0 = bk * kLuNB;  // slab-relative first row/column of the diagonal block
-    const double* inv = a.Winv + (b * (kOuterNB / kLuNB) + bk) * (kLuNB * kLuNB);
-    for (int e = tid; e < kLuNB * kLuNB; e += blockDim.x) iv[(e / kLuNB) * kSlabLdI + e % kLuNB] = inv[e];
-    __syncthreads();
-    {  // X_b <- T_bb^-1 X_b, in place (each warp reads and writes only its own columns)
+  while (step < it.nblk) {
+    int ns = step, nc = chunk;
+    next(ns, nc);
+    cp_async_wait<0>();
+    __syncthreads();  // item's operand landed; the other slot's previous item is consumed
+    if (ns < it.nblk) stage(ns, nc, ring + (slot ^ 1) * (kLuNB * kSlabLdA));
+    const double* A = ring + slot * (kLuNB * kSlabLdA);
+    const int s0 = it.blk(step) * kLuNB;
+    if (chunk < 0) {  // X_b <- T_bb^-1 X_b, in place (each warp reads and writes only its own columns)
       double acc[kLuNB / 8][2];
 #pragma unroll
       for (int mt = 0; mt < kLuNB / 8; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
@@ -566,42 +612,38 @@ __global__ void __launch_bounds__(128) slab_trsm_kernel(const SlabArgs a) {
       for (int kb = 0; kb < kLuNB; kb += 4) {
         const double bv = xs[(wc + g) * kSlabLdX + s0 + kb + t4];
 #pragma unroll
-        for (int mt = 0; mt < kLuNB / 8; ++mt) dmma_8x8x4(acc[mt][0], acc[mt][1], iv[(kb + t4) * kSlabLdI + mt * 8 + g], bv);
+        for (int mt = 0; mt < kLuNB / 8; ++mt) dmma_8x8x4(acc[mt][0], acc[mt][1], A[(kb + t4) * kSlabLdA + mt * 8 + g], bv);
       }
       __syncwarp();
 #pragma unroll
       for (int mt = 0; mt < kLuNB / 8; ++mt)
 #pragma unroll
         for (int h = 0; h < 2; ++h) xs[(wc + 2 * t4 + h) * kSlabLdX + s0 + mt * 8 + g] = acc[mt][h];
-    }
-    // X_i -= T_ib X_b over the rows still to be solved: below the block (L) or above it (U)
-    const int ra = UPPER ? 0 : s0 + kLuNB, rb = UPPER ? s0 : nbk;
-    for (int q0 = ra; q0 < rb; q0 += kSlabChunk) {
-      const int qn = min(kSlabChunk, rb - q0);
-      __syncthreads();  // previous chunk's A operand consumed; X_b visible
-      for (int e = tid; e < kLuNB * kSlabChunk; e += blockDim.x) {
-        const int mm = e % kSlabChunk, k = e / kSlabChunk;
-        as[k * kSlabLdA + mm] =
-            (mm < qn) ? -T[(long long)(a.r0 + s0 + k) * a.ldT + a.r0 + q0 + mm] : 0.0;
-      }
-      __syncthreads();
+    } else {  // X_q -= T_qb X_b for this chunk's rows
+      const int q0 = it.rows_lo(it.blk(step)) + chunk * kSlabChunk;
+      const int qn = min(kSlabChunk, it.rows_hi(it.blk(step)) - q0);
+      double bneg[kLuNB / 4];
+#pragma unroll
+      for (int kb = 0; kb < kLuNB; kb += 4) bneg[kb / 4] = -xs[(wc + g) * kSlabLdX + s0 + kb + t4];
       for (int mt = 0; mt < (qn + 7) / 8; ++mt) {
         const int r = q0 + mt * 8 + g;
         double c[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) c[h] = xs[(wc + 2 * t4 + h) * kSlabLdX + r];
 #pragma unroll
-        for (int kb = 0; kb < kLuNB; kb += 4)
-          dmma_8x8x4(c[0], c[1], as[(kb + t4) * kSlabLdA + mt * 8 + g], xs[(wc + g) * kSlabLdX + s0 + kb + t4]);
+        for (int kb = 0; kb < kLuNB; kb += 4) dmma_8x8x4(c[0], c[1], A[(kb + t4) * kSlabLdA + mt * 8 + g], bneg[kb / 4]);
 #pragma unroll
         for (int h = 0; h < 2; ++h) xs[(wc + 2 * t4 + h) * kSlabLdX + r] = c[h];
       }
     }
-    __syncthreads();
+    step = ns;
+    chunk = nc;
+    slot ^= 1;
   }
+  __syncthreads();
   for (int e = tid; e < kSlabCW * kOuterNB; e += blockDim.x) {
     const int r = e % kOuterNB, c = e / kOuterNB;
-    if (r < nbk && c0 + c < a.ncols) X[(long long)(c0 + c) * a.ldX + a.r0 + r] = xs[c * kSlabLdX + r];
+    if (r < a.nbk && c0 + c < a.ncols) X[(long long)(c0 + c) * a.ldX + a.r0 + r] = xs[c * kSlabLdX + r];
   }
 }
 
@@ -629,7 +671,7 @@ cudaError_t slab_trsm(int batch, const double* T, long long ldT, long long sT, i
   diag_inv_kernel<UPPER><<<dim3(batch, nblk), 32, 0, st>>>(T, ldT, sT, r0, nbk, w);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const size_t smem = (size_t)(kSlabCW * kSlabLdX + kLuNB * kSlabLdA + kLuNB * kSlabLdI) * sizeof(double);
+  const size_t smem = (size_t)(kSlabCW * kSlabLdX + 2 * kLuNB * kSlabLdA) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     e = cudaFuncSetAttribute(slab_trsm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
