@@ -18,23 +18,18 @@ __global__ void __launch_bounds__(kAsmThreads) leaf_assemble_kernel(const LeafAs
 }
 
 constexpr int kGatherThreads = 256;
-constexpr int kGatherPerThread = 4;
 
+// One warp per destination column: (slot, cc) are uniform over the column and the rows of each
+// section are a contiguous run in both source and destination, so loads and stores coalesce and
+// the only per-element index math is one 32-bit division by the section size.
 __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const GatherArgs a) {
   const long long node = blockIdx.x;
-  const long long total = (long long)a.nrows * a.ncols;
   const int s = a.s;
   const int nslots = a.kind == 0 ? a.NI + 1 + a.NE : (a.kind == 1 ? a.NI : 1 + a.NE);
   double* dst = a.dst + node * a.stride;
   const double* ch0 = a.child_HT + node * a.nchild * a.child_stride;
-  for (long long base = (long long)blockIdx.y * kGatherThreads * kGatherPerThread; base < total;
-       base += (long long)gridDim.y * kGatherThreads * kGatherPerThread)
-#pragma unroll
-  for (int it = 0; it < kGatherPerThread; ++it) {
-    const long long e = base + it * kGatherThreads + threadIdx.x;
-    if (e >= total) break;
-    const int r = int(e % a.nrows), col = int(e / a.nrows);
-    const int rsec = r / s, rr = r % s;
+  const int lane = threadIdx.x & 31, nw = kGatherThreads / 32;
+  for (int col = blockIdx.y * nw + (threadIdx.x >> 5); col < a.ncols; col += gridDim.y * nw) {
     int slot, cc;
     if (a.kind == 0) {
       const int nd = a.NI * s;
@@ -52,27 +47,29 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const GatherArgs
     } else if (a.kind == 1) {
       slot = col / s;
       cc = col % s;
+    } else if (col == 0) {
+      slot = 0;
+      cc = 0;
     } else {
-      if (col == 0) {
-        slot = 0;
-        cc = 0;
-      } else {
-        slot = 1 + (col - 1) / s;
-        cc = (col - 1) % s;
-      }
+      slot = 1 + (col - 1) / s;
+      cc = (col - 1) % s;
     }
-    const int* tab = a.src + 2 * (rsec * nslots + slot);
-    double v = 0.0;
+    double* dcol = dst + (long long)col * a.ld;
+    for (int r = lane; r < a.nrows; r += 32) {
+      const int rsec = r / s, rr = r - rsec * s;
+      const int* tab = a.src + 2 * (rsec * nslots + slot);
+      double v = 0.0;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int code = tab[k];
-      if (code < 0) continue;
-      const int child = code >> 6, rf = (code >> 3) & 7, cfp1 = code & 7;
-      const double* T = ch0 + child * a.child_stride;
-      const long long hc = cfp1 == 0 ? 0 : 1 + (long long)(cfp1 - 1) * s + cc;
-      v += T[hc * a.child_nb + rf * s + rr];
+      for (int k = 0; k < 2; ++k) {
+        const int code = __ldg(tab + k);
+        if (code < 0) continue;
+        const int child = code >> 6, rf = (code >> 3) & 7, cfp1 = code & 7;
+        const double* T = ch0 + child * a.child_stride;
+        const long long hc = cfp1 == 0 ? 0 : 1 + (long long)(cfp1 - 1) * s + cc;
+        v += T[hc * a.child_nb + rf * s + rr];
+      }
+      dcol[r] = v;
     }
-    dst[(long long)col * a.ld + r] = v;
   }
 }
 
@@ -154,9 +151,11 @@ void launch_leaf_assemble(const LeafAsmArgs& a, int n_leaves, cudaStream_t st) {
 }
 
 void launch_gather(const GatherArgs& a, int n_nodes, cudaStream_t st) {
-  const long long total = (long long)a.nrows * a.ncols;
-  const long long per = kGatherThreads * kGatherPerThread;
-  dim3 grid(n_nodes, (unsigned)std::min<long long>((total + per - 1) / per, 65535));
+  const int nw = kGatherThreads / 32;
+  // enough column groups to fill the GPU (~8 CTAs per SM over all nodes), each warp a column
+  const long long want = std::max<long long>(1, (148LL * 8 + n_nodes - 1) / n_nodes);
+  const long long groups = std::min<long long>((a.ncols + nw - 1) / nw, std::max<long long>(want, 1));
+  dim3 grid(n_nodes, (unsigned)std::min<long long>(groups, 65535));
   gather_kernel<<<grid, kGatherThreads, 0, st>>>(a);
 }
 
