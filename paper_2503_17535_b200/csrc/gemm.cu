@@ -1,5 +1,6 @@
 // gemm.cu -- tile-shape dispatch for the strided-batched DMMA DGEMM (gemm.cuh).
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -75,7 +76,11 @@ cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st) {
     cfg = 4;
     (void)work_tiles_big;
   }
-  return vec ? run_cfg<true>(cfg, a, st) : run_cfg<false>(cfg, a, st);
+  // seeding measured best at every k inside the build (merge 256 -> 232 ms); knob for sweeps
+  static const int seed_k = getenv("HPS_GEMM_SEED_K") ? atoi(getenv("HPS_GEMM_SEED_K")) : INT_MAX;
+  GemmArgs b = a;
+  b.seed_k_max = seed_k;
+  return vec ? run_cfg<true>(cfg, b, st) : run_cfg<false>(cfg, b, st);
 }
 
 }  // namespace hpsk
