@@ -233,6 +233,7 @@ def run_b200(args):
         out["configs_extra"] = {"config3_multi_rhs": bench_multi_rhs(solver, tree, torch, args)}
     del solver
     if world == 1 and not args.no_extras and not args.profile:
+        out["configs_extra"]["config3_new_sources"] = bench_new_sources(torch, args)
         out["configs_extra"]["config4_3d"] = bench_3d(torch)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"], par = cpu_baseline(args, prob, u_gpu)
@@ -270,6 +271,41 @@ def bench_multi_rhs(solver, tree, torch, args, nrhs=256, chunk=64):
                         f"chunks of {chunk}", "ms": ms, "ms_per_rhs": ms / nrhs,
             "rhs_dof_per_s": nrhs * tree.total_points / (ms / 1e3), "flops_per_rhs": flops_rhs,
             "achieved_tflops": flops_rhs * nrhs / (ms / 1e3) / 1e12, "linearity_rel": lin}
+
+
+def bench_new_sources(torch, args, nsrc=256, chunk=32):
+    """BASELINE configs[2] (ii): 256 new SOURCE right-hand sides against one stored build
+    (HpsSolver::solve_new_source: leaf re-solves with the kept LU factors, the upward source
+    pass through the stored merge factors, then the downward pass), chunks of 32 sources."""
+    import paper_2503_17535_b200 as H
+    from paper_2503_17535_b200 import problems as PR
+    prob = PR.helmholtz_bumps(k=args.k, seed=args.seed)
+    tree = H.build_uniform_tree(prob.lo, prob.hi, args.L, 2, args.p)
+    s = H.HpsSolver(tree, prob.terms, prob.source, literal_sign=False, root_implicit_S=not args.explicit_root,
+                    keep_factors=True)
+    s.build()
+    pts = torch.tensor(s.leaf_points(), device="cuda")
+    g = torch.tensor(prob.boundary(s.root_boundary_points()), device="cuda")
+    F = torch.empty((chunk, tree.n_leaves, tree.p ** 2), dtype=torch.float64, device="cuda")
+    G = g.reshape(1, -1).repeat(chunk, 1).contiguous()
+    U = torch.empty_like(F)
+    for i in range(chunk):  # seeded smooth sources
+        F[i] = torch.sin((1.0 + 0.1 * i) * pts[..., 0] - 0.5 * pts[..., 1] + 0.01 * i)
+    s.solve_new_source_device(F.data_ptr(), G.data_ptr(), chunk, U.data_ptr())  # warm-up (workspace)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(nsrc // chunk):
+        s.solve_new_source_device(F.data_ptr(), G.data_ptr(), chunk, U.data_ptr())
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    st = s.stats()
+    s.close()
+    return {"workload": f"2D Helmholtz p={tree.p} L={tree.L}: {nsrc} source RHS (smooth seeded fields) + boundary "
+                        f"data on one build with kept leaf factors, chunks of {chunk}",
+            "ms": ms, "ms_per_source": ms / nsrc, "rhs_dof_per_s": nsrc * tree.total_points / (ms / 1e3),
+            "build_ms_keep_factors": st["t_build_ms"], "device_gb": st["device_bytes"] / 1e9}
 
 
 def bench_3d(torch, L=4, p=8, steps=2):

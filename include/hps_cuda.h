@@ -80,7 +80,8 @@ typedef struct {
   int literal_sign;     /* 1: reference convention v_i = -L_ii^-1 f_i (local_solve.cpp:137); 0: corrected (+) */
   int root_implicit_S;  /* MergeOptions::implicit_S at the root (merge.hpp:104, solver.cpp:104) */
   int device;           /* CUDA device ordinal */
-  int reserved;
+  int keep_factors;     /* keep the leaf LU factors for hpsg_solve_new_source (LeafSolution::fac,
+                           local_solve.hpp:36); 2D p=16 L=8: +20 GB, batched leaf path */
 } hpsg_options;
 
 typedef struct {
@@ -141,6 +142,15 @@ int hpsg_part_solve_cut(hpsg_ctx* ctx, const double* d_g_root, int nrhs, double*
 int hpsg_solve(hpsg_ctx* ctx, const double* g_root, int nrhs, double* u_out, double* leaf_g_out);
 /* same with device pointers (no host copies); results are ready when the call returns */
 int hpsg_solve_device(hpsg_ctx* ctx, const double* d_g_root, int nrhs, double* d_u_out);
+/* HpsSolver::solve_new_source(leaf_f, RootBC::dirichlet, g_root), solver.hpp:71-72 /
+ * solver.cpp:285-307 (make_source_state :261-283, leaf_resolve_source local_solve.cpp:174-183,
+ * artifact_source_pass merge.cpp:514-567), for nsrc sources at once against the stored build:
+ * leaf_f: nsrc x n_leaves x p^dim source samples at the leaf Chebyshev points (only interior
+ * points are used), g_root: nsrc x root_bsize, u_out: nsrc x n_leaves x p^dim.  Needs
+ * keep_factors = 1 at create time.  The sign convention is the build's (literal_sign). */
+int hpsg_solve_new_source(hpsg_ctx* ctx, const double* leaf_f, const double* g_root, int nsrc, double* u_out);
+int hpsg_solve_new_source_device(hpsg_ctx* ctx, const double* d_leaf_f, const double* d_g_root, int nsrc,
+                                 double* d_u_out);
 /* HpsSolver::root_boundary_points(), solver.hpp:60 (root_bsize x 3) */
 int hpsg_root_boundary_points(hpsg_ctx* ctx, double* xyz);
 /* leaf_cheb_points over all leaves, mesh.hpp:73-74 (n_leaves x p^dim x 3) */

@@ -133,6 +133,10 @@ struct hpsg_ctx {
   // merges
   std::vector<Level> lv;  // index d = 0..L-1
   DevBuf Bscratch;
+  // new-source pass (keep_factors): per-leaf RHS -> v, leaf h, per level y = D^-1 h_int and node h
+  int src_nrhs = 0;
+  DevBuf srcF, srcR, srcH;
+  std::vector<std::unique_ptr<DevBuf>> srcY, srcHn;
   // solve workspace
   int ws_nrhs = 0;
   std::vector<std::unique_ptr<DevBuf>> G, GI;
@@ -338,6 +342,7 @@ void alloc_build(hpsg_ctx* c) {
     if (c->terms[i].role == HPSG_ROLE_SECOND_ORDER && c->terms[i].axis != c->terms[i].axis2) mixed = true;
   c->fused = hpsk::leaf_fused_supported(o.n, o.p, o.ni, o.nb, c->tree.dim, mixed) &&
              !(path && std::string(path) == "batched");
+  if (c->opts.keep_factors) c->fused = false;  // the batched path keeps [LU | v | Y] and the pivots per leaf
   if (c->T.cut) {
     c->fused = false;  // no leaf stage: the part's leaves are input nodes
   } else if (c->fused) {
@@ -673,11 +678,15 @@ void ensure_solve_ws(hpsg_ctx* c, int nrhs) {
 }
 
 // Downward pass + leaf reconstruction on device buffers.  d_g: root_bsize x nrhs; d_u: nrhs x n_leaves x npts.
-void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_leaf_g) {
+// new_source: use the source state of the last run_source_pass (y = D^-1 h_int per node, leaf v)
+// instead of the stored x_h / v columns (propagate / reconstruct_leaf with a SourceState,
+// solver.cpp:188-236): the leading row of every [lead; g] is 0 and the state is added after.
+void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_leaf_g, bool new_source = false) {
   const int Lh = c->T.L;
   ensure_solve_ws(c, nrhs);
   const int nb0 = c->lv[0].n_ext;
-  hpsk::launch_pack_root(c->G[0]->d(), d_g, nb0, nrhs, c->st);
+  const double lead = new_source ? 0.0 : 1.0;
+  hpsk::launch_pack_root(c->G[0]->d(), d_g, nb0, nrhs, c->st, lead);
   ++c->launches;
   for (int d = 0; d < Lh; ++d) {
     Level& L = c->lv[d];
@@ -703,7 +712,11 @@ void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_
       BatchedMat R{c->GI[0]->d(), L.n_int, sGI};
       ck(hpsk::bgetrs(1, L.n_int, nrhs, LU, L.piv.i(), R, c->st), "root getrs");
       c->launches += lu_launches(L.n_int, nrhs, false);
-      hpsk::launch_neg_add(c->GI[0]->d(), L.MD.d() + (long long)L.n_int * L.n_int, L.n_int, nrhs, L.n_int, c->st);
+      if (new_source)  // g_int = -(y + D^-1 C g)
+        hpsk::launch_axpby(c->GI[0]->d(), L.n_int, sGI, c->srcY[0]->d(), L.n_int, sGI, L.n_int, nrhs, 1, -1.0, -1.0,
+                           c->st);
+      else
+        hpsk::launch_neg_add(c->GI[0]->d(), L.MD.d() + (long long)L.n_int * L.n_int, L.n_int, nrhs, L.n_int, c->st);
       ++c->launches;
     } else {
       // g_int = S g + gtilde = -[x_h | X] [1; g]   (solver.cpp:207-208)
@@ -724,8 +737,14 @@ void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_
       g.alpha = -1.0;
       g.beta = 0.0;
       matvecs(c, g);
+      if (new_source) {  // g_int = S g + gtilde_new = -X g - y
+        hpsk::launch_axpby(c->GI[d]->d(), L.n_int, sGI, c->srcY[d]->d(), L.n_int, sGI, L.n_int, nrhs, L.nodes, 1.0,
+                           -1.0, c->st);
+        ++c->launches;
+      }
     }
     hpsk::ScatterArgs s{};
+    s.lead = lead;
     s.nchild = L.mt.nchild;
     s.nface = L.mt.nface;
     s.s = L.mt.s;
@@ -768,6 +787,13 @@ void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_
   g.D = c->Ui.d();
   g.ldd = o.ni;
   g.sD = (long long)o.ni * nrhs;
+  if (new_source) {  // u_i = Y_i g + v_new
+    ck(cudaMemcpyAsync(c->Ui.p, c->srcR.p, size_t(nl) * o.ni * nrhs * 8, cudaMemcpyDeviceToDevice, c->st), "v copy");
+    g.C = c->Ui.d();
+    g.ldc = o.ni;
+    g.sC = (long long)o.ni * nrhs;
+    g.beta = 1.0;
+  }
   matvecs(c, g);
   GemmArgs e;
   e.m = o.ne;
@@ -806,6 +832,140 @@ void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_
     ++c->launches;
   }
   ck(cudaGetLastError(), "solve kernels");
+}
+
+// New-source upward pass (make_source_state, solver.cpp:261-283) on device buffers, nrhs sources:
+//   leaves: v = sgn L_ii^-1 f_i from the kept factors (leaf_resolve_source, local_solve.cpp:174-183),
+//           h = Q_i v;
+//   levels: h_int / h_ext gathered from the children's h, y = D^-1 h_int (gtilde = -y) with the
+//           stored LU of D, h = h_ext - B y (artifact_source_pass, merge.cpp:514-567).
+void run_source_pass(hpsg_ctx* c, const double* d_f, int K) {
+  const hpsg::LeafOperators& o = c->ops;
+  const long long nl = c->T.n_leaves();
+  size_t* tot = &c->dev_bytes;
+  if (c->src_nrhs < K) {
+    c->srcR.alloc(size_t(nl) * o.ni * K * 8, tot);
+    c->srcH.alloc(size_t(nl) * o.nb * K * 8, tot);
+    c->srcY.resize(c->T.L);
+    c->srcHn.resize(c->T.L);
+    for (const Level& L : c->lv) {
+      if (!c->srcY[L.d]) c->srcY[L.d] = std::make_unique<DevBuf>();
+      c->srcY[L.d]->alloc(size_t(L.nodes) * L.n_int * K * 8, tot);
+      if (!c->global_root(L.d)) {
+        if (!c->srcHn[L.d]) c->srcHn[L.d] = std::make_unique<DevBuf>();
+        c->srcHn[L.d]->alloc(size_t(L.nodes) * L.n_ext * K * 8, tot);
+      }
+    }
+    c->src_nrhs = K;
+  }
+  const double sgn = c->opts.literal_sign ? -1.0 : 1.0;
+  hpsk::launch_pack_source(c->srcR.d(), d_f, c->interior.i(), o.ni, o.n, int(nl), K, sgn, c->st);
+  ++c->launches;
+  BatchedMat LU{c->leafM.d(), o.ni, c->strideLeafM()};
+  BatchedMat R{c->srcR.d(), o.ni, (long long)o.ni * K};
+  ck(hpsk::bgetrs(int(nl), o.ni, K, LU, c->leafPiv.i(), R, c->st), "leaf source getrs");
+  c->launches += lu_launches(o.ni, K, false);
+  GemmArgs q;  // h = Q_i v
+  q.m = o.nb;
+  q.n = K;
+  q.k = o.ni;
+  q.batch = int(nl);
+  q.A = c->Qi.d();
+  q.lda = o.nb;
+  q.sA = 0;
+  q.B = c->srcR.d();
+  q.ldb = o.ni;
+  q.sB = (long long)o.ni * K;
+  q.D = c->srcH.d();
+  q.ldd = o.nb;
+  q.sD = (long long)o.nb * K;
+  q.alpha = 1.0;
+  q.beta = 0.0;
+  gemm(c, q);
+  for (int d = c->T.L - 1; d >= 0; --d) {
+    Level& L = c->lv[d];
+    const bool root = c->global_root(d);
+    const int cnb = L.child_nb;
+    hpsk::GatherArgs ga{};
+    ga.s = L.mt.s;
+    ga.nchild = L.mt.nchild;
+    ga.child_nb = cnb;
+    ga.child_HT = d == c->T.L - 1 ? c->srcH.d() : c->srcHn[d + 1]->d();
+    ga.child_stride = (long long)cnb * K;
+    ga.src_rhs_stride = cnb;
+    ga.NI = L.mt.NI;
+    ga.NE = L.mt.NE;
+    ga.nrhs = K;
+    ga.ncols = 1;
+    // h_int: the h column of [D | h_int | C]
+    ga.src = L.md_src.i();
+    ga.kind = 0;
+    ga.col_offset = L.mt.NI * L.mt.s;
+    ga.nrows = L.n_int;
+    ga.dst = c->srcY[d]->d();
+    ga.ld = L.n_int;
+    ga.stride = (long long)L.n_int * K;
+    ga.dst_rhs_stride = L.n_int;
+    hpsk::launch_gather(ga, int(L.nodes), c->st);
+    ++c->launches;
+    if (!root) {  // h_ext: the h column of [h_ext | A]
+      ga.src = L.ah_src.i();
+      ga.kind = 2;
+      ga.col_offset = 0;
+      ga.nrows = L.n_ext;
+      ga.dst = c->srcHn[d]->d();
+      ga.ld = L.n_ext;
+      ga.stride = (long long)L.n_ext * K;
+      ga.dst_rhs_stride = L.n_ext;
+      hpsk::launch_gather(ga, int(L.nodes), c->st);
+      ++c->launches;
+    }
+    ck(cudaGetLastError(), "source gather");
+    BatchedMat D{L.MD.d(), L.n_int, L.strideMD()};
+    BatchedMat Y{c->srcY[d]->d(), L.n_int, (long long)L.n_int * K};
+    ck(hpsk::bgetrs(int(L.nodes), L.n_int, K, D, L.piv.i(), Y, c->st), "merge source getrs");
+    c->launches += lu_launches(L.n_int, K, false);
+    if (!root) {
+      // B = the children's T blocks coupling exterior rows to interface columns (scratch, as in the build)
+      hpsk::GatherArgs gb{};
+      gb.s = L.mt.s;
+      gb.nchild = L.mt.nchild;
+      gb.child_nb = cnb;
+      gb.child_HT = d == c->T.L - 1 ? c->leafHT.d() : c->lv[d + 1].AH.d();
+      gb.child_stride = d == c->T.L - 1 ? c->strideLeafHT() : c->lv[d + 1].strideAH();
+      gb.NI = L.mt.NI;
+      gb.NE = L.mt.NE;
+      gb.src = L.b_src.i();
+      gb.kind = 1;
+      gb.nrows = L.n_ext;
+      gb.ncols = L.n_int;
+      gb.dst = c->Bscratch.d();
+      gb.ld = L.n_ext;
+      gb.stride = (long long)L.n_ext * L.n_int;
+      hpsk::launch_gather(gb, int(L.nodes), c->st);
+      ++c->launches;
+      GemmArgs g;  // h = h_ext + B gtilde = h_ext - B y
+      g.m = L.n_ext;
+      g.n = K;
+      g.k = L.n_int;
+      g.batch = int(L.nodes);
+      g.A = c->Bscratch.d();
+      g.lda = L.n_ext;
+      g.sA = (long long)L.n_ext * L.n_int;
+      g.B = c->srcY[d]->d();
+      g.ldb = L.n_int;
+      g.sB = (long long)L.n_int * K;
+      g.C = c->srcHn[d]->d();
+      g.ldc = L.n_ext;
+      g.sC = (long long)L.n_ext * K;
+      g.D = c->srcHn[d]->d();
+      g.ldd = L.n_ext;
+      g.sD = (long long)L.n_ext * K;
+      g.alpha = -1.0;
+      g.beta = 1.0;
+      matvecs(c, g);
+    }
+  }
 }
 
 double solve_bytes(const hpsg_ctx* c, int nrhs) {
@@ -987,6 +1147,49 @@ int hpsg_solve(hpsg_ctx* c, const double* g_root, int nrhs, double* u_out, doubl
     c->stats.t_solve_ms = ms;
     c->stats.solve_bytes = solve_bytes(c, nrhs);
     c->stats.launches_solve = c->launches;
+  });
+}
+
+int hpsg_solve_new_source_device(hpsg_ctx* c, const double* d_f, const double* d_g, int nsrc, double* d_u) {
+  if (!c || !d_f || !d_g || !d_u || nsrc < 1) return HPSG_ERR_INVALID;
+  if (!c->built) return fail(c, HPSG_ERR_STATE, "solve_new_source: build() first");
+  if (!c->opts.keep_factors)
+    return fail(c, HPSG_ERR_STATE, "solve_new_source: create the solver with keep_factors = 1 (leaf factors)");
+  if (c->T.cut) return fail(c, HPSG_ERR_STATE, "solve_new_source: a cut part has no leaves");
+  return guarded(c, [&] {
+    c->launches = 0;
+    ck(cudaEventRecord(c->ev[4], c->st), "ev");
+    run_source_pass(c, d_f, nsrc);
+    run_solve(c, d_g, nsrc, d_u, nullptr, /*new_source=*/true);
+    ck(cudaEventRecord(c->ev[5], c->st), "ev");
+    ck(cudaEventSynchronize(c->ev[5]), "solve sync");
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]), "elapsed");
+    c->stats.t_solve_ms = ms;
+    c->stats.solve_bytes = solve_bytes(c, nsrc);
+    c->stats.launches_solve = c->launches;
+  });
+}
+
+int hpsg_solve_new_source(hpsg_ctx* c, const double* f, const double* g_root, int nsrc, double* u_out) {
+  if (!c || !f || !g_root || !u_out || nsrc < 1) return HPSG_ERR_INVALID;
+  if (!c->built) return fail(c, HPSG_ERR_STATE, "solve_new_source: build() first");
+  if (c->T.cut) return fail(c, HPSG_ERR_STATE, "solve_new_source: a cut part has no leaves");
+  const size_t nf = size_t(c->T.n_leaves()) * c->ops.n * nsrc;
+  const size_t nbr = size_t(c->lv[0].n_ext) * nsrc;
+  int rc = guarded(c, [&] {
+    c->srcF.alloc(nf * 8, &c->dev_bytes);
+    c->g_in.alloc(nbr * 8, &c->dev_bytes);
+    c->u_out.alloc(nf * 8, &c->dev_bytes);
+    ck(cudaMemcpyAsync(c->srcF.p, f, nf * 8, cudaMemcpyHostToDevice, c->st), "f H2D");
+    ck(cudaMemcpyAsync(c->g_in.p, g_root, nbr * 8, cudaMemcpyHostToDevice, c->st), "g H2D");
+  });
+  if (rc != HPSG_OK) return rc;
+  rc = hpsg_solve_new_source_device(c, c->srcF.d(), c->g_in.d(), nsrc, c->u_out.d());
+  if (rc != HPSG_OK) return rc;
+  return guarded(c, [&] {
+    ck(cudaMemcpyAsync(u_out, c->u_out.p, nf * 8, cudaMemcpyDeviceToHost, c->st), "u D2H");
+    ck(cudaStreamSynchronize(c->st), "u sync");
   });
 }
 

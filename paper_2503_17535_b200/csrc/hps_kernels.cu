@@ -26,10 +26,11 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const GatherArgs
   const long long node = blockIdx.x;
   const int s = a.s;
   const int nslots = a.kind == 0 ? a.NI + 1 + a.NE : (a.kind == 1 ? a.NI : 1 + a.NE);
-  double* dst = a.dst + node * a.stride;
-  const double* ch0 = a.child_HT + node * a.nchild * a.child_stride;
+  double* dst = a.dst + node * a.stride + blockIdx.z * a.dst_rhs_stride;
+  const double* ch0 = a.child_HT + node * a.nchild * a.child_stride + blockIdx.z * a.src_rhs_stride;
   const int lane = threadIdx.x & 31, nw = kGatherThreads / 32;
-  for (int col = blockIdx.y * nw + (threadIdx.x >> 5); col < a.ncols; col += gridDim.y * nw) {
+  for (int dcolumn = blockIdx.y * nw + (threadIdx.x >> 5); dcolumn < a.ncols; dcolumn += gridDim.y * nw) {
+    const int col = dcolumn + a.col_offset;
     int slot, cc;
     if (a.kind == 0) {
       const int nd = a.NI * s;
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const GatherArgs
       slot = 1 + (col - 1) / s;
       cc = (col - 1) % s;
     }
-    double* dcol = dst + (long long)col * a.ld;
+    double* dcol = dst + (long long)dcolumn * a.ld;
     for (int r = lane; r < a.nrows; r += 32) {
       const int rsec = r / s, rr = r - rsec * s;
       const int* tab = a.src + 2 * (rsec * nslots + slot);
@@ -85,7 +86,7 @@ __global__ void scatter_kernel(const ScatterArgs a) {
     const int c = e / (rows * a.nrhs);
     double v;
     if (r == 0) {
-      v = 1.0;
+      v = a.lead;
     } else {
       const int f = (r - 1) / a.s, i = (r - 1) % a.s;
       const int d = a.down[c * a.nface + f];
@@ -124,12 +125,12 @@ __global__ void leaf_output_kernel(const LeafOutArgs a) {
   }
 }
 
-__global__ void pack_root_kernel(double* G, const double* g, int nb, int nrhs) {
+__global__ void pack_root_kernel(double* G, const double* g, int nb, int nrhs, double lead) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int rows = nb + 1;
   if (e >= (long long)rows * nrhs) return;
   const int r = int(e % rows), c = int(e / rows);
-  G[e] = r == 0 ? 1.0 : g[(long long)c * nb + r - 1];
+  G[e] = r == 0 ? lead : g[(long long)c * nb + r - 1];
 }
 
 __global__ void unpack_leaf_g_kernel(double* out, const double* G, int nb, int nrhs, int n_leaves) {
@@ -155,7 +156,7 @@ void launch_gather(const GatherArgs& a, int n_nodes, cudaStream_t st) {
   // enough column groups to fill the GPU (~8 CTAs per SM over all nodes), each warp a column
   const long long want = std::max<long long>(1, (148LL * 8 + n_nodes - 1) / n_nodes);
   const long long groups = std::min<long long>((a.ncols + nw - 1) / nw, std::max<long long>(want, 1));
-  dim3 grid(n_nodes, (unsigned)std::min<long long>(groups, 65535));
+  dim3 grid(n_nodes, (unsigned)std::min<long long>(groups, 65535), a.nrhs);
   gather_kernel<<<grid, kGatherThreads, 0, st>>>(a);
 }
 
@@ -176,9 +177,51 @@ void launch_leaf_output(const LeafOutArgs& a, cudaStream_t st) {
   leaf_output_kernel<<<blocks, 256, 0, st>>>(a);
 }
 
-void launch_pack_root(double* G, const double* g, int nb, int nrhs, cudaStream_t st) {
+void launch_pack_root(double* G, const double* g, int nb, int nrhs, cudaStream_t st, double lead) {
   const long long tot = (long long)(nb + 1) * nrhs;
-  pack_root_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(G, g, nb, nrhs);
+  pack_root_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(G, g, nb, nrhs, lead);
+}
+
+namespace {
+__global__ void pack_source_kernel(double* R, const double* f, const int* interior, int ni, int npts, int n_leaves,
+                                   int nrhs, double sgn) {
+  const long long total = (long long)n_leaves * nrhs * ni;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = int(e % ni);
+    const long long lk = e / ni;
+    const int k = int(lk % nrhs);
+    const long long leaf = lk / nrhs;
+    R[e] = sgn * f[((long long)k * n_leaves + leaf) * npts + interior[r]];
+  }
+}
+__global__ void axpby_kernel(double* y, long long ldy, long long sy, const double* x, long long ldx, long long sx,
+                             int n, int nrhs, long long batch, double a, double b) {
+  const long long total = batch * nrhs * n;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = int(e % n);
+    const long long lk = e / n;
+    const int k = int(lk % nrhs);
+    const long long i = lk / nrhs;
+    double* yp = y + i * sy + (long long)k * ldy + r;
+    *yp = a * *yp + b * x[i * sx + (long long)k * ldx + r];
+  }
+}
+}  // namespace
+
+void launch_pack_source(double* R, const double* f, const int* interior, int ni, int npts, int n_leaves, int nrhs,
+                        double sgn, cudaStream_t st) {
+  const long long total = (long long)n_leaves * nrhs * ni;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 32);
+  pack_source_kernel<<<blocks, 256, 0, st>>>(R, f, interior, ni, npts, n_leaves, nrhs, sgn);
+}
+
+void launch_axpby(double* y, long long ldy, long long sy, const double* x, long long ldx, long long sx, int n,
+                  int nrhs, long long batch, double a, double b, cudaStream_t st) {
+  const long long total = batch * nrhs * n;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 32);
+  axpby_kernel<<<blocks, 256, 0, st>>>(y, ldy, sy, x, ldx, sx, n, nrhs, batch, a, b);
 }
 
 void launch_unpack_leaf_g(double* out, const double* G, int nb, int nrhs, int n_leaves, cudaStream_t st) {

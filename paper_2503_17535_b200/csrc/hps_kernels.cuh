@@ -81,6 +81,10 @@ struct GatherArgs {
   int nrows, ncols;
   double* dst;
   long long ld, stride;
+  // source-pass use (solver.cpp:261-283): logical columns start at col_offset, and nrhs
+  // right-hand sides are gathered at once (child source / destination offsets per RHS)
+  int col_offset = 0, nrhs = 1;
+  long long src_rhs_stride = 0, dst_rhs_stride = 0;
 };
 void launch_gather(const GatherArgs& a, int n_nodes, cudaStream_t st);
 
@@ -89,6 +93,7 @@ void launch_gather(const GatherArgs& a, int n_nodes, cudaStream_t st);
 // child's [1; g] column(s) from the parent's g_ext and the interface values g_int.
 struct ScatterArgs {
   int nchild, nface, s, nrhs;
+  double lead = 1.0;        // value of the leading row (1: apply the stored gtilde; 0: new-source pass)
   const int* down;          // nchild*nface
   const double* Gp;         // parent: (1 + nbp) x nrhs per node
   long long ldGp, strideGp;
@@ -117,7 +122,12 @@ struct LeafOutArgs {
 void launch_leaf_output(const LeafOutArgs& a, cudaStream_t st);
 
 // Fill a batch of (1 + nb) x nrhs columns with [1; g]: from a dense g (nb x nrhs, ld nb).
-void launch_pack_root(double* G, const double* g, int nb, int nrhs, cudaStream_t st);
+void launch_pack_root(double* G, const double* g, int nb, int nrhs, cudaStream_t st, double lead = 1.0);
+// new-source pass helpers: R[leaf][k][r] = sgn * f[k][leaf][interior[r]]; y <- a*y + b*x (n x nrhs blocks)
+void launch_pack_source(double* R, const double* f, const int* interior, int ni, int npts, int n_leaves, int nrhs,
+                        double sgn, cudaStream_t st);
+void launch_axpby(double* y, long long ldy, long long sy, const double* x, long long ldx, long long sx, int n,
+                  int nrhs, long long batch, double a, double b, cudaStream_t st);
 // Extract leaf boundary data (without the leading 1) for leaf_g_out.
 void launch_unpack_leaf_g(double* out, const double* G, int nb, int nrhs, int n_leaves, cudaStream_t st);
 

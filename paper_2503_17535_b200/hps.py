@@ -54,7 +54,7 @@ class _Part(C.Structure):
 
 
 class _Options(C.Structure):
-    _fields_ = [("literal_sign", C.c_int), ("root_implicit_S", C.c_int), ("device", C.c_int), ("reserved", C.c_int)]
+    _fields_ = [("literal_sign", C.c_int), ("root_implicit_S", C.c_int), ("device", C.c_int), ("keep_factors", C.c_int)]
 
 
 class _Stats(C.Structure):
@@ -89,6 +89,8 @@ def lib():
         L.hpsg_part_root_ht.argtypes = [vp, C.c_void_p]
         L.hpsg_part_set_cut_ht.argtypes = [vp, C.c_longlong, C.c_void_p]
         L.hpsg_part_solve_cut.argtypes = [vp, C.c_void_p, C.c_int, C.c_void_p]
+        L.hpsg_solve_new_source.argtypes = [vp, dp, dp, C.c_int, dp]
+        L.hpsg_solve_new_source_device.argtypes = [vp, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
         L.hpsg_build.argtypes = [vp]
         L.hpsg_solve.argtypes = [vp, dp, C.c_int, dp, dp]
         L.hpsg_solve_device.argtypes = [vp, C.c_void_p, C.c_int, C.c_void_p]
@@ -222,7 +224,7 @@ class HpsSolver:
     """
 
     def __init__(self, tree: UniformTree, terms, source: Field | None = None, literal_sign=True,
-                 root_implicit_S=False, device=0, part=None):
+                 root_implicit_S=False, device=0, part=None, keep_factors=False):
         L = lib()
         self.tree = tree
         keep = []
@@ -232,7 +234,7 @@ class HpsSolver:
             arr[i].field = t.field.to_c(keep)
         src = source.to_c(keep) if source is not None else None
         tr = _Tree(tree.dim, tree.p, tree.L, tree.lo, tree.hi)
-        op = _Options(int(literal_sign), int(root_implicit_S), device, 0)
+        op = _Options(int(literal_sign), int(root_implicit_S), device, int(keep_factors))
         self.part = tuple(part) if part is not None else (0, 0, tree.L)
         pt = _Part(*self.part)
         h = C.c_void_p()
@@ -297,6 +299,25 @@ class HpsSolver:
     def solve_device(self, d_g_ptr, nrhs, d_u_ptr):
         """Zero-copy solve on device pointers (e.g. torch.Tensor.data_ptr())."""
         self._check(lib().hpsg_solve_device(self._h, C.c_void_p(d_g_ptr), nrhs, C.c_void_p(d_u_ptr)), "solve")
+
+    def solve_new_source(self, leaf_f, g_root):
+        """HpsSolver::solve_new_source(leaf_f, RootBC::dirichlet, g_root) (solver.cpp:285-307) for
+        one or several sources: leaf_f (n_leaves, p^d) or (nsrc, n_leaves, p^d) samples at the leaf
+        points, g_root (nb,) or (nsrc, nb).  Needs keep_factors=True."""
+        f = np.ascontiguousarray(leaf_f, dtype=np.float64)
+        g = np.ascontiguousarray(g_root, dtype=np.float64)
+        single = f.ndim == 2
+        f3 = f.reshape(1, *f.shape) if single else f
+        g2 = g.reshape(1, -1) if g.ndim == 1 else g
+        nsrc = f3.shape[0]
+        assert f3.shape[1:] == (self.n_leaves, self.npts) and g2.shape == (nsrc, self.nb_root)
+        u = np.empty((nsrc, self.n_leaves, self.npts))
+        self._check(lib().hpsg_solve_new_source(self._h, _dp(f3), _dp(g2), nsrc, _dp(u)), "solve_new_source")
+        return u[0] if single else u
+
+    def solve_new_source_device(self, d_f_ptr, d_g_ptr, nsrc, d_u_ptr):
+        self._check(lib().hpsg_solve_new_source_device(self._h, C.c_void_p(d_f_ptr), C.c_void_p(d_g_ptr), nsrc,
+                                                       C.c_void_p(d_u_ptr)), "solve_new_source")
 
     # ---- subtree parts (include/hps_cuda.h hpsg_part_*)
     def root_ht_device(self, d_dst_ptr):
