@@ -526,7 +526,8 @@ void run_leaf_stage(hpsg_ctx* c) {
   // [L_ii | sgn f | -L_ie P] -> [LU | v_i | Y_i]
   ck(hpsk::lu_stats_init(c->leafStats.d(), nl, c->st), "stats init");
   BatchedMat M{c->leafM.d(), o.ni, sM};
-  ck(hpsk::bgetrf_aug(nl, o.ni, 1 + o.nb, M, c->leafPiv.i(), c->leafStats.d(), c->st), "leaf bgetrf");
+  ck(hpsk::bgetrf_aug(nl, o.ni, 1 + o.nb, M, c->leafPiv.i(), c->leafStats.d(), c->st, c->opts.keep_factors != 0),
+     "leaf bgetrf");
   c->launches += lu_launches(o.ni, 1 + o.nb, true);
   // [h | T] = Q_i [v | Y_i] + [0 | Q_e P]   (T = Q Y, h = Q v; local_solve.cpp:140-141)
   GemmArgs t;
@@ -598,7 +599,10 @@ void run_merge_level(hpsg_ctx* c, int d) {
   ck(hpsk::lu_stats_init(L.stats.d(), int(L.nodes), c->st), "stats init");
   const int m = (root && c->opts.root_implicit_S) ? 1 : 1 + L.n_ext;
   BatchedMat M{L.MD.d(), L.n_int, L.strideMD()};
-  ck(hpsk::bgetrf_aug(int(L.nodes), L.n_int, m, M, L.piv.i(), L.stats.d(), c->st), "merge bgetrf");
+  // L of D is needed afterwards only at the root with implicit S (the solve's bgetrs) and for the
+  // new-source pass (keep_factors); elsewhere X = D^-1 [h_int | C] is all that is kept
+  const bool keep_L = (root && c->opts.root_implicit_S) || c->opts.keep_factors;
+  ck(hpsk::bgetrf_aug(int(L.nodes), L.n_int, m, M, L.piv.i(), L.stats.d(), c->st, keep_L), "merge bgetrf");
   c->launches += lu_launches(L.n_int, m, true);
   if (!root && L.mt.s >= kSparseSchurMinS && !getenv("HPS_DENSE_SCHUR")) {
     // [h | T] = [h_ext | A] - B [x_h | X] over the nonzero blocks of B only: section e's rows get

@@ -172,7 +172,8 @@ __device__ __forceinline__ double leaf_entry(const LeafAsmArgs& a, const SM& s, 
 //
 // enz_idx/enz_val (optional, operators without mixed terms only): instead of writing the
 // exterior block E, record each interior row's 2*dim exterior line neighbours at slot
-// r*2*dim + 2*axis + (neighbour at node 0 ? 0 : 1) as (exterior position, value).
+// (2*axis + (neighbour at node 0 ? 0 : 1)) * ni + r as (exterior position, value) -- row-fastest,
+// so a warp reading one slot for consecutive rows hits consecutive banks.
 template <class SM>
 __device__ __forceinline__ void leaf_assemble_block(const LeafAsmArgs& a, long long leaf, double* M, long long ldM,
                                                     double* E, SM& s, int* enz_idx = nullptr,
@@ -247,7 +248,7 @@ __device__ __forceinline__ void leaf_assemble_block(const LeafAsmArgs& a, long l
         M[(long long)q * ldM + r] = v;
       } else if (enz_idx) {
         const int ax = (w - 1) / (p - 1);
-        const int slot = r * 2 * dim + 2 * ax + (jj[ax] == 0 ? 0 : 1);
+        const int slot = (2 * ax + (jj[ax] == 0 ? 0 : 1)) * ni + r;
         enz_idx[slot] = -q - 1;
         enz_val[slot] = v;
       } else {

@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs 
       for (int e = tid; e < ni * nb; e += kFT) {
         const int r = e % ni, j = e / ni;
         double acc = 0.0;
-        for (int z = 0; z < nz; ++z) acc += nz_val[r * nz + z] * Pm[j * ne + nz_idx[r * nz + z]];
+        for (int z = 0; z < nz; ++z) acc += nz_val[z * ni + r] * Pm[j * ne + nz_idx[z * ni + r]];
         R[(long long)(1 + j) * ni + r] = -acc;
       }
     }

@@ -834,7 +834,8 @@ cudaError_t factor_outer_panel(int batch, int n, int J, int Jend, BatchedMat M, 
   return cudaSuccess;
 }
 
-cudaError_t bgetrf_aug_lookahead(int batch, int n, int m, BatchedMat M, int* ipiv, double* stats, cudaStream_t st) {
+cudaError_t bgetrf_aug_lookahead(int batch, int n, int m, BatchedMat M, int* ipiv, double* stats, cudaStream_t st,
+                                 bool keep_L) {
   const int K = (n + kOuterNB - 1) / kOuterNB;
   HPS_TRY(lookahead_prepare(batch, 2 * K + 2));
   LookAhead& la = lookahead();
@@ -862,9 +863,10 @@ cudaError_t bgetrf_aug_lookahead(int batch, int n, int m, BatchedMat M, int* ipi
     block_perm_kernel<<<batch, 256, (size_t)(n - J) * sizeof(int), st>>>(ipiv, n, J, Jend, la.moved, la.nmoved);
     HPS_TRY(cudaGetLastError());
     {
-      const int ncols = J + (ncol - Jend);
+      const int left = keep_L ? J : 0;
+      const int ncols = left + (ncol - Jend);
       const int gy = std::max(1, std::min(65535, (ncols + 7) / 8));
-      apply_perm_kernel<<<dim3(batch, gy), 256, 0, st>>>(A, ld, sM, la.moved, la.nmoved, 0, J, Jend, ncol);
+      apply_perm_kernel<<<dim3(batch, gy), 256, 0, st>>>(A, ld, sM, la.moved, la.nmoved, 0, left, Jend, ncol);
       HPS_TRY(cudaGetLastError());
     }
     // U12 = L11^-1 A12 over the block's row slab
@@ -902,10 +904,11 @@ cudaError_t lu_stats_init(double* stats, int batch, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double* stats, cudaStream_t st) {
+cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double* stats, cudaStream_t st,
+                       bool keep_L) {
   if (batch <= 0 || n <= 0) return cudaSuccess;
   if (n > bgetrf_max_n()) return cudaErrorInvalidValue;
-  if (n > 2 * kOuterNB && getenv("HPS_LU_LOOKAHEAD")) return bgetrf_aug_lookahead(batch, n, m, M, ipiv, stats, st);
+  if (n > 2 * kOuterNB && getenv("HPS_LU_LOOKAHEAD")) return bgetrf_aug_lookahead(batch, n, m, M, ipiv, stats, st, keep_L);
   const long long ld = M.ld, sM = M.stride;
   double* A = M.p;
   auto at = [&](int r, int c) { return A + (long long)c * ld + r; };
@@ -918,7 +921,8 @@ cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double*
       const int nb = std::min(panel_width(n), Jend - j0);
       HPS_TRY(launch_panel(batch, n, j0, nb, M, ipiv, stats, st));
       Seg segs[3];
-      segs[0] = Seg{A, ld, sM, j0, 0};                              // factored L columns: swaps only
+      segs[0] = keep_L ? Seg{A, ld, sM, j0, 0}                       // factored L columns: swaps only
+                       : Seg{at(0, J), ld, sM, j0 - J, 0};          // (this outer block's only: the rest is dead)
       segs[1] = Seg{at(0, j0 + nb), ld, sM, Jend - j0 - nb, 1};      // rest of the outer panel: swaps + L11^-1
       segs[2] = Seg{at(0, Jend), ld, sM, ncol - Jend, 0};            // right of the outer panel: swaps only
       HPS_TRY(launch_swap_trsm(batch, n, j0, nb, A, ld, sM, ipiv, segs, 3, st));

@@ -34,7 +34,10 @@ cudaError_t lu_stats_init(double* stats, int batch, cudaStream_t st);
 
 // Factor the leading n x n block of each M (pivots in ipiv[b*n + i], 0-based rows)
 // and, if m > 0, overwrite the m RHS columns M[:, n:n+m] with A^-1 R.
-cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double* stats, cudaStream_t st);
+// keep_L = false: the L factor is dead after the augmented solve (merge blocks whose X = D^-1 C is
+// all that is kept), so row exchanges skip the L columns of finished outer blocks.
+cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double* stats, cudaStream_t st,
+                       bool keep_L = true);
 
 // Solve with stored factors: R <- A^-1 R for the LU in `LU` (from bgetrf_aug).
 cudaError_t bgetrs(int batch, int n, int m, BatchedMat LU, const int* ipiv, BatchedMat R, cudaStream_t st);
