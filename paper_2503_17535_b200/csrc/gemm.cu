@@ -5,6 +5,9 @@
 #include <cstdlib>
 
 #include "gemm.cuh"
+#include "gemm_tma.cuh"
+
+#include <cudaTypedefs.h>
 
 namespace hpsk {
 
@@ -63,6 +66,61 @@ static cudaError_t run_cfg(int cfg, const GemmArgs& a, cudaStream_t st) {
   }
 }
 
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3D map (rows, cols, batch) over a column-major strided batch; box (bx0, bx1, 1)
+bool make_map(CUtensorMap* map, const double* base, long long rows, long long cols, long long ld, long long stride,
+              int batch, unsigned bx0, unsigned bx1) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * 8) % 16 || ld < rows) return false;
+  const long long nb = stride ? batch : 1;
+  if (stride && ((stride * 8) % 16 || stride < ld * cols)) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)rows, (cuuint64_t)cols, (cuuint64_t)nb};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 8), (cuuint64_t)((stride ? stride : ld * cols) * 8)};
+  cuuint32_t box[3] = {bx0, bx1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
+bool launch_dgemm_tma(const GemmArgs& a, cudaStream_t st, cudaError_t* err) {
+  constexpr int BM = 64, BN = 64, BK = 16, WM = 32, WN = 32, ST = 3;
+  using Cfg = GemmCfg<BM, BN, BK, WM, WN, ST, true>;
+  if (a.k <= 0) return false;
+  CUtensorMap mA, mB;
+  if (!make_map(&mA, a.A, a.m, a.k, a.lda, a.sA, a.batch, BM + 4, BK)) return false;
+  if (!make_map(&mB, a.B, a.k, a.n, a.ldb, a.sB, a.batch, BK + 4, BN)) return false;
+  auto kern = dgemm_tma_kernel<BM, BN, BK, WM, WN, ST>;
+  static bool attr = false;
+  if (!attr) {
+    *err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes + 64);
+    if (*err != cudaSuccess) return true;
+    attr = true;
+  }
+  const long long tiles = (long long)((a.m + BM - 1) / BM) * ((a.n + BN - 1) / BN);
+  const unsigned ty = (unsigned)std::min<long long>(tiles, 65535), tz = (unsigned)((tiles + ty - 1) / ty);
+  if (tz > 65535) return false;
+  kern<<<dim3(a.batch, ty, tz), Cfg::kThreads, Cfg::kSmemBytes + 64, st>>>(mA, mB, a);
+  *err = cudaGetLastError();
+  return true;
+}
+
 cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st) {
   if (a.m <= 0 || a.n <= 0 || a.batch <= 0) return cudaSuccess;
   static const bool log = getenv("HPS_GEMM_LOG") != nullptr;  // developer knob: shape trace for launch lists
@@ -80,6 +138,11 @@ cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st) {
   static const int seed_k = getenv("HPS_GEMM_SEED_K") ? atoi(getenv("HPS_GEMM_SEED_K")) : INT_MAX;
   GemmArgs b = a;
   b.seed_k_max = seed_k;
+  static const bool use_tma = getenv("HPS_GEMM_TMA") ? atoi(getenv("HPS_GEMM_TMA")) != 0 : true;
+  if (use_tma && cfg == 4) {  // TMA-staged operands (same tiles); falls back when a map is not legal
+    cudaError_t e = cudaSuccess;
+    if (launch_dgemm_tma(b, st, &e)) return e;
+  }
   return vec ? run_cfg<true>(cfg, b, st) : run_cfg<false>(cfg, b, st);
 }
 
