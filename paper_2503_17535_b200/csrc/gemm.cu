@@ -99,15 +99,15 @@ bool make_map(CUtensorMap* map, const double* base, long long rows, long long co
 }
 }  // namespace
 
-bool launch_dgemm_tma(const GemmArgs& a, cudaStream_t st, cudaError_t* err) {
-  constexpr int BM = 64, BN = 64, BK = 16, WM = 32, WN = 32, ST = 3;
+template <int BM, int BN, int BK, int WM, int WN, int ST>
+bool run_tma(const GemmArgs& a, cudaStream_t st, cudaError_t* err) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, ST, true>;
   if (a.k <= 0) return false;
   CUtensorMap mA, mB;
   if (!make_map(&mA, a.A, a.m, a.k, a.lda, a.sA, a.batch, BM + 4, BK)) return false;
   if (!make_map(&mB, a.B, a.k, a.n, a.ldb, a.sB, a.batch, BK + 4, BN)) return false;
   auto kern = dgemm_tma_kernel<BM, BN, BK, WM, WN, ST>;
-  static bool attr = false;
+  static bool attr = false;  // per instantiation
   if (!attr) {
     *err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes + 64);
     if (*err != cudaSuccess) return true;
@@ -119,6 +119,19 @@ bool launch_dgemm_tma(const GemmArgs& a, cudaStream_t st, cudaError_t* err) {
   kern<<<dim3(a.batch, ty, tz), Cfg::kThreads, Cfg::kSmemBytes + 64, st>>>(mA, mB, a);
   *err = cudaGetLastError();
   return true;
+}
+
+bool launch_dgemm_tma(const GemmArgs& a, cudaStream_t st, cudaError_t* err) {
+  static const int tcfg = getenv("HPS_TMA_CFG") ? atoi(getenv("HPS_TMA_CFG")) : 0;  // tuning knob
+  switch (tcfg) {
+    case 1: return run_tma<64, 64, 16, 32, 32, 4>(a, st, err);
+    case 2: return run_tma<64, 64, 32, 32, 32, 2>(a, st, err);
+    case 3: return run_tma<64, 64, 32, 32, 32, 3>(a, st, err);
+    case 4: return run_tma<128, 64, 16, 32, 32, 3>(a, st, err);
+    case 5: return run_tma<64, 128, 16, 32, 32, 3>(a, st, err);
+    case 6: return run_tma<128, 128, 16, 32, 32, 3>(a, st, err);
+    default: return run_tma<64, 64, 16, 32, 32, 3>(a, st, err);
+  }
 }
 
 cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st) {

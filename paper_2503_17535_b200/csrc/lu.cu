@@ -443,7 +443,11 @@ constexpr int kOuterNB = 256;
 
 // GEPP panel width: 32 columns, or 16 when the panel of a matrix beyond 16 CTAs x 864 rows would
 // not fit the cluster's shared memory (2D L=9 / 3D L=4 roots, n up to 27,648)
-int panel_width(int n) { return n > kMaxCluster * kMaxRowsPerCta ? kLuNB / 2 : kLuNB; }
+int panel_width(int n) {
+  static const int forced = getenv("HPS_PANEL_WIDTH") ? atoi(getenv("HPS_PANEL_WIDTH")) : 0;  // tuning knob
+  if (forced == kLuNB / 2 || (forced == kLuNB && n <= kMaxCluster * kMaxRowsPerCta)) return forced;
+  return n > kMaxCluster * kMaxRowsPerCta ? kLuNB / 2 : kLuNB;
+}
 
 // C[rows, cols] += alpha * A[rows, k] * B[k, cols] on sub-blocks of strided batches.
 cudaError_t gemm_sub(int batch, int rows, int cols, int k, double alpha, const double* A, long long lda, long long sA,
@@ -870,6 +874,9 @@ cudaError_t bgetrf_aug_lookahead(int batch, int n, int m, BatchedMat M, int* ipi
       HPS_TRY(cudaGetLastError());
     }
     // U12 = L11^-1 A12 over the block's row slab
+    if (n >= kSlabMinN && Jend < ncol && !getenv("HPS_NO_SLAB_TRSM")) {
+      HPS_TRY(slab_trsm<false>(batch, A, ld, sM, J, Jend - J, at(0, Jend), ld, sM, ncol - Jend, st));
+    } else
     for (int j0 = J; j0 < Jend && Jend < ncol; j0 += kLuNB) {
       const int nb = std::min(kLuNB, Jend - j0);
       Seg seg{at(0, Jend), ld, sM, ncol - Jend, 1};
@@ -908,7 +915,11 @@ cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double*
                        bool keep_L) {
   if (batch <= 0 || n <= 0) return cudaSuccess;
   if (n > bgetrf_max_n()) return cudaErrorInvalidValue;
-  if (n > 2 * kOuterNB && getenv("HPS_LU_LOOKAHEAD")) return bgetrf_aug_lookahead(batch, n, m, M, ipiv, stats, st, keep_L);
+  // look-ahead pays where several matrices share the GPU (merges below the root: measured d1 -3 ms,
+  // d2 -1 ms at L=8); the single root matrix is panel-latency bound either way
+  static const int la_env = getenv("HPS_LU_LOOKAHEAD") ? atoi(getenv("HPS_LU_LOOKAHEAD")) : -1;
+  const bool la = la_env < 0 ? (batch >= 2 && n > 2 * kOuterNB) : (la_env > 0 && n > 2 * kOuterNB);
+  if (la) return bgetrf_aug_lookahead(batch, n, m, M, ipiv, stats, st, keep_L);
   const long long ld = M.ld, sM = M.stride;
   double* A = M.p;
   auto at = [&](int r, int c) { return A + (long long)c * ld + r; };
