@@ -485,13 +485,17 @@ cudaError_t gemm_sub(int batch, int rows, int cols, int k, double alpha, const d
     }                                                                                   \
   } while (0)
 
-// ---- slab triangular solves on the tensor cores (n >= kSlabMinN) -------------------------
+// ---- slab triangular solves on the tensor cores (n >= slab_min_n()) -------------------------
 // A 256-row slab solve X_slab <- T_slab^-1 X_slab (T unit-lower L or upper U of one outer
 // block) as ONE launch instead of 8 x (32-column TRSM + k=32 GEMM): the inverses of the
 // slab's 32x32 diagonal blocks are formed first (one warp per block), then every CTA keeps a
 // 32-column strip of X in shared memory and runs the blocked substitution with DMMA:
 // X_b = T_bb^-1 X_b, then X_i -= T_ib X_b for the remaining blocks i of the slab.
-constexpr int kSlabMinN = 512;
+constexpr int kSlabMinNDefault = 512;
+int slab_min_n() {
+  static const int v = getenv("HPS_SLAB_MIN_N") ? atoi(getenv("HPS_SLAB_MIN_N")) : kSlabMinNDefault;  // tuning knob
+  return v;
+}
 constexpr int kSlabCW = 32;                 // strip width (4 warps x 8 columns)
 constexpr int kSlabLdX = kOuterNB + 4;      // 260 = 4 mod 16: conflict-free B fragments
 constexpr int kSlabChunk = 64;              // rows of T staged per update step
@@ -699,7 +703,7 @@ cudaError_t back_subst(int batch, int n, int m, const double* U, long long ldU, 
   for (int ob = nouter - 1; ob >= 0; --ob) {
     const int r0 = ob * kOuterNB, r1 = std::min(n, r0 + kOuterNB);
     const int nsub = (r1 - r0 + kLuNB - 1) / kLuNB;
-    if (n >= kSlabMinN && m >= kSlabCW && !getenv("HPS_NO_SLAB_TRSM")) {
+    if (n >= slab_min_n() && m >= kSlabCW && !getenv("HPS_NO_SLAB_TRSM")) {
       HPS_TRY(slab_trsm<true>(batch, U, ldU, strideU, r0, r1 - r0, R, ldR, strideR, m, st));
       HPS_TRY(gemm_sub(batch, r0, m, r1 - r0, -1.0, U + (long long)r0 * ldU, ldU, strideU, R + r0, ldR, strideR, R,
                        ldR, strideR, st));
@@ -874,7 +878,7 @@ cudaError_t bgetrf_aug_lookahead(int batch, int n, int m, BatchedMat M, int* ipi
       HPS_TRY(cudaGetLastError());
     }
     // U12 = L11^-1 A12 over the block's row slab
-    if (n >= kSlabMinN && Jend < ncol && !getenv("HPS_NO_SLAB_TRSM")) {
+    if (n >= slab_min_n() && Jend < ncol && !getenv("HPS_NO_SLAB_TRSM")) {
       HPS_TRY(slab_trsm<false>(batch, A, ld, sM, J, Jend - J, at(0, Jend), ld, sM, ncol - Jend, st));
     } else
     for (int j0 = J; j0 < Jend && Jend < ncol; j0 += kLuNB) {
@@ -941,7 +945,7 @@ cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double*
                        at(j0 + nb, j0 + nb), ld, sM, st));
     }
     // (2) U12 = L11^-1 A12 over the outer block's row slab (blocked forward substitution)
-    if (n >= kSlabMinN && Jend < ncol && !getenv("HPS_NO_SLAB_TRSM")) {
+    if (n >= slab_min_n() && Jend < ncol && !getenv("HPS_NO_SLAB_TRSM")) {
       HPS_TRY(slab_trsm<false>(batch, A, ld, sM, J, Jend - J, at(0, Jend), ld, sM, ncol - Jend, st));
     } else
     for (int j0 = J; j0 < Jend && Jend < ncol; j0 += kLuNB) {
@@ -994,7 +998,7 @@ cudaError_t bgetrs(int batch, int n, int m, BatchedMat LU, const int* ipiv, Batc
   const double* L = LU.p;
   for (int J = 0; J < n; J += kOuterNB) {
     const int Jend = std::min(n, J + kOuterNB);
-    if (n >= kSlabMinN && m >= kSlabCW && !getenv("HPS_NO_SLAB_TRSM")) {
+    if (n >= slab_min_n() && m >= kSlabCW && !getenv("HPS_NO_SLAB_TRSM")) {
       HPS_TRY(slab_trsm<false>(batch, L, LU.ld, LU.stride, J, Jend - J, R.p, R.ld, R.stride, m, st));
     } else
     for (int j0 = J; j0 < Jend; j0 += kLuNB) {
