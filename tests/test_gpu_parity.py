@@ -199,11 +199,12 @@ def test_3d_variable_poisson_parity(p, L, literal):
         assert PR.rel_linf(s.solve(g), prob.exact(s.leaf_points())) < (1e-5 if L == 2 else 1e-6)
 
 
-def test_lookahead_lu_matches_default(monkeypatch):
-    """The opt-in look-ahead LU driver (side-stream panels, deferred block swaps) gives the same merge."""
+def test_lookahead_lu_matches_plain(monkeypatch):
+    """The look-ahead LU driver (default for n > 512: side-stream panels, deferred block swaps)
+    and the plain blocked driver give the same merges."""
     prob = PR.helmholtz_bumps()
     a = gpu_solver(prob, 16, 5, root_implicit=True)       # root D = 1792 > 512: both drivers apply
-    monkeypatch.setenv("HPS_LU_LOOKAHEAD", "1")
+    monkeypatch.setenv("HPS_LU_LOOKAHEAD", "0")
     b = gpu_solver(prob, 16, 5, root_implicit=True)
     g = prob.boundary(a.root_boundary_points())
     assert rel(b.solve(g), a.solve(g)) < 1e-12
