@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "gemm.cuh"
+#include "gemv.cuh"
 #include "lu.cuh"
 
 namespace hpsk {
@@ -962,6 +963,108 @@ cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double*
   return back_subst(batch, n, m, A, ld, sM, at(0, n), ld, sM, st);
 }
 
+// ---- single-matrix, few-RHS triangular solves (the implicit-root solve: n = 7168, 1 RHS) --------
+// Per 256-row slab: ONE CTA solves the slab (its eight 32x32 diagonal blocks one warp per RHS
+// with shuffle broadcasts, the in-slab updates by the whole CTA), then one streaming GEMV applies
+// the slab to every remaining row.  2 launches per slab instead of ~17.
+constexpr int kTrsvMaxRhs = 4;
+
+template <bool UPPER>
+__global__ void __launch_bounds__(256) slab_trsv_kernel(const double* T, long long ldT, int r0, int nbk, double* X,
+                                                         long long ldX, int m) {
+  // dynamic smem: tb[kLuNB][kOuterNB] (the sub-block's column block of the slab, all rows)
+  extern __shared__ __align__(16) double tb[];
+  __shared__ double xs[kTrsvMaxRhs][kOuterNB];
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < kTrsvMaxRhs * kOuterNB; e += 256) {
+    const int c = e / kOuterNB, r = e % kOuterNB;
+    xs[c][r] = (c < m && r < nbk) ? X[(long long)c * ldX + r0 + r] : 0.0;
+  }
+  const int nblk = (nbk + kLuNB - 1) / kLuNB;
+  for (int step = 0; step < nblk; ++step) {
+    const int bk = UPPER ? nblk - 1 - step : step;
+    const int s0 = bk * kLuNB, nb = min(kLuNB, nbk - s0);
+    const int ra = UPPER ? 0 : s0, rb = UPPER ? s0 + nb : nbk;  // rows touched: diag block + rest
+    __syncthreads();
+    // stage T[r0 + ra .. r0 + rb, r0 + s0 .. + nb) (column-major in tb: tb[k * kOuterNB + r])
+    for (int e = tid; e < kLuNB * kOuterNB; e += 256) {
+      const int k = e / kOuterNB, r = e % kOuterNB;
+      if (r >= ra && r < rb && k < nb) tb[e] = T[(long long)(r0 + s0 + k) * ldT + r0 + r];
+    }
+    __syncthreads();
+    if (w < m) {
+      double x = xs[w][s0 + lane < nbk ? s0 + lane : 0];
+      if (!UPPER) {
+        for (int k = 0; k < nb; ++k) {
+          const double xk = __shfl_sync(0xffffffffu, x, k);
+          if (lane > k && lane < nb) x -= tb[k * kOuterNB + s0 + lane] * xk;
+        }
+      } else {
+        for (int k = nb - 1; k >= 0; --k) {
+          if (lane == k) x /= tb[k * kOuterNB + s0 + k];
+          const double xk = __shfl_sync(0xffffffffu, x, k);
+          if (lane < k) x -= tb[k * kOuterNB + s0 + lane] * xk;
+        }
+      }
+      if (lane < nb) xs[w][s0 + lane] = x;
+    }
+    __syncthreads();
+    const int ua = UPPER ? 0 : s0 + nb, ub = UPPER ? s0 : nbk;
+    for (int r = ua + tid; r < ub; r += 256) {
+      double acc[kTrsvMaxRhs] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+      for (int k = 0; k < nb; ++k) {
+        const double t = tb[k * kOuterNB + r];
+#pragma unroll
+        for (int c = 0; c < kTrsvMaxRhs; ++c) acc[c] += t * xs[c][s0 + k];
+      }
+#pragma unroll
+      for (int c = 0; c < kTrsvMaxRhs; ++c)
+        if (c < m) xs[c][r] -= acc[c];
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < kTrsvMaxRhs * kOuterNB; e += 256) {
+    const int c = e / kOuterNB, r = e % kOuterNB;
+    if (c < m && r < nbk) X[(long long)c * ldX + r0 + r] = xs[c][r];
+  }
+}
+
+// X <- T^-1 X for one matrix (unit-lower L or upper U of an LU), m <= kTrsvMaxRhs
+template <bool UPPER>
+cudaError_t trsv_blocked(const double* T, long long ldT, int n, double* X, long long ldX, int m, cudaStream_t st) {
+  static double* scratch = nullptr;
+  const size_t scratch_elems = size_t(1) << 20;
+  if (!scratch) HPS_TRY(cudaMalloc(&scratch, scratch_elems * sizeof(double)));
+  const int nouter = (n + kOuterNB - 1) / kOuterNB;
+  for (int s = 0; s < nouter; ++s) {
+    const int ob = UPPER ? nouter - 1 - s : s;
+    const int J = ob * kOuterNB, Jend = std::min(n, J + kOuterNB);
+    const size_t smem = (size_t)kLuNB * kOuterNB * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      HPS_TRY(cudaFuncSetAttribute(slab_trsv_kernel<UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    slab_trsv_kernel<UPPER><<<1, 256, smem, st>>>(T, ldT, J, Jend - J, X, ldX, m);
+    HPS_TRY(cudaGetLastError());
+    GemvArgs g;  // the rows outside the slab: X_rest -= T[rest, J:Jend] X_slab
+    g.m = UPPER ? J : n - Jend;
+    g.k = Jend - J;
+    g.nv = m;
+    g.A = T + (long long)J * ldT + (UPPER ? 0 : Jend);
+    g.lda = ldT;
+    g.x = X + J;
+    g.ldx = ldX;
+    g.y = X + (UPPER ? 0 : Jend);
+    g.ldy = ldX;
+    g.alpha = -1.0;
+    g.beta = 1.0;
+    if (g.m > 0) HPS_TRY(launch_gemv(g, scratch, scratch_elems, st, nullptr));
+  }
+  return cudaSuccess;
+}
+
 cudaError_t bgetrs(int batch, int n, int m, BatchedMat LU, const int* ipiv, BatchedMat R, cudaStream_t st) {
   if (batch <= 0 || n <= 0 || m <= 0) return cudaSuccess;
   if ((size_t)n * 12 <= 200 * 1024) {
@@ -996,6 +1099,10 @@ cudaError_t bgetrs(int batch, int n, int m, BatchedMat LU, const int* ipiv, Batc
     HPS_TRY(cudaGetLastError());
   }
   const double* L = LU.p;
+  if (batch == 1 && m <= kTrsvMaxRhs && n >= 1024 && !getenv("HPS_NO_BLOCK_TRSV")) {
+    HPS_TRY(trsv_blocked<false>(L, LU.ld, n, R.p, R.ld, m, st));
+    return trsv_blocked<true>(L, LU.ld, n, R.p, R.ld, m, st);
+  }
   for (int J = 0; J < n; J += kOuterNB) {
     const int Jend = std::min(n, J + kOuterNB);
     if (n >= slab_min_n() && m >= kSlabCW && !getenv("HPS_NO_SLAB_TRSM")) {
