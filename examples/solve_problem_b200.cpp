@@ -19,6 +19,9 @@ int main(int argc, char** argv) {
   const int L = argc > 1 ? std::atoi(argv[1]) : 3;
   const int p = argc > 2 ? std::atoi(argv[2]) : 16;
   const bool literal = argc > 3 ? std::atoi(argv[3]) != 0 : false;
+  // 4th argument 1: build WITHOUT the source, then solve through solve_new_source (the
+  // repeated-source path, solver.cpp:285-307) with the manufactured source sampled per leaf
+  const bool new_source = argc > 4 ? std::atoi(argv[4]) != 0 : false;
   try {
     Box dom;
     dom.lo[0] = dom.lo[1] = -1.0;
@@ -43,17 +46,32 @@ int main(int argc, char** argv) {
     };
     SolverOptions opts;
     opts.literal_sign = literal;
-    HpsSolver solver(tree, Variant::dtn, 1.0, terms, f, opts);
+    opts.keep_factors = new_source;
+    HpsSolver solver(tree, Variant::dtn, 1.0, terms, new_source ? std::function<Real(const Point&)>() : f, opts);
     const auto t1 = std::chrono::steady_clock::now();
     solver.build();
     const auto t2 = std::chrono::steady_clock::now();
     const std::vector<Real> g = solver.sample_root_data(u);
-    SolutionField field = solver.solve(g);
-    const auto t3 = std::chrono::steady_clock::now();
-    // error_report (proj/src/problems.cpp:270-293) at the leaf Chebyshev points
     hpsg_tree t{tree.dim, tree.p, tree.L, dom.lo[0], dom.hi[0]};
     std::vector<double> xyz(size_t(tree.total_points()) * 3);
     hpsg_tree_leaf_points(&t, xyz.data());
+    SolutionField field;
+    if (new_source) {
+      const int np = p * p;
+      std::vector<std::vector<Real>> leaf_f(size_t(tree.n_leaves()), std::vector<Real>(size_t(np)));
+      for (long long l = 0; l < tree.n_leaves(); ++l)
+        for (int i = 0; i < np; ++i) {
+          Point x;
+          const size_t k = size_t(l * np + i);
+          x[0] = xyz[3 * k], x[1] = xyz[3 * k + 1];
+          leaf_f[size_t(l)][size_t(i)] = f(x);
+        }
+      field = solver.solve_new_source(leaf_f, RootBC::dirichlet, &g);
+    } else {
+      field = solver.solve(g);
+    }
+    const auto t3 = std::chrono::steady_clock::now();
+    // error_report (proj/src/problems.cpp:270-293) at the leaf Chebyshev points
     double num = 0, den = 0;
     const int npts = p * p;
     for (long long l = 0; l < tree.n_leaves(); ++l)

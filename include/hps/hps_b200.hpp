@@ -15,6 +15,7 @@
 // where a matrix is meant).  Link with -lhps_b200.
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cstdint>
 #include <functional>
@@ -94,8 +95,12 @@ struct SolverOptions {
   bool free_T_after_merge = false;
   bool quiet_warnings = false;
   bool literal_sign = true;       // reference v_i = -L_ii^-1 f_i (local_solve.cpp:137)
+  bool keep_factors = false;      // keep the leaf LU factors (LeafSolution::fac) for solve_new_source
   int device = 0;
 };
+
+// proj/include/hps/solver.hpp:30-32
+enum class RootBC { dirichlet, radiation };
 
 // proj/include/hps/solver.hpp:24-28
 struct SolutionField {
@@ -149,6 +154,7 @@ class HpsSolver {
     o.literal_sign = opts.literal_sign ? 1 : 0;
     o.root_implicit_S = opts.root_implicit_S ? 1 : 0;
     o.device = opts.device;
+    o.keep_factors = opts.keep_factors ? 1 : 0;
     const int rc = hpsg_create(&t, ct.data(), int(ct.size()), srcp, &o, &ctx_);
     if (rc != HPSG_OK) {
       const std::string msg = ctx_ ? hpsg_last_error(ctx_) : "no CUDA device";
@@ -198,6 +204,28 @@ class HpsSolver {
       for (long long l = 0; l < nl; ++l) (*leaf_g_out)[size_t(l)].assign(lg.begin() + l * nbl, lg.begin() + (l + 1) * nbl);
     }
     return f;
+  }
+
+  // proj/include/hps/solver.hpp:71-72 / solver.cpp:285-307: same operator, new source (per-leaf
+  // samples at the Chebyshev points), explicit root data; needs SolverOptions::keep_factors
+  SolutionField solve_new_source(const std::vector<std::vector<Real>>& leaf_f, RootBC root_bc,
+                                 const std::vector<Real>* g_root = nullptr) const {
+    if (root_bc != RootBC::dirichlet) throw Error("solve_new_source: radiation closure is not on this path");
+    if (!g_root) throw Error("solve_new_source: boundary data required");
+    const long long nl = tree_->n_leaves();
+    const int npts = tree_->dim == 2 ? tree_->p * tree_->p : tree_->p * tree_->p * tree_->p;
+    if ((long long)leaf_f.size() != nl) throw Error("make_source_state: wrong leaf count");
+    std::vector<double> f(size_t(nl) * npts), u(size_t(nl) * npts);
+    for (long long l = 0; l < nl; ++l) {
+      if ((int)leaf_f[size_t(l)].size() != npts) throw Error("make_source_state: wrong leaf sample count");
+      std::copy(leaf_f[size_t(l)].begin(), leaf_f[size_t(l)].end(), f.begin() + l * npts);
+    }
+    check(hpsg_solve_new_source(ctx_, f.data(), g_root->data(), 1, u.data()));
+    SolutionField out;
+    out.tree = tree_;
+    out.u.resize(size_t(nl));
+    for (long long l = 0; l < nl; ++l) out.u[size_t(l)].assign(u.begin() + l * npts, u.begin() + (l + 1) * npts);
+    return out;
   }
 
   int top_D_size() const {

@@ -176,13 +176,15 @@ def test_cpp_dropin_example_runs():
     import subprocess
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     exe = os.path.join(root, "examples", "solve_problem_b200")
-    if not os.path.exists(exe):
+    src = os.path.join(root, "examples", "solve_problem_b200.cpp")
+    if not os.path.exists(exe) or os.path.getmtime(exe) < os.path.getmtime(src):
         subprocess.run(["make", "-s", "-C", os.path.join(root, "paper_2503_17535_b200"), "example"], check=True)
-    r = subprocess.run([exe, "3", "16", "0"], capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0, r.stderr
-    rep = json.loads(r.stdout)
-    assert rep["N"] == 16384 and rep["top_D"] == 4 * 14 * 4
-    assert rep["rel_linf"] < 1e-8
+    for new_source in ("0", "1"):  # solve(), and solve_new_source() on a source-free build
+        r = subprocess.run([exe, "3", "16", "0", new_source], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        rep = json.loads(r.stdout)
+        assert rep["N"] == 16384 and rep["top_D"] == 4 * 14 * 4
+        assert rep["rel_linf"] < 1e-8
 
 
 @pytest.mark.parametrize("p,L,literal", [(6, 2, True), (8, 2, False), (8, 3, False)])
