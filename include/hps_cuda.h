@@ -82,7 +82,11 @@ typedef struct {
   int device;           /* CUDA device ordinal */
   int keep_factors;     /* keep the leaf LU factors for hpsg_solve_new_source (LeafSolution::fac,
                            local_solve.hpp:36); 2D p=16 L=8: +20 GB, batched leaf path */
+  int variant;          /* HPSG_VARIANT_DTN (HpsSolver<Real>) or HPSG_VARIANT_ITI (HpsSolver<Complex>,
+                           2D impedance-to-impedance maps, spectral.hpp:87) */
+  double eta;           /* ItI impedance parameter (HpsSolver ctor eta, solver.hpp:43) */
 } hpsg_options;
+enum { HPSG_VARIANT_DTN = 0, HPSG_VARIANT_ITI = 1 };
 
 typedef struct {
   int n_leaves;
@@ -142,6 +146,11 @@ int hpsg_part_solve_cut(hpsg_ctx* ctx, const double* d_g_root, int nrhs, double*
 int hpsg_solve(hpsg_ctx* ctx, const double* g_root, int nrhs, double* u_out, double* leaf_g_out);
 /* same with device pointers (no host copies); results are ready when the call returns */
 int hpsg_solve_device(hpsg_ctx* ctx, const double* d_g_root, int nrhs, double* d_u_out);
+/* ItI variant: HpsSolver<Complex>::solve(g_root) (solver.cpp:238-252) with complex data as
+ * interleaved (re, im) doubles: g_root nrhs x root_bsize incoming impedance data at the root
+ * boundary Gauss points, u_out nrhs x n_leaves x p^2.  Internally every complex matrix is carried
+ * in real-equivalent form [[re, -im], [im, re]]. */
+int hpsg_solve_complex(hpsg_ctx* ctx, const double* g_root, int nrhs, double* u_out);
 /* HpsSolver::solve_new_source(leaf_f, RootBC::dirichlet, g_root), solver.hpp:71-72 /
  * solver.cpp:285-307 (make_source_state :261-283, leaf_resolve_source local_solve.cpp:174-183,
  * artifact_source_pass merge.cpp:514-567), for nsrc sources at once against the stored build:

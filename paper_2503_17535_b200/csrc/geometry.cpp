@@ -467,6 +467,178 @@ void collect(double lo[3], double hi[3], int dim, int face, int levels, int q, c
 }
 }  // namespace
 
+// ---- ItI --------------------------------------------------------------------------------------
+namespace {
+// side2d (spectral.cpp:172-188): normal axis, outward sign, fixed Chebyshev node
+void side2d(int s, int p, int& axis, double& sign, int& fixed) {
+  switch (s) {
+    case 0: axis = 1, sign = -1.0, fixed = p - 1; break;
+    case 1: axis = 0, sign = +1.0, fixed = 0; break;
+    case 2: axis = 1, sign = +1.0, fixed = 0; break;
+    default: axis = 0, sign = -1.0, fixed = p - 1; break;
+  }
+}
+// normal_row_2d (spectral.cpp:204-211)
+void normal_row(int s, int run, int p, const HostMat& d1, HostMat& mat, int row) {
+  int axis, fixed;
+  double sign;
+  side2d(s, p, axis, sign, fixed);
+  for (int k = 0; k < p; ++k) {
+    const int col = axis == 0 ? k * p + run : run * p + k;
+    mat(row, col) += sign * d1(fixed, k);
+  }
+}
+// walk_tensor_idx (spectral.cpp:224-227)
+int walk_idx(int s, int run, int p) {
+  int axis, fixed;
+  double sign;
+  side2d(s, p, axis, sign, fixed);
+  return axis == 0 ? fixed * p + run : run * p + fixed;
+}
+}  // namespace
+
+ItiLeafOperators make_iti_leaf_operators(int p, double eta, double side) {
+  if (p < 4) throw std::runtime_error("assemble_iti_ops_2d: p must be >= 4");
+  if (!(eta > 0.0)) throw std::runtime_error("assemble_iti_ops_2d: eta must be positive");
+  ItiLeafOperators op;
+  op.p = p;
+  op.q = p - 2;
+  op.n = p * p;
+  op.nbc = 4 * p - 4;
+  op.nb = 4 * op.q;
+  op.eta = eta;
+  op.side = side;
+  for (int idx = 0; idx < op.n; ++idx) {
+    const int i1 = idx / p, i2 = idx % p;
+    if (i1 > 0 && i1 < p - 1 && i2 > 0 && i2 < p - 1) op.interior.push_back(idx);
+  }
+  op.ni = int(op.interior.size());
+  const int q = op.q;
+  const std::vector<double> cn = cheb_nodes(p);
+  std::vector<double> gx, gw;
+  gauss_rule(q, gx, gw);
+  const HostMat d1 = cheb_diff(p);
+  const double dscale = 2.0 / side;
+  const std::vector<double> cheb_asc(cn.rbegin(), cn.rend());
+  const HostMat c2g = bary_interp(cheb_asc, gx);  // q x p
+  // N and the sampling rows on the 4p double-counted layout (spectral.cpp:333-342)
+  HostMat N(4 * p, op.n), samp(4 * p, op.n);
+  for (int s = 0; s < 4; ++s)
+    for (int r = 0; r < p; ++r) {
+      const int run = p - 1 - r;
+      normal_row(s, run, p, d1, N, s * p + r);
+      samp(s * p + r, walk_idx(s, run, p)) = 1.0;
+    }
+  // the 4p-4 walk (iti_walk, spectral.cpp:214-222): Ntilde, G = Ntilde + i eta samp_walk, P
+  std::vector<std::pair<int, int>> walk;
+  for (int i1 = p - 1; i1 >= 1; --i1) walk.emplace_back(0, i1);
+  for (int i2 = p - 1; i2 >= 1; --i2) walk.emplace_back(1, i2);
+  for (int i1 = 0; i1 <= p - 2; ++i1) walk.emplace_back(2, i1);
+  for (int i2 = 0; i2 <= p - 2; ++i2) walk.emplace_back(3, i2);
+  op.Gr = HostMat(op.nbc, op.n);
+  op.Gi = HostMat(op.nbc, op.n);
+  op.P = HostMat(op.nbc, op.nb);
+  for (int r = 0; r < op.nbc; ++r) {
+    const int s = walk[r].first, run = walk[r].second;
+    normal_row(s, run, p, d1, op.Gr, r);
+    op.Gi(r, walk_idx(s, run, p)) = eta;
+    const HostMat row = bary_interp(gx, {cn[run]});
+    for (int j = 0; j < q; ++j) op.P(r, s * q + j) = row(0, j);
+  }
+  for (double& v : op.Gr.a) v *= dscale;
+  // QH = Q (N dscale - i eta samp), Q block-diagonal per side (spectral.cpp:362-366)
+  op.QHr = HostMat(op.nb, op.n);
+  op.QHi = HostMat(op.nb, op.n);
+  for (int s = 0; s < 4; ++s)
+    for (int i = 0; i < q; ++i)
+      for (int j = 0; j < op.n; ++j) {
+        double nr = 0.0, ni = 0.0;
+        for (int r = 0; r < p; ++r) {
+          nr += c2g(i, r) * N(s * p + r, j);
+          ni += c2g(i, r) * samp(s * p + r, j);
+        }
+        op.QHr(s * q + i, j) = dscale * nr;
+        op.QHi(s * q + i, j) = -eta * ni;
+      }
+  return op;
+}
+
+ItiMergeTables make_iti_merge_tables(int s) {
+  const MergeTables g = make_merge_tables(2, s);  // exterior sections and interface ids (MergeGeom)
+  ItiMergeTables t;
+  t.s = s;
+  const int nint_c = 8 * s, next_c = 8 * s, nbc_c = 4 * s;
+  t.n_int = 2 * nint_c;
+  t.n_ext = 2 * next_c;
+  t.child_nb = 2 * nbc_c;
+  auto ext_off = [&](int c, int f) { const int v = g.sec[c * 4 + f]; return v >= 0 ? v * s : -1; };
+  // slots grouped {a, c} then {b, d}, each child's interfaces by id (merge.cpp:351-375)
+  int slot_off[4][4];
+  for (auto& r : slot_off)
+    for (int& v : r) v = -1;
+  struct Slot { int k, of, nb, nbf, off; };
+  std::vector<Slot> slots;
+  const auto& ifs = ifaces(2);
+  int pos = 0;
+  for (int k : {0, 2, 1, 3})
+    for (size_t i = 0; i < ifs.size(); ++i) {
+      int of, nb, nbf;
+      if (ifs[i].clo == k) {
+        of = ifs[i].flo, nb = ifs[i].chi, nbf = ifs[i].fhi;
+      } else if (ifs[i].chi == k) {
+        of = ifs[i].fhi, nb = ifs[i].clo, nbf = ifs[i].flo;
+      } else {
+        continue;
+      }
+      slots.push_back({k, of, nb, nbf, pos});
+      slot_off[k][of] = pos;
+      pos += s;
+    }
+  // complex block (matrix dst, rows at complex offset r, cols at complex offset c of a complex
+  // R x C matrix placed at real column base cb) <- child k's T block (faces rf, cf) or h (rf)
+  auto tblock = [&](int dst, int R, int C, int cb, int r, int c, int k, int rf, int cf) {
+    for (int qr = 0; qr < 2; ++qr)
+      for (int qc = 0; qc < 2; ++qc)
+        t.blocks.push_back({dst, qr * R + r, cb + qc * C + c, k, qr * nbc_c + rf * s, 1 + qc * nbc_c + cf * s, s, s});
+  };
+  auto hblock = [&](int dst, int R, int col, int r, int k, int rf) {
+    for (int qr = 0; qr < 2; ++qr) t.blocks.push_back({dst, qr * R + r, col, k, qr * nbc_c + rf * s, 0, s, 1});
+  };
+  // exterior rows: h_ext, A, B from each child's exterior faces (merge.cpp:386-415)
+  for (int k = 0; k < 4; ++k)
+    for (int rf = 0; rf < 4; ++rf) {
+      const int roff = ext_off(k, rf);
+      if (roff < 0) continue;
+      hblock(2, next_c, 0, roff, k, rf);
+      for (int cf = 0; cf < 4; ++cf) {
+        if (ext_off(k, cf) >= 0)
+          tblock(2, next_c, next_c, 1, roff, ext_off(k, cf), k, rf, cf);  // A in [h_ext | A]
+        else
+          tblock(1, next_c, nint_c, 0, roff, slot_off[k][cf], k, rf, cf);  // B
+      }
+    }
+  // interface rows: g_owner + neighbour's outgoing data = 0 (merge.cpp:417-447)
+  for (const Slot& sl : slots) {
+    hblock(0, nint_c, 2 * nint_c, sl.off, sl.nb, sl.nbf);  // h_int column of [D | h_int | C]
+    for (int qr = 0; qr < 2; ++qr) t.blocks.push_back({0, qr * nint_c + sl.off, qr * nint_c + sl.off, -1, 0, 0, s, s});
+    for (int cf = 0; cf < 4; ++cf) {
+      if (ext_off(sl.nb, cf) >= 0)
+        tblock(0, nint_c, next_c, 2 * nint_c + 1, sl.off, ext_off(sl.nb, cf), sl.nb, sl.nbf, cf);  // C
+      else
+        tblock(0, nint_c, nint_c, 0, sl.off, slot_off[sl.nb][cf], sl.nb, sl.nbf, cf);  // D
+    }
+  }
+  // downward scatter per (child, real-equivalent face): real parts then imaginary parts
+  t.down.assign(4 * 8, 0);
+  for (int c = 0; c < 4; ++c)
+    for (int f = 0; f < 4; ++f) {
+      const int e = ext_off(c, f);
+      t.down[c * 8 + f] = e >= 0 ? e : -(slot_off[c][f]) - 1;
+      t.down[c * 8 + 4 + f] = e >= 0 ? next_c + e : -(nint_c + slot_off[c][f]) - 1;
+    }
+  return t;
+}
+
 std::vector<double> root_boundary_points(const UniformTree& t) {
   std::vector<double> gx, gw, out;
   gauss_rule(t.q, gx, gw);

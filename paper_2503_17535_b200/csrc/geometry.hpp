@@ -95,6 +95,40 @@ struct MergeTables {
 };
 MergeTables make_merge_tables(int dim, int s);
 
+// ---- ItI (impedance-to-impedance) variant, 2D ------------------------------
+// Leaf operators of assemble_iti_ops_2d (proj/src/spectral.cpp:312-368): the 4p-4 boundary walk
+// rows G = Ntilde + i eta I_walk, the Gauss interpolation P (walk x 4q) and QH = Q (N - i eta I)
+// (4q x p^2).  Complex matrices are held as (re, im) pairs.
+struct ItiLeafOperators {
+  int p = 0, q = 0, n = 0, ni = 0, nbc = 0, nb = 0;  // p^2, (p-2)^2, 4p-4, 4q
+  double eta = 0, side = 0;
+  std::vector<int> interior;   // tensor indices, increasing
+  HostMat Gr, Gi;              // nbc x n
+  HostMat P;                   // nbc x nb
+  HostMat QHr, QHi;            // nb x n
+};
+ItiLeafOperators make_iti_leaf_operators(int p, double eta, double side);
+
+// merge_iti (proj/src/merge.cpp:338-482) as block copies into the REAL-EQUIVALENT merge
+// matrices: a complex matrix Z = Zr + i Zi is stored as [[Zr, -Zi], [Zi, Zr]] and a vector as
+// [zr; zi], so the DtN LU / GEMM / downward machinery applies unchanged.  Every complex s x s
+// block copy becomes the 4 quadrant copies of the child's real-equivalent [h|T].
+struct BlockCopy {
+  int dst;      // 0: MD = [D | h_int | C], 1: B, 2: AH = [h_ext | A]
+  int dr, dc;   // destination offset (real-equivalent rows / columns of that matrix)
+  int child;    // source child, or -1: identity block (rows == cols)
+  int sr, sc;   // source offset in the child's [h | T] (column 0 = h)
+  int rows, cols;
+};
+struct ItiMergeTables {
+  int s = 0;                    // complex points per child face
+  int n_int = 0, n_ext = 0;     // real-equivalent sizes (2 x 8s each)
+  int child_nb = 0;             // real-equivalent child boundary size (2 x 4s)
+  std::vector<BlockCopy> blocks;
+  std::vector<int> down;        // 4 children x 8 real-equivalent faces (scatter table of the solve)
+};
+ItiMergeTables make_iti_merge_tables(int s);
+
 // Root boundary points in the reference's canonical section order
 // (HpsSolver::root_boundary_points, proj/src/solver.cpp:159-182).
 std::vector<double> root_boundary_points(const UniformTree& t);  // nb_root x 3

@@ -96,6 +96,9 @@ struct Level {
   // block-sparse Schur product: exterior section e only couples to the interfaces of its own
   // child (B_{e,i} = 0 otherwise), as contiguous interface runs {e, first interface, count}
   std::vector<std::array<int, 3>> schur_runs;
+  hpsg::ItiMergeTables it;  // ItI variant: block copies + real-equivalent scatter table
+  DevBuf iblocks;
+  int iti_nblocks = 0;
   long long strideMD() const { return (long long)n_int * (n_int + 1 + n_ext); }
   long long strideAH() const { return (long long)n_ext * (1 + n_ext); }
 };
@@ -111,6 +114,9 @@ struct hpsg_ctx {
   cudaEvent_t lev_ev[25] = {};  // merge level boundaries
   hpsg_tree tree{};
   hpsg_part part{};  // (0, 0, L) for the whole tree
+  bool iti = false;  // ItI variant (real-equivalent complex)
+  hpsg::ItiLeafOperators iops;
+  DevBuf iGr, iGi, iP, iQHs;
   hpsg_options opts{};
   hpsg::UniformTree T;
   hpsg::LeafOperators ops;
@@ -249,6 +255,8 @@ double counted_build_flops(const hpsg_ctx* c) {
   double f = c->T.cut ? 0.0
                       : c->T.n_leaves() * (2.0 / 3.0 * ni * ni * ni + 2 * ni * ni * ne + 2 * ni * ne * nb +
                                            2 * nb * n * nb + 2 * ni * ni + 2 * nb * n);
+  if (c->iti)  // real-equivalent leaf system: LU of 2n, 1 + 2nb right-hand sides, [h|T] = QH [v|Y]
+    f = c->T.n_leaves() * (2.0 / 3.0 * ni * ni * ni + 2 * ni * ni * (1 + nb) + 2 * nb * ni * (1 + nb));
   for (const Level& L : c->lv) {
     const double a = L.n_int, e = L.n_ext;
     double per;
@@ -272,6 +280,19 @@ void setup(hpsg_ctx* c) {
   c->T = hpsg::make_part_tree(t.dim, t.p, t.L, t.lo, t.hi, c->part.root_depth, c->part.root_index,
                               c->part.cut_depth);
   c->ops = hpsg::make_leaf_operators(t.dim, t.p, c->T.leaf_side);
+  c->iti = c->opts.variant == HPSG_VARIANT_ITI;
+  if (c->opts.variant != HPSG_VARIANT_DTN && !c->iti) throw HpsError{HPSG_ERR_INVALID, "hpsg_create: unknown variant"};
+  if (c->iti) {
+    if (t.dim != 2) throw HpsError{HPSG_ERR_INVALID, "local_solve_iti: 2D only"};
+    if (c->opts.root_implicit_S) throw HpsError{HPSG_ERR_INVALID, "merge_iti: implicit S is not supported"};
+    if (c->T.cut || c->T.root_depth) throw HpsError{HPSG_ERR_INVALID, "ItI: tree parts are not supported"};
+    if (c->opts.keep_factors) throw HpsError{HPSG_ERR_INVALID, "ItI: solve_new_source is not on this path"};
+    c->iops = hpsg::make_iti_leaf_operators(t.p, c->opts.eta, c->T.leaf_side);
+    // the generic leaf/solve code sees the real-equivalent leaf system: 2n rows, 2 x 4q boundary
+    c->ops.ni = 2 * c->iops.n;
+    c->ops.nb = 2 * c->iops.nb;
+    c->ops.ne = 0;
+  }
   const hpsg::LeafOperators& o = c->ops;
   const int nl = c->T.n_leaves();
   const int q = o.q;
@@ -288,6 +309,24 @@ void setup(hpsg_ctx* c) {
   for (int j = 0; j < o.nb; ++j)
     for (int i = 0; i < o.nb; ++i) zq[size_t(1 + j) * o.nb + i] = o.QeP(i, j);
   upload(c->ZQeP, zq, &c->dev_bytes, st);
+  if (c->iti) {
+    const hpsg::ItiLeafOperators& io = c->iops;
+    upload(c->iGr, io.Gr.a, &c->dev_bytes, st);
+    upload(c->iGi, io.Gi.a, &c->dev_bytes, st);
+    upload(c->iP, io.P.a, &c->dev_bytes, st);
+    // QH in real-equivalent form (2 nb x 2n): [[QHr, -QHi], [QHi, QHr]]
+    const int nb = io.nb, n = io.n;
+    std::vector<double> qh(size_t(2 * nb) * 2 * n, 0.0);
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < nb; ++i) {
+        const double r = io.QHr(i, j), im = io.QHi(i, j);
+        qh[size_t(j) * 2 * nb + i] = r;
+        qh[size_t(j) * 2 * nb + nb + i] = im;
+        qh[size_t(n + j) * 2 * nb + i] = -im;
+        qh[size_t(n + j) * 2 * nb + nb + i] = r;
+      }
+    upload(c->iQHs, qh, &c->dev_bytes, st);
+  }
 
   // merge levels: child face size s_d = q * 2^(L-1-d) (2D) / q^2 * 4^(L-1-d) (3D)
   c->lv.resize(c->T.L);
@@ -301,10 +340,26 @@ void setup(hpsg_ctx* c) {
     L.n_int = L.mt.n_int();
     L.n_ext = L.mt.n_ext();
     L.child_nb = L.mt.child_nb();
+    if (c->iti) {
+      L.it = hpsg::make_iti_merge_tables(s);
+      L.n_int = L.it.n_int;
+      L.n_ext = L.it.n_ext;
+      L.child_nb = L.it.child_nb;
+      L.mt.nface = 8;  // real-equivalent child faces for the scatter (re parts, then im parts)
+      L.mt.down = L.it.down;
+      std::vector<hpsk::DevBlockCopy> bl;  // the root forms no T/h: its list keeps the MD blocks only
+      for (const auto& b : L.it.blocks)
+        if (!(d == 0 && c->T.root_depth == 0) || b.dst == 0)
+          bl.push_back({b.dst, b.dr, b.dc, b.child, b.sr, b.sc, b.rows, b.cols});
+      L.iti_nblocks = int(bl.size());
+      std::vector<int> raw(bl.size() * 8);
+      std::memcpy(raw.data(), bl.data(), raw.size() * sizeof(int));
+      upload(L.iblocks, raw, &c->dev_bytes, st);
+    }
     if (L.n_int > hpsk::bgetrf_max_n())
       throw HpsError{HPSG_ERR_INVALID, hpsg::fmt("interface matrix of size %d exceeds the batched LU limit %d",
                                                  L.n_int, hpsk::bgetrf_max_n())};
-    for (int ch = 0; ch < L.mt.nchild; ++ch) {
+    for (int ch = 0; ch < (c->iti ? 0 : L.mt.nchild); ++ch) {
       std::vector<int> ext, itf;
       for (int f = 0; f < L.mt.nface; ++f) {
         const int v = L.mt.sec[ch * L.mt.nface + f];
@@ -326,8 +381,8 @@ void setup(hpsg_ctx* c) {
   }
   c->stats.n_leaves = c->T.cut ? 0 : nl;
   c->stats.n_points = c->T.cut ? 0 : (long long)nl * o.n;
-  c->stats.root_bsize = c->lv[0].n_ext;
-  c->stats.top_D_size = c->lv[0].n_int;
+  c->stats.root_bsize = c->iti ? c->lv[0].n_ext / 2 : c->lv[0].n_ext;
+  c->stats.top_D_size = c->iti ? c->lv[0].n_int / 2 : c->lv[0].n_int;
   c->stats.tree_depth = t.L;
   c->stats.min_rcond = 1.0;
 }
@@ -342,7 +397,7 @@ void alloc_build(hpsg_ctx* c) {
     if (c->terms[i].role == HPSG_ROLE_SECOND_ORDER && c->terms[i].axis != c->terms[i].axis2) mixed = true;
   c->fused = hpsk::leaf_fused_supported(o.n, o.p, o.ni, o.nb, c->tree.dim, mixed) &&
              !(path && std::string(path) == "batched");
-  if (c->opts.keep_factors) c->fused = false;  // the batched path keeps [LU | v | Y] and the pivots per leaf
+  if (c->opts.keep_factors || c->iti) c->fused = false;  // batched path: keeps [LU | v | Y] + pivots; ItI
   if (c->T.cut) {
     c->fused = false;  // no leaf stage: the part's leaves are input nodes
   } else if (c->fused) {
@@ -358,7 +413,7 @@ void alloc_build(hpsg_ctx* c) {
     c->yv_stride = (long long)o.ni * (1 + o.nb);
   } else {
     c->leafM.alloc(size_t(nl) * c->strideLeafM() * 8, tot);
-    c->leafE.alloc(size_t(nl) * o.ni * o.ne * 8, tot);
+    if (!c->iti) c->leafE.alloc(size_t(nl) * o.ni * o.ne * 8, tot);
     c->leafPiv.alloc(size_t(nl) * o.ni * 4, tot);
     c->yv = c->leafM.d() + (long long)o.ni * o.ni;
     c->yv_stride = c->strideLeafM();
@@ -461,6 +516,44 @@ void run_leaf_stage(hpsg_ctx* c) {
   a.E = c->leafE.d();
   a.strideE = (long long)o.ni * o.ne;
   a.bad_point = c->leafBad.i();
+  if (c->iti) {
+    // local_solve_iti (local_solve.cpp:145-172), real-equivalent: [B | f | [P;0], i[P;0]] -> LU -> [v | Y]
+    const hpsg::ItiLeafOperators& io = c->iops;
+    hpsk::ItiLeafArgs ia{};
+    ia.a = a;
+    ia.a.n = io.n;
+    ia.a.ni = io.ni;
+    ia.nbc = io.nbc;
+    ia.nbq = io.nb;
+    ia.Gr = c->iGr.d();
+    ia.Gi = c->iGi.d();
+    ia.P = c->iP.d();
+    hpsk::launch_iti_leaf_assemble(ia, nl, c->st);
+    ck(cudaGetLastError(), "iti leaf assemble");
+    ++c->launches;
+    ck(hpsk::lu_stats_init(c->leafStats.d(), nl, c->st), "stats init");
+    BatchedMat M{c->leafM.d(), o.ni, sM};
+    ck(hpsk::bgetrf_aug(nl, o.ni, 1 + o.nb, M, c->leafPiv.i(), c->leafStats.d(), c->st, false), "iti leaf bgetrf");
+    c->launches += lu_launches(o.ni, 1 + o.nb, true);
+    GemmArgs t;  // [h | T] = QH [v | Y]  (T = QH Y, h = QH v; local_solve.cpp:170-171)
+    t.m = o.nb;
+    t.n = 1 + o.nb;
+    t.k = o.ni;
+    t.batch = nl;
+    t.A = c->iQHs.d();
+    t.lda = o.nb;
+    t.sA = 0;
+    t.B = c->leafM.d() + (long long)o.ni * o.ni;
+    t.ldb = o.ni;
+    t.sB = sM;
+    t.D = c->leafHT.d();
+    t.ldd = o.nb;
+    t.sD = c->strideLeafHT();
+    t.alpha = 1.0;
+    t.beta = 0.0;
+    gemm(c, t);
+    return;
+  }
   if (c->fused) {
     hpsk::LeafFusedArgs f{};
     f.a = a;
@@ -558,6 +651,34 @@ void run_merge_level(hpsg_ctx* c, int d) {
   const double* child_HT = (d == c->T.L - 1) ? c->leafHT.d() : c->lv[d + 1].AH.d();
   const long long child_stride =
       (d == c->T.L - 1) ? c->strideLeafHT() : c->lv[d + 1].strideAH();
+  if (c->iti) {
+    // merge_iti (merge.cpp:338-482): zero-initialised real-equivalent blocks + block-list copies
+    ck(cudaMemsetAsync(L.MD.p, 0, size_t(L.nodes) * L.strideMD() * 8, c->st), "MD zero");
+    if (!root) {
+      ck(cudaMemsetAsync(c->Bscratch.p, 0, size_t(L.nodes) * L.n_ext * L.n_int * 8, c->st), "B zero");
+      ck(cudaMemsetAsync(L.AH.p, 0, size_t(L.nodes) * L.strideAH() * 8, c->st), "AH zero");
+    }
+    hpsk::BlockGatherArgs bg{};
+    bg.blocks = reinterpret_cast<const hpsk::DevBlockCopy*>(L.iblocks.p);
+    bg.nblocks = 0;
+    bg.nchild = L.mt.nchild;
+    bg.child_HT = child_HT;
+    bg.child_ld = L.child_nb;
+    bg.child_stride = child_stride;
+    bg.dst[0] = L.MD.d();
+    bg.ld[0] = L.n_int;
+    bg.stride[0] = L.strideMD();
+    bg.dst[1] = c->Bscratch.d();
+    bg.ld[1] = L.n_ext;
+    bg.stride[1] = (long long)L.n_ext * L.n_int;
+    bg.dst[2] = root ? nullptr : L.AH.d();
+    bg.ld[2] = L.n_ext;
+    bg.stride[2] = L.strideAH();
+    bg.nblocks = L.iti_nblocks;
+    hpsk::launch_block_gather(bg, int(L.nodes), c->st);
+    ck(cudaGetLastError(), "iti gather");
+    ++c->launches;
+  } else {
   hpsk::GatherArgs ga{};
   ga.s = L.mt.s;
   ga.nchild = L.mt.nchild;
@@ -596,6 +717,7 @@ void run_merge_level(hpsg_ctx* c, int d) {
     c->launches += 2;
   }
   ck(cudaGetLastError(), "gather");
+  }
   ck(hpsk::lu_stats_init(L.stats.d(), int(L.nodes), c->st), "stats init");
   const int m = (root && c->opts.root_implicit_S) ? 1 : 1 + L.n_ext;
   BatchedMat M{L.MD.d(), L.n_int, L.strideMD()};
@@ -604,7 +726,7 @@ void run_merge_level(hpsg_ctx* c, int d) {
   const bool keep_L = (root && c->opts.root_implicit_S) || c->opts.keep_factors;
   ck(hpsk::bgetrf_aug(int(L.nodes), L.n_int, m, M, L.piv.i(), L.stats.d(), c->st, keep_L), "merge bgetrf");
   c->launches += lu_launches(L.n_int, m, true);
-  if (!root && L.mt.s >= kSparseSchurMinS && !getenv("HPS_DENSE_SCHUR")) {
+  if (!root && !c->iti && L.mt.s >= kSparseSchurMinS && !getenv("HPS_DENSE_SCHUR")) {
     // [h | T] = [h_ext | A] - B [x_h | X] over the nonzero blocks of B only: section e's rows get
     // -B_{e,I} [x_h|X]_I for the runs I of interfaces of e's child (the other blocks of B are
     // structurally zero, merge.cpp:226-278), i.e. half the dense product in 2D, a quarter in 3D
@@ -799,6 +921,12 @@ void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_
     g.beta = 1.0;
   }
   matvecs(c, g);
+  if (c->iti) {  // all p^2 points are unknowns of the ItI leaf system: u = Y g + v, complex out
+    hpsk::launch_iti_leaf_output(d_u, c->Ui.d(), c->iops.n, nrhs, nl, c->st);
+    ++c->launches;
+    ck(cudaGetLastError(), "solve kernels");
+    return;
+  }
   GemmArgs e;
   e.m = o.ne;
   e.n = nrhs;
@@ -1110,6 +1238,7 @@ int hpsg_build(hpsg_ctx* c) {
 int hpsg_solve_device(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u) {
   if (!c || !d_g || !d_u || nrhs < 1) return HPSG_ERR_INVALID;
   if (!c->built) return fail(c, HPSG_ERR_STATE, "hpsg_solve: build() first");
+  if (c->iti) return fail(c, HPSG_ERR_STATE, "hpsg_solve: the ItI variant is complex (hpsg_solve_complex)");
   if (c->T.cut) return fail(c, HPSG_ERR_STATE, "hpsg_solve: a cut part has no leaves (hpsg_part_solve_cut)");
   return guarded(c, [&] {
     c->launches = 0;
@@ -1125,9 +1254,37 @@ int hpsg_solve_device(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u) {
   });
 }
 
+int hpsg_solve_complex(hpsg_ctx* c, const double* g_root, int nrhs, double* u_out) {
+  if (!c || !g_root || !u_out || nrhs < 1) return HPSG_ERR_INVALID;
+  if (!c->built) return fail(c, HPSG_ERR_STATE, "hpsg_solve: build() first");
+  if (!c->iti) return fail(c, HPSG_ERR_STATE, "hpsg_solve_complex: the solver is the DtN (real) variant");
+  return guarded(c, [&] {
+    c->launches = 0;
+    const int nb = c->lv[0].n_ext / 2;  // complex root boundary size
+    const size_t nu = size_t(c->T.n_leaves()) * c->iops.n * nrhs;
+    c->srcF.alloc(size_t(nb) * nrhs * 2 * 8, &c->dev_bytes);  // interleaved complex g (staging)
+    c->g_in.alloc(size_t(nb) * nrhs * 2 * 8, &c->dev_bytes);  // planar real-equivalent g
+    c->u_out.alloc(nu * 2 * 8, &c->dev_bytes);
+    ck(cudaEventRecord(c->ev[4], c->st), "ev");
+    ck(cudaMemcpyAsync(c->srcF.p, g_root, size_t(nb) * nrhs * 16, cudaMemcpyHostToDevice, c->st), "g H2D");
+    hpsk::launch_complex_to_planar(c->g_in.d(), c->srcF.d(), nb, nrhs, c->st);
+    ++c->launches;
+    run_solve(c, c->g_in.d(), nrhs, c->u_out.d(), nullptr);
+    ck(cudaMemcpyAsync(u_out, c->u_out.p, nu * 16, cudaMemcpyDeviceToHost, c->st), "u D2H");
+    ck(cudaEventRecord(c->ev[5], c->st), "ev");
+    ck(cudaEventSynchronize(c->ev[5]), "solve sync");
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]), "elapsed");
+    c->stats.t_solve_ms = ms;
+    c->stats.solve_bytes = solve_bytes(c, nrhs);
+    c->stats.launches_solve = c->launches;
+  });
+}
+
 int hpsg_solve(hpsg_ctx* c, const double* g_root, int nrhs, double* u_out, double* leaf_g_out) {
   if (!c || !g_root || !u_out || nrhs < 1) return HPSG_ERR_INVALID;
   if (!c->built) return fail(c, HPSG_ERR_STATE, "hpsg_solve: build() first");
+  if (c->iti) return fail(c, HPSG_ERR_STATE, "hpsg_solve: the ItI variant is complex (hpsg_solve_complex)");
   if (c->T.cut) return fail(c, HPSG_ERR_STATE, "hpsg_solve: a cut part has no leaves (hpsg_part_solve_cut)");
   return guarded(c, [&] {
     c->launches = 0;
@@ -1255,6 +1412,7 @@ int hpsg_get_leaf(hpsg_ctx* c, int ord, double* Y, double* v, double* Tm, double
   if (!c) return HPSG_ERR_INVALID;
   if (!c->built) return fail(c, HPSG_ERR_STATE, "hpsg_get_leaf: build() first");
   if (c->T.cut) return fail(c, HPSG_ERR_STATE, "hpsg_get_leaf: a cut part has no leaves");
+  if (c->iti) return fail(c, HPSG_ERR_STATE, "hpsg_get_leaf: not available for the ItI variant");
   if (ord < 0 || ord >= c->T.n_leaves()) return fail(c, HPSG_ERR_INVALID, "hpsg_get_leaf: bad ordinal");
   return guarded(c, [&] {
     const hpsg::LeafOperators& o = c->ops;
@@ -1294,6 +1452,7 @@ int hpsg_node_sizes(hpsg_ctx* c, int id, int* n_ext, int* n_int) {
 
 int hpsg_get_node(hpsg_ctx* c, int id, double* S, double* gtilde, double* Tm, double* h) {
   if (!c) return HPSG_ERR_INVALID;
+  if (c->iti) return fail(c, HPSG_ERR_STATE, "hpsg_get_node: not available for the ItI variant");
   if (!c->built) return fail(c, HPSG_ERR_STATE, "hpsg_get_node: build() first");
   return guarded(c, [&] {
     const Level* Lp = nullptr;
@@ -1328,7 +1487,7 @@ int hpsg_part_sizes(hpsg_ctx* c, long long* n_cut, int* cut_nb, int* root_nb) {
   if (!c) return HPSG_ERR_INVALID;
   if (n_cut) *n_cut = c->T.cut ? c->T.n_leaves() : 0;
   if (cut_nb) *cut_nb = c->T.cut ? c->leaf_nb() : 0;
-  if (root_nb) *root_nb = c->lv[0].n_ext;
+  if (root_nb) *root_nb = c->iti ? c->lv[0].n_ext / 2 : c->lv[0].n_ext;
   return HPSG_OK;
 }
 

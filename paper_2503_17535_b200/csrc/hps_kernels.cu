@@ -17,6 +17,115 @@ __global__ void __launch_bounds__(kAsmThreads) leaf_assemble_kernel(const LeafAs
   if (threadIdx.x == 0) a.bad_point[leaf] = s.bad;  // INT_MAX: all samples finite
 }
 
+__global__ void __launch_bounds__(kAsmThreads) iti_leaf_assemble_kernel(const ItiLeafArgs ia) {
+  __shared__ LeafAsmSmem s;
+  const LeafAsmArgs& a = ia.a;
+  const long long leaf = blockIdx.x;
+  const int tid = threadIdx.x, p = a.p, n = a.n, n2 = 2 * n, nbc = ia.nbc, nbq = ia.nbq;
+  const long long ld = n2, ncol = n2 + 1 + 2 * nbq;
+  double* M = a.M + leaf * a.strideM;
+  // zero fill (16-byte stores)
+  double2* m2 = reinterpret_cast<double2*>(M);
+  for (long long e = tid; e < ld * ncol / 2; e += kAsmThreads) m2[e] = make_double2(0.0, 0.0);
+  if (tid == 0) s.bad = INT_MAX;
+  for (int e = tid; e < p * p; e += kAsmThreads) s.D[e] = a.D[e], s.D2[e] = a.D2[e];
+  __syncthreads();
+  // coefficients and source at the leaf Chebyshev points (leaf_cheb_points, mesh.cpp:320-336)
+  const double* box = a.leaf_box + leaf * 6;
+  for (int i = tid; i < n; i += kAsmThreads) {
+    int ci[3];
+    leaf_decode(i, p, 2, ci);
+    double x[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < 2; ++k)
+      x[k] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(box[k], box[3 + k])),
+                       __dmul_rn(__dmul_rn(0.5, __dsub_rn(box[3 + k], box[k])), a.cheb[ci[k]]));
+    for (int t = 0; t < a.nterms; ++t) {
+      const double v = eval_field(a.terms[t].f, x, 2, leaf, i, n);
+      s.coef[t][i] = v;
+      if (!isfinite(v)) atomicMin(&s.bad, i);
+    }
+    s.fsrc[i] = a.has_source ? eval_field(a.source, x, 2, leaf, i, n) : 0.0;
+  }
+  __syncthreads();
+  // G rows (complex, shared by all leaves): [[Gr, -Gi], [Gi, Gr]]
+  for (int e = tid; e < nbc * n; e += kAsmThreads) {
+    const int r = e % nbc, c = e / nbc;
+    const double gr = ia.Gr[(long long)c * nbc + r], gi = ia.Gi[(long long)c * nbc + r];
+    M[(long long)c * ld + r] = gr;
+    M[(long long)(n + c) * ld + r] = -gi;
+    M[(long long)c * ld + n + r] = gi;
+    M[(long long)(n + c) * ld + n + r] = gr;
+  }
+  // interior rows of the discretized operator (real), entries on the grid lines through the point
+  const int per_row = 2 * (p - 1) + 1;
+  for (int e = tid; e < a.ni * per_row; e += kAsmThreads) {
+    const int k = e % a.ni, w = e / a.ni;
+    const int gi = a.interior[k];
+    int ii[3], jj[3];
+    leaf_decode(gi, p, 2, ii);
+    jj[0] = ii[0], jj[1] = ii[1], jj[2] = 0;
+    ii[2] = 0;
+    if (w > 0) {
+      const int ax = (w - 1) / (p - 1), k0 = (w - 1) % (p - 1);
+      jj[ax] = k0 < ii[ax] ? k0 : k0 + 1;
+    }
+    const int gj = jj[0] * p + jj[1];
+    const double v = leaf_entry(a, s, gi, ii, gj, jj);
+    M[(long long)gj * ld + nbc + k] = v;
+    M[(long long)(n + gj) * ld + n + nbc + k] = v;
+  }
+  // source column (real f on the interior rows) and the Y right-hand sides [P; 0], i [P; 0]
+  for (int k = tid; k < a.ni; k += kAsmThreads) M[(long long)n2 * ld + nbc + k] = s.fsrc[a.interior[k]];
+  for (int e = tid; e < nbc * nbq; e += kAsmThreads) {
+    const int r = e % nbc, j = e / nbc;
+    const double pv = ia.P[(long long)j * nbc + r];
+    M[(long long)(n2 + 1 + j) * ld + r] = pv;
+    M[(long long)(n2 + 1 + nbq + j) * ld + n + r] = pv;
+  }
+  __syncthreads();
+  if (tid == 0) a.bad_point[leaf] = s.bad;
+}
+
+__global__ void block_gather_kernel(const BlockGatherArgs a) {
+  const long long node = blockIdx.x;
+  const DevBlockCopy bc = a.blocks[blockIdx.y];
+  double* dst = a.dst[bc.dst] + node * a.stride[bc.dst];
+  const long long ld = a.ld[bc.dst];
+  if (bc.child < 0) {
+    for (int i = threadIdx.x; i < bc.rows; i += blockDim.x) dst[(long long)(bc.dc + i) * ld + bc.dr + i] = 1.0;
+    return;
+  }
+  const double* src = a.child_HT + (node * a.nchild + bc.child) * a.child_stride;
+  for (int e = threadIdx.x; e < bc.rows * bc.cols; e += blockDim.x) {
+    const int r = e % bc.rows, c = e / bc.rows;
+    dst[(long long)(bc.dc + c) * ld + bc.dr + r] = src[(long long)(bc.sc + c) * a.child_ld + bc.sr + r];
+  }
+}
+
+__global__ void iti_leaf_output_kernel(double* u, const double* Ui, int n, int nrhs, int n_leaves) {
+  const long long total = (long long)n_leaves * nrhs * n;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int pt = int(e % n);
+    const long long lk = e / n;
+    const long long leaf = lk % n_leaves;
+    const int k = int(lk / n_leaves);
+    const double* src = Ui + leaf * (2LL * n * nrhs) + (long long)k * 2 * n;
+    u[2 * e] = src[pt];
+    u[2 * e + 1] = src[n + pt];
+  }
+}
+
+__global__ void complex_to_planar_kernel(double* g_re, const double* g, int nb, int nrhs) {
+  const long long total = (long long)nb * nrhs;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = int(e % nb), k = int(e / nb);
+    g_re[(long long)k * 2 * nb + r] = g[2 * e];
+    g_re[(long long)k * 2 * nb + nb + r] = g[2 * e + 1];
+  }
+}
+
 constexpr int kGatherThreads = 256;
 
 // One warp per destination column: (slot, cc) are uniform over the column and the rows of each
@@ -146,6 +255,23 @@ __global__ void unpack_leaf_g_kernel(double* out, const double* G, int nb, int n
 }
 
 }  // namespace
+
+void launch_iti_leaf_assemble(const ItiLeafArgs& a, int n_leaves, cudaStream_t st) {
+  iti_leaf_assemble_kernel<<<n_leaves, kAsmThreads, 0, st>>>(a);
+}
+void launch_block_gather(const BlockGatherArgs& a, int n_nodes, cudaStream_t st) {
+  if (a.nblocks <= 0 || n_nodes <= 0) return;
+  block_gather_kernel<<<dim3(n_nodes, a.nblocks), 256, 0, st>>>(a);
+}
+void launch_iti_leaf_output(double* u, const double* Ui, int n, int nrhs, int n_leaves, cudaStream_t st) {
+  const long long total = (long long)n_leaves * nrhs * n;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 64);
+  iti_leaf_output_kernel<<<blocks, 256, 0, st>>>(u, Ui, n, nrhs, n_leaves);
+}
+void launch_complex_to_planar(double* g_re, const double* g, int nb, int nrhs, cudaStream_t st) {
+  const long long total = (long long)nb * nrhs;
+  complex_to_planar_kernel<<<(unsigned)std::max<long long>(1, (total + 255) / 256), 256, 0, st>>>(g_re, g, nb, nrhs);
+}
 
 void launch_leaf_assemble(const LeafAsmArgs& a, int n_leaves, cudaStream_t st) {
   leaf_assemble_kernel<<<n_leaves, kAsmThreads, 0, st>>>(a);

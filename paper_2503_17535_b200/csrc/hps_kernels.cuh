@@ -46,6 +46,40 @@ struct LeafAsmArgs {
 };
 void launch_leaf_assemble(const LeafAsmArgs& a, int n_leaves, cudaStream_t st);
 
+// ---- ItI variant (real-equivalent embedding; geometry.hpp ItiLeafOperators / ItiMergeTables) ----
+// Leaf system of local_solve_iti (proj/src/local_solve.cpp:145-172) in real-equivalent form:
+// M = [B_re | f_re | Prhs_re] with B = [G ; L(I_i, :)] (n x n complex) -> 2n x 2n real, f on the
+// interior rows, and the Y right-hand sides [P; 0] and i[P; 0] so that the solve returns the
+// real-equivalent Y directly.  M is 2n x (2n + 1 + 2 nb) per leaf, column-major, ld 2n.
+struct ItiLeafArgs {
+  LeafAsmArgs a;            // coefficient / geometry fields (a.n = p^2, a.ni interior count)
+  int nbc, nbq;             // 4p-4 walk rows, 4q Gauss boundary points
+  const double* Gr;         // nbc x n
+  const double* Gi;         // nbc x n
+  const double* P;          // nbc x nbq
+};
+void launch_iti_leaf_assemble(const ItiLeafArgs& a, int n_leaves, cudaStream_t st);
+
+struct DevBlockCopy {
+  int dst, dr, dc, child, sr, sc, rows, cols;
+};
+// Block-list merge gather (ItI): copies every listed block of the children's [h|T] into the
+// zero-initialised MD / B / AH of each node (identity blocks when child < 0).
+struct BlockGatherArgs {
+  const DevBlockCopy* blocks;
+  int nblocks, nchild;
+  const double* child_HT;
+  long long child_ld, child_stride;
+  double* dst[3];
+  long long ld[3], stride[3];
+};
+void launch_block_gather(const BlockGatherArgs& a, int n_nodes, cudaStream_t st);
+// u (interleaved complex, nrhs x n_leaves x n) from the real-equivalent leaf solution Ui
+// (per leaf 2n x nrhs, ld 2n)
+void launch_iti_leaf_output(double* u, const double* Ui, int n, int nrhs, int n_leaves, cudaStream_t st);
+// g_re (planar real-equivalent, nb_re x nrhs) from interleaved complex g (nrhs x nb)
+void launch_complex_to_planar(double* g_re, const double* g, int nb, int nrhs, cudaStream_t st);
+
 // Fused stage 1 (leaf_fused.cu): assembly + -L_ie P + GEPP/solve + [h|T] per leaf in one
 // persistent kernel over an L2-resident per-CTA workspace.
 struct LeafFusedArgs {

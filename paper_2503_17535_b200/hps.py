@@ -54,7 +54,8 @@ class _Part(C.Structure):
 
 
 class _Options(C.Structure):
-    _fields_ = [("literal_sign", C.c_int), ("root_implicit_S", C.c_int), ("device", C.c_int), ("keep_factors", C.c_int)]
+    _fields_ = [("literal_sign", C.c_int), ("root_implicit_S", C.c_int), ("device", C.c_int), ("keep_factors", C.c_int),
+                ("variant", C.c_int), ("eta", C.c_double)]
 
 
 class _Stats(C.Structure):
@@ -90,6 +91,7 @@ def lib():
         L.hpsg_part_set_cut_ht.argtypes = [vp, C.c_longlong, C.c_void_p]
         L.hpsg_part_solve_cut.argtypes = [vp, C.c_void_p, C.c_int, C.c_void_p]
         L.hpsg_solve_new_source.argtypes = [vp, dp, dp, C.c_int, dp]
+        L.hpsg_solve_complex.argtypes = [vp, dp, C.c_int, dp]
         L.hpsg_solve_new_source_device.argtypes = [vp, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
         L.hpsg_build.argtypes = [vp]
         L.hpsg_solve.argtypes = [vp, dp, C.c_int, dp, dp]
@@ -224,7 +226,7 @@ class HpsSolver:
     """
 
     def __init__(self, tree: UniformTree, terms, source: Field | None = None, literal_sign=True,
-                 root_implicit_S=False, device=0, part=None, keep_factors=False):
+                 root_implicit_S=False, device=0, part=None, keep_factors=False, variant="dtn", eta=1.0):
         L = lib()
         self.tree = tree
         keep = []
@@ -234,7 +236,11 @@ class HpsSolver:
             arr[i].field = t.field.to_c(keep)
         src = source.to_c(keep) if source is not None else None
         tr = _Tree(tree.dim, tree.p, tree.L, tree.lo, tree.hi)
-        op = _Options(int(literal_sign), int(root_implicit_S), device, int(keep_factors))
+        if variant not in ("dtn", "iti"):
+            raise HpsError(HPSG_ERR_INVALID, f"unknown variant {variant!r}")
+        self.variant = variant
+        op = _Options(int(literal_sign), int(root_implicit_S), device, int(keep_factors), 1 if variant == "iti" else 0,
+                      float(eta))
         self.part = tuple(part) if part is not None else (0, 0, tree.L)
         pt = _Part(*self.part)
         h = C.c_void_p()
@@ -299,6 +305,19 @@ class HpsSolver:
     def solve_device(self, d_g_ptr, nrhs, d_u_ptr):
         """Zero-copy solve on device pointers (e.g. torch.Tensor.data_ptr())."""
         self._check(lib().hpsg_solve_device(self._h, C.c_void_p(d_g_ptr), nrhs, C.c_void_p(d_u_ptr)), "solve")
+
+    def solve_complex(self, g_root):
+        """ItI variant (HpsSolver<Complex>::solve): g_root (nb,) or (nrhs, nb) complex incoming impedance
+        data at the root boundary points -> u (n_leaves, p^2) or (nrhs, n_leaves, p^2) complex."""
+        g = np.ascontiguousarray(g_root, dtype=np.complex128)
+        single = g.ndim == 1
+        g2 = g.reshape(1, -1) if single else g
+        nrhs = g2.shape[0]
+        assert g2.shape[1] == self.nb_root
+        u = np.empty((nrhs, self.n_leaves, self.npts), dtype=np.complex128)
+        self._check(lib().hpsg_solve_complex(self._h, g2.ctypes.data_as(C.POINTER(C.c_double)), nrhs,
+                                             u.ctypes.data_as(C.POINTER(C.c_double))), "solve")
+        return u[0] if single else u
 
     def solve_new_source(self, leaf_f, g_root):
         """HpsSolver::solve_new_source(leaf_f, RootBC::dirichlet, g_root) (solver.cpp:285-307) for
