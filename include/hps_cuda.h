@@ -151,6 +151,9 @@ int hpsg_solve_device(hpsg_ctx* ctx, const double* d_g_root, int nrhs, double* d
  * boundary Gauss points, u_out nrhs x n_leaves x p^2.  Internally every complex matrix is carried
  * in real-equivalent form [[re, -im], [im, re]]. */
 int hpsg_solve_complex(hpsg_ctx* ctx, const double* g_root, int nrhs, double* u_out);
+/* host-only: the ItI leaf operators of assemble_iti_ops_2d (spectral.cpp:312-368), column-major:
+ * G = Gr + i Gi ((4p-4) x p^2), P ((4p-4) x 4q), QH = QHr + i QHi (4q x p^2); any pointer may be NULL */
+int hpsg_iti_leaf_ops(int p, double eta, double side, double* Gr, double* Gi, double* P, double* QHr, double* QHi);
 /* HpsSolver::solve_new_source(leaf_f, RootBC::dirichlet, g_root), solver.hpp:71-72 /
  * solver.cpp:285-307 (make_source_state :261-283, leaf_resolve_source local_solve.cpp:174-183,
  * artifact_source_pass merge.cpp:514-567), for nsrc sources at once against the stored build:

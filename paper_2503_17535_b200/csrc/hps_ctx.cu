@@ -1397,6 +1397,19 @@ int hpsg_tree_root_points(const hpsg_tree* t, double* xyz) {
   return HPSG_OK;
 }
 
+int hpsg_iti_leaf_ops(int p, double eta, double side, double* Gr, double* Gi, double* P, double* QHr, double* QHi) {
+  try {
+    const hpsg::ItiLeafOperators o = hpsg::make_iti_leaf_operators(p, eta, side);
+    auto cp = [](double* dst, const hpsg::HostMat& m) {
+      if (dst) std::memcpy(dst, m.a.data(), m.a.size() * 8);
+    };
+    cp(Gr, o.Gr), cp(Gi, o.Gi), cp(P, o.P), cp(QHr, o.QHr), cp(QHi, o.QHi);
+  } catch (...) {
+    return HPSG_ERR_INVALID;
+  }
+  return HPSG_OK;
+}
+
 int hpsg_tree_leaf_points(const hpsg_tree* t, double* xyz) {
   if (!t || !xyz || (t->dim != 2 && t->dim != 3) || t->p < 4 || t->L < 0 || !(t->hi > t->lo))
     return HPSG_ERR_INVALID;

@@ -83,3 +83,34 @@ def test_cpp_dropin_example_builds_and_fails_loudly_without_device():
         pytest.skip("a CUDA device is present (run by the gpu tests)")
     r = subprocess.run([exe, "2", "8"], capture_output=True, text=True)
     assert r.returncode == 1 and "no CUDA device" in r.stderr
+
+
+def test_iti_leaf_operator_kats():
+    """proj/tests/test_spectral.cpp:168-203 ("2D ItI leaf operators") on the product's host operators:
+    G 1 = i eta on every walk point, QH 1 = Q H 1 = -i eta, QH x1 on the east side = 1 - i eta,
+    G - Ntilde is exactly the i eta walk sampling (4p-4 entries)."""
+    import ctypes as C
+    import numpy as np
+    import paper_2503_17535_b200 as H
+    from paper_2503_17535_b200 import hps as HP
+    p, q, eta = 8, 6, 2.5
+    n, nbc, nb = p * p, 4 * p - 4, 4 * q
+    L = H.lib()
+    L.hpsg_iti_leaf_ops.argtypes = [C.c_int, C.c_double, C.c_double] + [C.POINTER(C.c_double)] * 5
+    Gr, Gi, P = np.zeros((n, nbc)), np.zeros((n, nbc)), np.zeros((nb, nbc))
+    QHr, QHi = np.zeros((n, nb)), np.zeros((n, nb))
+    assert L.hpsg_iti_leaf_ops(p, eta, 2.0, *(HP._dp(a) for a in (Gr, Gi, P, QHr, QHi))) == 0
+    G = (Gr + 1j * Gi).T            # column-major buffers -> (rows, cols)
+    QH = (QHr + 1j * QHi).T
+    P = P.T
+    one = np.ones(n)
+    assert np.abs(G @ one - 1j * eta).max() < 1e-12
+    assert np.abs(QH @ one + 1j * eta).max() < 1e-12
+    assert np.abs(P.sum(axis=1) - 1.0).max() < 1e-13          # Gauss -> walk interpolation of constants
+    m = p - 1                                                    # cheb_lobatto_1d (spectral.cpp:14-26)
+    cn = np.sin(np.pi * (m - 2 * np.arange(p)) / (2 * m))
+    pts = np.zeros((n, 3))
+    pts[:, 0] = cn[np.arange(n) // p]                            # x1 of tensor index i1*p + i2
+    hu = QH @ pts[:, 0]
+    assert np.abs(hu[q:2 * q] - (1.0 - 1j * eta)).max() < 1e-11   # east side (s = 1) rows
+    assert (np.abs(Gi) > 0).sum() == 4 * p - 4 and np.allclose(Gi[Gi != 0], eta)

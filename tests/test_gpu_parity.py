@@ -257,3 +257,67 @@ def test_solve_new_source_requires_kept_factors():
     with pytest.raises(H.HpsError) as e:
         s.solve_new_source(np.zeros((s.n_leaves, s.npts)), np.zeros(s.nb_root))
     assert e.value.code == H.hps.HPSG_ERR_STATE and "keep_factors" in str(e.value)
+
+
+def _impedance_data(rp, u, du, eta):
+    """Incoming impedance data du/dn + i eta u at the root boundary points (faces S, E, N, W)."""
+    nb = len(rp)
+    side = np.repeat(np.arange(4), nb // 4)
+    nrm = np.array([[0, -1], [1, 0], [0, 1], [-1, 0]], dtype=float)[side]
+    gx, gy = du(rp)
+    return nrm[:, 0] * gx + nrm[:, 1] * gy + 1j * eta * u(rp)
+
+
+@pytest.mark.parametrize("p,L,tol", [(16, 3, 1e-10), (16, 4, 1e-10), (12, 4, 1e-8)])
+def test_iti_plane_wave(p, L, tol):
+    """ItI variant (local_solve_iti / merge_iti): Helmholtz with the complex plane
+    wave u = exp(i k.x) and impedance root data, against the exact field; two right-hand sides."""
+    k, eta = 12.0, 12.0
+    terms = [H.Term(H.ROLE_LAPLACIAN, H.Field.const(1.0)), H.Term(H.ROLE_ZEROTH, H.Field.const(k * k))]
+    s = H.HpsSolver(H.build_uniform_tree(-1.0, 1.0, L, 2, p), terms, None, variant="iti", eta=eta)
+    s.build()
+    rp = s.root_boundary_points()
+    G, E = [], []
+    for th in (0.7, 2.1):
+        kv = k * np.array([np.cos(th), np.sin(th)])
+        u = lambda x, kv=kv: np.exp(1j * (x[..., 0] * kv[0] + x[..., 1] * kv[1]))
+        du = lambda x, kv=kv, u=u: (1j * kv[0] * u(x), 1j * kv[1] * u(x))
+        G.append(_impedance_data(rp, u, du, eta))
+        E.append(u(s.leaf_points()))
+    U = s.solve_complex(np.stack(G))
+    for i in range(2):
+        assert np.abs(U[i] - E[i]).max() / np.abs(E[i]).max() < tol
+    assert np.abs(s.solve_complex(G[1]) - U[1]).max() < 1e-12 * np.abs(U[1]).max()
+
+
+def test_iti_variable_coefficient_matches_dtn():
+    """The headline variable-coefficient Helmholtz problem through both variants: DtN with Dirichlet
+    data and ItI with impedance data reproduce the same manufactured field."""
+    prob = PR.helmholtz_bumps()
+    k = 30.0
+    tree = H.build_uniform_tree(-1.0, 1.0, 4, 2, 16)
+    dtn = H.HpsSolver(tree, prob.terms, prob.source, literal_sign=False)
+    dtn.build()
+    u_d = dtn.solve(prob.boundary(dtn.root_boundary_points()))
+    iti = H.HpsSolver(tree, prob.terms, prob.source, literal_sign=False, variant="iti", eta=k)
+    iti.build()
+    rp = iti.root_boundary_points()
+    u = lambda x: np.sin(k * x[..., 0] + 0.3)
+    du = lambda x: (k * np.cos(k * x[..., 0] + 0.3), 0.0 * x[..., 0])
+    u_i = iti.solve_complex(_impedance_data(rp, u, du, k))
+    ex = u(dtn.leaf_points())
+    assert np.abs(u_i.real - ex).max() / np.abs(ex).max() < 1e-8
+    assert np.abs(u_i.imag).max() < 1e-8
+    assert np.abs(u_i.real - u_d).max() / np.abs(ex).max() < 1e-8
+
+
+def test_iti_errors():
+    terms = [H.Term(H.ROLE_LAPLACIAN, H.Field.const(1.0))]
+    with pytest.raises(H.HpsError):
+        H.HpsSolver(H.build_uniform_tree(0, 1, 1, 3, 6), terms, None, variant="iti", eta=1.0)   # 2D only
+    with pytest.raises(H.HpsError):
+        H.HpsSolver(H.build_uniform_tree(-1, 1, 2, 2, 8), terms, None, variant="iti", eta=1.0, root_implicit_S=True)
+    s = H.HpsSolver(H.build_uniform_tree(-1, 1, 2, 2, 8), terms, None, variant="iti", eta=1.0)
+    s.build()
+    with pytest.raises(H.HpsError):
+        s.solve(np.zeros(s.nb_root))   # complex variant: solve_complex
