@@ -85,6 +85,9 @@ typedef struct {
   int variant;          /* HPSG_VARIANT_DTN (HpsSolver<Real>) or HPSG_VARIANT_ITI (HpsSolver<Complex>,
                            2D impedance-to-impedance maps, spectral.hpp:87) */
   double eta;           /* ItI impedance parameter (HpsSolver ctor eta, solver.hpp:43) */
+  int build_root_T;     /* ItI: form and factor the root T for the radiation closure
+                           (SolverOptions::build_root_T, solver.hpp:19; solver.cpp:153-157) */
+  const hpsg_field* source_imag;  /* ItI: imaginary part of the complex source (NULL: real source) */
 } hpsg_options;
 enum { HPSG_VARIANT_DTN = 0, HPSG_VARIANT_ITI = 1 };
 
@@ -151,6 +154,10 @@ int hpsg_solve_device(hpsg_ctx* ctx, const double* d_g_root, int nrhs, double* d
  * boundary Gauss points, u_out nrhs x n_leaves x p^2.  Internally every complex matrix is carried
  * in real-equivalent form [[re, -im], [im, re]]. */
 int hpsg_solve_complex(hpsg_ctx* ctx, const double* g_root, int nrhs, double* u_out);
+/* HpsSolver::solve_radiation() (solver.cpp:254-259): root data g = -T_root^-1 h_root, then the
+ * downward pass; needs build_root_T.  u_out: n_leaves x p^2 interleaved complex; g_out (optional):
+ * the closing root data (root_bsize interleaved complex). */
+int hpsg_solve_radiation(hpsg_ctx* ctx, double* u_out, double* g_out);
 /* host-only: the ItI leaf operators of assemble_iti_ops_2d (spectral.cpp:312-368), column-major:
  * G = Gr + i Gi ((4p-4) x p^2), P ((4p-4) x 4q), QH = QHr + i QHi (4q x p^2); any pointer may be NULL */
 int hpsg_iti_leaf_ops(int p, double eta, double side, double* Gr, double* Gi, double* P, double* QHr, double* QHi);

@@ -115,6 +115,10 @@ struct hpsg_ctx {
   hpsg_tree tree{};
   hpsg_part part{};  // (0, 0, L) for the whole tree
   bool iti = false;  // ItI variant (real-equivalent complex)
+  bool root_T = false;  // ItI radiation closure: the root forms [h|T] and factors T
+  DevBuf radM, radPiv, radStats;  // [T_root | -h_root] -> [LU | g_rad]
+  hpsk::DevField source_im{};
+  int has_source_im = 0;
   hpsg::ItiLeafOperators iops;
   DevBuf iGr, iGi, iP, iQHs;
   hpsg_options opts{};
@@ -158,6 +162,8 @@ struct hpsg_ctx {
   long long strideLeafHT() const { return (long long)leaf_nb() * (1 + leaf_nb()); }
   // the merge at part depth d is the reference's root merge (no T/h, optional implicit S)
   bool global_root(int d) const { return d == 0 && T.root_depth == 0; }
+  // the merge at part depth d forms the node's [h|T] (every merge but the root, unless build_root_T)
+  bool forms_T(int d) const { return !global_root(d) || root_T; }
 };
 
 namespace {
@@ -260,7 +266,7 @@ double counted_build_flops(const hpsg_ctx* c) {
   for (const Level& L : c->lv) {
     const double a = L.n_int, e = L.n_ext;
     double per;
-    if (!c->global_root(L.d))
+    if (c->forms_T(L.d))
       per = 2.0 / 3.0 * a * a * a + 2 * a * a * e + 2 * e * a * e;
     else
       per = c->opts.root_implicit_S ? 2.0 / 3.0 * a * a * a : 2.0 / 3.0 * a * a * a + 2 * a * a * e;
@@ -288,6 +294,7 @@ void setup(hpsg_ctx* c) {
     if (c->T.cut || c->T.root_depth) throw HpsError{HPSG_ERR_INVALID, "ItI: tree parts are not supported"};
     if (c->opts.keep_factors) throw HpsError{HPSG_ERR_INVALID, "ItI: solve_new_source is not on this path"};
     c->iops = hpsg::make_iti_leaf_operators(t.p, c->opts.eta, c->T.leaf_side);
+    c->root_T = c->opts.build_root_T != 0;
     // the generic leaf/solve code sees the real-equivalent leaf system: 2n rows, 2 x 4q boundary
     c->ops.ni = 2 * c->iops.n;
     c->ops.nb = 2 * c->iops.nb;
@@ -349,7 +356,7 @@ void setup(hpsg_ctx* c) {
       L.mt.down = L.it.down;
       std::vector<hpsk::DevBlockCopy> bl;  // the root forms no T/h: its list keeps the MD blocks only
       for (const auto& b : L.it.blocks)
-        if (!(d == 0 && c->T.root_depth == 0) || b.dst == 0)
+        if (c->forms_T(d) || b.dst == 0)
           bl.push_back({b.dst, b.dr, b.dc, b.child, b.sr, b.sc, b.rows, b.cols});
       L.iti_nblocks = int(bl.size());
       std::vector<int> raw(bl.size() * 8);
@@ -428,12 +435,18 @@ void alloc_build(hpsg_ctx* c) {
     L.MD.alloc(size_t(L.nodes) * L.strideMD() * 8, tot);
     L.piv.alloc(size_t(L.nodes) * L.n_int * 4, tot);
     L.stats.alloc(size_t(L.nodes) * 3 * 8, tot);
-    if (!c->global_root(L.d)) {
+    if (c->forms_T(L.d)) {
       L.AH.alloc(size_t(L.nodes) * L.strideAH() * 8, tot);
       bmax = std::max(bmax, size_t(L.nodes) * L.n_ext * L.n_int * 8);
     }
   }
   c->Bscratch.alloc(bmax, tot);
+  if (c->root_T) {
+    const Level& R = c->lv[0];
+    c->radM.alloc(size_t(R.n_ext) * (R.n_ext + 1) * 8, tot);
+    c->radPiv.alloc(size_t(R.n_ext) * 4, tot);
+    c->radStats.alloc(3 * 8, tot);
+  }
 }
 
 void check_leaf_errors(hpsg_ctx* c) {
@@ -528,6 +541,8 @@ void run_leaf_stage(hpsg_ctx* c) {
     ia.Gr = c->iGr.d();
     ia.Gi = c->iGi.d();
     ia.P = c->iP.d();
+    ia.source_im = c->source_im;
+    ia.has_source_im = c->has_source_im;
     hpsk::launch_iti_leaf_assemble(ia, nl, c->st);
     ck(cudaGetLastError(), "iti leaf assemble");
     ++c->launches;
@@ -647,7 +662,7 @@ void run_leaf_stage(hpsg_ctx* c) {
 
 void run_merge_level(hpsg_ctx* c, int d) {
   Level& L = c->lv[d];
-  const bool root = c->global_root(d);
+  const bool root = !c->forms_T(d);
   const double* child_HT = (d == c->T.L - 1) ? c->leafHT.d() : c->lv[d + 1].AH.d();
   const long long child_stride =
       (d == c->T.L - 1) ? c->strideLeafHT() : c->lv[d + 1].strideAH();
@@ -1184,6 +1199,12 @@ int hpsg_create_part(const hpsg_tree* tree, const hpsg_part* part, const hpsg_te
       c->source = make_dev_field(c.get(), *source, true);
       c->has_source = 1;
     }
+    if (opts && opts->source_imag) {
+      if (!c->iti) throw HpsError{HPSG_ERR_INVALID, "hpsg_create: a complex source needs the ItI variant"};
+      c->source_im = make_dev_field(c.get(), *opts->source_imag, true);
+      c->has_source_im = 1;
+    }
+    c->opts.source_imag = nullptr;  // the caller's descriptor is not kept
     alloc_build(c.get());
     c->cut_set.assign(c->T.cut ? size_t(c->T.n_leaves()) : 0, 0);
     ck(cudaStreamSynchronize(c->st), "create sync");
@@ -1213,6 +1234,21 @@ int hpsg_build(hpsg_ctx* c) {
     for (int d = c->T.L - 1; d >= 0; --d) {
       ck(cudaEventRecord(c->lev_ev[d + 1], c->st), "ev");
       run_merge_level(c, d);
+    }
+    if (c->root_T) {
+      // radiation closure (solver.cpp:153-157, 254-259): factor [T_root | -h_root] once per build
+      const Level& R = c->lv[0];
+      const int n = R.n_ext;
+      ck(cudaMemcpyAsync(c->radM.p, R.AH.d() + n, size_t(n) * n * 8, cudaMemcpyDeviceToDevice, c->st), "T copy");
+      ck(cudaMemcpyAsync(c->radM.d() + (long long)n * n, R.AH.d(), size_t(n) * 8, cudaMemcpyDeviceToDevice, c->st),
+         "h copy");
+      hpsk::launch_axpby(c->radM.d() + (long long)n * n, n, n, c->radM.d() + (long long)n * n, n, n, n, 1, 1, 0.0,
+                         -1.0, c->st);
+      ck(hpsk::lu_stats_init(c->radStats.d(), 1, c->st), "stats init");
+      ck(hpsk::bgetrf_aug(1, n, 1, BatchedMat{c->radM.d(), n, (long long)n * (n + 1)}, c->radPiv.i(),
+                          c->radStats.d(), c->st),
+         "root T bgetrf");
+      c->launches += 3 + lu_launches(n, 1, true);
     }
     ck(cudaEventRecord(c->lev_ev[0], c->st), "ev");
     ck(cudaEventRecord(c->ev[3], c->st), "ev");
@@ -1277,6 +1313,36 @@ int hpsg_solve_complex(hpsg_ctx* c, const double* g_root, int nrhs, double* u_ou
     ck(cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]), "elapsed");
     c->stats.t_solve_ms = ms;
     c->stats.solve_bytes = solve_bytes(c, nrhs);
+    c->stats.launches_solve = c->launches;
+  });
+}
+
+int hpsg_solve_radiation(hpsg_ctx* c, double* u_out, double* g_out) {
+  if (!c || !u_out) return HPSG_ERR_INVALID;
+  if (!c->built) return fail(c, HPSG_ERR_STATE, "solve_radiation: build() first");
+  if (!c->root_T) return fail(c, HPSG_ERR_STATE, "solve_radiation: root T was not built");
+  return guarded(c, [&] {
+    c->launches = 0;
+    std::vector<double> st(3);
+    ck(cudaMemcpy(st.data(), c->radStats.p, 24, cudaMemcpyDeviceToHost), "stats");
+    if (st[2] >= 0) throw HpsError{HPSG_ERR_SINGULAR_MERGE, "solve_radiation: singular root T"};
+    const int n = c->lv[0].n_ext, nb = n / 2;
+    const double* g_re = c->radM.d() + (long long)n * n;
+    const size_t nu = size_t(c->T.n_leaves()) * c->iops.n;
+    c->u_out.alloc(nu * 2 * 8, &c->dev_bytes);
+    ck(cudaEventRecord(c->ev[4], c->st), "ev");
+    run_solve(c, g_re, 1, c->u_out.d(), nullptr);
+    ck(cudaMemcpyAsync(u_out, c->u_out.p, nu * 16, cudaMemcpyDeviceToHost, c->st), "u D2H");
+    ck(cudaEventRecord(c->ev[5], c->st), "ev");
+    ck(cudaEventSynchronize(c->ev[5]), "solve sync");
+    if (g_out) {
+      std::vector<double> g(n);
+      ck(cudaMemcpy(g.data(), g_re, size_t(n) * 8, cudaMemcpyDeviceToHost), "g D2H");
+      for (int i = 0; i < nb; ++i) g_out[2 * i] = g[i], g_out[2 * i + 1] = g[nb + i];
+    }
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]), "elapsed");
+    c->stats.t_solve_ms = ms;
     c->stats.launches_solve = c->launches;
   });
 }

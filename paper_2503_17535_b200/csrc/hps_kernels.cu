@@ -75,7 +75,19 @@ __global__ void __launch_bounds__(kAsmThreads) iti_leaf_assemble_kernel(const It
     M[(long long)(n + gj) * ld + n + nbc + k] = v;
   }
   // source column (real f on the interior rows) and the Y right-hand sides [P; 0], i [P; 0]
-  for (int k = tid; k < a.ni; k += kAsmThreads) M[(long long)n2 * ld + nbc + k] = s.fsrc[a.interior[k]];
+  for (int k = tid; k < a.ni; k += kAsmThreads) {
+    const int gi = a.interior[k];
+    M[(long long)n2 * ld + nbc + k] = s.fsrc[gi];
+    if (ia.has_source_im) {  // complex source: imaginary part on the imaginary rows
+      int ci[3];
+      leaf_decode(gi, p, 2, ci);
+      double x[3] = {0.0, 0.0, 0.0};
+      for (int q = 0; q < 2; ++q)
+        x[q] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(box[q], box[3 + q])),
+                         __dmul_rn(__dmul_rn(0.5, __dsub_rn(box[3 + q], box[q])), a.cheb[ci[q]]));
+      M[(long long)n2 * ld + n + nbc + k] = eval_field(ia.source_im, x, 2, leaf, gi, n);
+    }
+  }
   for (int e = tid; e < nbc * nbq; e += kAsmThreads) {
     const int r = e % nbc, j = e / nbc;
     const double pv = ia.P[(long long)j * nbc + r];

@@ -57,6 +57,8 @@ struct ItiLeafArgs {
   const double* Gr;         // nbc x n
   const double* Gi;         // nbc x n
   const double* P;          // nbc x nbq
+  DevField source_im;       // imaginary part of a complex source (has_source_im)
+  int has_source_im;
 };
 void launch_iti_leaf_assemble(const ItiLeafArgs& a, int n_leaves, cudaStream_t st);
 

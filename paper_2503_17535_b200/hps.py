@@ -55,7 +55,8 @@ class _Part(C.Structure):
 
 class _Options(C.Structure):
     _fields_ = [("literal_sign", C.c_int), ("root_implicit_S", C.c_int), ("device", C.c_int), ("keep_factors", C.c_int),
-                ("variant", C.c_int), ("eta", C.c_double)]
+                ("variant", C.c_int), ("eta", C.c_double), ("build_root_T", C.c_int),
+                ("source_imag", C.POINTER(_Field))]
 
 
 class _Stats(C.Structure):
@@ -92,6 +93,7 @@ def lib():
         L.hpsg_part_solve_cut.argtypes = [vp, C.c_void_p, C.c_int, C.c_void_p]
         L.hpsg_solve_new_source.argtypes = [vp, dp, dp, C.c_int, dp]
         L.hpsg_solve_complex.argtypes = [vp, dp, C.c_int, dp]
+        L.hpsg_solve_radiation.argtypes = [vp, dp, dp]
         L.hpsg_solve_new_source_device.argtypes = [vp, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
         L.hpsg_build.argtypes = [vp]
         L.hpsg_solve.argtypes = [vp, dp, C.c_int, dp, dp]
@@ -205,6 +207,16 @@ def tree_root_points(tree: UniformTree):
     return out
 
 
+def tree_leaf_points_of(tree: UniformTree):
+    """leaf_cheb_points over the whole tree without a solver (n_leaves, p^d, 3)."""
+    out = np.zeros((tree.n_leaves, tree.p ** tree.dim, 3))
+    tr = _Tree(tree.dim, tree.p, tree.L, tree.lo, tree.hi)
+    rc = lib().hpsg_tree_leaf_points(C.byref(tr), _dp(out))
+    if rc != HPSG_OK:
+        raise HpsError(rc, "hpsg_tree_leaf_points: invalid tree")
+    return out
+
+
 def bump_centers(seed, n=10, dim=2):
     """std::mt19937_64(seed) + uniform_real_distribution(-0.5,0.5) (proj/src/problems.cpp:126-141)."""
     out = np.zeros(3 * n)
@@ -226,7 +238,8 @@ class HpsSolver:
     """
 
     def __init__(self, tree: UniformTree, terms, source: Field | None = None, literal_sign=True,
-                 root_implicit_S=False, device=0, part=None, keep_factors=False, variant="dtn", eta=1.0):
+                 root_implicit_S=False, device=0, part=None, keep_factors=False, variant="dtn", eta=1.0,
+                 build_root_T=False, source_imag: Field | None = None):
         L = lib()
         self.tree = tree
         keep = []
@@ -240,7 +253,10 @@ class HpsSolver:
             raise HpsError(HPSG_ERR_INVALID, f"unknown variant {variant!r}")
         self.variant = variant
         op = _Options(int(literal_sign), int(root_implicit_S), device, int(keep_factors), 1 if variant == "iti" else 0,
-                      float(eta))
+                      float(eta), int(build_root_T))
+        if source_imag is not None:
+            self._src_im = source_imag.to_c(keep)
+            op.source_imag = C.pointer(self._src_im)
         self.part = tuple(part) if part is not None else (0, 0, tree.L)
         pt = _Part(*self.part)
         h = C.c_void_p()
@@ -318,6 +334,15 @@ class HpsSolver:
         self._check(lib().hpsg_solve_complex(self._h, g2.ctypes.data_as(C.POINTER(C.c_double)), nrhs,
                                              u.ctypes.data_as(C.POINTER(C.c_double))), "solve")
         return u[0] if single else u
+
+    def solve_radiation(self, want_g=False):
+        """HpsSolver::solve_radiation() (solver.cpp:254-259): root data closing T g = -h (ItI,
+        build_root_T=True) -> u (n_leaves, p^2) complex [, g (nb,) complex]."""
+        u = np.empty((self.n_leaves, self.npts), dtype=np.complex128)
+        g = np.empty(self.nb_root, dtype=np.complex128)
+        self._check(lib().hpsg_solve_radiation(self._h, u.ctypes.data_as(C.POINTER(C.c_double)),
+                                               g.ctypes.data_as(C.POINTER(C.c_double))), "solve_radiation")
+        return (u, g) if want_g else u
 
     def solve_new_source(self, leaf_f, g_root):
         """HpsSolver::solve_new_source(leaf_f, RootBC::dirichlet, g_root) (solver.cpp:285-307) for

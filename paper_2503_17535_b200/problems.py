@@ -106,3 +106,62 @@ CATALOG = {"poisson2d": poisson2d, "helmholtz_bumps": helmholtz_bumps, "laplace_
 def rel_linf(u, ref):
     """error_report rel L-inf (proj/src/problems.cpp:270-293)."""
     return float(np.abs(u - ref).max() / np.abs(ref).max())
+
+
+# ---- ItI problems (proj/src/problems.cpp:76-152) -------------------------------------------------
+@dataclass
+class ItiProblem:
+    name: str
+    eta: float
+    terms: list
+    source_re: Field | None
+    source_im: Field | None
+    impedance: Callable | None   # (points) -> incoming impedance data du/dn + i eta u (None: radiation)
+    exact: Callable | None = None
+    lo: float = -1.0
+    hi: float = 1.0
+    dim: int = 2
+
+
+def _impedance(x, u, grad, eta):
+    """du/dn + i eta u on the root boundary points (faces S, E, N, W of the square)."""
+    nb = len(x)
+    side = np.repeat(np.arange(4), nb // 4)
+    nrm = np.array([[0, -1], [1, 0], [0, 1], [-1, 0]], dtype=float)[side]
+    gx, gy = grad(x)
+    return nrm[:, 0] * gx + nrm[:, 1] * gy + 1j * eta * u(x)
+
+
+def helmholtz_robin2d(tree) -> ItiProblem:
+    """make_manufactured_2d_iti (problems.cpp:76-107): Delta u + (1 + exp(-50|x|^2)) u = f with
+    u = e^{20 i x1} + e^{30 i x2}, impedance data (eta = 1).  The complex source is sampled at the
+    leaf points of `tree` (SPEC.md:545 gate: p=16 L=4 rel Linf < 1e-6)."""
+    from .hps import FIELD_SAMPLED, tree_leaf_points_of
+    q = Field(FIELD_BUMPS, (1.0, 1.0, 50.0), centers=np.zeros((1, 3)))
+    terms = [Term(ROLE_LAPLACIAN, Field(FIELD_CONST, (1.0,))), Term(ROLE_ZEROTH, q)]
+
+    def u(x):
+        return np.exp(20j * x[..., 0]) + np.exp(30j * x[..., 1])
+
+    def grad(x):
+        return 20j * np.exp(20j * x[..., 0]), 30j * np.exp(30j * x[..., 1])
+
+    pts = tree_leaf_points_of(tree)
+    qv = 1.0 + np.exp(-50.0 * (pts[..., 0] ** 2 + pts[..., 1] ** 2))
+    f = -400.0 * np.exp(20j * pts[..., 0]) - 900.0 * np.exp(30j * pts[..., 1]) + qv * u(pts)
+    return ItiProblem("helmholtz_robin2d", 1.0, terms, Field(FIELD_SAMPLED, samples=np.ascontiguousarray(f.real)),
+                      Field(FIELD_SAMPLED, samples=np.ascontiguousarray(f.imag)),
+                      lambda x: _impedance(x, u, grad, 1.0), u)
+
+
+def scatter2d(k=20.0, seed=7) -> ItiProblem:
+    """make_scattering (problems.cpp:109-152): Delta u + k^2 (1 + q) u = -k^2 q e^{i k x1}, q = ten seeded
+    Gaussian bumps exp(-50 |x - z|^2), radiation closure at the root (eta = k)."""
+    z = bump_centers(seed, 10, 2)
+    k2 = k * k
+    terms = [Term(ROLE_LAPLACIAN, Field(FIELD_CONST, (1.0,))),
+             Term(ROLE_ZEROTH, Field(FIELD_BUMPS, (k2, k2, 50.0), centers=z))]
+    # -k^2 q (cos k x1 + i sin k x1): BUMPS_SIN with phases pi/2 (cos) and 0 (sin)
+    src_re = Field(FIELD_BUMPS_SIN, (-k2, 0.0, 50.0, k, 0.0, 0.0, np.pi / 2), centers=z)
+    src_im = Field(FIELD_BUMPS_SIN, (-k2, 0.0, 50.0, k, 0.0, 0.0, 0.0), centers=z)
+    return ItiProblem(f"scatter2d(k={k:g},seed={seed})", k, terms, src_re, src_im, None)

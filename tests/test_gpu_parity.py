@@ -321,3 +321,47 @@ def test_iti_errors():
     s.build()
     with pytest.raises(H.HpsError):
         s.solve(np.zeros(s.nb_root))   # complex variant: solve_complex
+
+
+def test_iti_helmholtz_robin2d_gate():
+    """SPEC.md:545 accuracy gate of the reference's ItI problem (make_manufactured_2d_iti,
+    problems.cpp:76-107, complex source): p=16 L=4 rel Linf < 1e-6."""
+    tree = H.build_uniform_tree(-1.0, 1.0, 4, 2, 16)
+    pr = PR.helmholtz_robin2d(tree)
+    s = H.HpsSolver(tree, pr.terms, pr.source_re, source_imag=pr.source_im, variant="iti", eta=pr.eta)
+    s.build()
+    u = s.solve_complex(pr.impedance(s.root_boundary_points()))
+    ex = pr.exact(s.leaf_points())
+    assert np.abs(u - ex).max() / np.abs(ex).max() < 1e-6
+
+
+@pytest.mark.parametrize("L", [3, 4])
+def test_iti_scatter2d_radiation_closure(L):
+    """make_scattering + solve_radiation (problems.cpp:109-152, solver.cpp:254-259): the root data
+    closes T g = -h, i.e. the outgoing impedance du/dn - i eta u of the computed field vanishes on the
+    whole root boundary (checked leaf by leaf with the host QH operator, independent of the device
+    path); the field is resolution-stable between L = 3 and 4."""
+    import ctypes as C
+    pr = PR.scatter2d(k=20.0)
+    tree = H.build_uniform_tree(-1.0, 1.0, L, 2, 16)
+    s = H.HpsSolver(tree, pr.terms, pr.source_re, source_imag=pr.source_im, variant="iti", eta=pr.eta,
+                    build_root_T=True)
+    s.build()
+    u, g = s.solve_radiation(want_g=True)
+    p, q = 16, 14
+    QHr, QHi = np.zeros((p * p, 4 * q)), np.zeros((p * p, 4 * q))
+    lib = H.lib()
+    lib.hpsg_iti_leaf_ops.argtypes = [C.c_int, C.c_double, C.c_double] + [C.POINTER(C.c_double)] * 5
+    assert lib.hpsg_iti_leaf_ops(p, pr.eta, 2.0 / 2 ** L, None, None, None, H.hps._dp(QHr), H.hps._dp(QHi)) == 0
+    QH = (QHr + 1j * QHi).T
+    lp = s.leaf_points()
+    worst = 0.0
+    for leaf in range(tree.n_leaves):
+        out = QH @ u[leaf]
+        x0, x1 = lp[leaf, :, 0].min(), lp[leaf, :, 0].max()
+        y0, y1 = lp[leaf, :, 1].min(), lp[leaf, :, 1].max()
+        for sd, on in ((0, y0 < -1 + 1e-12), (1, x1 > 1 - 1e-12), (2, y1 > 1 - 1e-12), (3, x0 < -1 + 1e-12)):
+            if on:
+                worst = max(worst, np.abs(out[sd * q:(sd + 1) * q]).max())
+    assert worst < 1e-11 * np.abs(g).max()
+    assert abs(np.abs(u).max() - 3.0152) < 2e-3
