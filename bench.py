@@ -235,6 +235,7 @@ def run_b200(args):
     if world == 1 and not args.no_extras and not args.profile:
         out["configs_extra"]["config3_new_sources"] = bench_new_sources(torch, args)
         out["configs_extra"]["config4_3d"] = bench_3d(torch)
+        out["configs_extra"]["iti_scatter2d"] = bench_iti(torch)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"], par = cpu_baseline(args, prob, u_gpu)
         out["accuracy"].update(par)
@@ -306,6 +307,30 @@ def bench_new_sources(torch, args, nsrc=256, chunk=32):
                         f"data on one build with kept leaf factors, chunks of {chunk}",
             "ms": ms, "ms_per_source": ms / nsrc, "rhs_dof_per_s": nsrc * tree.total_points / (ms / 1e3),
             "build_ms_keep_factors": st["t_build_ms"], "device_gb": st["device_bytes"] / 1e9}
+
+
+def bench_iti(torch, L=6, p=16, k=40.0, steps=2):
+    """SURVEY 8f rank 1 (ItI variant): make_scattering (problems.cpp:109-152) with the radiation closure,
+    build (leaf ItI maps, merge_iti, root T LU) + solve_radiation, complex128 in real-equivalent form."""
+    import paper_2503_17535_b200 as H
+    from paper_2503_17535_b200 import problems as PR
+    pr = PR.scatter2d(k=k)
+    tree = H.build_uniform_tree(-1.0, 1.0, L, 2, p)
+    s = H.HpsSolver(tree, pr.terms, pr.source_re, source_imag=pr.source_im, variant="iti", eta=pr.eta,
+                    build_root_T=True)
+    s.build()
+    s.solve_radiation()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        s.build()
+        u = s.solve_radiation()
+    ms = (time.perf_counter() - t0) / steps * 1e3
+    st = s.stats()
+    s.close()
+    return {"workload": f"ItI scatter2d k={k:g}, p={p}, L={L} (N={tree.total_points}), radiation closure",
+            "ms_per_step": ms, "value": tree.total_points / (ms / 1e3), "unit": "DOF/s (wall clock, host result)",
+            "build_ms": st["t_build_ms"], "solve_ms": st["t_solve_ms"], "max_abs_u": float(np.abs(u).max())}
 
 
 def bench_3d(torch, L=4, p=8, steps=2):
