@@ -158,6 +158,18 @@ int hpsg_solve_complex(hpsg_ctx* ctx, const double* g_root, int nrhs, double* u_
  * downward pass; needs build_root_T.  u_out: n_leaves x p^2 interleaved complex; g_out (optional):
  * the closing root data (root_bsize interleaved complex). */
 int hpsg_solve_radiation(hpsg_ctx* ctx, double* u_out, double* g_out);
+/* ---- output layer, on the device-resident solution of hpsg_solve_device /
+ * hpsg_solve_complex's device twin: d_u = n_leaves x p^dim values (is_complex: interleaved).
+ * evaluate_at(field, points) (downpass.hpp:19, downpass.cpp:13-95): points_host npts x 3 -> out_host
+ * (npts, or 2 npts interleaved); points outside the domain are rejected like the reference. */
+int hpsg_evaluate_at(hpsg_ctx* ctx, const double* d_u, int is_complex, const double* points_host, int npts,
+                     double* out_host);
+/* error_report(field, exact) (problems.hpp:81, problems.cpp:270-293) against a built-in exact
+ * field (exact_imag may be NULL): relative L-inf and L2 over every leaf Chebyshev point, reduced on
+ * the device (no copy of the solution). */
+int hpsg_error_report(hpsg_ctx* ctx, const double* d_u, int is_complex, const hpsg_field* exact,
+                      const hpsg_field* exact_imag, double* rel_linf, double* rel_l2);
+
 /* host-only: the ItI leaf operators of assemble_iti_ops_2d (spectral.cpp:312-368), column-major:
  * G = Gr + i Gi ((4p-4) x p^2), P ((4p-4) x 4q), QH = QHr + i QHi (4q x p^2); any pointer may be NULL */
 int hpsg_iti_leaf_ops(int p, double eta, double side, double* Gr, double* Gi, double* P, double* QHr, double* QHi);

@@ -1463,6 +1463,66 @@ int hpsg_tree_root_points(const hpsg_tree* t, double* xyz) {
   return HPSG_OK;
 }
 
+int hpsg_evaluate_at(hpsg_ctx* c, const double* d_u, int is_complex, const double* points, int npts, double* out) {
+  if (!c || !d_u || (npts > 0 && (!points || !out)) || npts < 0) return HPSG_ERR_INVALID;
+  if (c->T.cut || c->T.root_depth) return fail(c, HPSG_ERR_STATE, "evaluate_at: whole-tree solver only");
+  const int dim = c->tree.dim;
+  for (int i = 0; i < npts; ++i)
+    for (int k = 0; k < dim; ++k)
+      if (!(points[3 * i + k] >= c->tree.lo && points[3 * i + k] <= c->tree.hi))
+        return fail(c, HPSG_ERR_INVALID, "evaluate_at: point outside the domain");
+  return guarded(c, [&] {
+    DevBuf xin, res;
+    xin.alloc(size_t(npts) * 3 * 8, nullptr);
+    res.alloc(size_t(npts) * (is_complex ? 2 : 1) * 8, nullptr);
+    ck(cudaMemcpyAsync(xin.p, points, size_t(npts) * 24, cudaMemcpyHostToDevice, c->st), "points H2D");
+    hpsk::EvalArgs a{dim, c->tree.p, c->tree.L, is_complex ? 1 : 0, npts, c->tree.lo, c->tree.hi, c->cheb.d(), d_u,
+                     xin.d(), res.d()};
+    hpsk::launch_evaluate_at(a, c->st);
+    ck(cudaGetLastError(), "evaluate_at");
+    ck(cudaMemcpyAsync(out, res.p, size_t(npts) * (is_complex ? 2 : 1) * 8, cudaMemcpyDeviceToHost, c->st), "D2H");
+    ck(cudaStreamSynchronize(c->st), "evaluate_at sync");
+  });
+}
+
+int hpsg_error_report(hpsg_ctx* c, const double* d_u, int is_complex, const hpsg_field* exact,
+                      const hpsg_field* exact_imag, double* rel_linf, double* rel_l2) {
+  if (!c || !d_u || !exact || !rel_linf || !rel_l2) return HPSG_ERR_INVALID;
+  if (c->T.cut) return fail(c, HPSG_ERR_STATE, "error_report: a cut part has no leaves");
+  return guarded(c, [&] {
+    hpsk::ErrArgs a{};
+    a.dim = c->tree.dim;
+    a.p = c->tree.p;
+    a.npts_leaf = c->iti ? c->iops.n : c->ops.n;
+    a.is_complex = is_complex ? 1 : 0;
+    a.n_leaves = c->T.n_leaves();
+    a.leaf_box = c->leaf_box.d();
+    a.cheb = c->cheb.d();
+    a.u = d_u;
+    a.ex_re = make_dev_field(c, *exact, true);
+    a.has_im = exact_imag ? 1 : 0;
+    if (exact_imag) a.ex_im = make_dev_field(c, *exact_imag, true);
+    DevBuf part;
+    part.alloc(size_t(148 * 4) * 4 * 8, nullptr);
+    a.partial = part.d();
+    const int nb = hpsk::launch_error_partials(a, c->st);
+    ck(cudaGetLastError(), "error_report");
+    std::vector<double> h(size_t(nb) * 4);
+    ck(cudaMemcpyAsync(h.data(), part.p, h.size() * 8, cudaMemcpyDeviceToHost, c->st), "D2H");
+    ck(cudaStreamSynchronize(c->st), "error_report sync");
+    double ni = 0, di = 0, n2 = 0, d2 = 0;
+    for (int b = 0; b < nb; ++b) {
+      ni = std::max(ni, h[4 * b]);
+      di = std::max(di, h[4 * b + 1]);
+      n2 += h[4 * b + 2];
+      d2 += h[4 * b + 3];
+    }
+    if (!(di > 0.0)) throw HpsError{HPSG_ERR_INVALID, "error_report: zero-norm reference"};
+    *rel_linf = ni / di;
+    *rel_l2 = std::sqrt(n2 / d2);
+  });
+}
+
 int hpsg_iti_leaf_ops(int p, double eta, double side, double* Gr, double* Gi, double* P, double* QHr, double* QHi) {
   try {
     const hpsg::ItiLeafOperators o = hpsg::make_iti_leaf_operators(p, eta, side);

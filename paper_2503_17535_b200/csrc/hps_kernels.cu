@@ -138,6 +138,109 @@ __global__ void complex_to_planar_kernel(double* g_re, const double* g, int nb, 
   }
 }
 
+__global__ void evaluate_at_kernel(const EvalArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.npts) return;
+  const int p = a.p, dim = a.dim, nchild = dim == 2 ? 4 : 8;
+  double x[3] = {a.x[3 * i], a.x[3 * i + 1], a.x[3 * i + 2]};
+  double lo[3] = {a.lo, a.lo, a.lo}, hi[3] = {a.hi, a.hi, a.hi};
+  long long ord = 0;
+  for (int l = 0; l < a.L; ++l) {  // locate_leaf: child slot of the offsets (downpass.cpp:13-27)
+    int o[3] = {0, 0, 0};
+    for (int k = 0; k < dim; ++k) {
+      const double mid = 0.5 * (lo[k] + hi[k]);
+      o[k] = x[k] >= mid ? 1 : 0;
+      if (o[k]) lo[k] = mid; else hi[k] = mid;
+    }
+    const int q = (o[0] == 0 && o[1] == 0) ? 0 : (o[0] == 1 && o[1] == 0) ? 1 : (o[0] == 1 && o[1] == 1) ? 2 : 3;
+    ord = ord * nchild + q + (dim == 3 && o[2] ? 4 : 0);
+  }
+  // barycentric weights of the Chebyshev-Lobatto interpolant (downpass.cpp:31-53)
+  double w[3][kLeafMaxP];
+  for (int k = 0; k < dim; ++k) {
+    const double t = (2.0 * x[k] - lo[k] - hi[k]) / (hi[k] - lo[k]);
+    int hit = -1;
+    for (int j = 0; j < p; ++j)
+      if (t == a.cheb[j]) hit = j;
+    if (hit >= 0) {
+      for (int j = 0; j < p; ++j) w[k][j] = j == hit ? 1.0 : 0.0;
+      continue;
+    }
+    double den = 0.0;
+    for (int j = 0; j < p; ++j) {
+      double bw = (j % 2 == 0) ? 1.0 : -1.0;
+      if (j == 0 || j == p - 1) bw *= 0.5;
+      w[k][j] = bw / (t - a.cheb[j]);
+      den += w[k][j];
+    }
+    for (int j = 0; j < p; ++j) w[k][j] /= den;
+  }
+  const long long np = dim == 2 ? (long long)p * p : (long long)p * p * p;
+  const double* u = a.u + ord * np * (a.is_complex ? 2 : 1);
+  double re = 0.0, im = 0.0;
+  for (int i1 = 0; i1 < p; ++i1) {
+    if (w[0][i1] == 0.0) continue;
+    for (int i2 = 0; i2 < p; ++i2) {
+      if (w[1][i2] == 0.0) continue;
+      const double w12 = w[0][i1] * w[1][i2];
+      for (int i3 = 0; i3 < (dim == 3 ? p : 1); ++i3) {
+        const double ww = dim == 3 ? w12 * w[2][i3] : w12;
+        const long long idx = dim == 3 ? ((long long)i1 * p + i2) * p + i3 : (long long)i1 * p + i2;
+        if (a.is_complex) {
+          re += ww * u[2 * idx];
+          im += ww * u[2 * idx + 1];
+        } else {
+          re += ww * u[idx];
+        }
+      }
+    }
+  }
+  if (a.is_complex) {
+    a.out[2 * i] = re;
+    a.out[2 * i + 1] = im;
+  } else {
+    a.out[i] = re;
+  }
+}
+
+__global__ void __launch_bounds__(256) error_partials_kernel(const ErrArgs a) {
+  __shared__ double red[4][256];
+  const long long total = a.n_leaves * a.npts_leaf;
+  double ninf = 0.0, dinf = 0.0, n2 = 0.0, d2 = 0.0;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long leaf = e / a.npts_leaf;
+    const int pt = int(e % a.npts_leaf);
+    int ci[3];
+    leaf_decode(pt, a.p, a.dim, ci);
+    const double* box = a.leaf_box + leaf * 6;
+    double x[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < a.dim; ++k)
+      x[k] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(box[k], box[3 + k])),
+                       __dmul_rn(__dmul_rn(0.5, __dsub_rn(box[3 + k], box[k])), a.cheb[ci[k]]));
+    const double er = eval_field(a.ex_re, x, a.dim, leaf, pt, a.npts_leaf);
+    const double ei = a.has_im ? eval_field(a.ex_im, x, a.dim, leaf, pt, a.npts_leaf) : 0.0;
+    const double ur = a.is_complex ? a.u[2 * e] : a.u[e], ui = a.is_complex ? a.u[2 * e + 1] : 0.0;
+    const double dr = ur - er, di = ui - ei;
+    ninf = fmax(ninf, sqrt(dr * dr + di * di));
+    dinf = fmax(dinf, sqrt(er * er + ei * ei));
+    n2 += dr * dr + di * di;
+    d2 += er * er + ei * ei;
+  }
+  red[0][threadIdx.x] = ninf, red[1][threadIdx.x] = dinf, red[2][threadIdx.x] = n2, red[3][threadIdx.x] = d2;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      red[0][threadIdx.x] = fmax(red[0][threadIdx.x], red[0][threadIdx.x + o]);
+      red[1][threadIdx.x] = fmax(red[1][threadIdx.x], red[1][threadIdx.x + o]);
+      red[2][threadIdx.x] += red[2][threadIdx.x + o];
+      red[3][threadIdx.x] += red[3][threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < 4) a.partial[blockIdx.x * 4 + threadIdx.x] = red[threadIdx.x][0];
+}
+
 constexpr int kGatherThreads = 256;
 
 // One warp per destination column: (slot, cc) are uniform over the column and the rows of each
@@ -283,6 +386,16 @@ void launch_iti_leaf_output(double* u, const double* Ui, int n, int nrhs, int n_
 void launch_complex_to_planar(double* g_re, const double* g, int nb, int nrhs, cudaStream_t st) {
   const long long total = (long long)nb * nrhs;
   complex_to_planar_kernel<<<(unsigned)std::max<long long>(1, (total + 255) / 256), 256, 0, st>>>(g_re, g, nb, nrhs);
+}
+
+void launch_evaluate_at(const EvalArgs& a, cudaStream_t st) {
+  if (a.npts <= 0) return;
+  evaluate_at_kernel<<<(a.npts + 127) / 128, 128, 0, st>>>(a);
+}
+int launch_error_partials(const ErrArgs& a, cudaStream_t st) {
+  const int blocks = 148 * 4;
+  error_partials_kernel<<<blocks, 256, 0, st>>>(a);
+  return blocks;
 }
 
 void launch_leaf_assemble(const LeafAsmArgs& a, int n_leaves, cudaStream_t st) {

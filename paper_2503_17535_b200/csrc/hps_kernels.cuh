@@ -82,6 +82,32 @@ void launch_iti_leaf_output(double* u, const double* Ui, int n, int nrhs, int n_
 // g_re (planar real-equivalent, nb_re x nrhs) from interleaved complex g (nrhs x nb)
 void launch_complex_to_planar(double* g_re, const double* g, int nb, int nrhs, cudaStream_t st);
 
+// ---- output layer on the device -------------------------------------------
+// evaluate_at (proj/src/downpass.cpp:13-95): locate_leaf by midpoint descent + tensor barycentric
+// interpolation of the leaf's Chebyshev values; u: n_leaves x p^dim (real, or interleaved complex).
+struct EvalArgs {
+  int dim, p, L, is_complex, npts;
+  double lo, hi;
+  const double* cheb;   // p nodes, descending
+  const double* u;
+  const double* x;      // npts x 3
+  double* out;          // npts (real) or 2 npts (complex)
+};
+void launch_evaluate_at(const EvalArgs& a, cudaStream_t st);
+// error_report (proj/src/problems.cpp:270-293) partial reductions: per block {max|u-ex|, max|ex|,
+// sum|u-ex|^2, sum|ex|^2} over every leaf Chebyshev point; exact = re + i im (im may be kind < 0)
+struct ErrArgs {
+  int dim, p, npts_leaf, is_complex;
+  long long n_leaves;
+  const double* leaf_box;
+  const double* cheb;
+  const double* u;
+  DevField ex_re, ex_im;
+  int has_im;
+  double* partial;      // gridDim x 4
+};
+int launch_error_partials(const ErrArgs& a, cudaStream_t st);  // returns the number of blocks
+
 // Fused stage 1 (leaf_fused.cu): assembly + -L_ie P + GEPP/solve + [h|T] per leaf in one
 // persistent kernel over an L2-resident per-CTA workspace.
 struct LeafFusedArgs {

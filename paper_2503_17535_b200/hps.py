@@ -94,6 +94,9 @@ def lib():
         L.hpsg_solve_new_source.argtypes = [vp, dp, dp, C.c_int, dp]
         L.hpsg_solve_complex.argtypes = [vp, dp, C.c_int, dp]
         L.hpsg_solve_radiation.argtypes = [vp, dp, dp]
+        L.hpsg_evaluate_at.argtypes = [vp, C.c_void_p, C.c_int, dp, C.c_int, dp]
+        L.hpsg_error_report.argtypes = [vp, C.c_void_p, C.c_int, C.POINTER(_Field), C.POINTER(_Field),
+                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.hpsg_solve_new_source_device.argtypes = [vp, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
         L.hpsg_build.argtypes = [vp]
         L.hpsg_solve.argtypes = [vp, dp, C.c_int, dp, dp]
@@ -334,6 +337,26 @@ class HpsSolver:
         self._check(lib().hpsg_solve_complex(self._h, g2.ctypes.data_as(C.POINTER(C.c_double)), nrhs,
                                              u.ctypes.data_as(C.POINTER(C.c_double))), "solve")
         return u[0] if single else u
+
+    def evaluate_at(self, d_u_ptr, points, is_complex=False):
+        """evaluate_at(field, points) (downpass.cpp:13-95) on a device-resident solution (pointer to
+        n_leaves x p^d values, interleaved complex when is_complex) at host points (npts, 3)."""
+        x = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+        out = np.empty(len(x), dtype=np.complex128 if is_complex else np.float64)
+        self._check(lib().hpsg_evaluate_at(self._h, C.c_void_p(d_u_ptr), int(is_complex), _dp(x), len(x),
+                                           out.ctypes.data_as(C.POINTER(C.c_double))), "evaluate_at")
+        return out
+
+    def error_report(self, d_u_ptr, exact: Field, exact_imag: Field | None = None, is_complex=False):
+        """error_report (problems.cpp:270-293) on the device: (rel L-inf, rel L2) vs a built-in field."""
+        keep = []
+        fe = exact.to_c(keep)
+        fi = exact_imag.to_c(keep) if exact_imag is not None else None
+        li, l2 = C.c_double(), C.c_double()
+        self._check(lib().hpsg_error_report(self._h, C.c_void_p(d_u_ptr), int(is_complex), C.byref(fe),
+                                            C.byref(fi) if fi is not None else None, C.byref(li), C.byref(l2)),
+                    "error_report")
+        return li.value, l2.value
 
     def solve_radiation(self, want_g=False):
         """HpsSolver::solve_radiation() (solver.cpp:254-259): root data closing T g = -h (ItI,

@@ -365,3 +365,31 @@ def test_iti_scatter2d_radiation_closure(L):
                 worst = max(worst, np.abs(out[sd * q:(sd + 1) * q]).max())
     assert worst < 1e-11 * np.abs(g).max()
     assert abs(np.abs(u).max() - 3.0152) < 2e-3
+
+
+def test_evaluate_at_and_error_report():
+    """Device output layer: evaluate_at (downpass.cpp:13-95) reproduces the field at
+    the leaf Chebyshev points and interpolates spectrally inside leaves; error_report
+    (problems.cpp:270-293) reduced on the device equals the host computation."""
+    import torch
+    prob = PR.helmholtz_bumps()
+    s = gpu_solver(prob, 16, 4, literal=False, root_implicit=True)
+    g = torch.tensor(prob.boundary(s.root_boundary_points()), device="cuda")
+    u = torch.empty((s.n_leaves, s.npts), dtype=torch.float64, device="cuda")
+    s.solve_device(g.data_ptr(), 1, u.data_ptr())
+    lp = s.leaf_points()
+    pick = lp.reshape(-1, 3)[::97]
+    # leaf-boundary points belong to several leaves: locate_leaf's >= rule may pick a neighbour, whose
+    # polynomial agrees there to the HPS interface consistency (~1e-11)
+    assert np.abs(s.evaluate_at(u.data_ptr(), pick) - u.cpu().numpy().reshape(-1)[::97]).max() < 1e-9
+    rng = np.random.default_rng(0)
+    xs = np.zeros((200, 3))
+    xs[:, :2] = rng.uniform(-1, 1, (200, 2))
+    assert np.abs(s.evaluate_at(u.data_ptr(), xs) - prob.exact(xs)).max() < 1e-7
+    exact = H.Field(H.FIELD_PLANE_SIN, (1.0, 30.0, 0.0, 0.0, 0.3))   # u = sin(30 x1 + 0.3)
+    li, l2 = s.error_report(u.data_ptr(), exact)
+    uh, ex = u.cpu().numpy(), prob.exact(lp)
+    assert abs(li - np.abs(uh - ex).max() / np.abs(ex).max()) < 1e-14
+    assert abs(l2 - np.sqrt(((uh - ex) ** 2).sum() / (ex ** 2).sum())) < 1e-14
+    with pytest.raises(H.HpsError):
+        s.evaluate_at(u.data_ptr(), np.array([[1.5, 0.0, 0.0]]))
