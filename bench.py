@@ -236,6 +236,8 @@ def run_b200(args):
         out["configs_extra"]["config3_new_sources"] = bench_new_sources(torch, args)
         out["configs_extra"]["config4_3d"] = bench_3d(torch)
         out["configs_extra"]["iti_scatter2d"] = bench_iti(torch)
+        out["configs_extra"]["subtree_recompute_L8"] = bench_recompute(torch, args, 8, 2)
+        out["configs_extra"]["subtree_recompute_L9"] = bench_recompute(torch, args, 9, 2)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"], par = cpu_baseline(args, prob, u_gpu)
         out["accuracy"].update(par)
@@ -307,6 +309,37 @@ def bench_new_sources(torch, args, nsrc=256, chunk=32):
                         f"data on one build with kept leaf factors, chunks of {chunk}",
             "ms": ms, "ms_per_source": ms / nsrc, "rhs_dof_per_s": nsrc * tree.total_points / (ms / 1e3),
             "build_ms_keep_factors": st["t_build_ms"], "device_gb": st["device_bytes"] / 1e9}
+
+
+def bench_recompute(torch, args, L, depth, steps=1):
+    """The paper's memory strategy (subtree recomputation, PAPER.md:629 -- the BASELINE.md number is
+    this mode: 4.02 s at p=16 L=8 on an H100; L=9: 17.43 s): only the depth-`depth` subtree roots'
+    [h|T] survive the build, each subtree is rebuilt for its downward pass (one reused workspace)."""
+    import paper_2503_17535_b200 as H
+    from paper_2503_17535_b200 import problems as PR
+    from paper_2503_17535_b200.recompute import SubtreeRecomputeSolver
+    prob = PR.helmholtz_bumps(k=args.k, seed=args.seed)
+    tree = H.build_uniform_tree(prob.lo, prob.hi, L, 2, args.p)
+    rs = SubtreeRecomputeSolver(tree, prob.terms, prob.source, depth=depth, literal_sign=False,
+                                root_implicit_S=not args.explicit_root)
+    g = torch.tensor(prob.boundary(rs.root_boundary_points()), device="cuda")
+    u = torch.empty((1, tree.n_leaves, tree.p ** 2), dtype=torch.float64, device="cuda")
+    rs.build()
+    rs.solve_device(g, u)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        rs.build()
+        rs.solve_device(g, u)
+    torch.cuda.synchronize()
+    sec = (time.perf_counter() - t0) / steps
+    free, total = torch.cuda.mem_get_info()
+    rs.close()
+    paper = {8: 4.02, 9: 17.43}.get(L)
+    return {"workload": f"2D Helmholtz p={tree.p} L={L} (N={tree.total_points}), subtree recomputation at depth "
+                        f"{depth} (build + solve, wall clock)", "s_per_step": sec,
+            "value": tree.total_points / sec, "unit": "DOF/s", "device_used_gb": (total - free) / 1e9,
+            "paper_h100_subtree_recompute_s": paper, "speedup_vs_paper": (paper / sec) if paper else None}
 
 
 def bench_iti(torch, L=6, p=16, k=40.0, steps=2):

@@ -131,6 +131,9 @@ typedef struct {
 } hpsg_part;
 int hpsg_create_part(const hpsg_tree* tree, const hpsg_part* part, const hpsg_term* terms, int n_terms,
                      const hpsg_field* source, const hpsg_options* opts, hpsg_ctx** out);
+/* move a part to another subtree of the same depth (same sizes, new boxes): the device workspace is
+ * reused, so subtree recomputation costs no allocation; not for HPSG_FIELD_SAMPLED coefficients */
+int hpsg_part_retarget(hpsg_ctx* ctx, long long root_index);
 /* n_cut input nodes of cut_nb boundary points each (0 for a part with real leaves); root_nb =
  * boundary points of the part root */
 int hpsg_part_sizes(hpsg_ctx* ctx, long long* n_cut, int* cut_nb, int* root_nb);

@@ -1622,6 +1622,25 @@ int hpsg_get_node(hpsg_ctx* c, int id, double* S, double* gtilde, double* Tm, do
   });
 }
 
+int hpsg_part_retarget(hpsg_ctx* c, long long root_index) {
+  if (!c) return HPSG_ERR_INVALID;
+  if (c->T.root_depth == 0) return fail(c, HPSG_ERR_INVALID, "hpsg_part_retarget: the tree root has no siblings");
+  if (c->iti) return fail(c, HPSG_ERR_STATE, "hpsg_part_retarget: DtN parts only");
+  for (int i = 0; i < c->nterms; ++i)
+    if (c->terms[i].f.kind == HPSG_FIELD_SAMPLED)
+      return fail(c, HPSG_ERR_STATE, "hpsg_part_retarget: sampled coefficients are tied to their leaves");
+  if (c->has_source && c->source.kind == HPSG_FIELD_SAMPLED)
+    return fail(c, HPSG_ERR_STATE, "hpsg_part_retarget: a sampled source is tied to its leaves");
+  return guarded(c, [&] {
+    const hpsg_tree& t = c->tree;
+    c->T = hpsg::make_part_tree(t.dim, t.p, t.L, t.lo, t.hi, c->T.root_depth, root_index, c->part.cut_depth);
+    c->part.root_index = root_index;
+    if (!c->T.cut) upload(c->leaf_box, c->T.leaf_lo, &c->dev_bytes, c->st);
+    ck(cudaStreamSynchronize(c->st), "retarget sync");
+    c->built = false;
+  });
+}
+
 int hpsg_part_sizes(hpsg_ctx* c, long long* n_cut, int* cut_nb, int* root_nb) {
   if (!c) return HPSG_ERR_INVALID;
   if (n_cut) *n_cut = c->T.cut ? c->T.n_leaves() : 0;

@@ -89,6 +89,7 @@ def lib():
                                        C.POINTER(_Field), C.POINTER(_Options), C.POINTER(vp)]
         L.hpsg_part_sizes.argtypes = [vp, C.POINTER(C.c_longlong), C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.hpsg_part_root_ht.argtypes = [vp, C.c_void_p]
+        L.hpsg_part_retarget.argtypes = [vp, C.c_longlong]
         L.hpsg_part_set_cut_ht.argtypes = [vp, C.c_longlong, C.c_void_p]
         L.hpsg_part_solve_cut.argtypes = [vp, C.c_void_p, C.c_int, C.c_void_p]
         L.hpsg_solve_new_source.argtypes = [vp, dp, dp, C.c_int, dp]
@@ -390,6 +391,11 @@ class HpsSolver:
     def root_ht_device(self, d_dst_ptr):
         """[h|T] of the part root (nb_root x (1+nb_root), column-major) -> device buffer."""
         self._check(lib().hpsg_part_root_ht(self._h, C.c_void_p(d_dst_ptr)), "part_root_ht")
+
+    def retarget(self, root_index):
+        """Move this subtree part to sibling subtree `root_index` of the same depth (workspace reused)."""
+        self._check(lib().hpsg_part_retarget(self._h, root_index), "part_retarget")
+        self.part = (self.part[0], root_index, self.part[2])
 
     def set_cut_ht_device(self, k, d_src_ptr):
         """Input [h|T] (cut_nb x (1+cut_nb)) of cut node k from a device buffer."""

@@ -393,3 +393,25 @@ def test_evaluate_at_and_error_report():
     assert abs(l2 - np.sqrt(((uh - ex) ** 2).sum() / (ex ** 2).sum())) < 1e-14
     with pytest.raises(H.HpsError):
         s.evaluate_at(u.data_ptr(), np.array([[1.5, 0.0, 0.0]]))
+
+
+@pytest.mark.parametrize("depth,recompute", [(1, True), (2, True), (2, False)])
+def test_subtree_recompute_matches_store(depth, recompute):
+    """Subtree recomputation (paper's memory strategy): only the depth-d subtree roots'
+    [h|T] and the top merges survive the build; each subtree is rebuilt (one retargeted part, no
+    allocation) for its downward pass.  Same field as the store-mode solver."""
+    import torch
+    from paper_2503_17535_b200.recompute import SubtreeRecomputeSolver
+    prob = PR.helmholtz_bumps()
+    tree = H.build_uniform_tree(prob.lo, prob.hi, 5, 2, 16)
+    ref = H.HpsSolver(tree, prob.terms, prob.source, literal_sign=False, root_implicit_S=True)
+    ref.build()
+    g = prob.boundary(ref.root_boundary_points())
+    u_ref = ref.solve(np.stack([g, -0.5 * g]))
+    rs = SubtreeRecomputeSolver(tree, prob.terms, prob.source, depth=depth, literal_sign=False,
+                                root_implicit_S=True, recompute=recompute)
+    for _ in range(2):   # the second build/solve reuses the retargeted part
+        rs.build()
+        u = rs.solve_device(torch.tensor(np.stack([g, -0.5 * g]), device="cuda")).cpu().numpy()
+        assert rel(u, u_ref) < 1e-12
+    rs.close()
