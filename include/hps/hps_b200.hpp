@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <array>
+#include <complex>
 #include <cstdint>
 #include <functional>
 #include <stdexcept>
@@ -90,7 +91,7 @@ enum class Variant { dtn, iti };  // proj/include/hps/spectral.hpp:87
 
 // proj/include/hps/solver.hpp:17-22 (+ the B200 options)
 struct SolverOptions {
-  bool build_root_T = false;      // radiation closure: not on this path (ItI is a later row)
+  bool build_root_T = false;      // ItI radiation closure (HpsSolverComplex::solve_radiation)
   bool root_implicit_S = false;   // MergeOptions::implicit_S at the root
   bool free_T_after_merge = false;
   bool quiet_warnings = false;
@@ -116,7 +117,7 @@ class HpsSolver {
       : tree_(&tree), opts_(opts) {
     (void)eta;
     if (variant != Variant::dtn) throw Error("HpsSolver<Real> drives the DtN variant");
-    if (opts.build_root_T) throw Error("hps_b200: build_root_T (radiation closure) is not on this path");
+    if (opts.build_root_T) throw Error("hps_b200: build_root_T is the ItI radiation closure (HpsSolverComplex)");
     hpsg_tree t{tree.dim, tree.p, tree.L, tree.domain.lo[0], tree.domain.hi[0]};
     const long long npts = tree.total_points();
     // leaf Chebyshev points, sampled like build_leaf/discretize_operator do on the host
@@ -250,6 +251,121 @@ class HpsSolver {
   hpsg_ctx* ctx_ = nullptr;
   std::vector<std::vector<double>> samples_;
   std::vector<double> src_samples_;
+};
+
+// proj/include/hps/solver.hpp:40-117 for S = Complex (Variant::iti, 2D): impedance-to-impedance
+// maps, solve(g_root) with incoming impedance data, solve_radiation() with build_root_T.  Complex
+// coefficient fields are real here (the reference's CoefficientField is real); the source may be
+// complex.
+using Complex = std::complex<double>;
+struct SolutionFieldC {
+  const DiscretizationTree* tree = nullptr;
+  std::vector<std::vector<Complex>> u;
+};
+
+class HpsSolverComplex {
+ public:
+  HpsSolverComplex(const DiscretizationTree& tree, Variant variant, double eta, std::vector<CoefficientField> terms,
+                   std::function<Complex(const Point&)> source, SolverOptions opts = {})
+      : tree_(&tree) {
+    if (variant != Variant::iti) throw Error("HpsSolver<Complex> drives the ItI variant");
+    if (tree.dim != 2) throw Error("local_solve_iti: 2D only");
+    hpsg_tree t{tree.dim, tree.p, tree.L, tree.domain.lo[0], tree.domain.hi[0]};
+    const long long npts = tree.total_points();
+    std::vector<double> xyz(size_t(npts) * 3);
+    if (hpsg_tree_leaf_points(&t, xyz.data()) != HPSG_OK) throw Error("hps_b200: invalid tree");
+    auto point = [&](long long i) {
+      Point x;
+      x[0] = xyz[3 * i], x[1] = xyz[3 * i + 1], x[2] = xyz[3 * i + 2];
+      return x;
+    };
+    std::vector<std::vector<double>> samples;
+    std::vector<hpsg_term> ct;
+    for (const CoefficientField& f : terms) {
+      std::vector<double> sv(static_cast<size_t>(npts));
+      for (long long i = 0; i < npts; ++i) sv[size_t(i)] = f.eval(point(i));
+      samples.push_back(std::move(sv));
+      hpsg_term tt{};
+      tt.role = static_cast<int>(f.role);
+      tt.axis = f.axis;
+      tt.axis2 = f.axis2;
+      tt.field.kind = HPSG_FIELD_SAMPLED;
+      ct.push_back(tt);
+    }
+    for (size_t i = 0; i < ct.size(); ++i) ct[i].field.samples = samples[i].data();
+    std::vector<double> sre, sim;
+    hpsg_field fre{}, fim{};
+    hpsg_options o{};
+    o.literal_sign = opts.literal_sign ? 1 : 0;
+    o.device = opts.device;
+    o.variant = HPSG_VARIANT_ITI;
+    o.eta = eta;
+    o.build_root_T = opts.build_root_T ? 1 : 0;
+    const hpsg_field* srcp = nullptr;
+    if (source) {
+      sre.resize(size_t(npts));
+      sim.resize(size_t(npts));
+      for (long long i = 0; i < npts; ++i) {
+        const Complex v = source(point(i));
+        sre[size_t(i)] = v.real(), sim[size_t(i)] = v.imag();
+      }
+      fre.kind = fim.kind = HPSG_FIELD_SAMPLED;
+      fre.samples = sre.data();
+      fim.samples = sim.data();
+      srcp = &fre;
+      o.source_imag = &fim;
+    }
+    const int rc = hpsg_create(&t, ct.data(), int(ct.size()), srcp, &o, &ctx_);
+    if (rc != HPSG_OK) {
+      const std::string msg = ctx_ ? hpsg_last_error(ctx_) : "no CUDA device";
+      hpsg_destroy(ctx_);
+      ctx_ = nullptr;
+      throw Error(msg);
+    }
+  }
+  HpsSolverComplex(const HpsSolverComplex&) = delete;
+  HpsSolverComplex& operator=(const HpsSolverComplex&) = delete;
+  ~HpsSolverComplex() { hpsg_destroy(ctx_); }
+
+  void build() { check(hpsg_build(ctx_)); }
+
+  std::vector<Point> root_boundary_points() const {
+    hpsg_stats st{};
+    check(hpsg_get_stats(ctx_, &st));
+    std::vector<double> xyz(size_t(st.root_bsize) * 3);
+    check(hpsg_root_boundary_points(ctx_, xyz.data()));
+    std::vector<Point> pts(size_t(st.root_bsize));
+    for (size_t i = 0; i < pts.size(); ++i) pts[i][0] = xyz[3 * i], pts[i][1] = xyz[3 * i + 1], pts[i][2] = xyz[3 * i + 2];
+    return pts;
+  }
+
+  SolutionFieldC solve(const std::vector<Complex>& g_root) const {
+    std::vector<Complex> u(size_t(tree_->total_points()));
+    check(hpsg_solve_complex(ctx_, reinterpret_cast<const double*>(g_root.data()), 1,
+                             reinterpret_cast<double*>(u.data())));
+    return split(u);
+  }
+
+  SolutionFieldC solve_radiation() const {
+    std::vector<Complex> u(size_t(tree_->total_points()));
+    check(hpsg_solve_radiation(ctx_, reinterpret_cast<double*>(u.data()), nullptr));
+    return split(u);
+  }
+
+ private:
+  SolutionFieldC split(const std::vector<Complex>& u) const {
+    SolutionFieldC f;
+    f.tree = tree_;
+    const long long nl = tree_->n_leaves(), np = tree_->total_points() / nl;
+    f.u.resize(size_t(nl));
+    for (long long l = 0; l < nl; ++l) f.u[size_t(l)].assign(u.begin() + l * np, u.begin() + (l + 1) * np);
+    return f;
+  }
+  void check(int rc) const {
+    if (rc != HPSG_OK) throw Error(hpsg_last_error(ctx_));
+  }
+  const DiscretizationTree* tree_;
+  hpsg_ctx* ctx_ = nullptr;
 };
 
 }  // namespace b200

@@ -187,6 +187,22 @@ def test_cpp_dropin_example_runs():
         assert rep["rel_linf"] < 1e-8
 
 
+def test_cpp_example_iti_robin():
+    """examples/iti_robin_b200.cpp: the ItI variant through the C++ drop-in header
+    (HpsSolverComplex, complex host source, impedance root data; SPEC.md:545 gate at p=16 L=4)."""
+    import json
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "examples", "iti_robin_b200")
+    src = os.path.join(root, "examples", "iti_robin_b200.cpp")
+    if not os.path.exists(exe) or os.path.getmtime(exe) < os.path.getmtime(src):
+        subprocess.run(["make", "-s", "-C", os.path.join(root, "paper_2503_17535_b200"), "example"], check=True)
+    r = subprocess.run([exe, "4", "16"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert json.loads(r.stdout)["rel_linf"] < 1e-6
+
+
 @pytest.mark.parametrize("p,L,literal", [(6, 2, True), (8, 2, False), (8, 3, False)])
 def test_3d_variable_poisson_parity(p, L, literal):
     """BASELINE configs[3] operator (div(eps grad u), gradient terms from the bump-gradient field,
