@@ -604,6 +604,8 @@ void run_leaf_stage(hpsg_ctx* c) {
       fprintf(stderr, "leaf_fused grid %d (%d CTAs/SM)\n", c->fused_grid, hpsk::leaf_fused_ctas_per_sm());
       fprintf(stderr, "leaf_fused LU leaf 0 sub-phases: gepp %lld exchange %lld trsm %lld update %lld\n", h[33], h[34],
               h[35], h[36]);
+      fprintf(stderr, "leaf_fused GEPP leaf 0: stage %lld warp-body %lld subtrsm %lld subupdate %lld\n", h[40], h[41],
+              h[42], h[43]);
     }
     f.n_leaves = nl;
     ck(hpsk::launch_leaf_fused(f, c->fused_grid, c->st), "leaf_fused");

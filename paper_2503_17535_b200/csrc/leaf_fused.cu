@@ -8,13 +8,13 @@
 //   A. operator assembly + source sampling (leaf_common.cuh, sparse grid lines);
 //      the 2*dim exterior neighbours of each interior row go to a shared list
 //   B. R = -L_ie P from that list (4 nonzeros per row in 2D instead of a dense GEMM)
-//   C. blocked GEPP with the RHS riding along.  Per 32-column panel each thread
-//      holds one panel row in registers: pivot = warp-shuffle argmax + one shared
-//      round (ties -> lowest current row, the LAPACK/Eigen rule), pivot row
-//      broadcast through shared memory, rank-1 updates in registers, positions
-//      tracked and written back once; composite-permutation row exchange of the
-//      other columns; unit-lower TRSM of U12 into shared memory; DMMA trailing
-//      update with L21 and U12 in shared memory (accumulators seeded from W)
+//   C. blocked GEPP with the RHS riding along.  Per 32-column panel staged in shared
+//      memory, warp 0 factors 8-column sub-panels (pivot = exact warp argmax on the
+//      IEEE bits via REDUX, ties -> lowest current row, the LAPACK/Eigen rule; rows
+//      exchanged across the whole panel) and all warps apply each sub-panel's TRSM
+//      and k = 8 DMMA update; then one composite-permutation row exchange of the
+//      other columns, unit-lower TRSM of U12, DMMA trailing update with L21 and U12
+//      in shared memory (accumulators seeded from W)
 //   D. blocked back substitution (U blocks staged in shared memory) -> [v_i | Y_i]
 //   E. [h | T] = Q_i [v_i | Y_i] + [0 | Q_e P] over shared k-chunks, 8x8 DMMA
 //      tiles distributed over all warps (T = Q Y, h = Q v; :140-141)
@@ -28,7 +28,10 @@ namespace hpsk {
 
 namespace {
 
-constexpr int kFT = 256;          // threads per CTA (two CTAs per SM)
+#ifndef HPS_LEAF_FT
+#define HPS_LEAF_FT 256
+#endif
+constexpr int kFT = HPS_LEAF_FT;  // threads per CTA (256: two CTAs per SM)
 constexpr int kFW = kFT / 32;     // warps
 constexpr int kNB = 32;           // panel width / k chunk
 constexpr int kMaxNI = 196;       // interior points (2D p <= 16)
@@ -38,7 +41,10 @@ constexpr int kBLD = kNB + 4;     // B-operand (k-major) leading dim, (36 % 16) 
 constexpr int kTileCols = 128;    // B-operand columns staged at a time
 constexpr int kMaxNz = kMaxNI * 4;
 constexpr int kRowsPerLane = (kMaxNI + 31) / 32;
-constexpr int kSub = 8;           // sub-panel width factored by one warp inside a panel
+#ifndef HPS_LEAF_SUB
+#define HPS_LEAF_SUB 8
+#endif
+constexpr int kSub = HPS_LEAF_SUB;  // sub-panel width factored by one warp inside a panel
 
 struct FusedSmem {
   LeafAsmSmemT<256, 16> asmb;
@@ -105,6 +111,8 @@ __device__ void update_smem(int m, int n, int k, const double* A, int lda, const
 template <int NQ>
 __device__ __forceinline__ void gepp_warp_body(FusedSmem& s, int rows, int sb, int se, int pnb, int j0) {
   const int lane = threadIdx.x & 31;
+  double pmn = s.pmin, pmx = s.pmax;
+  int fz = s.first_zero;
   for (int j = sb; j < se; ++j) {
     double* pj = s.pan + j * kPLD;
     double bv = -1.0;
@@ -141,13 +149,12 @@ __device__ __forceinline__ void gepp_warp_body(FusedSmem& s, int rows, int sb, i
         s.prow[bp] = t;
       }
     }
-    if (lane == 0) {
-      if (!(bv > 0.0) || !isfinite(bv)) {
-        if (s.first_zero < 0) s.first_zero = j0 + j;
-      } else {
-        s.pmin = fmin(s.pmin, bv);
-        s.pmax = fmax(s.pmax, bv);
-      }
+    // pivot statistics in registers (bv is warp-uniform), flushed once after the sub-panel
+    if (!(bv > 0.0) || !isfinite(bv)) {
+      if (fz < 0) fz = j0 + j;
+    } else {
+      pmn = fmin(pmn, bv);
+      pmx = fmax(pmx, bv);
     }
     __syncwarp();
     const double pv = pj[j];
@@ -192,14 +199,23 @@ __device__ __forceinline__ void gepp_warp_body(FusedSmem& s, int rows, int sb, i
     }
     __syncwarp();
   }
+  if (lane == 0) s.pmin = pmn, s.pmax = pmx, s.first_zero = fz;
 }
 
 // GEPP of panel columns [j0, j0+pnb) over rows [j0, ni) of W by ONE warp on the panel staged in
 // s.pan (rows physically exchanged; lane-strided rows, no CTA barrier per column).  Pivot = max
 // |a| with NaN ranked as +inf, ties -> lowest current row (the LAPACK/Eigen rule).  Writes the
 // factored panel back to W and fills the moved-row list for the other columns.
-__device__ void panel_gepp_warp(FusedSmem& s, double* W, int ni, int j0, int pnb) {
+__device__ void panel_gepp_warp(FusedSmem& s, double* W, int ni, int j0, int pnb, long long* prof = nullptr) {
   const int tid = threadIdx.x;
+  long long t0 = prof ? clock64() : 0;
+  auto tick = [&](int k) {
+    if (prof) {
+      const long long t = clock64();
+      prof[k] += t - t0;
+      t0 = t;
+    }
+  };
   const int rows = ni - j0;
   for (int e = tid; e < pnb * rows; e += kFT) {
     const int c = e / rows, r = e - c * rows;
@@ -207,6 +223,7 @@ __device__ void panel_gepp_warp(FusedSmem& s, double* W, int ni, int j0, int pnb
   }
   for (int r = tid; r < rows; r += kFT) s.prow[r] = r;
   __syncthreads();
+  tick(40);
   // kSub-column sub-panels: warp 0 factors one (swaps span the whole panel), then all warps apply
   // its L11^-1 to the sub-panel's rows of the later panel columns and the k <= kSub DMMA update
   const int nq = (rows + 31) / 32;
@@ -224,6 +241,7 @@ __device__ void panel_gepp_warp(FusedSmem& s, double* W, int ni, int j0, int pnb
       }
     }
     __syncthreads();
+    tick(41);
     if (se >= pnb) break;
     // U12 rows [sb, se) of columns [se, pnb): unit-lower forward substitution
     for (int c = se + tid; c < pnb; c += kFT) {
@@ -240,6 +258,7 @@ __device__ void panel_gepp_warp(FusedSmem& s, double* W, int ni, int j0, int pnb
         if (sb + i < se) pc[sb + i] = x[i];
     }
     __syncthreads();
+    tick(42);
     // rows [se, rows) x columns [se, pnb) -= L21 (k = se - sb) * U12: 8x8 DMMA tiles over all warps
     {
       const int lane = tid & 31, g = lane >> 2, t4 = lane & 3;
@@ -268,6 +287,7 @@ __device__ void panel_gepp_warp(FusedSmem& s, double* W, int ni, int j0, int pnb
       }
     }
     __syncthreads();
+    tick(43);
   }
   if (tid == 0) s.n_moved = 0;
   __syncthreads();
@@ -287,7 +307,7 @@ __device__ void panel_gepp_warp(FusedSmem& s, double* W, int ni, int j0, int pnb
 
 }  // namespace
 
-__global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs f) {
+__global__ void __launch_bounds__(kFT, 512 / kFT) leaf_fused_kernel(const LeafFusedArgs f) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FusedSmem& s = *reinterpret_cast<FusedSmem*>(smem_raw);
   const LeafAsmArgs& a = f.a;
@@ -345,7 +365,7 @@ __global__ void __launch_bounds__(kFT, 2) leaf_fused_kernel(const LeafFusedArgs 
     for (int j0 = 0; j0 < ni; j0 += kNB) {
       const int pnb = min(kNB, ni - j0), rows = ni - j0;
       substamp(0);
-      panel_gepp_warp(s, W, ni, j0, pnb);
+      panel_gepp_warp(s, W, ni, j0, pnb, (f.prof && blockIdx.x == 0 && tid == 0 && iter == 0) ? f.prof : nullptr);
       substamp(1);
       // row exchange of every other column; chunks end on column boundaries
       {

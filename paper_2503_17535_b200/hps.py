@@ -17,7 +17,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhps_b200.so")
+LIB_PATH = os.environ.get("HPS_B200_LIB") or os.path.join(HERE, "libhps_b200.so")  # env: developer A/B builds
 
 # status codes (include/hps_cuda.h)
 HPSG_OK, HPSG_ERR_INVALID, HPSG_ERR_SINGULAR_LEAF, HPSG_ERR_SINGULAR_MERGE, HPSG_ERR_NONFINITE, HPSG_ERR_OOM, \
