@@ -63,40 +63,58 @@ struct FusedSmem {
 };
 
 // C[m x n] (global, ldc) = C - A[m x k] (smem, lda) * B[k x n] (smem, k-major ldb), k <= 32,
-// 32x32 warp tiles; the accumulators are seeded with C so its load overlaps the fragment loads.
+// (8 UM) x (8 UN) warp tiles; the accumulators are seeded with C so its load overlaps the fragment
+// loads, and the fragments are double-buffered in registers (the loads of k-slice k0+4 are in
+// flight while the DMMAs of k0 issue).
+#ifndef HPS_LEAF_UM
+#define HPS_LEAF_UM 4
+#endif
+#ifndef HPS_LEAF_UN
+#define HPS_LEAF_UN 2
+#endif
 __device__ void update_smem(int m, int n, int k, const double* A, int lda, const double* B, int ldb, double* C,
                             int ldc) {
+  constexpr int UM = HPS_LEAF_UM, UN = HPS_LEAF_UN;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t4 = lane & 3;
-  const int tm_n = (m + 31) / 32, tn_n = (n + 31) / 32;
+  const int tm_n = (m + 8 * UM - 1) / (8 * UM), tn_n = (n + 8 * UN - 1) / (8 * UN);
   for (int t = warp; t < tm_n * tn_n; t += kFW) {
-    const int m0 = (t % tm_n) * 32, n0 = (t / tm_n) * 32;
-    double acc[4][4][2];
+    const int m0 = (t % tm_n) * 8 * UM, n0 = (t / tm_n) * 8 * UN;
+    double acc[UM][UN][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < UM; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < UN; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int r = m0 + i * 8 + g, c = n0 + j * 8 + t4 * 2 + h;
           acc[i][j][h] = (r < m && c < n) ? C[(long long)c * ldc + r] : 0.0;
         }
-    for (int k0 = 0; k0 < k; k0 += 4) {
-      const int kk = k0 + t4;
-      double af[4], bf[4];
+    double af[2][UM], bf[2][UN];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = kk < k ? -A[kk * lda + m0 + i * 8 + g] : 0.0;
+    for (int i = 0; i < UM; ++i) af[0][i] = t4 < k ? -A[t4 * lda + m0 + i * 8 + g] : 0.0;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = kk < k ? B[(n0 + j * 8 + g) * ldb + kk] : 0.0;
+    for (int j = 0; j < UN; ++j) bf[0][j] = t4 < k ? B[(n0 + j * 8 + g) * ldb + t4] : 0.0;
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+    for (int k0 = 0; k0 < kNB; k0 += 4) {
+      const int cur = (k0 / 4) & 1;
+      if (k0 >= k) break;
+      if (k0 + 4 < kNB) {
+        const int kk = k0 + 4 + t4;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int i = 0; i < UM; ++i) af[cur ^ 1][i] = kk < k ? -A[kk * lda + m0 + i * 8 + g] : 0.0;
+#pragma unroll
+        for (int j = 0; j < UN; ++j) bf[cur ^ 1][j] = kk < k ? B[(n0 + j * 8 + g) * ldb + kk] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < UM; ++i)
+#pragma unroll
+        for (int j = 0; j < UN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < UM; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < UN; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int r = m0 + i * 8 + g, c = n0 + j * 8 + t4 * 2 + h;
@@ -401,46 +419,51 @@ __global__ void __launch_bounds__(kFT, 512 / kFT) leaf_fused_kernel(const LeafFu
         }
       }
       substamp(2);
-      // U12 = L11^-1 A12 for all columns right of the panel -> W and s.tile (k-major)
+      // per chunk of up to kTileCols columns right of the panel: stage A12 (k-major) in s.tile,
+      // U12 = L11^-1 A12 in shared memory (one thread per column), then U12 back to W (coalesced)
+      // alongside the DMMA trailing update that reads it from s.tile
       const int rc0 = j0 + pnb, nrc = ncol - rc0;
-      for (int c = tid; c < nrc; c += kFT) {
-        double* col = W + (long long)(rc0 + c) * ni + j0;
-        double x[kNB];
+      for (int cc0 = 0; cc0 < nrc; cc0 += kTileCols) {
+        const int ncc = min(kTileCols, nrc - cc0);
+        for (int e0 = 0; e0 < ncc * kNB; e0 += 8 * kFT) {
+          double t[8];
 #pragma unroll
-        for (int jj = 0; jj < kNB; ++jj) x[jj] = jj < pnb ? col[jj] : 0.0;
-#pragma unroll
-        for (int ii = 0; ii < kNB - 1; ++ii)
-#pragma unroll
-          for (int jj = ii + 1; jj < kNB; ++jj) x[jj] -= s.pan[ii * kPLD + jj] * x[ii];
-#pragma unroll
-        for (int jj = 0; jj < kNB; ++jj)
-          if (jj < pnb) col[jj] = x[jj];
-      }
-      __syncthreads();
-      substamp(3);
-      if (rows > pnb)
-        for (int cc0 = 0; cc0 < nrc; cc0 += kTileCols) {
-          const int ncc = min(kTileCols, nrc - cc0);
-          // stage U12[:, cc0:cc0+ncc] (k-major) -- 8 independent loads per thread per batch
-          for (int e0 = 0; e0 < ncc * kNB; e0 += 8 * kFT) {
-            double t[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int e = e0 + tid + u * kFT;
-              const int kk = e % kNB, c = e / kNB;
-              t[u] = (e < ncc * kNB && kk < pnb) ? W[(long long)(rc0 + cc0 + c) * ni + j0 + kk] : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int e = e0 + tid + u * kFT;
-              if (e < ncc * kNB) s.tile[(e / kNB) * kBLD + e % kNB] = t[u];
-            }
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + tid + u * kFT;
+            const int kk = e % kNB, c = e / kNB;
+            t[u] = (e < ncc * kNB && kk < pnb) ? W[(long long)(rc0 + cc0 + c) * ni + j0 + kk] : 0.0;
           }
-          __syncthreads();
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + tid + u * kFT;
+            if (e < ncc * kNB) s.tile[(e / kNB) * kBLD + e % kNB] = t[u];
+          }
+        }
+        __syncthreads();
+        for (int c = tid; c < ncc; c += kFT) {
+          double* col = s.tile + c * kBLD;
+          double x[kNB];
+#pragma unroll
+          for (int jj = 0; jj < kNB; ++jj) x[jj] = col[jj];
+#pragma unroll
+          for (int ii = 0; ii < kNB - 1; ++ii)
+#pragma unroll
+            for (int jj = ii + 1; jj < kNB; ++jj) x[jj] -= s.pan[ii * kPLD + jj] * x[ii];
+#pragma unroll
+          for (int jj = 0; jj < kNB; ++jj)
+            if (jj < pnb) col[jj] = x[jj];
+        }
+        __syncthreads();
+        for (int e = tid; e < ncc * pnb; e += kFT) {
+          const int kk = e % pnb, c = e / pnb;
+          W[(long long)(rc0 + cc0 + c) * ni + j0 + kk] = s.tile[c * kBLD + kk];
+        }
+        if (rows > pnb)
           update_smem(rows - pnb, ncc, pnb, s.pan + pnb, kPLD, s.tile, kBLD,
                       W + (long long)(rc0 + cc0) * ni + j0 + pnb, ni);
-          __syncthreads();
-        }
+        __syncthreads();
+      }
+      substamp(3);
       substamp(4);
     }
 
