@@ -16,11 +16,15 @@ namespace hpsk {
 constexpr int kLeafMaxPts = 512;  // p^d <= 512 (2D p <= 22, 3D p <= 8)
 constexpr int kLeafMaxP = 24;
 
-__device__ __forceinline__ double leaf_bumps(const DevField& f, const double* x, int dim) {
+// Loops over the spatial axes are unrolled at compile time (DIM = 2 or 3) so the point and index
+// arrays stay in registers; the runtime-dim entry points dispatch once.
+template <int DIM>
+__device__ __forceinline__ double leaf_bumps(const DevField& f, const double* x) {
   double s = 0.0;
   for (int j = 0; j < f.n_centers; ++j) {
     double r2 = 0.0;
-    for (int k = 0; k < dim; ++k) {
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) {
       const double d = x[k] - f.centers[3 * j + k];
       r2 += d * d;
     }
@@ -30,15 +34,15 @@ __device__ __forceinline__ double leaf_bumps(const DevField& f, const double* x,
 }
 
 // Device evaluation of the built-in fields (hps_cuda.h HPSG_FIELD_*).
-__device__ __forceinline__ double eval_field(const DevField& f, const double* x, int dim, long long leaf, int pt,
-                                             int npts) {
+template <int DIM>
+__device__ __forceinline__ double eval_field_t(const DevField& f, const double* x, long long leaf, int pt, int npts) {
   const double* c = f.c;
   switch (f.kind) {
     case 0: return c[0];
-    case 1: return c[0] + c[1] * leaf_bumps(f, x, dim);
+    case 1: return c[0] + c[1] * leaf_bumps<DIM>(f, x);
     case 2: return c[0] * sin(c[1] * x[0] + c[2] * x[1] + c[3] * x[2] + c[4]);
     case 3: return c[0] * cos(c[1] * x[0] + c[2] * x[1] + c[3] * x[2] + c[4]);
-    case 4: return c[0] * leaf_bumps(f, x, dim) * sin(c[3] * x[0] + c[4] * x[1] + c[5] * x[2] + c[6]);
+    case 4: return c[0] * leaf_bumps<DIM>(f, x) * sin(c[3] * x[0] + c[4] * x[1] + c[5] * x[2] + c[6]);
     case 5: {  // proj/src/problems.cpp:50-66
       const double X = x[0], Y = x[1];
       const double ux = 5.0 * exp(5.0 * X) * sin(5.0 * Y) + 10.0 * M_PI * cos(10.0 * M_PI * X) * sin(M_PI * Y);
@@ -51,33 +55,40 @@ __device__ __forceinline__ double eval_field(const DevField& f, const double* x,
       const int ax = int(c[3]);
       double s = 0.0;
       for (int j = 0; j < f.n_centers; ++j) {
-        double r2 = 0.0;
-        for (int k = 0; k < dim; ++k) {
+        double r2 = 0.0, dax = 0.0;
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
           const double d = x[k] - f.centers[3 * j + k];
           r2 += d * d;
+          if (k == ax) dax = d;
         }
-        s += -2.0 * c[2] * (x[ax] - f.centers[3 * j + ax]) * exp(-c[2] * r2);
+        s += -2.0 * c[2] * dax * exp(-c[2] * r2);
       }
       return c[1] * s;
     }
     case 8: {  // div(eps grad u), eps = c0 + c1 sum exp(-c2 r^2), u = prod_k sin(c3 x_k + c4)
       double sn[3], cs[3], u = 1.0;
-      for (int k = 0; k < dim; ++k) sn[k] = sin(c[3] * x[k] + c[4]), cs[k] = cos(c[3] * x[k] + c[4]), u *= sn[k];
+#pragma unroll
+      for (int k = 0; k < DIM; ++k) sn[k] = sin(c[3] * x[k] + c[4]), cs[k] = cos(c[3] * x[k] + c[4]), u *= sn[k];
       double eps = c[0], geps[3] = {0.0, 0.0, 0.0};
       for (int j = 0; j < f.n_centers; ++j) {
         double r2 = 0.0;
-        for (int k = 0; k < dim; ++k) {
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
           const double d = x[k] - f.centers[3 * j + k];
           r2 += d * d;
         }
         const double e = exp(-c[2] * r2);
         eps += c[1] * e;
-        for (int k = 0; k < dim; ++k) geps[k] += c[1] * -2.0 * c[2] * (x[k] - f.centers[3 * j + k]) * e;
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) geps[k] += c[1] * -2.0 * c[2] * (x[k] - f.centers[3 * j + k]) * e;
       }
-      double f2 = -dim * c[3] * c[3] * u * eps;
-      for (int k = 0; k < dim; ++k) {
+      double f2 = -DIM * c[3] * c[3] * u * eps;
+#pragma unroll
+      for (int k = 0; k < DIM; ++k) {
         double du = c[3] * cs[k];
-        for (int l = 0; l < dim; ++l)
+#pragma unroll
+        for (int l = 0; l < DIM; ++l)
           if (l != k) du *= sn[l];
         f2 += geps[k] * du;
       }
@@ -85,6 +96,20 @@ __device__ __forceinline__ double eval_field(const DevField& f, const double* x,
     }
     default: return __longlong_as_double(0x7ff8000000000000ULL);
   }
+}
+
+__device__ __forceinline__ double eval_field(const DevField& f, const double* x, int dim, long long leaf, int pt,
+                                             int npts) {
+  return dim == 3 ? eval_field_t<3>(f, x, leaf, pt, npts) : eval_field_t<2>(f, x, leaf, pt, npts);
+}
+
+// v[i] for a runtime axis i < DIM without dynamic register indexing
+template <int DIM>
+__device__ __forceinline__ int pick(const int* v, int i) {
+  int r = v[0];
+#pragma unroll
+  for (int k = 1; k < DIM; ++k) r = i == k ? v[k] : r;
+  return r;
 }
 
 __device__ __forceinline__ void leaf_decode(int idx, int p, int dim, int* c) {
@@ -111,22 +136,25 @@ using LeafAsmSmem = LeafAsmSmemT<kLeafMaxPts, kLeafMaxP>;
 
 // Value of the operator entry L(gi, gj) accumulated in the reference order (term, then axis):
 // proj/src/local_solve.cpp:63-83, each contribution rounded as s^k * (c_i * op_ij).
-template <class SM>
-__device__ __forceinline__ double leaf_entry(const LeafAsmArgs& a, const SM& s, int gi, const int* ii,
-                                             int gj, const int* jj) {
-  const int p = a.p, dim = a.dim;
+template <int DIM, class SM>
+__device__ __forceinline__ double leaf_entry(const LeafAsmArgs& a, const SM& s, int gi, const int* ii, int gj,
+                                             const int* jj) {
+  const int p = a.p;
   const double s1 = a.scale, s2 = a.scale * a.scale;
   bool same[3];
-  for (int k = 0; k < 3; ++k) same[k] = ii[k] == jj[k];
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) same[k] = ii[k] == jj[k];
   double val = 0.0;
   for (int t = 0; t < a.nterms; ++t) {
     const DevTerm& tm = a.terms[t];
     const double c = s.coef[t][gi];
     switch (tm.role) {
       case 0:  // laplacian: c s^2 sum_a D2_a
-        for (int ax = 0; ax < dim; ++ax) {
+#pragma unroll
+        for (int ax = 0; ax < DIM; ++ax) {
           bool ok = true;
-          for (int k = 0; k < dim; ++k)
+#pragma unroll
+          for (int k = 0; k < DIM; ++k)
             if (k != ax && !same[k]) ok = false;
           if (ok) val = __dadd_rn(val, __dmul_rn(s2, __dmul_rn(c, s.D2[jj[ax] * p + ii[ax]])));
         }
@@ -134,9 +162,10 @@ __device__ __forceinline__ double leaf_entry(const LeafAsmArgs& a, const SM& s, 
       case 1: {  // gradient: c s D_axis
         const int ax = tm.axis;
         bool ok = true;
-        for (int k = 0; k < dim; ++k)
+#pragma unroll
+        for (int k = 0; k < DIM; ++k)
           if (k != ax && !same[k]) ok = false;
-        if (ok) val = __dadd_rn(val, __dmul_rn(s1, __dmul_rn(c, s.D[jj[ax] * p + ii[ax]])));
+        if (ok) val = __dadd_rn(val, __dmul_rn(s1, __dmul_rn(c, s.D[pick<DIM>(jj, ax) * p + pick<DIM>(ii, ax)])));
         break;
       }
       case 2:  // zeroth: diag(c)
@@ -144,17 +173,20 @@ __device__ __forceinline__ double leaf_entry(const LeafAsmArgs& a, const SM& s, 
         break;
       default: {  // second_order
         const int a1 = tm.axis, a2 = tm.axis2;
+        const int j1 = pick<DIM>(jj, a1), i1 = pick<DIM>(ii, a1);
         if (a1 == a2) {
           bool ok = true;
-          for (int k = 0; k < dim; ++k)
+#pragma unroll
+          for (int k = 0; k < DIM; ++k)
             if (k != a1 && !same[k]) ok = false;
-          if (ok) val = __dadd_rn(val, __dmul_rn(s2, __dmul_rn(c, s.D2[jj[a1] * p + ii[a1]])));
+          if (ok) val = __dadd_rn(val, __dmul_rn(s2, __dmul_rn(c, s.D2[j1 * p + i1])));
         } else {
           bool ok = true;
-          for (int k = 0; k < dim; ++k)
+#pragma unroll
+          for (int k = 0; k < DIM; ++k)
             if (k != a1 && k != a2 && !same[k]) ok = false;
           if (ok) {
-            const double d = __dmul_rn(s.D[jj[a1] * p + ii[a1]], s.D[jj[a2] * p + ii[a2]]);
+            const double d = __dmul_rn(s.D[j1 * p + i1], s.D[pick<DIM>(jj, a2) * p + pick<DIM>(ii, a2)]);
             val = __dadd_rn(val, __dmul_rn(s2, __dmul_rn(c, d)));
           }
         }
@@ -162,6 +194,12 @@ __device__ __forceinline__ double leaf_entry(const LeafAsmArgs& a, const SM& s, 
     }
   }
   return val;
+}
+
+template <class SM>
+__device__ __forceinline__ double leaf_entry(const LeafAsmArgs& a, const SM& s, int gi, const int* ii, int gj,
+                                             const int* jj) {
+  return a.dim == 3 ? leaf_entry<3>(a, s, gi, ii, gj, jj) : leaf_entry<2>(a, s, gi, ii, gj, jj);
 }
 
 // One CTA assembles one leaf: M[:, 0:ni] = L(I_i, I_i), M[:, ni] = sgn * f(I_i) (ld = ldM),
@@ -174,11 +212,11 @@ __device__ __forceinline__ double leaf_entry(const LeafAsmArgs& a, const SM& s, 
 // exterior block E, record each interior row's 2*dim exterior line neighbours at slot
 // (2*axis + (neighbour at node 0 ? 0 : 1)) * ni + r as (exterior position, value) -- row-fastest,
 // so a warp reading one slot for consecutive rows hits consecutive banks.
-template <class SM>
-__device__ __forceinline__ void leaf_assemble_block(const LeafAsmArgs& a, long long leaf, double* M, long long ldM,
-                                                    double* E, SM& s, int* enz_idx = nullptr,
-                                                    double* enz_val = nullptr) {
-  const int tid = threadIdx.x, nthr = blockDim.x, p = a.p, dim = a.dim, n = a.n;
+template <int DIM, class SM>
+__device__ __forceinline__ void leaf_assemble_block_t(const LeafAsmArgs& a, long long leaf, double* M, long long ldM,
+                                                      double* E, SM& s, int* enz_idx, double* enz_val) {
+  constexpr int dim = DIM;
+  const int tid = threadIdx.x, nthr = blockDim.x, p = a.p, n = a.n;
   if (tid == 0) s.bad = INT_MAX;
   for (int e = tid; e < p * p; e += nthr) s.D[e] = a.D[e], s.D2[e] = a.D2[e];
   for (int r = tid; r < a.ni; r += nthr) s.pos[a.interior[r]] = r;
@@ -190,15 +228,16 @@ __device__ __forceinline__ void leaf_assemble_block(const LeafAsmArgs& a, long l
     int ci[3];
     leaf_decode(i, p, dim, ci);
     double x[3] = {0.0, 0.0, 0.0};
+#pragma unroll
     for (int k = 0; k < dim; ++k)
       x[k] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(box[k], box[3 + k])),
                        __dmul_rn(__dmul_rn(0.5, __dsub_rn(box[3 + k], box[k])), a.cheb[ci[k]]));
     for (int t = 0; t < a.nterms; ++t) {
-      const double v = eval_field(a.terms[t].f, x, dim, leaf, i, n);
+      const double v = eval_field_t<DIM>(a.terms[t].f, x, leaf, i, n);
       s.coef[t][i] = v;
       if (!isfinite(v)) atomicMin(&s.bad, i);
     }
-    s.fsrc[i] = a.has_source ? eval_field(a.source, x, dim, leaf, i, n) : 0.0;
+    s.fsrc[i] = a.has_source ? eval_field_t<DIM>(a.source, x, leaf, i, n) : 0.0;
   }
   bool mixed = false;
   for (int t = 0; t < a.nterms; ++t)
@@ -212,7 +251,7 @@ __device__ __forceinline__ void leaf_assemble_block(const LeafAsmArgs& a, long l
       int ii[3], jj[3];
       leaf_decode(gi, p, dim, ii);
       leaf_decode(gj, p, dim, jj);
-      const double v = leaf_entry(a, s, gi, ii, gj, jj);
+      const double v = leaf_entry<DIM>(a, s, gi, ii, gj, jj);
       if (cj < ni)
         M[(long long)cj * ldM + r] = v;
       else
@@ -237,18 +276,21 @@ __device__ __forceinline__ void leaf_assemble_block(const LeafAsmArgs& a, long l
       int ii[3], jj[3];
       leaf_decode(gi, p, dim, ii);
       jj[0] = ii[0], jj[1] = ii[1], jj[2] = ii[2];
+      int ax = 0;
       if (w > 0) {
-        const int ax = (w - 1) / (p - 1), k0 = (w - 1) % (p - 1);
-        jj[ax] = k0 < ii[ax] ? k0 : k0 + 1;  // skip the diagonal
+        ax = (w - 1) / (p - 1);
+        const int k0 = (w - 1) % (p - 1);
+#pragma unroll
+        for (int k = 0; k < DIM; ++k)
+          if (k == ax) jj[k] = k0 < ii[k] ? k0 : k0 + 1;  // skip the diagonal
       }
       const int gj = dim == 2 ? jj[0] * p + jj[1] : (jj[0] * p + jj[1]) * p + jj[2];
-      const double v = leaf_entry(a, s, gi, ii, gj, jj);
+      const double v = leaf_entry<DIM>(a, s, gi, ii, gj, jj);
       const int q = s.pos[gj];
       if (q >= 0) {
         M[(long long)q * ldM + r] = v;
       } else if (enz_idx) {
-        const int ax = (w - 1) / (p - 1);
-        const int slot = (2 * ax + (jj[ax] == 0 ? 0 : 1)) * ni + r;
+        const int slot = (2 * ax + (pick<DIM>(jj, ax) == 0 ? 0 : 1)) * ni + r;
         enz_idx[slot] = -q - 1;
         enz_val[slot] = v;
       } else {
@@ -259,6 +301,16 @@ __device__ __forceinline__ void leaf_assemble_block(const LeafAsmArgs& a, long l
   // RHS column 0 of the augmented block: sgn * f(I_i)
   for (int r = tid; r < ni; r += nthr) M[(long long)ni * ldM + r] = a.fsign * s.fsrc[a.interior[r]];
   __syncthreads();
+}
+
+template <class SM>
+__device__ __forceinline__ void leaf_assemble_block(const LeafAsmArgs& a, long long leaf, double* M, long long ldM,
+                                                    double* E, SM& s, int* enz_idx = nullptr,
+                                                    double* enz_val = nullptr) {
+  if (a.dim == 3)
+    leaf_assemble_block_t<3>(a, leaf, M, ldM, E, s, enz_idx, enz_val);
+  else
+    leaf_assemble_block_t<2>(a, leaf, M, ldM, E, s, enz_idx, enz_val);
 }
 
 }  // namespace hpsk
