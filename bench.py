@@ -238,6 +238,7 @@ def run_b200(args):
         out["configs_extra"]["iti_scatter2d"] = bench_iti(torch)
         out["configs_extra"]["subtree_recompute_L8"] = bench_recompute(torch, args, 8, 2)
         out["configs_extra"]["subtree_recompute_L9"] = bench_recompute(torch, args, 9, 2)
+        out["configs_extra"]["planner_L9_80GB"] = bench_planner(args, 9, 80e9)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"], par = cpu_baseline(args, prob, u_gpu)
         out["accuracy"].update(par)
@@ -333,13 +334,30 @@ def bench_recompute(torch, args, L, depth, steps=1):
         rs.solve_device(g, u)
     torch.cuda.synchronize()
     sec = (time.perf_counter() - t0) / steps
-    free, total = torch.cuda.mem_get_info()
+    lib_bytes = rs.top.stats()["device_bytes"] + rs.work.stats()["device_bytes"]
     rs.close()
     paper = {8: 4.02, 9: 17.43}.get(L)
     return {"workload": f"2D Helmholtz p={tree.p} L={L} (N={tree.total_points}), subtree recomputation at depth "
                         f"{depth} (build + solve, wall clock)", "s_per_step": sec,
-            "value": tree.total_points / sec, "unit": "DOF/s", "device_used_gb": (total - free) / 1e9,
+            "value": tree.total_points / sec, "unit": "DOF/s", "device_gb": lib_bytes / 1e9,
             "paper_h100_subtree_recompute_s": paper, "speedup_vs_paper": (paper / sec) if paper else None}
+
+
+def bench_planner(args, L, budget):
+    """SPEC planner make_plan on the real footprints (hpsg_estimate_bytes; nothing allocated): the
+    store footprint of a 2D p=16 tree and the subtree plan under an H100-sized budget."""
+    import paper_2503_17535_b200 as H
+    from paper_2503_17535_b200 import planner as PL
+    from paper_2503_17535_b200 import problems as PR
+    prob = PR.helmholtz_bumps(k=args.k, seed=args.seed)
+    tree = H.build_uniform_tree(prob.lo, prob.hi, L, 2, args.p)
+    opts = dict(literal_sign=False, root_implicit_S=not args.explicit_root)
+    whole = H.estimate_bytes(tree, prob.terms, prob.source, **opts)
+    plan = PL.make_plan(tree, prob.terms, prob.source, strategy="subtree", budget=budget, **opts)
+    return {"workload": f"planner: 2D Helmholtz p={tree.p} L={L} (N={tree.total_points}), budget {budget / 1e9:g} GB",
+            "store_gb": whole / 1e9, "plan": plan.strategy, "cut_depth": plan.cut_depth,
+            "subtree_height": plan.subtree_depth, "n_subtrees": plan.n_subtrees,
+            "plan_peak_gb": plan.est_bytes.get("peak", plan.est_bytes.get("whole", 0.0)) / 1e9}
 
 
 def bench_iti(torch, L=6, p=16, k=40.0, steps=2):

@@ -137,6 +137,13 @@ int hpsg_part_retarget(hpsg_ctx* ctx, long long root_index);
 /* n_cut input nodes of cut_nb boundary points each (0 for a part with real leaves); root_nb =
  * boundary points of the part root */
 int hpsg_part_sizes(hpsg_ctx* ctx, long long* n_cut, int* cut_nb, int* root_nb);
+/* Device footprint of a context (whole tree when part is NULL) without allocating it: the bytes
+ * hpsg_create_part would allocate plus, for nrhs > 0, what the first hpsg_solve of nrhs right-hand
+ * sides adds (solve workspace and the host-API staging of g and u; 0: build only).
+ * The input of the memory-budgeted planner (SPEC.md planner module, make_plan; the reference's
+ * proj/src/planner.cpp is a stub). */
+int hpsg_estimate_bytes(const hpsg_tree* tree, const hpsg_part* part, const hpsg_term* terms, int n_terms,
+                        const hpsg_field* source, const hpsg_options* opts, int nrhs, double* bytes);
 /* [h|T] of the part root after hpsg_build (root_depth > 0): device-to-device into d_dst
  * (root_nb x (1+root_nb)); MergeOutput::T/h, merge.hpp:58-66 */
 int hpsg_part_root_ht(hpsg_ctx* ctx, double* d_dst);

@@ -8,6 +8,7 @@ host mirror of the reference API (hps.py) plus the problem catalog
 """
 from .hps import (FIELD_BUMPS, FIELD_BUMPS_SIN, FIELD_CONST, FIELD_PLANE_COS, FIELD_PLANE_SIN,  # noqa: F401
                   FIELD_POISSON2D_SRC, FIELD_SAMPLED, ROLE_GRADIENT, ROLE_LAPLACIAN, ROLE_SECOND_ORDER, ROLE_ZEROTH,
-                  Field, HpsError, HpsSolver, Term, UniformTree, build_library, build_uniform_tree, bump_centers, lib,
+                  Field, HpsError, HpsSolver, Term, UniformTree, build_library, build_uniform_tree, bump_centers,
+                  estimate_bytes, lib,
                   tree_root_points)
 from . import problems  # noqa: F401

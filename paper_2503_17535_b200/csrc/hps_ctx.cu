@@ -49,6 +49,10 @@ void ck(cudaError_t e, const char* where) {
   if (e != cudaSuccess) throw CudaError{e, where};
 }
 
+// Footprint estimation (hpsg_estimate_bytes): while set, DevBuf::alloc and the uploads only count
+// bytes -- the context is created through the normal path without touching device memory.
+thread_local bool g_dry_alloc = false;
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -63,6 +67,10 @@ struct DevBuf {
     bytes = 0;
   }
   void alloc(size_t b, size_t* total) {
+    if (g_dry_alloc) {
+      if (total) *total += b;
+      return;
+    }
     if (b <= bytes && p) return;
     if (total) *total -= bytes;
     release();
@@ -82,7 +90,8 @@ struct DevBuf {
 template <class T>
 void upload(DevBuf& b, const std::vector<T>& v, size_t* total, cudaStream_t st) {
   b.alloc(v.size() * sizeof(T), total);
-  if (!v.empty()) ck(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st), "upload");
+  if (!v.empty() && !g_dry_alloc)
+    ck(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st), "upload");
 }
 
 struct Level {
@@ -245,7 +254,7 @@ hpsk::DevField make_dev_field(hpsg_ctx* c, const hpsg_field& f, bool is_source) 
     const size_t n = size_t(c->T.n_leaves()) * c->ops.n;
     auto b = std::make_unique<DevBuf>();
     b->alloc(n * 8, &c->dev_bytes);
-    ck(cudaMemcpyAsync(b->p, f.samples, n * 8, cudaMemcpyHostToDevice, c->st), "sampled field upload");
+    if (!g_dry_alloc) ck(cudaMemcpyAsync(b->p, f.samples, n * 8, cudaMemcpyHostToDevice, c->st), "sampled field upload");
     d.samples = b->d();
     c->field_bufs.push_back(std::move(b));
   }
@@ -1218,6 +1227,30 @@ int hpsg_create_part(const hpsg_tree* tree, const hpsg_part* part, const hpsg_te
   }
   *out = c.release();
   return HPSG_OK;
+}
+
+int hpsg_estimate_bytes(const hpsg_tree* tree, const hpsg_part* part, const hpsg_term* terms, int n_terms,
+                        const hpsg_field* source, const hpsg_options* opts, int nrhs, double* bytes) {
+  if (!bytes || nrhs < 0) return HPSG_ERR_INVALID;
+  const hpsg_part whole{0, 0, tree ? tree->L : 0};
+  hpsg_ctx* c = nullptr;
+  g_dry_alloc = true;
+  int rc = hpsg_create_part(tree, part ? part : &whole, terms, n_terms, source, opts, &c);
+  if (rc == HPSG_OK) {
+    rc = guarded(c, [&] {
+      if (nrhs > 0) {
+        ensure_solve_ws(c, nrhs);
+        if (!c->T.cut) {  // hpsg_solve's staging of g and u (the host-buffer API)
+          c->g_in.alloc(size_t(c->lv[0].n_ext) * nrhs * 8, &c->dev_bytes);
+          c->u_out.alloc(size_t(c->T.n_leaves()) * c->ops.n * nrhs * 8, &c->dev_bytes);
+        }
+      }
+    });
+    *bytes = double(c->dev_bytes);
+  }
+  g_dry_alloc = false;
+  hpsg_destroy(c);
+  return rc;
 }
 
 int hpsg_build(hpsg_ctx* c) {

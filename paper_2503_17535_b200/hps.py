@@ -88,6 +88,8 @@ def lib():
         L.hpsg_create_part.argtypes = [C.POINTER(_Tree), C.POINTER(_Part), C.POINTER(_Term), C.c_int,
                                        C.POINTER(_Field), C.POINTER(_Options), C.POINTER(vp)]
         L.hpsg_part_sizes.argtypes = [vp, C.POINTER(C.c_longlong), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.hpsg_estimate_bytes.argtypes = [C.POINTER(_Tree), C.POINTER(_Part), C.POINTER(_Term), C.c_int,
+                                          C.POINTER(_Field), C.POINTER(_Options), C.c_int, dp]
         L.hpsg_part_root_ht.argtypes = [vp, C.c_void_p]
         L.hpsg_part_retarget.argtypes = [vp, C.c_longlong]
         L.hpsg_part_set_cut_ht.argtypes = [vp, C.c_longlong, C.c_void_p]
@@ -226,6 +228,30 @@ def bump_centers(seed, n=10, dim=2):
     out = np.zeros(3 * n)
     lib().hpsg_bump_centers(seed, n, dim, _dp(out))
     return out.reshape(n, 3)
+
+
+# ----------------------------------------------------------------------------- footprint
+def estimate_bytes(tree: UniformTree, terms, source: Field | None = None, part=None, nrhs=1, literal_sign=True,
+                   root_implicit_S=False, device=0, keep_factors=False) -> float:
+    """Device bytes an HpsSolver(tree, terms, source, part=..., ...) would hold after its build and a
+    solve of nrhs right-hand sides, computed by the library's own allocation path without allocating
+    (include/hps_cuda.h hpsg_estimate_bytes).  DtN variant."""
+    L = lib()
+    keep = []
+    arr = (_Term * max(1, len(terms)))()
+    for i, t in enumerate(terms):
+        arr[i].role, arr[i].axis, arr[i].axis2 = t.role, t.axis, t.axis2
+        arr[i].field = t.field.to_c(keep)
+    src = source.to_c(keep) if source is not None else None
+    tr = _Tree(tree.dim, tree.p, tree.L, tree.lo, tree.hi)
+    op = _Options(int(literal_sign), int(root_implicit_S), device, int(keep_factors), 0, 1.0, 0)
+    pt = _Part(*(tuple(part) if part is not None else (0, 0, tree.L)))
+    out = np.zeros(1)
+    rc = L.hpsg_estimate_bytes(C.byref(tr), C.byref(pt), arr, len(terms), C.byref(src) if src is not None else None,
+                               C.byref(op), int(nrhs), _dp(out))
+    if rc != HPSG_OK:
+        raise HpsError(rc, "hpsg_estimate_bytes failed (invalid tree/part or no CUDA device)")
+    return float(out[0])
 
 
 # ----------------------------------------------------------------------------- solver
