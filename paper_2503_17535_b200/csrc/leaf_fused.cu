@@ -45,6 +45,10 @@ constexpr int kRowsPerLane = (kMaxNI + 31) / 32;
 #define HPS_LEAF_SUB 8
 #endif
 constexpr int kSub = HPS_LEAF_SUB;  // sub-panel width factored by one warp inside a panel
+#ifndef HPS_LEAF_PAIR
+#define HPS_LEAF_PAIR 1
+#endif
+constexpr bool kPairGepp = HPS_LEAF_PAIR;  // two-warp sub-panel GEPP for panels taller than 64 rows
 
 struct FusedSmem {
   LeafAsmSmemT<256, 16> asmb;
@@ -126,6 +130,24 @@ __device__ void update_smem(int m, int n, int k, const double* A, int lda, const
 // One warp factors the rows x pnb panel in s.pan.  Lane-strided rows r = j + 1 + lane + 32 q; the
 // slots past the last row are clamped onto it, so loads/stores need no predicates (the clamped
 // lanes recompute and store exactly the owner's value).
+// 1/x to full double precision (within 1 ulp) from the hardware approximation and two Newton steps:
+// four dependent FMAs instead of the IEEE division subroutine on the pivot chain
+#ifndef HPS_LEAF_FAST_RCP
+#define HPS_LEAF_FAST_RCP 1
+#endif
+HPS_DEV double pivot_rcp(double x) {
+#if HPS_LEAF_FAST_RCP
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+#else
+  return 1.0 / x;
+#endif
+}
+
 template <int NQ>
 __device__ __forceinline__ void gepp_warp_body(FusedSmem& s, int rows, int sb, int se, int pnb, int j0) {
   const int lane = threadIdx.x & 31;
@@ -177,7 +199,7 @@ __device__ __forceinline__ void gepp_warp_body(FusedSmem& s, int rows, int sb, i
     __syncwarp();
     const double pv = pj[j];
     if (fabs(pv) > 0.0 && j + 1 < rows) {
-      const double rinv = 1.0 / pv;
+      const double rinv = pivot_rcp(pv);
       int off[NQ];
       double l[NQ];
 #pragma unroll
@@ -220,6 +242,116 @@ __device__ __forceinline__ void gepp_warp_body(FusedSmem& s, int rows, int sb, i
   if (lane == 0) s.pmin = pmn, s.pmax = pmx, s.first_zero = fz;
 }
 
+// Two-warp variant of gepp_warp_body for tall panels: warp w (0 or 1) owns the lane-strided row
+// slots q = 2 qq + w, so each warp's pivot search and rank-1 update cover half the rows; per column
+// the two warp candidates meet through shared memory under a 64-thread named barrier, warp 0
+// exchanges the rows, a second named barrier publishes the exchange.  Stores are predicated (no
+// clamped duplicates: a duplicate in the other warp would race with the owner).  Same pivot rule and
+// arithmetic as gepp_warp_body.
+HPS_DEV void pair_bar() { asm volatile("bar.sync 1, 64;\n" ::: "memory"); }
+template <int NQH>
+__device__ __forceinline__ void gepp_pair_body(FusedSmem& s, int rows, int sb, int se, int pnb, int j0) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double pmn = s.pmin, pmx = s.pmax;
+  int fz = s.first_zero;
+  for (int j = sb; j < se; ++j) {
+    double* pj = s.pan + j * kPLD;
+    double bv = -1.0;
+    int bp = INT_MAX;
+    {
+      double a[NQH];
+#pragma unroll
+      for (int qq = 0; qq < NQH; ++qq) a[qq] = fabs(pj[min(j + lane + 32 * (2 * qq + w), rows - 1)]);
+#pragma unroll
+      for (int qq = 0; qq < NQH; ++qq) {
+        const int r = j + lane + 32 * (2 * qq + w);
+        const double av = isnan(a[qq]) ? INFINITY : a[qq];
+        if (r < rows && av > bv) bv = av, bp = r;
+      }
+    }
+    {
+      const unsigned long long key = bv >= 0.0 ? (unsigned long long)__double_as_longlong(bv) : 0ull;
+      const unsigned hi = unsigned(key >> 32), lo = unsigned(key);
+      const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+      const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+      bp = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? bp : INT_MAX);
+      bv = bp == INT_MAX ? -1.0 : __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+    }
+    if (lane == 0) s.cv[w] = bv, s.cp[w] = bp;
+    pair_bar();
+    {
+      const double ov = s.cv[w ^ 1];
+      const int op = s.cp[w ^ 1];
+      if (ov > bv || (ov == bv && op < bp)) bv = ov, bp = op;
+    }
+    if (w == 0 && bp != j) {
+      if (lane < pnb) {
+        const double t = s.pan[lane * kPLD + j];
+        s.pan[lane * kPLD + j] = s.pan[lane * kPLD + bp];
+        s.pan[lane * kPLD + bp] = t;
+      }
+      if (lane == 0) {
+        const int t = s.prow[j];
+        s.prow[j] = s.prow[bp];
+        s.prow[bp] = t;
+      }
+    }
+    if (!(bv > 0.0) || !isfinite(bv)) {
+      if (fz < 0) fz = j0 + j;
+    } else {
+      pmn = fmin(pmn, bv);
+      pmx = fmax(pmx, bv);
+    }
+    pair_bar();
+    const double pv = pj[j];
+    if (fabs(pv) > 0.0 && j + 1 < rows) {
+      const double rinv = pivot_rcp(pv);
+      int off[NQH];
+      bool own[NQH];
+      double l[NQH];
+#pragma unroll
+      for (int qq = 0; qq < NQH; ++qq) {
+        const int r = j + 1 + lane + 32 * (2 * qq + w);
+        own[qq] = r < rows;
+        off[qq] = min(r, rows - 1);
+      }
+#pragma unroll
+      for (int qq = 0; qq < NQH; ++qq) l[qq] = pj[off[qq]] * rinv;
+#pragma unroll
+      for (int qq = 0; qq < NQH; ++qq)
+        if (own[qq]) pj[off[qq]] = l[qq];
+      int c = j + 1;
+      for (; c + 4 <= se; c += 4) {
+        const double* pc = s.pan + c * kPLD;
+        double u[4], a[4][NQH];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) u[k] = pc[k * kPLD + j];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int qq = 0; qq < NQH; ++qq) a[k][qq] = pc[k * kPLD + off[qq]];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int qq = 0; qq < NQH; ++qq)
+            if (own[qq]) s.pan[(c + k) * kPLD + off[qq]] = a[k][qq] - l[qq] * u[k];
+      }
+      for (; c < se; ++c) {
+        double* pc = s.pan + c * kPLD;
+        const double u = pc[j];
+        double a[NQH];
+#pragma unroll
+        for (int qq = 0; qq < NQH; ++qq) a[qq] = pc[off[qq]];
+#pragma unroll
+        for (int qq = 0; qq < NQH; ++qq)
+          if (own[qq]) pc[off[qq]] = a[qq] - l[qq] * u;
+      }
+    }
+    __syncwarp();
+  }
+  if (threadIdx.x == 0) s.pmin = pmn, s.pmax = pmx, s.first_zero = fz;
+}
+
 // GEPP of panel columns [j0, j0+pnb) over rows [j0, ni) of W by ONE warp on the panel staged in
 // s.pan (rows physically exchanged; lane-strided rows, no CTA barrier per column).  Pivot = max
 // |a| with NaN ranked as +inf, ties -> lowest current row (the LAPACK/Eigen rule).  Writes the
@@ -247,7 +379,15 @@ __device__ void panel_gepp_warp(FusedSmem& s, double* W, int ni, int j0, int pnb
   const int nq = (rows + 31) / 32;
   for (int sb = 0; sb < pnb; sb += kSub) {
     const int se = min(sb + kSub, pnb);
-    if (tid < 32) {
+    if (kPairGepp && nq >= 3) {
+      if (tid < 64) {
+        switch (nq) {
+          case 3: case 4: gepp_pair_body<2>(s, rows, sb, se, pnb, j0); break;
+          case 5: case 6: gepp_pair_body<3>(s, rows, sb, se, pnb, j0); break;
+          default: gepp_pair_body<(kRowsPerLane + 1) / 2>(s, rows, sb, se, pnb, j0); break;
+        }
+      }
+    } else if (tid < 32) {
       switch (nq) {
         case 1: gepp_warp_body<1>(s, rows, sb, se, pnb, j0); break;
         case 2: gepp_warp_body<2>(s, rows, sb, se, pnb, j0); break;
