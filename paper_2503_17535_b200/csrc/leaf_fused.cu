@@ -669,15 +669,19 @@ __global__ void __launch_bounds__(kFT, 512 / kFT) leaf_fused_kernel(const LeafFu
       double acc[kMaxT][2];
 #pragma unroll
       for (int u = 0; u < kMaxT; ++u) acc[u][0] = acc[u][1] = 0.0;
-      for (int k0 = 0; k0 < ni; k0 += kNB) {
-        const int kc = min(kNB, ni - k0);
+      // k chunks of kEK = 64 rows (4 barrier rounds instead of 7): Q_i chunk in s.pan (ld kEQ), [v|Y_i]
+      // chunk in s.tile (ld kEQ); both leading dims are 4 mod 16 (conflict-free fragments)
+      constexpr int kEK = 64, kEQ = 68;
+      static_assert(kEK * kEQ <= kNB * kPLD && kEQ * 64 <= kTileCols * kBLD, "E-phase staging");
+      for (int k0 = 0; k0 < ni; k0 += kEK) {
+        const int kc = min(kEK, ni - k0);
         for (int e = tid; e < nb * kc; e += kFT) {
           const int r = e % nb, kk = e / nb;
-          s.pan[kk * kPLD + r] = f.Qi[(long long)(k0 + kk) * nb + r];
+          s.pan[kk * kEQ + r] = f.Qi[(long long)(k0 + kk) * nb + r];
         }
-        for (int e = tid; e < nr * kNB; e += kFT) {
-          const int kk = e % kNB, c = e / kNB;
-          s.tile[c * kBLD + kk] = kk < kc ? R[(long long)c * ni + k0 + kk] : 0.0;
+        for (int e = tid; e < nr * kEK; e += kFT) {
+          const int kk = e % kEK, c = e / kEK;
+          s.tile[c * kEQ + kk] = kk < kc ? R[(long long)c * ni + k0 + kk] : 0.0;
         }
         __syncthreads();
 #pragma unroll
@@ -687,8 +691,8 @@ __global__ void __launch_bounds__(kFT, 512 / kFT) leaf_fused_kernel(const LeafFu
             const int m0 = (t % tmn) * 8, n0 = (t / tmn) * 8;
             for (int kk = 0; kk < kc; kk += 4) {
               const int kq = kk + t4;
-              const double av = (kq < kc && m0 + g < nb) ? s.pan[kq * kPLD + m0 + g] : 0.0;
-              const double bv = (kq < kc && n0 + g < nr) ? s.tile[(n0 + g) * kBLD + kq] : 0.0;
+              const double av = (kq < kc && m0 + g < nb) ? s.pan[kq * kEQ + m0 + g] : 0.0;
+              const double bv = (kq < kc && n0 + g < nr) ? s.tile[(n0 + g) * kEQ + kq] : 0.0;
               dmma_8x8x4(acc[u][0], acc[u][1], av, bv);
             }
           }
@@ -727,7 +731,7 @@ __global__ void __launch_bounds__(kFT, 512 / kFT) leaf_fused_kernel(const LeafFu
 bool leaf_fused_supported(int n, int p, int ni, int nb, int dim, bool mixed_terms) {
   const int tmn = (nb + 7) / 8, tnn = (nb + 8) / 8;
   return !mixed_terms && n <= 256 && p <= 16 && ni <= kMaxNI && ni <= kFT && ni + 1 + nb <= kMaxCols &&
-         ni * 2 * dim <= kMaxNz && tmn * tnn <= 7 * kFW && 1 + nb <= kTileCols;
+         ni * 2 * dim <= kMaxNz && tmn * tnn <= 7 * kFW && 1 + nb <= kTileCols && nb <= 64 && 1 + nb <= 64;
 }
 
 long long leaf_fused_scratch_per_cta(int ni, int ne, int nb) { return (long long)ni * (ni + 1 + nb); }
