@@ -608,56 +608,55 @@ __global__ void __launch_bounds__(kFT, 512 / kFT) leaf_fused_kernel(const LeafFu
     }
 
     stamp(3);
-    // ---- D. back substitution on the 1+nb RHS columns
-    const int nblk = (ni + kNB - 1) / kNB;
-    for (int jb = nblk - 1; jb >= 0; --jb) {
-      const int r0 = jb * kNB, bnb = min(kNB, ni - r0);
-      for (int e = tid; e < bnb * bnb; e += kFT) {
-        const int r = e % bnb, c = e / bnb;
-        const double u = W[(long long)(r0 + c) * ni + r0 + r];
-        s.pan[c * kPLD + r] = u;
-        if (r == c) s.rdiag[r] = 1.0 / u;
-      }
-      __syncthreads();
-      for (int c = tid; c < nr; c += kFT) {
-        double* col = R + (long long)c * ni + r0;
-        double x[kNB];
-#pragma unroll
-        for (int jj = 0; jj < kNB; ++jj) x[jj] = jj < bnb ? col[jj] : 0.0;
-#pragma unroll
-        for (int jj = kNB - 1; jj >= 0; --jj) {
-          if (jj < bnb) {
-            x[jj] *= s.rdiag[jj];
-#pragma unroll
-            for (int ii = 0; ii < jj; ++ii) x[ii] -= s.pan[jj * kPLD + ii] * x[jj];
+    // ---- D. back substitution on the 1+nb RHS columns.  Per 32-row block: the diagonal U block
+    //      goes to the (dead) assembly buffer; warps 0-1 solve it for the <= 64 RHS columns while
+    //      warps 2-7 stage the U column block above it (one barrier for both); then the DMMA update.
+    {
+      double* sDg = reinterpret_cast<double*>(&s.asmb);  // kNB x kNB diagonal block, ld kNB
+      const int nblk = (ni + kNB - 1) / kNB;
+      for (int jb = nblk - 1; jb >= 0; --jb) {
+        const int r0 = jb * kNB, bnb = min(kNB, ni - r0);
+        for (int c = warp; c < bnb; c += kFW)
+          if (lane < bnb) {
+            const double u = W[(long long)(r0 + c) * ni + r0 + lane];
+            sDg[c * kNB + lane] = u;
+            if (lane == c) s.rdiag[c] = 1.0 / u;
           }
-        }
+        __syncthreads();
+        if (tid < 64) {
+          if (tid < nr) {
+            double* col = R + (long long)tid * ni + r0;
+            double x[kNB];
 #pragma unroll
-        for (int jj = 0; jj < kNB; ++jj) {
-          if (jj < bnb) col[jj] = x[jj];
-          s.tile[c * kBLD + jj] = jj < bnb ? x[jj] : 0.0;
-        }
-      }
-      __syncthreads();
-      if (r0 > 0) {
-        // stage the U column block U[0:r0, r0:r0+bnb] as the A operand
-        for (int e0 = 0; e0 < r0 * bnb; e0 += 8 * kFT) {
-          double t[8];
+            for (int jj = 0; jj < kNB; ++jj) x[jj] = jj < bnb ? col[jj] : 0.0;
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int e = e0 + tid + u * kFT;
-            t[u] = e < r0 * bnb ? W[(long long)(r0 + e / r0) * ni + e % r0] : 0.0;
+            for (int jj = kNB - 1; jj >= 0; --jj) {
+              if (jj < bnb) {
+                x[jj] *= s.rdiag[jj];
+#pragma unroll
+                for (int ii = 0; ii < jj; ++ii) x[ii] -= sDg[jj * kNB + ii] * x[jj];
+              }
+            }
+#pragma unroll
+            for (int jj = 0; jj < kNB; ++jj) {
+              if (jj < bnb) col[jj] = x[jj];
+              s.tile[tid * kBLD + jj] = jj < bnb ? x[jj] : 0.0;
+            }
           }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int e = e0 + tid + u * kFT;
-            if (e < r0 * bnb) s.pan[(e / r0) * kPLD + e % r0] = t[u];
+        } else if (r0 > 0) {
+          // U[0:r0, r0:r0+bnb] -> s.pan (A operand), one column per warp, rows over the lanes
+          for (int c = warp - 2; c < bnb; c += kFW - 2) {
+            const double* src = W + (long long)(r0 + c) * ni;
+#pragma unroll 4
+            for (int r = lane; r < r0; r += 32) s.pan[c * kPLD + r] = src[r];
           }
         }
         __syncthreads();
-        update_smem(r0, nr, bnb, s.pan, kPLD, s.tile, kBLD, R, ni);
+        if (r0 > 0) {
+          update_smem(r0, nr, bnb, s.pan, kPLD, s.tile, kBLD, R, ni);
+          __syncthreads();
+        }
       }
-      __syncthreads();
     }
 
     stamp(4);
@@ -731,7 +730,8 @@ __global__ void __launch_bounds__(kFT, 512 / kFT) leaf_fused_kernel(const LeafFu
 bool leaf_fused_supported(int n, int p, int ni, int nb, int dim, bool mixed_terms) {
   const int tmn = (nb + 7) / 8, tnn = (nb + 8) / 8;
   return !mixed_terms && n <= 256 && p <= 16 && ni <= kMaxNI && ni <= kFT && ni + 1 + nb <= kMaxCols &&
-         ni * 2 * dim <= kMaxNz && tmn * tnn <= 7 * kFW && 1 + nb <= kTileCols && nb <= 64 && 1 + nb <= 64;
+         ni * 2 * dim <= kMaxNz && tmn * tnn <= 7 * kFW && 1 + nb <= kTileCols && nb <= 64 && 1 + nb <= 64 &&
+         (size_t)kNB * kNB * 8 <= sizeof(LeafAsmSmemT<256, 16>);
 }
 
 long long leaf_fused_scratch_per_cta(int ni, int ne, int nb) { return (long long)ni * (ni + 1 + nb); }
