@@ -367,9 +367,16 @@ __device__ void panel_gepp_warp(FusedSmem& s, double* W, int ni, int j0, int pnb
     }
   };
   const int rows = ni - j0;
-  for (int e = tid; e < pnb * rows; e += kFT) {
-    const int c = e / rows, r = e - c * rows;
-    s.pan[c * kPLD + r] = W[(long long)(j0 + c) * ni + j0 + r];
+  if (tid < rows) {  // thread = row (rows <= 196 < kFT), 8 columns' loads in flight per batch
+    const double* src = W + (long long)j0 * ni + j0 + tid;
+    for (int c0 = 0; c0 < pnb; c0 += 8) {
+      double t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t[u] = c0 + u < pnb ? src[(long long)(c0 + u) * ni] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (c0 + u < pnb) s.pan[(c0 + u) * kPLD + tid] = t[u];
+    }
   }
   for (int r = tid; r < rows; r += kFT) s.prow[r] = r;
   __syncthreads();
@@ -594,9 +601,9 @@ __global__ void __launch_bounds__(kFT, 512 / kFT) leaf_fused_kernel(const LeafFu
             if (jj < pnb) col[jj] = x[jj];
         }
         __syncthreads();
-        for (int e = tid; e < ncc * pnb; e += kFT) {
-          const int kk = e % pnb, c = e / pnb;
-          W[(long long)(rc0 + cc0 + c) * ni + j0 + kk] = s.tile[c * kBLD + kk];
+        for (int e = tid; e < ncc * kNB; e += kFT) {
+          const int kk = e % kNB, c = e / kNB;  // compile-time divisor
+          if (kk < pnb) W[(long long)(rc0 + cc0 + c) * ni + j0 + kk] = s.tile[c * kBLD + kk];
         }
         if (rows > pnb)
           update_smem(rows - pnb, ncc, pnb, s.pan + pnb, kPLD, s.tile, kBLD,
@@ -716,7 +723,14 @@ __global__ void __launch_bounds__(kFT, 512 / kFT) leaf_fused_kernel(const LeafFu
     stamp(5);
     // ---- outputs: [v | Y_i] for the solve, pivot statistics
     double* Yv = f.Yv + leaf * f.strideYv;
-    for (int e = tid; e < ni * nr; e += kFT) __stcs(&Yv[e], R[e]);  // streamed: keep W resident in L2
+    for (int e0 = tid; e0 < ni * nr; e0 += 8 * kFT) {  // 8 loads in flight; streamed stores keep W in L2
+      double t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t[u] = e0 + u * kFT < ni * nr ? R[e0 + u * kFT] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (e0 + u * kFT < ni * nr) __stcs(&Yv[e0 + u * kFT], t[u]);
+    }
     if (tid == 0 && f.stats) {
       f.stats[3 * leaf + 0] = s.pmin;
       f.stats[3 * leaf + 1] = s.pmax;
