@@ -58,13 +58,13 @@ __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelA
   const int rank = cs > 1 ? (int)cluster_ctarank() : 0;
   const long long b = blockIdx.x / cs;
   double* M = a.M + b * a.stride;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;  // nthr <= kPanelThreads
   const int rows_total = a.n - a.j0;
   const int r_begin = rank * a.rpc;
   const int nr = max(0, min(rows_total - r_begin, a.rpc));
   const int nb = a.nb;
 
-  for (int e = tid; e < nr * nb; e += kPanelThreads) {
+  for (int e = tid; e < nr * nb; e += nthr) {
     const int r = e % nr, c = e / nr;
     pan[c * a.rpc + r] = M[(long long)(a.j0 + c) * a.ld + a.j0 + r_begin + r];
   }
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelA
     // ---- local argmax over panel rows >= j
     double bv = -1.0;
     int bi = INT_MAX;
-    for (int r = tid; r < nr; r += kPanelThreads) {
+    for (int r = tid; r < nr; r += nthr) {
       const int gr = r_begin + r;
       if (gr >= j) argmax_merge(bv, bi, fabs(pan[j * a.rpc + r]), gr);
     }
@@ -92,8 +92,8 @@ __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelA
     __syncthreads();
     const int own_j = j / a.rpc;
     if (warp == 0) {
-      bv = lane < kPanelThreads / 32 ? wv[lane] : -1.0;
-      bi = lane < kPanelThreads / 32 ? wi[lane] : INT_MAX;
+      bv = lane < nthr / 32 ? wv[lane] : -1.0;
+      bi = lane < nthr / 32 ? wi[lane] : INT_MAX;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelA
     // Row exchange without a barrier: row j takes the pivot row (nobody reads row j again in this
     // column), and the owner of row piv eliminates from the old row j (jrow) instead of pan.
     if (piv != j && own_j == rank)
-      for (int c = tid; c < nb; c += kPanelThreads) pan[c * a.rpc + (j - r_begin)] = urow[c];
+      for (int c = tid; c < nb; c += nthr) pan[c * a.rpc + (j - r_begin)] = urow[c];
 
     const double pv = urow[j];
     const double apv = fabs(pv);
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelA
     // Each thread only touches its own rows, and the next column reads other threads' rows only
     // after its first barrier, so no barrier closes the column.
     const double inv = apv > 0.0 ? 1.0 / pv : 0.0;
-    for (int r = tid; r < nr; r += kPanelThreads) {
+    for (int r = tid; r < nr; r += nthr) {
       const int gr = r_begin + r;
       if (gr <= j) continue;
       const bool swapped = (gr == piv && piv != j);
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelA
   }
   __syncthreads();
 
-  for (int e = tid; e < nr * nb; e += kPanelThreads) {
+  for (int e = tid; e < nr * nb; e += nthr) {
     const int r = e % nr, c = e / nr;
     M[(long long)(a.j0 + c) * a.ld + a.j0 + r_begin + r] = pan[c * a.rpc + r];
   }
@@ -395,7 +395,10 @@ cudaError_t launch_panel(int batch, int n, int j0, int nb, BatchedMat M, int* ip
     smem_set = std::max<size_t>(smem, 48 * 1024);
   }
   if (cs == 1) {
-    panel_getrf_kernel<<<batch, kPanelThreads, smem, st>>>(pa);
+    // single-CTA panels: one thread per row up to kPanelThreads (the 56- and 112-row panels of the
+    // deep merge levels would otherwise run 4-6 warps with no rows through every barrier)
+    const int threads = std::min(kPanelThreads, std::max(32, (rpc + 31) / 32 * 32));
+    panel_getrf_kernel<<<batch, threads, smem, st>>>(pa);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
