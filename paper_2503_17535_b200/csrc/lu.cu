@@ -245,13 +245,12 @@ __global__ void __launch_bounds__(kColThreads) swap_trsm_kernel(const SwapTrsmAr
   double v[kLuNB];
 #pragma unroll
   for (int jj = 0; jj < kLuNB; ++jj) v[jj] = jj < nb ? x[a.j0 + jj] : 0.0;
+  // column-oriented (right-looking) substitution: the updates of one step are independent FMAs,
+  // so the dependent chain is nb steps long instead of nb^2/2
 #pragma unroll
-  for (int jj = 1; jj < kLuNB; ++jj) {
-    double acc = v[jj];
+  for (int ii = 0; ii < kLuNB - 1; ++ii)
 #pragma unroll
-    for (int ii = 0; ii < jj; ++ii) acc -= L11[jj][ii] * v[ii];
-    v[jj] = acc;
-  }
+    for (int jj = ii + 1; jj < kLuNB; ++jj) v[jj] -= L11[jj][ii] * v[ii];
 #pragma unroll
   for (int jj = 0; jj < kLuNB; ++jj)
     if (jj < nb) x[a.j0 + jj] = v[jj];
@@ -272,9 +271,11 @@ __global__ void __launch_bounds__(kColThreads) trsm_upper_kernel(const TrsmUArgs
   const long long b = blockIdx.x;
   const double* U = a.U + b * a.strideU;
   const int nb = a.nb;
+  __shared__ double rdiag[kLuNB];
   for (int e = threadIdx.x; e < nb * nb; e += kColThreads) {
     const int r = e % nb, c = e / nb;
     U11[r][c] = U[(long long)(a.r0 + c) * a.ldU + a.r0 + r];
+    if (r == c) rdiag[r] = 1.0 / U11[r][c];
   }
   __syncthreads();
   const int col = blockIdx.y * kColThreads + threadIdx.x;
@@ -283,14 +284,13 @@ __global__ void __launch_bounds__(kColThreads) trsm_upper_kernel(const TrsmUArgs
   double v[kLuNB];
 #pragma unroll
   for (int jj = 0; jj < kLuNB; ++jj) v[jj] = jj < nb ? x[jj] : 0.0;
+  // column-oriented back substitution (independent FMAs per step; reciprocal of the diagonal)
 #pragma unroll
   for (int jj = kLuNB - 1; jj >= 0; --jj) {
     if (jj < nb) {
-      double acc = v[jj];
+      v[jj] *= rdiag[jj];
 #pragma unroll
-      for (int ii = jj + 1; ii < kLuNB; ++ii)
-        if (ii < nb) acc -= U11[jj][ii] * v[ii];
-      v[jj] = acc / U11[jj][jj];
+      for (int ii = 0; ii < jj; ++ii) v[ii] -= U11[ii][jj] * v[jj];
     }
   }
 #pragma unroll
