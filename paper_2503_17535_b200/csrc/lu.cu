@@ -990,10 +990,15 @@ __global__ void __launch_bounds__(256) slab_trsv_kernel(const double* T, long lo
     const int ra = UPPER ? 0 : s0, rb = UPPER ? s0 + nb : nbk;  // rows touched: diag block + rest
     __syncthreads();
     // stage T[r0 + ra .. r0 + rb, r0 + s0 .. + nb) (column-major in tb: tb[k * kOuterNB + r])
+    // cp.async: all 32 of a thread's loads in flight (a plain load/store loop waits one memory
+    // latency per element; rows outside [ra, rb) are zero-filled and never read)
     for (int e = tid; e < kLuNB * kOuterNB; e += 256) {
       const int k = e / kOuterNB, r = e % kOuterNB;
-      if (r >= ra && r < rb && k < nb) tb[e] = T[(long long)(r0 + s0 + k) * ldT + r0 + r];
+      const bool ok = r >= ra && r < rb && k < nb;
+      cp_async8(tb + e, ok ? T + (long long)(r0 + s0 + k) * ldT + r0 + r : T, ok);
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
     if (w < m) {
       double x = xs[w][s0 + lane < nbk ? s0 + lane : 0];
