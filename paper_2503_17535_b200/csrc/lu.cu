@@ -603,10 +603,12 @@ __global__ void __launch_bounds__(128) slab_trsm_kernel(const SlabArgs a) {
 
   int step = 0, chunk = -1, slot = 0;
   stage(step, chunk, ring);
-  for (int e = tid; e < kSlabCW * kOuterNB; e += blockDim.x) {
+  for (int e = tid; e < kSlabCW * kOuterNB; e += blockDim.x) {  // cp.async: every load in flight
     const int r = e % kOuterNB, c = e / kOuterNB;
-    xs[c * kSlabLdX + r] = (r < a.nbk && c0 + c < a.ncols) ? X[(long long)(c0 + c) * a.ldX + a.r0 + r] : 0.0;
+    const bool ok = r < a.nbk && c0 + c < a.ncols;
+    cp_async8(xs + c * kSlabLdX + r, ok ? X + (long long)(c0 + c) * a.ldX + a.r0 + r : X, ok);
   }
+  cp_async_commit();
   const int wc = warp * 8;  // this warp's 8 columns of the strip
   while (step < it.nblk) {
     int ns = step, nc = chunk;
