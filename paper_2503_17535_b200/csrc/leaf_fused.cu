@@ -367,17 +367,12 @@ __device__ void panel_gepp_warp(FusedSmem& s, double* W, int ni, int j0, int pnb
     }
   };
   const int rows = ni - j0;
-  if (tid < rows) {  // thread = row (rows <= 196 < kFT), 8 columns' loads in flight per batch
+  if (tid < rows) {  // thread = row (rows <= 196 < kFT); cp.async keeps all pnb loads in flight
     const double* src = W + (long long)j0 * ni + j0 + tid;
-    for (int c0 = 0; c0 < pnb; c0 += 8) {
-      double t[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) t[u] = c0 + u < pnb ? src[(long long)(c0 + u) * ni] : 0.0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (c0 + u < pnb) s.pan[(c0 + u) * kPLD + tid] = t[u];
-    }
+    for (int c = 0; c < pnb; ++c) cp_async8(s.pan + c * kPLD + tid, src + (long long)c * ni, true);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   for (int r = tid; r < rows; r += kFT) s.prow[r] = r;
   __syncthreads();
   tick(40);
@@ -508,8 +503,11 @@ __global__ void __launch_bounds__(kFT, 512 / kFT) leaf_fused_kernel(const LeafFu
       s.pmax = 0.0;
       s.first_zero = -1;
     }
-    if (p_in_smem)
-      for (int e = tid; e < ne * nb; e += kFT) s.tile[e] = f.P[e];
+    if (p_in_smem) {
+      for (int e = tid; e < ne * nb; e += kFT) cp_async8(s.tile + e, f.P + e, true);
+      cp_async_commit();
+      cp_async_wait<0>();
+    }
     __syncthreads();
     stamp(1);
     // ---- B. R[:, 1 + j] = -sum over the row's exterior neighbours of L_ie * P[e, j]
@@ -572,20 +570,13 @@ __global__ void __launch_bounds__(kFT, 512 / kFT) leaf_fused_kernel(const LeafFu
       const int rc0 = j0 + pnb, nrc = ncol - rc0;
       for (int cc0 = 0; cc0 < nrc; cc0 += kTileCols) {
         const int ncc = min(kTileCols, nrc - cc0);
-        for (int e0 = 0; e0 < ncc * kNB; e0 += 8 * kFT) {
-          double t[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int e = e0 + tid + u * kFT;
-            const int kk = e % kNB, c = e / kNB;
-            t[u] = (e < ncc * kNB && kk < pnb) ? W[(long long)(rc0 + cc0 + c) * ni + j0 + kk] : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int e = e0 + tid + u * kFT;
-            if (e < ncc * kNB) s.tile[(e / kNB) * kBLD + e % kNB] = t[u];
-          }
+        for (int e = tid; e < ncc * kNB; e += kFT) {  // cp.async: all loads in flight, rows >= pnb zero
+          const int kk = e % kNB, c = e / kNB;
+          const bool ok = kk < pnb;
+          cp_async8(s.tile + c * kBLD + kk, ok ? W + (long long)(rc0 + cc0 + c) * ni + j0 + kk : W, ok);
         }
+        cp_async_commit();
+        cp_async_wait<0>();
         __syncthreads();
         for (int c = tid; c < ncc; c += kFT) {
           double* col = s.tile + c * kBLD;
@@ -654,9 +645,10 @@ __global__ void __launch_bounds__(kFT, 512 / kFT) leaf_fused_kernel(const LeafFu
           // U[0:r0, r0:r0+bnb] -> s.pan (A operand), one column per warp, rows over the lanes
           for (int c = warp - 2; c < bnb; c += kFW - 2) {
             const double* src = W + (long long)(r0 + c) * ni;
-#pragma unroll 4
-            for (int r = lane; r < r0; r += 32) s.pan[c * kPLD + r] = src[r];
+            for (int r = lane; r < r0; r += 32) cp_async8(s.pan + c * kPLD + r, src + r, true);
           }
+          cp_async_commit();
+          cp_async_wait<0>();
         }
         __syncthreads();
         if (r0 > 0) {
@@ -681,14 +673,17 @@ __global__ void __launch_bounds__(kFT, 512 / kFT) leaf_fused_kernel(const LeafFu
       static_assert(kEK * kEQ <= kNB * kPLD && kEQ * 64 <= kTileCols * kBLD, "E-phase staging");
       for (int k0 = 0; k0 < ni; k0 += kEK) {
         const int kc = min(kEK, ni - k0);
+        // cp.async staging: every element's load in flight at once
         for (int e = tid; e < nb * kc; e += kFT) {
           const int r = e % nb, kk = e / nb;
-          s.pan[kk * kEQ + r] = f.Qi[(long long)(k0 + kk) * nb + r];
+          cp_async8(s.pan + kk * kEQ + r, f.Qi + (long long)(k0 + kk) * nb + r, true);
         }
         for (int e = tid; e < nr * kEK; e += kFT) {
           const int kk = e % kEK, c = e / kEK;
-          s.tile[c * kEQ + kk] = kk < kc ? R[(long long)c * ni + k0 + kk] : 0.0;
+          cp_async8(s.tile + c * kEQ + kk, kk < kc ? R + (long long)c * ni + k0 + kk : R, kk < kc);
         }
+        cp_async_commit();
+        cp_async_wait<0>();
         __syncthreads();
 #pragma unroll
         for (int u = 0; u < kMaxT; ++u) {
