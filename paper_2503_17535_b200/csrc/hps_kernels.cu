@@ -280,20 +280,31 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const GatherArgs
       cc = (col - 1) % s;
     }
     double* dcol = dst + (long long)dcolumn * a.ld;
-    for (int r = lane; r < a.nrows; r += 32) {
-      const int rsec = r / s, rr = r - rsec * s;
-      const int* tab = a.src + 2 * (rsec * nslots + slot);
-      double v = 0.0;
+    // four rows per lane per batch: every operand load of the batch is issued before its stores
+    // (the sources are read-only here, __ldg), so the loop is not one memory latency per row
+    for (int r0 = lane; r0 < a.nrows; r0 += 128) {
+      double v[4];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int code = __ldg(tab + k);
-        if (code < 0) continue;
-        const int child = code >> 6, rf = (code >> 3) & 7, cfp1 = code & 7;
-        const double* T = ch0 + child * a.child_stride;
-        const long long hc = cfp1 == 0 ? 0 : 1 + (long long)(cfp1 - 1) * s + cc;
-        v += T[hc * a.child_nb + rf * s + rr];
+      for (int q = 0; q < 4; ++q) {
+        const int r = r0 + 32 * q;
+        v[q] = 0.0;
+        if (r < a.nrows) {
+          const int rsec = r / s, rr = r - rsec * s;
+          const int* tab = a.src + 2 * (rsec * nslots + slot);
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int code = __ldg(tab + k);
+            if (code < 0) continue;
+            const int child = code >> 6, rf = (code >> 3) & 7, cfp1 = code & 7;
+            const double* T = ch0 + child * a.child_stride;
+            const long long hc = cfp1 == 0 ? 0 : 1 + (long long)(cfp1 - 1) * s + cc;
+            v[q] += __ldg(T + hc * a.child_nb + rf * s + rr);
+          }
+        }
       }
-      dcol[r] = v;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (r0 + 32 * q < a.nrows) dcol[r0 + 32 * q] = v[q];
     }
   }
 }
