@@ -27,10 +27,10 @@ __global__ void __launch_bounds__(kRows) gemv_kernel(const GemvArgs a, double* p
   const int k0 = chunk * kKChunk, k1 = min(a.k, k0 + kKChunk);
   const double* A = a.A + b * a.sA;
   const double* X = a.x + b * a.sx;
-  for (int e = threadIdx.x; e < (k1 - k0) * NV; e += kRows) {
-    const int kk = e % (k1 - k0), v = e / (k1 - k0);
-    xs[v][kk] = X[(long long)v * a.ldx + k0 + kk];
-  }
+  for (int v = 0; v < NV; ++v)  // cp.async: the x chunk's loads all in flight
+    for (int kk = threadIdx.x; kk < k1 - k0; kk += kRows) cp_async8(&xs[v][kk], X + (long long)v * a.ldx + k0 + kk, true);
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   if (row >= a.m) return;
   double acc[NV];
