@@ -220,11 +220,13 @@ __global__ void __launch_bounds__(kColThreads) swap_trsm_kernel(const SwapTrsmAr
   const long long b = blockIdx.x;
   const double* L = a.L + b * a.strideL;
   const int nb = a.nb;
-  for (int e = threadIdx.x; e < nb * nb; e += kColThreads) {
+  for (int e = threadIdx.x; e < nb * nb; e += kColThreads) {  // cp.async: all loads in flight
     const int r = e % nb, c = e / nb;
-    L11[r][c] = L[(long long)(a.j0 + c) * a.ldL + a.j0 + r];
+    cp_async8(&L11[r][c], L + (long long)(a.j0 + c) * a.ldL + a.j0 + r, true);
   }
+  cp_async_commit();
   for (int e = threadIdx.x; e < nb; e += kColThreads) piv[e] = a.ipiv[b * a.n + a.j0 + e];
+  cp_async_wait<0>();
   __syncthreads();
 
   int col = blockIdx.y * kColThreads + threadIdx.x;
@@ -272,11 +274,14 @@ __global__ void __launch_bounds__(kColThreads) trsm_upper_kernel(const TrsmUArgs
   const double* U = a.U + b * a.strideU;
   const int nb = a.nb;
   __shared__ double rdiag[kLuNB];
-  for (int e = threadIdx.x; e < nb * nb; e += kColThreads) {
+  for (int e = threadIdx.x; e < nb * nb; e += kColThreads) {  // cp.async: all loads in flight
     const int r = e % nb, c = e / nb;
-    U11[r][c] = U[(long long)(a.r0 + c) * a.ldU + a.r0 + r];
-    if (r == c) rdiag[r] = 1.0 / U11[r][c];
+    cp_async8(&U11[r][c], U + (long long)(a.r0 + c) * a.ldU + a.r0 + r, true);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  for (int r = threadIdx.x; r < nb; r += kColThreads) rdiag[r] = 1.0 / U11[r][r];
   __syncthreads();
   const int col = blockIdx.y * kColThreads + threadIdx.x;
   if (col >= a.ncols) return;
