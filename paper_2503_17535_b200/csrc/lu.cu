@@ -64,10 +64,12 @@ __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelA
   const int nr = max(0, min(rows_total - r_begin, a.rpc));
   const int nb = a.nb;
 
-  for (int e = tid; e < nr * nb; e += nthr) {
+  for (int e = tid; e < nr * nb; e += nthr) {  // cp.async: all of a thread's loads in flight
     const int r = e % nr, c = e / nr;
-    pan[c * a.rpc + r] = M[(long long)(a.j0 + c) * a.ld + a.j0 + r_begin + r];
+    cp_async8(pan + c * a.rpc + r, M + (long long)(a.j0 + c) * a.ld + a.j0 + r_begin + r, true);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
 
   double pmin = DBL_MAX, pmax = 0.0;
