@@ -240,6 +240,11 @@ int hpsg_dev_getrf_aug(int batch, int n, int m, double* M, long long ld, long lo
                        double* stats);
 int hpsg_dev_getrs(int batch, int n, int m, const double* LU, long long ld, long long stride, const int* ipiv,
                    double* R, long long ldr, long long strideR);
+/* Live timing of the DMMA GEMM inside the hot path (bench roofline of the GEMM): mode 1 starts
+ * recording (a CUDA event pair per launch on its own stream, plus 2mnk FLOPs per matrix), mode 0
+ * stops, mode 2 synchronises and returns the summed launch time (ms), FLOPs and launch count of the
+ * recording.  Instrumentation only: the product path records nothing unless started. */
+int hpsg_dev_gemm_timing(int mode, double* ms, double* flops, long long* launches);
 
 #ifdef __cplusplus
 }

@@ -1,4 +1,5 @@
 // gemm.cu -- tile-shape dispatch for the strided-batched DMMA DGEMM (gemm.cuh).
+#include <vector>
 #include <algorithm>
 #include <climits>
 #include <cstdio>
@@ -134,7 +135,66 @@ bool launch_dgemm_tma(const GemmArgs& a, cudaStream_t st, cudaError_t* err) {
   }
 }
 
+// Live GEMM timing (hpsg_dev_gemm_timing): while enabled, every launch is bracketed by CUDA events on
+// its own stream and its algorithmic FLOPs (2 m n k per matrix) are recorded; the sums are read after
+// the caller synchronises.  Off by default (no events on the product path).
+namespace {
+struct GemmTimer {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;
+  size_t used = 0;
+  double flops = 0.0;
+  long long launches = 0;
+};
+GemmTimer& gemm_timer() {
+  static GemmTimer t;
+  return t;
+}
+}  // namespace
+
+void gemm_timing_enable(bool on) {
+  GemmTimer& t = gemm_timer();
+  t.on = on;
+  t.used = 0;
+  t.flops = 0.0;
+  t.launches = 0;
+}
+
+bool gemm_timing_read(double* ms, double* flops, long long* launches) {
+  GemmTimer& t = gemm_timer();
+  double tot = 0.0;
+  for (size_t i = 0; i + 1 < t.used; i += 2) {
+    float x = 0.f;
+    if (cudaEventElapsedTime(&x, t.ev[i], t.ev[i + 1]) != cudaSuccess) return false;
+    tot += x;
+  }
+  *ms = tot;
+  *flops = t.flops;
+  *launches = t.launches;
+  return true;
+}
+
+static cudaError_t launch_dgemm_impl(const GemmArgs& a, cudaStream_t st);
+
 cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st) {
+  GemmTimer& t = gemm_timer();
+  if (!t.on || a.m <= 0 || a.n <= 0 || a.batch <= 0) return launch_dgemm_impl(a, st);
+  while (t.ev.size() < t.used + 2) {
+    cudaEvent_t e;
+    cudaError_t r = cudaEventCreate(&e);
+    if (r != cudaSuccess) return r;
+    t.ev.push_back(e);
+  }
+  cudaEventRecord(t.ev[t.used], st);
+  const cudaError_t r = launch_dgemm_impl(a, st);
+  cudaEventRecord(t.ev[t.used + 1], st);
+  t.used += 2;
+  t.flops += 2.0 * a.m * a.n * double(a.k) * a.batch;
+  ++t.launches;
+  return r;
+}
+
+static cudaError_t launch_dgemm_impl(const GemmArgs& a, cudaStream_t st) {
   if (a.m <= 0 || a.n <= 0 || a.batch <= 0) return cudaSuccess;
   static const bool log = getenv("HPS_GEMM_LOG") != nullptr;  // developer knob: shape trace for launch lists
   if (log) fprintf(stderr, "GEMM %d %d %d %d\n", a.m, a.n, a.k, a.batch);

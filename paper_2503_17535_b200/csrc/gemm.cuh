@@ -196,5 +196,8 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, STAGES, VEC>::kThr
 
 // Host launcher: picks a tile shape from the problem size.
 cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st);
+// live timing of every launch_dgemm (developer/bench instrumentation; see hpsg_dev_gemm_timing)
+void gemm_timing_enable(bool on);
+bool gemm_timing_read(double* ms, double* flops, long long* launches);
 
 }  // namespace hpsk

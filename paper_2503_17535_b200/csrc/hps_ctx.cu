@@ -1782,6 +1782,16 @@ extern "C" int hpsg_dev_dgemm(int m, int n, int k, int batch, double alpha, cons
   return e == cudaSuccess ? HPSG_OK : HPSG_ERR_CUDA;
 }
 
+extern "C" int hpsg_dev_gemm_timing(int mode, double* ms, double* flops, long long* launches) {
+  if (mode == 1 || mode == 0) {
+    hpsk::gemm_timing_enable(mode == 1);
+    return HPSG_OK;
+  }
+  if (!ms || !flops || !launches) return HPSG_ERR_INVALID;
+  if (cudaDeviceSynchronize() != cudaSuccess) return HPSG_ERR_CUDA;
+  return hpsk::gemm_timing_read(ms, flops, launches) ? HPSG_OK : HPSG_ERR_CUDA;
+}
+
 extern "C" int hpsg_dev_getrf_aug(int batch, int n, int m, double* M, long long ld, long long stride, int* ipiv,
                                   double* stats) {
   cudaError_t e = hpsk::lu_stats_init(stats, batch, 0);
