@@ -142,6 +142,7 @@ namespace {
 struct GemmTimer {
   bool on = false;
   std::vector<cudaEvent_t> ev;
+  std::vector<long long> shape;  // m, n, k, batch per launch (dumped with HPS_GEMM_TIMING_DUMP)
   size_t used = 0;
   double flops = 0.0;
   long long launches = 0;
@@ -163,10 +164,15 @@ void gemm_timing_enable(bool on) {
 bool gemm_timing_read(double* ms, double* flops, long long* launches) {
   GemmTimer& t = gemm_timer();
   double tot = 0.0;
+  const bool dump = getenv("HPS_GEMM_TIMING_DUMP") != nullptr;  // developer knob: per-launch table
   for (size_t i = 0; i + 1 < t.used; i += 2) {
     float x = 0.f;
     if (cudaEventElapsedTime(&x, t.ev[i], t.ev[i + 1]) != cudaSuccess) return false;
     tot += x;
+    if (dump) {
+      const long long* sh = &t.shape[2 * i];
+      fprintf(stderr, "GEMMT %lld %lld %lld %lld %.4f\n", sh[0], sh[1], sh[2], sh[3], x);
+    }
   }
   *ms = tot;
   *flops = t.flops;
@@ -186,6 +192,8 @@ cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st) {
     t.ev.push_back(e);
   }
   cudaEventRecord(t.ev[t.used], st);
+  t.shape.resize(2 * (t.used + 2));
+  t.shape[2 * t.used] = a.m, t.shape[2 * t.used + 1] = a.n, t.shape[2 * t.used + 2] = a.k, t.shape[2 * t.used + 3] = a.batch;
   const cudaError_t r = launch_dgemm_impl(a, st);
   cudaEventRecord(t.ev[t.used + 1], st);
   t.used += 2;
