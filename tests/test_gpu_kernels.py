@@ -114,3 +114,33 @@ def test_getrf_aug_narrow_panels_large_n():
     res = (A @ X - R).abs().max() / (A.abs().max() * X.abs().max() * n)
     assert res < 1e-14, float(res)
     assert st[0, 2].item() == -1
+
+
+def test_gemm_live_timing():
+    """hpsg_dev_gemm_timing (the bench's live GEMM roofline): records each launch's CUDA-event time and
+    its 2mnk FLOPs while on, nothing while off."""
+    import ctypes as C
+    L = lib()
+    L.hpsg_dev_gemm_timing.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                       C.POINTER(C.c_longlong)]
+    rng = np.random.default_rng(5)
+    m, n, k, b = 512, 384, 256, 3
+    A, B, Cm = colmajor(b, m, k, rng), colmajor(b, k, n, rng), colmajor(b, m, n, rng)
+    D = torch.zeros_like(Cm)
+
+    def gemm():
+        assert L.hpsg_dev_dgemm(m, n, k, b, 1.0, A.data_ptr(), m, m * k, B.data_ptr(), k, k * n, 0.0,
+                                Cm.data_ptr(), m, m * n, D.data_ptr(), m, m * n) == 0
+
+    ms, fl, nl = C.c_double(), C.c_double(), C.c_longlong()
+    assert L.hpsg_dev_gemm_timing(1, None, None, None) == 0
+    gemm()
+    gemm()
+    assert L.hpsg_dev_gemm_timing(2, C.byref(ms), C.byref(fl), C.byref(nl)) == 0
+    assert nl.value == 2 and fl.value == 2 * 2.0 * m * n * k * b and ms.value > 0.0
+    assert L.hpsg_dev_gemm_timing(0, None, None, None) == 0
+    gemm()  # not recorded after stop
+    assert L.hpsg_dev_gemm_timing(1, None, None, None) == 0
+    assert L.hpsg_dev_gemm_timing(2, C.byref(ms), C.byref(fl), C.byref(nl)) == 0
+    assert nl.value == 0 and fl.value == 0.0
+    assert L.hpsg_dev_gemm_timing(0, None, None, None) == 0
