@@ -258,8 +258,11 @@ __device__ __forceinline__ void leaf_assemble_block_t(const LeafAsmArgs& a, long
         E[(long long)(cj - ni) * ni + r] = v;
     }
   } else {
-    // zero fill (coalesced, 16-byte stores where aligned)
-    if (ldM == ni && (ni % 2) == 0 && ((reinterpret_cast<uintptr_t>(M) & 15) == 0)) {
+    // zero fill (coalesced; 32-byte STG.256 stores where aligned, else 16-byte)
+    if (ldM == ni && ((ni * ni) % 4) == 0 && ((reinterpret_cast<uintptr_t>(M) & 31) == 0)) {
+      for (int e = tid; e < ni * ni / 4; e += nthr)
+        asm volatile("st.global.v4.f64 [%0], {%1, %1, %1, %1};" ::"l"(M + 4 * (long long)e), "d"(0.0) : "memory");
+    } else if (ldM == ni && (ni % 2) == 0 && ((reinterpret_cast<uintptr_t>(M) & 15) == 0)) {
       double2* m2 = reinterpret_cast<double2*>(M);
       for (int e = tid; e < ni * ni / 2; e += nthr) m2[e] = make_double2(0.0, 0.0);
     } else {
