@@ -935,7 +935,8 @@ cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double*
   // look-ahead (panels of the next outer block on a high-priority side stream) measured at L=8:
   // d0 -1.7 ms, d1 -3 ms, d2 -1 ms; HPS_LU_LOOKAHEAD=0 turns it off
   const int la_env = getenv("HPS_LU_LOOKAHEAD") ? atoi(getenv("HPS_LU_LOOKAHEAD")) : 1;
-  const bool la = la_env > 0 && n > 2 * kOuterNB;
+  static const int la_min = getenv("HPS_LU_LOOKAHEAD_MIN_N") ? atoi(getenv("HPS_LU_LOOKAHEAD_MIN_N")) : 2 * kOuterNB;
+  const bool la = la_env > 0 && n > la_min && n > kOuterNB;  // tuning knob: smallest n for the look-ahead
   if (la) return bgetrf_aug_lookahead(batch, n, m, M, ipiv, stats, st, keep_L);
   const long long ld = M.ld, sM = M.stride;
   double* A = M.p;
