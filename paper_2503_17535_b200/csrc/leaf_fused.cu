@@ -514,11 +514,26 @@ __global__ void __launch_bounds__(kFT, 512 / kFT) leaf_fused_kernel(const LeafFu
     {
       const double* Pm = p_in_smem ? s.tile : f.P;
       const int nz = 2 * dim;
-      for (int e = tid; e < ni * nb; e += kFT) {
-        const int r = e % ni, j = e / ni;
-        double acc = 0.0;
-        for (int z = 0; z < nz; ++z) acc += nz_val[z * ni + r] * Pm[j * ne + nz_idx[z * ni + r]];
-        R[(long long)(1 + j) * ni + r] = -acc;
+      // rows over the lanes, columns over the warps (no per-element index division); a row's
+      // exterior neighbours are loaded once and reused for the warp's columns
+      for (int r0 = 0; r0 < ni; r0 += 32) {
+        const int r = r0 + lane;
+        if (r >= ni) break;
+        double zv[4];
+        int zi[4];
+#pragma unroll
+        for (int z = 0; z < 4; ++z) {
+          zv[z] = z < nz ? nz_val[z * ni + r] : 0.0;
+          zi[z] = z < nz ? nz_idx[z * ni + r] : 0;
+        }
+        for (int j = warp; j < nb; j += kFW) {
+          const double* Pj = Pm + j * ne;
+          double acc = 0.0;
+#pragma unroll
+          for (int z = 0; z < 4; ++z)
+            if (z < nz) acc += zv[z] * Pj[zi[z]];
+          R[(long long)(1 + j) * ni + r] = -acc;
+        }
       }
     }
     __syncthreads();
@@ -738,7 +753,7 @@ __global__ void __launch_bounds__(kFT, 512 / kFT) leaf_fused_kernel(const LeafFu
 
 bool leaf_fused_supported(int n, int p, int ni, int nb, int dim, bool mixed_terms) {
   const int tmn = (nb + 7) / 8, tnn = (nb + 8) / 8;
-  return !mixed_terms && n <= 256 && p <= 16 && ni <= kMaxNI && ni <= kFT && ni + 1 + nb <= kMaxCols &&
+  return !mixed_terms && dim == 2 && n <= 256 && p <= 16 && ni <= kMaxNI && ni <= kFT && ni + 1 + nb <= kMaxCols &&
          ni * 2 * dim <= kMaxNz && tmn * tnn <= 7 * kFW && 1 + nb <= kTileCols && nb <= 64 && 1 + nb <= 64 &&
          (size_t)kNB * kNB * 8 <= sizeof(LeafAsmSmemT<256, 16>);
 }
