@@ -18,6 +18,7 @@ constexpr int kPanelThreads = 256;
 constexpr int kRowsPerCta = 448;  // 448 x 32 doubles = 112 KiB of panel per CTA
 constexpr int kMaxCluster = 16;   // non-portable cluster size (same GPC)
 constexpr int kMaxRowsPerCta = 864;
+constexpr int kTrsvMaxRhs = 4;    // few-RHS triangular solves (slab_trsv_kernel): right-hand sides per call
 
 struct PanelArgs {
   double* M;
@@ -709,9 +710,18 @@ cudaError_t slab_trsm(int batch, const double* T, long long ldT, long long sT, i
 }
 
 // Blocked back substitution R <- U^-1 R, U = upper triangle of LU (n x n).
+}  // namespace
+template <bool UPPER>
+cudaError_t trsv_blocked(const double* T, long long ldT, int n, double* X, long long ldX, int m, cudaStream_t st);
+namespace {
+
 cudaError_t back_subst(int batch, int n, int m, const double* U, long long ldU, long long strideU, double* R,
                        long long ldR, long long strideR, cudaStream_t st) {
   if (m <= 0) return cudaSuccess;
+  // one large matrix with a few RHS (the implicit root's [D | h] factorization): the slab TRSV
+  // (one CTA per 256-row slab + a streaming GEMV) instead of a chain of 32x32 TRSM + GEMM launches
+  if (batch == 1 && m <= kTrsvMaxRhs && n >= 2 * kOuterNB && !getenv("HPS_NO_BLOCK_TRSV"))
+    return trsv_blocked<true>(U, ldU, n, R, ldR, m, st);
   const int nouter = (n + kOuterNB - 1) / kOuterNB;
   for (int ob = nouter - 1; ob >= 0; --ob) {
     const int r0 = ob * kOuterNB, r1 = std::min(n, r0 + kOuterNB);
@@ -980,7 +990,6 @@ cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double*
 // Per 256-row slab: ONE CTA solves the slab (its eight 32x32 diagonal blocks one warp per RHS
 // with shuffle broadcasts, the in-slab updates by the whole CTA), then one streaming GEMV applies
 // the slab to every remaining row.  2 launches per slab instead of ~17.
-constexpr int kTrsvMaxRhs = 4;
 
 template <bool UPPER>
 __global__ void __launch_bounds__(256) slab_trsv_kernel(const double* T, long long ldT, int r0, int nbk, double* X,
