@@ -8,6 +8,7 @@
 // shared memory and splits long k ranges over CTAs with an ordered (deterministic)
 // second-pass reduction.
 #include <algorithm>
+#include <cstdlib>
 
 #include "gemv.cuh"
 
@@ -84,12 +85,70 @@ __global__ void gemv_reduce_kernel(const GemvArgs a, const double* partial, int 
   }
 }
 
+// Short-k, few-CTA shape (the root substitution's slab updates: m <= 7168 rows, k = 256): one
+// row per thread makes every thread walk all k columns in dependent batches of 8 loads, so the
+// launch is latency-bound (~29 us whatever m is). Here a CTA covers 32 rows with 8 warps, warp w
+// streaming its own contiguous k range (coalesced 256-byte column segments, 8 loads in flight),
+// and the 8 partial sums are added in a fixed order through shared memory (deterministic).
+constexpr int kWideRows = 32, kWideWarps = 8;
+
+template <int NV>
+__global__ void __launch_bounds__(kWideRows* kWideWarps) gemv_wide_kernel(const GemvArgs a) {
+  __shared__ double part[kWideWarps][NV][kWideRows];
+  const long long b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row = blockIdx.y * kWideRows + lane;
+  const int kc = (a.k + kWideWarps - 1) / kWideWarps;
+  const int k0 = min(a.k, warp * kc), k1 = min(a.k, k0 + kc);
+  const double* X = a.x + b * a.sx;
+  double acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+  if (row < a.m) {
+    const double* ap = a.A + b * a.sA + row;
+    int kk = k0;
+    for (; kk + 8 <= k1; kk += 8) {
+      double t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t[u] = __ldg(ap + (long long)(kk + u) * a.lda);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v] += t[u] * __ldg(X + (long long)v * a.ldx + kk + u);
+    }
+    for (; kk < k1; ++kk) {
+      const double t = __ldg(ap + (long long)kk * a.lda);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) acc[v] += t * __ldg(X + (long long)v * a.ldx + kk);
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < NV; ++v) part[warp][v][lane] = acc[v];
+  __syncthreads();
+  if (warp < NV && row < a.m) {
+    const int v = warp;
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWideWarps; ++w) s += part[w][v][lane];
+    double* Y = a.y + b * a.sy;
+    double r = a.alpha * s;
+    if (a.beta != 0.0) r += a.beta * Y[(long long)v * a.ldy + row];
+    Y[(long long)v * a.ldy + row] = r;
+  }
+}
+
 template <int NV>
 cudaError_t run(const GemvArgs& a, double* scratch, size_t scratch_elems, cudaStream_t st, int* launches) {
   const int row_tiles = (a.m + kRows - 1) / kRows;
   int nchunks = (a.k + kKChunk - 1) / kKChunk;
   // split k only when the grid would otherwise be too small to fill the GPU
   const long long ctas = (long long)a.batch * row_tiles;
+  static const bool wide = getenv("HPS_GEMV_WIDE") ? atoi(getenv("HPS_GEMV_WIDE")) != 0 : true;  // A/B knob
+  if (wide && ctas < 296 && a.k <= kKChunk && a.k >= 2 * kWideWarps) {
+    gemv_wide_kernel<NV><<<dim3(a.batch, (a.m + kWideRows - 1) / kWideRows), kWideRows * kWideWarps, 0, st>>>(a);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+  }
   if (ctas >= 296 || !scratch || (size_t)a.batch * nchunks * NV * a.m > scratch_elems) nchunks = 1;
   if (nchunks == 1 && a.k > kKChunk) {
     // single pass over all of k: loop over chunks inside one CTA

@@ -49,7 +49,7 @@ def test_dgemm_broadcast_and_inplace():
 
 @pytest.mark.parametrize("n,m,b", [(5, 2, 3), (56, 113, 7), (112, 225, 5), (196, 57, 9), (224, 449, 3),
                                    (448, 897, 2), (896, 64, 2), (896, 1793, 1), (1792, 33, 1), (3584, 4, 1),
-                                   (600, 100, 3), (1000, 7, 2)])
+                                   (600, 100, 3), (1000, 7, 2), (2000, 1, 1), (1100, 3, 1)])
 def test_getrf_aug(n, m, b):
     rng = np.random.default_rng(n + m)
     A = rng.standard_normal((b, n, n))
