@@ -87,10 +87,11 @@ __global__ void gemv_reduce_kernel(const GemvArgs a, const double* partial, int 
 
 // Short-k, few-CTA shape (the root substitution's slab updates: m <= 7168 rows, k = 256): one
 // row per thread makes every thread walk all k columns in dependent batches of 8 loads, so the
-// launch is latency-bound (~29 us whatever m is). Here a CTA covers 32 rows with 8 warps, warp w
-// streaming its own contiguous k range (coalesced 256-byte column segments, 8 loads in flight),
-// and the 8 partial sums are added in a fixed order through shared memory (deterministic).
-constexpr int kWideRows = 32, kWideWarps = 8;
+// launch is latency-bound (~29 us whatever m is). Here a CTA covers 32 rows with 16 warps, warp w
+// streaming its own contiguous k range (coalesced 256-byte column segments, 16 loads in flight:
+// k = 256 is one batch per thread), and the 16 partial sums are added in a fixed order through
+// shared memory (deterministic).
+constexpr int kWideRows = 32, kWideWarps = 16, kWideU = 16;
 
 template <int NV>
 __global__ void __launch_bounds__(kWideRows* kWideWarps) gemv_wide_kernel(const GemvArgs a) {
@@ -107,12 +108,12 @@ __global__ void __launch_bounds__(kWideRows* kWideWarps) gemv_wide_kernel(const 
   if (row < a.m) {
     const double* ap = a.A + b * a.sA + row;
     int kk = k0;
-    for (; kk + 8 <= k1; kk += 8) {
-      double t[8];
+    for (; kk + kWideU <= k1; kk += kWideU) {
+      double t[kWideU];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) t[u] = __ldg(ap + (long long)(kk + u) * a.lda);
+      for (int u = 0; u < kWideU; ++u) t[u] = __ldg(ap + (long long)(kk + u) * a.lda);
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < kWideU; ++u)
 #pragma unroll
         for (int v = 0; v < NV; ++v) acc[v] += t[u] * __ldg(X + (long long)v * a.ldx + kk + u);
     }
