@@ -13,7 +13,8 @@ import numpy as np
 
 from .hps import (FIELD_BUMPS, FIELD_BUMPS_GRAD, FIELD_BUMPS_SIN, FIELD_CONST, FIELD_DIVGRAD_SRC, FIELD_PLANE_COS,
                   FIELD_PLANE_SIN, FIELD_POISSON2D_SRC,
-                  ROLE_GRADIENT, ROLE_LAPLACIAN, ROLE_ZEROTH, Field, Term, bump_centers)
+                  ROLE_GRADIENT, ROLE_LAPLACIAN, ROLE_ZEROTH, Field, Term)
+from .seeded import bump_centers  # pure Python: defining a problem never loads a shared object
 
 
 @dataclass
