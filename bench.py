@@ -14,9 +14,10 @@ data H2D, the whole solution field D2H inside the timed region).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
---impl reference times the reference algorithm on the host cores: the C++
-restatement in oracle/ (the reference itself needs Eigen, absent here), with
-all host threads.
+--impl reference times the REFERENCE itself on the host cores: its own unmodified
+sources (/root/reference/proj/src) compiled against an Eigen-API shim into
+oracle/_ref/libhps_ref.so, serial loops as written + threaded BLAS on every core;
+each step is a bounded sample scaled to the full L=8 step (bench.py reference_sample).
 
 Under torchrun (N>1) the default is the north star's subtree-sharded run (strong scaling:
 ONE L=8 problem over N GPUs, paper_2503_17535_b200/sharded.py): each rank builds its
@@ -213,12 +214,9 @@ def run_b200(args):
         "vs_baseline": value / world / PAPER_H100_DOFS,
         "vs_baseline_ref": "per-GPU DOF/s / 4.17e6 DOF/s (PAPER.md:629, H100 JAX subtree recompute, p=16 L=8, 4.02 s)",
         "dtype": "f64", "data": "synthetic (seeded bump potential, manufactured plane wave; coefficients evaluated on device)",
-        "config": {"workload": f"2D variable-coefficient Helmholtz DtN HPS, p={args.p}, L={args.L} uniform quadtree, "
-                               f"N={N} DOF (BASELINE configs[1])", "k": args.k, "seed": args.seed,
-                   "root": "explicit S" if args.explicit_root else "implicit S (MergeOptions::implicit_S)",
-                   "sign": "corrected (v=+L^-1 f); literal differs only in the sign of f",
-                   "l2": "inputs larger than L2 (each step streams > 40 GB of leaf/merge operands)",
-                   "parallelism": f"{world} independent replica(s)"},
+        "config": workload_config(args, world),
+        "parallelism": f"{world} independent replica(s)",
+        "sign": "corrected (v=+L^-1 f); literal differs only in the sign of f",
         "stages_ms": {"build": t_build, "leaf": st["t_leaf_ms"], "merge": st["t_merge_ms"], "solve": t_solve,
                       "merge_by_depth": [round(x, 3) for x in st["t_level_ms"]]},
         # dominant single kernel: leaf_fused_kernel (one launch per build, ~35% of the step in the
@@ -264,7 +262,8 @@ def run_b200(args):
         out["configs_extra"]["subtree_recompute_L9"] = bench_recompute(torch, args, 9, 2)
         out["configs_extra"]["planner_L9_80GB"] = bench_planner(args, 9, 80e9)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"], par = cpu_baseline(args, prob, u_gpu)
+        out["cpu_baseline"] = reference_sample(args, prob)
+        out["cpu_baseline_parallel_port"], par = parallel_port_baseline(args, prob, u_gpu)
         out["accuracy"].update(par)
     if world > 1:
         dist.barrier()
@@ -528,13 +527,10 @@ def run_sharded(args, world, rank, local):
         "vs_baseline": value / PAPER_H100_DOFS,
         "vs_baseline_ref": "job DOF/s / 4.17e6 DOF/s (PAPER.md:629, 1x H100 JAX subtree recompute, p=16 L=8, 4.02 s)",
         "dtype": "f64", "data": "synthetic (seeded bump potential, manufactured plane wave; coefficients evaluated on device)",
-        "config": {"workload": f"2D variable-coefficient Helmholtz DtN HPS, p={args.p}, L={args.L} uniform quadtree, "
-                               f"N={N} DOF (BASELINE configs[1])", "k": args.k, "seed": args.seed,
-                   "root": "explicit S" if args.explicit_root else "implicit S (MergeOptions::implicit_S)",
-                   "sign": "corrected (v=+L^-1 f); literal differs only in the sign of f",
-                   "l2": "inputs larger than L2 (each step streams > 40 GB of leaf/merge operands)",
-                   "parallelism": f"subtree-sharded over {world} GPUs: cut depth {plan.ds}, "
-                                  f"{plan.n_sub} subtrees, NCCL P2P of {up / 1e6:.0f} MB [h|T] up per build"},
+        "config": workload_config(args, world),
+        "parallelism": f"subtree-sharded over {world} GPUs: cut depth {plan.ds}, "
+                       f"{plan.n_sub} subtrees, NCCL P2P of {up / 1e6:.0f} MB [h|T] up per build",
+        "sign": "corrected (v=+L^-1 f); literal differs only in the sign of f",
         "roofline": {"bound": "tensor", "kernel": "build (batched DMMA LU/TRSM/GEMM pipeline), whole job",
                      "achieved": flops / (ms / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS * world, "unit": "TFLOP/s",
                      "frac": flops / (ms / 1e3) / 1e12 / (FP64_PEAK_TFLOPS * world), "traffic": None,
@@ -552,8 +548,54 @@ def run_sharded(args, world, rank, local):
         print(json.dumps(out), flush=True)
 
 
-def cpu_baseline(args, prob, u_gpu=None):
-    """Oracle (C++ restatement of the reference) on the host cores: full workload, one run."""
+def workload_config(args, world):
+    """The `config` object of both arms (identical dicts, so the driver can pair them)."""
+    N = (4 ** args.L) * args.p ** 2
+    return {"workload": f"2D variable-coefficient Helmholtz DtN HPS, p={args.p}, L={args.L} uniform quadtree, "
+                        f"N={N} DOF (BASELINE configs[1])", "k": args.k, "seed": args.seed,
+            "root": "explicit S" if args.explicit_root else "implicit S (MergeOptions::implicit_S)",
+            "l2": "inputs larger than L2 (each step streams > 40 GB of leaf/merge operands)"}
+
+
+def _oracle_terms(prob):
+    from oracle import oracle as O
+    keep, terms = [], []
+    for t in prob.terms:
+        f, k = O.make_field(t.field.kind, t.field.c, t.field.centers, t.field.samples)
+        keep += k
+        terms.append((t.role, t.axis, t.axis2, f))
+    src, k = O.make_field(prob.source.kind, prob.source.c, prob.source.centers, prob.source.samples)
+    keep += k
+    return terms, src, keep
+
+
+def reference_sample(args, prob, m=None):
+    """The REFERENCE's own build + solve (oracle/_ref: /root/reference/proj/src unmodified + the Eigen-API
+    shim) on the host cores, as written: serial leaf and merge loops, BLAS (Eigen's OpenMP GEMM in the
+    original build) on every core.  A full L=8 step takes minutes, so each step is a bounded sample scaled
+    to the whole step (ref_capi.h ref_bench_sample): one depth-(L-m) subtree built and solved end to end by
+    the reference x 4^(L-m), plus one reference merge_node + propagate step per top depth x 4^d."""
+    from oracle import ref as R
+    threads = os.cpu_count()
+    R.set_threads(threads)
+    m = m if m is not None else min(args.L, 5)
+    terms, src, keep = _oracle_terms(prob)
+    est = R.bench_sample(args.p, args.L, m, prob.lo, prob.hi, terms, src, root_implicit=not args.explicit_root)
+    N = (4 ** args.L) * args.p ** 2
+    top = args.L - m
+    sample = (f"reference HpsSolver build+solve of one depth-{top} subtree ({est['sub_leaves']} leaves, "
+              f"{est['sub_build_s']:.2f} s + {est['sub_solve_s']:.3f} s) x {4 ** top}, plus one reference "
+              f"merge_node + propagate per depth d < {top} (" +
+              ", ".join(f"d{d}: {est['merge_s'][d]:.2f}+{est['propagate_s'][d]:.3f} s x {4 ** d}" for d in range(top)) +
+              f"); estimated full step {est['est_s']:.1f} s")
+    return {"value": N / est["est_s"], "unit": "DOF/s", "cores": threads, "kind": "reference",
+            "schedule": "reference-faithful: serial leaf/merge loops (solver.cpp:144-151), threaded BLAS",
+            "sample": sample, "est_step_s": est["est_s"]}
+
+
+def parallel_port_baseline(args, prob, u_gpu=None):
+    """The oracle restatement (C++ port) on the host cores with OpenMP over leaves and merges: the FULL
+    workload, one build + solve (labelled: a parallel schedule the reference does not have)."""
     from oracle import oracle as O
     from tests.oracle_problems import oracle_solver
     threads = os.cpu_count()
@@ -567,35 +609,50 @@ def cpu_baseline(args, prob, u_gpu=None):
     t2 = time.perf_counter()
     N = s.n_leaves * s.npts
     res = {"value": N / (t2 - t0), "unit": "DOF/s", "cores": threads, "kind": "port",
-           "sample": f"full workload at L={args.cpu_L} (N={N}), one build+solve, OpenMP over leaves/merges "
-                     f"+ threaded OpenBLAS; build {t1 - t0:.2f} s, solve {t2 - t1:.2f} s"}
+           "schedule": "parallel port: OpenMP over leaves and over the merges of a level + threaded OpenBLAS",
+           "sample": f"full workload at L={args.cpu_L} (N={N}), one build+solve; build {t1 - t0:.2f} s, "
+                     f"solve {t2 - t1:.2f} s"}
     par = {}
     if u_gpu is not None and args.cpu_L == args.L:
         par["rel_linf_vs_oracle"] = float(np.abs(u_gpu - u).max() / np.abs(u).max())
+        par["parity_tol"] = 1e-10
+        par["parity_ok"] = bool(par["rel_linf_vs_oracle"] <= 1e-10)
     return res, par
+
+
+def native_libs():
+    """Shared objects of this repo mapped into the process (the reference arm must map only oracle/)."""
+    try:
+        with open("/proc/self/maps") as f:
+            paths = {line.split()[-1] for line in f if line.rstrip().endswith(".so") and ROOT in line}
+        return sorted(os.path.relpath(p, ROOT) for p in paths)
+    except OSError:
+        return []
 
 
 def run_reference(args):
     world, rank, _ = dist_setup()
     if rank != 0:
         return
-    from paper_2503_17535_b200 import problems as PR
+    from paper_2503_17535_b200 import problems as PR   # descriptors only: no shared object is loaded
     prob = PR.helmholtz_bumps(k=args.k, seed=args.seed)
-    times = []
-    res = None
+    vals, res = [], None
     for i in range(args.warmup + args.steps):
-        res, _ = cpu_baseline(args, prob)
+        res = reference_sample(args, prob)
         if i >= args.warmup:
-            times.append(res["value"])
-    value = float(np.median(times))
-    N = (4 ** args.cpu_L) * args.p ** 2
-    out = {"metric": METRIC, "impl": "reference", "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": N / value * 1e3, "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"2D variable-coefficient Helmholtz DtN HPS, p={args.p}, L={args.cpu_L}, N={N} DOF "
-                                  "(BASELINE configs[1])", "k": args.k, "seed": args.seed},
+            vals.append(res["value"])
+    value = float(np.median(vals))
+    libs = native_libs()
+    if any("libhps_b200" in x for x in libs):
+        raise SystemExit("reference arm mapped the product library: " + ", ".join(libs))
+    out = {"metric": METRIC, "impl": "reference", "value": value, "unit": "DOF/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": (4 ** args.L) * args.p ** 2 / value * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded bump potential, manufactured plane wave)",
+           "config": workload_config(args, world),
            "cpu_baseline": dict(res, value=value),
-           "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "native_libs": libs}
     print(json.dumps(out), flush=True)
 
 

@@ -68,6 +68,8 @@ def lib():
         L.ref_times.argtypes = [vp, dp, dp]
         L.ref_solve_problem.argtypes = [C.c_char_p, C.c_double, C.c_uint, C.c_int, C.c_int, C.c_int, C.c_double,
                                         C.c_int, dp]
+        L.ref_bench_sample.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.POINTER(Term), C.c_int,
+                                       C.POINTER(Field), C.c_int, dp]
         _lib = L
     return _lib
 
@@ -100,6 +102,20 @@ def solve_problem(name, p, L=3, adaptive=False, tol=1e-3, max_depth=10, k=0.0, s
     check(lib().ref_solve_problem(name.encode(), k, seed, p, int(adaptive), L, tol, max_depth, _dp(out)))
     keys = ["rel_linf", "rel_l2", "n_leaves", "N", "top_D_size", "tree_depth", "t_build_s", "t_solve_s"]
     return dict(zip(keys, out.tolist()))
+
+
+def bench_sample(p, L, m, lo, hi, terms, source, root_implicit=True):
+    """ref_bench_sample (ref_capi.h): the reference's full 2D build + solve time, estimated from one
+    depth-(L-m) subtree solved end to end plus one merge_node + propagate step per top depth."""
+    arr = (Term * max(1, len(terms)))()
+    for i, (role, axis, axis2, fld) in enumerate(terms):
+        arr[i].role, arr[i].axis, arr[i].axis2, arr[i].field = role, axis, axis2, fld
+    top = L - m
+    out = np.zeros(4 + 2 * max(top, 0))
+    check(lib().ref_bench_sample(p, L, m, lo, hi, arr, len(terms), C.byref(source) if source is not None else None,
+                                 int(root_implicit), _dp(out)))
+    return dict(est_s=out[0], sub_build_s=out[1], sub_solve_s=out[2], sub_leaves=int(out[3]),
+                merge_s=[out[4 + 2 * d] for d in range(top)], propagate_s=[out[5 + 2 * d] for d in range(top)])
 
 
 class RefSolver:

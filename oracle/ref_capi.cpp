@@ -423,4 +423,86 @@ int ref_solve_problem(const char* name, double k, unsigned seed, int p, int adap
   });
 }
 
+int ref_bench_sample(int p, int L, int m, double lo, double hi, const oracle_term* terms, int n_terms,
+                     const oracle_field* source, int root_implicit, double* out) {
+  return guard([&] {
+    if (m < 1 || m > L) throw std::runtime_error("ref_bench_sample: need 1 <= m <= L");
+    const int top = L - m;  // depths 0 .. top-1 are sampled one node each
+    // (1) one depth-`top` subtree, end to end, by the reference solver
+    const double side = (hi - lo) / double(1 << top);
+    void* sub = ref_create(2, p, m, lo, lo + side, terms, n_terms, source, nullptr, 0, 1.0, 0, 0);
+    if (!sub) throw std::runtime_error(g_err);
+    std::unique_ptr<RefHandle> hs(static_cast<RefHandle*>(sub));
+    double t0 = now_s();
+    hs->sr->build();
+    const double t_build = now_s() - t0;
+    const int nb = hps::node_boundary_size(*hs->tree, 0);
+    hps::VecR g = hps::VecR::Zero(nb);
+    for (int i = 0; i < nb; ++i) g[i] = std::sin(0.37 * i);
+    t0 = now_s();
+    const auto field = hs->sr->solve(g);
+    const double t_solve = now_s() - t0;
+    double est = std::pow(4.0, top) * (t_build + t_solve);
+    out[1] = t_build;
+    out[2] = t_solve;
+    out[3] = hs->tree->n_leaves();
+    // (2) one merge + propagate per top depth, children of the true size
+    hps::Box dom;
+    dom.lo = hps::Point(lo, lo, 0.0);
+    dom.hi = hps::Point(hi, hi, 0.0);
+    const hps::DiscretizationTree full = hps::build_uniform_tree(dom, L, 2, p);
+    for (int d = top - 1; d >= 0; --d) {
+      const int nid = full.levels[d][0];
+      const hps::TreeNode& node = full.nodes[nid];
+      std::vector<std::vector<hps::PanelLayout>> secs(4);
+      std::vector<hps::MatR> T(4);
+      std::vector<hps::VecR> h(4);
+      std::vector<hps::ChildView<Real>> views(4);
+      for (int c = 0; c < 4; ++c) {
+        const int cid = node.child[c];
+        for (int f = 0; f < 4; ++f) secs[c].push_back(hps::node_section_layout(full, cid, f));
+        const int n = hps::node_boundary_size(full, cid);
+        T[c] = hps::MatR(n, n);
+        h[c] = hps::VecR(n);
+        for (int j = 0; j < n; ++j) {
+          h[c][j] = std::cos(0.11 * j + c);
+          for (int i = 0; i < n; ++i) T[c](i, j) = std::sin(1.7 * i + 0.3 * j + c) + (i == j ? 4.0 : 0.0);
+        }
+        views[c].T = &T[c];
+        views[c].h = &h[c];
+        views[c].sections = &secs[c];
+        views[c].node_id = cid;
+      }
+      hps::MergeOptions mo;
+      mo.is_root = d == 0;
+      mo.implicit_S = d == 0 && root_implicit;
+      t0 = now_s();
+      hps::MergeOutput<Real> mout = hps::merge_node<Real>(2, hps::Variant::dtn, views, nullptr, mo);
+      const double t_merge = now_s() - t0;
+      // the propagate step of this node (solver.cpp:199-212): g_int, then the scatter into the children
+      const hps::MergeArtifact<Real>& art = mout.art;
+      hps::VecR gj = hps::VecR::Zero(art.n_ext);
+      for (int i = 0; i < art.n_ext; ++i) gj[i] = std::sin(0.21 * i);
+      t0 = now_s();
+      hps::VecR g_int = art.implicit ? hps::VecR(art.gtilde - art.apply_Dinv(hps::artifact_apply_C(art, views, gj)))
+                                     : hps::VecR(art.S_mat * gj + art.gtilde);
+      std::vector<hps::VecR> gc(4);
+      for (int c = 0; c < 4; ++c) {
+        const auto& offs = art.child_face_off[c];
+        gc[c].resize(offs[4]);
+        for (int f = 0; f < 4; ++f) {
+          const auto& mp = art.child_maps[c][f];
+          gc[c].segment(offs[f], mp.dst_len) =
+              mp.ext ? gj.segment(mp.offset, mp.src_len).eval() : g_int.segment(mp.offset, mp.src_len).eval();
+        }
+      }
+      const double t_prop = now_s() - t0;
+      out[4 + 2 * d] = t_merge;
+      out[5 + 2 * d] = t_prop;
+      est += std::pow(4.0, d) * (t_merge + t_prop);
+    }
+    out[0] = est;
+  });
+}
+
 }  // extern "C"

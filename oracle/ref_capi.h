@@ -73,6 +73,19 @@ void ref_times(void* h, double* t_build_s, double* t_solve_s);
 int ref_solve_problem(const char* name, double k, unsigned seed, int p, int adaptive, int L, double tol,
                       int max_depth, double* out);
 
+/* Bounded, extrapolated sample of the reference's full build + solve of a uniform 2D DtN problem
+ * (bench.py's reference arm).  The tree of depth L is split at depth L-m:
+ *   - one depth-(L-m) subtree is built and solved end to end by the reference (an HpsSolver over that
+ *     subtree's box, m levels, the same operator terms and source); the other 4^(L-m) - 1 subtrees cost the
+ *     same (uniform tree, identical shapes);
+ *   - for every depth d < L-m, one reference merge_node (merge.cpp:486-494) on four children of the true
+ *     size (child T/h synthetic: dense LU / GEMM time does not depend on the values) and the downward
+ *     propagate step of that node (solver.cpp:199-212) are timed; there are 4^d such nodes.
+ * out[0..3] = {estimated seconds of the full step, t_sub_build, t_sub_solve, leaves in the subtree};
+ * out[4 + 2d], out[5 + 2d] = {t_merge(d), t_propagate(d)} for d = 0 .. L-m-1. */
+int ref_bench_sample(int p, int L, int m, double lo, double hi, const oracle_term* terms, int n_terms,
+                     const oracle_field* source, int root_implicit, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -431,3 +431,27 @@ def test_subtree_recompute_matches_store(depth, recompute):
         u = rs.solve_device(torch.tensor(np.stack([g, -0.5 * g]), device="cuda")).cpu().numpy()
         assert rel(u, u_ref) < 1e-12
     rs.close()
+
+
+def test_headline_operator_L7_parity():
+    """BASELINE configs[1] operator at L = 7 (16,384 leaves, root D = 3584): GPU vs the parallel oracle
+    on identical inputs, <= 1e-10 (the L = 8 headline agreement is asserted by bench.py)."""
+    prob = PR.helmholtz_bumps()
+    s = gpu_solver(prob, 16, 7, literal=False, root_implicit=True)
+    o = oracle_solver(prob, 16, 7, literal=False, root_implicit=True, parallel=True)
+    o.build()
+    g = prob.boundary(s.root_boundary_points())
+    assert rel(s.solve(g), o.solve(g)) < 1e-10
+
+
+def test_config4_3d_L4_parity():
+    """BASELINE configs[3]: 3D variable-coefficient Poisson p=8, uniform octree L=4 (N = 2,097,152, root
+    D = 27,648, 16-column cluster panels) against the parallel oracle, <= 1e-10."""
+    prob = PR.poisson3d_var()
+    s = gpu_solver(prob, 8, 4, literal=False, root_implicit=True)
+    o = oracle_solver(prob, 8, 4, literal=False, root_implicit=True, parallel=True)
+    o.build()
+    g = prob.boundary(s.root_boundary_points())
+    u = s.solve(g)
+    assert rel(u, o.solve(g)) < 1e-10
+    assert PR.rel_linf(u, prob.exact(s.leaf_points())) < 1e-7
