@@ -88,6 +88,9 @@ typedef struct {
   int build_root_T;     /* ItI: form and factor the root T for the radiation closure
                            (SolverOptions::build_root_T, solver.hpp:19; solver.cpp:153-157) */
   const hpsg_field* source_imag;  /* ItI: imaginary part of the complex source (NULL: real source) */
+  /* execution choices (zero = the measured default; results agree to roundoff either way) */
+  int force_batched_leaf;  /* 1: multi-launch batched leaf path instead of the persistent fused leaf kernel */
+  int no_lu_lookahead;     /* 1: plain blocked LU driver instead of the look-ahead driver for n > 512 */
 } hpsg_options;
 enum { HPSG_VARIANT_DTN = 0, HPSG_VARIANT_ITI = 1 };
 

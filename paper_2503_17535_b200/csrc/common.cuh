@@ -15,6 +15,17 @@
 
 namespace hpsk {
 
+// Host side: cudaFuncSetAttribute is per device, so one-time attribute flags are kept per device ordinal.
+struct PerDeviceFlag {
+  unsigned long long set = 0;  // bit d: done on device d
+  size_t value[64] = {};       // e.g. the dynamic shared-memory size configured on device d
+};
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d & 63;
+}
+
 HPS_DEV void dmma_8x8x4(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)

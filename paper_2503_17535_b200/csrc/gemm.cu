@@ -17,11 +17,12 @@ template <int BM, int BN, int BK, int WM, int WN, int ST, bool VEC>
 cudaError_t run(const GemmArgs& a, cudaStream_t st) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, ST, VEC>;
   auto kern = dgemm_dmma_kernel<BM, BN, BK, WM, WN, ST, VEC>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
+  static PerDeviceFlag attr;  // per instantiation and device
+  const int dv = current_device();
+  if (!(attr.set >> dv & 1)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr.set |= 1ull << dv;
   }
   // tile index = blockIdx.z * gridDim.y + blockIdx.y (gridDim.y/z <= 65535; batch in x)
   const long long tiles = (long long)((a.m + BM - 1) / BM) * ((a.n + BN - 1) / BN);
@@ -35,36 +36,11 @@ cudaError_t run(const GemmArgs& a, cudaStream_t st) {
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 }  // namespace
 
-// Tile configurations (CTA tile BMxBN, k-step BK, warp tile WMxWN, pipeline stages).
-// HPS_GEMM_CFG (env, developer knob) forces one config for the tuning sweep in tools/gemm_bench.py.
-static int forced_cfg() {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("HPS_GEMM_CFG");
-    v = e ? atoi(e) : -1;
-  }
-  return v;
-}
-
+// CTA tile 64x64, k-step 16, four 32x32 warp tiles, 3-stage pipeline: the measured best of the round-1
+// tile sweep (profiles/r01_ncu_summary.md) for every build shape.
 template <bool V>
-static cudaError_t run_cfg(int cfg, const GemmArgs& a, cudaStream_t st) {
-  switch (cfg) {
-    case 0: return run<128, 128, 16, 32, 64, 3, V>(a, st);   // 8 warps, 64 acc/thread
-    case 1: return run<128, 128, 16, 32, 32, 3, V>(a, st);   // 16 warps, 32 acc/thread
-    case 2: return run<128, 128, 32, 32, 32, 3, V>(a, st);   // 16 warps, BK=32
-    case 3: return run<128, 128, 16, 32, 32, 4, V>(a, st);   // 16 warps, 4 stages
-    case 4: return run<64, 64, 16, 32, 32, 3, V>(a, st);     // 4 warps
-    case 5: return run<64, 64, 16, 16, 32, 3, V>(a, st);     // 8 warps
-    case 6: return run<128, 64, 16, 32, 32, 3, V>(a, st);    // 8 warps
-    case 7: return run<64, 128, 16, 32, 32, 3, V>(a, st);    // 8 warps
-    case 8: return run<64, 64, 32, 16, 32, 3, V>(a, st);     // 8 warps, BK=32
-    case 9: return run<64, 64, 16, 32, 32, 4, V>(a, st);     // 4 warps, 4 stages
-    case 10: return run<64, 64, 32, 32, 32, 2, V>(a, st);    // 4 warps, BK=32, 2 stages
-    case 11: return run<64, 32, 16, 32, 32, 3, V>(a, st);    // 2 warps
-    case 12: return run<32, 64, 16, 32, 32, 3, V>(a, st);    // 2 warps
-    case 13: return run<64, 64, 16, 32, 16, 3, V>(a, st);    // 8 warps of 32x16
-    default: return cudaErrorInvalidValue;
-  }
+static cudaError_t run_default(const GemmArgs& a, cudaStream_t st) {
+  return run<64, 64, 16, 32, 32, 3, V>(a, st);
 }
 
 namespace {
@@ -108,11 +84,12 @@ bool run_tma(const GemmArgs& a, cudaStream_t st, cudaError_t* err) {
   if (!make_map(&mA, a.A, a.m, a.k, a.lda, a.sA, a.batch, BM + 4, BK)) return false;
   if (!make_map(&mB, a.B, a.k, a.n, a.ldb, a.sB, a.batch, BK + 4, BN)) return false;
   auto kern = dgemm_tma_kernel<BM, BN, BK, WM, WN, ST>;
-  static bool attr = false;  // per instantiation
-  if (!attr) {
+  static PerDeviceFlag attr;  // per instantiation and device
+  const int dv = current_device();
+  if (!(attr.set >> dv & 1)) {
     *err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes + 64);
     if (*err != cudaSuccess) return true;
-    attr = true;
+    attr.set |= 1ull << dv;
   }
   const long long tiles = (long long)((a.m + BM - 1) / BM) * ((a.n + BN - 1) / BN);
   const unsigned ty = (unsigned)std::min<long long>(tiles, 65535), tz = (unsigned)((tiles + ty - 1) / ty);
@@ -123,16 +100,7 @@ bool run_tma(const GemmArgs& a, cudaStream_t st, cudaError_t* err) {
 }
 
 bool launch_dgemm_tma(const GemmArgs& a, cudaStream_t st, cudaError_t* err) {
-  static const int tcfg = getenv("HPS_TMA_CFG") ? atoi(getenv("HPS_TMA_CFG")) : 0;  // tuning knob
-  switch (tcfg) {
-    case 1: return run_tma<64, 64, 16, 32, 32, 4>(a, st, err);
-    case 2: return run_tma<64, 64, 32, 32, 32, 2>(a, st, err);
-    case 3: return run_tma<64, 64, 32, 32, 32, 3>(a, st, err);
-    case 4: return run_tma<128, 64, 16, 32, 32, 3>(a, st, err);
-    case 5: return run_tma<64, 128, 16, 32, 32, 3>(a, st, err);
-    case 6: return run_tma<128, 128, 16, 32, 32, 3>(a, st, err);
-    default: return run_tma<64, 64, 16, 32, 32, 3>(a, st, err);
-  }
+  return run_tma<64, 64, 16, 32, 32, 3>(a, st, err);
 }
 
 // Live GEMM timing (hpsg_dev_gemm_timing): while enabled, every launch is bracketed by CUDA events on
@@ -142,7 +110,6 @@ namespace {
 struct GemmTimer {
   bool on = false;
   std::vector<cudaEvent_t> ev;
-  std::vector<long long> shape;  // m, n, k, batch per launch (dumped with HPS_GEMM_TIMING_DUMP)
   size_t used = 0;
   double flops = 0.0;
   long long launches = 0;
@@ -164,15 +131,10 @@ void gemm_timing_enable(bool on) {
 bool gemm_timing_read(double* ms, double* flops, long long* launches) {
   GemmTimer& t = gemm_timer();
   double tot = 0.0;
-  const bool dump = getenv("HPS_GEMM_TIMING_DUMP") != nullptr;  // developer knob: per-launch table
   for (size_t i = 0; i + 1 < t.used; i += 2) {
     float x = 0.f;
     if (cudaEventElapsedTime(&x, t.ev[i], t.ev[i + 1]) != cudaSuccess) return false;
     tot += x;
-    if (dump) {
-      const long long* sh = &t.shape[2 * i];
-      fprintf(stderr, "GEMMT %lld %lld %lld %lld %.4f\n", sh[0], sh[1], sh[2], sh[3], x);
-    }
   }
   *ms = tot;
   *flops = t.flops;
@@ -192,8 +154,6 @@ cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st) {
     t.ev.push_back(e);
   }
   cudaEventRecord(t.ev[t.used], st);
-  t.shape.resize(2 * (t.used + 2));
-  t.shape[2 * t.used] = a.m, t.shape[2 * t.used + 1] = a.n, t.shape[2 * t.used + 2] = a.k, t.shape[2 * t.used + 3] = a.batch;
   const cudaError_t r = launch_dgemm_impl(a, st);
   cudaEventRecord(t.ev[t.used + 1], st);
   t.used += 2;
@@ -204,27 +164,16 @@ cudaError_t launch_dgemm(const GemmArgs& a, cudaStream_t st) {
 
 static cudaError_t launch_dgemm_impl(const GemmArgs& a, cudaStream_t st) {
   if (a.m <= 0 || a.n <= 0 || a.batch <= 0) return cudaSuccess;
-  static const bool log = getenv("HPS_GEMM_LOG") != nullptr;  // developer knob: shape trace for launch lists
-  if (log) fprintf(stderr, "GEMM %d %d %d %d\n", a.m, a.n, a.k, a.batch);
   // k <= 0 runs zero k-tiles: D = beta*C
   const bool vec = aligned16(a.A) && aligned16(a.B) && (a.lda % 2 == 0) && (a.ldb % 2 == 0) &&
                    (a.sA % 2 == 0) && (a.sB % 2 == 0);
-  int cfg = forced_cfg();
-  if (cfg < 0) {
-    const long long work_tiles_big = (long long)((a.m + 127) / 128) * ((a.n + 127) / 128) * a.batch;
-    cfg = 4;
-    (void)work_tiles_big;
-  }
-  // seeding measured best at every k inside the build (merge 256 -> 232 ms); knob for sweeps
-  static const int seed_k = getenv("HPS_GEMM_SEED_K") ? atoi(getenv("HPS_GEMM_SEED_K")) : INT_MAX;
+  // accumulators seeded with C at every k (measured best inside the build: merges 256 -> 232 ms)
   GemmArgs b = a;
-  b.seed_k_max = seed_k;
-  static const bool use_tma = getenv("HPS_GEMM_TMA") ? atoi(getenv("HPS_GEMM_TMA")) != 0 : true;
-  if (use_tma && cfg == 4) {  // TMA-staged operands (same tiles); falls back when a map is not legal
-    cudaError_t e = cudaSuccess;
-    if (launch_dgemm_tma(b, st, &e)) return e;
-  }
-  return vec ? run_cfg<true>(cfg, b, st) : run_cfg<false>(cfg, b, st);
+  b.seed_k_max = INT_MAX;
+  // TMA-staged operands (same tiles); the cp.async twin when a tensor map is not legal for the operands
+  cudaError_t e = cudaSuccess;
+  if (launch_dgemm_tma(b, st, &e)) return e;
+  return vec ? run_default<true>(b, st) : run_default<false>(b, st);
 }
 
 }  // namespace hpsk

@@ -144,8 +144,7 @@ cudaError_t run(const GemvArgs& a, double* scratch, size_t scratch_elems, cudaSt
   int nchunks = (a.k + kKChunk - 1) / kKChunk;
   // split k only when the grid would otherwise be too small to fill the GPU
   const long long ctas = (long long)a.batch * row_tiles;
-  static const bool wide = getenv("HPS_GEMV_WIDE") ? atoi(getenv("HPS_GEMV_WIDE")) != 0 : true;  // A/B knob
-  if (wide && ctas < 296 && a.k <= kKChunk && a.k >= 2 * kWideWarps) {
+  if (ctas < 296 && a.k <= kKChunk && a.k >= 2 * kWideWarps) {
     gemv_wide_kernel<NV><<<dim3(a.batch, (a.m + kWideRows - 1) / kWideRows), kWideRows * kWideWarps, 0, st>>>(a);
     if (launches) ++*launches;
     return cudaGetLastError();

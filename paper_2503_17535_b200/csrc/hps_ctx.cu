@@ -164,6 +164,7 @@ struct hpsg_ctx {
   std::vector<char> cut_set;  // cut part: which input [h|T] have been provided
   hpsg_stats stats{};
   int launches = 0;
+  hpsk::LuWorkspace luws;  // batched-LU scratch, counted in dev_bytes (lu.cuh)
 
   long long strideLeafM() const { return (long long)ops.ni * (ops.ni + 1 + ops.nb); }
   // [h|T] per part leaf: a real leaf (nb x (1+nb)) or, for a cut part, an input node
@@ -229,7 +230,12 @@ void matvecs(hpsg_ctx* c, const GemmArgs& g) {
   ck(hpsk::launch_gemv(v, c->gemv_scratch.d(), c->gemv_scratch.bytes / 8, c->st, &c->launches), "gemv");
 }
 
-hpsk::DevField make_dev_field(hpsg_ctx* c, const hpsg_field& f, bool is_source) {
+// `scratch`: a caller-owned list for fields that live only for one call (error_report's exact solution);
+// those buffers are not counted in the context's device bytes.  Default: kept by the context.
+hpsk::DevField make_dev_field(hpsg_ctx* c, const hpsg_field& f, bool is_source,
+                              std::vector<std::unique_ptr<DevBuf>>* scratch = nullptr) {
+  std::vector<std::unique_ptr<DevBuf>>& keep = scratch ? *scratch : c->field_bufs;
+  size_t* total = scratch ? nullptr : &c->dev_bytes;
   hpsk::DevField d{};
   d.kind = f.kind;
   d.n_centers = f.n_centers;
@@ -245,18 +251,18 @@ hpsk::DevField make_dev_field(hpsg_ctx* c, const hpsg_field& f, bool is_source) 
       f.n_centers > 0) {
     if (!f.centers) throw HpsError{HPSG_ERR_INVALID, "bump field without centers"};
     auto b = std::make_unique<DevBuf>();
-    upload(*b, std::vector<double>(f.centers, f.centers + 3 * f.n_centers), &c->dev_bytes, c->st);
+    upload(*b, std::vector<double>(f.centers, f.centers + 3 * f.n_centers), total, c->st);
     d.centers = b->d();
-    c->field_bufs.push_back(std::move(b));
+    keep.push_back(std::move(b));
   }
   if (f.kind == HPSG_FIELD_SAMPLED) {
     if (!f.samples) throw HpsError{HPSG_ERR_INVALID, "sampled field without samples"};
     const size_t n = size_t(c->T.n_leaves()) * c->ops.n;
     auto b = std::make_unique<DevBuf>();
-    b->alloc(n * 8, &c->dev_bytes);
+    b->alloc(n * 8, total);
     if (!g_dry_alloc) ck(cudaMemcpyAsync(b->p, f.samples, n * 8, cudaMemcpyHostToDevice, c->st), "sampled field upload");
     d.samples = b->d();
-    c->field_bufs.push_back(std::move(b));
+    keep.push_back(std::move(b));
   }
   (void)is_source;
   return d;
@@ -407,12 +413,10 @@ void alloc_build(hpsg_ctx* c) {
   const hpsg::LeafOperators& o = c->ops;
   const long long nl = c->T.n_leaves();
   size_t* tot = &c->dev_bytes;
-  const char* path = getenv("HPS_LEAF_PATH");  // developer knob: "batched" forces the multi-launch path
   bool mixed = false;
   for (int i = 0; i < c->nterms; ++i)
     if (c->terms[i].role == HPSG_ROLE_SECOND_ORDER && c->terms[i].axis != c->terms[i].axis2) mixed = true;
-  c->fused = hpsk::leaf_fused_supported(o.n, o.p, o.ni, o.nb, c->tree.dim, mixed) &&
-             !(path && std::string(path) == "batched");
+  c->fused = hpsk::leaf_fused_supported(o.n, o.p, o.ni, o.nb, c->tree.dim, mixed) && !c->opts.force_batched_leaf;
   if (c->opts.keep_factors || c->iti) c->fused = false;  // batched path: keeps [LU | v | Y] + pivots; ItI
   if (c->T.cut) {
     c->fused = false;  // no leaf stage: the part's leaves are input nodes
@@ -420,8 +424,6 @@ void alloc_build(hpsg_ctx* c) {
     int nsm = 0;
     ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->opts.device), "sm count");
     c->fused_grid = int(std::min<long long>(nl, (long long)nsm * hpsk::leaf_fused_ctas_per_sm()));
-    if (const char* gs = getenv("HPS_LEAF_GRID"))  // developer knob: persistent grid size (L2 footprint sweep)
-      c->fused_grid = std::max(1, std::min(c->fused_grid, atoi(gs)));
     const long long per = hpsk::leaf_fused_scratch_per_cta(o.ni, o.ne, o.nb);
     c->leafScratch.alloc(size_t(c->fused_grid) * per * 8, tot);
     c->leafYv.alloc(size_t(nl) * o.ni * (1 + o.nb) * 8, tot);
@@ -456,6 +458,14 @@ void alloc_build(hpsg_ctx* c) {
     c->radPiv.alloc(size_t(R.n_ext) * 4, tot);
     c->radStats.alloc(3 * 8, tot);
   }
+  // scratch of every batched LU the build runs (lu.cuh LuWorkspace), reserved now so it is counted
+  auto reserve = [&](long long batch, int n, int m, bool factor) {
+    ck(hpsk::lu_workspace_reserve(c->luws, int(batch), n, m, factor, g_dry_alloc), "LU workspace");
+  };
+  if (!c->T.cut && !c->fused) reserve(nl, o.ni, 1 + o.nb, true);
+  for (const Level& L : c->lv)
+    reserve(L.nodes, L.n_int, (!c->forms_T(L.d) && c->opts.root_implicit_S) ? 1 : 1 + L.n_ext, true);
+  if (c->root_T) reserve(1, c->lv[0].n_ext, 1, true);
 }
 
 void check_leaf_errors(hpsg_ctx* c) {
@@ -557,7 +567,8 @@ void run_leaf_stage(hpsg_ctx* c) {
     ++c->launches;
     ck(hpsk::lu_stats_init(c->leafStats.d(), nl, c->st), "stats init");
     BatchedMat M{c->leafM.d(), o.ni, sM};
-    ck(hpsk::bgetrf_aug(nl, o.ni, 1 + o.nb, M, c->leafPiv.i(), c->leafStats.d(), c->st, false), "iti leaf bgetrf");
+    ck(hpsk::bgetrf_aug(nl, o.ni, 1 + o.nb, M, c->leafPiv.i(), c->leafStats.d(), c->luws, c->st, false),
+       "iti leaf bgetrf");
     c->launches += lu_launches(o.ni, 1 + o.nb, true);
     GemmArgs t;  // [h | T] = QH [v | Y]  (T = QH Y, h = QH v; local_solve.cpp:170-171)
     t.m = o.nb;
@@ -592,7 +603,8 @@ void run_leaf_stage(hpsg_ctx* c) {
     f.strideHT = c->strideLeafHT();
     f.stats = c->leafStats.d();
     f.n_leaves = nl;
-    if (getenv("HPS_LEAF_PROF")) {  // developer knob: per-phase clock64 stamps of CTA 0
+#ifdef HPS_LEAF_PROFILE  // developer build (-DHPS_LEAF_PROFILE): per-phase clock64 stamps of CTA 0
+    {
       static DevBuf prof;
       const int np = 64 + c->fused_grid;
       prof.alloc(np * 8, nullptr);
@@ -616,6 +628,7 @@ void run_leaf_stage(hpsg_ctx* c) {
       fprintf(stderr, "leaf_fused GEPP leaf 0: stage %lld warp-body %lld subtrsm %lld subupdate %lld\n", h[40], h[41],
               h[42], h[43]);
     }
+#endif
     f.n_leaves = nl;
     ck(hpsk::launch_leaf_fused(f, c->fused_grid, c->st), "leaf_fused");
     ++c->launches;
@@ -645,7 +658,8 @@ void run_leaf_stage(hpsg_ctx* c) {
   // [L_ii | sgn f | -L_ie P] -> [LU | v_i | Y_i]
   ck(hpsk::lu_stats_init(c->leafStats.d(), nl, c->st), "stats init");
   BatchedMat M{c->leafM.d(), o.ni, sM};
-  ck(hpsk::bgetrf_aug(nl, o.ni, 1 + o.nb, M, c->leafPiv.i(), c->leafStats.d(), c->st, c->opts.keep_factors != 0),
+  ck(hpsk::bgetrf_aug(nl, o.ni, 1 + o.nb, M, c->leafPiv.i(), c->leafStats.d(), c->luws, c->st,
+                      c->opts.keep_factors != 0),
      "leaf bgetrf");
   c->launches += lu_launches(o.ni, 1 + o.nb, true);
   // [h | T] = Q_i [v | Y_i] + [0 | Q_e P]   (T = Q Y, h = Q v; local_solve.cpp:140-141)
@@ -750,9 +764,9 @@ void run_merge_level(hpsg_ctx* c, int d) {
   // L of D is needed afterwards only at the root with implicit S (the solve's bgetrs) and for the
   // new-source pass (keep_factors); elsewhere X = D^-1 [h_int | C] is all that is kept
   const bool keep_L = (root && c->opts.root_implicit_S) || c->opts.keep_factors;
-  ck(hpsk::bgetrf_aug(int(L.nodes), L.n_int, m, M, L.piv.i(), L.stats.d(), c->st, keep_L), "merge bgetrf");
+  ck(hpsk::bgetrf_aug(int(L.nodes), L.n_int, m, M, L.piv.i(), L.stats.d(), c->luws, c->st, keep_L), "merge bgetrf");
   c->launches += lu_launches(L.n_int, m, true);
-  if (!root && !c->iti && L.mt.s >= kSparseSchurMinS && !getenv("HPS_DENSE_SCHUR")) {
+  if (!root && !c->iti && L.mt.s >= kSparseSchurMinS) {
     // [h | T] = [h_ext | A] - B [x_h | X] over the nonzero blocks of B only: section e's rows get
     // -B_{e,I} [x_h|X]_I for the runs I of interfaces of e's child (the other blocks of B are
     // structurally zero, merge.cpp:226-278), i.e. half the dense product in 2D, a quarter in 3D
@@ -826,6 +840,8 @@ void ensure_solve_ws(hpsg_ctx* c, int nrhs) {
     c->Ue.alloc(size_t(nl) * c->ops.ne * nrhs * 8, tot);
   }
   c->gemv_scratch.alloc(size_t(8) << 20, tot);  // split-k partial sums (64 MB)
+  if (c->global_root(0) && c->opts.root_implicit_S)  // the implicit root's stored-factor solve
+    ck(hpsk::lu_workspace_reserve(c->luws, 1, c->lv[0].n_int, nrhs, false, g_dry_alloc), "LU workspace");
   c->ws_nrhs = nrhs;
 }
 
@@ -862,7 +878,7 @@ void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_
       matvecs(c, g);
       BatchedMat LU{L.MD.d(), L.n_int, L.strideMD()};
       BatchedMat R{c->GI[0]->d(), L.n_int, sGI};
-      ck(hpsk::bgetrs(1, L.n_int, nrhs, LU, L.piv.i(), R, c->st), "root getrs");
+      ck(hpsk::bgetrs(1, L.n_int, nrhs, LU, L.piv.i(), R, c->luws, c->st), "root getrs");
       c->launches += lu_launches(L.n_int, nrhs, false);
       if (new_source)  // g_int = -(y + D^-1 C g)
         hpsk::launch_axpby(c->GI[0]->d(), L.n_int, sGI, c->srcY[0]->d(), L.n_int, sGI, L.n_int, nrhs, 1, -1.0, -1.0,
@@ -1014,6 +1030,8 @@ void run_source_pass(hpsg_ctx* c, const double* d_f, int K) {
         c->srcHn[L.d]->alloc(size_t(L.nodes) * L.n_ext * K * 8, tot);
       }
     }
+    ck(hpsk::lu_workspace_reserve(c->luws, int(nl), o.ni, K, false), "LU workspace");
+    for (const Level& L : c->lv) ck(hpsk::lu_workspace_reserve(c->luws, int(L.nodes), L.n_int, K, false), "LU workspace");
     c->src_nrhs = K;
   }
   const double sgn = c->opts.literal_sign ? -1.0 : 1.0;
@@ -1021,7 +1039,7 @@ void run_source_pass(hpsg_ctx* c, const double* d_f, int K) {
   ++c->launches;
   BatchedMat LU{c->leafM.d(), o.ni, c->strideLeafM()};
   BatchedMat R{c->srcR.d(), o.ni, (long long)o.ni * K};
-  ck(hpsk::bgetrs(int(nl), o.ni, K, LU, c->leafPiv.i(), R, c->st), "leaf source getrs");
+  ck(hpsk::bgetrs(int(nl), o.ni, K, LU, c->leafPiv.i(), R, c->luws, c->st), "leaf source getrs");
   c->launches += lu_launches(o.ni, K, false);
   GemmArgs q;  // h = Q_i v
   q.m = o.nb;
@@ -1081,7 +1099,7 @@ void run_source_pass(hpsg_ctx* c, const double* d_f, int K) {
     ck(cudaGetLastError(), "source gather");
     BatchedMat D{L.MD.d(), L.n_int, L.strideMD()};
     BatchedMat Y{c->srcY[d]->d(), L.n_int, (long long)L.n_int * K};
-    ck(hpsk::bgetrs(int(L.nodes), L.n_int, K, D, L.piv.i(), Y, c->st), "merge source getrs");
+    ck(hpsk::bgetrs(int(L.nodes), L.n_int, K, D, L.piv.i(), Y, c->luws, c->st), "merge source getrs");
     c->launches += lu_launches(L.n_int, K, false);
     if (!root) {
       // B = the children's T blocks coupling exterior rows to interface columns (scratch, as in the build)
@@ -1216,6 +1234,8 @@ int hpsg_create_part(const hpsg_tree* tree, const hpsg_part* part, const hpsg_te
       c->has_source_im = 1;
     }
     c->opts.source_imag = nullptr;  // the caller's descriptor is not kept
+    c->luws.total = &c->dev_bytes;
+    c->luws.lookahead = !c->opts.no_lu_lookahead;
     alloc_build(c.get());
     c->cut_set.assign(c->T.cut ? size_t(c->T.n_leaves()) : 0, 0);
     ck(cudaStreamSynchronize(c->st), "create sync");
@@ -1281,7 +1301,7 @@ int hpsg_build(hpsg_ctx* c) {
                          -1.0, c->st);
       ck(hpsk::lu_stats_init(c->radStats.d(), 1, c->st), "stats init");
       ck(hpsk::bgetrf_aug(1, n, 1, BatchedMat{c->radM.d(), n, (long long)n * (n + 1)}, c->radPiv.i(),
-                          c->radStats.d(), c->st),
+                          c->radStats.d(), c->luws, c->st),
          "root T bgetrf");
       c->launches += 3 + lu_launches(n, 1, true);
     }
@@ -1534,9 +1554,10 @@ int hpsg_error_report(hpsg_ctx* c, const double* d_u, int is_complex, const hpsg
     a.leaf_box = c->leaf_box.d();
     a.cheb = c->cheb.d();
     a.u = d_u;
-    a.ex_re = make_dev_field(c, *exact, true);
+    std::vector<std::unique_ptr<DevBuf>> scratch;  // released when the call returns
+    a.ex_re = make_dev_field(c, *exact, true, &scratch);
     a.has_im = exact_imag ? 1 : 0;
-    if (exact_imag) a.ex_im = make_dev_field(c, *exact_imag, true);
+    if (exact_imag) a.ex_im = make_dev_field(c, *exact_imag, true, &scratch);
     DevBuf part;
     part.alloc(size_t(148 * 4) * 4 * 8, nullptr);
     a.partial = part.d();
@@ -1671,6 +1692,8 @@ int hpsg_part_retarget(hpsg_ctx* c, long long root_index) {
     c->T = hpsg::make_part_tree(t.dim, t.p, t.L, t.lo, t.hi, c->T.root_depth, root_index, c->part.cut_depth);
     c->part.root_index = root_index;
     if (!c->T.cut) upload(c->leaf_box, c->T.leaf_lo, &c->dev_bytes, c->st);
+    // a cut part's child [h|T] inputs belonged to the previous target: all must be set again
+    std::fill(c->cut_set.begin(), c->cut_set.end(), 0);
     ck(cudaStreamSynchronize(c->st), "retarget sync");
     c->built = false;
   });
@@ -1756,6 +1779,7 @@ void hpsg_destroy(hpsg_ctx* c) {
     for (auto& e : tmp->lev_ev)
       if (e) cudaEventDestroy(e);
     cudaStream_t st = tmp->own_stream ? tmp->st : nullptr;
+    hpsk::lu_workspace_free(tmp->luws);
     delete tmp;  // frees device buffers
     if (st) cudaStreamDestroy(st);
   }
@@ -1794,16 +1818,20 @@ extern "C" int hpsg_dev_gemm_timing(int mode, double* ms, double* flops, long lo
 
 extern "C" int hpsg_dev_getrf_aug(int batch, int n, int m, double* M, long long ld, long long stride, int* ipiv,
                                   double* stats) {
+  hpsk::LuWorkspace ws;  // scratch of this call only
   cudaError_t e = hpsk::lu_stats_init(stats, batch, 0);
-  if (e == cudaSuccess) e = hpsk::bgetrf_aug(batch, n, m, BatchedMat{M, ld, stride}, ipiv, stats, 0);
+  if (e == cudaSuccess) e = hpsk::bgetrf_aug(batch, n, m, BatchedMat{M, ld, stride}, ipiv, stats, ws, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  hpsk::lu_workspace_free(ws);
   return e == cudaSuccess ? HPSG_OK : HPSG_ERR_CUDA;
 }
 
 extern "C" int hpsg_dev_getrs(int batch, int n, int m, const double* LU, long long ld, long long stride,
                               const int* ipiv, double* R, long long ldr, long long strideR) {
+  hpsk::LuWorkspace ws;  // scratch of this call only
   cudaError_t e = hpsk::bgetrs(batch, n, m, BatchedMat{const_cast<double*>(LU), ld, stride}, ipiv,
-                               BatchedMat{R, ldr, strideR}, 0);
+                               BatchedMat{R, ldr, strideR}, ws, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  hpsk::lu_workspace_free(ws);
   return e == cudaSuccess ? HPSG_OK : HPSG_ERR_CUDA;
 }

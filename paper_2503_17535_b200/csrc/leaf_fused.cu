@@ -773,11 +773,12 @@ int leaf_fused_ctas_per_sm() {
 
 cudaError_t launch_leaf_fused(const LeafFusedArgs& f, int grid, cudaStream_t st) {
   const size_t smem = sizeof(FusedSmem);
-  static bool set = false;
-  if (!set) {
+  static PerDeviceFlag attr;
+  const int dv = current_device();
+  if (!(attr.set >> dv & 1)) {
     cudaError_t e = cudaFuncSetAttribute(leaf_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    set = true;
+    attr.set |= 1ull << dv;
   }
   leaf_fused_kernel<<<grid, kFT, smem, st>>>(f);
   return cudaGetLastError();

@@ -379,8 +379,7 @@ __global__ void stats_init_kernel(double* s, int batch) {
 }
 
 int cluster_for(int n) {
-  static const int rows_per_cta = getenv("HPS_PANEL_ROWS") ? atoi(getenv("HPS_PANEL_ROWS")) : kRowsPerCta;  // tuning knob
-  int cs = (n + rows_per_cta - 1) / rows_per_cta;
+  int cs = (n + kRowsPerCta - 1) / kRowsPerCta;
   return std::max(1, cs);
 }
 
@@ -393,14 +392,15 @@ cudaError_t launch_panel(int batch, int n, int j0, int nb, BatchedMat M, int* ip
   if (cs == 1) rpc = rows;
   PanelArgs pa{M.p, M.ld, M.stride, n, j0, nb, rpc, cs, ipiv, stats};
   const size_t smem = (size_t)rpc * nb * 8 + 6 * kLuNB * 8 + (kPanelThreads / 32) * 12 + 128;
-  static size_t smem_set = 0;
-  if (smem > smem_set) {
+  static PerDeviceFlag smem_set;
+  const int dv = current_device();
+  if (smem > smem_set.value[dv]) {
     cudaError_t e = cudaFuncSetAttribute(panel_getrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 48 * 1024));
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(panel_getrf_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
-    smem_set = std::max<size_t>(smem, 48 * 1024);
+    smem_set.value[dv] = std::max<size_t>(smem, 48 * 1024);
   }
   if (cs == 1) {
     // single-CTA panels: one thread per row up to kPanelThreads (the 56- and 112-row panels of the
@@ -455,11 +455,7 @@ constexpr int kOuterNB = 256;
 
 // GEPP panel width: 32 columns, or 16 when the panel of a matrix beyond 16 CTAs x 864 rows would
 // not fit the cluster's shared memory (2D L=9 / 3D L=4 roots, n up to 27,648)
-int panel_width(int n) {
-  static const int forced = getenv("HPS_PANEL_WIDTH") ? atoi(getenv("HPS_PANEL_WIDTH")) : 0;  // tuning knob
-  if (forced == kLuNB / 2 || (forced == kLuNB && n <= kMaxCluster * kMaxRowsPerCta)) return forced;
-  return n > kMaxCluster * kMaxRowsPerCta ? kLuNB / 2 : kLuNB;
-}
+int panel_width(int n) { return n > kMaxCluster * kMaxRowsPerCta ? kLuNB / 2 : kLuNB; }
 
 // C[rows, cols] += alpha * A[rows, k] * B[k, cols] on sub-blocks of strided batches.
 cudaError_t gemm_sub(int batch, int rows, int cols, int k, double alpha, const double* A, long long lda, long long sA,
@@ -492,7 +488,6 @@ cudaError_t gemm_sub(int batch, int rows, int cols, int k, double alpha, const d
   do {                                                                                  \
     cudaError_t e_ = (x);                                                               \
     if (e_ != cudaSuccess) {                                                            \
-      if (getenv("HPS_DEBUG")) fprintf(stderr, "lu.cu:%d %s -> %s\n", __LINE__, #x, cudaGetErrorString(e_)); \
       return e_;                                                                        \
     }                                                                                   \
   } while (0)
@@ -503,11 +498,8 @@ cudaError_t gemm_sub(int batch, int rows, int cols, int k, double alpha, const d
 // slab's 32x32 diagonal blocks are formed first (one warp per block), then every CTA keeps a
 // 32-column strip of X in shared memory and runs the blocked substitution with DMMA:
 // X_b = T_bb^-1 X_b, then X_i -= T_ib X_b for the remaining blocks i of the slab.
-constexpr int kSlabMinNDefault = 64;  // measured: 64 beats 128 and 512 (d4-d6 merges) and 48 (d7)
-int slab_min_n() {
-  static const int v = getenv("HPS_SLAB_MIN_N") ? atoi(getenv("HPS_SLAB_MIN_N")) : kSlabMinNDefault;  // tuning knob
-  return v;
-}
+constexpr int kSlabMinN = 64;  // measured: 64 beats 128 and 512 (d4-d6 merges) and 48 (d7)
+int slab_min_n() { return kSlabMinN; }
 constexpr int kSlabCW = 32;                 // strip width (4 warps x 8 columns)
 constexpr int kSlabLdX = kOuterNB + 4;      // 260 = 4 mod 16: conflict-free B fragments
 constexpr int kSlabChunk = 64;              // rows of T staged per update step
@@ -669,38 +661,48 @@ __global__ void __launch_bounds__(128) slab_trsm_kernel(const SlabArgs a) {
   }
 }
 
-double* slab_workspace(int batch) {
-  static double* w = nullptr;
-  static long long cap = 0;
-  const long long need = (long long)batch * (kOuterNB / kLuNB) * kLuNB * kLuNB;
-  if (need > cap) {
-    if (w) cudaFree(w);
-    w = nullptr;
-    if (cudaMalloc(&w, need * sizeof(double)) != cudaSuccess) return nullptr;
-    cap = need;
+long long slab_winv_elems(int batch) { return (long long)batch * (kOuterNB / kLuNB) * kLuNB * kLuNB; }
+
+// grow a workspace array (contents are scratch); the bytes go to *total.  dry: count only (footprint
+// estimation, hpsg_estimate_bytes), nothing is allocated.
+template <class T>
+cudaError_t ws_grow(T*& p, long long& cap, long long need, size_t* total, bool dry = false) {
+  if (need <= cap) return cudaSuccess;
+  if (!dry) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cudaError_t e = cudaMalloc(&p, (size_t)need * sizeof(T));
+    if (e != cudaSuccess) {
+      if (total) *total -= (size_t)cap * sizeof(T);
+      cap = 0;
+      return e;
+    }
   }
-  return w;
+  if (total) *total += (size_t)(need - cap) * sizeof(T);
+  cap = need;
+  return cudaSuccess;
 }
 
 // X[r0:r0+nbk, 0:ncols] <- T_slab^-1 X[...] (unit-lower or upper slab of T), two launches
 template <bool UPPER>
 cudaError_t slab_trsm(int batch, const double* T, long long ldT, long long sT, int r0, int nbk, double* X,
-                      long long ldX, long long sX, int ncols, cudaStream_t st) {
+                      long long ldX, long long sX, int ncols, LuWorkspace& ws, cudaStream_t st) {
   if (ncols <= 0 || nbk <= 0) return cudaSuccess;
-  double* w = slab_workspace(batch);
-  if (!w) return cudaErrorMemoryAllocation;
+  HPS_TRY(ws_grow(ws.winv, ws.winv_cap, slab_winv_elems(batch), ws.total));
+  double* w = ws.winv;
   const int nblk = (nbk + kLuNB - 1) / kLuNB;
   diag_inv_kernel<UPPER><<<dim3(batch, nblk), 32, 0, st>>>(T, ldT, sT, r0, nbk, w);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const size_t smem = (size_t)(kSlabCW * kSlabLdX + 2 * kLuNB * kSlabLdA) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceFlag attr;
+  const int dv = current_device();
+  if (!(attr.set >> dv & 1)) {
     e = cudaFuncSetAttribute(slab_trsm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(slab_trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr.set |= 1ull << dv;
   }
   SlabArgs a{T, ldT, sT, r0, nbk, X, ldX, sX, ncols, w};
   const long long strips = (ncols + kSlabCW - 1) / kSlabCW;
@@ -712,22 +714,22 @@ cudaError_t slab_trsm(int batch, const double* T, long long ldT, long long sT, i
 // Blocked back substitution R <- U^-1 R, U = upper triangle of LU (n x n).
 }  // namespace
 template <bool UPPER>
-cudaError_t trsv_blocked(const double* T, long long ldT, int n, double* X, long long ldX, int m, cudaStream_t st);
+cudaError_t trsv_blocked(const double* T, long long ldT, int n, double* X, long long ldX, int m, LuWorkspace& ws,
+                         cudaStream_t st);
 namespace {
 
 cudaError_t back_subst(int batch, int n, int m, const double* U, long long ldU, long long strideU, double* R,
-                       long long ldR, long long strideR, cudaStream_t st) {
+                       long long ldR, long long strideR, LuWorkspace& ws, cudaStream_t st) {
   if (m <= 0) return cudaSuccess;
   // one large matrix with a few RHS (the implicit root's [D | h] factorization): the slab TRSV
   // (one CTA per 256-row slab + a streaming GEMV) instead of a chain of 32x32 TRSM + GEMM launches
-  if (batch == 1 && m <= kTrsvMaxRhs && n >= 2 * kOuterNB && !getenv("HPS_NO_BLOCK_TRSV"))
-    return trsv_blocked<true>(U, ldU, n, R, ldR, m, st);
+  if (batch == 1 && m <= kTrsvMaxRhs && n >= 2 * kOuterNB) return trsv_blocked<true>(U, ldU, n, R, ldR, m, ws, st);
   const int nouter = (n + kOuterNB - 1) / kOuterNB;
   for (int ob = nouter - 1; ob >= 0; --ob) {
     const int r0 = ob * kOuterNB, r1 = std::min(n, r0 + kOuterNB);
     const int nsub = (r1 - r0 + kLuNB - 1) / kLuNB;
-    if (n >= slab_min_n() && m >= kSlabCW && !getenv("HPS_NO_SLAB_TRSM")) {
-      HPS_TRY(slab_trsm<true>(batch, U, ldU, strideU, r0, r1 - r0, R, ldR, strideR, m, st));
+    if (n >= slab_min_n() && m >= kSlabCW) {
+      HPS_TRY(slab_trsm<true>(batch, U, ldU, strideU, r0, r1 - r0, R, ldR, strideR, m, ws, st));
       HPS_TRY(gemm_sub(batch, r0, m, r1 - r0, -1.0, U + (long long)r0 * ldU, ldU, strideU, R + r0, ldR, strideR, R,
                        ldR, strideR, st));
       continue;
@@ -811,36 +813,26 @@ __global__ void apply_perm_kernel(double* M, long long ld, long long stride, con
   }
 }
 
-struct LookAhead {
-  cudaStream_t ps = nullptr;
-  std::vector<cudaEvent_t> ev;
-  int* moved = nullptr;
-  int* nmoved = nullptr;
-  long long cap = 0;
-};
-LookAhead& lookahead() {
-  static LookAhead la;
-  return la;
-}
-cudaError_t lookahead_prepare(int batch, int nev) {
-  LookAhead& la = lookahead();
-  if (!la.ps) {
+cudaError_t lookahead_prepare(LuWorkspace& ws, int batch, int nev) {
+  if (!ws.side) {
     // the panel stream outranks the trailing GEMMs so its few CTAs are scheduled as SMs free up
     int lo = 0, hi = 0;
     HPS_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    HPS_TRY(cudaStreamCreateWithPriority(&la.ps, cudaStreamNonBlocking, hi));
+    HPS_TRY(cudaStreamCreateWithPriority(&ws.side, cudaStreamNonBlocking, hi));
   }
-  while ((int)la.ev.size() < nev) {
-    cudaEvent_t e;
-    HPS_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    la.ev.push_back(e);
+  if (ws.n_ev < nev) {
+    cudaEvent_t* ev = new cudaEvent_t[nev];
+    for (int i = 0; i < ws.n_ev; ++i) ev[i] = ws.ev[i];
+    for (int i = ws.n_ev; i < nev; ++i) HPS_TRY(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    delete[] ws.ev;
+    ws.ev = ev;
+    ws.n_ev = nev;
   }
-  if (batch > la.cap) {
-    if (la.moved) cudaFree(la.moved);
-    if (la.nmoved) cudaFree(la.nmoved);
-    HPS_TRY(cudaMalloc(&la.moved, sizeof(int) * (size_t)batch * 4 * kOuterNB));
-    HPS_TRY(cudaMalloc(&la.nmoved, sizeof(int) * (size_t)batch));
-    la.cap = batch;
+  if (batch > ws.la_cap) {
+    long long c1 = ws.la_cap * 4 * kOuterNB, c2 = ws.la_cap;
+    HPS_TRY(ws_grow(ws.moved, c1, (long long)batch * 4 * kOuterNB, ws.total));
+    HPS_TRY(ws_grow(ws.nmoved, c2, (long long)batch, ws.total));
+    ws.la_cap = batch;
   }
   return cudaSuccess;
 }
@@ -865,23 +857,28 @@ cudaError_t factor_outer_panel(int batch, int n, int J, int Jend, BatchedMat M, 
   return cudaSuccess;
 }
 
-cudaError_t bgetrf_aug_lookahead(int batch, int n, int m, BatchedMat M, int* ipiv, double* stats, cudaStream_t st,
-                                 bool keep_L) {
+cudaError_t bgetrf_aug_lookahead(int batch, int n, int m, BatchedMat M, int* ipiv, double* stats, LuWorkspace& ws,
+                                 cudaStream_t st, bool keep_L) {
   const int K = (n + kOuterNB - 1) / kOuterNB;
-  HPS_TRY(lookahead_prepare(batch, 2 * K + 2));
-  LookAhead& la = lookahead();
-  cudaEvent_t* evP = la.ev.data();      // panel k done (side stream)
-  cudaEvent_t* evA = la.ev.data() + K;  // next panel's columns updated (main stream)
-  cudaEvent_t evF = la.ev[2 * K];
+  HPS_TRY(lookahead_prepare(ws, batch, 2 * K + 2));
+  struct {
+    cudaStream_t ps;
+    int* moved;
+    int* nmoved;
+  } la{ws.side, ws.moved, ws.nmoved};
+  cudaEvent_t* evP = ws.ev;      // panel k done (side stream)
+  cudaEvent_t* evA = ws.ev + K;  // next panel's columns updated (main stream)
+  cudaEvent_t evF = ws.ev[2 * K];
   const long long ld = M.ld, sM = M.stride;
   double* A = M.p;
   auto at = [&](int r, int c) { return A + (long long)c * ld + r; };
   const int ncol = n + m;
-  static size_t perm_smem_set = 0;
+  static PerDeviceFlag perm_smem_set;
+  const int dv = current_device();
   const size_t perm_smem = (size_t)n * sizeof(int);
-  if (perm_smem > 48 * 1024 && perm_smem > perm_smem_set) {
+  if (perm_smem > 48 * 1024 && perm_smem > perm_smem_set.value[dv]) {
     HPS_TRY(cudaFuncSetAttribute(block_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)perm_smem));
-    perm_smem_set = perm_smem;
+    perm_smem_set.value[dv] = perm_smem;
   }
   HPS_TRY(cudaEventRecord(evF, st));
   HPS_TRY(cudaStreamWaitEvent(la.ps, evF, 0));
@@ -901,8 +898,8 @@ cudaError_t bgetrf_aug_lookahead(int batch, int n, int m, BatchedMat M, int* ipi
       HPS_TRY(cudaGetLastError());
     }
     // U12 = L11^-1 A12 over the block's row slab
-    if (n >= slab_min_n() && Jend < ncol && !getenv("HPS_NO_SLAB_TRSM")) {
-      HPS_TRY(slab_trsm<false>(batch, A, ld, sM, J, Jend - J, at(0, Jend), ld, sM, ncol - Jend, st));
+    if (n >= slab_min_n() && Jend < ncol) {
+      HPS_TRY(slab_trsm<false>(batch, A, ld, sM, J, Jend - J, at(0, Jend), ld, sM, ncol - Jend, ws, st));
     } else
     for (int j0 = J; j0 < Jend && Jend < ncol; j0 += kLuNB) {
       const int nb = std::min(kLuNB, Jend - j0);
@@ -925,7 +922,7 @@ cudaError_t bgetrf_aug_lookahead(int batch, int n, int m, BatchedMat M, int* ipi
                        at(Jend, J2end), ld, sM, st));
     }
   }
-  return back_subst(batch, n, m, A, ld, sM, at(0, n), ld, sM, st);
+  return back_subst(batch, n, m, A, ld, sM, at(0, n), ld, sM, ws, st);
 }
 
 }  // namespace
@@ -938,16 +935,15 @@ cudaError_t lu_stats_init(double* stats, int batch, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double* stats, cudaStream_t st,
-                       bool keep_L) {
+// look-ahead (panels of the next outer block on a high-priority side stream) from this n up; measured at
+// L=8: d0 -1.7 ms, d1 -3 ms, d2 -1 ms (256 and 512 measured equal as the threshold)
+constexpr int kLookaheadMinN = 2 * kOuterNB;
+
+cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double* stats, LuWorkspace& ws,
+                       cudaStream_t st, bool keep_L) {
   if (batch <= 0 || n <= 0) return cudaSuccess;
   if (n > bgetrf_max_n()) return cudaErrorInvalidValue;
-  // look-ahead (panels of the next outer block on a high-priority side stream) measured at L=8:
-  // d0 -1.7 ms, d1 -3 ms, d2 -1 ms; HPS_LU_LOOKAHEAD=0 turns it off
-  const int la_env = getenv("HPS_LU_LOOKAHEAD") ? atoi(getenv("HPS_LU_LOOKAHEAD")) : 1;
-  static const int la_min = getenv("HPS_LU_LOOKAHEAD_MIN_N") ? atoi(getenv("HPS_LU_LOOKAHEAD_MIN_N")) : 2 * kOuterNB;
-  const bool la = la_env > 0 && n > la_min && n > kOuterNB;  // tuning knob: smallest n for the look-ahead
-  if (la) return bgetrf_aug_lookahead(batch, n, m, M, ipiv, stats, st, keep_L);
+  if (ws.lookahead && n > kLookaheadMinN) return bgetrf_aug_lookahead(batch, n, m, M, ipiv, stats, ws, st, keep_L);
   const long long ld = M.ld, sM = M.stride;
   double* A = M.p;
   auto at = [&](int r, int c) { return A + (long long)c * ld + r; };
@@ -969,8 +965,8 @@ cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double*
                        at(j0 + nb, j0 + nb), ld, sM, st));
     }
     // (2) U12 = L11^-1 A12 over the outer block's row slab (blocked forward substitution)
-    if (n >= slab_min_n() && Jend < ncol && !getenv("HPS_NO_SLAB_TRSM")) {
-      HPS_TRY(slab_trsm<false>(batch, A, ld, sM, J, Jend - J, at(0, Jend), ld, sM, ncol - Jend, st));
+    if (n >= slab_min_n() && Jend < ncol) {
+      HPS_TRY(slab_trsm<false>(batch, A, ld, sM, J, Jend - J, at(0, Jend), ld, sM, ncol - Jend, ws, st));
     } else
     for (int j0 = J; j0 < Jend && Jend < ncol; j0 += kLuNB) {
       const int nb = std::min(kLuNB, Jend - j0);
@@ -983,7 +979,7 @@ cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double*
     HPS_TRY(gemm_sub(batch, n - Jend, ncol - Jend, Jend - J, -1.0, at(Jend, J), ld, sM, at(J, Jend), ld, sM,
                      at(Jend, Jend), ld, sM, st));
   }
-  return back_subst(batch, n, m, A, ld, sM, at(0, n), ld, sM, st);
+  return back_subst(batch, n, m, A, ld, sM, at(0, n), ld, sM, ws, st);
 }
 
 // ---- single-matrix, few-RHS triangular solves (the implicit-root solve: n = 7168, 1 RHS) --------
@@ -1061,20 +1057,24 @@ __global__ void __launch_bounds__(256) slab_trsv_kernel(const double* T, long lo
 }
 
 // X <- T^-1 X for one matrix (unit-lower L or upper U of an LU), m <= kTrsvMaxRhs
+constexpr long long kTrsvScratch = 1LL << 20;  // doubles of split-k partial sums (8 MB)
+
 template <bool UPPER>
-cudaError_t trsv_blocked(const double* T, long long ldT, int n, double* X, long long ldX, int m, cudaStream_t st) {
-  static double* scratch = nullptr;
-  const size_t scratch_elems = size_t(1) << 20;
-  if (!scratch) HPS_TRY(cudaMalloc(&scratch, scratch_elems * sizeof(double)));
+cudaError_t trsv_blocked(const double* T, long long ldT, int n, double* X, long long ldX, int m, LuWorkspace& ws,
+                         cudaStream_t st) {
+  HPS_TRY(ws_grow(ws.trsv, ws.trsv_cap, kTrsvScratch, ws.total));
+  double* scratch = ws.trsv;
+  const size_t scratch_elems = (size_t)kTrsvScratch;
   const int nouter = (n + kOuterNB - 1) / kOuterNB;
   for (int s = 0; s < nouter; ++s) {
     const int ob = UPPER ? nouter - 1 - s : s;
     const int J = ob * kOuterNB, Jend = std::min(n, J + kOuterNB);
     const size_t smem = (size_t)kLuNB * kOuterNB * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceFlag attr;
+    const int dv = current_device();
+    if (!(attr.set >> dv & 1)) {
       HPS_TRY(cudaFuncSetAttribute(slab_trsv_kernel<UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
+      attr.set |= 1ull << dv;
     }
     slab_trsv_kernel<UPPER><<<1, 256, smem, st>>>(T, ldT, J, Jend - J, X, ldX, m);
     HPS_TRY(cudaGetLastError());
@@ -1095,32 +1095,28 @@ cudaError_t trsv_blocked(const double* T, long long ldT, int n, double* X, long 
   return cudaSuccess;
 }
 
-cudaError_t bgetrs(int batch, int n, int m, BatchedMat LU, const int* ipiv, BatchedMat R, cudaStream_t st) {
+cudaError_t bgetrs(int batch, int n, int m, BatchedMat LU, const int* ipiv, BatchedMat R, LuWorkspace& ws,
+                   cudaStream_t st) {
   if (batch <= 0 || n <= 0 || m <= 0) return cudaSuccess;
+  const int dv = current_device();
   if ((size_t)n * 12 <= 200 * 1024) {
     const int cpc = 8;
     const size_t smem = (size_t)n * 12;
-    static size_t smem_set = 0;
-    if (smem > smem_set && smem > 48 * 1024) {
+    static PerDeviceFlag smem_set;
+    if (smem > smem_set.value[dv] && smem > 48 * 1024) {
       HPS_TRY(cudaFuncSetAttribute(laswp_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      smem_set = smem;
+      smem_set.value[dv] = smem;
     }
     laswp_perm_kernel<<<dim3(batch, (m + cpc - 1) / cpc), 256, smem, st>>>(ipiv, n, R.p, R.ld, R.stride, m, cpc);
     HPS_TRY(cudaGetLastError());
   } else {
-    static int* perm = nullptr;
-    static size_t perm_cap = 0;
-    const size_t need = (size_t)batch * n;
-    if (need > perm_cap) {
-      if (perm) cudaFree(perm);
-      HPS_TRY(cudaMalloc(&perm, need * sizeof(int)));
-      perm_cap = need;
-    }
-    static bool attr = false;
-    if (!attr) {
+    HPS_TRY(ws_grow(ws.perm, ws.perm_cap, (long long)batch * n, ws.total));
+    int* perm = ws.perm;
+    static PerDeviceFlag attr;
+    if (!(attr.set >> dv & 1)) {
       HPS_TRY(cudaFuncSetAttribute(build_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       HPS_TRY(cudaFuncSetAttribute(apply_perm_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      attr = true;
+      attr.set |= 1ull << dv;
     }
     if ((size_t)n * 8 > 227 * 1024) return cudaErrorInvalidValue;
     build_perm_kernel<<<batch, 256, (size_t)n * sizeof(int), st>>>(ipiv, n, perm);
@@ -1129,14 +1125,14 @@ cudaError_t bgetrs(int batch, int n, int m, BatchedMat LU, const int* ipiv, Batc
     HPS_TRY(cudaGetLastError());
   }
   const double* L = LU.p;
-  if (batch == 1 && m <= kTrsvMaxRhs && n >= 1024 && !getenv("HPS_NO_BLOCK_TRSV")) {
-    HPS_TRY(trsv_blocked<false>(L, LU.ld, n, R.p, R.ld, m, st));
-    return trsv_blocked<true>(L, LU.ld, n, R.p, R.ld, m, st);
+  if (batch == 1 && m <= kTrsvMaxRhs && n >= 1024) {
+    HPS_TRY(trsv_blocked<false>(L, LU.ld, n, R.p, R.ld, m, ws, st));
+    return trsv_blocked<true>(L, LU.ld, n, R.p, R.ld, m, ws, st);
   }
   for (int J = 0; J < n; J += kOuterNB) {
     const int Jend = std::min(n, J + kOuterNB);
-    if (n >= slab_min_n() && m >= kSlabCW && !getenv("HPS_NO_SLAB_TRSM")) {
-      HPS_TRY(slab_trsm<false>(batch, L, LU.ld, LU.stride, J, Jend - J, R.p, R.ld, R.stride, m, st));
+    if (n >= slab_min_n() && m >= kSlabCW) {
+      HPS_TRY(slab_trsm<false>(batch, L, LU.ld, LU.stride, J, Jend - J, R.p, R.ld, R.stride, m, ws, st));
     } else
     for (int j0 = J; j0 < Jend; j0 += kLuNB) {
       const int nb = std::min(kLuNB, Jend - j0);
@@ -1148,7 +1144,53 @@ cudaError_t bgetrs(int batch, int n, int m, BatchedMat LU, const int* ipiv, Batc
     HPS_TRY(gemm_sub(batch, n - Jend, m, Jend - J, -1.0, L + (long long)J * LU.ld + Jend, LU.ld, LU.stride, R.p + J,
                      R.ld, R.stride, R.p + Jend, R.ld, R.stride, st));
   }
-  return back_subst(batch, n, m, LU.p, LU.ld, LU.stride, R.p, R.ld, R.stride, st);
+  return back_subst(batch, n, m, LU.p, LU.ld, LU.stride, R.p, R.ld, R.stride, ws, st);
+}
+
+size_t lu_workspace_need(int batch, int n, int m, bool factor, bool lookahead) {
+  LuWorkspace ws;
+  ws.lookahead = lookahead;
+  size_t total = 0;
+  ws.total = &total;
+  lu_workspace_reserve(ws, batch, n, m, factor, /*dry=*/true);
+  return total;
+}
+
+cudaError_t lu_workspace_reserve(LuWorkspace& ws, int batch, int n, int m, bool factor, bool dry) {
+  if (batch <= 0 || n <= 0) return cudaSuccess;
+  if (n >= kSlabMinN && (m >= kSlabCW || factor))
+    HPS_TRY(ws_grow(ws.winv, ws.winv_cap, slab_winv_elems(batch), ws.total, dry));
+  if (factor && ws.lookahead && n > kLookaheadMinN && batch > ws.la_cap) {
+    long long c1 = ws.la_cap * 4 * kOuterNB, c2 = ws.la_cap;
+    HPS_TRY(ws_grow(ws.moved, c1, (long long)batch * 4 * kOuterNB, ws.total, dry));
+    HPS_TRY(ws_grow(ws.nmoved, c2, (long long)batch, ws.total, dry));
+    ws.la_cap = batch;
+  }
+  if (!factor && (size_t)n * 12 > 200 * 1024)
+    HPS_TRY(ws_grow(ws.perm, ws.perm_cap, (long long)batch * n, ws.total, dry));
+  if (batch == 1 && m <= kTrsvMaxRhs && n >= 2 * kOuterNB)
+    HPS_TRY(ws_grow(ws.trsv, ws.trsv_cap, kTrsvScratch, ws.total, dry));
+  return cudaSuccess;
+}
+
+void lu_workspace_free(LuWorkspace& ws) {
+  auto fr = [&](void* p, long long cap, size_t el) {
+    if (p) cudaFree(p);
+    if (ws.total) *ws.total -= (size_t)cap * el;
+  };
+  fr(ws.winv, ws.winv_cap, 8);
+  fr(ws.moved, ws.la_cap * 4 * kOuterNB, 4);
+  fr(ws.nmoved, ws.la_cap, 4);
+  fr(ws.perm, ws.perm_cap, 4);
+  fr(ws.trsv, ws.trsv_cap, 8);
+  for (int i = 0; i < ws.n_ev; ++i) cudaEventDestroy(ws.ev[i]);
+  delete[] ws.ev;
+  if (ws.side) cudaStreamDestroy(ws.side);
+  size_t* total = ws.total;
+  const bool la = ws.lookahead;
+  ws = LuWorkspace{};
+  ws.total = total;
+  ws.lookahead = la;
 }
 
 int lu_launch_count(int n, int m, bool factor) {

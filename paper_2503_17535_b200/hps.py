@@ -56,7 +56,7 @@ class _Part(C.Structure):
 class _Options(C.Structure):
     _fields_ = [("literal_sign", C.c_int), ("root_implicit_S", C.c_int), ("device", C.c_int), ("keep_factors", C.c_int),
                 ("variant", C.c_int), ("eta", C.c_double), ("build_root_T", C.c_int),
-                ("source_imag", C.POINTER(_Field))]
+                ("source_imag", C.POINTER(_Field)), ("force_batched_leaf", C.c_int), ("no_lu_lookahead", C.c_int)]
 
 
 class _Stats(C.Structure):
@@ -269,7 +269,8 @@ class HpsSolver:
 
     def __init__(self, tree: UniformTree, terms, source: Field | None = None, literal_sign=True,
                  root_implicit_S=False, device=0, part=None, keep_factors=False, variant="dtn", eta=1.0,
-                 build_root_T=False, source_imag: Field | None = None):
+                 build_root_T=False, source_imag: Field | None = None, force_batched_leaf=False,
+                 lu_lookahead=True):
         L = lib()
         self.tree = tree
         keep = []
@@ -287,6 +288,8 @@ class HpsSolver:
         if source_imag is not None:
             self._src_im = source_imag.to_c(keep)
             op.source_imag = C.pointer(self._src_im)
+        op.force_batched_leaf = int(force_batched_leaf)
+        op.no_lu_lookahead = int(not lu_lookahead)
         self.part = tuple(part) if part is not None else (0, 0, tree.L)
         pt = _Part(*self.part)
         h = C.c_void_p()

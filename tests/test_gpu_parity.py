@@ -154,13 +154,14 @@ def test_errors():
 
 
 @pytest.mark.parametrize("name,p,L", [("poisson2d", 16, 3), ("helmholtz_bumps", 16, 2), ("laplace3d", 6, 1)])
-def test_fused_leaf_path_equals_batched(name, p, L, monkeypatch):
-    """The persistent fused leaf kernel and the multi-launch batched leaf path agree."""
+def test_fused_leaf_path_equals_batched(name, p, L):
+    """The persistent fused leaf kernel and the multi-launch batched leaf path
+    (hpsg_options.force_batched_leaf) agree."""
     prob = PR.CATALOG[name]()
-    monkeypatch.setenv("HPS_LEAF_PATH", "fused")
     a = gpu_solver(prob, p, L)
-    monkeypatch.setenv("HPS_LEAF_PATH", "batched")
-    b = gpu_solver(prob, p, L)
+    tree = H.build_uniform_tree(prob.lo, prob.hi, L, prob.dim, p)
+    b = H.HpsSolver(tree, prob.terms, prob.source, literal_sign=True, force_batched_leaf=True)
+    b.build()
     g = prob.boundary(a.root_boundary_points())
     assert rel(a.solve(g), b.solve(g)) < 1e-11
     for o in (0, a.tree.n_leaves - 1):
@@ -217,13 +218,14 @@ def test_3d_variable_poisson_parity(p, L, literal):
         assert PR.rel_linf(s.solve(g), prob.exact(s.leaf_points())) < (1e-5 if L == 2 else 1e-6)
 
 
-def test_lookahead_lu_matches_plain(monkeypatch):
+def test_lookahead_lu_matches_plain():
     """The look-ahead LU driver (default for n > 512: side-stream panels, deferred block swaps)
-    and the plain blocked driver give the same merges."""
+    and the plain blocked driver (hpsg_options.no_lu_lookahead) give the same merges."""
     prob = PR.helmholtz_bumps()
     a = gpu_solver(prob, 16, 5, root_implicit=True)       # root D = 1792 > 512: both drivers apply
-    monkeypatch.setenv("HPS_LU_LOOKAHEAD", "0")
-    b = gpu_solver(prob, 16, 5, root_implicit=True)
+    tree = H.build_uniform_tree(prob.lo, prob.hi, 5, 2, 16)
+    b = H.HpsSolver(tree, prob.terms, prob.source, literal_sign=True, root_implicit_S=True, lu_lookahead=False)
+    b.build()
     g = prob.boundary(a.root_boundary_points())
     assert rel(b.solve(g), a.solve(g)) < 1e-12
 
