@@ -50,7 +50,11 @@ enum {
   HPSG_FIELD_POISSON2D_SRC = 5,  /* source of make_manufactured_2d_dtn, proj/src/problems.cpp:62-66 */
   HPSG_FIELD_SAMPLED = 6,
   HPSG_FIELD_BUMPS_GRAD = 7,     /* d/dx_a of HPSG_FIELD_BUMPS: c1 * sum_j -2 c2 (x_a - z_ja) exp(-c2 |x - z_j|^2), a = c3 */
-  HPSG_FIELD_DIVGRAD_SRC = 8     /* div(eps grad u), eps = BUMPS(c0,c1,c2), u = prod_k sin(c3 x_k + c4) (3D config 4) */
+  HPSG_FIELD_DIVGRAD_SRC = 8,    /* div(eps grad u), eps = BUMPS(c0,c1,c2), u = prod_k sin(c3 x_k + c4) (3D config 4) */
+  HPSG_FIELD_WAVEFRONT_SRC = 9,  /* Laplacian of atan(c0 |x - (c1,c2,c3)|^2 - 0.7): make_wavefront_3d, problems.cpp:154-179 */
+  HPSG_FIELD_PB_EPS = 10,        /* c0 + (c1 - c0) exp(-c2 rho), rho = sum_j exp(-c3 |x - z_j|^2): PoissonBoltzmannSpec::eps
+                                    (smooth), problems.cpp:187-191 */
+  HPSG_FIELD_PB_EPS_GRAD = 11    /* d/dx_a of HPSG_FIELD_PB_EPS, a = c4 (PoissonBoltzmannSpec::grad_eps, :200-205) */
 };
 typedef struct {
   int kind;
@@ -118,6 +122,34 @@ int hpsg_create(const hpsg_tree* tree, const hpsg_term* terms, int n_terms, cons
                 const hpsg_options* opts, hpsg_ctx** out);
 /* HpsSolver::build(), solver.hpp:48 / solver.cpp:144-151: leaf stage + all merge levels */
 int hpsg_build(hpsg_ctx* ctx);
+
+/* General tree: the reference's DiscretizationTree (proj/include/hps/mesh.hpp:28-61), e.g. an adaptive,
+ * level-restricted octree from refine_adaptive (mesh.cpp:233-318).  Node 0 is the root; node i has
+ * n_children[i] = 0 (leaf) or 2^dim children in the child_offset slot order (mesh.hpp:24-25), stored in
+ * children[8*i .. 8*i+7]; lo/hi (3 per node) are the reference's boxes (children are exact halves).
+ * Merges of children with different refinement project the finer interface onto the coarser one
+ * (merge.cpp:201-211, 264-266) and undo it in the downward pass.  DtN variant; hpsg_build,
+ * hpsg_solve(_device), hpsg_root_boundary_points, hpsg_leaf_points and hpsg_get_stats apply; the
+ * uniform-tree entry points (parts, new sources, ItI, getters) return HPSG_ERR_STATE.
+ * Replaces HpsSolver(const DiscretizationTree&, ...) (solver.hpp:43-45) for arbitrary trees. */
+typedef struct {
+  int dim, p;
+  int n_nodes;
+  const int* depth;       /* n_nodes */
+  const int* n_children;  /* n_nodes */
+  const int* children;    /* n_nodes x 8 */
+  const double* lo;       /* n_nodes x 3 */
+  const double* hi;       /* n_nodes x 3 */
+} hpsg_tree_desc;
+int hpsg_create_tree(const hpsg_tree_desc* tree, const hpsg_term* terms, int n_terms, const hpsg_field* source,
+                     const hpsg_options* opts, hpsg_ctx** out);
+/* refine_adaptive(domain [lo,hi] (3 each), RefinementCriterion{tol, p, fields}, max_depth, &unresolved)
+ * (proj/src/mesh.cpp:233-318, with enforce_level_restriction :141-167): 3D, built-in fields evaluated on the
+ * host.  Writes the tree as node arrays in the reference's construction order (n_nodes x {depth, n_children,
+ * children[8], lo[3], hi[3]}); returns HPSG_ERR_INVALID with *n_nodes set when cap is too small. */
+int hpsg_refine_adaptive(int p, const double* lo, const double* hi, double tol, int max_depth,
+                         const hpsg_field* fields, int n_fields, int cap, int* n_nodes, int* depth, int* n_children,
+                         int* children, double* lo_out, double* hi_out, int* n_unresolved);
 
 /* ---- subtree-sharded builds (the staged build_leaf/merge_internal API of
  * solver.hpp:51-56 at subtree granularity).  A PART is the subtree rooted at node

@@ -318,10 +318,6 @@ UniformTree make_uniform_tree(int dim, int p, int L, double lo, double hi) {
   return make_part_tree(dim, p, L, lo, hi, 0, 0, L);
 }
 
-namespace {
-struct Iface {
-  int clo, flo, chi, fhi;
-};
 const std::vector<Iface>& ifaces(int dim) {
   // proj/src/merge.cpp:20-33
   static const std::vector<Iface> i2 = {{0, 1, 1, 3}, {1, 2, 2, 0}, {3, 1, 2, 3}, {0, 2, 3, 0}};
@@ -343,7 +339,6 @@ int ext_qpos(int dim, int c, int f) {
   const int ua = axis == 0 ? 1 : 0, va = axis == 2 ? 1 : 2;
   return off[ua] * 2 + off[va];
 }
-}  // namespace
 
 MergeTables make_merge_tables(int dim, int s) {
   MergeTables m;

@@ -73,6 +73,15 @@ UniformTree make_uniform_tree(int dim, int p, int L, double lo, double hi);
 UniformTree make_part_tree(int dim, int p, int L_full, double lo, double hi, int root_depth, long long root_index,
                            int cut_depth);
 
+// Merge interfaces (proj/src/merge.cpp:20-33): the low child's high face meets the high child's low face.
+struct Iface {
+  int clo, flo;
+  int chi, fhi;
+};
+const std::vector<Iface>& ifaces(int dim);
+// exterior position (quadrant / half of the parent face) of child c's face f, or -1 (merge.cpp:41-56)
+int ext_qpos(int dim, int c, int f);
+
 // Merge of one level (all nodes at depth d of a uniform tree share it).
 // Child boundary layout: faces in reference order, s points per face section.
 // Parent exterior: faces in order, each split into nquad child sections

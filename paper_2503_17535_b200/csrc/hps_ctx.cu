@@ -24,159 +24,17 @@
 #include <string>
 #include <vector>
 
-#include "../../include/hps_cuda.h"
-#include "gemm.cuh"
-#include "geometry.hpp"
-#include "hps_kernels.cuh"
-#include "lu.cuh"
-#include "gemv.cuh"
+#include "ctx_internal.cuh"
 
 using hpsk::BatchedMat;
 using hpsk::GemmArgs;
 
-namespace {
-
-struct CudaError {
-  cudaError_t e;
-  std::string where;
-};
-struct HpsError {
-  int code;
-  std::string msg;
-};
-
-void ck(cudaError_t e, const char* where) {
-  if (e != cudaSuccess) throw CudaError{e, where};
-}
-
-// Footprint estimation (hpsg_estimate_bytes): while set, DevBuf::alloc and the uploads only count
-// bytes -- the context is created through the normal path without touching device memory.
+namespace hpsctx {
 thread_local bool g_dry_alloc = false;
+}  // namespace hpsctx
+using namespace hpsctx;
 
-struct DevBuf {
-  void* p = nullptr;
-  size_t bytes = 0;
-  DevBuf() = default;
-  DevBuf(const DevBuf&) = delete;
-  DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr, o.bytes = 0; }
-  ~DevBuf() { release(); }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
-  }
-  void alloc(size_t b, size_t* total) {
-    if (g_dry_alloc) {
-      if (total) *total += b;
-      return;
-    }
-    if (b <= bytes && p) return;
-    if (total) *total -= bytes;
-    release();
-    if (b == 0) return;
-    cudaError_t e = cudaMalloc(&p, b);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      throw HpsError{HPSG_ERR_OOM, hpsg::fmt("cudaMalloc(%.3f GB) failed: %s", b / 1e9, cudaGetErrorString(e))};
-    }
-    bytes = b;
-    if (total) *total += b;
-  }
-  double* d() const { return static_cast<double*>(p); }
-  int* i() const { return static_cast<int*>(p); }
-};
-
-template <class T>
-void upload(DevBuf& b, const std::vector<T>& v, size_t* total, cudaStream_t st) {
-  b.alloc(v.size() * sizeof(T), total);
-  if (!v.empty() && !g_dry_alloc)
-    ck(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st), "upload");
-}
-
-struct Level {
-  int d = 0;
-  long long nodes = 0;
-  hpsg::MergeTables mt;
-  int n_int = 0, n_ext = 0, child_nb = 0;
-  DevBuf MD, piv, stats;  // [D | h_int | C] -> [LU | x_h | X]
-  DevBuf AH;              // [h | T] of the level's nodes (input of level d-1); unused at the root
-  DevBuf md_src, b_src, ah_src, down;
-  // block-sparse Schur product: exterior section e only couples to the interfaces of its own
-  // child (B_{e,i} = 0 otherwise), as contiguous interface runs {e, first interface, count}
-  std::vector<std::array<int, 3>> schur_runs;
-  hpsg::ItiMergeTables it;  // ItI variant: block copies + real-equivalent scatter table
-  DevBuf iblocks;
-  int iti_nblocks = 0;
-  long long strideMD() const { return (long long)n_int * (n_int + 1 + n_ext); }
-  long long strideAH() const { return (long long)n_ext * (1 + n_ext); }
-};
-
-}  // namespace
-
-struct hpsg_ctx {
-  std::string err;
-  int dev = 0;
-  cudaStream_t st = nullptr;
-  bool own_stream = true;
-  cudaEvent_t ev[8] = {};
-  cudaEvent_t lev_ev[25] = {};  // merge level boundaries
-  hpsg_tree tree{};
-  hpsg_part part{};  // (0, 0, L) for the whole tree
-  bool iti = false;  // ItI variant (real-equivalent complex)
-  bool root_T = false;  // ItI radiation closure: the root forms [h|T] and factors T
-  DevBuf radM, radPiv, radStats;  // [T_root | -h_root] -> [LU | g_rad]
-  hpsk::DevField source_im{};
-  int has_source_im = 0;
-  hpsg::ItiLeafOperators iops;
-  DevBuf iGr, iGi, iP, iQHs;
-  hpsg_options opts{};
-  hpsg::UniformTree T;
-  hpsg::LeafOperators ops;
-  size_t dev_bytes = 0;
-  // problem
-  int nterms = 0;
-  hpsk::DevTerm terms[hpsk::kMaxTerms]{};
-  hpsk::DevField source{};
-  int has_source = 0;
-  std::vector<std::unique_ptr<DevBuf>> field_bufs;
-  // operators
-  DevBuf leaf_box, cheb, Dm, D2m, interior, exterior, P, Qi, ZQeP;
-  // leaf stage
-  DevBuf leafM, leafE, leafPiv, leafStats, leafBad, leafHT;
-  DevBuf leafYv, leafScratch;  // fused leaf path
-  bool fused = false;
-  int fused_grid = 0;
-  double* yv = nullptr;        // [v_i | Y_i] of leaf 0 (ni x (1+nb), ld ni)
-  long long yv_stride = 0;
-  // merges
-  std::vector<Level> lv;  // index d = 0..L-1
-  DevBuf Bscratch;
-  // new-source pass (keep_factors): per-leaf RHS -> v, leaf h, per level y = D^-1 h_int and node h
-  int src_nrhs = 0;
-  DevBuf srcF, srcR, srcH;
-  std::vector<std::unique_ptr<DevBuf>> srcY, srcHn;
-  // solve workspace
-  int ws_nrhs = 0;
-  std::vector<std::unique_ptr<DevBuf>> G, GI;
-  DevBuf Ui, Ue, g_in, u_out, lg_out, gemv_scratch;
-  bool built = false;
-  std::vector<char> cut_set;  // cut part: which input [h|T] have been provided
-  hpsg_stats stats{};
-  int launches = 0;
-  hpsk::LuWorkspace luws;  // batched-LU scratch, counted in dev_bytes (lu.cuh)
-
-  long long strideLeafM() const { return (long long)ops.ni * (ops.ni + 1 + ops.nb); }
-  // [h|T] per part leaf: a real leaf (nb x (1+nb)) or, for a cut part, an input node
-  int leaf_nb() const { return T.cut ? lv[T.L - 1].child_nb : ops.nb; }
-  long long strideLeafHT() const { return (long long)leaf_nb() * (1 + leaf_nb()); }
-  // the merge at part depth d is the reference's root merge (no T/h, optional implicit S)
-  bool global_root(int d) const { return d == 0 && T.root_depth == 0; }
-  // the merge at part depth d forms the node's [h|T] (every merge but the root, unless build_root_T)
-  bool forms_T(int d) const { return !global_root(d) || root_T; }
-};
-
-namespace {
+namespace hpsctx {
 
 int fail(hpsg_ctx* c, int code, const std::string& msg) {
   if (c) c->err = msg;
@@ -233,21 +91,23 @@ void matvecs(hpsg_ctx* c, const GemmArgs& g) {
 // `scratch`: a caller-owned list for fields that live only for one call (error_report's exact solution);
 // those buffers are not counted in the context's device bytes.  Default: kept by the context.
 hpsk::DevField make_dev_field(hpsg_ctx* c, const hpsg_field& f, bool is_source,
-                              std::vector<std::unique_ptr<DevBuf>>* scratch = nullptr) {
+                              std::vector<std::unique_ptr<DevBuf>>* scratch) {
   std::vector<std::unique_ptr<DevBuf>>& keep = scratch ? *scratch : c->field_bufs;
   size_t* total = scratch ? nullptr : &c->dev_bytes;
   hpsk::DevField d{};
   d.kind = f.kind;
   d.n_centers = f.n_centers;
   for (int i = 0; i < 8; ++i) d.c[i] = f.c[i];
-  if (f.kind < HPSG_FIELD_CONST || f.kind > HPSG_FIELD_DIVGRAD_SRC)
+  if (f.kind < HPSG_FIELD_CONST || f.kind > HPSG_FIELD_PB_EPS_GRAD)
     throw HpsError{HPSG_ERR_INVALID, hpsg::fmt("unknown field kind %d", f.kind)};
   if (f.kind == HPSG_FIELD_POISSON2D_SRC && c->tree.dim != 2)
     throw HpsError{HPSG_ERR_INVALID, "HPSG_FIELD_POISSON2D_SRC is a 2D field"};
   if (f.kind == HPSG_FIELD_BUMPS_GRAD && (f.c[3] < 0 || f.c[3] >= c->tree.dim || f.c[3] != double(int(f.c[3]))))
     throw HpsError{HPSG_ERR_INVALID, "HPSG_FIELD_BUMPS_GRAD: c[3] must be an axis index"};
+  if (f.kind == HPSG_FIELD_PB_EPS_GRAD && (f.c[4] < 0 || f.c[4] >= 3 || f.c[4] != double(int(f.c[4]))))
+    throw HpsError{HPSG_ERR_INVALID, "HPSG_FIELD_PB_EPS_GRAD: c[4] must be an axis index"};
   if ((f.kind == HPSG_FIELD_BUMPS || f.kind == HPSG_FIELD_BUMPS_SIN || f.kind == HPSG_FIELD_BUMPS_GRAD ||
-       f.kind == HPSG_FIELD_DIVGRAD_SRC) &&
+       f.kind == HPSG_FIELD_DIVGRAD_SRC || f.kind == HPSG_FIELD_PB_EPS || f.kind == HPSG_FIELD_PB_EPS_GRAD) &&
       f.n_centers > 0) {
     if (!f.centers) throw HpsError{HPSG_ERR_INVALID, "bump field without centers"};
     auto b = std::make_unique<DevBuf>();
@@ -257,7 +117,7 @@ hpsk::DevField make_dev_field(hpsg_ctx* c, const hpsg_field& f, bool is_source,
   }
   if (f.kind == HPSG_FIELD_SAMPLED) {
     if (!f.samples) throw HpsError{HPSG_ERR_INVALID, "sampled field without samples"};
-    const size_t n = size_t(c->T.n_leaves()) * c->ops.n;
+    const size_t n = size_t(c->gen ? gen_n_leaves(c) : c->T.n_leaves()) * c->ops.n;
     auto b = std::make_unique<DevBuf>();
     b->alloc(n * 8, total);
     if (!g_dry_alloc) ck(cudaMemcpyAsync(b->p, f.samples, n * 8, cudaMemcpyHostToDevice, c->st), "sampled field upload");
@@ -266,6 +126,46 @@ hpsk::DevField make_dev_field(hpsg_ctx* c, const hpsg_field& f, bool is_source,
   }
   (void)is_source;
   return d;
+}
+
+// operator terms and source (CoefficientField, local_solve.hpp:17-23): validated as discretize_operator
+// does (local_solve.cpp:63-83) and uploaded; leaf_order (general trees) permutes sampled fields into the
+// leaf-group-major order of the leaf stage
+void set_terms(hpsg_ctx* c, const hpsg_term* terms, int n_terms, const hpsg_field* source,
+               const std::vector<int>* leaf_order) {
+  if (n_terms < 0 || n_terms > hpsk::kMaxTerms)
+    throw HpsError{HPSG_ERR_INVALID, hpsg::fmt("hpsg_create: 0..%d operator terms supported", hpsk::kMaxTerms)};
+  const int dim = c->tree.dim;
+  std::vector<std::vector<double>> perm;
+  auto prep = [&](const hpsg_field& f) {
+    hpsg_field g = f;
+    if (leaf_order && f.kind == HPSG_FIELD_SAMPLED && f.samples) {
+      const size_t np = size_t(c->ops.n);
+      perm.emplace_back(leaf_order->size() * np);
+      for (size_t i = 0; i < leaf_order->size(); ++i)
+        std::memcpy(perm.back().data() + i * np, f.samples + size_t((*leaf_order)[i]) * np, np * 8);
+      g.samples = perm.back().data();
+    }
+    return g;
+  };
+  c->nterms = n_terms;
+  for (int i = 0; i < n_terms; ++i) {
+    const hpsg_term& t = terms[i];
+    if (t.role < 0 || t.role > 3) throw HpsError{HPSG_ERR_INVALID, "discretize_operator: bad term role"};
+    if (t.role == HPSG_ROLE_GRADIENT && (t.axis < 0 || t.axis >= dim))
+      throw HpsError{HPSG_ERR_INVALID, "discretize_operator: bad gradient axis"};
+    if (t.role == HPSG_ROLE_SECOND_ORDER && (t.axis < 0 || t.axis >= dim || t.axis2 < 0 || t.axis2 >= dim))
+      throw HpsError{HPSG_ERR_INVALID, "discretize_operator: bad second_order axes"};
+    c->terms[i].role = t.role;
+    c->terms[i].axis = t.axis;
+    c->terms[i].axis2 = t.axis2;
+    c->terms[i].f = make_dev_field(c, prep(t.field), false);
+  }
+  if (source) {
+    c->source = make_dev_field(c, prep(*source), true);
+    c->has_source = 1;
+  }
+  if (!perm.empty()) ck(cudaStreamSynchronize(c->st), "field upload");  // the permuted host copies die here
 }
 
 double counted_build_flops(const hpsg_ctx* c) {
@@ -1158,7 +1058,7 @@ double solve_bytes(const hpsg_ctx* c, int nrhs) {
   return b;
 }
 
-}  // namespace
+}  // namespace hpsctx
 
 extern "C" {
 
@@ -1207,27 +1107,8 @@ int hpsg_create_part(const hpsg_tree* tree, const hpsg_part* part, const hpsg_te
     ck(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking), "stream");
     for (auto& e : c->ev) ck(cudaEventCreate(&e), "event");
     for (auto& e : c->lev_ev) ck(cudaEventCreate(&e), "event");
-    if (n_terms < 0 || n_terms > hpsk::kMaxTerms)
-      throw HpsError{HPSG_ERR_INVALID, hpsg::fmt("hpsg_create: 0..%d operator terms supported", hpsk::kMaxTerms)};
     setup(c.get());
-    c->nterms = n_terms;
-    for (int i = 0; i < n_terms; ++i) {
-      const hpsg_term& t = terms[i];
-      if (t.role < 0 || t.role > 3) throw HpsError{HPSG_ERR_INVALID, "discretize_operator: bad term role"};
-      if (t.role == HPSG_ROLE_GRADIENT && (t.axis < 0 || t.axis >= tree->dim))
-        throw HpsError{HPSG_ERR_INVALID, "discretize_operator: bad gradient axis"};
-      if (t.role == HPSG_ROLE_SECOND_ORDER &&
-          (t.axis < 0 || t.axis >= tree->dim || t.axis2 < 0 || t.axis2 >= tree->dim))
-        throw HpsError{HPSG_ERR_INVALID, "discretize_operator: bad second_order axes"};
-      c->terms[i].role = t.role;
-      c->terms[i].axis = t.axis;
-      c->terms[i].axis2 = t.axis2;
-      c->terms[i].f = make_dev_field(c.get(), t.field, false);
-    }
-    if (source) {
-      c->source = make_dev_field(c.get(), *source, true);
-      c->has_source = 1;
-    }
+    set_terms(c.get(), terms, n_terms, source, nullptr);
     if (opts && opts->source_imag) {
       if (!c->iti) throw HpsError{HPSG_ERR_INVALID, "hpsg_create: a complex source needs the ItI variant"};
       c->source_im = make_dev_field(c.get(), *opts->source_imag, true);
@@ -1247,6 +1128,34 @@ int hpsg_create_part(const hpsg_tree* tree, const hpsg_part* part, const hpsg_te
   }
   *out = c.release();
   return HPSG_OK;
+}
+
+int hpsg_create_tree(const hpsg_tree_desc* tree, const hpsg_term* terms, int n_terms, const hpsg_field* source,
+                     const hpsg_options* opts, hpsg_ctx** out) {
+  if (!out || !tree) return HPSG_ERR_INVALID;
+  *out = nullptr;
+  if (hpsg_device_count() <= 0) return HPSG_ERR_NO_DEVICE;
+  auto c = std::make_unique<hpsg_ctx>();
+  if (opts)
+    c->opts = *opts;
+  else
+    c->opts.literal_sign = 1;
+  const int rc = guarded(c.get(), [&] {
+    ck(cudaSetDevice(c->opts.device), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking), "stream");
+    for (auto& e : c->ev) ck(cudaEventCreate(&e), "event");
+    for (auto& e : c->lev_ev) ck(cudaEventCreate(&e), "event");
+    if (c->opts.source_imag) throw HpsError{HPSG_ERR_INVALID, "hpsg_create_tree: general trees are DtN (real)"};
+    c->luws.total = &c->dev_bytes;
+    c->luws.lookahead = !c->opts.no_lu_lookahead;
+    gen_setup(c.get(), tree);
+    const std::vector<int> order = gen_leaf_group_order(c.get());
+    set_terms(c.get(), terms, n_terms, source, &order);
+    gen_alloc(c.get());
+    ck(cudaStreamSynchronize(c->st), "create sync");
+  });
+  *out = c.release();
+  return rc;
 }
 
 int hpsg_estimate_bytes(const hpsg_tree* tree, const hpsg_part* part, const hpsg_term* terms, int n_terms,
@@ -1281,6 +1190,19 @@ int hpsg_build(hpsg_ctx* c) {
     for (size_t k = 0; k < c->cut_set.size(); ++k)
       if (!c->cut_set[k])
         throw HpsError{HPSG_ERR_STATE, hpsg::fmt("hpsg_build: input [h|T] of cut node %lld not set", (long long)k)};
+    if (c->gen) {  // general (adaptive) tree: general.cu
+      gen_build(c);
+      float a = 0, b = 0;
+      ck(cudaEventElapsedTime(&a, c->ev[0], c->ev[1]), "elapsed");
+      ck(cudaEventElapsedTime(&b, c->ev[2], c->ev[3]), "elapsed");
+      c->stats.t_leaf_ms = a;
+      c->stats.t_merge_ms = b;
+      c->stats.t_build_ms = a + b;
+      c->stats.n_levels = 0;
+      c->stats.launches_build = c->launches;
+      c->built = true;
+      return;
+    }
     ck(cudaEventRecord(c->ev[0], c->st), "ev");
     if (!c->T.cut) run_leaf_stage(c);
     ck(cudaEventRecord(c->ev[1], c->st), "ev");
@@ -1334,19 +1256,23 @@ int hpsg_solve_device(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u) {
   return guarded(c, [&] {
     c->launches = 0;
     ck(cudaEventRecord(c->ev[4], c->st), "ev");
-    run_solve(c, d_g, nrhs, d_u, nullptr);
+    if (c->gen)
+      gen_solve(c, d_g, nrhs, d_u, nullptr);
+    else
+      run_solve(c, d_g, nrhs, d_u, nullptr);
     ck(cudaEventRecord(c->ev[5], c->st), "ev");
     ck(cudaEventSynchronize(c->ev[5]), "solve sync");
     float ms = 0;
     ck(cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]), "elapsed");
     c->stats.t_solve_ms = ms;
-    c->stats.solve_bytes = solve_bytes(c, nrhs);
+    c->stats.solve_bytes = c->gen ? 0.0 : solve_bytes(c, nrhs);
     c->stats.launches_solve = c->launches;
   });
 }
 
 int hpsg_solve_complex(hpsg_ctx* c, const double* g_root, int nrhs, double* u_out) {
   if (!c || !g_root || !u_out || nrhs < 1) return HPSG_ERR_INVALID;
+  if (c->gen) return fail(c, HPSG_ERR_STATE, "not available on general (adaptive) trees: uniform-tree entry point");
   if (!c->built) return fail(c, HPSG_ERR_STATE, "hpsg_solve: build() first");
   if (!c->iti) return fail(c, HPSG_ERR_STATE, "hpsg_solve_complex: the solver is the DtN (real) variant");
   return guarded(c, [&] {
@@ -1374,6 +1300,7 @@ int hpsg_solve_complex(hpsg_ctx* c, const double* g_root, int nrhs, double* u_ou
 
 int hpsg_solve_radiation(hpsg_ctx* c, double* u_out, double* g_out) {
   if (!c || !u_out) return HPSG_ERR_INVALID;
+  if (c->gen) return fail(c, HPSG_ERR_STATE, "not available on general (adaptive) trees: uniform-tree entry point");
   if (!c->built) return fail(c, HPSG_ERR_STATE, "solve_radiation: build() first");
   if (!c->root_T) return fail(c, HPSG_ERR_STATE, "solve_radiation: root T was not built");
   return guarded(c, [&] {
@@ -1409,14 +1336,17 @@ int hpsg_solve(hpsg_ctx* c, const double* g_root, int nrhs, double* u_out, doubl
   if (c->T.cut) return fail(c, HPSG_ERR_STATE, "hpsg_solve: a cut part has no leaves (hpsg_part_solve_cut)");
   return guarded(c, [&] {
     c->launches = 0;
-    const size_t nbr = size_t(c->lv[0].n_ext) * nrhs;
-    const size_t nu = size_t(c->T.n_leaves()) * c->ops.n * nrhs;
+    const size_t nbr = size_t(c->gen ? c->stats.root_bsize : c->lv[0].n_ext) * nrhs;
+    const size_t nu = size_t(c->gen ? gen_n_leaves(c) : c->T.n_leaves()) * c->ops.n * nrhs;
     c->g_in.alloc(nbr * 8, &c->dev_bytes);
     c->u_out.alloc(nu * 8, &c->dev_bytes);
     if (leaf_g_out) c->lg_out.alloc(size_t(c->T.n_leaves()) * c->ops.nb * nrhs * 8, &c->dev_bytes);
     ck(cudaEventRecord(c->ev[4], c->st), "ev");
     ck(cudaMemcpyAsync(c->g_in.p, g_root, nbr * 8, cudaMemcpyHostToDevice, c->st), "g H2D");
-    run_solve(c, c->g_in.d(), nrhs, c->u_out.d(), leaf_g_out ? c->lg_out.d() : nullptr);
+    if (c->gen)
+      gen_solve(c, c->g_in.d(), nrhs, c->u_out.d(), leaf_g_out ? c->lg_out.d() : nullptr);
+    else
+      run_solve(c, c->g_in.d(), nrhs, c->u_out.d(), leaf_g_out ? c->lg_out.d() : nullptr);
     ck(cudaMemcpyAsync(u_out, c->u_out.p, nu * 8, cudaMemcpyDeviceToHost, c->st), "u D2H");
     if (leaf_g_out)
       ck(cudaMemcpyAsync(leaf_g_out, c->lg_out.p, size_t(c->T.n_leaves()) * c->ops.nb * nrhs * 8,
@@ -1427,13 +1357,14 @@ int hpsg_solve(hpsg_ctx* c, const double* g_root, int nrhs, double* u_out, doubl
     float ms = 0;
     ck(cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]), "elapsed");
     c->stats.t_solve_ms = ms;
-    c->stats.solve_bytes = solve_bytes(c, nrhs);
+    c->stats.solve_bytes = c->gen ? 0.0 : solve_bytes(c, nrhs);
     c->stats.launches_solve = c->launches;
   });
 }
 
 int hpsg_solve_new_source_device(hpsg_ctx* c, const double* d_f, const double* d_g, int nsrc, double* d_u) {
   if (!c || !d_f || !d_g || !d_u || nsrc < 1) return HPSG_ERR_INVALID;
+  if (c->gen) return fail(c, HPSG_ERR_STATE, "not available on general (adaptive) trees: uniform-tree entry point");
   if (!c->built) return fail(c, HPSG_ERR_STATE, "solve_new_source: build() first");
   if (!c->opts.keep_factors)
     return fail(c, HPSG_ERR_STATE, "solve_new_source: create the solver with keep_factors = 1 (leaf factors)");
@@ -1455,6 +1386,7 @@ int hpsg_solve_new_source_device(hpsg_ctx* c, const double* d_f, const double* d
 
 int hpsg_solve_new_source(hpsg_ctx* c, const double* f, const double* g_root, int nsrc, double* u_out) {
   if (!c || !f || !g_root || !u_out || nsrc < 1) return HPSG_ERR_INVALID;
+  if (c->gen) return fail(c, HPSG_ERR_STATE, "not available on general (adaptive) trees: uniform-tree entry point");
   if (!c->built) return fail(c, HPSG_ERR_STATE, "solve_new_source: build() first");
   if (c->T.cut) return fail(c, HPSG_ERR_STATE, "solve_new_source: a cut part has no leaves");
   const size_t nf = size_t(c->T.n_leaves()) * c->ops.n * nsrc;
@@ -1478,7 +1410,7 @@ int hpsg_solve_new_source(hpsg_ctx* c, const double* f, const double* g_root, in
 int hpsg_root_boundary_points(hpsg_ctx* c, double* xyz) {
   if (!c || !xyz) return HPSG_ERR_INVALID;
   return guarded(c, [&] {
-    const std::vector<double> p = hpsg::root_boundary_points(c->T);
+    const std::vector<double> p = c->gen ? gen_root_points(c) : hpsg::root_boundary_points(c->T);
     std::memcpy(xyz, p.data(), p.size() * 8);
   });
 }
@@ -1503,7 +1435,11 @@ static void tree_leaf_points(const hpsg::UniformTree& T, double* xyz) {
 
 int hpsg_leaf_points(hpsg_ctx* c, double* xyz) {
   if (!c || !xyz) return HPSG_ERR_INVALID;
-  return guarded(c, [&] { tree_leaf_points(c->T, xyz); });
+  return guarded(c, [&] {
+    if (!c->gen) return tree_leaf_points(c->T, xyz);
+    const std::vector<double> p = gen_leaf_points(c);
+    std::memcpy(xyz, p.data(), p.size() * 8);
+  });
 }
 
 int hpsg_tree_root_points(const hpsg_tree* t, double* xyz) {
@@ -1520,6 +1456,7 @@ int hpsg_tree_root_points(const hpsg_tree* t, double* xyz) {
 
 int hpsg_evaluate_at(hpsg_ctx* c, const double* d_u, int is_complex, const double* points, int npts, double* out) {
   if (!c || !d_u || (npts > 0 && (!points || !out)) || npts < 0) return HPSG_ERR_INVALID;
+  if (c->gen) return fail(c, HPSG_ERR_STATE, "not available on general (adaptive) trees: uniform-tree entry point");
   if (c->T.cut || c->T.root_depth) return fail(c, HPSG_ERR_STATE, "evaluate_at: whole-tree solver only");
   const int dim = c->tree.dim;
   for (int i = 0; i < npts; ++i)
@@ -1543,6 +1480,7 @@ int hpsg_evaluate_at(hpsg_ctx* c, const double* d_u, int is_complex, const doubl
 int hpsg_error_report(hpsg_ctx* c, const double* d_u, int is_complex, const hpsg_field* exact,
                       const hpsg_field* exact_imag, double* rel_linf, double* rel_l2) {
   if (!c || !d_u || !exact || !rel_linf || !rel_l2) return HPSG_ERR_INVALID;
+  if (c->gen) return fail(c, HPSG_ERR_STATE, "not available on general (adaptive) trees: uniform-tree entry point");
   if (c->T.cut) return fail(c, HPSG_ERR_STATE, "error_report: a cut part has no leaves");
   return guarded(c, [&] {
     hpsk::ErrArgs a{};
@@ -1605,6 +1543,7 @@ int hpsg_tree_leaf_points(const hpsg_tree* t, double* xyz) {
 
 int hpsg_get_leaf(hpsg_ctx* c, int ord, double* Y, double* v, double* Tm, double* h) {
   if (!c) return HPSG_ERR_INVALID;
+  if (c->gen) return fail(c, HPSG_ERR_STATE, "not available on general (adaptive) trees: uniform-tree entry point");
   if (!c->built) return fail(c, HPSG_ERR_STATE, "hpsg_get_leaf: build() first");
   if (c->T.cut) return fail(c, HPSG_ERR_STATE, "hpsg_get_leaf: a cut part has no leaves");
   if (c->iti) return fail(c, HPSG_ERR_STATE, "hpsg_get_leaf: not available for the ItI variant");
@@ -1634,6 +1573,7 @@ int hpsg_get_leaf(hpsg_ctx* c, int ord, double* Y, double* v, double* Tm, double
 
 int hpsg_node_sizes(hpsg_ctx* c, int id, int* n_ext, int* n_int) {
   if (!c || !n_ext || !n_int) return HPSG_ERR_INVALID;
+  if (c->gen) return fail(c, HPSG_ERR_STATE, "not available on general (adaptive) trees: uniform-tree entry point");
   for (const Level& L : c->lv) {
     const long long f = c->T.level_first_id(L.d);
     if (id >= f && id < f + L.nodes) {
@@ -1647,6 +1587,7 @@ int hpsg_node_sizes(hpsg_ctx* c, int id, int* n_ext, int* n_int) {
 
 int hpsg_get_node(hpsg_ctx* c, int id, double* S, double* gtilde, double* Tm, double* h) {
   if (!c) return HPSG_ERR_INVALID;
+  if (c->gen) return fail(c, HPSG_ERR_STATE, "not available on general (adaptive) trees: uniform-tree entry point");
   if (c->iti) return fail(c, HPSG_ERR_STATE, "hpsg_get_node: not available for the ItI variant");
   if (!c->built) return fail(c, HPSG_ERR_STATE, "hpsg_get_node: build() first");
   return guarded(c, [&] {
@@ -1680,6 +1621,7 @@ int hpsg_get_node(hpsg_ctx* c, int id, double* S, double* gtilde, double* Tm, do
 
 int hpsg_part_retarget(hpsg_ctx* c, long long root_index) {
   if (!c) return HPSG_ERR_INVALID;
+  if (c->gen) return fail(c, HPSG_ERR_STATE, "not available on general (adaptive) trees: uniform-tree entry point");
   if (c->T.root_depth == 0) return fail(c, HPSG_ERR_INVALID, "hpsg_part_retarget: the tree root has no siblings");
   if (c->iti) return fail(c, HPSG_ERR_STATE, "hpsg_part_retarget: DtN parts only");
   for (int i = 0; i < c->nterms; ++i)
@@ -1709,6 +1651,7 @@ int hpsg_part_sizes(hpsg_ctx* c, long long* n_cut, int* cut_nb, int* root_nb) {
 
 int hpsg_part_root_ht(hpsg_ctx* c, double* d_dst) {
   if (!c || !d_dst) return HPSG_ERR_INVALID;
+  if (c->gen) return fail(c, HPSG_ERR_STATE, "not available on general (adaptive) trees: uniform-tree entry point");
   if (!c->built) return fail(c, HPSG_ERR_STATE, "hpsg_part_root_ht: build() first");
   if (c->global_root(0)) return fail(c, HPSG_ERR_STATE, "hpsg_part_root_ht: the tree root has no [h|T]");
   return guarded(c, [&] {
@@ -1720,6 +1663,7 @@ int hpsg_part_root_ht(hpsg_ctx* c, double* d_dst) {
 
 int hpsg_part_set_cut_ht(hpsg_ctx* c, long long k, const double* d_src) {
   if (!c || !d_src) return HPSG_ERR_INVALID;
+  if (c->gen) return fail(c, HPSG_ERR_STATE, "not available on general (adaptive) trees: uniform-tree entry point");
   if (!c->T.cut) return fail(c, HPSG_ERR_STATE, "hpsg_part_set_cut_ht: not a cut part");
   if (k < 0 || k >= c->T.n_leaves()) return fail(c, HPSG_ERR_INVALID, "hpsg_part_set_cut_ht: bad cut node index");
   return guarded(c, [&] {
@@ -1734,6 +1678,7 @@ int hpsg_part_set_cut_ht(hpsg_ctx* c, long long k, const double* d_src) {
 
 int hpsg_part_solve_cut(hpsg_ctx* c, const double* d_g_root, int nrhs, double* d_g_cut) {
   if (!c || !d_g_root || !d_g_cut || nrhs < 1) return HPSG_ERR_INVALID;
+  if (c->gen) return fail(c, HPSG_ERR_STATE, "not available on general (adaptive) trees: uniform-tree entry point");
   if (!c->built) return fail(c, HPSG_ERR_STATE, "hpsg_part_solve_cut: build() first");
   if (!c->T.cut) return fail(c, HPSG_ERR_STATE, "hpsg_part_solve_cut: the part has real leaves (hpsg_solve)");
   return guarded(c, [&] {

@@ -8,6 +8,7 @@
 #pragma once
 
 #include <climits>
+#include <cmath>
 
 #include "hps_kernels.cuh"
 
@@ -19,7 +20,7 @@ constexpr int kLeafMaxP = 24;
 // Loops over the spatial axes are unrolled at compile time (DIM = 2 or 3) so the point and index
 // arrays stay in registers; the runtime-dim entry points dispatch once.
 template <int DIM>
-__device__ __forceinline__ double leaf_bumps(const DevField& f, const double* x) {
+__host__ __device__ __forceinline__ double leaf_bumps(const DevField& f, const double* x) {
   double s = 0.0;
   for (int j = 0; j < f.n_centers; ++j) {
     double r2 = 0.0;
@@ -33,9 +34,11 @@ __device__ __forceinline__ double leaf_bumps(const DevField& f, const double* x)
   return s;
 }
 
-// Device evaluation of the built-in fields (hps_cuda.h HPSG_FIELD_*).
+// Evaluation of the built-in fields (hps_cuda.h HPSG_FIELD_*): on the device inside the leaf kernels, on the
+// host for the adaptive-refinement criterion (hpsg_refine_adaptive).
 template <int DIM>
-__device__ __forceinline__ double eval_field_t(const DevField& f, const double* x, long long leaf, int pt, int npts) {
+__host__ __device__ __forceinline__ double eval_field_t(const DevField& f, const double* x, long long leaf, int pt,
+                                                        int npts) {
   const double* c = f.c;
   switch (f.kind) {
     case 0: return c[0];
@@ -94,7 +97,31 @@ __device__ __forceinline__ double eval_field_t(const DevField& f, const double* 
       }
       return f2;
     }
-    default: return __longlong_as_double(0x7ff8000000000000ULL);
+    case 9: {  // make_wavefront_3d source (proj/src/problems.cpp:154-179): Laplacian of atan(a rho^2 - 0.7)
+      const double a = c[0];
+      const double d0 = x[0] - c[1], d1 = x[1] - c[2], d2 = x[2] - c[3];
+      const double r2 = d0 * d0 + d1 * d1 + d2 * d2;
+      const double w = a * r2 - 0.7;
+      const double s = 1.0 + w * w;
+      return -2.0 * w / (s * s) * 4.0 * a * a * r2 + 6.0 * a / s;
+    }
+    case 10:    // PoissonBoltzmannSpec::eps, smooth (problems.cpp:187-191): eps0 + (eps_inf - eps0) exp(-A rho)
+    case 11: {  // grad_eps[axis c4] (problems.cpp:200-205)
+      double rho = 0.0, g[3] = {0.0, 0.0, 0.0};
+      for (int j = 0; j < f.n_centers; ++j) {
+        const double e0 = x[0] - f.centers[3 * j], e1 = x[1] - f.centers[3 * j + 1], e2 = x[2] - f.centers[3 * j + 2];
+        const double e = exp(-c[3] * (e0 * e0 + e1 * e1 + e2 * e2));
+        rho += e;
+        const double t = -2.0 * c[3] * e;
+        g[0] += t * e0;
+        g[1] += t * e1;
+        g[2] += t * e2;
+      }
+      if (f.kind == 10) return c[0] + (c[1] - c[0]) * exp(-c[2] * rho);
+      const int ax = int(c[4]);
+      return (c[1] - c[0]) * exp(-c[2] * rho) * (-c[2]) * (ax == 0 ? g[0] : ax == 1 ? g[1] : g[2]);
+    }
+    default: return NAN;
   }
 }
 

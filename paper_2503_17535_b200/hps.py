@@ -24,7 +24,7 @@ HPSG_OK, HPSG_ERR_INVALID, HPSG_ERR_SINGULAR_LEAF, HPSG_ERR_SINGULAR_MERGE, HPSG
     HPSG_ERR_CUDA, HPSG_ERR_STATE, HPSG_ERR_NO_DEVICE = range(9)
 
 FIELD_CONST, FIELD_BUMPS, FIELD_PLANE_SIN, FIELD_PLANE_COS, FIELD_BUMPS_SIN, FIELD_POISSON2D_SRC, FIELD_SAMPLED, \
-    FIELD_BUMPS_GRAD, FIELD_DIVGRAD_SRC = range(9)
+    FIELD_BUMPS_GRAD, FIELD_DIVGRAD_SRC, FIELD_WAVEFRONT_SRC, FIELD_PB_EPS, FIELD_PB_EPS_GRAD = range(12)
 ROLE_LAPLACIAN, ROLE_GRADIENT, ROLE_ZEROTH, ROLE_SECOND_ORDER = range(4)
 
 
@@ -87,6 +87,8 @@ def lib():
                                   C.POINTER(vp)]
         L.hpsg_create_part.argtypes = [C.POINTER(_Tree), C.POINTER(_Part), C.POINTER(_Term), C.c_int,
                                        C.POINTER(_Field), C.POINTER(_Options), C.POINTER(vp)]
+        L.hpsg_create_tree.argtypes = [C.POINTER(_TreeDesc), C.POINTER(_Term), C.c_int, C.POINTER(_Field),
+                                       C.POINTER(_Options), C.POINTER(vp)]
         L.hpsg_part_sizes.argtypes = [vp, C.POINTER(C.c_longlong), C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.hpsg_estimate_bytes.argtypes = [C.POINTER(_Tree), C.POINTER(_Part), C.POINTER(_Term), C.c_int,
                                           C.POINTER(_Field), C.POINTER(_Options), C.c_int, dp]
@@ -203,6 +205,66 @@ def build_uniform_tree(lo, hi, L, dim, p):
     return UniformTree(dim=dim, p=p, L=L, lo=lo, hi=hi)
 
 
+class _TreeDesc(C.Structure):
+    _fields_ = [("dim", C.c_int), ("p", C.c_int), ("n_nodes", C.c_int), ("depth", C.POINTER(C.c_int)),
+                ("n_children", C.POINTER(C.c_int)), ("children", C.POINTER(C.c_int)),
+                ("lo", C.POINTER(C.c_double)), ("hi", C.POINTER(C.c_double))]
+
+
+class GeneralTree:
+    """The reference's DiscretizationTree (proj/include/hps/mesh.hpp:28-61) as node arrays: any tree --
+    adaptive, level-restricted octrees from refine_adaptive (mesh.cpp:233-318) or uniform ones.
+    depth (n,), n_children (n,), children (n, 8), lo / hi (n, 3); node 0 is the root; leaves are
+    enumerated depth-first (DiscretizationTree::finalize, mesh.cpp:54-71)."""
+
+    def __init__(self, dim, p, depth, n_children, children, lo, hi):
+        self.dim, self.p = int(dim), int(p)
+        self.depth = np.ascontiguousarray(depth, dtype=np.int32)
+        self.n_children = np.ascontiguousarray(n_children, dtype=np.int32)
+        self.children = np.ascontiguousarray(np.asarray(children).reshape(-1, 8), dtype=np.int32)
+        self.lo = np.ascontiguousarray(np.asarray(lo, dtype=np.float64).reshape(-1, 3))
+        self.hi = np.ascontiguousarray(np.asarray(hi, dtype=np.float64).reshape(-1, 3))
+        self.n_nodes = len(self.depth)
+        nc = 4 if self.dim == 2 else 8
+        leaves, stack = [], [0]
+        while stack:
+            i = stack.pop()
+            if self.n_children[i] == 0:
+                leaves.append(i)
+            else:
+                stack.extend(int(c) for c in self.children[i, :nc][::-1])
+        self.leaves = np.array(leaves, dtype=np.int32)
+
+    @classmethod
+    def from_arrays(cls, d, dim, p):
+        """From a dict with keys depth, n_children, children, lo, hi (e.g. oracle.ref.RefSolver.tree())."""
+        return cls(dim, p, d["depth"], d["n_children"], d["children"], d["lo"], d["hi"])
+
+    @property
+    def q(self):
+        return self.p - 2
+
+    @property
+    def n_leaves(self):
+        return len(self.leaves)
+
+    @property
+    def total_points(self):
+        return self.n_leaves * self.p ** self.dim
+
+    @property
+    def leaf_boundary_size(self):
+        return 2 * self.dim * self.q ** (self.dim - 1)
+
+    def total_nodes(self):
+        return self.n_nodes
+
+    def desc(self):
+        return _TreeDesc(self.dim, self.p, self.n_nodes, self.depth.ctypes.data_as(C.POINTER(C.c_int)),
+                         self.n_children.ctypes.data_as(C.POINTER(C.c_int)),
+                         self.children.ctypes.data_as(C.POINTER(C.c_int)), _dp(self.lo), _dp(self.hi))
+
+
 def tree_root_points(tree: UniformTree):
     """Root boundary points of a tree without a solver (hpsg_tree_root_points; solver.cpp:159-182)."""
     out = np.zeros((tree.root_boundary_size, 3))
@@ -228,6 +290,36 @@ def bump_centers(seed, n=10, dim=2):
     out = np.zeros(3 * n)
     lib().hpsg_bump_centers(seed, n, dim, _dp(out))
     return out.reshape(n, 3)
+
+
+def refine_adaptive(lo, hi, p, fields, tol=1e-3, max_depth=10, cap=1 << 20):
+    """refine_adaptive(domain, RefinementCriterion{tol, p, test_fields}, max_depth) (proj/src/mesh.cpp:233-318)
+    in 3D on [lo,hi]^3 with built-in fields -> (GeneralTree, n_unresolved)."""
+    keep = []
+    arr = (_Field * len(fields))()
+    for i, f in enumerate(fields):
+        arr[i] = f.to_c(keep)
+    lo3, hi3 = np.full(3, float(lo)), np.full(3, float(hi))
+    n, nu = C.c_int(), C.c_int()
+    L = lib()
+    ip = C.POINTER(C.c_int)
+    L.hpsg_refine_adaptive.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_double, C.c_int,
+                                       C.POINTER(_Field), C.c_int, C.c_int, ip, ip, ip, ip, C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double), ip]
+    rc = L.hpsg_refine_adaptive(p, _dp(lo3), _dp(hi3), tol, max_depth, arr, len(fields), 0, C.byref(n), None, None,
+                                None, None, None, C.byref(nu))
+    if rc != HPSG_OK and n.value == 0:
+        raise HpsError(rc, "hpsg_refine_adaptive failed")
+    nn = n.value
+    depth, nch = np.zeros(nn, np.int32), np.zeros(nn, np.int32)
+    ch = np.zeros((nn, 8), np.int32)
+    tlo, thi = np.zeros((nn, 3)), np.zeros((nn, 3))
+    ipn = lambda a: a.ctypes.data_as(ip)  # noqa: E731
+    rc = L.hpsg_refine_adaptive(p, _dp(lo3), _dp(hi3), tol, max_depth, arr, len(fields), nn, C.byref(n), ipn(depth),
+                                ipn(nch), ipn(ch), _dp(tlo), _dp(thi), C.byref(nu))
+    if rc != HPSG_OK:
+        raise HpsError(rc, "hpsg_refine_adaptive failed")
+    return GeneralTree(3, p, depth, nch, ch, tlo, thi), nu.value
 
 
 # ----------------------------------------------------------------------------- footprint
@@ -279,7 +371,7 @@ class HpsSolver:
             arr[i].role, arr[i].axis, arr[i].axis2 = t.role, t.axis, t.axis2
             arr[i].field = t.field.to_c(keep)
         src = source.to_c(keep) if source is not None else None
-        tr = _Tree(tree.dim, tree.p, tree.L, tree.lo, tree.hi)
+        tr = _Tree(tree.dim, tree.p, tree.L, tree.lo, tree.hi) if isinstance(tree, UniformTree) else None
         if variant not in ("dtn", "iti"):
             raise HpsError(HPSG_ERR_INVALID, f"unknown variant {variant!r}")
         self.variant = variant
@@ -290,11 +382,19 @@ class HpsSolver:
             op.source_imag = C.pointer(self._src_im)
         op.force_batched_leaf = int(force_batched_leaf)
         op.no_lu_lookahead = int(not lu_lookahead)
-        self.part = tuple(part) if part is not None else (0, 0, tree.L)
-        pt = _Part(*self.part)
         h = C.c_void_p()
-        rc = L.hpsg_create_part(C.byref(tr), C.byref(pt), arr, len(terms), C.byref(src) if src is not None else None,
-                                C.byref(op), C.byref(h))
+        if isinstance(tree, GeneralTree):  # hpsg_create_tree: adaptive / arbitrary trees
+            if part is not None:
+                raise HpsError(HPSG_ERR_INVALID, "parts are uniform-tree only")
+            self.part = None
+            self._desc = tree.desc()
+            rc = L.hpsg_create_tree(C.byref(self._desc), arr, len(terms), C.byref(src) if src is not None else None,
+                                    C.byref(op), C.byref(h))
+        else:
+            self.part = tuple(part) if part is not None else (0, 0, tree.L)
+            pt = _Part(*self.part)
+            rc = L.hpsg_create_part(C.byref(tr), C.byref(pt), arr, len(terms),
+                                    C.byref(src) if src is not None else None, C.byref(op), C.byref(h))
         self._h = h
         if rc != HPSG_OK:
             msg = L.hpsg_last_error(h).decode() if h.value else "no CUDA device"
@@ -302,6 +402,11 @@ class HpsSolver:
             raise HpsError(rc, f"hpsg_create: {msg}")
         self.root_implicit_S = root_implicit_S
         self.npts = tree.p ** tree.dim
+        if self.part is None:
+            st = self.stats()
+            self.n_cut, self.cut_nb, self.nb_root = 0, 0, st["root_bsize"]
+            self.n_leaves = tree.n_leaves
+            return
         nc, cnb, rnb = C.c_longlong(), C.c_int(), C.c_int()
         self._check(L.hpsg_part_sizes(h, C.byref(nc), C.byref(cnb), C.byref(rnb)), "part_sizes")
         self.n_cut, self.cut_nb, self.nb_root = nc.value, cnb.value, rnb.value

@@ -11,8 +11,8 @@ from typing import Callable
 
 import numpy as np
 
-from .hps import (FIELD_BUMPS, FIELD_BUMPS_GRAD, FIELD_BUMPS_SIN, FIELD_CONST, FIELD_DIVGRAD_SRC, FIELD_PLANE_COS,
-                  FIELD_PLANE_SIN, FIELD_POISSON2D_SRC,
+from .hps import (FIELD_BUMPS, FIELD_BUMPS_GRAD, FIELD_BUMPS_SIN, FIELD_CONST, FIELD_DIVGRAD_SRC, FIELD_PB_EPS,
+                  FIELD_PB_EPS_GRAD, FIELD_PLANE_COS, FIELD_PLANE_SIN, FIELD_POISSON2D_SRC, FIELD_WAVEFRONT_SRC,
                   ROLE_GRADIENT, ROLE_LAPLACIAN, ROLE_ZEROTH, Field, Term)
 from .seeded import bump_centers  # pure Python: defining a problem never loads a shared object
 
@@ -100,8 +100,34 @@ def poisson3d_var(seed=11, n_bumps=5, amp=0.5, alpha=4.0, omega=2.0, phase=0.5) 
     return Problem("poisson3d_var", 3, -1.0, 1.0, terms, src, u, u)
 
 
+def wavefront3d(alpha=30.0) -> Problem:
+    """make_wavefront_3d (proj/src/problems.cpp:154-179): Laplace(u) = f on [0,1]^3 with the spherical front
+    u = atan(alpha |x - c|^2 - 0.7), c = (1/2, 1/2, 1/2), Dirichlet data from u.  The paper's Table 1 problem
+    (adaptive octrees); its refinement field is the source."""
+    def u(x):
+        r2 = ((x[..., :3] - 0.5) ** 2).sum(axis=-1)
+        return np.arctan(alpha * r2 - 0.7)
+
+    src = Field(FIELD_WAVEFRONT_SRC, (alpha, 0.5, 0.5, 0.5))
+    return Problem("wavefront3d", 3, 0.0, 1.0, [Term(ROLE_LAPLACIAN, Field(FIELD_CONST, (1.0,)))], src, u, u)
+
+
+def poisson_boltzmann3d(seed=20260810, n_centers=50, delta=45.0, eps0=16.0, eps_inf=100.0, amp=10.0) -> Problem:
+    """make_poisson_boltzmann with the smooth permittivity (proj/src/problems.cpp:181-253):
+    eps Lap(u) + grad(eps).grad(u) = -rho on [-1,1]^3, u = 0 on the boundary, rho = sum_j exp(-delta |x - z_j|^2)
+    over 50 seeded centers (make_pb_spec: std::mt19937_64, U(-1/2, 1/2)), eps = eps0 + (eps_inf - eps0) exp(-amp rho).
+    No closed-form solution (accuracy is judged by self-convergence)."""
+    z = bump_centers(seed, n_centers, 3)
+    c = (eps0, eps_inf, amp, delta)
+    terms = [Term(ROLE_LAPLACIAN, Field(FIELD_PB_EPS, c, centers=z))]
+    terms += [Term(ROLE_GRADIENT, Field(FIELD_PB_EPS_GRAD, c + (float(a),), centers=z), axis=a) for a in range(3)]
+    src = Field(FIELD_BUMPS, (0.0, -1.0, delta), centers=z)
+    return Problem("poisson_boltzmann3d", 3, -1.0, 1.0, terms, src, lambda x: np.zeros(x.shape[:-1]), None)
+
+
 CATALOG = {"poisson2d": poisson2d, "helmholtz_bumps": helmholtz_bumps, "laplace_poly2d": laplace_poly2d,
-           "laplace3d": poisson3d_const, "poisson3d_var": poisson3d_var}
+           "laplace3d": poisson3d_const, "poisson3d_var": poisson3d_var, "wavefront3d": wavefront3d,
+           "poisson_boltzmann3d": poisson_boltzmann3d}
 
 
 def rel_linf(u, ref):
