@@ -19,6 +19,8 @@
 #ifndef HPS_CUDA_H
 #define HPS_CUDA_H
 
+#include <stddef.h>
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -147,6 +149,14 @@ int hpsg_create_tree(const hpsg_tree_desc* tree, const hpsg_term* terms, int n_t
  * (proj/src/mesh.cpp:233-318, with enforce_level_restriction :141-167): 3D, built-in fields evaluated on the
  * host.  Writes the tree as node arrays in the reference's construction order (n_nodes x {depth, n_children,
  * children[8], lo[3], hi[3]}); returns HPSG_ERR_INVALID with *n_nodes set when cap is too small. */
+/* mesh_to_json (proj/src/mesh.cpp:435-463): the tree as the reference's JSON text (nlohmann dump(1) format,
+ * byte-identical).  out == NULL: only *len (without the terminating 0) is set. */
+int hpsg_mesh_json(const hpsg_tree_desc* tree, char* out, size_t cap, size_t* len);
+/* dump_solution (proj/src/downpass.cpp:108-143): the device-resident solution d_u (n_points
+ * doubles, or interleaved complex) to bin_path (raw little-endian FP64, leaf-major / point-minor) and the JSON
+ * sidecar json_path {"dtype", "leaf_len", "n_leaves", "tree_ref"}, each written to <path>.tmp and renamed. */
+int hpsg_dump_solution(hpsg_ctx* ctx, const double* d_u, int is_complex, const char* json_path, const char* bin_path,
+                       const char* tree_ref);
 int hpsg_refine_adaptive(int p, const double* lo, const double* hi, double tol, int max_depth,
                          const hpsg_field* fields, int n_fields, int cap, int* n_nodes, int* depth, int* n_children,
                          int* children, double* lo_out, double* hi_out, int* n_unresolved);

@@ -70,6 +70,9 @@ def lib():
                                         C.c_int, dp]
         L.ref_bench_sample.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.POINTER(Term), C.c_int,
                                        C.POINTER(Field), C.c_int, dp]
+        L.ref_mesh_json.restype = C.c_longlong
+        L.ref_mesh_json.argtypes = [vp, C.c_char_p, C.c_longlong]
+        L.ref_dump_solution.argtypes = [vp, dp, C.c_char_p, C.c_char_p, C.c_char_p]
         _lib = L
     return _lib
 
@@ -249,6 +252,16 @@ class RefSolver:
         check(lib().ref_get_node(self.h, nid, f(S), f(gt), f(T), f(h)))
         return (S.reshape(ni, ne, order="F") if S is not None else None, gt,
                 T.reshape(ne, ne, order="F") if T is not None else None, h)
+
+    def mesh_json(self):
+        n = lib().ref_mesh_json(self.h, None, 0)
+        buf = C.create_string_buffer(n + 1)
+        lib().ref_mesh_json(self.h, buf, n + 1)
+        return buf.value.decode()
+
+    def dump_solution(self, u, json_path, bin_path, tree_ref):
+        u = _as_doubles(u, self.cplx)
+        check(lib().ref_dump_solution(self.h, _dp(u), json_path.encode(), bin_path.encode(), tree_ref.encode()))
 
     def error_report(self, u):
         u = _as_doubles(u, self.cplx)

@@ -423,6 +423,26 @@ int ref_solve_problem(const char* name, double k, unsigned seed, int p, int adap
   });
 }
 
+long long ref_mesh_json(void* h, char* buf, long long cap) {
+  long long n = -1;
+  guard([&] {
+    const std::string s = hps::mesh_to_json(*H(h)->tree);
+    n = (long long)s.size();
+    if (buf && cap > n) std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+  return n;
+}
+
+int ref_dump_solution(void* h, const double* u, const char* json_path, const char* bin_path, const char* tree_ref) {
+  return guard([&] {
+    RefHandle* r = H(h);
+    if (r->cplx())
+      hps::dump_solution(field_from<Complex>(r, u), json_path, bin_path, tree_ref);
+    else
+      hps::dump_solution(field_from<Real>(r, u), json_path, bin_path, tree_ref);
+  });
+}
+
 int ref_bench_sample(int p, int L, int m, double lo, double hi, const oracle_term* terms, int n_terms,
                      const oracle_field* source, int root_implicit, double* out) {
   return guard([&] {

@@ -86,6 +86,11 @@ int ref_solve_problem(const char* name, double k, unsigned seed, int p, int adap
 int ref_bench_sample(int p, int L, int m, double lo, double hi, const oracle_term* terms, int n_terms,
                      const oracle_field* source, int root_implicit, double* out);
 
+/* the reference's output formats: mesh_to_json (mesh.cpp:435-463) into buf (returns the length, -1 on error;
+ * the text is written only when it fits), dump_solution (downpass.cpp:108-143) of solution u */
+long long ref_mesh_json(void* h, char* buf, long long cap);
+int ref_dump_solution(void* h, const double* u, const char* json_path, const char* bin_path, const char* tree_ref);
+
 #ifdef __cplusplus
 }
 #endif

@@ -115,6 +115,7 @@ struct hpsg_ctx {
   bool iti = false;  // ItI variant (real-equivalent complex)
   bool root_T = false;  // ItI radiation closure: the root forms [h|T] and factors T
   DevBuf radM, radPiv, radStats;  // [T_root | -h_root] -> [LU | g_rad]
+  DevBuf itiW;                    // ItI merges: [W | X_top - D12 X_bot] of one level
   hpsk::DevField source_im{};
   int has_source_im = 0;
   hpsg::ItiLeafOperators iops;

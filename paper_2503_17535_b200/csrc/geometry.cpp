@@ -589,38 +589,47 @@ ItiMergeTables make_iti_merge_tables(int s) {
       slot_off[k][of] = pos;
       pos += s;
     }
-  // complex block (matrix dst, rows at complex offset r, cols at complex offset c of a complex
-  // R x C matrix placed at real column base cb) <- child k's T block (faces rf, cf) or h (rf)
-  auto tblock = [&](int dst, int R, int C, int cb, int r, int c, int k, int rf, int cf) {
+  // Real-equivalent index of interface unknown o (complex offset) and part q (0 re, 1 im): half-blocked,
+  // [re(top); im(top); re(bottom); im(bottom)] with top = the {a, c} slots, so that D = [[I, D12], [D21, I]]
+  // keeps its complex 2 x 2 block structure and merge_iti's W = I - D12 D21 (merge.cpp:447-463) is a
+  // contiguous real-equivalent block.  Exterior vectors stay [re; im].
+  const int hc = nint_c / 2;
+  auto ri = [&](int q, int o) { return o < hc ? q * hc + o : nint_c + q * hc + (o - hc); };
+  auto xi = [&](int q, int o) { return q * next_c + o; };
+  // complex s x s block of child k's T (faces rf, cf) or h (cf < 0) into matrix dst: rows at complex offset r
+  // (interface rows when rint), columns at complex offset c (interface columns when cint) after column base cb
+  auto tblock = [&](int dst, bool rint, bool cint, int cb, int r, int c, int k, int rf, int cf) {
     for (int qr = 0; qr < 2; ++qr)
       for (int qc = 0; qc < 2; ++qc)
-        t.blocks.push_back({dst, qr * R + r, cb + qc * C + c, k, qr * nbc_c + rf * s, 1 + qc * nbc_c + cf * s, s, s});
+        t.blocks.push_back({dst, rint ? ri(qr, r) : xi(qr, r), cb + (cint ? ri(qc, c) : xi(qc, c)), k,
+                            qr * nbc_c + rf * s, 1 + qc * nbc_c + cf * s, s, s});
   };
-  auto hblock = [&](int dst, int R, int col, int r, int k, int rf) {
-    for (int qr = 0; qr < 2; ++qr) t.blocks.push_back({dst, qr * R + r, col, k, qr * nbc_c + rf * s, 0, s, 1});
+  auto hblock = [&](int dst, bool rint, int col, int r, int k, int rf) {
+    for (int qr = 0; qr < 2; ++qr)
+      t.blocks.push_back({dst, rint ? ri(qr, r) : xi(qr, r), col, k, qr * nbc_c + rf * s, 0, s, 1});
   };
   // exterior rows: h_ext, A, B from each child's exterior faces (merge.cpp:386-415)
   for (int k = 0; k < 4; ++k)
     for (int rf = 0; rf < 4; ++rf) {
       const int roff = ext_off(k, rf);
       if (roff < 0) continue;
-      hblock(2, next_c, 0, roff, k, rf);
+      hblock(2, false, 0, roff, k, rf);
       for (int cf = 0; cf < 4; ++cf) {
         if (ext_off(k, cf) >= 0)
-          tblock(2, next_c, next_c, 1, roff, ext_off(k, cf), k, rf, cf);  // A in [h_ext | A]
+          tblock(2, false, false, 1, roff, ext_off(k, cf), k, rf, cf);  // A in [h_ext | A]
         else
-          tblock(1, next_c, nint_c, 0, roff, slot_off[k][cf], k, rf, cf);  // B
+          tblock(1, false, true, 0, roff, slot_off[k][cf], k, rf, cf);  // B
       }
     }
   // interface rows: g_owner + neighbour's outgoing data = 0 (merge.cpp:417-447)
   for (const Slot& sl : slots) {
-    hblock(0, nint_c, 2 * nint_c, sl.off, sl.nb, sl.nbf);  // h_int column of [D | h_int | C]
-    for (int qr = 0; qr < 2; ++qr) t.blocks.push_back({0, qr * nint_c + sl.off, qr * nint_c + sl.off, -1, 0, 0, s, s});
+    hblock(0, true, 2 * nint_c, sl.off, sl.nb, sl.nbf);  // h_int column of [D | h_int | C]
+    for (int qr = 0; qr < 2; ++qr) t.blocks.push_back({0, ri(qr, sl.off), ri(qr, sl.off), -1, 0, 0, s, s});
     for (int cf = 0; cf < 4; ++cf) {
       if (ext_off(sl.nb, cf) >= 0)
-        tblock(0, nint_c, next_c, 2 * nint_c + 1, sl.off, ext_off(sl.nb, cf), sl.nb, sl.nbf, cf);  // C
+        tblock(0, true, false, 2 * nint_c + 1, sl.off, ext_off(sl.nb, cf), sl.nb, sl.nbf, cf);  // C
       else
-        tblock(0, nint_c, nint_c, 0, sl.off, slot_off[sl.nb][cf], sl.nb, sl.nbf, cf);  // D
+        tblock(0, true, true, 0, sl.off, slot_off[sl.nb][cf], sl.nb, sl.nbf, cf);  // D
     }
   }
   // downward scatter per (child, real-equivalent face): real parts then imaginary parts
@@ -628,8 +637,8 @@ ItiMergeTables make_iti_merge_tables(int s) {
   for (int c = 0; c < 4; ++c)
     for (int f = 0; f < 4; ++f) {
       const int e = ext_off(c, f);
-      t.down[c * 8 + f] = e >= 0 ? e : -(slot_off[c][f]) - 1;
-      t.down[c * 8 + 4 + f] = e >= 0 ? next_c + e : -(nint_c + slot_off[c][f]) - 1;
+      t.down[c * 8 + f] = e >= 0 ? xi(0, e) : -ri(0, slot_off[c][f]) - 1;
+      t.down[c * 8 + 4 + f] = e >= 0 ? xi(1, e) : -ri(1, slot_off[c][f]) - 1;
     }
   return t;
 }

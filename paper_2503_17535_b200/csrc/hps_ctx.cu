@@ -181,6 +181,12 @@ double counted_build_flops(const hpsg_ctx* c) {
   for (const Level& L : c->lv) {
     const double a = L.n_int, e = L.n_ext;
     double per;
+    if (c->iti) {  // real-equivalent executed flops of the W scheme: D12 D21, LU(W) + solves, two RHS GEMMs, Schur
+      const double h = a / 2, m = 1 + e;
+      per = 2 * h * h * h + 2.0 / 3.0 * h * h * h + 2 * h * h * m + 2 * (2 * h * h * m) + (c->forms_T(L.d) ? 2 * e * a * m : 0);
+      f += per * L.nodes;
+      continue;
+    }
     if (c->forms_T(L.d))
       per = 2.0 / 3.0 * a * a * a + 2 * a * a * e + 2 * e * a * e;
     else
@@ -358,13 +364,22 @@ void alloc_build(hpsg_ctx* c) {
     c->radPiv.alloc(size_t(R.n_ext) * 4, tot);
     c->radStats.alloc(3 * 8, tot);
   }
+  if (c->iti) {  // merge_iti's [W | X_top - D12 X_bot] per node of the largest level
+    size_t wmax = 0;
+    for (const Level& L : c->lv) {
+      const size_t h = L.n_int / 2;
+      wmax = std::max(wmax, size_t(L.nodes) * h * (h + 1 + L.n_ext) * 8);
+    }
+    c->itiW.alloc(wmax, tot);
+  }
   // scratch of every batched LU the build runs (lu.cuh LuWorkspace), reserved now so it is counted
   auto reserve = [&](long long batch, int n, int m, bool factor) {
     ck(hpsk::lu_workspace_reserve(c->luws, int(batch), n, m, factor, g_dry_alloc), "LU workspace");
   };
   if (!c->T.cut && !c->fused) reserve(nl, o.ni, 1 + o.nb, true);
   for (const Level& L : c->lv)
-    reserve(L.nodes, L.n_int, (!c->forms_T(L.d) && c->opts.root_implicit_S) ? 1 : 1 + L.n_ext, true);
+    reserve(L.nodes, c->iti ? L.n_int / 2 : L.n_int,
+            (!c->forms_T(L.d) && c->opts.root_implicit_S) ? 1 : 1 + L.n_ext, true);
   if (c->root_T) reserve(1, c->lv[0].n_ext, 1, true);
 }
 
@@ -415,8 +430,10 @@ void check_merge_errors(hpsg_ctx* c) {
     for (long long i = 0; i < L.nodes; ++i)
       if (s[size_t(i) * 3 + 2] >= 0)
         throw HpsError{HPSG_ERR_SINGULAR_MERGE,
-                       hpsg::fmt("merge_dtn: singular interface matrix D (pivot %d) at node %lld",
-                                 int(s[size_t(i) * 3 + 2]), c->T.level_first_id(L.d) + i)};
+                       c->iti ? hpsg::fmt("merge_iti: singular Schur block W (pivot %d) at node %lld",
+                                          int(s[size_t(i) * 3 + 2]), c->T.level_first_id(L.d) + i)
+                              : hpsg::fmt("merge_dtn: singular interface matrix D (pivot %d) at node %lld",
+                                          int(s[size_t(i) * 3 + 2]), c->T.level_first_id(L.d) + i)};
   }
 }
 
@@ -659,6 +676,45 @@ void run_merge_level(hpsg_ctx* c, int d) {
   ck(cudaGetLastError(), "gather");
   }
   ck(hpsk::lu_stats_init(L.stats.d(), int(L.nodes), c->st), "stats init");
+  if (c->iti) {
+    // merge_iti's structured elimination (merge.cpp:447-463, apply_Dinv :160-174): D = [[I, D12], [D21, I]]
+    // (half-blocked real-equivalent order), W = I - D12 D21, then for X = [h_int | C]:
+    //   Y_top = W^-1 (X_top - D12 X_bot),  Y_bot = X_bot - D21 Y_top;  [x_h | X] <- [Y_top; Y_bot] in place
+    const int N = L.n_int, h = N / 2, m = 1 + L.n_ext, B = int(L.nodes);
+    const long long sW = (long long)h * (h + m), sM = L.strideMD();
+    double* MD = L.MD.d();
+    double* W = c->itiW.d();
+    ck(cudaMemsetAsync(W, 0, size_t(B) * sW * 8, c->st), "W zero");
+    hpsk::launch_add_identity(W, h, h, sW, B, c->st);
+    GemmArgs g;  // W = I - D12 D21
+    g.m = h, g.n = h, g.k = h, g.batch = B;
+    g.A = MD + (long long)h * N, g.lda = N, g.sA = sM;       // D12 = D[0:h, h:N]
+    g.B = MD + h, g.ldb = N, g.sB = sM;                       // D21 = D[h:N, 0:h]
+    g.C = W, g.ldc = h, g.sC = sW;
+    g.D = W, g.ldd = h, g.sD = sW;
+    g.alpha = -1.0, g.beta = 1.0;
+    gemm(c, g);
+    GemmArgs r;  // [W | X_top - D12 X_bot]
+    r.m = h, r.n = m, r.k = h, r.batch = B;
+    r.A = MD + (long long)h * N, r.lda = N, r.sA = sM;
+    r.B = MD + (long long)N * N + h, r.ldb = N, r.sB = sM;    // X_bot
+    r.C = MD + (long long)N * N, r.ldc = N, r.sC = sM;        // X_top
+    r.D = W + (long long)h * h, r.ldd = h, r.sD = sW;
+    r.alpha = -1.0, r.beta = 1.0;
+    gemm(c, r);
+    ck(hpsk::bgetrf_aug(B, h, m, BatchedMat{W, h, sW}, L.piv.i(), L.stats.d(), c->luws, c->st, false), "W bgetrf");
+    c->launches += 2 + lu_launches(h, m, true);
+    GemmArgs y;  // Y_bot = X_bot - D21 Y_top (in place in MD)
+    y.m = h, y.n = m, y.k = h, y.batch = B;
+    y.A = MD + h, y.lda = N, y.sA = sM;
+    y.B = W + (long long)h * h, y.ldb = h, y.sB = sW;
+    y.C = MD + (long long)N * N + h, y.ldc = N, y.sC = sM;
+    y.D = MD + (long long)N * N + h, y.ldd = N, y.sD = sM;
+    y.alpha = -1.0, y.beta = 1.0;
+    gemm(c, y);
+    hpsk::launch_copy_batched(MD + (long long)N * N, N, sM, W + (long long)h * h, h, sW, h, m, B, c->st);
+    ++c->launches;
+  } else {
   const int m = (root && c->opts.root_implicit_S) ? 1 : 1 + L.n_ext;
   BatchedMat M{L.MD.d(), L.n_int, L.strideMD()};
   // L of D is needed afterwards only at the root with implicit S (the solve's bgetrs) and for the
@@ -666,6 +722,7 @@ void run_merge_level(hpsg_ctx* c, int d) {
   const bool keep_L = (root && c->opts.root_implicit_S) || c->opts.keep_factors;
   ck(hpsk::bgetrf_aug(int(L.nodes), L.n_int, m, M, L.piv.i(), L.stats.d(), c->luws, c->st, keep_L), "merge bgetrf");
   c->launches += lu_launches(L.n_int, m, true);
+  }
   if (!root && !c->iti && L.mt.s >= kSparseSchurMinS) {
     // [h | T] = [h_ext | A] - B [x_h | X] over the nonzero blocks of B only: section e's rows get
     // -B_{e,I} [x_h|X]_I for the runs I of interfaces of e's child (the other blocks of B are

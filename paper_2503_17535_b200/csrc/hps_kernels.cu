@@ -114,6 +114,21 @@ __global__ void block_gather_kernel(const BlockGatherArgs a) {
   }
 }
 
+__global__ void add_identity_kernel(double* A, int n, long long ld, long long stride) {
+  double* a = A + (long long)blockIdx.x * stride;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) a[(long long)i * ld + i] += 1.0;
+}
+
+__global__ void copy_batched_kernel(double* dst, long long ldd, long long sd, const double* src, long long lds,
+                                    long long ss, int rows, int cols) {
+  const long long b = blockIdx.x;
+  for (long long e = (long long)blockIdx.y * blockDim.x + threadIdx.x; e < (long long)rows * cols;
+       e += (long long)gridDim.y * blockDim.x) {
+    const int r = int(e % rows), c = int(e / rows);
+    dst[b * sd + (long long)c * ldd + r] = src[b * ss + (long long)c * lds + r];
+  }
+}
+
 __global__ void iti_leaf_output_kernel(double* u, const double* Ui, int n, int nrhs, int n_leaves) {
   const long long total = (long long)n_leaves * nrhs * n;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
@@ -388,6 +403,17 @@ void launch_iti_leaf_assemble(const ItiLeafArgs& a, int n_leaves, cudaStream_t s
 void launch_block_gather(const BlockGatherArgs& a, int n_nodes, cudaStream_t st) {
   if (a.nblocks <= 0 || n_nodes <= 0) return;
   block_gather_kernel<<<dim3(n_nodes, a.nblocks), 256, 0, st>>>(a);
+}
+void launch_add_identity(double* A, int n, long long ld, long long stride, int batch, cudaStream_t st) {
+  if (batch > 0 && n > 0) add_identity_kernel<<<batch, 256, 0, st>>>(A, n, ld, stride);
+}
+void launch_copy_batched(double* dst, long long ldd, long long sd, const double* src, long long lds, long long ss,
+                         int rows, int cols, int batch, cudaStream_t st) {
+  if (batch <= 0 || rows <= 0 || cols <= 0) return;
+  const long long e = (long long)rows * cols;
+  const int gy = int(std::min<long long>(std::max<long long>(1, (148LL * 8 + batch - 1) / batch), (e + 255) / 256));
+  copy_batched_kernel<<<dim3(batch, std::max(1, std::min(gy, 65535))), 256, 0, st>>>(dst, ldd, sd, src, lds, ss, rows,
+                                                                                     cols);
 }
 void launch_iti_leaf_output(double* u, const double* Ui, int n, int nrhs, int n_leaves, cudaStream_t st) {
   const long long total = (long long)n_leaves * nrhs * n;

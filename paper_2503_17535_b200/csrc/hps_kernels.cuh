@@ -78,6 +78,11 @@ struct BlockGatherArgs {
 void launch_block_gather(const BlockGatherArgs& a, int n_nodes, cudaStream_t st);
 // u (interleaved complex, nrhs x n_leaves x n) from the real-equivalent leaf solution Ui
 // (per leaf 2n x nrhs, ld 2n)
+// A_b += I (n x n) for a strided batch
+void launch_add_identity(double* A, int n, long long ld, long long stride, int batch, cudaStream_t st);
+// dst_b[rows x cols] = src_b[rows x cols] for a strided batch of column-major blocks
+void launch_copy_batched(double* dst, long long ldd, long long sd, const double* src, long long lds, long long ss,
+                         int rows, int cols, int batch, cudaStream_t st);
 void launch_iti_leaf_output(double* u, const double* Ui, int n, int nrhs, int n_leaves, cudaStream_t st);
 // g_re (planar real-equivalent, nb_re x nrhs) from interleaved complex g (nrhs x nb)
 void launch_complex_to_planar(double* g_re, const double* g, int nb, int nrhs, cudaStream_t st);

@@ -88,15 +88,18 @@ def test_node_artifacts_vs_reference_large_D(L):
             assert rel(a, b) < 1e-12
 
 
-ITI_TOL = 1e-9
+ITI_TOL = 5e-9
 
 
 def test_iti_vs_reference():
     """HpsSolver<Complex> (ItI, local_solve_iti / merge_iti) on the reference's own problem
     make_manufactured_2d_iti with the reference's boundary sampler (problems.cpp:76-107, 328-353).
-    Tolerance 1e-9: the product eliminates the merge interface with an LU of the full real-equivalent D,
-    the reference with the half-size W = I - D12 D21 (merge.cpp:447-463); both FP64-stable, measured
-    difference 3.9e-10 at L=3."""
+    Tolerance 5e-9 (measured 3.9e-10 at L=3, 1.9e-9 at L=4): both eliminate the merge interfaces through
+    W = I - D12 D21 (merge.cpp:447-463), but the product factors each leaf's complex B = [G; L(Ii,:)]
+    (local_solve.cpp:145-172) in real-equivalent form, whose row pivoting differs from the complex one; the
+    leaf rows mix impedance rows (~1e3) and interior collocation rows (~1e6), so the two roundoff
+    patterns differ at the ~1e-9 level of the L=4 build (the reference's own error vs the exact field is
+    1.0e-9 there, the product's 1.6e-9)."""
     fx = golden("ref_helmholtz_robin2d_p16_L3.npz")
     tree = H.build_uniform_tree(-1.0, 1.0, 3, 2, 16)
     pr = PR.helmholtz_robin2d(tree)
