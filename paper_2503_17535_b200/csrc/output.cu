@@ -3,8 +3,9 @@
 //                  leaf-major / point-minor, written to <bin>.tmp and renamed, then a JSON sidecar
 //                  {"dtype", "leaf_len", "n_leaves", "tree_ref"} the same way;
 //   mesh_to_json   (proj/src/mesh.cpp:435-463): {"dim", "nodes": [{"children", "depth", "hi", "id", "lo"}], "p", "q"}.
-// Both JSON texts are byte-identical to nlohmann::json::dump(1) (keys sorted, one-space indentation,
-// shortest round-trip doubles with ".0" on integral values), which the reference uses.
+// Both JSON texts are byte-identical to the reference's nlohmann::json::dump(1) output (keys sorted,
+// one-space indentation, shortest round-trip doubles with ".0" on integral values; the image's nlohmann
+// prints integer arrays on one line), checked against the reference build in tests/test_refine.py.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -68,8 +69,9 @@ extern "C" int hpsg_mesh_json(const hpsg_tree_desc* t, char* out, size_t cap, si
     std::vector<std::string> ch;
     if (t->n_children[i])
       for (int c = 0; c < nchild; ++c) ch.push_back(std::to_string(t->children[8 * i + c]));
-    n += indent(3) + "\"children\": ";
-    json_array(n, ch, 3);
+    n += indent(3) + "\"children\": [";  // this nlohmann build prints integer arrays on one line
+    for (size_t k = 0; k < ch.size(); ++k) n += (k ? "," : "") + ch[k];
+    n += "]";
     n += ",\n" + indent(3) + "\"depth\": " + std::to_string(t->depth[i]) + ",\n";
     std::vector<std::string> hi{json_double(t->hi[3 * i]), json_double(t->hi[3 * i + 1]), json_double(t->hi[3 * i + 2])};
     std::vector<std::string> lo{json_double(t->lo[3 * i]), json_double(t->lo[3 * i + 1]), json_double(t->lo[3 * i + 2])};

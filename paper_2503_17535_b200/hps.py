@@ -292,6 +292,20 @@ def bump_centers(seed, n=10, dim=2):
     return out.reshape(n, 3)
 
 
+def mesh_json(tree: GeneralTree) -> str:
+    """mesh_to_json (proj/src/mesh.cpp:435-463), byte-identical to the reference's output."""
+    L = lib()
+    L.hpsg_mesh_json.argtypes = [C.POINTER(_TreeDesc), C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
+    d = tree.desc()
+    n = C.c_size_t()
+    if L.hpsg_mesh_json(C.byref(d), None, 0, C.byref(n)) != HPSG_OK:
+        raise HpsError(HPSG_ERR_INVALID, "hpsg_mesh_json failed")
+    buf = C.create_string_buffer(n.value + 1)
+    if L.hpsg_mesh_json(C.byref(d), buf, n.value + 1, C.byref(n)) != HPSG_OK:
+        raise HpsError(HPSG_ERR_INVALID, "hpsg_mesh_json failed")
+    return buf.value.decode()
+
+
 def refine_adaptive(lo, hi, p, fields, tol=1e-3, max_depth=10, cap=1 << 20):
     """refine_adaptive(domain, RefinementCriterion{tol, p, test_fields}, max_depth) (proj/src/mesh.cpp:233-318)
     in 3D on [lo,hi]^3 with built-in fields -> (GeneralTree, n_unresolved)."""
@@ -561,6 +575,12 @@ class HpsSolver:
         self._check(lib().hpsg_get_node(self._h, node_id, _dp(S), _dp(gt), _dp(T), _dp(h)), "get_node")
         return (S.reshape(ni, ne, order="F") if S is not None else None, gt,
                 T.reshape(ne, ne, order="F") if T is not None else None, h)
+
+    def dump_solution(self, d_u_ptr, json_path, bin_path, tree_ref, is_complex=False):
+        """dump_solution (proj/src/downpass.cpp:108-143) of a device-resident solution."""
+        lib().hpsg_dump_solution.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_char_p, C.c_char_p, C.c_char_p]
+        self._check(lib().hpsg_dump_solution(self._h, C.c_void_p(d_u_ptr), int(is_complex), json_path.encode(),
+                                             bin_path.encode(), tree_ref.encode()), "dump_solution")
 
     def set_stream(self, stream_handle):
         """Run on a caller-owned cudaStream_t (int handle, e.g. torch.cuda.current_stream().cuda_stream)."""

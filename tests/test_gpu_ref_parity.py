@@ -146,3 +146,27 @@ def test_new_source_vs_reference():
         f = np.cos(2.0 * pts[..., 0]) * np.exp(pts[..., 1])
         g = np.cos(prob.boundary(r.root_points()))
         assert rel(s4.solve_new_source(f, g).reshape(r.n_leaves, -1), r.solve_new_source(f, g)) < TOL
+
+
+def test_dump_solution_matches_reference(tmp_path):
+    """dump_solution (downpass.cpp:108-143) of a device-resident solution: the JSON sidecar is
+    byte-identical to the reference's and the raw FP64 payload (leaf-major, point-minor) decodes to the
+    reference's field within the parity tolerance."""
+    import torch
+    fx = golden("ref_poisson2d_p16_L3.npz")
+    prob = PR.poisson2d()
+    s = gpu_dtn(prob, 16, 3, False)
+    g = torch.tensor(fx["g"], device="cuda")
+    u = torch.empty((s.n_leaves, s.npts), dtype=torch.float64, device="cuda")
+    s.solve_device(g.data_ptr(), 1, u.data_ptr())
+    s.dump_solution(u.data_ptr(), str(tmp_path / "u.json"), str(tmp_path / "u.bin"), "mesh.json")
+    got = np.fromfile(tmp_path / "u.bin", dtype="<f8").reshape(s.n_leaves, s.npts)
+    assert rel(got, fx["u"]) < TOL
+    text = (tmp_path / "u.json").read_text()
+    assert text == '{\n "dtype": "float64",\n "leaf_len": 256,\n "n_leaves": 64,\n "tree_ref": "mesh.json"\n}\n'
+    if LIVE:
+        r = ref_solver(prob, 16, 3)
+        r.build()
+        r.dump_solution(r.solve(fx["g"]), str(tmp_path / "r.json"), str(tmp_path / "r.bin"), "mesh.json")
+        assert (tmp_path / "r.json").read_text() == text
+        assert rel(np.fromfile(tmp_path / "r.bin", dtype="<f8").reshape(got.shape), got) < TOL

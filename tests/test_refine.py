@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from paper_2503_17535_b200 import problems as PR
-from paper_2503_17535_b200.hps import FIELD_CONST, FIELD_PB_EPS_GRAD, Field, refine_adaptive
+from paper_2503_17535_b200.hps import FIELD_CONST, FIELD_PB_EPS_GRAD, Field, mesh_json, refine_adaptive
 
 R = pytest.importorskip("oracle.ref")
 
@@ -70,3 +70,17 @@ def test_level_restriction_and_constant_field():
     assert max_face_gap(tr) <= 1                       # 2:1 restriction (SPEC acceptance 6)
     one, _ = refine_adaptive(0.0, 1.0, 8, [Field(FIELD_CONST, (3.0,))], tol=1e-6, max_depth=5)
     assert one.n_nodes == 1 and one.n_leaves == 1
+
+
+def test_mesh_json_equals_reference():
+    """mesh_to_json (mesh.cpp:435-463) of an adaptive tree and of a 2D uniform tree: the product's text is
+    byte-identical to the reference's (nlohmann dump(1))."""
+    if not R.available():
+        pytest.skip("reference build not available")
+    prob = PR.wavefront3d()
+    tr, _ = refine_adaptive(0.0, 1.0, 8, [prob.source], tol=1e-2, max_depth=5)
+    r = R.RefSolver(problem="wavefront3d", p=8, adaptive=True, tol=1e-2, max_depth=5)
+    assert mesh_json(tr) == r.mesh_json()
+    from tests.test_gpu_general import uniform_as_general
+    r2 = R.RefSolver(problem="poisson2d", p=16, L=2)
+    assert mesh_json(uniform_as_general(2, 16, 2, -1.0, 1.0)) == r2.mesh_json()
