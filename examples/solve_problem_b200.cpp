@@ -52,19 +52,14 @@ int main(int argc, char** argv) {
     solver.build();
     const auto t2 = std::chrono::steady_clock::now();
     const std::vector<Real> g = solver.sample_root_data(u);
-    hpsg_tree t{tree.dim, tree.p, tree.L, dom.lo[0], dom.hi[0]};
-    std::vector<double> xyz(size_t(tree.total_points()) * 3);
-    hpsg_tree_leaf_points(&t, xyz.data());
+    const std::vector<Point> pts = leaf_cheb_points(tree);
     SolutionField field;
     if (new_source) {
       const int np = p * p;
       std::vector<std::vector<Real>> leaf_f(size_t(tree.n_leaves()), std::vector<Real>(size_t(np)));
       for (long long l = 0; l < tree.n_leaves(); ++l)
         for (int i = 0; i < np; ++i) {
-          Point x;
-          const size_t k = size_t(l * np + i);
-          x[0] = xyz[3 * k], x[1] = xyz[3 * k + 1];
-          leaf_f[size_t(l)][size_t(i)] = f(x);
+          leaf_f[size_t(l)][size_t(i)] = f(pts[size_t(l * np + i)]);
         }
       field = solver.solve_new_source(leaf_f, RootBC::dirichlet, &g);
     } else {
@@ -76,9 +71,7 @@ int main(int argc, char** argv) {
     const int npts = p * p;
     for (long long l = 0; l < tree.n_leaves(); ++l)
       for (int i = 0; i < npts; ++i) {
-        Point x;
-        const size_t k = size_t(l * npts + i);
-        x[0] = xyz[3 * k], x[1] = xyz[3 * k + 1];
+        const Point& x = pts[size_t(l * npts + i)];
         num = std::fmax(num, std::fabs(field.u[size_t(l)][size_t(i)] - u(x)));
         den = std::fmax(den, std::fabs(u(x)));
       }

@@ -149,6 +149,19 @@ int hpsg_create_tree(const hpsg_tree_desc* tree, const hpsg_term* terms, int n_t
  * (proj/src/mesh.cpp:233-318, with enforce_level_restriction :141-167): 3D, built-in fields evaluated on the
  * host.  Writes the tree as node arrays in the reference's construction order (n_nodes x {depth, n_children,
  * children[8], lo[3], hi[3]}); returns HPSG_ERR_INVALID with *n_nodes set when cap is too small. */
+/* refine_adaptive with caller point functions (the reference's RefinementCriterion::test_fields,
+ * std::function<Real(const Point&)>, mesh.hpp:63-68): fns[i](users[i], x[3]). */
+typedef double (*hpsg_point_fn)(void* user, const double* x);
+int hpsg_refine_adaptive_cb(int p, const double* lo, const double* hi, double tol, int max_depth,
+                            hpsg_point_fn const* fns, void* const* users, int n_fields, int cap, int* n_nodes,
+                            int* depth, int* n_children, int* children, double* lo_out, double* hi_out,
+                            int* n_unresolved);
+/* enforce_level_restriction (mesh.cpp:141-167) of a tree: refinement only, node order kept, new nodes
+ * appended in the reference's split order. */
+int hpsg_enforce_level_restriction(const hpsg_tree_desc* tree, int cap, int* n_nodes, int* depth, int* n_children,
+                                   int* children, double* lo, double* hi);
+/* leaf_cheb_points of every leaf of a tree (DFS order, leaf-major; mesh.cpp:320-340) */
+int hpsg_tree_desc_leaf_points(const hpsg_tree_desc* tree, double* xyz);
 /* mesh_to_json (proj/src/mesh.cpp:435-463): the tree as the reference's JSON text (nlohmann dump(1) format,
  * byte-identical).  out == NULL: only *len (without the terminating 0) is set. */
 int hpsg_mesh_json(const hpsg_tree_desc* tree, char* out, size_t cap, size_t* len);

@@ -782,3 +782,101 @@ extern "C" int hpsg_refine_adaptive(int p, const double* lo, const double* hi, d
     return HPSG_ERR_INVALID;
   }
 }
+
+namespace {
+struct CbField {
+  hpsg_point_fn fn;
+  void* user;
+};
+double cb_field(const void* ctx, const double* x) {
+  const CbField* f = static_cast<const CbField*>(ctx);
+  return f->fn(f->user, x);
+}
+int write_tree(const hpsg::GTree& t, int cap, int* n_nodes, int* depth, int* n_children, int* children, double* lo,
+               double* hi) {
+  const int n = int(t.depth.size());
+  *n_nodes = n;
+  if (n > cap) return HPSG_ERR_INVALID;
+  for (int i = 0; i < n; ++i) {
+    if (depth) depth[i] = t.depth[i];
+    if (n_children) n_children[i] = t.nch[i];
+    for (int k = 0; k < 8; ++k)
+      if (children) children[8 * i + k] = t.child[i][k];
+    for (int k = 0; k < 3; ++k) {
+      if (lo) lo[3 * i + k] = t.lo[3 * i + k];
+      if (hi) hi[3 * i + k] = t.hi[3 * i + k];
+    }
+  }
+  return HPSG_OK;
+}
+hpsg::GTree read_tree(const hpsg_tree_desc* d) {
+  hpsg::GTree t;
+  t.dim = d->dim;
+  t.p = d->p;
+  const int n = d->n_nodes;
+  t.depth.assign(d->depth, d->depth + n);
+  t.nch.assign(d->n_children, d->n_children + n);
+  t.child.resize(n);
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < 8; ++k) t.child[i][k] = d->children[8 * i + k];
+  t.lo.assign(d->lo, d->lo + 3 * n);
+  t.hi.assign(d->hi, d->hi + 3 * n);
+  return t;
+}
+}  // namespace
+
+extern "C" int hpsg_refine_adaptive_cb(int p, const double* lo, const double* hi, double tol, int max_depth,
+                                       hpsg_point_fn const* fns, void* const* users, int n_fields, int cap,
+                                       int* n_nodes, int* depth, int* n_children, int* children, double* lo_out,
+                                       double* hi_out, int* n_unresolved) {
+  if (!lo || !hi || !fns || n_fields < 1 || !n_nodes || p < 4) return HPSG_ERR_INVALID;
+  try {
+    std::vector<CbField> f(n_fields);
+    std::vector<std::pair<hpsg::PointField, const void*>> pf;
+    for (int i = 0; i < n_fields; ++i) {
+      f[i] = {fns[i], users ? users[i] : nullptr};
+      pf.push_back({cb_field, &f[i]});
+    }
+    const hpsg::RefineResult r = hpsg::refine_adaptive(lo, hi, p, tol, max_depth, pf);
+    if (n_unresolved) *n_unresolved = int(r.unresolved.size());
+    return write_tree(r.tree, cap, n_nodes, depth, n_children, children, lo_out, hi_out);
+  } catch (const std::exception&) {
+    return HPSG_ERR_INVALID;
+  }
+}
+
+extern "C" int hpsg_enforce_level_restriction(const hpsg_tree_desc* in, int cap, int* n_nodes, int* depth,
+                                              int* n_children, int* children, double* lo, double* hi) {
+  if (!in || !n_nodes) return HPSG_ERR_INVALID;
+  try {
+    hpsg::GTree t = read_tree(in);
+    hpsg::finalize_gtree(t);
+    std::vector<long long> anchor(3 * t.depth.size(), 0);  // integer coordinates (TreeNode::anchor)
+    for (int d = 0; d <= t.max_depth(); ++d)
+      for (int id : t.levels[d])
+        for (int c = 0; c < t.nch[id]; ++c)
+          for (int k = 0; k < 3; ++k) {
+            static const int off[8][3] = {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {0, 1, 0},
+                                          {0, 0, 1}, {1, 0, 1}, {1, 1, 1}, {0, 1, 1}};
+            anchor[3 * t.child[id][c] + k] = k < t.dim ? 2 * anchor[3 * id + k] + off[c][k] : 0;
+          }
+    hpsg::enforce_level_restriction(t, anchor);
+    return write_tree(t, cap, n_nodes, depth, n_children, children, lo, hi);
+  } catch (const std::exception&) {
+    return HPSG_ERR_INVALID;
+  }
+}
+
+extern "C" int hpsg_tree_desc_leaf_points(const hpsg_tree_desc* d, double* xyz) {
+  if (!d || !xyz) return HPSG_ERR_INVALID;
+  try {
+    hpsg::GeneralPlan g;
+    g.tree = read_tree(d);
+    hpsg::finalize_gtree(g.tree);
+    const std::vector<double> pts = hpsg::general_leaf_points(g);
+    std::memcpy(xyz, pts.data(), pts.size() * 8);
+    return HPSG_OK;
+  } catch (const std::exception&) {
+    return HPSG_ERR_INVALID;
+  }
+}
