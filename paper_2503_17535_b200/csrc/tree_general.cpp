@@ -6,7 +6,9 @@
 #include <cmath>
 #include <map>
 #include <set>
+#include <exception>
 #include <stdexcept>
+#include <thread>
 
 namespace hpsg {
 
@@ -642,7 +644,11 @@ RefineResult refine_adaptive(const double* lo, const double* hi, int p, double t
   res.anchor = {0, 0, 0};
   MutTree m{t, res.anchor};
   // phase 1: independent per-field refinement
+  // (decisions for one field never depend on another field's samples, mesh.cpp:250-252: one host thread
+  // per field; the union below is order-independent)
   std::vector<FieldRefiner> refiners(fields.size());
+  std::vector<std::thread> pool;
+  std::vector<std::exception_ptr> errs(fields.size());
   for (size_t f = 0; f < fields.size(); ++f) {
     FieldRefiner& r = refiners[f];
     r.f = fields[f].first;
@@ -652,8 +658,17 @@ RefineResult refine_adaptive(const double* lo, const double* hi, int p, double t
     r.tol = tol;
     r.sup = 0.0;
     r.max_depth = max_depth;
-    r.refine(lo, hi, 0, {0, 0, 0}, r.sample(lo, hi));
+    pool.emplace_back([&r, &errs, f, lo, hi] {
+      try {
+        r.refine(lo, hi, 0, {0, 0, 0}, r.sample(lo, hi));
+      } catch (...) {
+        errs[f] = std::current_exception();
+      }
+    });
   }
+  for (auto& th : pool) th.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
   // union of the per-field trees
   std::set<std::pair<int, std::array<long long, 3>>> splits;
   for (const auto& r : refiners) splits.insert(r.want_split.begin(), r.want_split.end());

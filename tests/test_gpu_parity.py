@@ -457,3 +457,21 @@ def test_config4_3d_L4_parity():
     u = s.solve(g)
     assert rel(u, o.solve(g)) < 1e-10
     assert PR.rel_linf(u, prob.exact(s.leaf_points())) < 1e-7
+
+
+def test_cpp_adaptive_wavefront_example():
+    """examples/adaptive_wavefront_b200.cpp: the reference's adaptive 3D flow through the C++ drop-in
+    (refine_adaptive -> DiscretizationTree -> HpsSolver on the level-restricted octree, corrected sign)."""
+    import json
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "examples", "adaptive_wavefront_b200")
+    src = os.path.join(root, "examples", "adaptive_wavefront_b200.cpp")
+    if not os.path.exists(exe) or os.path.getmtime(exe) < os.path.getmtime(src):
+        subprocess.run(["make", "-s", "-C", os.path.join(root, "paper_2503_17535_b200"), "example"], check=True)
+    r = subprocess.run([exe, "8", "3e-4", "5"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    rep = json.loads(r.stdout)
+    assert rep["n_leaves"] == 456 and rep["top_D"] == 8208   # the reference's tree for this criterion
+    assert rep["rel_linf"] < 1e-3
