@@ -45,10 +45,14 @@ constexpr int kRowsPerLane = (kMaxNI + 31) / 32;
 #define HPS_LEAF_SUB 8
 #endif
 constexpr int kSub = HPS_LEAF_SUB;  // sub-panel width factored by one warp inside a panel
+static_assert(kSub % 4 == 0, "sub-panel width: multiple of 4 (register GEPP write-back rounds)");
 #ifndef HPS_LEAF_PAIR
 #define HPS_LEAF_PAIR 1
 #endif
 constexpr bool kPairGepp = HPS_LEAF_PAIR;  // two-warp sub-panel GEPP for panels taller than 64 rows
+#ifndef HPS_LEAF_REG_GEPP
+#define HPS_LEAF_REG_GEPP 1  // register-resident sub-panel (gepp_pair_regs); 0: shared-memory streaming
+#endif
 
 struct FusedSmem {
   LeafAsmSmemT<256, 16> asmb;
@@ -352,6 +356,137 @@ __device__ __forceinline__ void gepp_pair_body(FusedSmem& s, int rows, int sb, i
   if (threadIdx.x == 0) s.pmin = pmn, s.pmax = pmx, s.first_zero = fz;
 }
 
+// Register-resident two-warp sub-panel GEPP (same pivot rule and arithmetic as gepp_pair_body): the
+// sub-panel's rows live in registers (warp w owns the lane-strided row slots 2 qq + w) and are never
+// moved between threads during the elimination -- each slot carries its current row position, a pivot
+// exchange only swaps two positions, and the pivot row reaches the other slots through an 8-value shared
+// broadcast.  The composite row permutation is applied to the panel's other columns once at the end.
+// Per column: two 64-thread named barriers and no shared-memory streaming of the sub-panel.
+template <int NQH>
+__device__ __forceinline__ void gepp_pair_regs(FusedSmem& s, int rows, int sb, int se, int pnb, int j0) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int ncs = se - sb;
+  double v[NQH][kSub];
+  int pos[NQH], org[NQH];
+  bool act[NQH];  // valid and not yet a pivot
+#pragma unroll
+  for (int qq = 0; qq < NQH; ++qq) {
+    const int r = sb + lane + 32 * (2 * qq + w);
+    act[qq] = r < rows;
+    pos[qq] = r;
+    const int rr = min(r, rows - 1);
+    org[qq] = s.prow[rr];
+#pragma unroll
+    for (int c = 0; c < kSub; ++c) v[qq][c] = c < ncs ? s.pan[(sb + c) * kPLD + rr] : 0.0;
+  }
+  double pmn = s.pmin, pmx = s.pmax;
+  int fz = s.first_zero;
+#pragma unroll
+  for (int jj = 0; jj < kSub; ++jj) {
+    if (jj < ncs) {  // (no break: the loop must unroll so v[][jj] stays in registers)
+    const int j = sb + jj;
+    double bv = -1.0;
+    int bp = INT_MAX;
+#pragma unroll
+    for (int qq = 0; qq < NQH; ++qq) {
+      const double a = fabs(v[qq][jj]);
+      const double av = isnan(a) ? INFINITY : a;
+      if (act[qq] && (av > bv || (av == bv && pos[qq] < bp))) bv = av, bp = pos[qq];
+    }
+    {
+      const unsigned long long key = bv >= 0.0 ? (unsigned long long)__double_as_longlong(bv) : 0ull;
+      const unsigned hi = unsigned(key >> 32), lo = unsigned(key);
+      const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+      const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+      bp = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? bp : INT_MAX);
+      bv = bp == INT_MAX ? -1.0 : __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+    }
+    if (lane == 0) s.cv[w] = bv, s.cp[w] = bp;
+    pair_bar();
+    {
+      const double ov = s.cv[w ^ 1];
+      const int op = s.cp[w ^ 1];
+      if (ov > bv || (ov == bv && op < bp)) bv = ov, bp = op;
+    }
+    if (!(bv > 0.0) || !isfinite(bv)) {
+      if (fz < 0) fz = j0 + j;
+    } else {
+      pmn = fmin(pmn, bv);
+      pmx = fmax(pmx, bv);
+    }
+    // the pivot slot publishes its row; positions j and bp trade places
+#pragma unroll
+    for (int qq = 0; qq < NQH; ++qq) {
+      if (act[qq] && pos[qq] == bp) {
+#pragma unroll
+        for (int c = 0; c < kSub; ++c)
+          if (c >= jj) s.urow[c] = v[qq][c];
+      }
+    }
+#pragma unroll
+    for (int qq = 0; qq < NQH; ++qq) {
+      const int pq = pos[qq];
+      pos[qq] = pq == j ? bp : (pq == bp ? j : pq);
+      if (pos[qq] == j) act[qq] = false;  // the pivot slot now holds row j
+    }
+    pair_bar();
+    const double pv = s.urow[jj];
+    if (fabs(pv) > 0.0) {
+      const double rinv = pivot_rcp(pv);
+      double u[kSub];
+#pragma unroll
+      for (int c = 0; c < kSub; ++c) u[c] = c > jj && c < ncs ? s.urow[c] : 0.0;
+#pragma unroll
+      for (int qq = 0; qq < NQH; ++qq) {
+        if (act[qq]) {
+          const double l = v[qq][jj] * rinv;
+          v[qq][jj] = l;
+#pragma unroll
+          for (int c = 0; c < kSub; ++c)
+            if (c > jj) v[qq][c] -= l * u[c];
+        }
+      }
+    }
+    }
+  }
+  // write back: the sub-panel from registers; the panel's other columns get the same row permutation,
+  // four columns per round (read all, barrier, write all, barrier)
+#pragma unroll
+  for (int qq = 0; qq < NQH; ++qq) {
+    const int r = sb + lane + 32 * (2 * qq + w);
+    if (r < rows) s.prow[pos[qq]] = org[qq];
+  }
+  for (int c0 = 0; c0 < pnb; c0 += 4) {
+    if (c0 + 4 > sb && c0 < se) continue;  // sub-panel columns (kSub is a multiple of 4)
+    double t[NQH][4];
+#pragma unroll
+    for (int qq = 0; qq < NQH; ++qq) {
+      const int r = min(sb + lane + 32 * (2 * qq + w), rows - 1);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) t[qq][k] = c0 + k < pnb ? s.pan[(c0 + k) * kPLD + r] : 0.0;
+    }
+    pair_bar();
+#pragma unroll
+    for (int qq = 0; qq < NQH; ++qq) {
+      if (sb + lane + 32 * (2 * qq + w) < rows) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (c0 + k < pnb) s.pan[(c0 + k) * kPLD + pos[qq]] = t[qq][k];
+      }
+    }
+    pair_bar();
+  }
+#pragma unroll
+  for (int qq = 0; qq < NQH; ++qq) {
+    if (sb + lane + 32 * (2 * qq + w) < rows) {
+#pragma unroll
+      for (int c = 0; c < kSub; ++c)
+        if (c < ncs) s.pan[(sb + c) * kPLD + pos[qq]] = v[qq][c];
+    }
+  }
+  if (threadIdx.x == 0) s.pmin = pmn, s.pmax = pmx, s.first_zero = fz;
+}
+
 // GEPP of panel columns [j0, j0+pnb) over rows [j0, ni) of W by ONE warp on the panel staged in
 // s.pan (rows physically exchanged; lane-strided rows, no CTA barrier per column).  Pivot = max
 // |a| with NaN ranked as +inf, ties -> lowest current row (the LAPACK/Eigen rule).  Writes the
@@ -383,11 +518,19 @@ __device__ void panel_gepp_warp(FusedSmem& s, double* W, int ni, int j0, int pnb
     const int se = min(sb + kSub, pnb);
     if (kPairGepp && nq >= 3) {
       if (tid < 64) {
+#if HPS_LEAF_REG_GEPP
+        switch (nq) {
+          case 3: case 4: gepp_pair_regs<2>(s, rows, sb, se, pnb, j0); break;
+          case 5: case 6: gepp_pair_regs<3>(s, rows, sb, se, pnb, j0); break;
+          default: gepp_pair_regs<(kRowsPerLane + 1) / 2>(s, rows, sb, se, pnb, j0); break;
+        }
+#else
         switch (nq) {
           case 3: case 4: gepp_pair_body<2>(s, rows, sb, se, pnb, j0); break;
           case 5: case 6: gepp_pair_body<3>(s, rows, sb, se, pnb, j0); break;
           default: gepp_pair_body<(kRowsPerLane + 1) / 2>(s, rows, sb, se, pnb, j0); break;
         }
+#endif
       }
     } else if (tid < 32) {
       switch (nq) {
