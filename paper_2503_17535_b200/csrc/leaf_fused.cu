@@ -51,7 +51,8 @@ static_assert(kSub % 4 == 0, "sub-panel width: multiple of 4 (register GEPP writ
 #endif
 constexpr bool kPairGepp = HPS_LEAF_PAIR;  // two-warp sub-panel GEPP for panels taller than 64 rows
 #ifndef HPS_LEAF_REG_GEPP
-#define HPS_LEAF_REG_GEPP 1  // register-resident sub-panel (gepp_pair_regs); 0: shared-memory streaming
+#define HPS_LEAF_REG_GEPP 0  // 1: register-resident sub-panel (gepp_pair_regs): bit-identical, but measured
+                             // slower at the 128-register cap (leaf 104.6 -> 120.6 ms, spills); kept for study
 #endif
 
 struct FusedSmem {

@@ -25,7 +25,5 @@ for _ in range(3):
 g = prob.boundary(s.root_boundary_points())
 u = s.solve(g)
 err = PR.rel_linf(u, prob.exact(s.leaf_points()))
-os.makedirs("gpurun_out", exist_ok=True)
-np.save(f"gpurun_out/leaf_ab_u_{os.path.basename(path)}_{L}.npy", u)
 print(f"{os.path.basename(path)} L={L}: leaf ms {ts}, build ms {s.stats()['t_build_ms']:.1f}, "
-      f"rel_linf vs exact {err:.3e}", flush=True)
+      f"rel_linf vs exact {err:.3e}, checksum {float(np.abs(u).sum()):.17g} {float(u[::97].sum()):.17g}", flush=True)
