@@ -45,8 +45,8 @@ METRIC = "HPS build+solve seconds & DOF/s (2D p=16 L=8) at 1/2/4/8 B200; rel err
 PAPER_H100_DOFS = 16777216 / 4.02
 FP64_PEAK_TFLOPS = 37.155     # profiles/r01_fp64_peak.json (DMMA microbench; MEASURED_PEAKS.json has no FP64 entry)
 # dram__bytes_read.sum + dram__bytes_write.sum of one leaf_fused_kernel launch at p=16 L=8
-# (ncu --set full of the current kernel, profiles/r01_ncu_summary.md "v8")
-LEAF_KERNEL_DRAM_BYTES = 21.00e9 + 71.02e9
+# (ncu --set full of the current kernel, profiles/r02_ncu_summary.md)
+LEAF_KERNEL_DRAM_BYTES = 18.89e9 + 69.29e9
 
 
 def load_peaks():
