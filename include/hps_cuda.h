@@ -268,6 +268,35 @@ int hpsg_set_stream(hpsg_ctx* ctx, void* stream);
 const char* hpsg_last_error(hpsg_ctx* ctx);
 void hpsg_destroy(hpsg_ctx* ctx);
 
+/* ---- subtree-sharded build/solve over `world` ranks, one GPU each (replaces the
+ * single-process HpsSolver(tree, spec, opts) + build() + solve() of solver.cpp:33-252 when the caller
+ * runs one process per GPU).  The tree is cut at depth ds (smallest with nchild^ds >= world);
+ * depth-ds subtree k belongs to rank k*world/nchild^ds (a contiguous DFS leaf range, mesh.cpp:54-71);
+ * nodes above the cut are merged by the owner of their first subtree.  The only transfers are the
+ * [h|T] of a child whose owner differs from its parent's (upward, merge.cpp:226-278) and its boundary
+ * data (downward, solver.cpp:210-224), sent through the caller's transport on the shard's stream —
+ * typically ncclGroupStart / ncclSend / ncclRecv / ncclGroupEnd.  Every call is
+ * collective: all ranks call it in the same order.  Real (DtN) uniform trees only. */
+typedef struct {
+  void* user;
+  int (*group_begin)(void* user);                                     /* may be NULL */
+  int (*send)(void* user, const void* d_buf, size_t bytes, int peer, void* stream);
+  int (*recv)(void* user, void* d_buf, size_t bytes, int peer, void* stream);
+  int (*group_end)(void* user, void* stream);                         /* may be NULL */
+} hpsg_transport;
+typedef struct hpsg_shard hpsg_shard;
+/* tr may be NULL for world == 1; opts->device selects this rank's GPU */
+int hpsg_shard_create(const hpsg_tree* tree, const hpsg_term* terms, int n_terms, const hpsg_field* source,
+                      const hpsg_options* opts, int world, int rank, const hpsg_transport* tr, hpsg_shard** out);
+int hpsg_shard_build(hpsg_shard* s);
+/* d_g_root (nrhs x root_bsize, device) is read on the root owner (rank 0) only; d_u receives this rank's
+ * leaves: nrhs x n_leaves_here x p^dim (device), the leaves [first_leaf, first_leaf + n_leaves_here) of
+ * the DFS order */
+int hpsg_shard_solve_device(hpsg_shard* s, const double* d_g_root, int nrhs, double* d_u);
+int hpsg_shard_info(hpsg_shard* s, int* cut_depth, long long* first_leaf, long long* n_leaves_here);
+const char* hpsg_shard_last_error(hpsg_shard* s);
+void hpsg_shard_destroy(hpsg_shard* s);
+
 /* centers of the seeded Gaussian-bump fields: std::mt19937_64(seed) with
  * uniform_real_distribution(-0.5, 0.5), as make_scattering / make_pb_spec draw them
  * (proj/src/problems.cpp:126-141, :240-249).  out: n x 3 (z = 0 in 2D). */
