@@ -262,6 +262,7 @@ def run_b200(args):
         out["configs_extra"]["subtree_recompute_L9"] = bench_recompute(torch, args, 9, 2)
         out["configs_extra"]["planner_L9_80GB"] = bench_planner(args, 9, 80e9)
         out["configs_extra"]["config5_adaptive_3d"] = bench_adaptive(torch)
+        out["configs_extra"]["cpp_adapter_e2e_L8"] = bench_adapter_e2e(torch, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = reference_sample(args, prob)
         out["cpu_baseline_parallel_port"], par = parallel_port_baseline(args, prob, u_gpu)
@@ -440,6 +441,25 @@ def bench_3d(torch, L=4, p=8, steps=2):
            "counted_build_tflops": st["build_flops"] / st["t_build_ms"] / 1e9,
            "rel_linf_vs_exact": err, "device_gb": st["device_bytes"] / 1e9}
     s.close()
+    return out
+
+
+def bench_adapter_e2e(torch, args):
+    """The headline workload through the reference-facing C++ drop-in (include/hps/hps_b200.hpp) as a caller
+    of hps::HpsSolver<Real> writes it: std::function fields sampled on the host at all 16.8 M leaf points
+    (every host core), build(), sample_root_data(), solve() into the per-leaf SolutionField
+    (examples/adapter_e2e_b200.cpp, host clock).  The second of two runs is reported."""
+    exe = os.path.join(ROOT, "examples", "adapter_e2e_b200")
+    if not os.path.exists(exe):
+        return {"skipped": "examples/adapter_e2e_b200 not built (make -C paper_2503_17535_b200 example)"}
+    torch.cuda.empty_cache()
+    r = subprocess.run([exe, str(args.L), "2", "0"], capture_output=True, text=True, timeout=900)
+    if r.returncode != 0:
+        return {"error": (r.stderr or r.stdout)[-400:]}
+    rows = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    out = dict(rows[-1])
+    out["note"] = ("host clock; t_setup = tree + host sampling of 3 std::function fields + upload; t_solve includes "
+                   "sample_root_data, the H2D of g and the D2H of u into per-leaf vectors")
     return out
 
 

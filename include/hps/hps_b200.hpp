@@ -20,9 +20,12 @@
 #include <complex>
 #include <cstdint>
 #include <cstdio>
+#include <exception>
 #include <functional>
+#include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -287,6 +290,8 @@ struct SolverOptions {
   bool literal_sign = true;       // reference v_i = -L_ii^-1 f_i (local_solve.cpp:137)
   bool keep_factors = false;      // keep the leaf LU factors (LeafSolution::fac) for solve_new_source
   int device = 0;
+  int host_threads = 1;           // host threads sampling std::function fields (the reference samples
+                                  // serially; > 1 requires thread-safe callables, 0 = every core)
 };
 
 // proj/include/hps/solver.hpp:15
@@ -321,35 +326,75 @@ class HpsSolver {
     if (opts.build_root_T) throw Error("hps_b200: build_root_T is the ItI radiation closure (HpsSolverComplex)");
     tree.describe(desc_);
     const long long npts = tree.total_points();
-    // leaf Chebyshev points (leaf_cheb_points, DFS order), sampled like build_leaf/discretize_operator do on the host
-    std::vector<double> xyz(size_t(npts) * 3);
-    if (hpsg_tree_desc_leaf_points(&desc_.d, xyz.data()) != HPSG_OK) throw Error("hps_b200: invalid tree");
-    auto sample = [&](const std::function<Real(const Point&)>& fn) {
-      std::vector<double> s(static_cast<size_t>(npts));
-      for (long long i = 0; i < npts; ++i) {
-        Point x;
-        x[0] = xyz[3 * i], x[1] = xyz[3 * i + 1], x[2] = xyz[3 * i + 2];
-        s[size_t(i)] = fn(x);
+    // every field sampled at the leaf Chebyshev points (leaf_cheb_points, DFS order) as build_leaf /
+    // discretize_operator do on the host, in one pass over the leaves (each point is formed once, with the
+    // same expression as leaf_cheb_points), over host_threads threads
+    std::vector<const std::function<Real(const Point&)>*> fns;
+    for (const CoefficientField& f : terms) fns.push_back(&f.eval);
+    if (source) fns.push_back(&source);
+    std::vector<std::unique_ptr<double[]>> smp;
+    for (size_t i = 0; i < fns.size(); ++i) smp.emplace_back(new double[size_t(npts)]);
+    {
+      std::vector<double> cn(size_t(tree.p));
+      if (hpsg_cheb_nodes(tree.p, cn.data()) != HPSG_OK) throw Error("hps_b200: invalid tree");
+      const int np = tree.dim == 2 ? tree.p * tree.p : tree.p * tree.p * tree.p;
+      auto leaf_range = [&](long long l0, long long l1) {
+        std::vector<double> m(size_t(3 * tree.p));
+        for (long long l = l0; l < l1; ++l) {
+          const Box& b = tree.nodes[size_t(tree.leaves[size_t(l)])].box;
+          for (int k = 0; k < tree.dim; ++k)
+            for (int i = 0; i < tree.p; ++i)
+              m[size_t(k * tree.p + i)] = 0.5 * (b.lo[k] + b.hi[k]) + 0.5 * (b.hi[k] - b.lo[k]) * cn[size_t(i)];
+          const size_t base = size_t(l) * size_t(np);
+          for (int pt = 0; pt < np; ++pt) {
+            Point x;
+            if (tree.dim == 2) {
+              x[0] = m[size_t(pt / tree.p)], x[1] = m[size_t(tree.p + pt % tree.p)], x[2] = 0.0;
+            } else {
+              x[0] = m[size_t(pt / (tree.p * tree.p))], x[1] = m[size_t(tree.p + (pt / tree.p) % tree.p)];
+              x[2] = m[size_t(2 * tree.p + pt % tree.p)];
+            }
+            for (size_t f = 0; f < fns.size(); ++f) smp[f][base + size_t(pt)] = (*fns[f])(x);
+          }
+        }
+      };
+      const long long nl = tree.n_leaves();
+      const int nth = opts.host_threads > 0 ? opts.host_threads : int(std::max(1u, std::thread::hardware_concurrency()));
+      if (nth <= 1 || nl < 64) {
+        leaf_range(0, nl);
+      } else {
+        std::vector<std::thread> th;
+        std::vector<std::exception_ptr> err(static_cast<size_t>(nth));
+        const long long chunk = (nl + nth - 1) / nth;
+        for (int t = 0; t < nth; ++t)
+          th.emplace_back([&, t] {
+            try {
+              leaf_range(std::min(nl, t * chunk), std::min(nl, (t + 1) * chunk));
+            } catch (...) {
+              err[size_t(t)] = std::current_exception();
+            }
+          });
+        for (auto& x : th) x.join();
+        for (auto& e : err)
+          if (e) std::rethrow_exception(e);
       }
-      return s;
-    };
+    }
     std::vector<hpsg_term> ct;
-    for (const CoefficientField& f : terms) {
-      samples_.push_back(sample(f.eval));
+    for (size_t i = 0; i < terms.size(); ++i) {
+      const CoefficientField& f = terms[i];
       hpsg_term tt{};
       tt.role = static_cast<int>(f.role);
       tt.axis = f.axis;
       tt.axis2 = f.axis2;
       tt.field.kind = HPSG_FIELD_SAMPLED;
+      tt.field.samples = smp[i].get();
       ct.push_back(tt);
     }
-    for (size_t i = 0; i < ct.size(); ++i) ct[i].field.samples = samples_[i].data();
     hpsg_field src{};
     const hpsg_field* srcp = nullptr;
     if (source) {
-      src_samples_ = sample(source);
       src.kind = HPSG_FIELD_SAMPLED;
-      src.samples = src_samples_.data();
+      src.samples = smp.back().get();
       srcp = &src;
     }
     hpsg_options o{};
@@ -375,8 +420,6 @@ class HpsSolver {
       ctx_ = nullptr;
       throw Error(msg);
     }
-    samples_.clear();  // uploaded
-    src_samples_.clear();
   }
   HpsSolver(const HpsSolver&) = delete;
   HpsSolver& operator=(const HpsSolver&) = delete;
@@ -403,7 +446,9 @@ class HpsSolver {
 
   SolutionField solve(const std::vector<Real>& g_root, std::vector<std::vector<Real>>* leaf_g_out = nullptr) const {
     const long long nl = tree_->n_leaves();
-    if (g_root.size() != root_boundary_points().size()) throw Error("solve: boundary data of the wrong length");
+    hpsg_stats st{};
+    check(hpsg_get_stats(ctx_, &st));
+    if (g_root.size() != size_t(st.root_bsize)) throw Error("solve: boundary data of the wrong length");
     const int npts = tree_->dim == 2 ? tree_->p * tree_->p : tree_->p * tree_->p * tree_->p;
     const int nbl = 2 * tree_->dim * (tree_->dim == 2 ? tree_->q : tree_->q * tree_->q);
     std::vector<double> u(size_t(nl) * npts), lg;
@@ -512,8 +557,6 @@ class HpsSolver {
   DiscretizationTree::Desc desc_;
   SolverOptions opts_;
   hpsg_ctx* ctx_ = nullptr;
-  std::vector<std::vector<double>> samples_;
-  std::vector<double> src_samples_;
 };
 
 // proj/include/hps/solver.hpp:40-117 for S = Complex (Variant::iti, 2D): impedance-to-impedance

@@ -306,6 +306,9 @@ void hpsg_bump_centers(unsigned long long seed, int n, int dim, double* out);
  * tree in DFS order (n_leaves x p^dim x 3), so callers can sample std::function fields into
  * HPSG_FIELD_SAMPLED arrays before hpsg_create (mesh.cpp:320-336, solver.cpp:49-57). */
 int hpsg_tree_leaf_points(const hpsg_tree* tree, double* xyz);
+/* cheb_nodes(p) (proj/src/spectral.cpp:14-26): the p Chebyshev points on [-1, 1], descending from +1; a
+ * leaf's points are 0.5 (lo + hi) + 0.5 (hi - lo) t per axis (leaf_cheb_points, mesh.cpp:320-336) */
+int hpsg_cheb_nodes(int p, double* t);
 /* Host-only: root boundary points in canonical section order (root_bsize x 3), no device needed */
 int hpsg_tree_root_points(const hpsg_tree* tree, double* xyz);
 

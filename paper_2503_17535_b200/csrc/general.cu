@@ -873,8 +873,7 @@ extern "C" int hpsg_tree_desc_leaf_points(const hpsg_tree_desc* d, double* xyz) 
     hpsg::GeneralPlan g;
     g.tree = read_tree(d);
     hpsg::finalize_gtree(g.tree);
-    const std::vector<double> pts = hpsg::general_leaf_points(g);
-    std::memcpy(xyz, pts.data(), pts.size() * 8);
+    hpsg::general_leaf_points_into(g, xyz);
     return HPSG_OK;
   } catch (const std::exception&) {
     return HPSG_ERR_INVALID;

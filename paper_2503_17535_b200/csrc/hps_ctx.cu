@@ -1598,6 +1598,13 @@ int hpsg_tree_leaf_points(const hpsg_tree* t, double* xyz) {
   return HPSG_OK;
 }
 
+int hpsg_cheb_nodes(int p, double* t) {
+  if (p < 2 || !t) return HPSG_ERR_INVALID;
+  const std::vector<double> cn = hpsg::cheb_nodes(p);
+  std::copy(cn.begin(), cn.end(), t);
+  return HPSG_OK;
+}
+
 int hpsg_get_leaf(hpsg_ctx* c, int ord, double* Y, double* v, double* Tm, double* h) {
   if (!c) return HPSG_ERR_INVALID;
   if (c->gen) return fail(c, HPSG_ERR_STATE, "not available on general (adaptive) trees: uniform-tree entry point");

@@ -787,23 +787,35 @@ std::vector<double> general_root_points(const GeneralPlan& g) {
   return out;
 }
 
-std::vector<double> general_leaf_points(const GeneralPlan& g) {
+void general_leaf_points_into(const GeneralPlan& g, double* out) {
   const GTree& t = g.tree;
   const std::vector<double> cn = cheb_nodes(t.p);
-  std::vector<double> out;
-  for (int id : t.leaves) {
+  const int np = t.dim == 2 ? t.p * t.p : t.p * t.p * t.p;
+  std::vector<double> m(size_t(3 * t.p));
+  for (size_t l = 0; l < t.leaves.size(); ++l) {
+    const int id = t.leaves[l];
     const double* lo = &t.lo[3 * id];
     const double* hi = &t.hi[3 * id];
-    auto map1 = [&](double s, int k) { return 0.5 * (lo[k] + hi[k]) + 0.5 * (hi[k] - lo[k]) * s; };
+    for (int k = 0; k < 3; ++k)  // per-axis mapped nodes, same expression as leaf_cheb_points
+      for (int i = 0; i < t.p; ++i) m[size_t(k * t.p + i)] = 0.5 * (lo[k] + hi[k]) + 0.5 * (hi[k] - lo[k]) * cn[size_t(i)];
+    double* o = out + l * size_t(np) * 3;
     if (t.dim == 2) {
       for (int i1 = 0; i1 < t.p; ++i1)
-        for (int i2 = 0; i2 < t.p; ++i2) out.insert(out.end(), {map1(cn[i1], 0), map1(cn[i2], 1), 0.0});
+        for (int i2 = 0; i2 < t.p; ++i2, o += 3) o[0] = m[size_t(i1)], o[1] = m[size_t(t.p + i2)], o[2] = 0.0;
     } else {
       for (int i1 = 0; i1 < t.p; ++i1)
         for (int i2 = 0; i2 < t.p; ++i2)
-          for (int i3 = 0; i3 < t.p; ++i3) out.insert(out.end(), {map1(cn[i1], 0), map1(cn[i2], 1), map1(cn[i3], 2)});
+          for (int i3 = 0; i3 < t.p; ++i3, o += 3)
+            o[0] = m[size_t(i1)], o[1] = m[size_t(t.p + i2)], o[2] = m[size_t(2 * t.p + i3)];
     }
   }
+}
+
+std::vector<double> general_leaf_points(const GeneralPlan& g) {
+  const GTree& t = g.tree;
+  const size_t np = t.dim == 2 ? size_t(t.p) * t.p : size_t(t.p) * t.p * t.p;
+  std::vector<double> out(t.leaves.size() * np * 3);
+  general_leaf_points_into(g, out.data());
   return out;
 }
 

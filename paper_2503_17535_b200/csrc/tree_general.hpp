@@ -128,5 +128,6 @@ void enforce_level_restriction(GTree& t, std::vector<long long>& anchor);
 std::vector<double> general_root_points(const GeneralPlan& g);
 // Chebyshev points of every leaf (leaf-major, DFS order)
 std::vector<double> general_leaf_points(const GeneralPlan& g);
+void general_leaf_points_into(const GeneralPlan& g, double* out);
 
 }  // namespace hpsg

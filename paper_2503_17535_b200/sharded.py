@@ -253,9 +253,10 @@ def run_dist(shard: ShardedHps, g_root=None, nrhs=1, build=True, solve=True):
                 w.wait()
             for h, t in staged:
                 t.copy_(h)
-            if any(t.is_cuda for _, _, t in recvs):
-                # the C-ABI parts read received buffers through plain device pointers
-                torch.cuda.current_stream().synchronize()
+            # no host synchronisation: with NCCL, wait() orders the transfers before later work on
+            # torch's current stream, which is the stream every part of this rank runs on
+            # (CudaParts.make -> set_stream), so the merges that read the received buffers through
+            # plain device pointers queue behind them on the device
 
     if build:
         shard.build_local()
