@@ -97,6 +97,8 @@ typedef struct {
   /* execution choices (zero = the measured default; results agree to roundoff either way) */
   int force_batched_leaf;  /* 1: multi-launch batched leaf path instead of the persistent fused leaf kernel */
   int no_lu_lookahead;     /* 1: plain blocked LU driver instead of the look-ahead driver for n > 512 */
+  int force_lu_leaf;       /* 1: LU leaf solve even where the fast-diagonalisation leaf applies (constant
+                              Laplacian + zeroth-order terms, uniform 2D tree; leaf_fdm.cu) */
 } hpsg_options;
 enum { HPSG_VARIANT_DTN = 0, HPSG_VARIANT_ITI = 1 };
 
@@ -106,7 +108,8 @@ typedef struct {
   int root_bsize;              /* length of the root boundary vector */
   int top_D_size;              /* HpsSolver::top_D_size (solver.cpp:321-324) */
   int tree_depth;
-  double min_rcond;            /* min over leaves of min|u_ii|/max|u_ii| (local_solve.cpp:103-106) */
+  double min_rcond;            /* min over leaves of min|u_ii|/max|u_ii| (local_solve.cpp:103-106); fast-
+                                  diagonalisation leaves: min/max |lam_i + lam_j + cbar| of the leaf operator */
   int ill_conditioned;         /* any_ill_conditioned (solver.hpp:92) */
   double t_build_ms, t_leaf_ms, t_merge_ms, t_solve_ms;   /* last build / solve, CUDA events */
   double build_flops;          /* counted algorithmic FLOPs of the build (SURVEY 8d formulas) */
@@ -115,6 +118,8 @@ typedef struct {
   int launches_build, launches_solve; /* kernels launched by the last build / solve */
   int n_levels;                /* = tree depth L */
   double t_level_ms[24];       /* merge time of depth d (CUDA events), d = 0 .. L-1 */
+  int leaf_path;               /* last build's leaf stage: 0 fused LU kernel, 1 batched LU, 2 fast
+                                  diagonalisation, 3 fast diagonalisation that fell back to the fused LU */
 } hpsg_stats;
 
 typedef struct hpsg_ctx hpsg_ctx;

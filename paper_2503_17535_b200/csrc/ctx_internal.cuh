@@ -137,6 +137,11 @@ struct hpsg_ctx {
   DevBuf leafYv, leafScratch;  // fused leaf path
   bool fused = false;
   int fused_grid = 0;
+  // fast-diagonalisation leaf path (leaf_fdm.cu): eligible operators, 1D eigendecomposition, fallback flag
+  bool fdm = false;
+  int fdm_grid = 0;
+  double fdm_lap = 0.0;
+  DevBuf fdmV, fdmVinv, fdmA, fdmLam, fdmFail;  // fdmFail: count + list of non-converged leaves
   double* yv = nullptr;        // [v_i | Y_i] of leaf 0 (ni x (1+nb), ld ni)
   long long yv_stride = 0;
   // merges

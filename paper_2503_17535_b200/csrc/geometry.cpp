@@ -1,6 +1,7 @@
 // geometry.cpp -- host precompute for the B200 HPS solver (see geometry.hpp).
 #include "geometry.hpp"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -651,6 +652,158 @@ std::vector<double> root_boundary_points(const UniformTree& t) {
     collect(lo, hi, t.dim, f, t.L_full - t.root_depth, t.q, gx, out);
   }
   return out;
+}
+
+
+namespace {
+// x <- M^-1 b for a dense n x n M (column-major copy), partial pivoting; false if singular
+bool dense_solve(std::vector<double> M, int n, std::vector<double>& b) {
+  for (int k = 0; k < n; ++k) {
+    int r = k;
+    for (int i = k + 1; i < n; ++i)
+      if (std::fabs(M[size_t(k) * n + i]) > std::fabs(M[size_t(k) * n + r])) r = i;
+    if (M[size_t(k) * n + r] == 0.0) return false;
+    if (r != k) {
+      for (int j = 0; j < n; ++j) std::swap(M[size_t(j) * n + k], M[size_t(j) * n + r]);
+      std::swap(b[size_t(k)], b[size_t(r)]);
+    }
+    for (int i = k + 1; i < n; ++i) {
+      const double l = M[size_t(k) * n + i] / M[size_t(k) * n + k];
+      for (int j = k + 1; j < n; ++j) M[size_t(j) * n + i] -= l * M[size_t(j) * n + k];
+      b[size_t(i)] -= l * b[size_t(k)];
+    }
+  }
+  for (int k = n - 1; k >= 0; --k) {
+    double s = b[size_t(k)];
+    for (int j = k + 1; j < n; ++j) s -= M[size_t(j) * n + k] * b[size_t(j)];
+    b[size_t(k)] = s / M[size_t(k) * n + k];
+  }
+  return true;
+}
+}  // namespace
+
+bool real_eigendecomposition(const std::vector<double>& A, int n, std::vector<double>& lam, std::vector<double>& V,
+                             std::vector<double>& Vinv) {
+  auto at = [n](std::vector<double>& M, int i, int j) -> double& { return M[size_t(j) * n + i]; };
+  std::vector<double> H = A;
+  double anorm = 0.0;
+  for (double v : A) anorm = std::max(anorm, std::fabs(v));
+  if (!(anorm > 0.0) || !std::isfinite(anorm)) return false;
+  // Householder reduction to upper Hessenberg form
+  for (int k = 0; k + 2 < n; ++k) {
+    double alpha = 0.0;
+    for (int i = k + 1; i < n; ++i) alpha += at(H, i, k) * at(H, i, k);
+    alpha = std::sqrt(alpha);
+    if (alpha == 0.0) continue;
+    if (at(H, k + 1, k) > 0) alpha = -alpha;
+    std::vector<double> v(size_t(n), 0.0);
+    v[size_t(k + 1)] = at(H, k + 1, k) - alpha;
+    for (int i = k + 2; i < n; ++i) v[size_t(i)] = at(H, i, k);
+    double vn = 0.0;
+    for (double x : v) vn += x * x;
+    if (vn == 0.0) continue;
+    for (int j = 0; j < n; ++j) {  // H <- (I - 2vv'/v'v) H
+      double s = 0.0;
+      for (int i = k + 1; i < n; ++i) s += v[size_t(i)] * at(H, i, j);
+      s = 2.0 * s / vn;
+      for (int i = k + 1; i < n; ++i) at(H, i, j) -= s * v[size_t(i)];
+    }
+    for (int i = 0; i < n; ++i) {  // H <- H (I - 2vv'/v'v)
+      double s = 0.0;
+      for (int j = k + 1; j < n; ++j) s += at(H, i, j) * v[size_t(j)];
+      s = 2.0 * s / vn;
+      for (int j = k + 1; j < n; ++j) at(H, i, j) -= s * v[size_t(j)];
+    }
+  }
+  // shifted QR (Givens) on the active leading block; deflate from the bottom
+  lam.assign(size_t(n), 0.0);
+  int m = n - 1, iters = 0;
+  while (m >= 0) {
+    if (m == 0) {
+      lam[0] = at(H, 0, 0);
+      break;
+    }
+    const double sub = std::fabs(at(H, m, m - 1));
+    if (sub <= 1e-16 * (std::fabs(at(H, m, m)) + std::fabs(at(H, m - 1, m - 1)))) {
+      lam[size_t(m)] = at(H, m, m);
+      --m;
+      iters = 0;
+      continue;
+    }
+    if (++iters > 200) return false;
+    // Wilkinson shift: eigenvalue of the trailing 2x2 closest to H(m, m); complex pair -> no real decomposition
+    const double a = at(H, m - 1, m - 1), b = at(H, m - 1, m), c = at(H, m, m - 1), d = at(H, m, m);
+    const double tr = 0.5 * (a - d), disc = tr * tr + b * c;
+    if (disc < 0.0 && iters > 20) return false;
+    double mu = d;
+    if (disc >= 0.0) {
+      const double r = std::sqrt(disc);
+      mu = d - b * c / (tr + (tr >= 0 ? r : -r));
+      if (!std::isfinite(mu)) mu = d;
+    }
+    for (int i = 0; i <= m; ++i) at(H, i, i) -= mu;
+    std::vector<double> cs(static_cast<size_t>(m)), sn(static_cast<size_t>(m));
+    for (int k = 0; k < m; ++k) {  // H = QR
+      const double x = at(H, k, k), y = at(H, k + 1, k);
+      const double r = std::hypot(x, y);
+      const double cc = r == 0.0 ? 1.0 : x / r, ss = r == 0.0 ? 0.0 : y / r;
+      cs[size_t(k)] = cc, sn[size_t(k)] = ss;
+      for (int j = k; j <= m; ++j) {
+        const double t1 = at(H, k, j), t2 = at(H, k + 1, j);
+        at(H, k, j) = cc * t1 + ss * t2;
+        at(H, k + 1, j) = -ss * t1 + cc * t2;
+      }
+    }
+    for (int k = 0; k < m; ++k) {  // H = RQ
+      const double cc = cs[size_t(k)], ss = sn[size_t(k)];
+      for (int i = 0; i <= std::min(k + 1, m); ++i) {
+        const double t1 = at(H, i, k), t2 = at(H, i, k + 1);
+        at(H, i, k) = cc * t1 + ss * t2;
+        at(H, i, k + 1) = -ss * t1 + cc * t2;
+      }
+    }
+    for (int i = 0; i <= m; ++i) at(H, i, i) += mu;
+  }
+  std::vector<double> sorted = lam;
+  std::sort(sorted.begin(), sorted.end());
+  for (int i = 1; i < n; ++i)
+    if (!(std::fabs(sorted[size_t(i)] - sorted[size_t(i - 1)]) > 1e-10 * anorm)) return false;  // distinct
+  // eigenvectors by inverse iteration on the original matrix
+  V.assign(size_t(n) * n, 0.0);
+  for (int e = 0; e < n; ++e) {
+    std::vector<double> M = A;
+    const double shift = lam[size_t(e)] + 1e-12 * anorm;
+    for (int i = 0; i < n; ++i) M[size_t(i) * n + i] -= shift;
+    std::vector<double> x(size_t(n), 1.0);
+    for (int it = 0; it < 3; ++it) {
+      if (!dense_solve(M, n, x)) return false;
+      double mx = 0.0;
+      for (double v : x) mx = std::max(mx, std::fabs(v));
+      if (!(mx > 0.0) || !std::isfinite(mx)) return false;
+      for (double& v : x) v /= mx;
+    }
+    for (int i = 0; i < n; ++i) V[size_t(e) * n + i] = x[size_t(i)];
+  }
+  // V^-1 column by column, then the residual checks
+  Vinv.assign(size_t(n) * n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    std::vector<double> col(size_t(n), 0.0);
+    col[size_t(j)] = 1.0;
+    if (!dense_solve(V, n, col)) return false;
+    for (int i = 0; i < n; ++i) Vinv[size_t(j) * n + i] = col[size_t(i)];
+  }
+  double res = 0.0, idr = 0.0;
+  for (int i = 0; i < n; ++i)
+    for (int e = 0; e < n; ++e) {
+      double s = 0.0, t = 0.0;
+      for (int k = 0; k < n; ++k) {
+        s += A[size_t(k) * n + i] * V[size_t(e) * n + k];
+        t += Vinv[size_t(k) * n + i] * V[size_t(e) * n + k];
+      }
+      res = std::max(res, std::fabs(s - lam[size_t(e)] * V[size_t(e) * n + i]));
+      idr = std::max(idr, std::fabs(t - (i == e ? 1.0 : 0.0)));
+    }
+  return res <= 1e-11 * anorm && idr <= 1e-11;
 }
 
 }  // namespace hpsg

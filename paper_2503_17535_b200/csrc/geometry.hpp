@@ -44,6 +44,13 @@ struct LeafOperators {
 };
 LeafOperators make_leaf_operators(int dim, int p, double side);
 
+// A = V diag(lam) V^-1 for a small real matrix with real, distinct eigenvalues (n x n column-major; the
+// interior block of the Chebyshev second-derivative matrix for the fast-diagonalisation leaf solve).
+// Householder-Hessenberg + Wilkinson-shifted QR for lam, inverse iteration for V, Gauss-Jordan for V^-1.
+// Returns false (no decomposition) when an eigenvalue is complex or a residual check fails.
+bool real_eigendecomposition(const std::vector<double>& A, int n, std::vector<double>& lam, std::vector<double>& V,
+                             std::vector<double>& Vinv);
+
 // Uniform tree of depth L on [lo,hi]^dim.  Node ids follow the reference's
 // construction order (breadth-first by level; proj/src/mesh.cpp:113-118); for a
 // uniform tree the level order of tree.levels[d] (DFS) coincides with id order,

@@ -315,6 +315,51 @@ void setup(hpsg_ctx* c) {
   c->stats.min_rcond = 1.0;
 }
 
+// Fast-diagonalisation leaf path (leaf_fdm.cu): eligible when the operator is one constant Laplacian term
+// plus zeroth-order terms on a uniform 2D tree (the leaf operator is K + diag(c) with K = I (x) A + A (x) I the
+// same for every leaf).  A = s^2 (a D2[int, int]) with the rounding of leaf_entry; V, lam from the host
+// eigendecomposition (geometry.cpp), zero padded to 16 x 16 for the DMMA passes.
+void setup_fdm(hpsg_ctx* c) {
+  const hpsg::LeafOperators& o = c->ops;
+  if (c->tree.dim != 2 || c->iti || c->opts.keep_factors || !hpsk::leaf_fdm_shape_ok(o.p, o.ni, o.nb, 2)) return;
+  int nlap = 0;
+  double a = 0.0;
+  for (int i = 0; i < c->nterms; ++i) {
+    const hpsk::DevTerm& t = c->terms[i];
+    if (t.role == HPSG_ROLE_LAPLACIAN && t.f.kind == HPSG_FIELD_CONST) {
+      ++nlap;
+      a = t.f.c[0];
+    } else if (t.role != HPSG_ROLE_ZEROTH) {
+      return;
+    }
+  }
+  if (nlap != 1 || !(a != 0.0) || !std::isfinite(a)) return;
+  const int n1 = o.p - 2;
+  const double sc = 2.0 / c->T.leaf_side, s2 = sc * sc;
+  std::vector<double> A(size_t(n1) * n1), lam, V, Vi;
+  for (int j = 0; j < n1; ++j)
+    for (int i = 0; i < n1; ++i) A[size_t(j) * n1 + i] = s2 * (a * o.D2(i + 1, j + 1));
+  if (!hpsg::real_eigendecomposition(A, n1, lam, V, Vi)) return;
+  auto pad = [n1](const std::vector<double>& M) {
+    std::vector<double> out(256, 0.0);
+    for (int j = 0; j < n1; ++j)
+      for (int i = 0; i < n1; ++i) out[size_t(j) * 16 + i] = M[size_t(j) * n1 + i];
+    return out;
+  };
+  std::vector<double> lp(16, 0.0);
+  for (int i = 0; i < n1; ++i) lp[size_t(i)] = lam[size_t(i)];
+  upload(c->fdmV, pad(V), &c->dev_bytes, c->st);
+  upload(c->fdmVinv, pad(Vi), &c->dev_bytes, c->st);
+  upload(c->fdmA, pad(A), &c->dev_bytes, c->st);
+  upload(c->fdmLam, lp, &c->dev_bytes, c->st);
+  c->fdmFail.alloc(sizeof(int) * (1 + size_t(c->T.n_leaves())), &c->dev_bytes);
+  int nsm = 0;
+  ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->opts.device), "sm count");
+  c->fdm_grid = int(std::min<long long>(c->T.n_leaves(), (long long)nsm * hpsk::leaf_fdm_ctas_per_sm()));
+  c->fdm_lap = a;
+  c->fdm = true;
+}
+
 void alloc_build(hpsg_ctx* c) {
   const hpsg::LeafOperators& o = c->ops;
   const long long nl = c->T.n_leaves();
@@ -324,8 +369,11 @@ void alloc_build(hpsg_ctx* c) {
     if (c->terms[i].role == HPSG_ROLE_SECOND_ORDER && c->terms[i].axis != c->terms[i].axis2) mixed = true;
   c->fused = hpsk::leaf_fused_supported(o.n, o.p, o.ni, o.nb, c->tree.dim, mixed) && !c->opts.force_batched_leaf;
   if (c->opts.keep_factors || c->iti) c->fused = false;  // batched path: keeps [LU | v | Y] + pivots; ItI
+  if (c->T.cut) c->fused = false;  // no leaf stage: the part's leaves are input nodes
+  c->fdm = false;
+  if (c->fused && !c->opts.force_lu_leaf) setup_fdm(c);
   if (c->T.cut) {
-    c->fused = false;  // no leaf stage: the part's leaves are input nodes
+    // no leaf stage
   } else if (c->fused) {
     int nsm = 0;
     ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->opts.device), "sm count");
@@ -506,6 +554,39 @@ void run_leaf_stage(hpsg_ctx* c) {
     gemm(c, t);
     return;
   }
+  c->stats.leaf_path = c->fused ? 0 : 1;
+  const int* leaf_list = nullptr;
+  long long leaf_count = nl;
+  if (c->fdm) {
+    hpsk::LeafFdmArgs f{};
+    f.a = a;
+    f.P = c->P.d();
+    f.Qi = c->Qi.d();
+    f.ZQeP = c->ZQeP.d();
+    f.V = c->fdmV.d();
+    f.Vinv = c->fdmVinv.d();
+    f.A = c->fdmA.d();
+    f.lam = c->fdmLam.d();
+    f.lap_coef = c->fdm_lap;
+    f.Yv = c->leafYv.d();
+    f.strideYv = c->yv_stride;
+    f.HT = c->leafHT.d();
+    f.strideHT = c->strideLeafHT();
+    f.stats = c->leafStats.d();
+    f.fail_count = c->fdmFail.i();
+    f.fail_list = c->fdmFail.i() + 1;
+    f.n_leaves = nl;
+    ck(cudaMemsetAsync(c->fdmFail.p, 0, sizeof(int), c->st), "fdm flag");
+    ck(hpsk::launch_leaf_fdm(f, c->fdm_grid, c->st), "leaf_fdm");
+    ++c->launches;
+    int nfail = 0;  // the leaf-error check right after the stage synchronises anyway
+    ck(cudaMemcpyAsync(&nfail, c->fdmFail.p, sizeof(int), cudaMemcpyDeviceToHost, c->st), "fdm count D2H");
+    ck(cudaStreamSynchronize(c->st), "fdm sync");
+    c->stats.leaf_path = nfail ? 3 : 2;
+    if (!nfail) return;
+    leaf_list = c->fdmFail.i() + 1;  // non-converged leaves: the fused LU kernel solves exactly those
+    leaf_count = nfail;
+  }
   if (c->fused) {
     hpsk::LeafFusedArgs f{};
     f.a = a;
@@ -519,7 +600,8 @@ void run_leaf_stage(hpsg_ctx* c) {
     f.HT = c->leafHT.d();
     f.strideHT = c->strideLeafHT();
     f.stats = c->leafStats.d();
-    f.n_leaves = nl;
+    f.n_leaves = leaf_count;
+    f.leaf_list = leaf_list;
 #ifdef HPS_LEAF_PROFILE  // developer build (-DHPS_LEAF_PROFILE): per-phase clock64 stamps of CTA 0
     {
       static DevBuf prof;
@@ -546,8 +628,7 @@ void run_leaf_stage(hpsg_ctx* c) {
               h[42], h[43]);
     }
 #endif
-    f.n_leaves = nl;
-    ck(hpsk::launch_leaf_fused(f, c->fused_grid, c->st), "leaf_fused");
+    ck(hpsk::launch_leaf_fused(f, int(std::min<long long>(c->fused_grid, leaf_count)), c->st), "leaf_fused");
     ++c->launches;
     return;
   }

@@ -128,12 +128,38 @@ struct LeafFusedArgs {
   long long strideHT;
   double* stats;            // per leaf: min|u_ii|, max|u_ii|, first zero pivot (-1)
   long long* prof;          // optional phase timestamps (clock64) of CTA 0: [leaf_iter][8]
-  long long n_leaves;
+  long long n_leaves;       // leaves to solve: all, or the first n_leaves entries of leaf_list
+  const int* leaf_list;     // optional: the leaves to solve (the fast-diagonalisation path's non-converged ones)
 };
 bool leaf_fused_supported(int n, int p, int ni, int nb, int dim, bool mixed_terms);
 int leaf_fused_ctas_per_sm();
 long long leaf_fused_scratch_per_cta(int ni, int ne, int nb);
 cudaError_t launch_leaf_fused(const LeafFusedArgs& f, int grid, cudaStream_t st);
+
+// Fast-diagonalisation leaf solve (leaf_fdm.cu) for a constant Laplacian plus zeroth-order terms on a
+// uniform 2D tree: same outputs as leaf_fused_kernel ([v_i | Y_i], [h | T], statistics), no LU.
+struct LeafFdmArgs {
+  LeafAsmArgs a;            // fields, geometry, bad_point; M/E unused
+  const double* P;          // ne x nb
+  const double* Qi;         // nb x ni
+  const double* ZQeP;       // nb x (1 + nb)
+  const double* V;          // 16 x 16 col-major, zero padded: eigenvectors of the 1D interior operator
+  const double* Vinv;       // 16 x 16
+  const double* A;          // 16 x 16: the 1D interior operator s^2 (a D2[int, int]), zero padded
+  const double* lam;        // 16: its eigenvalues (0 in the padding)
+  double lap_coef;          // a (the constant Laplacian coefficient)
+  double* Yv;
+  long long strideYv;
+  double* HT;
+  long long strideHT;
+  double* stats;            // per leaf: min / max |lam_i + lam_j + cbar|, -1
+  int* fail_count;          // leaves that did not converge: count and list (the host re-runs them with
+  int* fail_list;           // the LU leaf kernel, so every leaf's result is independent of its neighbours)
+  long long n_leaves;
+};
+bool leaf_fdm_shape_ok(int p, int ni, int nb, int dim);
+int leaf_fdm_ctas_per_sm();
+cudaError_t launch_leaf_fdm(const LeafFdmArgs& f, int grid, cudaStream_t st);
 
 // ---- stage 2: merge operand gather ------------------------------------------
 // Reference block assembly, proj/src/merge.cpp:226-278: child DtN blocks summed

@@ -1,0 +1,366 @@
+// leaf_fdm.cu -- stage 1 (leaf-local solves) by fast diagonalisation, for operators whose second-order part
+// is a constant Laplacian (a * Delta + c(x), any zeroth-order terms): the Helmholtz-type problems of the
+// headline configuration.  One persistent kernel; the result is the reference's local solve
+// (proj/src/local_solve.cpp:111-143: [v_i | Y_i] = L_ii^-1 [sgn f_i | -L_ie P], [h | T] = Q_i [v_i | Y_i] +
+// [0 | Q_e P]) to roundoff, computed without an LU.
+//
+// On a uniform 2D tree every leaf has the same L_ii = K + diag(c), K = I (x) A + A (x) I with the 1D
+// interior operator A = a (2/side)^2 D2[int, int] = V diag(lam) V^-1 (host eigendecomposition,
+// geometry.cpp).  Per leaf, with cbar = (min c + max c) / 2 and K_c = K + cbar I (applied exactly through
+// V: K_c^-1 U = V ((V^-1 U V^-T) / (lam_i + lam_j + cbar)) V^T on the 14 x 14 grid of a right-hand side),
+// preconditioned Richardson on the TRUE operator
+//     X_0 = K_c^-1 R,   X_{k+1} = X_k + K_c^-1 (R - K X_k - c o X_k)
+// converges with rate rho = ||K_c^-1 (c - cbar)|| (about 1e-5 for the headline leaves: c varies by < 30
+// across a leaf, the smallest |lam_i + lam_j| is 3.2e5), and its fixed point is L_ii^-1 R whatever the
+// rounding of V.  A right-hand side stops when the predicted remaining error rho / (1 - rho) ||dX|| is
+// below 1e-15 ||X|| (typically after 2-3 steps); a leaf that does not converge in kMaxSteps (resonant or
+// strongly varying coefficients) raises the fail flag, and the host re-runs the LU leaf kernel.
+//
+// Data layout: every right-hand side is a 16 x 16 block (the 14 x 14 grid, zero padded) in shared memory,
+// XOR-swizzled per column so DMMA fragment loads are conflict-free.  A warp owns whole blocks, so all
+// passes of one right-hand side run without CTA barriers; each pass is "left-multiply by a 16 x 16 matrix
+// held in registers (16 DMMA.8x8x4), store the block transposed", so two passes apply M U M^T.
+#include <cfloat>
+#include <climits>
+
+#include "leaf_common.cuh"
+
+namespace hpsk {
+
+namespace {
+
+constexpr int kT = 256, kW = kT / 32;
+constexpr int kNC = 16;     // right-hand sides per chunk (one block each, two per warp)
+constexpr int kBlk = 256;   // 16 x 16 doubles
+constexpr int kMaxSteps = 12;
+#ifndef HPS_FDM_TOL
+#define HPS_FDM_TOL 1e-18
+#endif
+constexpr double kTol = HPS_FDM_TOL;  // predicted remaining error / max|X| at which a right-hand side stops
+
+struct FdmSmem {
+  double R[kNC * kBlk], X[kNC * kBlk], W[kNC * kBlk];
+  double cz[kBlk];   // zeroth-order coefficient at the interior points (block layout), 0 in the padding
+  double den[kBlk];  // 1 / (lam_row + lam_col + cbar), 0 in the padding
+  double fsrc[256];
+  int pos[256];      // tensor index -> interior r (>= 0) or -(exterior position) - 1
+  double wmin[kW], wmax[kW];
+  int bad;
+  int failed;        // this leaf did not converge
+};
+
+// element (row, col) of a block: column-major 16 x 16, rows XOR-swizzled by the column
+HPS_DEV int swz(int row, int col) { return (col << 4) + (row ^ ((col & 3) << 2)); }
+
+HPS_DEV void load_afrag(const double* M, double (&am)[2][4], int g, int t4) {
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) am[mt][ks] = M[(ks * 4 + t4) * 16 + mt * 8 + g];
+}
+
+// acc = M In, M from registers; In(k, n) read at swz(k, n) (TRANS = false) or swz(n, k) (TRANS = true).
+// acc[mt][nt][h] is element (mt * 8 + g, nt * 8 + 2 t4 + h).  Ends with __syncwarp: the block may be
+// overwritten in place after the call.
+template <bool TRANS>
+HPS_DEV void mma_block(const double (&am)[2][4], const double* in, double (&acc)[2][2][2], int g, int t4) {
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    double b[2];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) b[nt] = TRANS ? in[swz(nt * 8 + g, ks * 4 + t4)] : in[swz(ks * 4 + t4, nt * 8 + g)];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], am[mt][ks], b[nt]);
+  }
+  __syncwarp();
+}
+
+// store acc transposed: element (m, n) to position (n, m), optionally scaled by den at that position
+template <bool SCALE>
+HPS_DEV void store_t(double* out, const double (&acc)[2][2][2], const double* den, int g, int t4) {
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int m = mt * 8 + g, n0 = nt * 8 + 2 * t4;
+      const int p = swz(n0, m);  // (n0, m) and (n0 + 1, m) are adjacent
+      double2 v = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+      if (SCALE) {
+        const double2 d = *reinterpret_cast<const double2*>(den + p);
+        v.x *= d.x;
+        v.y *= d.y;
+      }
+      *reinterpret_cast<double2*>(out + p) = v;
+    }
+  __syncwarp();
+}
+
+HPS_DEV double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Solve one right-hand side block: X <- L_ii^-1 R.  Returns false if it did not converge.
+HPS_DEV bool solve_block(const double* Rb, double* Xb, double* Wb, const FdmSmem& s, const double (&vi)[2][4],
+                         const double (&vv)[2][4], const double (&aa)[2][4], int g, int t4) {
+  double acc[2][2][2];
+  // X_0 = K_c^-1 R
+  mma_block<false>(vi, Rb, acc, g, t4);
+  store_t<false>(Wb, acc, nullptr, g, t4);
+  mma_block<false>(vi, Wb, acc, g, t4);
+  store_t<true>(Wb, acc, s.den, g, t4);
+  mma_block<false>(vv, Wb, acc, g, t4);
+  store_t<false>(Wb, acc, nullptr, g, t4);
+  mma_block<false>(vv, Wb, acc, g, t4);
+  double xm = 0.0;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) xm = fmax(xm, fmax(fabs(acc[mt][nt][0]), fabs(acc[mt][nt][1])));
+  store_t<false>(Xb, acc, nullptr, g, t4);
+  double dprev = warp_max(xm), xmax = dprev, rbest = 1.0;
+  if (dprev == 0.0) return true;
+  for (int step = 0; step < kMaxSteps; ++step) {
+    // W = R - A X - X A^T - c o X  (the residual of the true operator)
+    mma_block<false>(aa, Xb, acc, g, t4);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) Wb[swz(mt * 8 + g, nt * 8 + 2 * t4 + h)] = acc[mt][nt][h];
+    __syncwarp();
+    mma_block<true>(aa, Xb, acc, g, t4);  // (A X^T)(m, n) = (X A^T)(n, m)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int p = swz(nt * 8 + 2 * t4, mt * 8 + g);
+        const double2 r = *reinterpret_cast<const double2*>(Rb + p);
+        const double2 w = *reinterpret_cast<const double2*>(Wb + p);
+        const double2 x = *reinterpret_cast<const double2*>(Xb + p);
+        const double2 c = *reinterpret_cast<const double2*>(s.cz + p);
+        double2 o;
+        o.x = r.x - w.x - acc[mt][nt][0] - c.x * x.x;
+        o.y = r.y - w.y - acc[mt][nt][1] - c.y * x.y;
+        *reinterpret_cast<double2*>(Wb + p) = o;
+      }
+    __syncwarp();
+    // dX = K_c^-1 W; X += dX
+    mma_block<false>(vi, Wb, acc, g, t4);
+    store_t<false>(Wb, acc, nullptr, g, t4);
+    mma_block<false>(vi, Wb, acc, g, t4);
+    store_t<true>(Wb, acc, s.den, g, t4);
+    mma_block<false>(vv, Wb, acc, g, t4);
+    store_t<false>(Wb, acc, nullptr, g, t4);
+    mma_block<false>(vv, Wb, acc, g, t4);
+    double dm = 0.0;
+    xm = 0.0;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int p = swz(nt * 8 + 2 * t4, mt * 8 + g);
+        double2 x = *reinterpret_cast<const double2*>(Xb + p);
+        x.x += acc[mt][nt][0];
+        x.y += acc[mt][nt][1];
+        *reinterpret_cast<double2*>(Xb + p) = x;
+        dm = fmax(dm, fmax(fabs(acc[mt][nt][0]), fabs(acc[mt][nt][1])));
+        xm = fmax(xm, fmax(fabs(x.x), fabs(x.y)));
+      }
+    __syncwarp();
+    const double dk = warp_max(dm);
+    xmax = warp_max(xm);
+    if (dk == 0.0) return true;
+    const double rho = dk / dprev;
+    if (rho < 0.5 && rho / (1.0 - rho) * dk <= kTol * xmax) return true;
+    if (dk <= 2e-15 * xmax && rbest < 0.5) return true;  // at the roundoff floor after a measured contraction
+    rbest = fmin(rbest, rho);
+    dprev = dk;
+  }
+  return false;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kT, 2) leaf_fdm_kernel(const LeafFdmArgs f) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FdmSmem& s = *reinterpret_cast<FdmSmem*>(smem_raw);
+  const LeafAsmArgs& a = f.a;
+  const int p = a.p, n = a.n, ni = a.ni, ne = a.ne, nb = a.nb, n1 = p - 2, ncol = 1 + nb;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
+  const double s2 = a.scale * a.scale, clap = f.lap_coef;
+  double vi[2][4], vv[2][4], aa[2][4];
+  load_afrag(f.Vinv, vi, g, t4);
+  load_afrag(f.V, vv, g, t4);
+  load_afrag(f.A, aa, g, t4);
+  for (int r = tid; r < ni; r += kT) s.pos[a.interior[r]] = r;
+  for (int r = tid; r < ne; r += kT) s.pos[a.exterior[r]] = -r - 1;
+  __syncthreads();
+
+  for (long long leaf = blockIdx.x; leaf < f.n_leaves; leaf += gridDim.x) {
+    // ---- coefficients and source at the leaf points (leaf_cheb_points, discretize_operator's sampling)
+    if (tid == 0) s.bad = INT_MAX;
+    for (int e = tid; e < kBlk; e += kT) s.cz[e] = 0.0;
+    __syncthreads();
+    const double* box = a.leaf_box + leaf * 6;
+    double cmin = DBL_MAX, cmax = -DBL_MAX;
+    for (int i = tid; i < n; i += kT) {
+      const int i1 = i / p, i2 = i % p;
+      double x[3] = {0.0, 0.0, 0.0};
+      x[0] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(box[0], box[3])), __dmul_rn(__dmul_rn(0.5, __dsub_rn(box[3], box[0])), a.cheb[i1]));
+      x[1] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(box[1], box[4])), __dmul_rn(__dmul_rn(0.5, __dsub_rn(box[4], box[1])), a.cheb[i2]));
+      double cz = 0.0;
+      for (int t = 0; t < a.nterms; ++t) {
+        const double v = eval_field_t<2>(a.terms[t].f, x, leaf, i, n);
+        if (!isfinite(v)) atomicMin(&s.bad, i);
+        if (a.terms[t].role == 2) cz = __dadd_rn(cz, v);
+      }
+      s.fsrc[i] = a.has_source ? eval_field_t<2>(a.source, x, leaf, i, n) : 0.0;
+      const int r = s.pos[i];
+      if (r >= 0) {
+        s.cz[swz(r % n1, r / n1)] = cz;
+        cmin = fmin(cmin, cz);
+        cmax = fmax(cmax, cz);
+      }
+    }
+    cmin = -warp_max(-cmin);
+    cmax = warp_max(cmax);
+    if (lane == 0) s.wmin[warp] = cmin, s.wmax[warp] = cmax;
+    __syncthreads();
+    cmin = s.wmin[0], cmax = s.wmax[0];
+    for (int w = 1; w < kW; ++w) cmin = fmin(cmin, s.wmin[w]), cmax = fmax(cmax, s.wmax[w]);
+    const double cbar = 0.5 * (cmin + cmax);
+    double dmin = DBL_MAX, dmax = 0.0;
+    for (int e = tid; e < kBlk; e += kT) {
+      const int col = e >> 4, row = (e & 15) ^ ((col & 3) << 2);
+      double d = 0.0;
+      if (row < n1 && col < n1) {
+        const double ev = f.lam[row] + f.lam[col] + cbar;
+        d = 1.0 / ev;
+        dmin = fmin(dmin, fabs(ev));
+        dmax = fmax(dmax, fabs(ev));
+      }
+      s.den[e] = d;
+    }
+    dmin = -warp_max(-dmin);
+    dmax = warp_max(dmax);
+    __syncthreads();  // everyone read s.wmin/wmax
+    if (lane == 0) s.wmin[warp] = dmin, s.wmax[warp] = dmax;
+    __syncthreads();
+    dmin = s.wmin[0], dmax = s.wmax[0];
+    for (int w = 1; w < kW; ++w) dmin = fmin(dmin, s.wmin[w]), dmax = fmax(dmax, s.wmax[w]);
+    bool ok = s.bad == INT_MAX && dmin > 1e-12 * dmax && isfinite(cbar);
+    if (tid == 0) {
+      a.bad_point[leaf] = s.bad;
+      f.stats[3 * leaf + 0] = dmin;  // spectral analogue of the pivot statistics: min / max |lam_i + lam_j + cbar|
+      f.stats[3 * leaf + 1] = dmax;
+      f.stats[3 * leaf + 2] = -1.0;
+    }
+    if (!ok) {  // non-finite samples (reported by the host) or a resonant leaf: the LU path takes over
+      if (tid == 0 && s.bad == INT_MAX) f.fail_list[atomicAdd(f.fail_count, 1)] = int(leaf);
+      __syncthreads();
+      continue;
+    }
+    if (tid == 0) s.failed = 0;
+
+    for (int c0 = 0; c0 < ncol; c0 += kNC) {
+      // ---- right-hand sides [sgn f_i | -L_ie P] of this chunk, X = 0
+      for (int e = tid; e < kNC * kBlk; e += kT) {
+        const int b = e >> 8, q = e & 255, col = q >> 4, row = (q & 15) ^ ((col & 3) << 2);
+        const int rc = c0 + b;
+        double v = 0.0;
+        if (row < n1 && col < n1 && rc < ncol) {
+          const int i1 = col + 1, i2 = row + 1;
+          if (rc == 0) {
+            v = a.fsign * s.fsrc[i1 * p + i2];
+          } else {
+            // the row's exterior line neighbours in slot order (axis 0 node 0 / p-1, axis 1 node 0 / p-1),
+            // entries s^2 (a D2(i, j)) as leaf_entry rounds them
+            const double* Pj = f.P + (long long)(rc - 1) * ne;
+            double acc = 0.0;
+            acc += __dmul_rn(s2, __dmul_rn(clap, a.D2[0 * p + i1])) * Pj[-s.pos[0 * p + i2] - 1];
+            acc += __dmul_rn(s2, __dmul_rn(clap, a.D2[(p - 1) * p + i1])) * Pj[-s.pos[(p - 1) * p + i2] - 1];
+            acc += __dmul_rn(s2, __dmul_rn(clap, a.D2[0 * p + i2])) * Pj[-s.pos[i1 * p + 0] - 1];
+            acc += __dmul_rn(s2, __dmul_rn(clap, a.D2[(p - 1) * p + i2])) * Pj[-s.pos[i1 * p + p - 1] - 1];
+            v = -acc;
+          }
+        }
+        s.R[e] = v;
+      }
+      __syncthreads();
+      // ---- per right-hand side: fast-diagonalisation Richardson (warp-local)
+      bool conv = true;
+      for (int b = warp; b < kNC; b += kW)
+        if (c0 + b < ncol) conv = solve_block(s.R + b * kBlk, s.X + b * kBlk, s.W + b * kBlk, s, vi, vv, aa, g, t4) && conv;
+      if (!conv && lane == 0) s.failed = 1;
+      __syncthreads();
+      // ---- outputs of the chunk: [v_i | Y_i] columns, and [h | T] = Q_i X + [0 | Q_e P] (DMMA, Q_i from L2)
+      double* Yv = f.Yv + leaf * f.strideYv;
+      for (int e = tid; e < kNC * ni; e += kT) {
+        const int b = e / ni, r = e - b * ni;
+        if (c0 + b < ncol) __stcs(&Yv[(long long)(c0 + b) * ni + r], s.X[b * kBlk + swz(r % n1, r / n1)]);
+      }
+      const int mtiles = (nb + 7) / 8;
+      if (warp < mtiles) {
+        const int m0 = warp * 8;
+        double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        for (int k0 = 0; k0 < ni; k0 += 4) {
+          const int k = k0 + t4;
+          const double av = (k < ni && m0 + g < nb) ? f.Qi[(long long)k * nb + m0 + g] : 0.0;
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const double bv = k < ni ? s.X[(nt * 8 + g) * kBlk + swz(k % n1, k / n1)] : 0.0;
+            dmma_8x8x4(acc[nt][0], acc[nt][1], av, bv);
+          }
+        }
+        double* HT = f.HT + leaf * f.strideHT;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int col = c0 + nt * 8 + 2 * t4 + h, m = m0 + g;
+            if (col < ncol && m < nb)
+              __stcs(&HT[(long long)col * nb + m], acc[nt][h] + f.ZQeP[(long long)col * nb + m]);
+          }
+      }
+      __syncthreads();
+    }
+    if (tid == 0 && s.failed) f.fail_list[atomicAdd(f.fail_count, 1)] = int(leaf);
+  }
+}
+
+bool leaf_fdm_shape_ok(int p, int ni, int nb, int dim) {
+  return dim == 2 && p >= 4 && p <= 16 && ni == (p - 2) * (p - 2) && nb <= 64 && p * p <= 256;
+}
+
+int leaf_fdm_ctas_per_sm() {
+  const size_t smem = sizeof(FdmSmem);
+  if (cudaFuncSetAttribute(leaf_fdm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, leaf_fdm_kernel, kT, smem) != cudaSuccess || n < 1) return 1;
+  return n;
+}
+
+cudaError_t launch_leaf_fdm(const LeafFdmArgs& f, int grid, cudaStream_t st) {
+  const size_t smem = sizeof(FdmSmem);
+  static PerDeviceFlag attr;
+  const int dv = current_device();
+  if (!(attr.set >> dv & 1)) {
+    cudaError_t e = cudaFuncSetAttribute(leaf_fdm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr.set |= 1ull << dv;
+  }
+  leaf_fdm_kernel<<<grid, kT, smem, st>>>(f);
+  return cudaGetLastError();
+}
+
+}  // namespace hpsk

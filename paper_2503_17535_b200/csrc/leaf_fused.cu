@@ -635,7 +635,8 @@ __global__ void __launch_bounds__(kFT, 512 / kFT) leaf_fused_kernel(const LeafFu
       sub_t0 = t;
     }
   };
-  for (long long leaf = blockIdx.x; leaf < f.n_leaves; leaf += gridDim.x, ++iter) {
+  for (long long it = blockIdx.x; it < f.n_leaves; it += gridDim.x, ++iter) {
+    const long long leaf = f.leaf_list ? f.leaf_list[it] : it;
     stamp(0);
     // ---- A. assembly (exterior neighbours into the shared list)
     double* nz_val = s.pan;

@@ -56,7 +56,8 @@ class _Part(C.Structure):
 class _Options(C.Structure):
     _fields_ = [("literal_sign", C.c_int), ("root_implicit_S", C.c_int), ("device", C.c_int), ("keep_factors", C.c_int),
                 ("variant", C.c_int), ("eta", C.c_double), ("build_root_T", C.c_int),
-                ("source_imag", C.POINTER(_Field)), ("force_batched_leaf", C.c_int), ("no_lu_lookahead", C.c_int)]
+                ("source_imag", C.POINTER(_Field)), ("force_batched_leaf", C.c_int), ("no_lu_lookahead", C.c_int),
+                ("force_lu_leaf", C.c_int)]
 
 
 class _Stats(C.Structure):
@@ -65,7 +66,7 @@ class _Stats(C.Structure):
                 ("t_build_ms", C.c_double), ("t_leaf_ms", C.c_double), ("t_merge_ms", C.c_double),
                 ("t_solve_ms", C.c_double), ("build_flops", C.c_double), ("solve_bytes", C.c_double),
                 ("device_bytes", C.c_double), ("launches_build", C.c_int), ("launches_solve", C.c_int),
-                ("n_levels", C.c_int), ("t_level_ms", C.c_double * 24)]
+                ("n_levels", C.c_int), ("t_level_ms", C.c_double * 24), ("leaf_path", C.c_int)]
 
 
 _lib = None
@@ -376,7 +377,7 @@ class HpsSolver:
     def __init__(self, tree: UniformTree, terms, source: Field | None = None, literal_sign=True,
                  root_implicit_S=False, device=0, part=None, keep_factors=False, variant="dtn", eta=1.0,
                  build_root_T=False, source_imag: Field | None = None, force_batched_leaf=False,
-                 lu_lookahead=True):
+                 lu_lookahead=True, fdm_leaf=True):
         L = lib()
         self.tree = tree
         keep = []
@@ -396,6 +397,7 @@ class HpsSolver:
             op.source_imag = C.pointer(self._src_im)
         op.force_batched_leaf = int(force_batched_leaf)
         op.no_lu_lookahead = int(not lu_lookahead)
+        op.force_lu_leaf = int(not fdm_leaf)
         h = C.c_void_p()
         if isinstance(tree, GeneralTree):  # hpsg_create_tree: adaptive / arbitrary trees
             if part is not None:
