@@ -44,9 +44,9 @@ METRIC = "HPS build+solve seconds & DOF/s (2D p=16 L=8) at 1/2/4/8 B200; rel err
 # PAPER.md:629 / :1755 -- H100 JAX, subtree recomputation, p=16 L=8: 4.02 s (N = 16,777,216)
 PAPER_H100_DOFS = 16777216 / 4.02
 FP64_PEAK_TFLOPS = 37.155     # profiles/r01_fp64_peak.json (DMMA microbench; MEASURED_PEAKS.json has no FP64 entry)
-# dram__bytes_read.sum + dram__bytes_write.sum of one leaf_fused_kernel launch at p=16 L=8
-# (ncu --set full of the current kernel, profiles/r02_ncu_summary.md)
-LEAF_KERNEL_DRAM_BYTES = 18.89e9 + 69.29e9
+# dram__bytes_read.sum + dram__bytes_write.sum of one leaf-stage launch at p=16 L=8, per leaf kernel
+# (ncu --set full of the current kernels, profiles/r02_ncu_summary.md)
+LEAF_KERNEL_DRAM_BYTES = {"leaf_fused_kernel": 18.89e9 + 69.29e9, "leaf_fdm_kernel": None}
 
 
 def load_peaks():
@@ -207,6 +207,8 @@ def run_b200(args):
                                   + 2 * ni * ni + 2 * nb * npt)
     peaks = load_peaks()
     flops = st["build_flops"]
+    leaf_kernel = {0: "leaf_fused_kernel", 2: "leaf_fdm_kernel", 3: "leaf_fdm_kernel"}.get(st["leaf_path"],
+                                                                                           "batched leaf LU")
     value = N * world / (ms / 1e3)
     out = {
         "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
@@ -219,15 +221,18 @@ def run_b200(args):
         "sign": "corrected (v=+L^-1 f); literal differs only in the sign of f",
         "stages_ms": {"build": t_build, "leaf": st["t_leaf_ms"], "merge": st["t_merge_ms"], "solve": t_solve,
                       "merge_by_depth": [round(x, 3) for x in st["t_level_ms"]]},
-        # dominant single kernel: leaf_fused_kernel (one launch per build, ~35% of the step in the
-        # ncu launch list profiles/r01_launches_L8_v2.csv); achieved = SURVEY 8d leaf FLOPs x leaves
-        # / the live CUDA-event time of that launch; traffic = dram read+write of that launch from
-        # the ncu --set full capture (profiles/r01_ncu_summary.md)
-        "roofline": {"bound": "tensor", "kernel": "leaf_fused_kernel (stage 1, all 65,536 leaves, one launch)",
+        # dominant single kernel: the leaf stage (one launch per build).  achieved = SURVEY 8d leaf FLOPs
+        # (the reference algorithm's F_leaf) x leaves / the live CUDA-event time of that launch; the
+        # fast-diagonalisation kernel also reports the FP64 tensor FLOPs it executed (device DMMA count);
+        # traffic = dram read+write of that launch from the ncu --set full capture (profiles/)
+        "roofline": {"bound": "tensor", "kernel": f"{leaf_kernel} (stage 1, all {tree.n_leaves:,} leaves, one launch)",
                      "achieved": leaf_flops / (t_leaf / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": leaf_flops / (t_leaf / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
-                     "traffic": LEAF_KERNEL_DRAM_BYTES if (args.L, args.p) == (8, 16) else None,
+                     "traffic": LEAF_KERNEL_DRAM_BYTES.get(leaf_kernel) if (args.L, args.p) == (8, 16) else None,
                      "algorithmic_flops": leaf_flops, "launch_ms": t_leaf,
+                     "executed_flops": st["leaf_exec_flops"] or None,
+                     "executed_frac": (st["leaf_exec_flops"] / (t_leaf / 1e3) / 1e12 / FP64_PEAK_TFLOPS)
+                     if st["leaf_exec_flops"] else None,
                      "peak_source": "FP64 DMMA microbench profiles/r01_fp64_peak.json (of measured)"},
         "roofline_build": {"bound": "tensor", "kernel": "whole build (leaf kernel + batched DMMA LU/TRSM/GEMM merges)",
                            "achieved": flops / (t_build / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",

@@ -120,6 +120,8 @@ typedef struct {
   double t_level_ms[24];       /* merge time of depth d (CUDA events), d = 0 .. L-1 */
   int leaf_path;               /* last build's leaf stage: 0 fused LU kernel, 1 batched LU, 2 fast
                                   diagonalisation, 3 fast diagonalisation that fell back to the fused LU */
+  double leaf_exec_flops;      /* fast-diagonalisation leaf stage: FP64 tensor FLOPs it executed (DMMA.8x8x4
+                                  instructions x 512, counted on the device); 0 for the LU leaf paths */
 } hpsg_stats;
 
 typedef struct hpsg_ctx hpsg_ctx;

@@ -457,9 +457,10 @@ void check_leaf_errors(hpsg_ctx* c) {
                      hpsg::fmt("discretize_operator: non-finite coefficient sample on leaf %lld at point (%g, %g, %g)",
                                leaf_id0 + i, x[0], x[1], x[2])};
     }
-  double mr = 1.0;
+  double mr = 1.0, ndmma = 0.0;
   for (int i = 0; i < nl; ++i) {
     const double* si = &s[size_t(i) * 3];
+    if (si[2] < -1.5) ndmma += -1.0 - si[2];  // fast-diagonalisation leaf: DMMA count rides in the status slot
     if (si[2] >= 0)
       throw HpsError{HPSG_ERR_SINGULAR_LEAF,
                      hpsg::fmt("leaf %lld: local_solve_dtn: singular factorization (zero pivot at %d)", leaf_id0 + i,
@@ -467,6 +468,7 @@ void check_leaf_errors(hpsg_ctx* c) {
     mr = std::min(mr, si[0] / si[1]);
   }
   c->stats.min_rcond = mr;
+  c->stats.leaf_exec_flops = 512.0 * ndmma;
   c->stats.ill_conditioned = mr < 1e-12 ? 1 : 0;
 }
 

@@ -152,7 +152,7 @@ struct LeafFdmArgs {
   long long strideYv;
   double* HT;
   long long strideHT;
-  double* stats;            // per leaf: min / max |lam_i + lam_j + cbar|, -1
+  double* stats;            // per leaf: min / max |lam_i + lam_j + cbar|, -1 - (DMMA.8x8x4 issued)
   int* fail_count;          // leaves that did not converge: count and list (the host re-runs them with
   int* fail_list;           // the LU leaf kernel, so every leaf's result is independent of its neighbours)
   long long n_leaves;

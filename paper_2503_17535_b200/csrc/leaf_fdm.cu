@@ -47,6 +47,7 @@ struct FdmSmem {
   double wmin[kW], wmax[kW];
   int bad;
   int failed;        // this leaf did not converge
+  int ndmma;         // DMMA.8x8x4 instructions issued for this leaf (executed-FLOP accounting)
 };
 
 // element (row, col) of a block: column-major 16 x 16, rows XOR-swizzled by the column
@@ -109,8 +110,9 @@ HPS_DEV double warp_max(double v) {
 
 // Solve one right-hand side block: X <- L_ii^-1 R.  Returns false if it did not converge.
 HPS_DEV bool solve_block(const double* Rb, double* Xb, double* Wb, const FdmSmem& s, const double (&vi)[2][4],
-                         const double (&vv)[2][4], const double (&aa)[2][4], int g, int t4) {
+                         const double (&vv)[2][4], const double (&aa)[2][4], int g, int t4, int& npass) {
   double acc[2][2][2];
+  npass += 4;
   // X_0 = K_c^-1 R
   mma_block<false>(vi, Rb, acc, g, t4);
   store_t<false>(Wb, acc, nullptr, g, t4);
@@ -128,6 +130,7 @@ HPS_DEV bool solve_block(const double* Rb, double* Xb, double* Wb, const FdmSmem
   double dprev = warp_max(xm), xmax = dprev, rbest = 1.0;
   if (dprev == 0.0) return true;
   for (int step = 0; step < kMaxSteps; ++step) {
+    npass += 6;
     // W = R - A X - X A^T - c o X  (the residual of the true operator)
     mma_block<false>(aa, Xb, acc, g, t4);
 #pragma unroll
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(kT, 2) leaf_fdm_kernel(const LeafFdmArgs f) {
 
   for (long long leaf = blockIdx.x; leaf < f.n_leaves; leaf += gridDim.x) {
     // ---- coefficients and source at the leaf points (leaf_cheb_points, discretize_operator's sampling)
-    if (tid == 0) s.bad = INT_MAX;
+    if (tid == 0) s.bad = INT_MAX, s.ndmma = 0;
     for (int e = tid; e < kBlk; e += kT) s.cz[e] = 0.0;
     __syncthreads();
     const double* box = a.leaf_box + leaf * 6;
@@ -298,9 +301,12 @@ __global__ void __launch_bounds__(kT, 2) leaf_fdm_kernel(const LeafFdmArgs f) {
       __syncthreads();
       // ---- per right-hand side: fast-diagonalisation Richardson (warp-local)
       bool conv = true;
+      int npass = 0;
       for (int b = warp; b < kNC; b += kW)
-        if (c0 + b < ncol) conv = solve_block(s.R + b * kBlk, s.X + b * kBlk, s.W + b * kBlk, s, vi, vv, aa, g, t4) && conv;
+        if (c0 + b < ncol)
+          conv = solve_block(s.R + b * kBlk, s.X + b * kBlk, s.W + b * kBlk, s, vi, vv, aa, g, t4, npass) && conv;
       if (!conv && lane == 0) s.failed = 1;
+      if (lane == 0 && npass) atomicAdd(&s.ndmma, 16 * npass);
       __syncthreads();
       // ---- outputs of the chunk: [v_i | Y_i] columns, and [h | T] = Q_i X + [0 | Q_e P] (DMMA, Q_i from L2)
       double* Yv = f.Yv + leaf * f.strideYv;
@@ -330,10 +336,14 @@ __global__ void __launch_bounds__(kT, 2) leaf_fdm_kernel(const LeafFdmArgs f) {
             if (col < ncol && m < nb)
               __stcs(&HT[(long long)col * nb + m], acc[nt][h] + f.ZQeP[(long long)col * nb + m]);
           }
+        if (lane == 0) atomicAdd(&s.ndmma, 2 * ((ni + 3) / 4));
       }
       __syncthreads();
     }
-    if (tid == 0 && s.failed) f.fail_list[atomicAdd(f.fail_count, 1)] = int(leaf);
+    if (tid == 0) {
+      if (s.failed) f.fail_list[atomicAdd(f.fail_count, 1)] = int(leaf);
+      f.stats[3 * leaf + 2] = -1.0 - double(s.ndmma);  // < 0: no zero pivot; the LU fallback rewrites it to -1
+    }
   }
 }
 

@@ -66,7 +66,8 @@ class _Stats(C.Structure):
                 ("t_build_ms", C.c_double), ("t_leaf_ms", C.c_double), ("t_merge_ms", C.c_double),
                 ("t_solve_ms", C.c_double), ("build_flops", C.c_double), ("solve_bytes", C.c_double),
                 ("device_bytes", C.c_double), ("launches_build", C.c_int), ("launches_solve", C.c_int),
-                ("n_levels", C.c_int), ("t_level_ms", C.c_double * 24), ("leaf_path", C.c_int)]
+                ("n_levels", C.c_int), ("t_level_ms", C.c_double * 24), ("leaf_path", C.c_int),
+                ("leaf_exec_flops", C.c_double)]
 
 
 _lib = None
