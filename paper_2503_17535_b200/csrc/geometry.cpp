@@ -242,6 +242,24 @@ LeafOperators make_leaf_operators(int dim, int p, double side) {
   return op;
 }
 
+void q_interior_factors(const LeafOperators& op, std::vector<double>& G, std::vector<double>& d, double& ds) {
+  const int p = op.p, q = op.q, n1 = p - 2;
+  std::vector<double> gx, gw;
+  gauss_rule(q, gx, gw);
+  const std::vector<double> cn = cheb_nodes(p);
+  const std::vector<double> cheb_up(cn.rbegin(), cn.rend());
+  const HostMat c2g = bary_interp(cheb_up, gx);  // the same interpolant make_leaf_operators uses
+  const double sgn[4] = {-1, 1, 1, -1};
+  const int fixed[4] = {p - 1, 0, 0, p - 1};
+  G.assign(size_t(q) * n1, 0.0);
+  d.assign(size_t(4) * n1, 0.0);
+  for (int i = 0; i < q; ++i)
+    for (int m = 0; m < n1; ++m) G[size_t(i) * n1 + m] = c2g(i, p - 2 - m);
+  for (int s = 0; s < 4; ++s)
+    for (int k = 0; k < n1; ++k) d[size_t(s) * n1 + k] = sgn[s] * op.D(fixed[s], k + 1);
+  ds = 2.0 / op.side;
+}
+
 long long UniformTree::level_first_id(int d) const {
   // reference id of the first node at part depth d (breadth-first ids of the FULL tree, mesh.cpp:113-118)
   long long id = 0, cnt = 1;

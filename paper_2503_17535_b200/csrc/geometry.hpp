@@ -44,6 +44,13 @@ struct LeafOperators {
 };
 LeafOperators make_leaf_operators(int dim, int p, double side);
 
+// 2D: the interior part of Q is separable per side s (geometry.cpp, make_leaf_operators):
+//   Qi(s q + i, (i1, i2)) = ds * G(i, m) * d_s(k),  G(i, m) = c2g(i, p-1-(m+1)),  d_s(k) = sgn_s D(fixed_s, k+1)
+// with (m, k) = (i1-1, i2-1) on the S/N sides (normal axis 2) and (i2-1, i1-1) on E/W (normal axis 1).
+// G: q x (p-2) row-major, d: 4 x (p-2) row-major, ds = 2 / side.  [h|T] = Q_i [v|Y_i] then costs two
+// (p-2)-term contractions per boundary point instead of a dense ni-term row.
+void q_interior_factors(const LeafOperators& op, std::vector<double>& G, std::vector<double>& d, double& ds);
+
 // A = V diag(lam) V^-1 for a small real matrix with real, distinct eigenvalues (n x n column-major; the
 // interior block of the Chebyshev second-derivative matrix for the fast-diagonalisation leaf solve).
 // Householder-Hessenberg + Wilkinson-shifted QR for lam, inverse iteration for V, Gauss-Jordan for V^-1.

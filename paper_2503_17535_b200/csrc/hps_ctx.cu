@@ -352,10 +352,17 @@ void setup_fdm(hpsg_ctx* c) {
   upload(c->fdmVinv, pad(Vi), &c->dev_bytes, c->st);
   upload(c->fdmA, pad(A), &c->dev_bytes, c->st);
   upload(c->fdmLam, lp, &c->dev_bytes, c->st);
+  std::vector<double> qG, qd;
+  hpsg::q_interior_factors(o, qG, qd, c->fdm_qds);
+  upload(c->fdmQG, qG, &c->dev_bytes, c->st);
+  upload(c->fdmQd, qd, &c->dev_bytes, c->st);
+  c->fdmRtab.alloc(sizeof(double) * 256 * size_t(o.nb), &c->dev_bytes);
+  c->fdmRhat.alloc(sizeof(double) * 256 * size_t(o.nb), &c->dev_bytes);
+  c->fdm_prepped = false;
   c->fdmFail.alloc(sizeof(int) * (1 + size_t(c->T.n_leaves())), &c->dev_bytes);
   int nsm = 0;
   ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->opts.device), "sm count");
-  c->fdm_grid = int(std::min<long long>(c->T.n_leaves(), (long long)nsm * hpsk::leaf_fdm_ctas_per_sm()));
+  c->fdm_grid = int(std::min<long long>(c->T.n_leaves(), (long long)nsm * hpsk::leaf_fdm_ctas_per_sm(o.p)));
   c->fdm_lap = a;
   c->fdm = true;
 }
@@ -570,6 +577,11 @@ void run_leaf_stage(hpsg_ctx* c) {
     f.A = c->fdmA.d();
     f.lam = c->fdmLam.d();
     f.lap_coef = c->fdm_lap;
+    f.qG = c->fdmQG.d();
+    f.qd = c->fdmQd.d();
+    f.qds = c->fdm_qds;
+    f.Rtab = c->fdmRtab.d();
+    f.Rhat = c->fdmRhat.d();
     f.Yv = c->leafYv.d();
     f.strideYv = c->yv_stride;
     f.HT = c->leafHT.d();
@@ -579,6 +591,11 @@ void run_leaf_stage(hpsg_ctx* c) {
     f.fail_list = c->fdmFail.i() + 1;
     f.n_leaves = nl;
     ck(cudaMemsetAsync(c->fdmFail.p, 0, sizeof(int), c->st), "fdm flag");
+    if (!c->fdm_prepped) {  // once per context: the leaf-independent right-hand sides
+      ck(hpsk::launch_leaf_fdm_prep(f, c->st), "leaf_fdm_prep");
+      ++c->launches;
+      c->fdm_prepped = true;
+    }
     ck(hpsk::launch_leaf_fdm(f, c->fdm_grid, c->st), "leaf_fdm");
     ++c->launches;
     int nfail = 0;  // the leaf-error check right after the stage synchronises anyway

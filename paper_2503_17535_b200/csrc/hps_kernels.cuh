@@ -148,6 +148,11 @@ struct LeafFdmArgs {
   const double* A;          // 16 x 16: the 1D interior operator s^2 (a D2[int, int]), zero padded
   const double* lam;        // 16: its eigenvalues (0 in the padding)
   double lap_coef;          // a (the constant Laplacian coefficient)
+  const double* qG;         // separable Q_i (geometry.hpp q_interior_factors): G q x (p-2), d 4 x (p-2), ds
+  const double* qd;
+  double qds;
+  double* Rtab;             // 4(p-2) blocks of 16 x 16: -L_ie P per column (block layout) and R^ = V^-1 R V^-T,
+  double* Rhat;             // written by launch_leaf_fdm_prep, read by every leaf
   double* Yv;
   long long strideYv;
   double* HT;
@@ -158,7 +163,8 @@ struct LeafFdmArgs {
   long long n_leaves;
 };
 bool leaf_fdm_shape_ok(int p, int ni, int nb, int dim);
-int leaf_fdm_ctas_per_sm();
+int leaf_fdm_ctas_per_sm(int p);
+cudaError_t launch_leaf_fdm_prep(const LeafFdmArgs& f, cudaStream_t st);
 cudaError_t launch_leaf_fdm(const LeafFdmArgs& f, int grid, cudaStream_t st);
 
 // ---- stage 2: merge operand gather ------------------------------------------

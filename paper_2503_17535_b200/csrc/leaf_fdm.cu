@@ -44,14 +44,20 @@ struct FdmSmem {
   double den[kBlk];  // 1 / (lam_row + lam_col + cbar), 0 in the padding
   double fsrc[256];
   int pos[256];      // tensor index -> interior r (>= 0) or -(exterior position) - 1
+  double qGt[14 * 16];  // separable Q_i: G^T ((p-2) x q, row stride 16) and d (4 x (p-2))
+  double qd[4 * 14];
   double wmin[kW], wmax[kW];
   int bad;
   int failed;        // this leaf did not converge
   int ndmma;         // DMMA.8x8x4 instructions issued for this leaf (executed-FLOP accounting)
 };
 
-// element (row, col) of a block: column-major 16 x 16, rows XOR-swizzled by the column
-HPS_DEV int swz(int row, int col) { return (col << 4) + (row ^ ((col & 3) << 2)); }
+// element (row, col) of a block: column-major 16 x 16, rows XOR-swizzled by the column with the bit-reversed
+// low two column bits (x 4).  Conflict-free for the DMMA fragment loads (scalar, both orientations) and for the
+// row-pair (double2) accesses of the transposed stores and the residual: within any quarter warp the columns
+// g, g+1 of a pair land in opposite halves of the banks.
+HPS_DEV int swx(int col) { return ((col & 1) << 3) | ((col & 2) << 1); }
+HPS_DEV int swz(int row, int col) { return (col << 4) + (row ^ swx(col)); }
 
 HPS_DEV void load_afrag(const double* M, double (&am)[2][4], int g, int t4) {
 #pragma unroll
@@ -63,8 +69,9 @@ HPS_DEV void load_afrag(const double* M, double (&am)[2][4], int g, int t4) {
 // acc = M In, M from registers; In(k, n) read at swz(k, n) (TRANS = false) or swz(n, k) (TRANS = true).
 // acc[mt][nt][h] is element (mt * 8 + g, nt * 8 + 2 t4 + h).  Ends with __syncwarp: the block may be
 // overwritten in place after the call.
-template <bool TRANS>
-HPS_DEV void mma_block(const double (&am)[2][4], const double* in, double (&acc)[2][2][2], int g, int t4) {
+template <bool TRANS, bool SCALE = false>
+HPS_DEV void mma_block(const double (&am)[2][4], const double* in, double (&acc)[2][2][2], int g, int t4,
+                       const double* den = nullptr) {
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -73,7 +80,10 @@ HPS_DEV void mma_block(const double (&am)[2][4], const double* in, double (&acc)
   for (int ks = 0; ks < 4; ++ks) {
     double b[2];
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) b[nt] = TRANS ? in[swz(nt * 8 + g, ks * 4 + t4)] : in[swz(ks * 4 + t4, nt * 8 + g)];
+    for (int nt = 0; nt < 2; ++nt) {
+      const int e = TRANS ? swz(nt * 8 + g, ks * 4 + t4) : swz(ks * 4 + t4, nt * 8 + g);
+      b[nt] = SCALE ? in[e] * den[e] : in[e];
+    }
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -109,16 +119,23 @@ HPS_DEV double warp_max(double v) {
 }
 
 // Solve one right-hand side block: X <- L_ii^-1 R.  Returns false if it did not converge.
+// hat: Xb already holds R^ = V^-1 R V^-T (the leaf-independent columns -L_ie P, precomputed once by
+// leaf_fdm_prep_kernel); otherwise R^ is formed here from Rb (the source column).
 HPS_DEV bool solve_block(const double* Rb, double* Xb, double* Wb, const FdmSmem& s, const double (&vi)[2][4],
-                         const double (&vv)[2][4], const double (&aa)[2][4], int g, int t4, int& npass) {
+                         const double (&vv)[2][4], const double (&aa)[2][4], int g, int t4, int& npass, bool hat) {
   double acc[2][2][2];
-  npass += 4;
-  // X_0 = K_c^-1 R
-  mma_block<false>(vi, Rb, acc, g, t4);
-  store_t<false>(Wb, acc, nullptr, g, t4);
-  mma_block<false>(vi, Wb, acc, g, t4);
-  store_t<true>(Wb, acc, s.den, g, t4);
-  mma_block<false>(vv, Wb, acc, g, t4);
+  // X_0 = K_c^-1 R = V (den o R^) V^T
+  if (hat) {
+    npass += 2;
+    mma_block<false, true>(vv, Xb, acc, g, t4, s.den);
+  } else {
+    npass += 4;
+    mma_block<false>(vi, Rb, acc, g, t4);
+    store_t<false>(Wb, acc, nullptr, g, t4);
+    mma_block<false>(vi, Wb, acc, g, t4);
+    store_t<true>(Wb, acc, s.den, g, t4);
+    mma_block<false>(vv, Wb, acc, g, t4);
+  }
   store_t<false>(Wb, acc, nullptr, g, t4);
   mma_block<false>(vv, Wb, acc, g, t4);
   double xm = 0.0;
@@ -127,7 +144,10 @@ HPS_DEV bool solve_block(const double* Rb, double* Xb, double* Wb, const FdmSmem
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) xm = fmax(xm, fmax(fabs(acc[mt][nt][0]), fabs(acc[mt][nt][1])));
   store_t<false>(Xb, acc, nullptr, g, t4);
-  double dprev = warp_max(xm), xmax = dprev, rbest = 1.0;
+  double dprev = warp_max(xm), rbest = 1.0;
+  // max|X_k| >= max|X_0| - sum of the corrections so far: the stopping tests use that lower bound as the
+  // scale (one warp reduction per step)
+  double xmax = dprev;
   if (dprev == 0.0) return true;
   for (int step = 0; step < kMaxSteps; ++step) {
     npass += 6;
@@ -165,7 +185,6 @@ HPS_DEV bool solve_block(const double* Rb, double* Xb, double* Wb, const FdmSmem
     store_t<false>(Wb, acc, nullptr, g, t4);
     mma_block<false>(vv, Wb, acc, g, t4);
     double dm = 0.0;
-    xm = 0.0;
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -176,11 +195,10 @@ HPS_DEV bool solve_block(const double* Rb, double* Xb, double* Wb, const FdmSmem
         x.y += acc[mt][nt][1];
         *reinterpret_cast<double2*>(Xb + p) = x;
         dm = fmax(dm, fmax(fabs(acc[mt][nt][0]), fabs(acc[mt][nt][1])));
-        xm = fmax(xm, fmax(fabs(x.x), fabs(x.y)));
       }
     __syncwarp();
     const double dk = warp_max(dm);
-    xmax = warp_max(xm);
+    xmax -= dk;
     if (dk == 0.0) return true;
     const double rho = dk / dprev;
     if (rho < 0.5 && rho / (1.0 - rho) * dk <= kTol * xmax) return true;
@@ -191,21 +209,22 @@ HPS_DEV bool solve_block(const double* Rb, double* Xb, double* Wb, const FdmSmem
   return false;
 }
 
-}  // namespace
-
+template <int P>
 __global__ void __launch_bounds__(kT, 2) leaf_fdm_kernel(const LeafFdmArgs f) {
+  constexpr int N1 = P - 2, NI = N1 * N1, NE = 4 * P - 4, NB = 4 * N1, NPT = P * P;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FdmSmem& s = *reinterpret_cast<FdmSmem*>(smem_raw);
   const LeafAsmArgs& a = f.a;
-  const int p = a.p, n = a.n, ni = a.ni, ne = a.ne, nb = a.nb, n1 = p - 2, ncol = 1 + nb;
+  constexpr int ncol = 1 + NB;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
-  const double s2 = a.scale * a.scale, clap = f.lap_coef;
   double vi[2][4], vv[2][4], aa[2][4];
   load_afrag(f.Vinv, vi, g, t4);
   load_afrag(f.V, vv, g, t4);
   load_afrag(f.A, aa, g, t4);
-  for (int r = tid; r < ni; r += kT) s.pos[a.interior[r]] = r;
-  for (int r = tid; r < ne; r += kT) s.pos[a.exterior[r]] = -r - 1;
+  for (int r = tid; r < NI; r += kT) s.pos[a.interior[r]] = r;
+  for (int r = tid; r < NE; r += kT) s.pos[a.exterior[r]] = -r - 1;
+  for (int e = tid; e < N1 * N1; e += kT) s.qGt[(e % N1) * 16 + e / N1] = f.qG[e];   // G(i, m) -> qGt[m][i]
+  for (int e = tid; e < 4 * N1; e += kT) s.qd[e] = f.qd[e];
   __syncthreads();
 
   for (long long leaf = blockIdx.x; leaf < f.n_leaves; leaf += gridDim.x) {
@@ -215,21 +234,21 @@ __global__ void __launch_bounds__(kT, 2) leaf_fdm_kernel(const LeafFdmArgs f) {
     __syncthreads();
     const double* box = a.leaf_box + leaf * 6;
     double cmin = DBL_MAX, cmax = -DBL_MAX;
-    for (int i = tid; i < n; i += kT) {
-      const int i1 = i / p, i2 = i % p;
+    for (int i = tid; i < NPT; i += kT) {
+      const int i1 = i / P, i2 = i % P;
       double x[3] = {0.0, 0.0, 0.0};
       x[0] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(box[0], box[3])), __dmul_rn(__dmul_rn(0.5, __dsub_rn(box[3], box[0])), a.cheb[i1]));
       x[1] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(box[1], box[4])), __dmul_rn(__dmul_rn(0.5, __dsub_rn(box[4], box[1])), a.cheb[i2]));
       double cz = 0.0;
       for (int t = 0; t < a.nterms; ++t) {
-        const double v = eval_field_t<2>(a.terms[t].f, x, leaf, i, n);
+        const double v = eval_field_t<2>(a.terms[t].f, x, leaf, i, NPT);
         if (!isfinite(v)) atomicMin(&s.bad, i);
         if (a.terms[t].role == 2) cz = __dadd_rn(cz, v);
       }
-      s.fsrc[i] = a.has_source ? eval_field_t<2>(a.source, x, leaf, i, n) : 0.0;
+      s.fsrc[i] = a.has_source ? eval_field_t<2>(a.source, x, leaf, i, NPT) : 0.0;
       const int r = s.pos[i];
       if (r >= 0) {
-        s.cz[swz(r % n1, r / n1)] = cz;
+        s.cz[swz(r % N1, r / N1)] = cz;
         cmin = fmin(cmin, cz);
         cmax = fmax(cmax, cz);
       }
@@ -243,9 +262,9 @@ __global__ void __launch_bounds__(kT, 2) leaf_fdm_kernel(const LeafFdmArgs f) {
     const double cbar = 0.5 * (cmin + cmax);
     double dmin = DBL_MAX, dmax = 0.0;
     for (int e = tid; e < kBlk; e += kT) {
-      const int col = e >> 4, row = (e & 15) ^ ((col & 3) << 2);
+      const int col = e >> 4, row = (e & 15) ^ swx(col);
       double d = 0.0;
-      if (row < n1 && col < n1) {
+      if (row < N1 && col < N1) {
         const double ev = f.lam[row] + f.lam[col] + cbar;
         d = 1.0 / ev;
         dmin = fmin(dmin, fabs(ev));
@@ -274,72 +293,72 @@ __global__ void __launch_bounds__(kT, 2) leaf_fdm_kernel(const LeafFdmArgs f) {
     }
     if (tid == 0) s.failed = 0;
 
-    for (int c0 = 0; c0 < ncol; c0 += kNC) {
-      // ---- right-hand sides [sgn f_i | -L_ie P] of this chunk, X = 0
-      for (int e = tid; e < kNC * kBlk; e += kT) {
-        const int b = e >> 8, q = e & 255, col = q >> 4, row = (q & 15) ^ ((col & 3) << 2);
-        const int rc = c0 + b;
-        double v = 0.0;
-        if (row < n1 && col < n1 && rc < ncol) {
-          const int i1 = col + 1, i2 = row + 1;
-          if (rc == 0) {
-            v = a.fsign * s.fsrc[i1 * p + i2];
-          } else {
-            // the row's exterior line neighbours in slot order (axis 0 node 0 / p-1, axis 1 node 0 / p-1),
-            // entries s^2 (a D2(i, j)) as leaf_entry rounds them
-            const double* Pj = f.P + (long long)(rc - 1) * ne;
-            double acc = 0.0;
-            acc += __dmul_rn(s2, __dmul_rn(clap, a.D2[0 * p + i1])) * Pj[-s.pos[0 * p + i2] - 1];
-            acc += __dmul_rn(s2, __dmul_rn(clap, a.D2[(p - 1) * p + i1])) * Pj[-s.pos[(p - 1) * p + i2] - 1];
-            acc += __dmul_rn(s2, __dmul_rn(clap, a.D2[0 * p + i2])) * Pj[-s.pos[i1 * p + 0] - 1];
-            acc += __dmul_rn(s2, __dmul_rn(clap, a.D2[(p - 1) * p + i2])) * Pj[-s.pos[i1 * p + p - 1] - 1];
-            v = -acc;
-          }
-        }
-        s.R[e] = v;
-      }
-      __syncthreads();
-      // ---- per right-hand side: fast-diagonalisation Richardson (warp-local)
+    // ---- per warp: its columns c = warp + 1, warp + 1 + kW, ... (mod ncol; column 0, the source, goes to the last
+    // warp), each solved, written and contracted to [h | T] without CTA barriers
+    {
+      double* Rb = s.R + warp * 2 * kBlk;
+      double* Xb = s.X + warp * 2 * kBlk;
+      double* Wb = s.W + warp * 2 * kBlk;
       bool conv = true;
       int npass = 0;
-      for (int b = warp; b < kNC; b += kW)
-        if (c0 + b < ncol)
-          conv = solve_block(s.R + b * kBlk, s.X + b * kBlk, s.W + b * kBlk, s, vi, vv, aa, g, t4, npass) && conv;
-      if (!conv && lane == 0) s.failed = 1;
-      if (lane == 0 && npass) atomicAdd(&s.ndmma, 16 * npass);
-      __syncthreads();
-      // ---- outputs of the chunk: [v_i | Y_i] columns, and [h | T] = Q_i X + [0 | Q_e P] (DMMA, Q_i from L2)
-      double* Yv = f.Yv + leaf * f.strideYv;
-      for (int e = tid; e < kNC * ni; e += kT) {
-        const int b = e / ni, r = e - b * ni;
-        if (c0 + b < ncol) __stcs(&Yv[(long long)(c0 + b) * ni + r], s.X[b * kBlk + swz(r % n1, r / n1)]);
-      }
-      const int mtiles = (nb + 7) / 8;
-      if (warp < mtiles) {
-        const int m0 = warp * 8;
-        double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-        for (int k0 = 0; k0 < ni; k0 += 4) {
-          const int k = k0 + t4;
-          const double av = (k < ni && m0 + g < nb) ? f.Qi[(long long)k * nb + m0 + g] : 0.0;
+      for (int c = warp + 1; c < ncol + 1; c += kW) {
+        const int col = c == ncol ? 0 : c;
+        // right-hand side: column 0 = sgn f_i (formed here); columns 1.. = -L_ie P, the same for every leaf
+        // (constant Laplacian): R and R^ = V^-1 R V^-T from the prep tables (L2-resident)
+        if (col > 0) {
+          const double2* Rt = reinterpret_cast<const double2*>(f.Rtab + (long long)(col - 1) * kBlk);
+          const double2* Rh = reinterpret_cast<const double2*>(f.Rhat + (long long)(col - 1) * kBlk);
 #pragma unroll
-          for (int nt = 0; nt < 2; ++nt) {
-            const double bv = k < ni ? s.X[(nt * 8 + g) * kBlk + swz(k % n1, k / n1)] : 0.0;
-            dmma_8x8x4(acc[nt][0], acc[nt][1], av, bv);
+          for (int e = lane; e < kBlk / 2; e += 32) {
+            reinterpret_cast<double2*>(Rb)[e] = __ldg(Rt + e);
+            reinterpret_cast<double2*>(Xb)[e] = __ldg(Rh + e);
+          }
+        } else {
+          for (int e = lane; e < kBlk; e += 32) {
+            const int cc = e >> 4, row = (e & 15) ^ swx(cc);
+            Rb[e] = (row < N1 && cc < N1) ? a.fsign * s.fsrc[(cc + 1) * P + row + 1] : 0.0;
           }
         }
-        double* HT = f.HT + leaf * f.strideHT;
+        __syncwarp();
+        conv = solve_block(Rb, Xb, Wb, s, vi, vv, aa, g, t4, npass, col > 0) && conv;
+        // [v_i | Y_i] column (interior index r = (i1-1) N1 + (i2-1)); X^T into W for the contractions
+        double* Yv = f.Yv + leaf * f.strideYv + (long long)col * NI;
+        for (int r = lane; r < NI; r += 32) __stcs(&Yv[r], Xb[swz(r % N1, r / N1)]);
+        for (int e = lane; e < kBlk; e += 32) {
+          const int cc = e >> 4, row = (e & 15) ^ swx(cc);
+          Wb[e] = Xb[swz(cc, row)];
+        }
+        __syncwarp();
+        // [h | T] = Q_i X + [0 | Q_e P] through the separable Q_i (geometry.cpp q_interior_factors):
+        // u_s(m) = sum_k d_s(k) X(line m, k), then h_s(i) = ds sum_m G(i, m) u_s(m).  Block element (row, col)
+        // = X(i1 = col + 1, i2 = row + 1): the S/N sides contract rows (read from X^T), E/W columns (from X).
+        double* U = Rb;  // R is free after the solve: [side][16]
+        for (int e = lane; e < 4 * N1; e += 32) {
+          const int sd = e / N1, m = e - sd * N1;
+          const double* Xs = (sd & 1) ? Xb : Wb;
+          const double* dv = s.qd + sd * N1;
+          double acc = 0.0;
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
+          for (int k = 0; k < N1; ++k) acc = fma(dv[k], Xs[swz(m, k)], acc);
+          U[sd * 16 + m] = acc;
+        }
+        __syncwarp();
+        double* HT = f.HT + leaf * f.strideHT + (long long)col * NB;
+        const double* zq = f.ZQeP + (long long)col * NB;
+        for (int row = lane; row < NB; row += 32) {
+          const int sd = row / N1, i = row - sd * N1;
+          const double* u = U + sd * 16;
+          double acc = 0.0;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int col = c0 + nt * 8 + 2 * t4 + h, m = m0 + g;
-            if (col < ncol && m < nb)
-              __stcs(&HT[(long long)col * nb + m], acc[nt][h] + f.ZQeP[(long long)col * nb + m]);
-          }
-        if (lane == 0) atomicAdd(&s.ndmma, 2 * ((ni + 3) / 4));
+          for (int m = 0; m < N1; ++m) acc = fma(s.qGt[m * 16 + i], u[m], acc);
+          __stcs(&HT[row], f.qds * acc + __ldg(zq + row));
+        }
+        __syncwarp();
       }
-      __syncthreads();
+      if (!conv && lane == 0) s.failed = 1;
+      if (lane == 0 && npass) atomicAdd(&s.ndmma, 16 * npass);
     }
+    __syncthreads();
     if (tid == 0) {
       if (s.failed) f.fail_list[atomicAdd(f.fail_count, 1)] = int(leaf);
       f.stats[3 * leaf + 2] = -1.0 - double(s.ndmma);  // < 0: no zero pivot; the LU fallback rewrites it to -1
@@ -347,29 +366,111 @@ __global__ void __launch_bounds__(kT, 2) leaf_fdm_kernel(const LeafFdmArgs f) {
   }
 }
 
+// The leaf-independent right-hand sides -L_ie P (constant Laplacian; the zeroth-order term only enters L_ii)
+// in the block layout, and R^ = V^-1 R V^-T: one warp per column, the same arithmetic the leaf kernel used
+// to run per leaf, so the results are unchanged.
+template <int P>
+__global__ void __launch_bounds__(32) leaf_fdm_prep_kernel(const LeafFdmArgs f) {
+  constexpr int N1 = P - 2, NE = 4 * P - 4;
+  __shared__ __align__(16) double R[kBlk], W[kBlk];
+  __shared__ int pos[256];
+  const LeafAsmArgs& a = f.a;
+  const int lane = threadIdx.x, g = lane >> 2, t4 = lane & 3, rc = blockIdx.x + 1;
+  const double s2 = a.scale * a.scale, clap = f.lap_coef;
+  for (int r = lane; r < N1 * N1; r += 32) pos[a.interior[r]] = r;
+  for (int r = lane; r < NE; r += 32) pos[a.exterior[r]] = -r - 1;
+  __syncwarp();
+  for (int q = lane; q < kBlk; q += 32) {
+    const int col = q >> 4, row = (q & 15) ^ swx(col);
+    double v = 0.0;
+    if (row < N1 && col < N1) {
+      const int i1 = col + 1, i2 = row + 1;
+      // the row's exterior line neighbours in slot order (axis 0 node 0 / p-1, axis 1 node 0 / p-1), entries
+      // s^2 (a D2(i, j)) as leaf_entry rounds them
+      const double* Pj = f.P + (long long)(rc - 1) * NE;
+      double acc = 0.0;
+      acc += __dmul_rn(s2, __dmul_rn(clap, a.D2[0 * P + i1])) * Pj[-pos[0 * P + i2] - 1];
+      acc += __dmul_rn(s2, __dmul_rn(clap, a.D2[(P - 1) * P + i1])) * Pj[-pos[(P - 1) * P + i2] - 1];
+      acc += __dmul_rn(s2, __dmul_rn(clap, a.D2[0 * P + i2])) * Pj[-pos[i1 * P + 0] - 1];
+      acc += __dmul_rn(s2, __dmul_rn(clap, a.D2[(P - 1) * P + i2])) * Pj[-pos[i1 * P + P - 1] - 1];
+      v = -acc;
+    }
+    R[q] = v;
+  }
+  __syncwarp();
+  double vi[2][4], acc[2][2][2];
+  load_afrag(f.Vinv, vi, g, t4);
+  mma_block<false>(vi, R, acc, g, t4);
+  store_t<false>(W, acc, nullptr, g, t4);
+  mma_block<false>(vi, W, acc, g, t4);
+  store_t<false>(W, acc, nullptr, g, t4);
+  for (int q = lane; q < kBlk; q += 32) {
+    f.Rtab[(long long)(rc - 1) * kBlk + q] = R[q];
+    f.Rhat[(long long)(rc - 1) * kBlk + q] = W[q];
+  }
+}
+
+using FdmKernel = void (*)(const LeafFdmArgs);
+FdmKernel fdm_kernel_for(int p) {
+  switch (p) {
+    case 4: return leaf_fdm_kernel<4>;
+    case 5: return leaf_fdm_kernel<5>;
+    case 6: return leaf_fdm_kernel<6>;
+    case 7: return leaf_fdm_kernel<7>;
+    case 8: return leaf_fdm_kernel<8>;
+    case 9: return leaf_fdm_kernel<9>;
+    case 10: return leaf_fdm_kernel<10>;
+    case 11: return leaf_fdm_kernel<11>;
+    case 12: return leaf_fdm_kernel<12>;
+    case 13: return leaf_fdm_kernel<13>;
+    case 14: return leaf_fdm_kernel<14>;
+    case 15: return leaf_fdm_kernel<15>;
+    case 16: return leaf_fdm_kernel<16>;
+    default: return nullptr;
+  }
+}
+
+}  // namespace
+
 bool leaf_fdm_shape_ok(int p, int ni, int nb, int dim) {
   return dim == 2 && p >= 4 && p <= 16 && ni == (p - 2) * (p - 2) && nb <= 64 && p * p <= 256;
 }
 
-int leaf_fdm_ctas_per_sm() {
+int leaf_fdm_ctas_per_sm(int p) {
   const size_t smem = sizeof(FdmSmem);
-  if (cudaFuncSetAttribute(leaf_fdm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return 1;
+  FdmKernel k = fdm_kernel_for(p);
+  if (!k || cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, leaf_fdm_kernel, kT, smem) != cudaSuccess || n < 1) return 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kT, smem) != cudaSuccess || n < 1) return 1;
   return n;
+}
+
+cudaError_t launch_leaf_fdm_prep(const LeafFdmArgs& f, cudaStream_t st) {
+  const int nb = 4 * (f.a.p - 2);
+  switch (f.a.p) {
+#define HPS_FDM_PREP(PP) \
+  case PP: leaf_fdm_prep_kernel<PP><<<nb, 32, 0, st>>>(f); break;
+    HPS_FDM_PREP(4) HPS_FDM_PREP(5) HPS_FDM_PREP(6) HPS_FDM_PREP(7) HPS_FDM_PREP(8) HPS_FDM_PREP(9) HPS_FDM_PREP(10)
+    HPS_FDM_PREP(11) HPS_FDM_PREP(12) HPS_FDM_PREP(13) HPS_FDM_PREP(14) HPS_FDM_PREP(15) HPS_FDM_PREP(16)
+#undef HPS_FDM_PREP
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_leaf_fdm(const LeafFdmArgs& f, int grid, cudaStream_t st) {
   const size_t smem = sizeof(FdmSmem);
-  static PerDeviceFlag attr;
+  const int p = f.a.p;
+  FdmKernel k = fdm_kernel_for(p);
+  if (!k) return cudaErrorInvalidValue;
+  static PerDeviceFlag attr[17];
   const int dv = current_device();
-  if (!(attr.set >> dv & 1)) {
-    cudaError_t e = cudaFuncSetAttribute(leaf_fdm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (!(attr[p].set >> dv & 1)) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr.set |= 1ull << dv;
+    attr[p].set |= 1ull << dv;
   }
-  leaf_fdm_kernel<<<grid, kT, smem, st>>>(f);
+  k<<<grid, kT, smem, st>>>(f);
   return cudaGetLastError();
 }
 
