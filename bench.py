@@ -46,7 +46,7 @@ PAPER_H100_DOFS = 16777216 / 4.02
 FP64_PEAK_TFLOPS = 37.155     # profiles/r01_fp64_peak.json (DMMA microbench; MEASURED_PEAKS.json has no FP64 entry)
 # dram__bytes_read.sum + dram__bytes_write.sum of one leaf-stage launch at p=16 L=8, per leaf kernel
 # (ncu --set full of the current kernels, profiles/r02_ncu_summary.md)
-LEAF_KERNEL_DRAM_BYTES = {"leaf_fused_kernel": 18.89e9 + 69.29e9, "leaf_fdm_kernel": None}
+LEAF_KERNEL_DRAM_BYTES = {"leaf_fused_kernel": 18.89e9 + 69.29e9, "leaf_fdm_kernel": 4.663e9 + 7.480e9}
 
 
 def load_peaks():

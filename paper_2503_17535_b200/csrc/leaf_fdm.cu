@@ -30,7 +30,7 @@ namespace hpsk {
 namespace {
 
 constexpr int kT = 256, kW = kT / 32;
-constexpr int kNC = 16;     // right-hand sides per chunk (one block each, two per warp)
+constexpr int kNC = 8;      // block slots (one per warp)
 constexpr int kBlk = 256;   // 16 x 16 doubles
 constexpr int kMaxSteps = 12;
 #ifndef HPS_FDM_TOL
@@ -44,8 +44,8 @@ struct FdmSmem {
   double den[kBlk];  // 1 / (lam_row + lam_col + cbar), 0 in the padding
   double fsrc[256];
   int pos[256];      // tensor index -> interior r (>= 0) or -(exterior position) - 1
-  double qGt[14 * 16];  // separable Q_i: G^T ((p-2) x q, row stride 16) and d (4 x (p-2))
-  double qd[4 * 14];
+  double qDm[kBlk];  // separable Q_i as DMMA A operands (16 x 16 col-major, zero padded): rows s = d_s
+  double qGm[kBlk];  // (side normal derivatives on the interior nodes) and G (Chebyshev -> Gauss, q x (p-2))
   double wmin[kW], wmax[kW];
   int bad;
   int failed;        // this leaf did not converge
@@ -118,6 +118,15 @@ HPS_DEV double warp_max(double v) {
   return v;
 }
 
+// |v| to within a relative 2^-20 from above, as the high word of |v|: non-negative doubles order like their high
+// words, so maxima reduce on the integer pipes (one redux per warp) and stay off the FP64 pipe the DMMAs use.
+// The Richardson stopping tests only need these magnitudes as scales.
+HPS_DEV unsigned abs_hi(double v) { return (unsigned)__double2hiint(v) & 0x7fffffffu; }
+HPS_DEV double warp_max_hi(unsigned hi) {
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  return hi == 0u ? 0.0 : __hiloint2double((int)hi, (int)0xffffffffu);
+}
+
 // Solve one right-hand side block: X <- L_ii^-1 R.  Returns false if it did not converge.
 // hat: Xb already holds R^ = V^-1 R V^-T (the leaf-independent columns -L_ie P, precomputed once by
 // leaf_fdm_prep_kernel); otherwise R^ is formed here from Rb (the source column).
@@ -138,13 +147,14 @@ HPS_DEV bool solve_block(const double* Rb, double* Xb, double* Wb, const FdmSmem
   }
   store_t<false>(Wb, acc, nullptr, g, t4);
   mma_block<false>(vv, Wb, acc, g, t4);
-  double xm = 0.0;
+  unsigned xm = 0u;
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) xm = fmax(xm, fmax(fabs(acc[mt][nt][0]), fabs(acc[mt][nt][1])));
+    for (int nt = 0; nt < 2; ++nt) xm = max(xm, max(abs_hi(acc[mt][nt][0]), abs_hi(acc[mt][nt][1])));
   store_t<false>(Xb, acc, nullptr, g, t4);
-  double dprev = warp_max(xm), rbest = 1.0;
+  double dprev = warp_max_hi(xm);
+  bool contracted = false;
   // max|X_k| >= max|X_0| - sum of the corrections so far: the stopping tests use that lower bound as the
   // scale (one warp reduction per step)
   double xmax = dprev;
@@ -184,7 +194,7 @@ HPS_DEV bool solve_block(const double* Rb, double* Xb, double* Wb, const FdmSmem
     mma_block<false>(vv, Wb, acc, g, t4);
     store_t<false>(Wb, acc, nullptr, g, t4);
     mma_block<false>(vv, Wb, acc, g, t4);
-    double dm = 0.0;
+    unsigned dm = 0u;
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -194,16 +204,18 @@ HPS_DEV bool solve_block(const double* Rb, double* Xb, double* Wb, const FdmSmem
         x.x += acc[mt][nt][0];
         x.y += acc[mt][nt][1];
         *reinterpret_cast<double2*>(Xb + p) = x;
-        dm = fmax(dm, fmax(fabs(acc[mt][nt][0]), fabs(acc[mt][nt][1])));
+        dm = max(dm, max(abs_hi(acc[mt][nt][0]), abs_hi(acc[mt][nt][1])));
       }
     __syncwarp();
-    const double dk = warp_max(dm);
+    const double dk = warp_max_hi(dm);
     xmax -= dk;
     if (dk == 0.0) return true;
-    const double rho = dk / dprev;
-    if (rho < 0.5 && rho / (1.0 - rho) * dk <= kTol * xmax) return true;
-    if (dk <= 2e-15 * xmax && rbest < 0.5) return true;  // at the roundoff floor after a measured contraction
-    rbest = fmin(rbest, rho);
+    // measured contraction rho = dk / dprev; stop when the predicted remaining error rho / (1 - rho) dk is below
+    // kTol xmax, or at the roundoff floor after a contraction (division-free forms)
+    const bool contracts = 2.0 * dk < dprev;
+    if (contracts && dk * dk <= kTol * xmax * (dprev - dk)) return true;
+    if (dk <= 2e-15 * xmax && contracted) return true;
+    contracted = contracted || contracts;
     dprev = dk;
   }
   return false;
@@ -223,8 +235,11 @@ __global__ void __launch_bounds__(kT, 2) leaf_fdm_kernel(const LeafFdmArgs f) {
   load_afrag(f.A, aa, g, t4);
   for (int r = tid; r < NI; r += kT) s.pos[a.interior[r]] = r;
   for (int r = tid; r < NE; r += kT) s.pos[a.exterior[r]] = -r - 1;
-  for (int e = tid; e < N1 * N1; e += kT) s.qGt[(e % N1) * 16 + e / N1] = f.qG[e];   // G(i, m) -> qGt[m][i]
-  for (int e = tid; e < 4 * N1; e += kT) s.qd[e] = f.qd[e];
+  for (int e = tid; e < kBlk; e += kT) {
+    const int row = e & 15, col = e >> 4;
+    s.qGm[e] = (row < N1 && col < N1) ? f.qG[row * N1 + col] : 0.0;   // G(i, m), q = N1
+    s.qDm[e] = (row < 4 && col < N1) ? f.qd[row * N1 + col] : 0.0;    // d_s(k)
+  }
   __syncthreads();
 
   for (long long leaf = blockIdx.x; leaf < f.n_leaves; leaf += gridDim.x) {
@@ -296,11 +311,11 @@ __global__ void __launch_bounds__(kT, 2) leaf_fdm_kernel(const LeafFdmArgs f) {
     // ---- per warp: its columns c = warp + 1, warp + 1 + kW, ... (mod ncol; column 0, the source, goes to the last
     // warp), each solved, written and contracted to [h | T] without CTA barriers
     {
-      double* Rb = s.R + warp * 2 * kBlk;
-      double* Xb = s.X + warp * 2 * kBlk;
-      double* Wb = s.W + warp * 2 * kBlk;
+      double* Rb = s.R + warp * kBlk;
+      double* Xb = s.X + warp * kBlk;
+      double* Wb = s.W + warp * kBlk;
       bool conv = true;
-      int npass = 0;
+      int npass = 0, nout = 0;
       for (int c = warp + 1; c < ncol + 1; c += kW) {
         const int col = c == ncol ? 0 : c;
         // right-hand side: column 0 = sgn f_i (formed here); columns 1.. = -L_ie P, the same for every leaf
@@ -321,42 +336,59 @@ __global__ void __launch_bounds__(kT, 2) leaf_fdm_kernel(const LeafFdmArgs f) {
         }
         __syncwarp();
         conv = solve_block(Rb, Xb, Wb, s, vi, vv, aa, g, t4, npass, col > 0) && conv;
-        // [v_i | Y_i] column (interior index r = (i1-1) N1 + (i2-1)); X^T into W for the contractions
+        // [v_i | Y_i] column (interior index r = (i1-1) N1 + (i2-1))
         double* Yv = f.Yv + leaf * f.strideYv + (long long)col * NI;
+#pragma unroll
         for (int r = lane; r < NI; r += 32) __stcs(&Yv[r], Xb[swz(r % N1, r / N1)]);
-        for (int e = lane; e < kBlk; e += 32) {
-          const int cc = e >> 4, row = (e & 15) ^ swx(cc);
-          Wb[e] = Xb[swz(cc, row)];
-        }
-        __syncwarp();
-        // [h | T] = Q_i X + [0 | Q_e P] through the separable Q_i (geometry.cpp q_interior_factors):
-        // u_s(m) = sum_k d_s(k) X(line m, k), then h_s(i) = ds sum_m G(i, m) u_s(m).  Block element (row, col)
-        // = X(i1 = col + 1, i2 = row + 1): the S/N sides contract rows (read from X^T), E/W columns (from X).
-        double* U = Rb;  // R is free after the solve: [side][16]
-        for (int e = lane; e < 4 * N1; e += 32) {
-          const int sd = e / N1, m = e - sd * N1;
-          const double* Xs = (sd & 1) ? Xb : Wb;
-          const double* dv = s.qd + sd * N1;
-          double acc = 0.0;
+        // [h | T] = Q_i X + [0 | Q_e P] through the separable Q_i (geometry.cpp q_interior_factors), on DMMA:
+        // U = Dm X (rows S, N: u_s(m) = sum_k d_s(k) X(k, m)) and Dm X^T (rows E, W), then H = G U^T, h = ds H.
+        // Block element (row, col) = X(i1 = col + 1, i2 = row + 1).  U goes to Rb (free after the solve) as a
+        // B operand: element (m, side) at swz(m, side); rows 4..7 of Dm are zero, so are those sides.
+        {
+          double ad[4];
 #pragma unroll
-          for (int k = 0; k < N1; ++k) acc = fma(dv[k], Xs[swz(m, k)], acc);
-          U[sd * 16 + m] = acc;
-        }
-        __syncwarp();
-        double* HT = f.HT + leaf * f.strideHT + (long long)col * NB;
-        const double* zq = f.ZQeP + (long long)col * NB;
-        for (int row = lane; row < NB; row += 32) {
-          const int sd = row / N1, i = row - sd * N1;
-          const double* u = U + sd * 16;
-          double acc = 0.0;
+          for (int ks = 0; ks < 4; ++ks) ad[ks] = s.qDm[(ks * 4 + t4) * 16 + g];
+          double u[2][2][2];  // [pass][nt][h]: element (side g, m = nt * 8 + 2 t4 + h)
 #pragma unroll
-          for (int m = 0; m < N1; ++m) acc = fma(s.qGt[m * 16 + i], u[m], acc);
-          __stcs(&HT[row], f.qds * acc + __ldg(zq + row));
+          for (int ps = 0; ps < 2; ++ps)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) u[ps][nt][0] = u[ps][nt][1] = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              dmma_8x8x4(u[0][nt][0], u[0][nt][1], ad[ks], Xb[swz(ks * 4 + t4, nt * 8 + g)]);   // Dm X
+              dmma_8x8x4(u[1][nt][0], u[1][nt][1], ad[ks], Xb[swz(nt * 8 + g, ks * 4 + t4)]);   // Dm X^T
+            }
+          __syncwarp();
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) Rb[swz(nt * 8 + 2 * t4 + h, g)] = (g & 1) ? u[1][nt][h] : u[0][nt][h];
+          __syncwarp();
+          double hh[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // [mt][h]: element (i = mt * 8 + g, side = 2 t4 + h)
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const double bv = Rb[swz(ks * 4 + t4, g)];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) dmma_8x8x4(hh[mt][0], hh[mt][1], s.qGm[(ks * 4 + t4) * 16 + mt * 8 + g], bv);
+          }
+          double* HT = f.HT + leaf * f.strideHT + (long long)col * NB;
+          const double* zq = f.ZQeP + (long long)col * NB;
+          if (t4 < 2)
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int i = mt * 8 + g, row = (2 * t4 + h) * N1 + i;
+                if (i < N1) __stcs(&HT[row], f.qds * hh[mt][h] + __ldg(zq + row));
+              }
+          nout += 24;  // DMMA: two 8-row passes and one 8-column pass
+          __syncwarp();
         }
-        __syncwarp();
       }
       if (!conv && lane == 0) s.failed = 1;
-      if (lane == 0 && npass) atomicAdd(&s.ndmma, 16 * npass);
+      if (lane == 0 && npass) atomicAdd(&s.ndmma, 16 * npass + nout);
     }
     __syncthreads();
     if (tid == 0) {
