@@ -42,9 +42,6 @@ HPS_DEV void argmax_merge(double& v, int& i, double v2, int i2) {
 // candidates and pulls the pivot row (and row j for the pivot owner) through DSMEM.
 // Remote CTAs only ever read the published slots, so the local swap/elimination needs no
 // second barrier; slot reuse two columns later is ordered by the intervening barrier.
-// NBT: the panel width as a compile-time constant (32 or 16; 0 = runtime a.nb) so the row elimination below
-// is unrolled with all of a row's loads in flight before its FMAs.
-template <int NBT>
 __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelArgs a) {
   extern __shared__ __align__(16) double sm[];
   double* pan = sm;                               // [nb][rpc]
@@ -66,7 +63,7 @@ __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelA
   const int rows_total = a.n - a.j0;
   const int r_begin = rank * a.rpc;
   const int nr = max(0, min(rows_total - r_begin, a.rpc));
-  const int nb = NBT ? NBT : a.nb;
+  const int nb = a.nb;
 
   for (int e = tid; e < nr * nb; e += nthr) {  // cp.async: all of a thread's loads in flight
     const int r = e % nr, c = e / nr;
@@ -179,19 +176,7 @@ __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelA
       if (apv > 0.0) {
         const double l = (swapped ? jrow[j] : pan[j * a.rpc + r]) * inv;
         pan[j * a.rpc + r] = l;
-        if (NBT) {
-          const double* src = swapped ? jrow : pan + r;
-          const int sst = swapped ? 1 : a.rpc;
-          double v[NBT > 0 ? NBT : 1], u[NBT > 0 ? NBT : 1];
-#pragma unroll
-          for (int c = 0; c < NBT; ++c)
-            if (c > j) v[c] = src[c * sst], u[c] = urow[c];
-#pragma unroll
-          for (int c = 0; c < NBT; ++c)
-            if (c > j) pan[c * a.rpc + r] = v[c] - l * u[c];
-        } else {
-          for (int c = j + 1; c < nb; ++c) pan[c * a.rpc + r] = (swapped ? jrow[c] : pan[c * a.rpc + r]) - l * urow[c];
-        }
+        for (int c = j + 1; c < nb; ++c) pan[c * a.rpc + r] = (swapped ? jrow[c] : pan[c * a.rpc + r]) - l * urow[c];
       } else if (swapped) {
         for (int c = j; c < nb; ++c) pan[c * a.rpc + r] = jrow[c];
       }
@@ -407,23 +392,21 @@ cudaError_t launch_panel(int batch, int n, int j0, int nb, BatchedMat M, int* ip
   if (cs == 1) rpc = rows;
   PanelArgs pa{M.p, M.ld, M.stride, n, j0, nb, rpc, cs, ipiv, stats};
   const size_t smem = (size_t)rpc * nb * 8 + 6 * kLuNB * 8 + (kPanelThreads / 32) * 12 + 128;
-  void (*kern)(const PanelArgs) = nb == 32 ? panel_getrf_kernel<32> : nb == 16 ? panel_getrf_kernel<16> : panel_getrf_kernel<0>;
-  const int ki = nb == 32 ? 0 : nb == 16 ? 1 : 2;
-  static PerDeviceFlag smem_set[3];
+  static PerDeviceFlag smem_set;
   const int dv = current_device();
-  if (smem > smem_set[ki].value[dv]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (smem > smem_set.value[dv]) {
+    cudaError_t e = cudaFuncSetAttribute(panel_getrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 48 * 1024));
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(panel_getrf_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
-    smem_set[ki].value[dv] = std::max<size_t>(smem, 48 * 1024);
+    smem_set.value[dv] = std::max<size_t>(smem, 48 * 1024);
   }
   if (cs == 1) {
     // single-CTA panels: one thread per row up to kPanelThreads (the 56- and 112-row panels of the
     // deep merge levels would otherwise run 4-6 warps with no rows through every barrier)
     const int threads = std::min(kPanelThreads, std::max(32, (rpc + 31) / 32 * 32));
-    kern<<<batch, threads, smem, st>>>(pa);
+    panel_getrf_kernel<<<batch, threads, smem, st>>>(pa);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -438,7 +421,7 @@ cudaError_t launch_panel(int batch, int n, int j0, int nb, BatchedMat M, int* ip
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, pa);
+  return cudaLaunchKernelEx(&cfg, panel_getrf_kernel, pa);
 }
 
 cudaError_t launch_swap_trsm(int batch, int n, int j0, int nb, const double* L, long long ldL, long long strideL,
