@@ -1,0 +1,96 @@
+"""The fast-diagonalisation leaf solve (csrc/leaf_fdm.cu) against the LU leaf kernel and the oracle.
+
+The FDM path replaces the leaf LU (proj/src/local_solve.cpp:111-143) for operators whose second-order part
+is one constant Laplacian term (the headline Helmholtz problem): L_ii = K + diag(c), solved by Richardson on the
+true operator, preconditioned with the exactly diagonalisable K + cbar I.  Its fixed point is L_ii^-1 R, so the
+leaf artifacts equal the LU ones to roundoff (tolerance 1e-12 relative; measured ~5e-15) and the solution meets
+the north-star 1e-10 against the oracle.  Leaves that do not converge fall back to the LU kernel.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+import paper_2503_17535_b200 as H  # noqa: E402
+from paper_2503_17535_b200 import problems as PR  # noqa: E402
+from tests.oracle_problems import oracle_solver  # noqa: E402
+
+LEAF_PATH_FDM, LEAF_PATH_FDM_FALLBACK, LEAF_PATH_FUSED_LU = 2, 3, 0
+
+
+def rel(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(np.asarray(b)).max(), 1e-300))
+
+
+def solver(prob, p, L, fdm=True, literal=True):
+    tree = H.build_uniform_tree(prob.lo, prob.hi, L, prob.dim, p)
+    s = H.HpsSolver(tree, prob.terms, prob.source, literal_sign=literal, root_implicit_S=True, fdm_leaf=fdm)
+    s.build()
+    return s
+
+
+def test_fdm_path_selection():
+    """Constant Laplacian + zeroth order -> FDM; variable first-order terms (poisson2d) -> LU kernel."""
+    h = solver(PR.helmholtz_bumps(), 16, 4)
+    assert h.stats()["leaf_path"] in (LEAF_PATH_FDM, LEAF_PATH_FDM_FALLBACK)
+    assert h.stats()["leaf_exec_flops"] > 0
+    p = solver(PR.poisson2d(), 16, 3)
+    assert p.stats()["leaf_path"] == LEAF_PATH_FUSED_LU
+    assert p.stats()["leaf_exec_flops"] == 0
+    f = solver(PR.helmholtz_bumps(), 16, 4, fdm=False)
+    assert f.stats()["leaf_path"] == LEAF_PATH_FUSED_LU
+
+
+@pytest.mark.parametrize("p,L", [(16, 4), (16, 5), (12, 4), (8, 5)])
+def test_fdm_leaf_artifacts_equal_lu(p, L):
+    """[v | Y_i] and [h | T] of FDM leaves equal the LU kernel's to roundoff; the solutions agree."""
+    prob = PR.helmholtz_bumps()
+    a, b = solver(prob, p, L), solver(prob, p, L, fdm=False)
+    assert a.stats()["leaf_path"] in (LEAF_PATH_FDM, LEAF_PATH_FDM_FALLBACK)
+    n = a.tree.n_leaves
+    for o in (0, 1, n // 3, n - 1):
+        for x, y in zip(a.get_leaf(o), b.get_leaf(o)):
+            assert rel(x, y) < 1e-12
+    g = prob.boundary(a.root_boundary_points())
+    assert rel(a.solve(g), b.solve(g)) < 1e-10
+
+
+@pytest.mark.parametrize("p,L", [(16, 3), (16, 5), (12, 4)])
+@pytest.mark.parametrize("literal", [True, False])
+def test_fdm_solution_vs_oracle(p, L, literal):
+    """North-star parity (1e-10) of the FDM build against the oracle, both sign conventions.  L = 3 at k = 30 has
+    leaves whose Richardson contraction is too weak: they fall back to the LU kernel (leaf_path 3)."""
+    prob = PR.helmholtz_bumps()
+    s = solver(prob, p, L, literal=literal)
+    o = oracle_solver(prob, p, L, literal=literal, root_implicit=True, parallel=True)
+    o.build()
+    g = prob.boundary(s.root_boundary_points())
+    assert rel(s.solve(g), o.solve(g)) < 1e-10
+    if (p, L) == (16, 3):
+        assert s.stats()["leaf_path"] == LEAF_PATH_FDM_FALLBACK
+
+
+def test_fdm_executed_flops_bounds():
+    """Device DMMA count: every column runs its initial solve (2 passes of 16 DMMA.8x8x4 = 8192 FLOP each for
+    the precomputed R^ columns, 4 for the source column) plus 1 .. kMaxSteps = 12 Richardson steps of 6 passes,
+    and 24 DMMA for its [h | T] contraction."""
+    prob = PR.helmholtz_bumps()
+    s = solver(prob, 16, 5)   # L = 5: every leaf converges (no LU fallback)
+    st = s.stats()
+    assert st["leaf_path"] == LEAF_PATH_FDM
+    ncol, nl = 57, s.tree.n_leaves
+    per_pass = 16 * 512
+    lo = nl * ncol * (2 + 6) * per_pass
+    hi = nl * ncol * (4 + 6 * 12) * per_pass + nl * ncol * 24 * 512
+    assert lo <= st["leaf_exec_flops"] <= hi
+
+
+def test_fdm_repeated_builds_identical():
+    """The leaf-independent right-hand side tables are prepared once per context: a second build is bitwise
+    identical to the first."""
+    prob = PR.helmholtz_bumps()
+    s = solver(prob, 16, 4)
+    g = prob.boundary(s.root_boundary_points())
+    u0 = s.solve(g)
+    s.build()
+    assert np.array_equal(s.solve(g), u0)
