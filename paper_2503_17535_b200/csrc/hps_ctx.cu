@@ -159,7 +159,22 @@ void set_terms(hpsg_ctx* c, const hpsg_term* terms, int n_terms, const hpsg_fiel
     c->terms[i].role = t.role;
     c->terms[i].axis = t.axis;
     c->terms[i].axis2 = t.axis2;
-    c->terms[i].f = make_dev_field(c, prep(t.field), false);
+    hpsg_field fld = t.field;
+    if (t.role == HPSG_ROLE_LAPLACIAN && fld.kind == HPSG_FIELD_SAMPLED && fld.samples) {
+      // a host-sampled Laplacian coefficient that is one value everywhere (the usual std::function returning
+      // a constant) is that constant: the leaf operators are bit-identical, and the fast-diagonalisation leaf
+      // solve applies (setup_fdm requires a CONST Laplacian coefficient)
+      const size_t n = size_t(c->gen ? gen_n_leaves(c) : c->T.n_leaves()) * c->ops.n;
+      const double v0 = fld.samples[0];
+      bool same = n > 0 && std::isfinite(v0);
+      for (size_t k = 1; same && k < n; ++k) same = std::memcmp(&fld.samples[k], &v0, sizeof(double)) == 0;
+      if (same) {
+        fld = hpsg_field{};
+        fld.kind = HPSG_FIELD_CONST;
+        fld.c[0] = v0;
+      }
+    }
+    c->terms[i].f = make_dev_field(c, prep(fld), false);
   }
   if (source) {
     c->source = make_dev_field(c, prep(*source), true);

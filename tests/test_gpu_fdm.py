@@ -94,3 +94,27 @@ def test_fdm_repeated_builds_identical():
     u0 = s.solve(g)
     s.build()
     assert np.array_equal(s.solve(g), u0)
+
+
+def test_sampled_constant_laplacian_takes_fdm():
+    """A host-sampled Laplacian coefficient that is one value everywhere (a std::function returning a constant,
+    the C++ adapter's path) is recognised as that constant: the FDM leaf applies and the build is bitwise the
+    built-in constant field's.  A sampled coefficient with one differing sample stays on the LU kernel."""
+    prob = PR.helmholtz_bumps()
+    tree = H.build_uniform_tree(prob.lo, prob.hi, 4, 2, 16)
+    a = H.HpsSolver(tree, prob.terms, prob.source, root_implicit_S=True)
+    a.build()
+    lap = prob.terms[0].field.c[0]
+    smp = np.full((tree.n_leaves, 16 * 16), lap)
+    b = H.HpsSolver(tree, [H.Term(H.ROLE_LAPLACIAN, H.Field(H.FIELD_SAMPLED, samples=smp)), prob.terms[1]],
+                    prob.source, root_implicit_S=True)
+    b.build()
+    assert b.stats()["leaf_path"] in (LEAF_PATH_FDM, LEAF_PATH_FDM_FALLBACK)
+    g = prob.boundary(a.root_boundary_points())
+    assert np.array_equal(a.solve(g), b.solve(g))
+    smp2 = smp.copy()
+    smp2[3, 7] = np.nextafter(lap, 2 * lap)
+    c = H.HpsSolver(tree, [H.Term(H.ROLE_LAPLACIAN, H.Field(H.FIELD_SAMPLED, samples=smp2)), prob.terms[1]],
+                    prob.source, root_implicit_S=True)
+    c.build()
+    assert c.stats()["leaf_path"] == LEAF_PATH_FUSED_LU
