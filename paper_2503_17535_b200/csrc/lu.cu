@@ -1056,6 +1056,69 @@ __global__ void __launch_bounds__(256) slab_trsv_kernel(const double* T, long lo
   }
 }
 
+// The same slab solve on a cluster of 8 CTAs: CTA j owns the slab's 32-row block j and loads its part of the
+// slab's T at once (8 CTAs' loads in flight instead of one CTA staging 8 column blocks one after another).
+// Step k (k = 0..7 for L, 7..0 for U): CTA k solves its diagonal block (the shuffle chain of slab_trsv_kernel)
+// and publishes x_k; after one cluster barrier every CTA still to be solved pulls x_k through DSMEM and
+// subtracts T_jk x_k.  Per row the subtractions happen in the same order with the same FMA chains as
+// slab_trsv_kernel, so the results are bit-identical.
+constexpr int kTrsvCluster = kOuterNB / kLuNB;  // 8
+template <bool UPPER>
+__global__ void __launch_bounds__(128) slab_trsv_cluster_kernel(const double* T, long long ldT, int r0, int nbk,
+                                                                 double* X, long long ldX, int m) {
+  extern __shared__ __align__(16) double tb[];  // [kOuterNB columns][kLuNB rows]: this CTA's rows of the slab
+  __shared__ double xpub[kTrsvMaxRhs][kLuNB];
+  const int j = (int)cluster_ctarank();
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int nblk = (nbk + kLuNB - 1) / kLuNB;
+  const int rj0 = j * kLuNB, nbj = max(0, min(kLuNB, nbk - rj0));
+  const int c_lo = UPPER ? rj0 : 0, c_hi = UPPER ? nbk : rj0 + nbj;
+  if (nbj > 0) {
+    for (int e = tid; e < (c_hi - c_lo) * kLuNB; e += blockDim.x) {
+      const int c = c_lo + e / kLuNB, rr = e % kLuNB;
+      const bool ok = rr < nbj;
+      cp_async8(tb + c * kLuNB + rr, ok ? T + (long long)(r0 + c) * ldT + r0 + rj0 + rr : T, ok);
+    }
+  }
+  cp_async_commit();
+  double x = (w < m && lane < nbj) ? X[(long long)w * ldX + r0 + rj0 + lane] : 0.0;
+  cp_async_wait<0>();
+  __syncthreads();
+  for (int step = 0; step < nblk; ++step) {
+    const int k = UPPER ? nblk - 1 - step : step;
+    if (j == k && w < m) {
+      const int nb = nbj;
+      if (!UPPER) {
+        for (int kk = 0; kk < nb; ++kk) {
+          const double xk = __shfl_sync(0xffffffffu, x, kk);
+          if (lane > kk && lane < nb) x -= tb[(rj0 + kk) * kLuNB + lane] * xk;
+        }
+      } else {
+        const double dinv = lane < nb ? 1.0 / tb[(rj0 + lane) * kLuNB + lane] : 0.0;
+        for (int kk = nb - 1; kk >= 0; --kk) {
+          if (lane == kk) x *= dinv;
+          const double xk = __shfl_sync(0xffffffffu, x, kk);
+          if (lane < kk) x -= tb[(rj0 + kk) * kLuNB + lane] * xk;
+        }
+      }
+      xpub[w][lane] = x;
+    }
+    cluster_sync();
+    if ((UPPER ? j < k : j > k) && w < m && nbj > 0) {
+      const double xk = dsmem_ld_f64(dsmem_map(&xpub[w][lane], k));  // lane c: x_k[c]
+      const int nbk_k = min(kLuNB, nbk - k * kLuNB);
+      double acc = 0.0;
+      for (int c = 0; c < nbk_k; ++c) {
+        const double v = __shfl_sync(0xffffffffu, xk, c);
+        acc += tb[(k * kLuNB + c) * kLuNB + lane] * v;
+      }
+      if (lane < nbj) x -= acc;
+    }
+  }
+  if (w < m && lane < nbj) X[(long long)w * ldX + r0 + rj0 + lane] = x;
+  cluster_sync();  // the last step's DSMEM reads are done before any CTA exits
+}
+
 // X <- T^-1 X for one matrix (unit-lower L or upper U of an LU), m <= kTrsvMaxRhs
 constexpr long long kTrsvScratch = 1LL << 20;  // doubles of split-k partial sums (8 MB)
 
@@ -1073,11 +1136,36 @@ cudaError_t trsv_blocked(const double* T, long long ldT, int n, double* X, long 
     static PerDeviceFlag attr;
     const int dv = current_device();
     if (!(attr.set >> dv & 1)) {
-      HPS_TRY(cudaFuncSetAttribute(slab_trsv_kernel<UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      HPS_TRY(cudaFuncSetAttribute(slab_trsv_cluster_kernel<UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
       attr.set |= 1ull << dv;
     }
-    slab_trsv_kernel<UPPER><<<1, 256, smem, st>>>(T, ldT, J, Jend - J, X, ldX, m);
-    HPS_TRY(cudaGetLastError());
+#ifndef HPS_TRSV_CLUSTER
+#define HPS_TRSV_CLUSTER 1
+#endif
+    if (!HPS_TRSV_CLUSTER) {  // developer A/B: the one-CTA slab solve
+      static PerDeviceFlag attr1;
+      if (!(attr1.set >> dv & 1)) {
+        HPS_TRY(cudaFuncSetAttribute(slab_trsv_kernel<UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr1.set |= 1ull << dv;
+      }
+      slab_trsv_kernel<UPPER><<<1, 256, smem, st>>>(T, ldT, J, Jend - J, X, ldX, m);
+      HPS_TRY(cudaGetLastError());
+    } else {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(kTrsvCluster);
+      cfg.blockDim = dim3(128);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = kTrsvCluster;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      HPS_TRY(cudaLaunchKernelEx(&cfg, slab_trsv_cluster_kernel<UPPER>, T, ldT, J, Jend - J, X, ldX, m));
+    }
     GemvArgs g;  // the rows outside the slab: X_rest -= T[rest, J:Jend] X_slab
     g.m = UPPER ? J : n - Jend;
     g.k = Jend - J;
