@@ -14,7 +14,14 @@ namespace hpsk {
 
 namespace {
 
-constexpr int kPanelThreads = 256;
+#ifndef HPS_PANEL_THREADS
+#define HPS_PANEL_THREADS 512
+#endif
+#ifndef HPS_PANEL_UNROLL
+#define HPS_PANEL_UNROLL 4
+#endif
+constexpr int kPanelThreads = HPS_PANEL_THREADS;
+constexpr int kPanelUnroll = HPS_PANEL_UNROLL;
 constexpr int kRowsPerCta = 448;  // 448 x 32 doubles = 112 KiB of panel per CTA
 constexpr int kMaxCluster = 16;   // non-portable cluster size (same GPC)
 constexpr int kMaxRowsPerCta = 864;
@@ -176,6 +183,7 @@ __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelA
       if (apv > 0.0) {
         const double l = (swapped ? jrow[j] : pan[j * a.rpc + r]) * inv;
         pan[j * a.rpc + r] = l;
+#pragma unroll kPanelUnroll
         for (int c = j + 1; c < nb; ++c) pan[c * a.rpc + r] = (swapped ? jrow[c] : pan[c * a.rpc + r]) - l * urow[c];
       } else if (swapped) {
         for (int c = j; c < nb; ++c) pan[c * a.rpc + r] = jrow[c];
