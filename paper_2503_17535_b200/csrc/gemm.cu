@@ -99,8 +99,20 @@ bool run_tma(const GemmArgs& a, cudaStream_t st, cudaError_t* err) {
   return true;
 }
 
+#ifndef HPS_GEMM_BM
+#define HPS_GEMM_BM 64
+#endif
+#ifndef HPS_GEMM_BN
+#define HPS_GEMM_BN 64
+#endif
+#ifndef HPS_GEMM_BK
+#define HPS_GEMM_BK 16
+#endif
+#ifndef HPS_GEMM_ST
+#define HPS_GEMM_ST 3
+#endif
 bool launch_dgemm_tma(const GemmArgs& a, cudaStream_t st, cudaError_t* err) {
-  return run_tma<64, 64, 16, 32, 32, 3>(a, st, err);
+  return run_tma<HPS_GEMM_BM, HPS_GEMM_BN, HPS_GEMM_BK, 32, 32, HPS_GEMM_ST>(a, st, err);
 }
 
 // Live GEMM timing (hpsg_dev_gemm_timing): while enabled, every launch is bracketed by CUDA events on

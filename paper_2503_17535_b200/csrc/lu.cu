@@ -22,7 +22,10 @@ namespace {
 #endif
 constexpr int kPanelThreads = HPS_PANEL_THREADS;
 constexpr int kPanelUnroll = HPS_PANEL_UNROLL;
-constexpr int kRowsPerCta = 448;  // 448 x 32 doubles = 112 KiB of panel per CTA
+#ifndef HPS_PANEL_ROWS
+#define HPS_PANEL_ROWS 448
+#endif
+constexpr int kRowsPerCta = HPS_PANEL_ROWS;  // 448 x 32 doubles = 112 KiB of panel per CTA
 constexpr int kMaxCluster = 16;   // non-portable cluster size (same GPC)
 constexpr int kMaxRowsPerCta = 864;
 constexpr int kTrsvMaxRhs = 4;    // few-RHS triangular solves (slab_trsv_kernel): right-hand sides per call
