@@ -119,7 +119,9 @@ typedef struct {
   int n_levels;                /* = tree depth L */
   double t_level_ms[24];       /* merge time of depth d (CUDA events), d = 0 .. L-1 */
   int leaf_path;               /* last build's leaf stage: 0 fused LU kernel, 1 batched LU, 2 fast
-                                  diagonalisation, 3 fast diagonalisation that fell back to the fused LU */
+                                  diagonalisation, 3 fast diagonalisation that fell back to the fused LU,
+                                  4 ItI by block elimination (fast-diagonalisation interior solve + reduced
+                                  boundary LU), 5 ItI block elimination that fell back to the full LU */
   double leaf_exec_flops;      /* fast-diagonalisation leaf stage: FP64 tensor FLOPs it executed (DMMA.8x8x4
                                   instructions x 512, counted on the device); 0 for the LU leaf paths */
 } hpsg_stats;

@@ -142,7 +142,8 @@ struct hpsg_ctx {
   int fdm_grid = 0;
   double fdm_lap = 0.0, fdm_qds = 0.0;
   DevBuf fdmV, fdmVinv, fdmA, fdmLam, fdmFail, fdmQG, fdmQd, fdmRtab, fdmRhat;
-  bool fdm_prepped = false;  // fdmFail: count + list of non-converged leaves
+  bool fdm_prepped = false;
+  DevBuf itiGire, itiGiim, itiGere, itiGeim, itiGAt, itiGAb, itiPc, fdmPid, itiPos;  // ItI block elimination operands  // fdmFail: count + list of non-converged leaves
   double* yv = nullptr;        // [v_i | Y_i] of leaf 0 (ni x (1+nb), ld ni)
   long long yv_stride = 0;
   // merges

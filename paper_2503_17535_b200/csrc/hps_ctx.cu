@@ -334,9 +334,12 @@ void setup(hpsg_ctx* c) {
 // plus zeroth-order terms on a uniform 2D tree (the leaf operator is K + diag(c) with K = I (x) A + A (x) I the
 // same for every leaf).  A = s^2 (a D2[int, int]) with the rounding of leaf_entry; V, lam from the host
 // eigendecomposition (geometry.cpp), zero padded to 16 x 16 for the DMMA passes.
+// ItI (c->iti): the same interior solve serves local_solve_iti by block elimination of the leaf system
+// [G; L_int] (local_solve.cpp:145-172) -- see run_leaf_stage.
 void setup_fdm(hpsg_ctx* c) {
   const hpsg::LeafOperators& o = c->ops;
-  if (c->tree.dim != 2 || c->iti || c->opts.keep_factors || !hpsk::leaf_fdm_shape_ok(o.p, o.ni, o.nb, 2)) return;
+  const int pp = c->tree.p, n1p = pp - 2;
+  if (c->tree.dim != 2 || c->opts.keep_factors || !hpsk::leaf_fdm_shape_ok(pp, n1p * n1p, 4 * n1p, 2)) return;
   int nlap = 0;
   double a = 0.0;
   for (int i = 0; i < c->nterms; ++i) {
@@ -349,11 +352,12 @@ void setup_fdm(hpsg_ctx* c) {
     }
   }
   if (nlap != 1 || !(a != 0.0) || !std::isfinite(a)) return;
-  const int n1 = o.p - 2;
+  const int n1 = pp - 2;
   const double sc = 2.0 / c->T.leaf_side, s2 = sc * sc;
   std::vector<double> A(size_t(n1) * n1), lam, V, Vi;
   for (int j = 0; j < n1; ++j)
     for (int i = 0; i < n1; ++i) A[size_t(j) * n1 + i] = s2 * (a * o.D2(i + 1, j + 1));
+  (void)n1p;
   if (!hpsg::real_eigendecomposition(A, n1, lam, V, Vi)) return;
   auto pad = [n1](const std::vector<double>& M) {
     std::vector<double> out(256, 0.0);
@@ -367,17 +371,62 @@ void setup_fdm(hpsg_ctx* c) {
   upload(c->fdmVinv, pad(Vi), &c->dev_bytes, c->st);
   upload(c->fdmA, pad(A), &c->dev_bytes, c->st);
   upload(c->fdmLam, lp, &c->dev_bytes, c->st);
-  std::vector<double> qG, qd;
-  hpsg::q_interior_factors(o, qG, qd, c->fdm_qds);
-  upload(c->fdmQG, qG, &c->dev_bytes, c->st);
-  upload(c->fdmQd, qd, &c->dev_bytes, c->st);
-  c->fdmRtab.alloc(sizeof(double) * 256 * size_t(o.nb), &c->dev_bytes);
-  c->fdmRhat.alloc(sizeof(double) * 256 * size_t(o.nb), &c->dev_bytes);
+  size_t ntab = size_t(o.nb);
+  if (!c->iti) {
+    std::vector<double> qG, qd;
+    hpsg::q_interior_factors(o, qG, qd, c->fdm_qds);
+    upload(c->fdmQG, qG, &c->dev_bytes, c->st);
+    upload(c->fdmQd, qd, &c->dev_bytes, c->st);
+  } else {
+    // block elimination operands (all leaves share them): G split by exterior / interior columns, the stacked
+    // real-equivalent G_i rows for the source term, [[P, 0], [0, P]], and P = I for the -L_ie tables
+    const hpsg::ItiLeafOperators& io = c->iops;
+    const int nbc = io.nbc, ne = 4 * pp - 4, nir = n1p * n1p, nbq = io.nb;
+    ntab = size_t(ne);
+    std::vector<double> gire(size_t(nbc) * nir), giim(size_t(nbc) * nir), gere(size_t(nbc) * ne),
+        geim(size_t(nbc) * ne), gat(size_t(nbc) * 2 * nir), gab(size_t(nbc) * 2 * nir),
+        pc(size_t(2 * nbc) * 2 * nbq, 0.0), pid(size_t(ne) * ne, 0.0);
+    for (int k = 0; k < nir; ++k)
+      for (int r = 0; r < nbc; ++r) {
+        const double gr = io.Gr(r, o.interior[k]), gi = io.Gi(r, o.interior[k]);
+        gire[size_t(k) * nbc + r] = gr;
+        giim[size_t(k) * nbc + r] = gi;
+        gat[size_t(k) * nbc + r] = gr;
+        gat[size_t(nir + k) * nbc + r] = -gi;
+        gab[size_t(k) * nbc + r] = gi;
+        gab[size_t(nir + k) * nbc + r] = gr;
+      }
+    for (int e = 0; e < ne; ++e)
+      for (int r = 0; r < nbc; ++r) {
+        gere[size_t(e) * nbc + r] = io.Gr(r, o.exterior[e]);
+        geim[size_t(e) * nbc + r] = io.Gi(r, o.exterior[e]);
+      }
+    for (int j = 0; j < nbq; ++j)
+      for (int r = 0; r < nbc; ++r) {
+        pc[size_t(j) * 2 * nbc + r] = io.P(r, j);
+        pc[size_t(nbq + j) * 2 * nbc + nbc + r] = io.P(r, j);
+      }
+    for (int e = 0; e < ne; ++e) pid[size_t(e) * ne + e] = 1.0;
+    std::vector<int> pos(size_t(pp) * pp, 0);
+    for (int k = 0; k < nir; ++k) pos[size_t(o.interior[k])] = k;
+    for (int e = 0; e < ne; ++e) pos[size_t(o.exterior[e])] = -e - 1;
+    upload(c->itiPos, pos, &c->dev_bytes, c->st);
+    upload(c->itiGire, gire, &c->dev_bytes, c->st);
+    upload(c->itiGiim, giim, &c->dev_bytes, c->st);
+    upload(c->itiGere, gere, &c->dev_bytes, c->st);
+    upload(c->itiGeim, geim, &c->dev_bytes, c->st);
+    upload(c->itiGAt, gat, &c->dev_bytes, c->st);
+    upload(c->itiGAb, gab, &c->dev_bytes, c->st);
+    upload(c->itiPc, pc, &c->dev_bytes, c->st);
+    upload(c->fdmPid, pid, &c->dev_bytes, c->st);
+  }
+  c->fdmRtab.alloc(sizeof(double) * 256 * ntab, &c->dev_bytes);
+  c->fdmRhat.alloc(sizeof(double) * 256 * ntab, &c->dev_bytes);
   c->fdm_prepped = false;
   c->fdmFail.alloc(sizeof(int) * (1 + size_t(c->T.n_leaves())), &c->dev_bytes);
   int nsm = 0;
   ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->opts.device), "sm count");
-  c->fdm_grid = int(std::min<long long>(c->T.n_leaves(), (long long)nsm * hpsk::leaf_fdm_ctas_per_sm(o.p)));
+  c->fdm_grid = int(std::min<long long>(c->T.n_leaves(), (long long)nsm * hpsk::leaf_fdm_ctas_per_sm(pp)));
   c->fdm_lap = a;
   c->fdm = true;
 }
@@ -393,7 +442,7 @@ void alloc_build(hpsg_ctx* c) {
   if (c->opts.keep_factors || c->iti) c->fused = false;  // batched path: keeps [LU | v | Y] + pivots; ItI
   if (c->T.cut) c->fused = false;  // no leaf stage: the part's leaves are input nodes
   c->fdm = false;
-  if (c->fused && !c->opts.force_lu_leaf) setup_fdm(c);
+  if ((c->fused || c->iti) && !c->opts.force_lu_leaf) setup_fdm(c);
   if (c->T.cut) {
     // no leaf stage
   } else if (c->fused) {
@@ -509,6 +558,151 @@ void check_merge_errors(hpsg_ctx* c) {
   }
 }
 
+// local_solve_iti (local_solve.cpp:145-172) by block elimination of the leaf system b = [G; L_int] (G: the
+// impedance rows on the 4p-4 boundary points, L_int: the interior rows of the real operator):
+//   Z = L_ii^-1 [f_i | -L_ie]                                   (fast-diagonalisation solve, real)
+//   S = G_e + G_i W,  W = -L_ii^-1 L_ie  (complex 4p-4 square)   the reduced boundary system
+//   S [u_e(v) | u_e(Y) | u_e(iY)] = [-G_i z | P | iP]            (real-equivalent batched LU, 2(4p-4))
+//   u_i = W u_e (+ z for v),  u = [u_e; u_i] scattered to tensor order: the same [v | Y | iY] the real-
+// equivalent LU of b produces, to roundoff.  Scratch lives in leafM's (unused here) system block.  Returns false
+// when some leaf's Richardson iteration did not converge (the caller then runs the LU path for all leaves).
+bool run_iti_fdm_leaf(hpsg_ctx* c, const hpsk::LeafAsmArgs& a0) {
+  const hpsg::ItiLeafOperators& io = c->iops;
+  const hpsg::LeafOperators& o = c->ops;
+  const int nl = c->T.n_leaves();
+  const long long sM = c->strideLeafM();
+  const int p = c->tree.p, n1 = p - 2, nir = n1 * n1, ne = 4 * p - 4, nbc = io.nbc, nbq = io.nb, n = io.n;
+  const int ld2 = 2 * n, mrhs = 1 + 2 * nbq, ls = 2 * nbc;
+  if (nbc != ne || o.ni != ld2) return false;
+  double* base = c->leafM.d();
+  const long long zoff = 0, soff = (long long)nir * (2 + ne), uoff = soff + (long long)ls * (ls + mrhs);
+  if (uoff + 2LL * nir * mrhs > (long long)ld2 * ld2) return false;
+  hpsk::LeafFdmArgs f{};
+  f.a = a0;
+  f.a.n = n;
+  f.a.ni = nir;
+  f.a.ne = ne;
+  f.a.nb = 4 * n1;
+  f.a.fsign = 1.0;  // local_solve_iti: rhs_v = f_i (no sign flip)
+  f.P = c->fdmPid.d();
+  f.V = c->fdmV.d();
+  f.Vinv = c->fdmVinv.d();
+  f.A = c->fdmA.d();
+  f.lam = c->fdmLam.d();
+  f.lap_coef = c->fdm_lap;
+  f.Rtab = c->fdmRtab.d();
+  f.Rhat = c->fdmRhat.d();
+  f.Yv = base + zoff;
+  f.strideYv = sM;
+  f.stats = c->leafStats.d();
+  f.fail_count = c->fdmFail.i();
+  f.fail_list = c->fdmFail.i() + 1;
+  f.n_leaves = nl;
+  f.iti = 1;
+  f.source_im = c->source_im;
+  f.has_source_im = c->has_source_im;
+  ck(cudaMemsetAsync(c->fdmFail.p, 0, sizeof(int), c->st), "fdm flag");
+  if (!c->fdm_prepped) {
+    ck(hpsk::launch_leaf_fdm_prep(f, c->st), "leaf_fdm_prep");
+    ++c->launches;
+    c->fdm_prepped = true;
+  }
+  ck(hpsk::launch_leaf_fdm(f, c->fdm_grid, c->st), "leaf_fdm (ItI)");
+  ++c->launches;
+  int nfail = 0;
+  ck(cudaMemcpyAsync(&nfail, c->fdmFail.p, sizeof(int), cudaMemcpyDeviceToHost, c->st), "fdm count D2H");
+  ck(cudaStreamSynchronize(c->st), "fdm sync");
+  if (nfail) return false;
+  // reduced boundary system S~ = [[S_re, -S_im], [S_im, S_re]] with the right-hand sides riding along
+  double* St = base + soff;
+  const double* W = base + zoff + 2LL * nir;
+  auto sgemm = [&](double* D, const double* A, const double* Cm, double alpha, double beta) {
+    GemmArgs g;
+    g.m = nbc;
+    g.n = ne;
+    g.k = nir;
+    g.batch = nl;
+    g.A = A;
+    g.lda = nbc;
+    g.sA = 0;
+    g.B = W;
+    g.ldb = nir;
+    g.sB = sM;
+    g.C = Cm;
+    g.ldc = nbc;
+    g.sC = 0;
+    g.D = D;
+    g.ldd = ls;
+    g.sD = sM;
+    g.alpha = alpha;
+    g.beta = beta;
+    gemm(c, g);
+  };
+  sgemm(St, c->itiGire.d(), c->itiGere.d(), 1.0, 1.0);                            // S_re
+  sgemm(St + (long long)ne * ls + nbc, c->itiGire.d(), c->itiGere.d(), 1.0, 1.0);  // S_re
+  sgemm(St + nbc, c->itiGiim.d(), c->itiGeim.d(), 1.0, 1.0);                       // S_im
+  sgemm(St + (long long)ne * ls, c->itiGiim.d(), c->itiGeim.d(), -1.0, -1.0);     // -S_im
+  for (int half = 0; half < 2; ++half) {  // -G_i z: [re; im] from the stacked real-equivalent rows of G_i
+    GemmArgs g;
+    g.m = nbc;
+    g.n = 1;
+    g.k = 2 * nir;
+    g.batch = nl;
+    g.A = half ? c->itiGAb.d() : c->itiGAt.d();
+    g.lda = nbc;
+    g.sA = 0;
+    g.B = base + zoff;
+    g.ldb = 2 * nir;
+    g.sB = sM;
+    g.D = St + (long long)2 * ne * ls + half * nbc;
+    g.ldd = ls;
+    g.sD = sM;
+    g.alpha = -1.0;
+    g.beta = 0.0;
+    gemm(c, g);
+  }
+  hpsk::launch_copy_batched(St + (long long)(2 * ne + 1) * ls, ls, sM, c->itiPc.d(), ls, 0, ls, 2 * nbq, nl, c->st);
+  ++c->launches;
+  ck(hpsk::lu_stats_init(c->leafStats.d(), nl, c->st), "stats init");
+  ck(hpsk::bgetrf_aug(nl, ls, mrhs, BatchedMat{St, ls, sM}, c->leafPiv.i(), c->leafStats.d(), c->luws, c->st, false),
+     "iti reduced boundary LU");
+  c->launches += lu_launches(ls, mrhs, true);
+  // interior unknowns u_i = W u_e (re and im halves)
+  for (int half = 0; half < 2; ++half) {
+    GemmArgs g;
+    g.m = nir;
+    g.n = mrhs;
+    g.k = ne;
+    g.batch = nl;
+    g.A = W;
+    g.lda = nir;
+    g.sA = sM;
+    g.B = St + (long long)2 * ne * ls + half * ne;
+    g.ldb = ls;
+    g.sB = sM;
+    g.D = base + uoff + (long long)half * nir * mrhs;
+    g.ldd = nir;
+    g.sD = sM;
+    gemm(c, g);
+  }
+  hpsk::ItiFdmAssembleArgs aa{};
+  aa.Z = base + zoff;
+  aa.Ue = St + (long long)2 * ne * ls;
+  aa.Ure = base + uoff;
+  aa.Uim = base + uoff + (long long)nir * mrhs;
+  aa.M = base + (long long)ld2 * ld2;
+  aa.stride = sM;
+  aa.pos = c->itiPos.i();
+  aa.n = n;
+  aa.ne = ne;
+  aa.nir = nir;
+  aa.mrhs = mrhs;
+  hpsk::launch_iti_fdm_assemble(aa, nl, c->st);
+  ck(cudaGetLastError(), "iti fdm assemble");
+  ++c->launches;
+  return true;
+}
+
 void run_leaf_stage(hpsg_ctx* c) {
   const hpsg::LeafOperators& o = c->ops;
   const int nl = c->T.n_leaves();
@@ -551,6 +745,9 @@ void run_leaf_stage(hpsg_ctx* c) {
     ia.P = c->iP.d();
     ia.source_im = c->source_im;
     ia.has_source_im = c->has_source_im;
+    c->stats.leaf_path = 4;
+    if (!(c->fdm && run_iti_fdm_leaf(c, a))) {
+    c->stats.leaf_path = c->fdm ? 5 : 1;
     hpsk::launch_iti_leaf_assemble(ia, nl, c->st);
     ck(cudaGetLastError(), "iti leaf assemble");
     ++c->launches;
@@ -559,6 +756,7 @@ void run_leaf_stage(hpsg_ctx* c) {
     ck(hpsk::bgetrf_aug(nl, o.ni, 1 + o.nb, M, c->leafPiv.i(), c->leafStats.d(), c->luws, c->st, false),
        "iti leaf bgetrf");
     c->launches += lu_launches(o.ni, 1 + o.nb, true);
+    }
     GemmArgs t;  // [h | T] = QH [v | Y]  (T = QH Y, h = QH v; local_solve.cpp:170-171)
     t.m = o.nb;
     t.n = 1 + o.nb;

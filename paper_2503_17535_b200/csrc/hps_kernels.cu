@@ -324,6 +324,34 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const GatherArgs
   }
 }
 
+// ItI leaf by block elimination (run_leaf_stage): the leaf's [v | Y | iY] columns in real-equivalent tensor
+// order from the interior solution U_i = W U_e (+ z on the source column) and the exterior solution U_e.
+__global__ void iti_fdm_assemble_kernel(const ItiFdmAssembleArgs a) {
+  const long long leaf = blockIdx.x;
+  const double* Z = a.Z + leaf * a.stride;       // z_re, z_im: columns 0, 1 (nir each)
+  const double* Ue = a.Ue + leaf * a.stride;     // 2 ne x mrhs, ld 2 ne
+  const double* Ure = a.Ure + leaf * a.stride;   // nir x mrhs
+  const double* Uim = a.Uim + leaf * a.stride;
+  double* M = a.M + leaf * a.stride;             // [v | Y | iY]: 2n x mrhs, ld 2n
+  const int n = a.n, ne = a.ne, nir = a.nir;
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < n * a.mrhs; e += gridDim.y * blockDim.x) {
+    const int c = e / n, t = e - c * n;
+    const int pos = a.pos[t];
+    double re, im;
+    if (pos >= 0) {
+      re = Ure[(long long)c * nir + pos];
+      im = Uim[(long long)c * nir + pos];
+      if (c == 0) re += Z[pos], im += Z[nir + pos];
+    } else {
+      const int x = -pos - 1;
+      re = Ue[(long long)c * 2 * ne + x];
+      im = Ue[(long long)c * 2 * ne + ne + x];
+    }
+    M[(long long)c * 2 * n + t] = re;
+    M[(long long)c * 2 * n + n + t] = im;
+  }
+}
+
 __global__ void scatter_kernel(const ScatterArgs a) {
   const long long parent = blockIdx.x;
   const int child_nb = a.nface * a.s;
@@ -414,6 +442,10 @@ void launch_copy_batched(double* dst, long long ldd, long long sd, const double*
   const int gy = int(std::min<long long>(std::max<long long>(1, (148LL * 8 + batch - 1) / batch), (e + 255) / 256));
   copy_batched_kernel<<<dim3(batch, std::max(1, std::min(gy, 65535))), 256, 0, st>>>(dst, ldd, sd, src, lds, ss, rows,
                                                                                      cols);
+}
+void launch_iti_fdm_assemble(const ItiFdmAssembleArgs& a, int n_leaves, cudaStream_t st) {
+  const int gy = std::max(1, std::min(64, (a.n * a.mrhs + 255) / 256));
+  iti_fdm_assemble_kernel<<<dim3(n_leaves, gy), 256, 0, st>>>(a);
 }
 void launch_iti_leaf_output(double* u, const double* Ui, int n, int nrhs, int n_leaves, cudaStream_t st) {
   const long long total = (long long)n_leaves * nrhs * n;

@@ -62,6 +62,20 @@ struct ItiLeafArgs {
 };
 void launch_iti_leaf_assemble(const ItiLeafArgs& a, int n_leaves, cudaStream_t st);
 
+// ItI leaf by block elimination of [G; L_int] (local_solve.cpp:145-172): the leaf outputs in the layout of the
+// real-equivalent LU path ([v | Y | iY], 2n rows in tensor order) from U_e (exterior) and U_i = W U_e (interior)
+struct ItiFdmAssembleArgs {
+  const double* Z;      // per leaf: z_re, z_im (nir each) = L_ii^-1 f_i
+  const double* Ue;     // per leaf: 2 ne x mrhs (ld 2 ne), stacked re / im
+  const double* Ure;    // per leaf: nir x mrhs
+  const double* Uim;
+  double* M;            // per leaf: [v | Y | iY] (2n x mrhs, ld 2n)
+  long long stride;     // per-leaf stride of every array above
+  const int* pos;       // tensor index -> interior position (>= 0) or -(exterior position) - 1
+  int n, ne, nir, mrhs;
+};
+void launch_iti_fdm_assemble(const ItiFdmAssembleArgs& a, int n_leaves, cudaStream_t st);
+
 struct DevBlockCopy {
   int dst, dr, dc, child, sr, sc, rows, cols;
 };
@@ -153,6 +167,9 @@ struct LeafFdmArgs {
   double qds;
   double* Rtab;             // 4(p-2) blocks of 16 x 16: -L_ie P per column (block layout) and R^ = V^-1 R V^-T,
   double* Rhat;             // written by launch_leaf_fdm_prep, read by every leaf
+  int iti = 0;              // ItI mode: P = I (ne columns), two source columns, output Z = L_ii^-1 [f_i | -L_ie]
+  DevField source_im;       // (Yv = Z, strideYv), no [h|T]
+  int has_source_im = 0;
   double* Yv;
   long long strideYv;
   double* HT;

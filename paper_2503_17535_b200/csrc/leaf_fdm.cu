@@ -42,7 +42,7 @@ struct FdmSmem {
   double R[kNC * kBlk], X[kNC * kBlk], W[kNC * kBlk];
   double cz[kBlk];   // zeroth-order coefficient at the interior points (block layout), 0 in the padding
   double den[kBlk];  // 1 / (lam_row + lam_col + cbar), 0 in the padding
-  double fsrc[256];
+  double fsrc[2][256];  // source samples: real part (and the imaginary part in the ItI mode)
   int pos[256];      // tensor index -> interior r (>= 0) or -(exterior position) - 1
   double qDm[kBlk];  // separable Q_i as DMMA A operands (16 x 16 col-major, zero padded): rows s = d_s
   double qGm[kBlk];  // (side normal derivatives on the interior nodes) and G (Chebyshev -> Gauss, q x (p-2))
@@ -227,7 +227,10 @@ __global__ void __launch_bounds__(kT, 2) leaf_fdm_kernel(const LeafFdmArgs f) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FdmSmem& s = *reinterpret_cast<FdmSmem*>(smem_raw);
   const LeafAsmArgs& a = f.a;
-  constexpr int ncol = 1 + NB;
+  // DtN: column 0 = sgn f_i, columns 1..NB = -L_ie P.  ItI mode: columns 0, 1 = Re f_i, Im f_i, columns
+  // 2..NE+1 = -L_ie e_k (the prep tables were made with P = I), output Z = L_ii^-1 [f_i | -L_ie] only.
+  const int nsrc = f.iti ? 2 : 1;
+  const int ncol = nsrc + (f.iti ? 4 * P - 4 : NB);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
   double vi[2][4], vv[2][4], aa[2][4];
   load_afrag(f.Vinv, vi, g, t4);
@@ -237,8 +240,8 @@ __global__ void __launch_bounds__(kT, 2) leaf_fdm_kernel(const LeafFdmArgs f) {
   for (int r = tid; r < NE; r += kT) s.pos[a.exterior[r]] = -r - 1;
   for (int e = tid; e < kBlk; e += kT) {
     const int row = e & 15, col = e >> 4;
-    s.qGm[e] = (row < N1 && col < N1) ? f.qG[row * N1 + col] : 0.0;   // G(i, m), q = N1
-    s.qDm[e] = (row < 4 && col < N1) ? f.qd[row * N1 + col] : 0.0;    // d_s(k)
+    s.qGm[e] = (!f.iti && row < N1 && col < N1) ? f.qG[row * N1 + col] : 0.0;   // G(i, m), q = N1
+    s.qDm[e] = (!f.iti && row < 4 && col < N1) ? f.qd[row * N1 + col] : 0.0;    // d_s(k)
   }
   __syncthreads();
 
@@ -260,7 +263,8 @@ __global__ void __launch_bounds__(kT, 2) leaf_fdm_kernel(const LeafFdmArgs f) {
         if (!isfinite(v)) atomicMin(&s.bad, i);
         if (a.terms[t].role == 2) cz = __dadd_rn(cz, v);
       }
-      s.fsrc[i] = a.has_source ? eval_field_t<2>(a.source, x, leaf, i, NPT) : 0.0;
+      s.fsrc[0][i] = a.has_source ? eval_field_t<2>(a.source, x, leaf, i, NPT) : 0.0;
+      if (f.iti) s.fsrc[1][i] = f.has_source_im ? eval_field_t<2>(f.source_im, x, leaf, i, NPT) : 0.0;
       const int r = s.pos[i];
       if (r >= 0) {
         s.cz[swz(r % N1, r / N1)] = cz;
@@ -318,11 +322,11 @@ __global__ void __launch_bounds__(kT, 2) leaf_fdm_kernel(const LeafFdmArgs f) {
       int npass = 0, nout = 0;
       for (int c = warp + 1; c < ncol + 1; c += kW) {
         const int col = c == ncol ? 0 : c;
-        // right-hand side: column 0 = sgn f_i (formed here); columns 1.. = -L_ie P, the same for every leaf
-        // (constant Laplacian): R and R^ = V^-1 R V^-T from the prep tables (L2-resident)
-        if (col > 0) {
-          const double2* Rt = reinterpret_cast<const double2*>(f.Rtab + (long long)(col - 1) * kBlk);
-          const double2* Rh = reinterpret_cast<const double2*>(f.Rhat + (long long)(col - 1) * kBlk);
+        // right-hand side: the source column(s) (formed here); then -L_ie P (-L_ie in the ItI mode), the same for
+        // every leaf (constant Laplacian): R and R^ = V^-1 R V^-T from the prep tables (L2-resident)
+        if (col >= nsrc) {
+          const double2* Rt = reinterpret_cast<const double2*>(f.Rtab + (long long)(col - nsrc) * kBlk);
+          const double2* Rh = reinterpret_cast<const double2*>(f.Rhat + (long long)(col - nsrc) * kBlk);
 #pragma unroll
           for (int e = lane; e < kBlk / 2; e += 32) {
             reinterpret_cast<double2*>(Rb)[e] = __ldg(Rt + e);
@@ -331,15 +335,19 @@ __global__ void __launch_bounds__(kT, 2) leaf_fdm_kernel(const LeafFdmArgs f) {
         } else {
           for (int e = lane; e < kBlk; e += 32) {
             const int cc = e >> 4, row = (e & 15) ^ swx(cc);
-            Rb[e] = (row < N1 && cc < N1) ? a.fsign * s.fsrc[(cc + 1) * P + row + 1] : 0.0;
+            Rb[e] = (row < N1 && cc < N1) ? a.fsign * s.fsrc[col][(cc + 1) * P + row + 1] : 0.0;
           }
         }
         __syncwarp();
-        conv = solve_block(Rb, Xb, Wb, s, vi, vv, aa, g, t4, npass, col > 0) && conv;
-        // [v_i | Y_i] column (interior index r = (i1-1) N1 + (i2-1))
+        conv = solve_block(Rb, Xb, Wb, s, vi, vv, aa, g, t4, npass, col >= nsrc) && conv;
+        // [v_i | Y_i] column (interior index r = (i1-1) N1 + (i2-1)); ItI mode: the column of Z
         double* Yv = f.Yv + leaf * f.strideYv + (long long)col * NI;
 #pragma unroll
         for (int r = lane; r < NI; r += 32) __stcs(&Yv[r], Xb[swz(r % N1, r / N1)]);
+        if (f.iti) {
+          __syncwarp();
+          continue;
+        }
         // [h | T] = Q_i X + [0 | Q_e P] through the separable Q_i (geometry.cpp q_interior_factors), on DMMA:
         // U = Dm X (rows S, N: u_s(m) = sum_k d_s(k) X(k, m)) and Dm X^T (rows E, W), then H = G U^T, h = ds H.
         // Block element (row, col) = X(i1 = col + 1, i2 = row + 1).  U goes to Rb (free after the solve) as a
@@ -478,7 +486,7 @@ int leaf_fdm_ctas_per_sm(int p) {
 }
 
 cudaError_t launch_leaf_fdm_prep(const LeafFdmArgs& f, cudaStream_t st) {
-  const int nb = 4 * (f.a.p - 2);
+  const int nb = f.iti ? 4 * f.a.p - 4 : 4 * (f.a.p - 2);
   switch (f.a.p) {
 #define HPS_FDM_PREP(PP) \
   case PP: leaf_fdm_prep_kernel<PP><<<nb, 32, 0, st>>>(f); break;

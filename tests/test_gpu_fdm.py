@@ -118,3 +118,44 @@ def test_sampled_constant_laplacian_takes_fdm():
                     prob.source, root_implicit_S=True)
     c.build()
     assert c.stats()["leaf_path"] == LEAF_PATH_FUSED_LU
+
+
+LEAF_PATH_ITI_ELIM, LEAF_PATH_ITI_LU_FALLBACK = 4, 5
+
+
+@pytest.mark.parametrize("L,path", [(6, LEAF_PATH_ITI_ELIM), (3, LEAF_PATH_ITI_LU_FALLBACK)])
+def test_iti_block_elimination_equals_lu(L, path):
+    """ItI leaves by block elimination of [G; L_int] (fast-diagonalisation interior solve + the reduced
+    4p-4 impedance system, local_solve.cpp:145-172) against the real-equivalent LU of the full leaf system:
+    the radiation-closed scatter2d solutions agree to 1e-9 (measured 2.5e-10 at L = 6; the ItI parity floor of
+    this suite is 5e-9, test_gpu_ref_parity.py, from complex vs real-equivalent pivoting).  At L = 3 (k = 40, leaf side 1/4) the interior
+    Richardson iteration does not contract fast enough: the whole leaf stage falls back to the LU."""
+    pr = PR.scatter2d(k=40.0)
+    tree = H.build_uniform_tree(-1.0, 1.0, L, 2, 16)
+    out = []
+    for fdm in (True, False):
+        s = H.HpsSolver(tree, pr.terms, pr.source_re, source_imag=pr.source_im, variant="iti", eta=pr.eta,
+                        build_root_T=True, fdm_leaf=fdm)
+        s.build()
+        out.append((s.stats()["leaf_path"], s.solve_radiation()))
+        s.close()
+    assert out[0][0] == path and out[1][0] == 1
+    assert rel(out[0][1], out[1][1]) < 1e-9
+
+
+def test_iti_block_elimination_plane_wave():
+    """Exact-solution gate of the eliminated ItI leaves: the impedance plane-wave problem to 1e-10 at p=16 L=4."""
+    k, eta = 12.0, 12.0
+    terms = [H.Term(H.ROLE_LAPLACIAN, H.Field.const(1.0)), H.Term(H.ROLE_ZEROTH, H.Field.const(k * k))]
+    s = H.HpsSolver(H.build_uniform_tree(-1.0, 1.0, 4, 2, 16), terms, None, variant="iti", eta=eta)
+    s.build()
+    assert s.stats()["leaf_path"] == LEAF_PATH_ITI_ELIM
+    from tests.test_gpu_parity import _impedance_data
+    rp = s.root_boundary_points()
+    kv = k * np.array([np.cos(0.7), np.sin(0.7)])
+    u = lambda x: np.exp(1j * (x[..., 0] * kv[0] + x[..., 1] * kv[1]))
+    du = lambda x: (1j * kv[0] * u(x), 1j * kv[1] * u(x))
+    g = _impedance_data(rp, u, du, eta)
+    ex = u(s.leaf_points())
+    U = s.solve_complex(g)
+    assert np.abs(U - ex).max() / np.abs(ex).max() < 1e-10
