@@ -29,6 +29,7 @@ struct GemmArgs {
   long long ldd = 0, sD = 0;
   double alpha = 1.0, beta = 0.0;
   int seed_k_max = 0;  // set by launch_dgemm: accumulators seeded with C when k <= this
+  const int* drow = nullptr;  // optional output row map: row r of the product goes to D row drow[r] (beta = 0)
 };
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool VEC>
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, STAGES, VEC>::kThr
           v *= p.alpha;
           if (p.beta != 0.0) v += p.beta * C[(long long)col * p.ldc + row];
         }
-        D[(long long)col * p.ldd + row] = v;
+        D[(long long)col * p.ldd + (p.drow ? __ldg(p.drow + row) : row)] = v;
       }
     }
   }

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, STAGES, true>::kTh
           v *= p.alpha;
           if (p.beta != 0.0) v += p.beta * C[(long long)col * p.ldc + row];
         }
-        D[(long long)col * p.ldd + row] = v;
+        D[(long long)col * p.ldd + (p.drow ? __ldg(p.drow + row) : row)] = v;
       }
   }
 }

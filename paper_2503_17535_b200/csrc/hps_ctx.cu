@@ -993,7 +993,9 @@ void run_merge_level(hpsg_ctx* c, int d) {
     // merge_iti's structured elimination (merge.cpp:447-463, apply_Dinv :160-174): D = [[I, D12], [D21, I]]
     // (half-blocked real-equivalent order), W = I - D12 D21, then for X = [h_int | C]:
     //   Y_top = W^-1 (X_top - D12 X_bot),  Y_bot = X_bot - D21 Y_top;  [x_h | X] <- [Y_top; Y_bot] in place
-    const int N = L.n_int, h = N / 2, m = 1 + L.n_ext, B = int(L.nodes);
+    // only [h_int | C's real-unit columns] are solved: the imaginary-unit columns of C are i times them, and so
+    // are those of X; they are filled in after the solve (half the RHS work of the real-equivalent form)
+    const int N = L.n_int, h = N / 2, m = 1 + L.n_ext, mh = 1 + L.n_ext / 2, B = int(L.nodes);
     const long long sW = (long long)h * (h + m), sM = L.strideMD();
     double* MD = L.MD.d();
     double* W = c->itiW.d();
@@ -1008,25 +1010,26 @@ void run_merge_level(hpsg_ctx* c, int d) {
     g.alpha = -1.0, g.beta = 1.0;
     gemm(c, g);
     GemmArgs r;  // [W | X_top - D12 X_bot]
-    r.m = h, r.n = m, r.k = h, r.batch = B;
+    r.m = h, r.n = mh, r.k = h, r.batch = B;
     r.A = MD + (long long)h * N, r.lda = N, r.sA = sM;
     r.B = MD + (long long)N * N + h, r.ldb = N, r.sB = sM;    // X_bot
     r.C = MD + (long long)N * N, r.ldc = N, r.sC = sM;        // X_top
     r.D = W + (long long)h * h, r.ldd = h, r.sD = sW;
     r.alpha = -1.0, r.beta = 1.0;
     gemm(c, r);
-    ck(hpsk::bgetrf_aug(B, h, m, BatchedMat{W, h, sW}, L.piv.i(), L.stats.d(), c->luws, c->st, false), "W bgetrf");
-    c->launches += 2 + lu_launches(h, m, true);
+    ck(hpsk::bgetrf_aug(B, h, mh, BatchedMat{W, h, sW}, L.piv.i(), L.stats.d(), c->luws, c->st, false), "W bgetrf");
+    c->launches += 2 + lu_launches(h, mh, true);
     GemmArgs y;  // Y_bot = X_bot - D21 Y_top (in place in MD)
-    y.m = h, y.n = m, y.k = h, y.batch = B;
+    y.m = h, y.n = mh, y.k = h, y.batch = B;
     y.A = MD + h, y.lda = N, y.sA = sM;
     y.B = W + (long long)h * h, y.ldb = h, y.sB = sW;
     y.C = MD + (long long)N * N + h, y.ldc = N, y.sC = sM;
     y.D = MD + (long long)N * N + h, y.ldd = N, y.sD = sM;
     y.alpha = -1.0, y.beta = 1.0;
     gemm(c, y);
-    hpsk::launch_copy_batched(MD + (long long)N * N, N, sM, W + (long long)h * h, h, sW, h, m, B, c->st);
-    ++c->launches;
+    hpsk::launch_copy_batched(MD + (long long)N * N, N, sM, W + (long long)h * h, h, sW, h, mh, B, c->st);
+    hpsk::launch_iti_fill_im_half(MD + (long long)N * N, N, sM, B, N / 2, N / 4, 1, mh, L.n_ext / 2, c->st);
+    c->launches += 2;
   } else {
   const int m = (root && c->opts.root_implicit_S) ? 1 : 1 + L.n_ext;
   BatchedMat M{L.MD.d(), L.n_int, L.strideMD()};
@@ -1064,10 +1067,11 @@ void run_merge_level(hpsg_ctx* c, int d) {
       gemm(c, g);
     }
   } else if (!root) {
-    // [h | T] = [h_ext | A] - B [x_h | X]   (merge.cpp:294-295 with gtilde = -x_h)
+    // [h | T] = [h_ext | A] - B [x_h | X]   (merge.cpp:294-295 with gtilde = -x_h); ItI: the real-unit columns,
+    // the imaginary-unit columns of T are filled in from them
     GemmArgs g;
     g.m = L.n_ext;
-    g.n = 1 + L.n_ext;
+    g.n = c->iti ? 1 + L.n_ext / 2 : 1 + L.n_ext;
     g.k = L.n_int;
     g.batch = int(L.nodes);
     g.A = c->Bscratch.d();
@@ -1085,6 +1089,11 @@ void run_merge_level(hpsg_ctx* c, int d) {
     g.alpha = -1.0;
     g.beta = 1.0;
     gemm(c, g);
+    if (c->iti) {
+      hpsk::launch_iti_fill_im_half(L.AH.d(), L.n_ext, L.strideAH(), int(L.nodes), L.n_ext / 2, 0, 1,
+                                    1 + L.n_ext / 2, L.n_ext / 2, c->st);
+      ++c->launches;
+    }
   }
 }
 
@@ -1225,6 +1234,37 @@ void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_
   g.D = c->Ui.d();
   g.ldd = o.ni;
   g.sD = (long long)o.ni * nrhs;
+  if (nrhs > 4 && !new_source && !c->iti) {
+    // many right-hand sides (DMMA GEMMs): the products land directly in u (nrhs x n_leaves x npts) through the
+    // interior / exterior row maps, instead of a staging pass through Ui / Ue and leaf_output_kernel
+    g.D = d_u;
+    g.ldd = (long long)nl * o.n;
+    g.sD = o.n;
+    g.drow = c->interior.i();
+    gemm(c, g);
+    GemmArgs e;
+    e.m = o.ne;
+    e.n = nrhs;
+    e.k = o.nb;
+    e.batch = nl;
+    e.A = c->P.d();
+    e.lda = o.ne;
+    e.sA = 0;
+    e.B = c->G[Lh]->d() + 1;
+    e.ldb = ldGL;
+    e.sB = sGL;
+    e.D = d_u;
+    e.ldd = (long long)nl * o.n;
+    e.sD = o.n;
+    e.drow = c->exterior.i();
+    gemm(c, e);
+    if (d_leaf_g) {
+      hpsk::launch_unpack_leaf_g(d_leaf_g, c->G[Lh]->d(), o.nb, nrhs, nl, c->st);
+      ++c->launches;
+    }
+    ck(cudaGetLastError(), "solve kernels");
+    return;
+  }
   if (new_source) {  // u_i = Y_i g + v_new
     ck(cudaMemcpyAsync(c->Ui.p, c->srcR.p, size_t(nl) * o.ni * nrhs * 8, cudaMemcpyDeviceToDevice, c->st), "v copy");
     g.C = c->Ui.d();

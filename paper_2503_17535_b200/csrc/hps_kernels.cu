@@ -324,6 +324,25 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const GatherArgs
   }
 }
 
+// ItI real-equivalent columns of an imaginary unit are i times those of the matching real unit: for a complex
+// column z stored as rows (re_row(o), im_row(o)), the column of i z holds (-im, re).  Fills columns
+// [col_im0, col_im0 + ncols) from [col_re0, ...) of every node; half-blocked interface order (hc > 0:
+// re_row(o) = o < hc ? o : 2 hc + (o - hc), im_row = re_row + hc) or plain exterior order (hc = 0:
+// re_row(o) = o, im_row = o + nc).
+__global__ void iti_fill_im_half_kernel(double* X, long long ld, long long stride, int nc, int hc, int col_re0,
+                                        int col_im0, int ncols) {
+  double* Xb = X + blockIdx.x * stride;
+  const long long tot = (long long)nc * ncols;
+  for (long long e = blockIdx.y * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.y * blockDim.x) {
+    const int j = int(e / nc), o = int(e - (long long)j * nc);
+    const int rr = hc ? (o < hc ? o : 2 * hc + (o - hc)) : o;
+    const int ri = hc ? rr + hc : o + nc;
+    const double re = Xb[(long long)(col_re0 + j) * ld + rr], im = Xb[(long long)(col_re0 + j) * ld + ri];
+    Xb[(long long)(col_im0 + j) * ld + rr] = -im;
+    Xb[(long long)(col_im0 + j) * ld + ri] = re;
+  }
+}
+
 // ItI leaf by block elimination (run_leaf_stage): the leaf's [v | Y | iY] columns in real-equivalent tensor
 // order from the interior solution U_i = W U_e (+ z on the source column) and the exterior solution U_e.
 __global__ void iti_fdm_assemble_kernel(const ItiFdmAssembleArgs a) {
@@ -442,6 +461,12 @@ void launch_copy_batched(double* dst, long long ldd, long long sd, const double*
   const int gy = int(std::min<long long>(std::max<long long>(1, (148LL * 8 + batch - 1) / batch), (e + 255) / 256));
   copy_batched_kernel<<<dim3(batch, std::max(1, std::min(gy, 65535))), 256, 0, st>>>(dst, ldd, sd, src, lds, ss, rows,
                                                                                      cols);
+}
+void launch_iti_fill_im_half(double* X, long long ld, long long stride, int batch, int nc, int hc, int col_re0,
+                             int col_im0, int ncols, cudaStream_t st) {
+  const long long tot = (long long)nc * ncols;
+  const int gy = (int)std::max<long long>(1, std::min<long long>((tot + 255) / 256, (148LL * 8 + batch - 1) / batch));
+  iti_fill_im_half_kernel<<<dim3(batch, gy), 256, 0, st>>>(X, ld, stride, nc, hc, col_re0, col_im0, ncols);
 }
 void launch_iti_fdm_assemble(const ItiFdmAssembleArgs& a, int n_leaves, cudaStream_t st) {
   const int gy = std::max(1, std::min(64, (a.n * a.mrhs + 255) / 256));

@@ -75,6 +75,9 @@ struct ItiFdmAssembleArgs {
   int n, ne, nir, mrhs;
 };
 void launch_iti_fdm_assemble(const ItiFdmAssembleArgs& a, int n_leaves, cudaStream_t st);
+// the real-equivalent columns of imaginary units from those of the real units (i z = (-im, re)), see hps_kernels.cu
+void launch_iti_fill_im_half(double* X, long long ld, long long stride, int batch, int nc, int hc, int col_re0,
+                             int col_im0, int ncols, cudaStream_t st);
 
 struct DevBlockCopy {
   int dst, dr, dc, child, sr, sc, rows, cols;
