@@ -572,7 +572,8 @@ bool run_iti_fdm_leaf(hpsg_ctx* c, const hpsk::LeafAsmArgs& a0) {
   const int nl = c->T.n_leaves();
   const long long sM = c->strideLeafM();
   const int p = c->tree.p, n1 = p - 2, nir = n1 * n1, ne = 4 * p - 4, nbc = io.nbc, nbq = io.nb, n = io.n;
-  const int ld2 = 2 * n, mrhs = 1 + 2 * nbq, ls = 2 * nbc;
+  // right-hand sides [-G_i z | P]: the iY columns of the LU path's [v | Y | iY] are i Y, filled in at the end
+  const int ld2 = 2 * n, mrhs = 1 + nbq, ls = 2 * nbc;
   if (nbc != ne || o.ni != ld2) return false;
   double* base = c->leafM.d();
   const long long zoff = 0, soff = (long long)nir * (2 + ne), uoff = soff + (long long)ls * (ls + mrhs);
@@ -661,7 +662,7 @@ bool run_iti_fdm_leaf(hpsg_ctx* c, const hpsk::LeafAsmArgs& a0) {
     g.beta = 0.0;
     gemm(c, g);
   }
-  hpsk::launch_copy_batched(St + (long long)(2 * ne + 1) * ls, ls, sM, c->itiPc.d(), ls, 0, ls, 2 * nbq, nl, c->st);
+  hpsk::launch_copy_batched(St + (long long)(2 * ne + 1) * ls, ls, sM, c->itiPc.d(), ls, 0, ls, nbq, nl, c->st);
   ++c->launches;
   ck(hpsk::lu_stats_init(c->leafStats.d(), nl, c->st), "stats init");
   ck(hpsk::bgetrf_aug(nl, ls, mrhs, BatchedMat{St, ls, sM}, c->leafPiv.i(), c->leafStats.d(), c->luws, c->st, false),
@@ -698,8 +699,9 @@ bool run_iti_fdm_leaf(hpsg_ctx* c, const hpsk::LeafAsmArgs& a0) {
   aa.nir = nir;
   aa.mrhs = mrhs;
   hpsk::launch_iti_fdm_assemble(aa, nl, c->st);
+  hpsk::launch_iti_fill_im_half(base + (long long)ld2 * ld2, ld2, sM, nl, n, 0, 1, 1 + nbq, nbq, c->st);
   ck(cudaGetLastError(), "iti fdm assemble");
-  ++c->launches;
+  c->launches += 2;
   return true;
 }
 
@@ -757,9 +759,9 @@ void run_leaf_stage(hpsg_ctx* c) {
        "iti leaf bgetrf");
     c->launches += lu_launches(o.ni, 1 + o.nb, true);
     }
-    GemmArgs t;  // [h | T] = QH [v | Y]  (T = QH Y, h = QH v; local_solve.cpp:170-171)
-    t.m = o.nb;
-    t.n = 1 + o.nb;
+    GemmArgs t;  // [h | T] = QH [v | Y]  (T = QH Y, h = QH v; local_solve.cpp:170-171): the real-unit columns,
+    t.m = o.nb;  // the imaginary-unit ones filled in after
+    t.n = 1 + o.nb / 2;
     t.k = o.ni;
     t.batch = nl;
     t.A = c->iQHs.d();
@@ -774,6 +776,9 @@ void run_leaf_stage(hpsg_ctx* c) {
     t.alpha = 1.0;
     t.beta = 0.0;
     gemm(c, t);
+    hpsk::launch_iti_fill_im_half(c->leafHT.d(), o.nb, c->strideLeafHT(), nl, o.nb / 2, 0, 1, 1 + o.nb / 2, o.nb / 2,
+                                  c->st);
+    ++c->launches;
     return;
   }
   c->stats.leaf_path = c->fused ? 0 : 1;
