@@ -43,7 +43,7 @@ sys.path.insert(0, ROOT)
 METRIC = "HPS build+solve seconds & DOF/s (2D p=16 L=8) at 1/2/4/8 B200; rel err vs oracle"
 # PAPER.md:629 / :1755 -- H100 JAX, subtree recomputation, p=16 L=8: 4.02 s (N = 16,777,216)
 PAPER_H100_DOFS = 16777216 / 4.02
-FP64_PEAK_TFLOPS = 37.155     # profiles/r01_fp64_peak.json (DMMA microbench; MEASURED_PEAKS.json has no FP64 entry)
+FP64_PEAK_TFLOPS = 37.155     # DMMA microbench: profiles/r01_fp64_peak.json 37.155, re-measured with SM clocks at 1965 MHz in profiles/r02_fp64_peak.json 37.148 (MEASURED_PEAKS.json has no FP64 entry)
 # dram__bytes_read.sum + dram__bytes_write.sum of one leaf-stage launch at p=16 L=8, per leaf kernel
 # (ncu --set full of the current kernels, profiles/r02_ncu_summary.md)
 LEAF_KERNEL_DRAM_BYTES = {"leaf_fused_kernel": 18.89e9 + 69.29e9, "leaf_fdm_kernel": 4.663e9 + 7.480e9}
