@@ -108,6 +108,21 @@ def test_multi_rhs_and_linearity():
     assert rel(s.solve(2 * G[0] - 3 * G[1]), 2 * U[0] - 3 * U[1]) < 1e-11
 
 
+@pytest.mark.parametrize("name,p,L", [("helmholtz_bumps", 16, 4), ("poisson2d", 12, 3)])
+def test_many_rhs_gemm_path(name, p, L):
+    """More than 4 right-hand sides take the DMMA GEMM path whose leaf products land in u through the interior /
+    exterior row maps (no staging pass): equal to one-RHS solves, with the leaves' boundary data."""
+    prob = PR.CATALOG[name]()
+    s = gpu_solver(prob, p, L, literal=False, root_implicit=True)
+    rng = np.random.default_rng(11)
+    G = rng.standard_normal((9, s.nb_root))
+    U, LG = s.solve(G, want_leaf_g=True)
+    for i in (0, 4, 8):
+        u1, lg1 = s.solve(G[i], want_leaf_g=True)
+        assert rel(U[i], u1) < 1e-12
+        assert rel(LG[i], lg1) < 1e-12
+
+
 def test_3d_laplace_parity():
     prob = PR.CATALOG["laplace3d"]()
     for p, L in [(6, 1), (6, 2)]:
