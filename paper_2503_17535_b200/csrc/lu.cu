@@ -208,6 +208,145 @@ __global__ void __launch_bounds__(kPanelThreads) panel_getrf_kernel(const PanelA
   if (cs > 1) cluster_sync();  // keep the published slots alive until remote readers are done
 }
 
+// Register-resident variant of panel_getrf_kernel for 32-column panels with <= kPanelThreads rows per CTA: each
+// thread keeps its row of the panel in registers (the elimination reads and writes no shared memory; the column
+// loop is unrolled so the row indexes registers), everything else is panel_getrf_kernel's protocol: warp
+// candidates -> warp 0 -> published candidate row / row j -> one cluster barrier -> warp 0 pulls the cluster
+// candidates and the pivot row through DSMEM -> one CTA barrier -> exchange + elimination.  Each warp's best lane
+// writes its row to the warp's slot before the first barrier, so the CTA candidate row is in shared memory when
+// warp 0 picks it.  Same pivots and arithmetic as panel_getrf_kernel (bit-identical factors).
+#ifndef HPS_PANEL_REGROW
+#define HPS_PANEL_REGROW 1
+#endif
+__global__ void __launch_bounds__(kPanelThreads) panel_getrf_regrow_kernel(const PanelArgs a) {
+  constexpr int NB = kLuNB, NW = kPanelThreads / 32;
+  __shared__ double wrow[NW][NB];           // each warp's candidate row
+  __shared__ double cand_row[2][NB];        // published CTA candidate row (double-buffered by column parity)
+  __shared__ double jrow_pub[2][NB];        // published row j
+  __shared__ double urow[NB], jrow[NB];     // the pivot row, the old row j (pivot owner)
+  __shared__ double wv[NW], cand_v[2];
+  __shared__ int wi[NW], cand_i[2], s_piv;
+  const int cs = a.cs;
+  const int rank = cs > 1 ? (int)cluster_ctarank() : 0;
+  const long long b = blockIdx.x / cs;
+  double* M = a.M + b * a.stride;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int rows_total = a.n - a.j0;
+  const int r_begin = rank * a.rpc;
+  const int nr = max(0, min(rows_total - r_begin, a.rpc));
+  const int gr = r_begin + tid;
+  const bool have = tid < nr;
+  double row[NB];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) row[c] = have ? M[(long long)(a.j0 + c) * a.ld + a.j0 + gr] : 0.0;
+  double pmin = DBL_MAX, pmax = 0.0;
+  int first_zero = -1;
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const int buf = j & 1;
+    double bv = (have && gr >= j) ? fabs(row[j]) : -1.0;
+    int bi = (have && gr >= j) ? gr : INT_MAX;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      argmax_merge(bv, bi, v2, i2);
+    }
+    if (have && gr == bi) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c) wrow[warp][c] = row[c];
+    }
+    const int own_j = j / a.rpc;
+    if (have && gr == j) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c) jrow_pub[buf][c] = row[c];
+    }
+    if (lane == 0) wv[warp] = bv, wi[warp] = bi;
+    __syncthreads();
+    if (warp == 0) {
+      double cv = lane < nw ? wv[lane] : -1.0;
+      int ci = lane < nw ? wi[lane] : INT_MAX, cw = lane;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, cv, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, ci, o);
+        const int w2 = __shfl_xor_sync(0xffffffffu, cw, o);
+        if (v2 > cv || (v2 == cv && i2 < ci)) cv = v2, ci = i2, cw = w2;
+      }
+      if (lane == 0) cand_v[buf] = cv, cand_i[buf] = ci;
+      cand_row[buf][lane] = ci != INT_MAX ? wrow[cw][lane] : 0.0;
+    }
+    if (cs > 1)
+      cluster_sync();
+    else
+      __syncthreads();
+    if (warp == 0) {
+      double gv = -1.0;
+      int gi = INT_MAX, go = 0;
+      if (lane < cs) {
+        gv = cs > 1 ? dsmem_ld_f64(dsmem_map(&cand_v[buf], lane)) : cand_v[buf];
+        gi = cs > 1 ? dsmem_ld_s32(dsmem_map(&cand_i[buf], lane)) : cand_i[buf];
+        go = lane;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, gv, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, gi, o);
+        const int o2 = __shfl_xor_sync(0xffffffffu, go, o);
+        if (v2 > gv || (v2 == gv && i2 < gi)) gv = v2, gi = i2, go = o2;
+      }
+      const int piv = (gi == INT_MAX) ? j : gi;
+      const int own_p = (gi == INT_MAX) ? own_j : go;
+      if (lane == 0) s_piv = piv;
+      if (gi == INT_MAX)
+        urow[lane] = (own_j == rank || cs == 1) ? jrow_pub[buf][lane] : dsmem_ld_f64(dsmem_map(&jrow_pub[buf][lane], own_j));
+      else
+        urow[lane] = (own_p == rank || cs == 1) ? cand_row[buf][lane] : dsmem_ld_f64(dsmem_map(&cand_row[buf][lane], own_p));
+      if (own_p == rank && piv != j)
+        jrow[lane] = (own_j == rank || cs == 1) ? jrow_pub[buf][lane] : dsmem_ld_f64(dsmem_map(&jrow_pub[buf][lane], own_j));
+    }
+    __syncthreads();
+    const int piv = s_piv;
+    if (piv != j && have && gr == j) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c) row[c] = urow[c];
+    }
+    const double pv = urow[j];
+    const double apv = fabs(pv);
+    if (!(apv > 0.0) || !isfinite(apv)) {
+      if (first_zero < 0) first_zero = a.j0 + j;
+    } else {
+      pmin = fmin(pmin, apv);
+      pmax = fmax(pmax, apv);
+    }
+    if (rank == 0 && tid == 0) a.ipiv[b * a.n + a.j0 + j] = a.j0 + piv;
+    const double inv = apv > 0.0 ? 1.0 / pv : 0.0;
+    if (have && gr > j) {
+      const bool swapped = (gr == piv && piv != j);
+      if (swapped) {  // the old row j moves here whole, its earlier multipliers included
+#pragma unroll
+        for (int c = 0; c < NB; ++c) row[c] = jrow[c];
+      }
+      if (apv > 0.0) {
+        const double l = row[j] * inv;
+        row[j] = l;
+#pragma unroll
+        for (int c = j + 1; c < NB; ++c) row[c] = row[c] - l * urow[c];
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NB; ++c)
+    if (have) M[(long long)(a.j0 + c) * a.ld + a.j0 + gr] = row[c];
+  if (rank == 0 && tid == 0 && a.stats) {
+    double* st = a.stats + 3 * b;
+    st[0] = fmin(st[0], pmin);
+    st[1] = fmax(st[1], pmax);
+    if (first_zero >= 0 && st[2] < 0) st[2] = first_zero;
+  }
+  if (cs > 1) cluster_sync();  // keep the published slots alive until remote readers are done
+}
+
 struct Seg {
   double* base;  // column 0 of the segment for matrix 0 (row index = matrix row)
   long long ld, stride;
@@ -413,11 +552,31 @@ cudaError_t launch_panel(int batch, int n, int j0, int nb, BatchedMat M, int* ip
     if (e != cudaSuccess) return e;
     smem_set.value[dv] = std::max<size_t>(smem, 48 * 1024);
   }
+#ifndef HPS_REGROW_MIN_CS
+#define HPS_REGROW_MIN_CS 4
+#endif
+#ifndef HPS_REGROW_SINGLE_MIN_ROWS
+#define HPS_REGROW_SINGLE_MIN_ROWS 100000
+#endif
+  // measured: the register-resident panel pays from 4-CTA clusters up (the 2-CTA n = 896 panels are slower)
+  const bool regrow = HPS_PANEL_REGROW && nb == kLuNB && rpc <= kPanelThreads &&
+                      (cs >= HPS_REGROW_MIN_CS || (cs == 1 && rpc >= HPS_REGROW_SINGLE_MIN_ROWS));
+  if (regrow) {
+    static PerDeviceFlag rset;
+    if (!(rset.set >> dv & 1)) {
+      cudaError_t e = cudaFuncSetAttribute(panel_getrf_regrow_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+      rset.set |= 1ull << dv;
+    }
+  }
   if (cs == 1) {
     // single-CTA panels: one thread per row up to kPanelThreads (the 56- and 112-row panels of the
     // deep merge levels would otherwise run 4-6 warps with no rows through every barrier)
     const int threads = std::min(kPanelThreads, std::max(32, (rpc + 31) / 32 * 32));
-    panel_getrf_kernel<<<batch, threads, smem, st>>>(pa);
+    if (regrow)
+      panel_getrf_regrow_kernel<<<batch, threads, 0, st>>>(pa);
+    else
+      panel_getrf_kernel<<<batch, threads, smem, st>>>(pa);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -432,6 +591,10 @@ cudaError_t launch_panel(int batch, int n, int j0, int nb, BatchedMat M, int* ip
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (regrow) {
+    cfg.dynamicSmemBytes = 0;
+    return cudaLaunchKernelEx(&cfg, panel_getrf_regrow_kernel, pa);
+  }
   return cudaLaunchKernelEx(&cfg, panel_getrf_kernel, pa);
 }
 
