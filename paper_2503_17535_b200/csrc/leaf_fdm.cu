@@ -29,8 +29,14 @@ namespace hpsk {
 
 namespace {
 
-constexpr int kT = 256, kW = kT / 32;
-constexpr int kNC = 8;      // block slots (one per warp)
+#ifndef HPS_FDM_WARPS
+#define HPS_FDM_WARPS 8
+#endif
+#ifndef HPS_FDM_MINB
+#define HPS_FDM_MINB 2
+#endif
+constexpr int kT = 32 * HPS_FDM_WARPS, kW = kT / 32;
+constexpr int kNC = kW;     // block slots (one per warp)
 constexpr int kBlk = 256;   // 16 x 16 doubles
 constexpr int kMaxSteps = 12;
 #ifndef HPS_FDM_TOL
@@ -222,7 +228,7 @@ HPS_DEV bool solve_block(const double* Rb, double* Xb, double* Wb, const FdmSmem
 }
 
 template <int P>
-__global__ void __launch_bounds__(kT, 2) leaf_fdm_kernel(const LeafFdmArgs f) {
+__global__ void __launch_bounds__(kT, HPS_FDM_MINB) leaf_fdm_kernel(const LeafFdmArgs f) {
   constexpr int N1 = P - 2, NI = N1 * N1, NE = 4 * P - 4, NB = 4 * N1, NPT = P * P;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FdmSmem& s = *reinterpret_cast<FdmSmem*>(smem_raw);
