@@ -250,6 +250,15 @@ int hpsg_error_report(hpsg_ctx* ctx, const double* d_u, int is_complex, const hp
 /* host-only: the ItI leaf operators of assemble_iti_ops_2d (spectral.cpp:312-368), column-major:
  * G = Gr + i Gi ((4p-4) x p^2), P ((4p-4) x 4q), QH = QHr + i QHi (4q x p^2); any pointer may be NULL */
 int hpsg_iti_leaf_ops(int p, double eta, double side, double* Gr, double* Gi, double* P, double* QHr, double* QHi);
+/* host-only: the operators of the fast-diagonalisation leaf solve for a constant Laplacian coefficient a on leaves
+ * of side `side` (2D, p in 4..16, n1 = p-2): A = s^2 (a D2[int, int]) (n1 x n1, s = 2/side, the rounding of the
+ * leaf assembly), its eigendecomposition A = V diag(lam) V^-1, and the separable interior Q factors
+ * Q_i(s q + i, (i1, i2)) = ds G(i, m) d_s(k) (G: q x n1 row-major, d: 4 x n1 row-major), with (m, k) = (i1-1,
+ * i2-1) on the S / N sides and (i2-1, i1-1) on E / W.  Returns
+ * HPSG_ERR_INVALID when A has no real eigendecomposition (the solver then keeps the LU leaf).  Any pointer may be
+ * NULL. */
+int hpsg_fdm_leaf_ops(int p, double side, double a, double* A, double* lam, double* V, double* Vinv, double* G,
+                      double* d, double* ds, double* Qi);   /* Qi: the dense interior Q (4q x (p-2)^2, column-major) */
 /* HpsSolver::solve_new_source(leaf_f, RootBC::dirichlet, g_root), solver.hpp:71-72 /
  * solver.cpp:285-307 (make_source_state :261-283, leaf_resolve_source local_solve.cpp:174-183,
  * artifact_source_pass merge.cpp:514-567), for nsrc sources at once against the stored build:

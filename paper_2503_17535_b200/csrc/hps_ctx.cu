@@ -1945,6 +1945,31 @@ int hpsg_iti_leaf_ops(int p, double eta, double side, double* Gr, double* Gi, do
   return HPSG_OK;
 }
 
+int hpsg_fdm_leaf_ops(int p, double side, double a, double* A, double* lam, double* V, double* Vinv, double* G,
+                      double* d, double* ds, double* Qi) {
+  if (p < 4 || p > 16 || !(side > 0.0) || !std::isfinite(a) || a == 0.0) return HPSG_ERR_INVALID;
+  try {
+    const hpsg::LeafOperators o = hpsg::make_leaf_operators(2, p, side);
+    const int n1 = p - 2;
+    const double sc = 2.0 / side, s2 = sc * sc;
+    std::vector<double> Am(size_t(n1) * n1), l, v, vi;
+    for (int j = 0; j < n1; ++j)
+      for (int i = 0; i < n1; ++i) Am[size_t(j) * n1 + i] = s2 * (a * o.D2(i + 1, j + 1));  // as setup_fdm
+    if (!hpsg::real_eigendecomposition(Am, n1, l, v, vi)) return HPSG_ERR_INVALID;
+    std::vector<double> g, dd;
+    double dsv = 0.0;
+    hpsg::q_interior_factors(o, g, dd, dsv);
+    auto cp = [](double* dst, const std::vector<double>& m) {
+      if (dst) std::memcpy(dst, m.data(), m.size() * 8);
+    };
+    cp(A, Am), cp(lam, l), cp(V, v), cp(Vinv, vi), cp(G, g), cp(d, dd), cp(Qi, o.Qi.a);
+    if (ds) *ds = dsv;
+  } catch (...) {
+    return HPSG_ERR_INVALID;
+  }
+  return HPSG_OK;
+}
+
 int hpsg_tree_leaf_points(const hpsg_tree* t, double* xyz) {
   if (!t || !xyz || (t->dim != 2 && t->dim != 3) || t->p < 4 || t->L < 0 || !(t->hi > t->lo))
     return HPSG_ERR_INVALID;

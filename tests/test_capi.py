@@ -114,3 +114,42 @@ def test_iti_leaf_operator_kats():
     hu = QH @ pts[:, 0]
     assert np.abs(hu[q:2 * q] - (1.0 - 1j * eta)).max() < 1e-11   # east side (s = 1) rows
     assert (np.abs(Gi) > 0).sum() == 4 * p - 4 and np.allclose(Gi[Gi != 0], eta)
+
+
+def test_fdm_leaf_operator_host_math():
+    """Host side of the fast-diagonalisation leaf solve (hpsg_fdm_leaf_ops): A = s^2 a D2[int, int] has a real
+    eigendecomposition A = V diag(lam) V^-1 to roundoff, and the separable factors reproduce the interior Q
+    (the product's make_leaf_operators Q, itself checked against the reference in test_ref_parity) bit for bit."""
+    import ctypes as C
+    import numpy as np
+    import paper_2503_17535_b200 as H
+    from paper_2503_17535_b200 import hps as HP
+    L = H.lib()
+    dp = C.POINTER(C.c_double)
+    L.hpsg_fdm_leaf_ops.argtypes = [C.c_int, C.c_double, C.c_double] + [dp] * 8
+    for p, side, a in [(16, 2.0 / 256, 1.0), (12, 0.25, 2.5), (8, 2.0, -0.7)]:
+        n1, q = p - 2, p - 2
+        A, V, Vi = (np.zeros((n1, n1)) for _ in range(3))
+        lam = np.zeros(n1)
+        G, d = np.zeros((q, n1)), np.zeros((4, n1))
+        ds = C.c_double()
+        Qi = np.zeros((n1 * n1, 4 * q))
+        assert L.hpsg_fdm_leaf_ops(p, side, a, HP._dp(A), HP._dp(lam), HP._dp(V), HP._dp(Vi), HP._dp(G), HP._dp(d),
+                                   C.byref(ds), HP._dp(Qi)) == 0
+        Qi = Qi.T                        # (4q, n1^2), interior column r = (i1-1) n1 + (i2-1)
+        A, V, Vi = A.T, V.T, Vi.T        # column-major -> (rows, cols)
+        scale = np.abs(A).max()
+        assert np.abs(V @ np.diag(lam) @ Vi - A).max() < 1e-12 * scale
+        assert np.abs(V @ Vi - np.eye(n1)).max() < 1e-12
+        assert np.all(np.isreal(lam)) and len(set(lam.round(6))) == n1
+        assert abs(ds.value - 2.0 / side) < 1e-15 * ds.value
+        # the separable factors reproduce the dense interior Q exactly (one product per entry, same rounding)
+        Qs = np.zeros_like(Qi)
+        for sd in range(4):
+            for i in range(q):
+                for i1 in range(n1):
+                    for i2 in range(n1):
+                        m, k = (i1, i2) if sd in (0, 2) else (i2, i1)
+                        Qs[sd * q + i, i1 * n1 + i2] = ds.value * (G[i, m] * d[sd, k])
+        assert np.array_equal(Qs, Qi)
+    assert L.hpsg_fdm_leaf_ops(3, 1.0, 1.0, *([None] * 8)) != 0
