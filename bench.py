@@ -251,6 +251,10 @@ def run_b200(args):
                            "achieved": flops / (t_build / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                            "frac": flops / (t_build / 1e3) / 1e12 / FP64_PEAK_TFLOPS, "algorithmic_flops": flops,
                            "note": "SURVEY 8d dense-equivalent counts; the block-sparse Schur products skip zero blocks"},
+        # the leaf kernel above is the one the round-1 review named; by launch-time share the dominant kernel is now
+        # the DMMA GEMM (all launches together ~49 % of the step, profiles/r02_launch_summary_v3.txt), whose live
+        # roofline is roofline_gemm (the largest launch keeps the DMMA pipe 91 % active, profiles/r02_gemm_d1_*)
+        "dominant_kernel": "dgemm_tma_kernel (roofline_gemm)",
         "roofline_gemm": None if gemm_live is None else {
             "bound": "tensor", "kernel": f"dgemm_tma_kernel (all {gemm_live['launches']} build launches: LU trailing "
                                          "updates + block-sparse Schur products)",
