@@ -326,8 +326,9 @@ def bench_multi_rhs(solver, tree, torch, args, nrhs=256, chunk=64):
 
 def bench_new_sources(torch, args, nsrc=256, chunk=32):
     """BASELINE configs[2] (ii): 256 new SOURCE right-hand sides against one stored build
-    (HpsSolver::solve_new_source: leaf re-solves with the kept LU factors, the upward source
-    pass through the stored merge factors, then the downward pass), chunks of 32 sources."""
+    (HpsSolver::solve_new_source: leaf re-solves -- the fast-diagonalisation iteration on the new sources where
+    the leaves allow it, else the kept LU factors -- the upward source pass through the stored merge factors,
+    then the downward pass), chunks of 32 sources."""
     import paper_2503_17535_b200 as H
     from paper_2503_17535_b200 import problems as PR
     prob = PR.helmholtz_bumps(k=args.k, seed=args.seed)
@@ -354,7 +355,8 @@ def bench_new_sources(torch, args, nsrc=256, chunk=32):
     st = s.stats()
     s.close()
     return {"workload": f"2D Helmholtz p={tree.p} L={tree.L}: {nsrc} source RHS (smooth seeded fields) + boundary "
-                        f"data on one build with kept leaf factors, chunks of {chunk}",
+                        f"data on one keep_factors build (leaf path {st['leaf_path']}: 2 = fast-diagonalisation re-solves, "
+                        f"1 = kept LU factors), chunks of {chunk}",
             "ms": ms, "ms_per_source": ms / nsrc, "rhs_dof_per_s": nsrc * tree.total_points / (ms / 1e3),
             "build_ms_keep_factors": st["t_build_ms"], "device_gb": st["device_bytes"] / 1e9}
 

@@ -339,7 +339,7 @@ void setup(hpsg_ctx* c) {
 void setup_fdm(hpsg_ctx* c) {
   const hpsg::LeafOperators& o = c->ops;
   const int pp = c->tree.p, n1p = pp - 2;
-  if (c->tree.dim != 2 || c->opts.keep_factors || !hpsk::leaf_fdm_shape_ok(pp, n1p * n1p, 4 * n1p, 2)) return;
+  if (c->tree.dim != 2 || !hpsk::leaf_fdm_shape_ok(pp, n1p * n1p, 4 * n1p, 2)) return;
   int nlap = 0;
   double a = 0.0;
   for (int i = 0; i < c->nterms; ++i) {
@@ -438,11 +438,14 @@ void alloc_build(hpsg_ctx* c) {
   bool mixed = false;
   for (int i = 0; i < c->nterms; ++i)
     if (c->terms[i].role == HPSG_ROLE_SECOND_ORDER && c->terms[i].axis != c->terms[i].axis2) mixed = true;
-  c->fused = hpsk::leaf_fused_supported(o.n, o.p, o.ni, o.nb, c->tree.dim, mixed) && !c->opts.force_batched_leaf;
-  if (c->opts.keep_factors || c->iti) c->fused = false;  // batched path: keeps [LU | v | Y] + pivots; ItI
-  if (c->T.cut) c->fused = false;  // no leaf stage: the part's leaves are input nodes
+  const bool fused_ok = hpsk::leaf_fused_supported(o.n, o.p, o.ni, o.nb, c->tree.dim, mixed) &&
+                        !c->opts.force_batched_leaf && !c->T.cut;  // cut parts: no leaf stage (input nodes)
+  c->fused = fused_ok && !c->opts.keep_factors && !c->iti;  // batched path: keeps [LU | v | Y] + pivots; ItI
   c->fdm = false;
-  if ((c->fused || c->iti) && !c->opts.force_lu_leaf) setup_fdm(c);
+  if ((fused_ok || c->iti) && !c->opts.force_lu_leaf) setup_fdm(c);
+  // keep_factors with fast-diagonalisation leaves: no leaf factors to keep -- solve_new_source re-runs the
+  // iteration on the new sources (run_source_pass)
+  if (c->fdm && c->opts.keep_factors && !c->iti) c->fused = true;
   if (c->T.cut) {
     // no leaf stage
   } else if (c->fused) {
@@ -705,10 +708,39 @@ bool run_iti_fdm_leaf(hpsg_ctx* c, const hpsk::LeafAsmArgs& a0) {
   return true;
 }
 
-void run_leaf_stage(hpsg_ctx* c) {
+hpsk::LeafAsmArgs leaf_asm_args(hpsg_ctx* c);
+
+// the fast-diagonalisation kernel's arguments for the build (run_leaf_stage adjusts them for ItI; the new-source
+// pass switches to source mode)
+hpsk::LeafFdmArgs fdm_args(hpsg_ctx* c) {
+  hpsk::LeafFdmArgs f{};
+  f.a = leaf_asm_args(c);
+  f.P = c->P.d();
+  f.Qi = c->Qi.d();
+  f.ZQeP = c->ZQeP.d();
+  f.V = c->fdmV.d();
+  f.Vinv = c->fdmVinv.d();
+  f.A = c->fdmA.d();
+  f.lam = c->fdmLam.d();
+  f.lap_coef = c->fdm_lap;
+  f.qG = c->fdmQG.d();
+  f.qd = c->fdmQd.d();
+  f.qds = c->fdm_qds;
+  f.Rtab = c->fdmRtab.d();
+  f.Rhat = c->fdmRhat.d();
+  f.Yv = c->leafYv.d();
+  f.strideYv = c->yv_stride;
+  f.HT = c->leafHT.d();
+  f.strideHT = c->strideLeafHT();
+  f.stats = c->leafStats.d();
+  f.fail_count = c->fdmFail.i();
+  f.fail_list = c->fdmFail.i() + 1;
+  f.n_leaves = c->T.n_leaves();
+  return f;
+}
+
+hpsk::LeafAsmArgs leaf_asm_args(hpsg_ctx* c) {
   const hpsg::LeafOperators& o = c->ops;
-  const int nl = c->T.n_leaves();
-  const long long sM = c->strideLeafM();
   hpsk::LeafAsmArgs a{};
   a.dim = c->tree.dim;
   a.p = c->tree.p;
@@ -729,10 +761,18 @@ void run_leaf_stage(hpsg_ctx* c) {
   a.interior = c->interior.i();
   a.exterior = c->exterior.i();
   a.M = c->leafM.d();
-  a.strideM = sM;
+  a.strideM = c->strideLeafM();
   a.E = c->leafE.d();
   a.strideE = (long long)o.ni * o.ne;
   a.bad_point = c->leafBad.i();
+  return a;
+}
+
+void run_leaf_stage(hpsg_ctx* c) {
+  const hpsg::LeafOperators& o = c->ops;
+  const int nl = c->T.n_leaves();
+  const long long sM = c->strideLeafM();
+  const hpsk::LeafAsmArgs a = leaf_asm_args(c);
   if (c->iti) {
     // local_solve_iti (local_solve.cpp:145-172), real-equivalent: [B | f | [P;0], i[P;0]] -> LU -> [v | Y]
     const hpsg::ItiLeafOperators& io = c->iops;
@@ -785,29 +825,7 @@ void run_leaf_stage(hpsg_ctx* c) {
   const int* leaf_list = nullptr;
   long long leaf_count = nl;
   if (c->fdm) {
-    hpsk::LeafFdmArgs f{};
-    f.a = a;
-    f.P = c->P.d();
-    f.Qi = c->Qi.d();
-    f.ZQeP = c->ZQeP.d();
-    f.V = c->fdmV.d();
-    f.Vinv = c->fdmVinv.d();
-    f.A = c->fdmA.d();
-    f.lam = c->fdmLam.d();
-    f.lap_coef = c->fdm_lap;
-    f.qG = c->fdmQG.d();
-    f.qd = c->fdmQd.d();
-    f.qds = c->fdm_qds;
-    f.Rtab = c->fdmRtab.d();
-    f.Rhat = c->fdmRhat.d();
-    f.Yv = c->leafYv.d();
-    f.strideYv = c->yv_stride;
-    f.HT = c->leafHT.d();
-    f.strideHT = c->strideLeafHT();
-    f.stats = c->leafStats.d();
-    f.fail_count = c->fdmFail.i();
-    f.fail_list = c->fdmFail.i() + 1;
-    f.n_leaves = nl;
+    hpsk::LeafFdmArgs f = fdm_args(c);
     ck(cudaMemsetAsync(c->fdmFail.p, 0, sizeof(int), c->st), "fdm flag");
     if (!c->fdm_prepped) {  // once per context: the leaf-independent right-hand sides
       ck(hpsk::launch_leaf_fdm_prep(f, c->st), "leaf_fdm_prep");
@@ -820,6 +838,21 @@ void run_leaf_stage(hpsg_ctx* c) {
     ck(cudaMemcpyAsync(&nfail, c->fdmFail.p, sizeof(int), cudaMemcpyDeviceToHost, c->st), "fdm count D2H");
     ck(cudaStreamSynchronize(c->st), "fdm sync");
     c->stats.leaf_path = nfail ? 3 : 2;
+    if (nfail && c->opts.keep_factors) {
+      // solve_new_source needs every leaf's solve operator: when some leaf does not converge, the context moves to
+      // the batched LU leaf path, which keeps the factors (its buffers are allocated now)
+      const long long nl2 = c->T.n_leaves();
+      c->leafM.alloc(size_t(nl2) * c->strideLeafM() * 8, &c->dev_bytes);
+      c->leafE.alloc(size_t(nl2) * o.ni * o.ne * 8, &c->dev_bytes);
+      c->leafPiv.alloc(size_t(nl2) * o.ni * 4, &c->dev_bytes);
+      c->yv = c->leafM.d() + (long long)o.ni * o.ni;
+      c->yv_stride = c->strideLeafM();
+      c->fused = false;
+      c->fdm = false;
+      ck(hpsk::lu_workspace_reserve(c->luws, int(nl2), o.ni, 1 + o.nb, true, false), "LU workspace");
+      run_leaf_stage(c);
+      return;
+    }
     if (!nfail) return;
     leaf_list = c->fdmFail.i() + 1;  // non-converged leaves: the fused LU kernel solves exactly those
     leaf_count = nfail;
@@ -1352,10 +1385,29 @@ void run_source_pass(hpsg_ctx* c, const double* d_f, int K) {
   const double sgn = c->opts.literal_sign ? -1.0 : 1.0;
   hpsk::launch_pack_source(c->srcR.d(), d_f, c->interior.i(), o.ni, o.n, int(nl), K, sgn, c->st);
   ++c->launches;
-  BatchedMat LU{c->leafM.d(), o.ni, c->strideLeafM()};
-  BatchedMat R{c->srcR.d(), o.ni, (long long)o.ni * K};
-  ck(hpsk::bgetrs(int(nl), o.ni, K, LU, c->leafPiv.i(), R, c->luws, c->st), "leaf source getrs");
-  c->launches += lu_launches(o.ni, K, false);
+  if (c->fdm) {
+    // v = L_ii^-1 (sgn f_i) by the fast-diagonalisation iteration, in place (leaf_resolve_source,
+    // local_solve.cpp:174-183, without stored factors)
+    hpsk::LeafFdmArgs f = fdm_args(c);
+    f.src_cols = K;
+    f.Yv = c->srcR.d();
+    f.strideYv = (long long)o.ni * K;
+    f.stats = nullptr;
+    ck(cudaMemsetAsync(c->fdmFail.p, 0, sizeof(int), c->st), "fdm flag");
+    ck(hpsk::launch_leaf_fdm(f, c->fdm_grid, c->st), "leaf_fdm (sources)");
+    ++c->launches;
+    int nfail = 0;
+    ck(cudaMemcpyAsync(&nfail, c->fdmFail.p, sizeof(int), cudaMemcpyDeviceToHost, c->st), "fdm count D2H");
+    ck(cudaStreamSynchronize(c->st), "fdm sync");
+    if (nfail)
+      throw HpsError{HPSG_ERR_INVALID, hpsg::fmt("solve_new_source: the fast-diagonalisation leaf solve did not "
+                                                 "converge on %d leaves; set hpsg_options.force_lu_leaf", nfail)};
+  } else {
+    BatchedMat LU{c->leafM.d(), o.ni, c->strideLeafM()};
+    BatchedMat R{c->srcR.d(), o.ni, (long long)o.ni * K};
+    ck(hpsk::bgetrs(int(nl), o.ni, K, LU, c->leafPiv.i(), R, c->luws, c->st), "leaf source getrs");
+    c->launches += lu_launches(o.ni, K, false);
+  }
   GemmArgs q;  // h = Q_i v
   q.m = o.nb;
   q.n = K;

@@ -173,6 +173,7 @@ struct LeafFdmArgs {
   int iti = 0;              // ItI mode: P = I (ne columns), two source columns, output Z = L_ii^-1 [f_i | -L_ie]
   DevField source_im;       // (Yv = Z, strideYv), no [h|T]
   int has_source_im = 0;
+  int src_cols = 0;         // source mode (> 0): src_cols columns per leaf read from Yv and solved in place
   double* Yv;
   long long strideYv;
   double* HT;

@@ -235,8 +235,11 @@ __global__ void __launch_bounds__(kT, HPS_FDM_MINB) leaf_fdm_kernel(const LeafFd
   const LeafAsmArgs& a = f.a;
   // DtN: column 0 = sgn f_i, columns 1..NB = -L_ie P.  ItI mode: columns 0, 1 = Re f_i, Im f_i, columns
   // 2..NE+1 = -L_ie e_k (the prep tables were made with P = I), output Z = L_ii^-1 [f_i | -L_ie] only.
-  const int nsrc = f.iti ? 2 : 1;
-  const int ncol = nsrc + (f.iti ? 4 * P - 4 : NB);
+  // Source mode (f.src_cols > 0, the new-source pass of solve_new_source): every column is a source read from
+  // f.Yv itself (sgn f_i in interior order, packed by the caller) and overwritten with L_ii^-1 of it.
+  const bool srcmode = f.src_cols > 0;
+  const int nsrc = srcmode ? f.src_cols : (f.iti ? 2 : 1);
+  const int ncol = srcmode ? f.src_cols : nsrc + (f.iti ? 4 * P - 4 : NB);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
   double vi[2][4], vv[2][4], aa[2][4];
   load_afrag(f.Vinv, vi, g, t4);
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(kT, HPS_FDM_MINB) leaf_fdm_kernel(const LeafFd
         if (!isfinite(v)) atomicMin(&s.bad, i);
         if (a.terms[t].role == 2) cz = __dadd_rn(cz, v);
       }
-      s.fsrc[0][i] = a.has_source ? eval_field_t<2>(a.source, x, leaf, i, NPT) : 0.0;
+      s.fsrc[0][i] = (a.has_source && !srcmode) ? eval_field_t<2>(a.source, x, leaf, i, NPT) : 0.0;
       if (f.iti) s.fsrc[1][i] = f.has_source_im ? eval_field_t<2>(f.source_im, x, leaf, i, NPT) : 0.0;
       const int r = s.pos[i];
       if (r >= 0) {
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(kT, HPS_FDM_MINB) leaf_fdm_kernel(const LeafFd
     dmin = s.wmin[0], dmax = s.wmax[0];
     for (int w = 1; w < kW; ++w) dmin = fmin(dmin, s.wmin[w]), dmax = fmax(dmax, s.wmax[w]);
     bool ok = s.bad == INT_MAX && dmin > 1e-12 * dmax && isfinite(cbar);
-    if (tid == 0) {
+    if (tid == 0 && !srcmode) {
       a.bad_point[leaf] = s.bad;
       f.stats[3 * leaf + 0] = dmin;  // spectral analogue of the pivot statistics: min / max |lam_i + lam_j + cbar|
       f.stats[3 * leaf + 1] = dmax;
@@ -338,6 +341,12 @@ __global__ void __launch_bounds__(kT, HPS_FDM_MINB) leaf_fdm_kernel(const LeafFd
             reinterpret_cast<double2*>(Rb)[e] = __ldg(Rt + e);
             reinterpret_cast<double2*>(Xb)[e] = __ldg(Rh + e);
           }
+        } else if (srcmode) {
+          const double* src = f.Yv + leaf * f.strideYv + (long long)col * NI;
+          for (int e = lane; e < kBlk; e += 32) {
+            const int cc = e >> 4, row = (e & 15) ^ swx(cc);
+            Rb[e] = (row < N1 && cc < N1) ? src[cc * N1 + row] : 0.0;
+          }
         } else {
           for (int e = lane; e < kBlk; e += 32) {
             const int cc = e >> 4, row = (e & 15) ^ swx(cc);
@@ -345,12 +354,12 @@ __global__ void __launch_bounds__(kT, HPS_FDM_MINB) leaf_fdm_kernel(const LeafFd
           }
         }
         __syncwarp();
-        conv = solve_block(Rb, Xb, Wb, s, vi, vv, aa, g, t4, npass, col >= nsrc) && conv;
+        conv = solve_block(Rb, Xb, Wb, s, vi, vv, aa, g, t4, npass, !srcmode && col >= nsrc) && conv;
         // [v_i | Y_i] column (interior index r = (i1-1) N1 + (i2-1)); ItI mode: the column of Z
         double* Yv = f.Yv + leaf * f.strideYv + (long long)col * NI;
 #pragma unroll
         for (int r = lane; r < NI; r += 32) __stcs(&Yv[r], Xb[swz(r % N1, r / N1)]);
-        if (f.iti) {
+        if (f.iti || srcmode) {
           __syncwarp();
           continue;
         }
@@ -407,7 +416,7 @@ __global__ void __launch_bounds__(kT, HPS_FDM_MINB) leaf_fdm_kernel(const LeafFd
     __syncthreads();
     if (tid == 0) {
       if (s.failed) f.fail_list[atomicAdd(f.fail_count, 1)] = int(leaf);
-      f.stats[3 * leaf + 2] = -1.0 - double(s.ndmma);  // < 0: no zero pivot; the LU fallback rewrites it to -1
+      if (!srcmode) f.stats[3 * leaf + 2] = -1.0 - double(s.ndmma);  // < 0: no zero pivot; the LU fallback rewrites it
     }
   }
 }
