@@ -159,3 +159,30 @@ def test_iti_block_elimination_plane_wave():
     ex = u(s.leaf_points())
     U = s.solve_complex(g)
     assert np.abs(U - ex).max() / np.abs(ex).max() < 1e-10
+
+
+@pytest.mark.parametrize("p", [4, 5, 6, 7, 10])
+def test_fdm_small_and_odd_orders(p):
+    """Every compiled leaf order (the kernel is instantiated for p = 4..16) matches the LU leaf kernel."""
+    prob = PR.helmholtz_bumps(k=6.0)
+    a, b = solver(prob, p, 4), solver(prob, p, 4, fdm=False)
+    assert a.stats()["leaf_path"] in (LEAF_PATH_FDM, LEAF_PATH_FDM_FALLBACK)
+    for o in (0, a.tree.n_leaves - 1):
+        for x, y in zip(a.get_leaf(o), b.get_leaf(o)):
+            assert rel(x, y) < 1e-12
+    g = prob.boundary(a.root_boundary_points())
+    assert rel(a.solve(g), b.solve(g)) < 1e-10
+
+
+def test_fdm_negative_laplacian_coefficient():
+    """-Delta u + c u = f (a negative constant Laplacian coefficient, positive zeroth-order term): the
+    eigendecomposition and the Richardson iteration are sign-agnostic."""
+    terms = [H.Term(H.ROLE_LAPLACIAN, H.Field.const(-1.0)), H.Term(H.ROLE_ZEROTH, H.Field.const(4.0))]
+    tree = H.build_uniform_tree(-1.0, 1.0, 4, 2, 12)
+    out = []
+    for fdm in (True, False):
+        s = H.HpsSolver(tree, terms, H.Field.const(1.0), literal_sign=False, fdm_leaf=fdm)
+        s.build()
+        out.append((s.stats()["leaf_path"], s.solve(np.zeros(s.nb_root))))
+    assert out[0][0] == LEAF_PATH_FDM
+    assert rel(out[0][1], out[1][1]) < 1e-11
