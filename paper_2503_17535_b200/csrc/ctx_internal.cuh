@@ -167,6 +167,9 @@ struct hpsg_ctx {
   long long strideLeafM() const { return (long long)ops.ni * (ops.ni + 1 + ops.nb); }
   // [h|T] per part leaf: a real leaf (nb x (1+nb)) or, for a cut part, an input node
   int leaf_nb() const { return T.cut ? lv[T.L - 1].child_nb : ops.nb; }
+  // leading dimension of the leaves' [1; g] columns in the solve: 1 + nb rounded up to even for leaf-owning
+  // contexts (16-byte aligned columns: the leaf products' B operand is TMA-legal), 1 + nb for cut inputs
+  long long ldG_leaf() const { return T.cut ? 1 + leaf_nb() : (2 + (long long)leaf_nb()) & ~1LL; }
   long long strideLeafHT() const { return (long long)leaf_nb() * (1 + leaf_nb()); }
   // the merge at part depth d is the reference's root merge (no T/h, optional implicit S)
   bool global_root(int d) const { return d == 0 && T.root_depth == 0; }

@@ -1144,8 +1144,8 @@ void ensure_solve_ws(hpsg_ctx* c, int nrhs) {
   for (int d = 0; d <= Lh; ++d) {
     if (!c->G[d]) c->G[d] = std::make_unique<DevBuf>();
     const long long nodes = c->T.level_count(d);
-    const long long nb = d < Lh ? c->lv[d].n_ext : c->leaf_nb();
-    c->G[d]->alloc(size_t(nodes) * (1 + nb) * nrhs * 8, tot);
+    const long long ldg = d < Lh ? 1 + c->lv[d].n_ext : c->ldG_leaf();
+    c->G[d]->alloc(size_t(nodes) * ldg * nrhs * 8, tot);
     if (d < Lh) {
       if (!c->GI[d]) c->GI[d] = std::make_unique<DevBuf>();
       c->GI[d]->alloc(size_t(nodes) * c->lv[d].n_int * nrhs * 8, tot);
@@ -1242,14 +1242,14 @@ void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_
     s.ldGI = L.n_int;
     s.strideGI = sGI;
     s.Gc = c->G[d + 1]->d();
-    s.ldGc = 1 + L.child_nb;
-    s.strideGc = (long long)(1 + L.child_nb) * nrhs;
+    s.ldGc = d + 1 == Lh ? c->ldG_leaf() : 1 + L.child_nb;
+    s.strideGc = s.ldGc * nrhs;
     hpsk::launch_scatter(s, int(L.nodes), c->st);
     ++c->launches;
   }
   if (c->T.cut) {
     // cut part: the boundary data of its input nodes is the result (nrhs x n_cut x cut_nb)
-    hpsk::launch_unpack_leaf_g(d_leaf_g, c->G[Lh]->d(), c->leaf_nb(), nrhs, c->T.n_leaves(), c->st);
+    hpsk::launch_unpack_leaf_g(d_leaf_g, c->G[Lh]->d(), c->leaf_nb(), c->ldG_leaf(), nrhs, c->T.n_leaves(), c->st);
     ++c->launches;
     ck(cudaGetLastError(), "solve kernels");
     return;
@@ -1257,7 +1257,7 @@ void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_
   // leaves: u_i = [v | Y_i][1; g],  u_e = P g   (solver.cpp:230-236)
   const hpsg::LeafOperators& o = c->ops;
   const int nl = c->T.n_leaves();
-  const long long ldGL = 1 + o.nb, sGL = ldGL * nrhs;
+  const long long ldGL = c->ldG_leaf(), sGL = ldGL * nrhs;
   GemmArgs g;
   g.m = o.ni;
   g.n = nrhs;
@@ -1297,7 +1297,7 @@ void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_
     e.drow = c->exterior.i();
     gemm(c, e);
     if (d_leaf_g) {
-      hpsk::launch_unpack_leaf_g(d_leaf_g, c->G[Lh]->d(), o.nb, nrhs, nl, c->st);
+      hpsk::launch_unpack_leaf_g(d_leaf_g, c->G[Lh]->d(), o.nb, ldGL, nrhs, nl, c->st);
       ++c->launches;
     }
     ck(cudaGetLastError(), "solve kernels");
@@ -1350,7 +1350,7 @@ void run_solve(hpsg_ctx* c, const double* d_g, int nrhs, double* d_u, double* d_
   hpsk::launch_leaf_output(lo, c->st);
   ++c->launches;
   if (d_leaf_g) {
-    hpsk::launch_unpack_leaf_g(d_leaf_g, c->G[Lh]->d(), o.nb, nrhs, nl, c->st);
+    hpsk::launch_unpack_leaf_g(d_leaf_g, c->G[Lh]->d(), o.nb, ldGL, nrhs, nl, c->st);
     ++c->launches;
   }
   ck(cudaGetLastError(), "solve kernels");

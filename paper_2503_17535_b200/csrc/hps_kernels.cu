@@ -430,7 +430,7 @@ __global__ void pack_root_kernel(double* G, const double* g, int nb, int nrhs, d
   G[e] = r == 0 ? lead : g[(long long)c * nb + r - 1];
 }
 
-__global__ void unpack_leaf_g_kernel(double* out, const double* G, int nb, int nrhs, int n_leaves) {
+__global__ void unpack_leaf_g_kernel(double* out, const double* G, int nb, long long ldg, int nrhs, int n_leaves) {
   const long long total = (long long)nb * nrhs * n_leaves;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
@@ -438,7 +438,7 @@ __global__ void unpack_leaf_g_kernel(double* out, const double* G, int nb, int n
     const long long lr = e / nb;
     const long long leaf = lr % n_leaves;
     const int rhs = int(lr / n_leaves);
-    out[e] = G[leaf * (long long)(nb + 1) * nrhs + (long long)rhs * (nb + 1) + 1 + r];
+    out[e] = G[leaf * ldg * nrhs + (long long)rhs * ldg + 1 + r];
   }
 }
 
@@ -569,10 +569,10 @@ void launch_axpby(double* y, long long ldy, long long sy, const double* x, long 
   axpby_kernel<<<blocks, 256, 0, st>>>(y, ldy, sy, x, ldx, sx, n, nrhs, batch, a, b);
 }
 
-void launch_unpack_leaf_g(double* out, const double* G, int nb, int nrhs, int n_leaves, cudaStream_t st) {
+void launch_unpack_leaf_g(double* out, const double* G, int nb, long long ldg, int nrhs, int n_leaves, cudaStream_t st) {
   const long long total = (long long)nb * nrhs * n_leaves;
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 64);
-  unpack_leaf_g_kernel<<<blocks, 256, 0, st>>>(out, G, nb, nrhs, n_leaves);
+  unpack_leaf_g_kernel<<<blocks, 256, 0, st>>>(out, G, nb, ldg, nrhs, n_leaves);
 }
 
 }  // namespace hpsk

@@ -249,6 +249,6 @@ void launch_pack_source(double* R, const double* f, const int* interior, int ni,
 void launch_axpby(double* y, long long ldy, long long sy, const double* x, long long ldx, long long sx, int n,
                   int nrhs, long long batch, double a, double b, cudaStream_t st);
 // Extract leaf boundary data (without the leading 1) for leaf_g_out.
-void launch_unpack_leaf_g(double* out, const double* G, int nb, int nrhs, int n_leaves, cudaStream_t st);
+void launch_unpack_leaf_g(double* out, const double* G, int nb, long long ldg, int nrhs, int n_leaves, cudaStream_t st);
 
 }  // namespace hpsk
