@@ -110,6 +110,8 @@ struct hpsg_ctx {
   bool own_stream = true;
   cudaEvent_t ev[8] = {};
   cudaEvent_t lev_ev[25] = {};  // merge level boundaries
+  cudaStream_t gst = nullptr;   // merge gathers of B and [h_ext | A], overlapped with the level's LU
+  cudaEvent_t gev[2] = {};      // [0]: main stream up to the level, [1]: those gathers done
   hpsg_tree tree{};
   hpsg_part part{};  // (0, 0, L) for the whole tree
   bool iti = false;  // ItI variant (real-equivalent complex)

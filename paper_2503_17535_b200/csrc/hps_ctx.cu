@@ -953,6 +953,9 @@ void run_leaf_stage(hpsg_ctx* c) {
   gemm(c, t);
 }
 
+#ifndef HPS_GATHER_OVERLAP
+#define HPS_GATHER_OVERLAP 1
+#endif
 void run_merge_level(hpsg_ctx* c, int d) {
   Level& L = c->lv[d];
   const bool root = !c->forms_T(d);
@@ -995,6 +998,39 @@ void run_merge_level(hpsg_ctx* c, int d) {
   ga.child_stride = child_stride;
   ga.NI = L.mt.NI;
   ga.NE = L.mt.NE;
+  if (!root) {
+    // B and [h_ext | A] are only needed by the Schur product: gathered on a second stream while the main
+    // stream gathers [D | h_int | C] and factors it (the gathers are HBM-bound, the LU latency-bound)
+    if (HPS_GATHER_OVERLAP && !c->gst) {
+      ck(cudaStreamCreateWithFlags(&c->gst, cudaStreamNonBlocking), "gather stream");
+      for (auto& e : c->gev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "gather event");
+    }
+    cudaStream_t gs = c->st;
+    if (HPS_GATHER_OVERLAP) {
+      ck(cudaEventRecord(c->gev[0], c->st), "gather fork");
+      ck(cudaStreamWaitEvent(c->gst, c->gev[0], 0), "gather fork wait");
+      gs = c->gst;
+    }
+    hpsk::GatherArgs gb = ga;
+    gb.src = L.b_src.i();
+    gb.kind = 1;
+    gb.nrows = L.n_ext;
+    gb.ncols = L.n_int;
+    gb.dst = c->Bscratch.d();
+    gb.ld = L.n_ext;
+    gb.stride = (long long)L.n_ext * L.n_int;
+    hpsk::launch_gather(gb, int(L.nodes), gs);
+    gb.src = L.ah_src.i();
+    gb.kind = 2;
+    gb.nrows = L.n_ext;
+    gb.ncols = 1 + L.n_ext;
+    gb.dst = L.AH.d();
+    gb.ld = L.n_ext;
+    gb.stride = L.strideAH();
+    hpsk::launch_gather(gb, int(L.nodes), gs);
+    c->launches += 2;
+    if (HPS_GATHER_OVERLAP) ck(cudaEventRecord(c->gev[1], c->gst), "gather join");
+  }
   // [D | h_int | C]
   ga.src = L.md_src.i();
   ga.kind = 0;
@@ -1005,25 +1041,6 @@ void run_merge_level(hpsg_ctx* c, int d) {
   ga.stride = L.strideMD();
   hpsk::launch_gather(ga, int(L.nodes), c->st);
   ++c->launches;
-  if (!root) {
-    ga.src = L.b_src.i();
-    ga.kind = 1;
-    ga.nrows = L.n_ext;
-    ga.ncols = L.n_int;
-    ga.dst = c->Bscratch.d();
-    ga.ld = L.n_ext;
-    ga.stride = (long long)L.n_ext * L.n_int;
-    hpsk::launch_gather(ga, int(L.nodes), c->st);
-    ga.src = L.ah_src.i();
-    ga.kind = 2;
-    ga.nrows = L.n_ext;
-    ga.ncols = 1 + L.n_ext;
-    ga.dst = L.AH.d();
-    ga.ld = L.n_ext;
-    ga.stride = L.strideAH();
-    hpsk::launch_gather(ga, int(L.nodes), c->st);
-    c->launches += 2;
-  }
   ck(cudaGetLastError(), "gather");
   }
   ck(hpsk::lu_stats_init(L.stats.d(), int(L.nodes), c->st), "stats init");
@@ -1077,6 +1094,7 @@ void run_merge_level(hpsg_ctx* c, int d) {
   ck(hpsk::bgetrf_aug(int(L.nodes), L.n_int, m, M, L.piv.i(), L.stats.d(), c->luws, c->st, keep_L), "merge bgetrf");
   c->launches += lu_launches(L.n_int, m, true);
   }
+  if (!root && !c->iti && HPS_GATHER_OVERLAP) ck(cudaStreamWaitEvent(c->st, c->gev[1], 0), "gather join wait");
   if (!root && !c->iti && L.mt.s >= kSparseSchurMinS) {
     // [h | T] = [h_ext | A] - B [x_h | X] over the nonzero blocks of B only: section e's rows get
     // -B_{e,I} [x_h|X]_I for the runs I of interfaces of e's child (the other blocks of B are
@@ -2222,6 +2240,10 @@ void hpsg_destroy(hpsg_ctx* c) {
       if (e) cudaEventDestroy(e);
     for (auto& e : tmp->lev_ev)
       if (e) cudaEventDestroy(e);
+    if (tmp->gst) cudaStreamSynchronize(tmp->gst);
+    for (auto& e : tmp->gev)
+      if (e) cudaEventDestroy(e);
+    if (tmp->gst) cudaStreamDestroy(tmp->gst);
     cudaStream_t st = tmp->own_stream ? tmp->st : nullptr;
     hpsk::lu_workspace_free(tmp->luws);
     delete tmp;  // frees device buffers
