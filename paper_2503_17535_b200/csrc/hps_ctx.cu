@@ -1019,7 +1019,9 @@ void run_merge_level(hpsg_ctx* c, int d) {
     gb.dst = c->Bscratch.d();
     gb.ld = L.n_ext;
     gb.stride = (long long)L.n_ext * L.n_int;
+    gb.skip_zero = L.mt.s >= kSparseSchurMinS;   // the block-sparse Schur product reads only B's nonzero blocks
     hpsk::launch_gather(gb, int(L.nodes), gs);
+    gb.skip_zero = false;
     gb.src = L.ah_src.i();
     gb.kind = 2;
     gb.nrows = L.n_ext;

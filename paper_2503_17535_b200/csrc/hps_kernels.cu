@@ -1,5 +1,6 @@
 // hps_kernels.cu -- see hps_kernels.cuh.
 #include <climits>
+#include <stdexcept>
 
 #include "hps_kernels.cuh"
 #include "leaf_common.cuh"
@@ -259,16 +260,19 @@ __global__ void __launch_bounds__(256) error_partials_kernel(const ErrArgs a) {
 constexpr int kGatherThreads = 256;
 
 // One warp per destination column: (slot, cc) are uniform over the column and the rows of each
-// section are a contiguous run in both source and destination, so loads and stores coalesce and
-// the only per-element index math is one 32-bit division by the section size.
+// section are a contiguous run in both source and destination, so loads and stores coalesce.  The
+// column's per-section source offsets (at most 32 sections: NI, NE <= 24) are resolved once into shared
+// memory; a row then costs one multiply-high (section = r / s) and one shared load per source.
 __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const GatherArgs a) {
+  __shared__ long long soff[kGatherThreads / 32][32][2];
   const long long node = blockIdx.x;
   const int s = a.s;
   const int nslots = a.kind == 0 ? a.NI + 1 + a.NE : (a.kind == 1 ? a.NI : 1 + a.NE);
   double* dst = a.dst + node * a.stride + blockIdx.z * a.dst_rhs_stride;
   const double* ch0 = a.child_HT + node * a.nchild * a.child_stride + blockIdx.z * a.src_rhs_stride;
-  const int lane = threadIdx.x & 31, nw = kGatherThreads / 32;
-  for (int dcolumn = blockIdx.y * nw + (threadIdx.x >> 5); dcolumn < a.ncols; dcolumn += gridDim.y * nw) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kGatherThreads / 32;
+  const int nsec = (a.nrows + s - 1) / s;   // <= 32 (launch_gather)
+  for (int dcolumn = blockIdx.y * nw + warp; dcolumn < a.ncols; dcolumn += gridDim.y * nw) {
     const int col = dcolumn + a.col_offset;
     int slot, cc;
     if (a.kind == 0) {
@@ -294,32 +298,47 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const GatherArgs
       slot = 1 + (col - 1) / s;
       cc = (col - 1) % s;
     }
+    __syncwarp();
+    if (lane < nsec) {
+      const int* tab = a.src + 2 * (lane * nslots + slot);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int code = __ldg(tab + k);
+        long long o = -1;
+        if (code >= 0) {
+          const int child = code >> 6, rf = (code >> 3) & 7, cfp1 = code & 7;
+          const long long hc = cfp1 == 0 ? 0 : 1 + (long long)(cfp1 - 1) * s + cc;
+          o = child * a.child_stride + hc * a.child_nb + rf * s;
+        }
+        soff[warp][lane][k] = o;
+      }
+    }
+    __syncwarp();
     double* dcol = dst + (long long)dcolumn * a.ld;
     // four rows per lane per batch: every operand load of the batch is issued before its stores
     // (the sources are read-only here, __ldg), so the loop is not one memory latency per row
     for (int r0 = lane; r0 < a.nrows; r0 += 128) {
       double v[4];
+      bool nz[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int r = r0 + 32 * q;
         v[q] = 0.0;
+        nz[q] = false;
         if (r < a.nrows) {
-          const int rsec = r / s, rr = r - rsec * s;
-          const int* tab = a.src + 2 * (rsec * nslots + slot);
+          const int rsec = a.smagic ? (int)__umulhi((unsigned)r, a.smagic) : r / s, rr = r - rsec * s;
 #pragma unroll
           for (int k = 0; k < 2; ++k) {
-            const int code = __ldg(tab + k);
-            if (code < 0) continue;
-            const int child = code >> 6, rf = (code >> 3) & 7, cfp1 = code & 7;
-            const double* T = ch0 + child * a.child_stride;
-            const long long hc = cfp1 == 0 ? 0 : 1 + (long long)(cfp1 - 1) * s + cc;
-            v[q] += __ldg(T + hc * a.child_nb + rf * s + rr);
+            const long long o = soff[warp][rsec][k];
+            if (o < 0) continue;
+            nz[q] = true;
+            v[q] += __ldg(ch0 + o + rr);
           }
         }
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        if (r0 + 32 * q < a.nrows) dcol[r0 + 32 * q] = v[q];
+        if (r0 + 32 * q < a.nrows && (nz[q] || !a.skip_zero)) dcol[r0 + 32 * q] = v[q];
     }
   }
 }
@@ -496,7 +515,11 @@ void launch_leaf_assemble(const LeafAsmArgs& a, int n_leaves, cudaStream_t st) {
   leaf_assemble_kernel<<<n_leaves, kAsmThreads, 0, st>>>(a);
 }
 
-void launch_gather(const GatherArgs& a, int n_nodes, cudaStream_t st) {
+void launch_gather(const GatherArgs& a0, int n_nodes, cudaStream_t st) {
+  GatherArgs a = a0;
+  if ((a.nrows + a.s - 1) / a.s > 32) throw std::runtime_error("gather: more than 32 row sections");
+  // r / s as a multiply-high by ceil(2^32 / s): exact while r * s < 2^32
+  a.smagic = (a.s > 1 && (long long)a.nrows * a.s < (1LL << 32)) ? unsigned(((1ULL << 32) + a.s - 1) / a.s) : 0u;
   const int nw = kGatherThreads / 32;
   // enough column groups to fill the GPU (~8 CTAs per SM over all nodes), each warp a column
   const long long want = std::max<long long>(1, (148LL * 8 + n_nodes - 1) / n_nodes);

@@ -205,6 +205,10 @@ struct GatherArgs {
   // right-hand sides are gathered at once (child source / destination offsets per RHS)
   int col_offset = 0, nrhs = 1;
   long long src_rhs_stride = 0, dst_rhs_stride = 0;
+  // rows with no source (structurally zero blocks) are not stored: set when the consumer reads only the
+  // nonzero blocks (the block-sparse Schur product's B)
+  bool skip_zero = false;
+  unsigned smagic = 0;      // set by launch_gather
 };
 void launch_gather(const GatherArgs& a, int n_nodes, cudaStream_t st);
 
