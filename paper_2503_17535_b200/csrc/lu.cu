@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <climits>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -674,7 +675,13 @@ cudaError_t gemm_sub(int batch, int rows, int cols, int k, double alpha, const d
 // X_b = T_bb^-1 X_b, then X_i -= T_ib X_b for the remaining blocks i of the slab.
 constexpr int kSlabMinN = 64;  // measured: 64 beats 128 and 512 (d4-d6 merges) and 48 (d7)
 int slab_min_n() { return kSlabMinN; }
-constexpr int kSlabCW = 32;                 // strip width (4 warps x 8 columns)
+constexpr int kSlabCW = 32;                 // strip width (4 column groups x 8 columns)
+#ifndef HPS_SLAB_WARPS
+#define HPS_SLAB_WARPS 8
+#endif
+constexpr int kSlabWarps = HPS_SLAB_WARPS;  // 4: one warp per column group; 8: two warps per group split the rows
+constexpr int kSlabThreads = 32 * kSlabWarps;
+constexpr int kSlabRowSplit = kSlabWarps / 4;
 constexpr int kSlabLdX = kOuterNB + 4;      // 260 = 4 mod 16: conflict-free B fragments
 constexpr int kSlabChunk = 64;              // rows of T staged per update step
 constexpr int kSlabLdA = kSlabChunk + 4;    // 68
@@ -687,6 +694,8 @@ struct SlabArgs {
   long long ldX, strideX;
   int ncols;
   const double* Winv;   // [batch][kOuterNB / 32][32 x 32] diagonal-block inverses (column-major)
+  bool vec2;            // T, X 16-byte aligned with even leading dimensions, strides and r0: pairs of rows move as one
+                        // 16-byte cp.async / store
 };
 
 template <bool UPPER>
@@ -737,7 +746,7 @@ struct SlabItems {
 };
 
 template <bool UPPER>
-__global__ void __launch_bounds__(128) slab_trsm_kernel(const SlabArgs a) {
+__global__ void __launch_bounds__(kSlabThreads, kSlabWarps >= 16 ? 2 : 1) slab_trsm_kernel(const SlabArgs a) {
   extern __shared__ __align__(16) double smem[];
   double* xs = smem;                          // [kSlabCW][kSlabLdX]: X strip, k-major per column
   double* ring = xs + kSlabCW * kSlabLdX;     // 2 x [kLuNB][kSlabLdA]: A operand ([k][m]) per item
@@ -755,13 +764,22 @@ __global__ void __launch_bounds__(128) slab_trsm_kernel(const SlabArgs a) {
     const int bk = it.blk(step);
     if (chunk < 0) {
       const double* inv = winv + bk * (kLuNB * kLuNB);  // column-major: (m, k) at m + 32 k
-      for (int e = tid; e < kLuNB * kLuNB; e += blockDim.x) cp_async8(dst + (e / kLuNB) * kSlabLdA + e % kLuNB, inv + e, true);
+      for (int e = 2 * tid; e < kLuNB * kLuNB; e += 2 * blockDim.x)
+        cp_async16(dst + (e / kLuNB) * kSlabLdA + e % kLuNB, inv + e, 16);
     } else {
       const int q0 = it.rows_lo(bk) + chunk * kSlabChunk, qn = min(kSlabChunk, it.rows_hi(bk) - q0);
       const double* src = T + (long long)(a.r0 + bk * kLuNB) * a.ldT + a.r0 + q0;
-      for (int e = tid; e < kLuNB * kSlabChunk; e += blockDim.x) {
-        const int mm = e % kSlabChunk, k = e / kSlabChunk;
-        cp_async8(dst + k * kSlabLdA + mm, mm < qn ? src + (long long)k * a.ldT + mm : src, mm < qn);
+      if (a.vec2) {
+        for (int e = tid; e < kLuNB * kSlabChunk / 2; e += blockDim.x) {
+          const int mm = 2 * (e % (kSlabChunk / 2)), k = e / (kSlabChunk / 2);
+          const int valid = max(0, min(2, qn - mm)) * 8;
+          cp_async16(dst + k * kSlabLdA + mm, valid ? src + (long long)k * a.ldT + mm : src, valid);
+        }
+      } else {
+        for (int e = tid; e < kLuNB * kSlabChunk; e += blockDim.x) {
+          const int mm = e % kSlabChunk, k = e / kSlabChunk;
+          cp_async8(dst + k * kSlabLdA + mm, mm < qn ? src + (long long)k * a.ldT + mm : src, mm < qn);
+        }
       }
     }
     cp_async_commit();
@@ -777,13 +795,27 @@ __global__ void __launch_bounds__(128) slab_trsm_kernel(const SlabArgs a) {
 
   int step = 0, chunk = -1, slot = 0;
   stage(step, chunk, ring);
-  for (int e = tid; e < kSlabCW * kOuterNB; e += blockDim.x) {  // cp.async: every load in flight
-    const int r = e % kOuterNB, c = e / kOuterNB;
-    const bool ok = r < a.nbk && c0 + c < a.ncols;
-    cp_async8(xs + c * kSlabLdX + r, ok ? X + (long long)(c0 + c) * a.ldX + a.r0 + r : X, ok);
+  // cp.async: every load in flight; rows up to the 32-row padding of the last diagonal block (zero-filled
+  // past nbk: the padded inverse blocks multiply them by zero)
+  const int nbr = it.nblk * kLuNB;
+  for (int c = warp; c < kSlabCW; c += kSlabWarps) {
+    const bool okc = c0 + c < a.ncols;
+    const double* xc = X + (long long)(c0 + c) * a.ldX + a.r0;
+    if (a.vec2) {
+      for (int r = 2 * lane; r < nbr; r += 64) {
+        const int valid = okc ? max(0, min(2, a.nbk - r)) * 8 : 0;
+        cp_async16(xs + c * kSlabLdX + r, valid ? xc + r : X, valid);
+      }
+    } else {
+      for (int r = lane; r < nbr; r += 32) {
+        const bool ok = okc && r < a.nbk;
+        cp_async8(xs + c * kSlabLdX + r, ok ? xc + r : X, ok);
+      }
+    }
   }
   cp_async_commit();
-  const int wc = warp * 8;  // this warp's 8 columns of the strip
+  const int wc = (warp & 3) * 8;  // this warp's 8 columns of the strip
+  const int rh = warp >> 2;       // its share of the rows (kSlabRowSplit > 1)
   while (step < it.nblk) {
     int ns = step, nc = chunk;
     next(ns, nc);
@@ -793,35 +825,52 @@ __global__ void __launch_bounds__(128) slab_trsm_kernel(const SlabArgs a) {
     const double* A = ring + slot * (kLuNB * kSlabLdA);
     const int s0 = it.blk(step) * kLuNB;
     if (chunk < 0) {  // X_b <- T_bb^-1 X_b, in place (each warp reads and writes only its own columns)
-      double acc[kLuNB / 8][2];
+      constexpr int kT = kLuNB / 8 / kSlabRowSplit;  // 8-row tiles of this warp
+      double acc[kT][2];
 #pragma unroll
-      for (int mt = 0; mt < kLuNB / 8; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+      for (int i = 0; i < kT; ++i) acc[i][0] = acc[i][1] = 0.0;
 #pragma unroll
       for (int kb = 0; kb < kLuNB; kb += 4) {
         const double bv = xs[(wc + g) * kSlabLdX + s0 + kb + t4];
 #pragma unroll
-        for (int mt = 0; mt < kLuNB / 8; ++mt) dmma_8x8x4(acc[mt][0], acc[mt][1], A[(kb + t4) * kSlabLdA + mt * 8 + g], bv);
+        for (int i = 0; i < kT; ++i)
+          dmma_8x8x4(acc[i][0], acc[i][1], A[(kb + t4) * kSlabLdA + (rh * kT + i) * 8 + g], bv);
       }
-      __syncwarp();
+      if (kSlabRowSplit > 1)
+        __syncthreads();  // the other row half has read X_b
+      else
+        __syncwarp();
 #pragma unroll
-      for (int mt = 0; mt < kLuNB / 8; ++mt)
+      for (int i = 0; i < kT; ++i)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) xs[(wc + 2 * t4 + h) * kSlabLdX + s0 + mt * 8 + g] = acc[mt][h];
+        for (int h = 0; h < 2; ++h) xs[(wc + 2 * t4 + h) * kSlabLdX + s0 + (rh * kT + i) * 8 + g] = acc[i][h];
     } else {  // X_q -= T_qb X_b for this chunk's rows
       const int q0 = it.rows_lo(it.blk(step)) + chunk * kSlabChunk;
       const int qn = min(kSlabChunk, it.rows_hi(it.blk(step)) - q0);
       double bneg[kLuNB / 4];
 #pragma unroll
       for (int kb = 0; kb < kLuNB; kb += 4) bneg[kb / 4] = -xs[(wc + g) * kSlabLdX + s0 + kb + t4];
-      for (int mt = 0; mt < (qn + 7) / 8; ++mt) {
+      // two independent 8-row tiles per iteration (two DMMA accumulation chains in flight); the second tile
+      // of an odd count is computed on padding rows and not stored
+      const int nmt = (qn + 7) / 8;
+      for (int mt = 2 * rh; mt < nmt; mt += 2 * kSlabRowSplit) {
         const int r = q0 + mt * 8 + g;
-        double c[2];
+        double c[2], d[2];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) c[h] = xs[(wc + 2 * t4 + h) * kSlabLdX + r];
+        for (int h = 0; h < 2; ++h) {
+          c[h] = xs[(wc + 2 * t4 + h) * kSlabLdX + r];
+          d[h] = xs[(wc + 2 * t4 + h) * kSlabLdX + r + 8];
+        }
 #pragma unroll
-        for (int kb = 0; kb < kLuNB; kb += 4) dmma_8x8x4(c[0], c[1], A[(kb + t4) * kSlabLdA + mt * 8 + g], bneg[kb / 4]);
+        for (int kb = 0; kb < kLuNB; kb += 4) {
+          dmma_8x8x4(c[0], c[1], A[(kb + t4) * kSlabLdA + mt * 8 + g], bneg[kb / 4]);
+          dmma_8x8x4(d[0], d[1], A[(kb + t4) * kSlabLdA + mt * 8 + 8 + g], bneg[kb / 4]);
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) xs[(wc + 2 * t4 + h) * kSlabLdX + r] = c[h];
+        if (mt + 1 < nmt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) xs[(wc + 2 * t4 + h) * kSlabLdX + r + 8] = d[h];
       }
     }
     step = ns;
@@ -829,9 +878,19 @@ __global__ void __launch_bounds__(128) slab_trsm_kernel(const SlabArgs a) {
     slot ^= 1;
   }
   __syncthreads();
-  for (int e = tid; e < kSlabCW * kOuterNB; e += blockDim.x) {
-    const int r = e % kOuterNB, c = e / kOuterNB;
-    if (r < a.nbk && c0 + c < a.ncols) X[(long long)(c0 + c) * a.ldX + a.r0 + r] = xs[c * kSlabLdX + r];
+  for (int c = warp; c < kSlabCW && c0 + c < a.ncols; c += kSlabWarps) {
+    double* xc = X + (long long)(c0 + c) * a.ldX + a.r0;
+    const double* sc = xs + c * kSlabLdX;
+    if (a.vec2) {
+      for (int r = 2 * lane; r < a.nbk; r += 64) {
+        if (r + 1 < a.nbk)
+          *reinterpret_cast<double2*>(xc + r) = *reinterpret_cast<const double2*>(sc + r);
+        else
+          xc[r] = sc[r];
+      }
+    } else {
+      for (int r = lane; r < a.nbk; r += 32) xc[r] = sc[r];
+    }
   }
 }
 
@@ -878,10 +937,12 @@ cudaError_t slab_trsm(int batch, const double* T, long long ldT, long long sT, i
     if (e != cudaSuccess) return e;
     attr.set |= 1ull << dv;
   }
-  SlabArgs a{T, ldT, sT, r0, nbk, X, ldX, sX, ncols, w};
+  const bool vec2 = ldT % 2 == 0 && sT % 2 == 0 && ldX % 2 == 0 && sX % 2 == 0 && r0 % 2 == 0 &&
+                    reinterpret_cast<uintptr_t>(T) % 16 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0;
+  SlabArgs a{T, ldT, sT, r0, nbk, X, ldX, sX, ncols, w, vec2};
   const long long strips = (ncols + kSlabCW - 1) / kSlabCW;
   if (strips > 65535) return cudaErrorInvalidConfiguration;
-  slab_trsm_kernel<UPPER><<<dim3(batch, (unsigned)strips), 128, smem, st>>>(a);
+  slab_trsm_kernel<UPPER><<<dim3(batch, (unsigned)strips), kSlabThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
