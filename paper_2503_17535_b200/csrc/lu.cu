@@ -850,27 +850,30 @@ __global__ void __launch_bounds__(kSlabThreads, kSlabWarps >= 16 ? 2 : 1) slab_t
       double bneg[kLuNB / 4];
 #pragma unroll
       for (int kb = 0; kb < kLuNB; kb += 4) bneg[kb / 4] = -xs[(wc + g) * kSlabLdX + s0 + kb + t4];
-      // two independent 8-row tiles per iteration (two DMMA accumulation chains in flight); the second tile
-      // of an odd count is computed on padding rows and not stored
+#ifndef HPS_SLAB_CHAINS
+#define HPS_SLAB_CHAINS 4
+#endif
+      // kCh independent 8-row tiles per iteration (kCh DMMA accumulation chains in flight); tiles past the
+      // chunk's last are computed on padding rows and not stored
+      constexpr int kCh = HPS_SLAB_CHAINS;
       const int nmt = (qn + 7) / 8;
-      for (int mt = 2 * rh; mt < nmt; mt += 2 * kSlabRowSplit) {
+      for (int mt = kCh * rh; mt < nmt; mt += kCh * kSlabRowSplit) {
         const int r = q0 + mt * 8 + g;
-        double c[2], d[2];
+        double c[kCh][2];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          c[h] = xs[(wc + 2 * t4 + h) * kSlabLdX + r];
-          d[h] = xs[(wc + 2 * t4 + h) * kSlabLdX + r + 8];
-        }
+        for (int i = 0; i < kCh; ++i)
 #pragma unroll
-        for (int kb = 0; kb < kLuNB; kb += 4) {
-          dmma_8x8x4(c[0], c[1], A[(kb + t4) * kSlabLdA + mt * 8 + g], bneg[kb / 4]);
-          dmma_8x8x4(d[0], d[1], A[(kb + t4) * kSlabLdA + mt * 8 + 8 + g], bneg[kb / 4]);
-        }
+          for (int h = 0; h < 2; ++h) c[i][h] = xs[(wc + 2 * t4 + h) * kSlabLdX + r + 8 * i];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) xs[(wc + 2 * t4 + h) * kSlabLdX + r] = c[h];
-        if (mt + 1 < nmt)
+        for (int kb = 0; kb < kLuNB; kb += 4)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) xs[(wc + 2 * t4 + h) * kSlabLdX + r + 8] = d[h];
+          for (int i = 0; i < kCh; ++i)
+            dmma_8x8x4(c[i][0], c[i][1], A[(kb + t4) * kSlabLdA + (mt + i) * 8 + g], bneg[kb / 4]);
+#pragma unroll
+        for (int i = 0; i < kCh; ++i)
+          if (mt + i < nmt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) xs[(wc + 2 * t4 + h) * kSlabLdX + r + 8 * i] = c[i][h];
       }
     }
     step = ns;
