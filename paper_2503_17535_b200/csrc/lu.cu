@@ -673,7 +673,10 @@ cudaError_t gemm_sub(int batch, int rows, int cols, int k, double alpha, const d
 // slab's 32x32 diagonal blocks are formed first (one warp per block), then every CTA keeps a
 // 32-column strip of X in shared memory and runs the blocked substitution with DMMA:
 // X_b = T_bb^-1 X_b, then X_i -= T_ib X_b for the remaining blocks i of the slab.
-constexpr int kSlabMinN = 64;  // measured: 64 beats 128 and 512 (d4-d6 merges) and 48 (d7)
+#ifndef HPS_SLAB_MIN_N
+#define HPS_SLAB_MIN_N 64
+#endif
+constexpr int kSlabMinN = HPS_SLAB_MIN_N;  // measured: 64 beats 128 and 512 (d4-d6 merges) and 48 (d7)
 int slab_min_n() { return kSlabMinN; }
 constexpr int kSlabCW = 32;                 // strip width (4 column groups x 8 columns)
 #ifndef HPS_SLAB_WARPS
