@@ -87,6 +87,7 @@ struct Level {
   // block-sparse Schur product: exterior section e only couples to the interfaces of its own
   // child (B_{e,i} = 0 otherwise), as contiguous interface runs {e, first interface, count}
   std::vector<std::array<int, 3>> schur_runs;
+  bool t_partial = false;  // depth 1 below an implicit root: the root-exterior rows of [h|T] not formed yet
   hpsg::ItiMergeTables it;  // ItI variant: block copies + real-equivalent scatter table
   DevBuf iblocks;
   int iti_nblocks = 0;

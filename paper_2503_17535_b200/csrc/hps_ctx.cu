@@ -956,6 +956,90 @@ void run_leaf_stage(hpsg_ctx* c) {
 #ifndef HPS_GATHER_OVERLAP
 #define HPS_GATHER_OVERLAP 1
 #endif
+
+// One block-sparse Schur product run (section e = r[0], interfaces r[1] .. r[1] + r[2]) for nodes
+// [node0, node0 + batch) of a level: [h|T]_e -= B_{e,I} [x_h|X]_I.
+GemmArgs schur_run_args(hpsg_ctx* c, const Level& L, const std::array<int, 3>& r, int node0, int batch) {
+  const int sz = L.mt.s;
+  GemmArgs g;
+  g.m = sz;
+  g.n = 1 + L.n_ext;
+  g.k = r[2] * sz;
+  g.batch = batch;
+  g.A = c->Bscratch.d() + (long long)node0 * L.n_ext * L.n_int + (long long)r[1] * sz * L.n_ext + (long long)r[0] * sz;
+  g.lda = L.n_ext;
+  g.sA = (long long)L.n_ext * L.n_int;
+  g.B = L.MD.d() + (long long)node0 * L.strideMD() + (long long)L.n_int * L.n_int + (long long)r[1] * sz;
+  g.ldb = L.n_int;
+  g.sB = L.strideMD();
+  g.D = L.AH.d() + (long long)node0 * L.strideAH() + (long long)r[0] * sz;
+  g.C = g.D;
+  g.ldc = L.n_ext;
+  g.sC = L.strideAH();
+  g.ldd = L.n_ext;
+  g.sD = L.strideAH();
+  g.alpha = -1.0;
+  g.beta = 1.0;
+  return g;
+}
+
+// The children of an implicit root (root_implicit_S, no root [h|T]): the root's merge reads only the rows of
+// their [h|T] on its interfaces (D, h_int and C; merge.cpp:226-278) -- the rows on the root's exterior would
+// form its A and B, which an implicit root never uses.  The build skips those Schur rows (half of the depth-1
+// product) and hpsg_get_node completes them on request (complete_partial_T), bitwise the same values.
+#ifndef HPS_SKIP_ROOT_EXT_ROWS
+#define HPS_SKIP_ROOT_EXT_ROWS 1
+#endif
+bool skips_root_ext_rows(const hpsg_ctx* c, int d) {
+  return HPS_SKIP_ROOT_EXT_ROWS && d == 1 && c->global_root(0) && !c->forms_T(0) && !c->iti &&
+         c->lv[1].mt.s >= kSparseSchurMinS;
+}
+// whether the root reads the rows of exterior section e of depth-1 node `node` (the root's child node % nchild)
+bool root_needs_rows(const hpsg_ctx* c, int node, int e) {
+  const hpsg::MergeTables& rt = c->lv[0].mt;
+  const int nquad = c->lv[1].mt.NE / c->lv[1].mt.nface;
+  const int ch = node % rt.nchild, f = e / nquad;
+  return rt.sec[ch * rt.nface + f] < 0;  // the face lies on one of the root's interfaces
+}
+
+void gather_B(hpsg_ctx* c, const Level& L, const double* child_HT, long long child_stride, cudaStream_t st);
+
+// Completes the depth-1 [h|T] rows the build left out (skips_root_ext_rows): B again (Bscratch is level
+// scratch), then the skipped runs.  Same GEMM per element as the build would have run.
+void complete_partial_T(hpsg_ctx* c, int d) {
+  Level& L = c->lv[d];
+  if (!L.t_partial) return;
+  const double* child_HT = (d == c->T.L - 1) ? c->leafHT.d() : c->lv[d + 1].AH.d();
+  const long long child_stride = (d == c->T.L - 1) ? c->strideLeafHT() : c->lv[d + 1].strideAH();
+  gather_B(c, L, child_HT, child_stride, c->st);
+  for (int node = 0; node < int(L.nodes); ++node)
+    for (const auto& r : L.schur_runs)
+      if (!root_needs_rows(c, node, r[0])) gemm(c, schur_run_args(c, L, r, node, 1));
+  L.t_partial = false;
+}
+// B = the children's T blocks coupling exterior rows to interface columns (Bscratch, level scratch)
+void gather_B(hpsg_ctx* c, const Level& L, const double* child_HT, long long child_stride, cudaStream_t st) {
+  hpsk::GatherArgs gb{};
+  gb.s = L.mt.s;
+  gb.nchild = L.mt.nchild;
+  gb.child_nb = L.child_nb;
+  gb.child_HT = child_HT;
+  gb.child_stride = child_stride;
+  gb.NI = L.mt.NI;
+  gb.NE = L.mt.NE;
+  gb.src = L.b_src.i();
+  gb.kind = 1;
+  gb.nrows = L.n_ext;
+  gb.ncols = L.n_int;
+  gb.dst = c->Bscratch.d();
+  gb.ld = L.n_ext;
+  gb.stride = (long long)L.n_ext * L.n_int;
+  gb.skip_zero = L.mt.s >= kSparseSchurMinS;   // the block-sparse Schur product reads only B's nonzero blocks
+  hpsk::launch_gather(gb, int(L.nodes), st);
+  ck(cudaGetLastError(), "B gather");
+  ++c->launches;
+}
+
 void run_merge_level(hpsg_ctx* c, int d) {
   Level& L = c->lv[d];
   const bool root = !c->forms_T(d);
@@ -1011,17 +1095,8 @@ void run_merge_level(hpsg_ctx* c, int d) {
       ck(cudaStreamWaitEvent(c->gst, c->gev[0], 0), "gather fork wait");
       gs = c->gst;
     }
+    gather_B(c, L, child_HT, child_stride, gs);
     hpsk::GatherArgs gb = ga;
-    gb.src = L.b_src.i();
-    gb.kind = 1;
-    gb.nrows = L.n_ext;
-    gb.ncols = L.n_int;
-    gb.dst = c->Bscratch.d();
-    gb.ld = L.n_ext;
-    gb.stride = (long long)L.n_ext * L.n_int;
-    gb.skip_zero = L.mt.s >= kSparseSchurMinS;   // the block-sparse Schur product reads only B's nonzero blocks
-    hpsk::launch_gather(gb, int(L.nodes), gs);
-    gb.skip_zero = false;
     gb.src = L.ah_src.i();
     gb.kind = 2;
     gb.nrows = L.n_ext;
@@ -1030,7 +1105,7 @@ void run_merge_level(hpsg_ctx* c, int d) {
     gb.ld = L.n_ext;
     gb.stride = L.strideAH();
     hpsk::launch_gather(gb, int(L.nodes), gs);
-    c->launches += 2;
+    ++c->launches;
     if (HPS_GATHER_OVERLAP) ck(cudaEventRecord(c->gev[1], c->gst), "gather join");
   }
   // [D | h_int | C]
@@ -1100,29 +1175,16 @@ void run_merge_level(hpsg_ctx* c, int d) {
   if (!root && !c->iti && L.mt.s >= kSparseSchurMinS) {
     // [h | T] = [h_ext | A] - B [x_h | X] over the nonzero blocks of B only: section e's rows get
     // -B_{e,I} [x_h|X]_I for the runs I of interfaces of e's child (the other blocks of B are
-    // structurally zero, merge.cpp:226-278), i.e. half the dense product in 2D, a quarter in 3D
-    const int sz = L.mt.s;
-    for (const auto& r : L.schur_runs) {
-      GemmArgs g;
-      g.m = sz;
-      g.n = 1 + L.n_ext;
-      g.k = r[2] * sz;
-      g.batch = int(L.nodes);
-      g.A = c->Bscratch.d() + (long long)r[1] * sz * L.n_ext + (long long)r[0] * sz;
-      g.lda = L.n_ext;
-      g.sA = (long long)L.n_ext * L.n_int;
-      g.B = L.MD.d() + (long long)L.n_int * L.n_int + (long long)r[1] * sz;
-      g.ldb = L.n_int;
-      g.sB = L.strideMD();
-      g.C = L.AH.d() + (long long)r[0] * sz;
-      g.ldc = L.n_ext;
-      g.sC = L.strideAH();
-      g.D = L.AH.d() + (long long)r[0] * sz;
-      g.ldd = L.n_ext;
-      g.sD = L.strideAH();
-      g.alpha = -1.0;
-      g.beta = 1.0;
-      gemm(c, g);
+    // structurally zero, merge.cpp:226-278), i.e. half the dense product in 2D, a quarter in 3D.
+    // Below an implicit root, the rows of the root's exterior faces are left for later (skips_root_ext_rows)
+    if (skips_root_ext_rows(c, d)) {
+      for (int node = 0; node < int(L.nodes); ++node)
+        for (const auto& r : L.schur_runs)
+          if (root_needs_rows(c, node, r[0])) gemm(c, schur_run_args(c, L, r, node, 1));
+      L.t_partial = true;
+    } else {
+      for (const auto& r : L.schur_runs) gemm(c, schur_run_args(c, L, r, 0, int(L.nodes)));
+      L.t_partial = false;
     }
   } else if (!root) {
     // [h | T] = [h_ext | A] - B [x_h | X]   (merge.cpp:294-295 with gtilde = -x_h); ItI: the real-unit columns,
@@ -2130,6 +2192,10 @@ int hpsg_get_node(hpsg_ctx* c, int id, double* S, double* gtilde, double* Tm, do
       for (size_t i = 0; i < size_t(L.n_int) * L.n_ext; ++i) S[i] = -xs[L.n_int + i];
     }
     if ((Tm || h) && !c->global_root(L.d)) {
+      if (L.t_partial) {
+        complete_partial_T(c, L.d);
+        ck(cudaStreamSynchronize(c->st), "node sync");
+      }
       std::vector<double> ht(size_t(L.n_ext) * (1 + L.n_ext));
       ck(cudaMemcpy(ht.data(), L.AH.d() + idx * L.strideAH(), ht.size() * 8, cudaMemcpyDeviceToHost), "node D2H");
       if (Tm) std::memcpy(Tm, ht.data() + L.n_ext, size_t(L.n_ext) * L.n_ext * 8);

@@ -495,3 +495,25 @@ def test_cpp_adaptive_wavefront_example():
     rep = json.loads(r.stdout)
     assert rep["n_leaves"] == 456 and rep["top_D"] == 8208   # the reference's tree for this criterion
     assert rep["rel_linf"] < 1e-3
+
+
+@pytest.mark.parametrize("implicit", [False, True])
+def test_depth1_rows_completed_on_request(implicit):
+    """Below an implicit root the build leaves the root-exterior rows of the depth-1 [h | T] unformed (the root
+    never reads them); hpsg_get_node completes them on request.  The completed T and h match the oracle, and
+    neither the completion nor a rebuild changes the solution (bitwise)."""
+    prob = PR.helmholtz_bumps()
+    s = gpu_solver(prob, 16, 4, root_implicit=implicit)
+    o = oracle_solver(prob, 16, 4)
+    o.build()
+    g = prob.boundary(s.root_boundary_points())
+    u0 = s.solve(g)
+    for nid in (1, 2, 3, 4):
+        got, ref = s.get_node(nid), o.get_node(nid)
+        for a, b in zip(got[2:], ref[2:]):
+            assert np.abs(a - b).max() / np.abs(b).max() < 1e-10
+    assert np.array_equal(s.solve(g), u0)
+    s.build()
+    assert np.array_equal(s.solve(g), u0)
+    again = s.get_node(3)
+    assert np.array_equal(again[2], s.get_node(3)[2])
