@@ -87,7 +87,12 @@ struct Level {
   // block-sparse Schur product: exterior section e only couples to the interfaces of its own
   // child (B_{e,i} = 0 otherwise), as contiguous interface runs {e, first interface, count}
   std::vector<std::array<int, 3>> schur_runs;
-  bool t_partial = false;  // depth 1 below an implicit root: the root-exterior rows of [h|T] not formed yet
+  // Schur rows of sections on the domain boundary (skips_boundary_rows): per run, the nodes whose rows are
+  // formed in the build (run_off/run_cnt into run_map) and the rest (rest_off/rest_cnt), formed on request;
+  // ah_mask[node][section] = 1 on the boundary.  t_partial: those rows not formed yet
+  DevBuf run_map, ah_mask;
+  std::vector<int> run_off, run_cnt, rest_off, rest_cnt;
+  bool t_partial = false;
   hpsg::ItiMergeTables it;  // ItI variant: block copies + real-equivalent scatter table
   DevBuf iblocks;
   int iti_nblocks = 0;

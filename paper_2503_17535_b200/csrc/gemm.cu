@@ -81,8 +81,9 @@ bool run_tma(const GemmArgs& a, cudaStream_t st, cudaError_t* err) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, ST, true>;
   if (a.k <= 0) return false;
   CUtensorMap mA, mB;
-  if (!make_map(&mA, a.A, a.m, a.k, a.lda, a.sA, a.batch, BM + 4, BK)) return false;
-  if (!make_map(&mB, a.B, a.k, a.n, a.ldb, a.sB, a.batch, BK + 4, BN)) return false;
+  const int extent = a.bmap ? a.bmap_extent : a.batch;  // the maps span every batch index the launch may touch
+  if (!make_map(&mA, a.A, a.m, a.k, a.lda, a.sA, extent, BM + 4, BK)) return false;
+  if (!make_map(&mB, a.B, a.k, a.n, a.ldb, a.sB, extent, BK + 4, BN)) return false;
   auto kern = dgemm_tma_kernel<BM, BN, BK, WM, WN, ST>;
   static PerDeviceFlag attr;  // per instantiation and device
   const int dv = current_device();

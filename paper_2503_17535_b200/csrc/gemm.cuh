@@ -30,6 +30,9 @@ struct GemmArgs {
   double alpha = 1.0, beta = 0.0;
   int seed_k_max = 0;  // set by launch_dgemm: accumulators seeded with C when k <= this
   const int* drow = nullptr;  // optional output row map: row r of the product goes to D row drow[r] (beta = 0)
+  // optional batch map: launch batch i works on batch index bmap[i] (< bmap_extent) of A, B, C and D
+  const int* bmap = nullptr;
+  int bmap_extent = 0;
 };
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool VEC>
@@ -99,7 +102,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, STAGES, VEC>::kThr
   if (tile >= (long long)tiles_m * ((p.n + BN - 1) / BN)) return;
   const int tm = int(tile % tiles_m), tn = int(tile / tiles_m);
   const int m0 = tm * BM, n0 = tn * BN;
-  const long long b = blockIdx.x;  // batch in x (gridDim.y/z are capped at 65535)
+  const long long b = p.bmap ? __ldg(p.bmap + blockIdx.x) : blockIdx.x;  // batch in x (gridDim.y/z <= 65535)
   const double* A = p.A + b * p.sA;
   const double* B = p.B + b * p.sB;
 

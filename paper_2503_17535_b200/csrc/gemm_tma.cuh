@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, STAGES, true>::kTh
   if (tile >= (long long)tiles_m * ((p.n + BN - 1) / BN)) return;
   const int tm = int(tile % tiles_m), tn = int(tile / tiles_m);
   const int m0 = tm * BM, n0 = tn * BN;
-  const int b = blockIdx.x;
+  const int b = p.bmap ? __ldg(p.bmap + blockIdx.x) : blockIdx.x;
   const int bA = p.sA ? b : 0, bB = p.sB ? b : 0;  // stride-0 operands broadcast over the batch
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

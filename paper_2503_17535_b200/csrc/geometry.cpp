@@ -359,6 +359,20 @@ int ext_qpos(int dim, int c, int f) {
   return off[ua] * 2 + off[va];
 }
 
+bool face_on_domain_boundary(int dim, int d, long long idx, int f) {
+  const int nchild = dim == 2 ? 4 : 8;
+  const int axis = dim == 2 ? ((f == 1 || f == 3) ? 0 : 1) : f / 2;
+  const int high = dim == 2 ? ((f == 1 || f == 2) ? 1 : 0) : f % 2;
+  long long pos = 0;  // the node's grid position along `axis` at depth d (child digits, most significant first)
+  for (int k = 0; k < d; ++k) {
+    long long div = 1;
+    for (int j = k + 1; j < d; ++j) div *= nchild;
+    const int c = int((idx / div) % nchild);
+    pos = 2 * pos + kChildOffset[c][axis];
+  }
+  return high ? pos == (1LL << d) - 1 : pos == 0;
+}
+
 MergeTables make_merge_tables(int dim, int s) {
   MergeTables m;
   m.dim = dim;

@@ -95,6 +95,8 @@ struct Iface {
 const std::vector<Iface>& ifaces(int dim);
 // exterior position (quadrant / half of the parent face) of child c's face f, or -1 (merge.cpp:41-56)
 int ext_qpos(int dim, int c, int f);
+// whether face f of node idx (DFS order) at depth d of a uniform tree lies on the domain boundary
+bool face_on_domain_boundary(int dim, int d, long long idx, int f);
 
 // Merge of one level (all nodes at depth d of a uniform tree share it).
 // Child boundary layout: faces in reference order, s points per face section.

@@ -64,6 +64,7 @@ int lu_launches(int n, int m, bool factor) { return hpsk::lu_launch_count(n, m, 
 
 // block-sparse Schur products from this face size up (below it one dense GEMM launch is cheaper)
 constexpr int kSparseSchurMinS = 32;
+void plan_boundary_rows(hpsg_ctx* c, Level& L, cudaStream_t st);
 
 // Solve-time products: a streaming GEMV for up to 4 right-hand sides (HBM-bound), the DMMA
 // GEMM beyond that (multi-RHS solves become compute-bound, config 3).
@@ -321,6 +322,7 @@ void setup(hpsg_ctx* c) {
     upload(L.b_src, L.mt.b_src, &c->dev_bytes, st);
     upload(L.ah_src, L.mt.ah_src, &c->dev_bytes, st);
     upload(L.down, L.mt.down, &c->dev_bytes, st);
+    plan_boundary_rows(c, L, st);
   }
   c->stats.n_leaves = c->T.cut ? 0 : nl;
   c->stats.n_points = c->T.cut ? 0 : (long long)nl * o.n;
@@ -983,40 +985,79 @@ GemmArgs schur_run_args(hpsg_ctx* c, const Level& L, const std::array<int, 3>& r
   return g;
 }
 
-// The children of an implicit root (root_implicit_S, no root [h|T]): the root's merge reads only the rows of
-// their [h|T] on its interfaces (D, h_int and C; merge.cpp:226-278) -- the rows on the root's exterior would
-// form its A and B, which an implicit root never uses.  The build skips those Schur rows (half of the depth-1
-// product) and hpsg_get_node completes them on request (complete_partial_T), bitwise the same values.
-#ifndef HPS_SKIP_ROOT_EXT_ROWS
-#define HPS_SKIP_ROOT_EXT_ROWS 1
+// Rows of [h|T] on the domain boundary.  Below a root that forms no [h|T] (DtN; root_implicit_S or not), a
+// node's rows for faces on the domain boundary feed only its parent's A and B rows for the same boundary faces
+// (merge.cpp:226-278: D, C and h_int take the rows of interface faces), and the root never forms A or B -- so
+// neither the build (the parent's D, C, h_int, hence every S and gtilde) nor the solve reads them.  The build
+// skips those Schur rows (half of the depth-1 product in 2D, a quarter at depth 2, ...); hpsg_get_node forms
+// them on request (complete_partial_T), the same GEMM per element as the build would have run.
+#ifndef HPS_SKIP_BOUNDARY_ROWS
+#define HPS_SKIP_BOUNDARY_ROWS 1
 #endif
-bool skips_root_ext_rows(const hpsg_ctx* c, int d) {
-  return HPS_SKIP_ROOT_EXT_ROWS && d == 1 && c->global_root(0) && !c->forms_T(0) && !c->iti &&
-         c->lv[1].mt.s >= kSparseSchurMinS;
+bool skips_boundary_rows(const hpsg_ctx* c, const Level& L) {
+  return HPS_SKIP_BOUNDARY_ROWS && L.d >= 1 && c->T.root_depth == 0 && !c->T.cut && !c->forms_T(0) && !c->iti &&
+         L.mt.s >= kSparseSchurMinS;
 }
-// whether the root reads the rows of exterior section e of depth-1 node `node` (the root's child node % nchild)
-bool root_needs_rows(const hpsg_ctx* c, int node, int e) {
-  const hpsg::MergeTables& rt = c->lv[0].mt;
-  const int nquad = c->lv[1].mt.NE / c->lv[1].mt.nface;
-  const int ch = node % rt.nchild, f = e / nquad;
-  return rt.sec[ch * rt.nface + f] < 0;  // the face lies on one of the root's interfaces
+
+// per-run node lists and the boundary-section mask of one level (plan time)
+void plan_boundary_rows(hpsg_ctx* c, Level& L, cudaStream_t st) {
+  L.run_off.clear(), L.run_cnt.clear(), L.rest_off.clear(), L.rest_cnt.clear();
+  L.t_partial = false;
+  if (!skips_boundary_rows(c, L)) return;
+  const int dim = c->T.dim, NE = L.mt.NE, nquad = NE / L.mt.nface;
+  std::vector<int> map, mask(size_t(L.nodes) * NE);
+  for (long long i = 0; i < L.nodes; ++i)
+    for (int e = 0; e < NE; ++e) mask[size_t(i) * NE + e] = hpsg::face_on_domain_boundary(dim, L.d, i, e / nquad);
+  for (const auto& r : L.schur_runs) {
+    std::vector<int> need, rest;
+    for (long long i = 0; i < L.nodes; ++i) (mask[size_t(i) * NE + r[0]] ? rest : need).push_back(int(i));
+    L.run_off.push_back(int(map.size())), L.run_cnt.push_back(int(need.size()));
+    map.insert(map.end(), need.begin(), need.end());
+    L.rest_off.push_back(int(map.size())), L.rest_cnt.push_back(int(rest.size()));
+    map.insert(map.end(), rest.begin(), rest.end());
+  }
+  upload(L.run_map, map, &c->dev_bytes, st);
+  upload(L.ah_mask, mask, &c->dev_bytes, st);
+}
+
+// the Schur runs of one level over a node list (all nodes when cnt == nodes)
+void schur_runs_over(hpsg_ctx* c, Level& L, bool rest) {
+  for (size_t i = 0; i < L.schur_runs.size(); ++i) {
+    if (L.run_cnt.empty()) {
+      if (!rest) gemm(c, schur_run_args(c, L, L.schur_runs[i], 0, int(L.nodes)));
+      continue;
+    }
+    const int cnt = rest ? L.rest_cnt[i] : L.run_cnt[i], off = rest ? L.rest_off[i] : L.run_off[i];
+    if (cnt == 0) continue;
+    GemmArgs g = schur_run_args(c, L, L.schur_runs[i], 0, cnt);
+    if (cnt < int(L.nodes)) g.bmap = L.run_map.i() + off, g.bmap_extent = int(L.nodes);
+    gemm(c, g);
+  }
+  if (!rest) L.t_partial = false;
+  for (int n : L.rest_cnt)
+    if (n > 0 && !rest) L.t_partial = true;
 }
 
 void gather_B(hpsg_ctx* c, const Level& L, const double* child_HT, long long child_stride, cudaStream_t st);
+void gather_AH(hpsg_ctx* c, const Level& L, const double* child_HT, long long child_stride, cudaStream_t st,
+               const int* row_mask);
 
-// Completes the depth-1 [h|T] rows the build left out (skips_root_ext_rows): B again (Bscratch is level
-// scratch), then the skipped runs.  Same GEMM per element as the build would have run.
+// Forms the boundary rows the build skipped at depth d and below (deepest first: a level's A and B rows for
+// boundary sections come from its children's boundary rows): those rows of [h_ext | A] again, B again
+// (Bscratch is level scratch), then the skipped runs.
 void complete_partial_T(hpsg_ctx* c, int d) {
-  Level& L = c->lv[d];
-  if (!L.t_partial) return;
-  const double* child_HT = (d == c->T.L - 1) ? c->leafHT.d() : c->lv[d + 1].AH.d();
-  const long long child_stride = (d == c->T.L - 1) ? c->strideLeafHT() : c->lv[d + 1].strideAH();
-  gather_B(c, L, child_HT, child_stride, c->st);
-  for (int node = 0; node < int(L.nodes); ++node)
-    for (const auto& r : L.schur_runs)
-      if (!root_needs_rows(c, node, r[0])) gemm(c, schur_run_args(c, L, r, node, 1));
-  L.t_partial = false;
+  for (int dd = int(c->lv.size()) - 1; dd >= d; --dd) {
+    Level& L = c->lv[dd];
+    if (!L.t_partial) continue;
+    const double* child_HT = (dd == c->T.L - 1) ? c->leafHT.d() : c->lv[dd + 1].AH.d();
+    const long long child_stride = (dd == c->T.L - 1) ? c->strideLeafHT() : c->lv[dd + 1].strideAH();
+    gather_AH(c, L, child_HT, child_stride, c->st, L.ah_mask.i());
+    gather_B(c, L, child_HT, child_stride, c->st);
+    schur_runs_over(c, L, true);
+    L.t_partial = false;
+  }
 }
+
 // B = the children's T blocks coupling exterior rows to interface columns (Bscratch, level scratch)
 void gather_B(hpsg_ctx* c, const Level& L, const double* child_HT, long long child_stride, cudaStream_t st) {
   hpsk::GatherArgs gb{};
@@ -1037,6 +1078,30 @@ void gather_B(hpsg_ctx* c, const Level& L, const double* child_HT, long long chi
   gb.skip_zero = L.mt.s >= kSparseSchurMinS;   // the block-sparse Schur product reads only B's nonzero blocks
   hpsk::launch_gather(gb, int(L.nodes), st);
   ck(cudaGetLastError(), "B gather");
+  ++c->launches;
+}
+
+// [h_ext | A] of the level's nodes into AH (row_mask: only the rows of the marked sections)
+void gather_AH(hpsg_ctx* c, const Level& L, const double* child_HT, long long child_stride, cudaStream_t st,
+               const int* row_mask) {
+  hpsk::GatherArgs ga{};
+  ga.s = L.mt.s;
+  ga.nchild = L.mt.nchild;
+  ga.child_nb = L.child_nb;
+  ga.child_HT = child_HT;
+  ga.child_stride = child_stride;
+  ga.NI = L.mt.NI;
+  ga.NE = L.mt.NE;
+  ga.src = L.ah_src.i();
+  ga.kind = 2;
+  ga.nrows = L.n_ext;
+  ga.ncols = 1 + L.n_ext;
+  ga.dst = L.AH.d();
+  ga.ld = L.n_ext;
+  ga.stride = L.strideAH();
+  ga.row_mask = row_mask;
+  hpsk::launch_gather(ga, int(L.nodes), st);
+  ck(cudaGetLastError(), "AH gather");
   ++c->launches;
 }
 
@@ -1096,16 +1161,7 @@ void run_merge_level(hpsg_ctx* c, int d) {
       gs = c->gst;
     }
     gather_B(c, L, child_HT, child_stride, gs);
-    hpsk::GatherArgs gb = ga;
-    gb.src = L.ah_src.i();
-    gb.kind = 2;
-    gb.nrows = L.n_ext;
-    gb.ncols = 1 + L.n_ext;
-    gb.dst = L.AH.d();
-    gb.ld = L.n_ext;
-    gb.stride = L.strideAH();
-    hpsk::launch_gather(gb, int(L.nodes), gs);
-    ++c->launches;
+    gather_AH(c, L, child_HT, child_stride, gs, nullptr);
     if (HPS_GATHER_OVERLAP) ck(cudaEventRecord(c->gev[1], c->gst), "gather join");
   }
   // [D | h_int | C]
@@ -1176,16 +1232,8 @@ void run_merge_level(hpsg_ctx* c, int d) {
     // [h | T] = [h_ext | A] - B [x_h | X] over the nonzero blocks of B only: section e's rows get
     // -B_{e,I} [x_h|X]_I for the runs I of interfaces of e's child (the other blocks of B are
     // structurally zero, merge.cpp:226-278), i.e. half the dense product in 2D, a quarter in 3D.
-    // Below an implicit root, the rows of the root's exterior faces are left for later (skips_root_ext_rows)
-    if (skips_root_ext_rows(c, d)) {
-      for (int node = 0; node < int(L.nodes); ++node)
-        for (const auto& r : L.schur_runs)
-          if (root_needs_rows(c, node, r[0])) gemm(c, schur_run_args(c, L, r, node, 1));
-      L.t_partial = true;
-    } else {
-      for (const auto& r : L.schur_runs) gemm(c, schur_run_args(c, L, r, 0, int(L.nodes)));
-      L.t_partial = false;
-    }
+    // Rows on the domain boundary are left for later (skips_boundary_rows)
+    schur_runs_over(c, L, false);
   } else if (!root) {
     // [h | T] = [h_ext | A] - B [x_h | X]   (merge.cpp:294-295 with gtilde = -x_h); ItI: the real-unit columns,
     // the imaginary-unit columns of T are filled in from them

@@ -337,8 +337,12 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(const GatherArgs
         }
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (r0 + 32 * q < a.nrows && (nz[q] || !a.skip_zero)) dcol[r0 + 32 * q] = v[q];
+      for (int q = 0; q < 4; ++q) {
+        const int r = r0 + 32 * q;
+        if (r < a.nrows && (nz[q] || !a.skip_zero) &&
+            (!a.row_mask || a.row_mask[node * nsec + (a.smagic ? (int)__umulhi((unsigned)r, a.smagic) : r / s)]))
+          dcol[r] = v[q];
+      }
     }
   }
 }

@@ -208,6 +208,7 @@ struct GatherArgs {
   // rows with no source (structurally zero blocks) are not stored: set when the consumer reads only the
   // nonzero blocks (the block-sparse Schur product's B)
   bool skip_zero = false;
+  const int* row_mask = nullptr;  // optional [node][row section]: rows of sections with 0 are not stored
   unsigned smagic = 0;      // set by launch_gather
 };
 void launch_gather(const GatherArgs& a, int n_nodes, cudaStream_t st);
