@@ -250,7 +250,7 @@ def run_b200(args):
         "roofline_build": {"bound": "tensor", "kernel": "whole build (leaf kernel + batched DMMA LU/TRSM/GEMM merges)",
                            "achieved": flops / (t_build / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                            "frac": flops / (t_build / 1e3) / 1e12 / FP64_PEAK_TFLOPS, "algorithmic_flops": flops,
-                           "note": "SURVEY 8d dense-equivalent counts; the block-sparse Schur products skip zero blocks"},
+                           "note": "SURVEY 8d dense-equivalent counts (a rate equivalent to the reference algorithm, not executed FLOPs): the block-sparse Schur products skip zero blocks and the rows of [h|T] on the domain boundary, which nothing reads (executed GEMM FLOPs: roofline_gemm)"},
         # the leaf kernel above is the one the round-1 review named; by launch-time share the dominant kernel is now
         # the DMMA GEMM (all launches together ~49 % of the step, profiles/r02_launch_summary_v3.txt), whose live
         # roofline is roofline_gemm (the largest launch keeps the DMMA pipe 91 % active, profiles/r02_gemm_d1_*)
