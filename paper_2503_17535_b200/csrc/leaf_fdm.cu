@@ -44,18 +44,26 @@ constexpr int kMaxSteps = 12;
 #endif
 constexpr double kTol = HPS_FDM_TOL;  // predicted remaining error / max|X| at which a right-hand side stops
 
+#ifndef HPS_FDM_LPB
+#define HPS_FDM_LPB 4
+#endif
+// leaves per CTA iteration: their columns are dealt to the warps as one sequence, so the end-of-iteration barrier
+// waits for ceil(kLPB ncol / kW) columns per warp instead of kLPB ceil(ncol / kW) (L=8 leaf stage 17.3 -> 17.0 ms)
+constexpr int kLPB = HPS_FDM_LPB;
+
 struct FdmSmem {
   double R[kNC * kBlk], X[kNC * kBlk], W[kNC * kBlk];
-  double cz[kBlk];   // zeroth-order coefficient at the interior points (block layout), 0 in the padding
-  double den[kBlk];  // 1 / (lam_row + lam_col + cbar), 0 in the padding
-  double fsrc[2][256];  // source samples: real part (and the imaginary part in the ItI mode)
+  double cz[kLPB][kBlk];   // zeroth-order coefficient at the interior points (block layout), 0 in the padding
+  double den[kLPB][kBlk];  // 1 / (lam_row + lam_col + cbar), 0 in the padding
+  double fsrc[kLPB][2][256];  // source samples: real part (and the imaginary part in the ItI mode)
   int pos[256];      // tensor index -> interior r (>= 0) or -(exterior position) - 1
   double qDm[kBlk];  // separable Q_i as DMMA A operands (16 x 16 col-major, zero padded): rows s = d_s
   double qGm[kBlk];  // (side normal derivatives on the interior nodes) and G (Chebyshev -> Gauss, q x (p-2))
-  double wmin[kW], wmax[kW];
-  int bad;
-  int failed;        // this leaf did not converge
-  int ndmma;         // DMMA.8x8x4 instructions issued for this leaf (executed-FLOP accounting)
+  double wmin[kLPB][kW], wmax[kLPB][kW];
+  int bad[kLPB];
+  int failed[kLPB];  // the leaf did not converge
+  int ndmma[kLPB];   // DMMA.8x8x4 instructions issued for the leaf (executed-FLOP accounting)
+  int ok[kLPB];      // the leaf takes the fast-diagonalisation path
 };
 
 // element (row, col) of a block: column-major 16 x 16, rows XOR-swizzled by the column with the bit-reversed
@@ -136,19 +144,20 @@ HPS_DEV double warp_max_hi(unsigned hi) {
 // Solve one right-hand side block: X <- L_ii^-1 R.  Returns false if it did not converge.
 // hat: Xb already holds R^ = V^-1 R V^-T (the leaf-independent columns -L_ie P, precomputed once by
 // leaf_fdm_prep_kernel); otherwise R^ is formed here from Rb (the source column).
-HPS_DEV bool solve_block(const double* Rb, double* Xb, double* Wb, const FdmSmem& s, const double (&vi)[2][4],
-                         const double (&vv)[2][4], const double (&aa)[2][4], int g, int t4, int& npass, bool hat) {
+HPS_DEV bool solve_block(const double* Rb, double* Xb, double* Wb, const double* cz, const double* den,
+                         const double (&vi)[2][4], const double (&vv)[2][4], const double (&aa)[2][4], int g, int t4,
+                         int& npass, bool hat) {
   double acc[2][2][2];
   // X_0 = K_c^-1 R = V (den o R^) V^T
   if (hat) {
     npass += 2;
-    mma_block<false, true>(vv, Xb, acc, g, t4, s.den);
+    mma_block<false, true>(vv, Xb, acc, g, t4, den);
   } else {
     npass += 4;
     mma_block<false>(vi, Rb, acc, g, t4);
     store_t<false>(Wb, acc, nullptr, g, t4);
     mma_block<false>(vi, Wb, acc, g, t4);
-    store_t<true>(Wb, acc, s.den, g, t4);
+    store_t<true>(Wb, acc, den, g, t4);
     mma_block<false>(vv, Wb, acc, g, t4);
   }
   store_t<false>(Wb, acc, nullptr, g, t4);
@@ -185,7 +194,7 @@ HPS_DEV bool solve_block(const double* Rb, double* Xb, double* Wb, const FdmSmem
         const double2 r = *reinterpret_cast<const double2*>(Rb + p);
         const double2 w = *reinterpret_cast<const double2*>(Wb + p);
         const double2 x = *reinterpret_cast<const double2*>(Xb + p);
-        const double2 c = *reinterpret_cast<const double2*>(s.cz + p);
+        const double2 c = *reinterpret_cast<const double2*>(cz + p);
         double2 o;
         o.x = r.x - w.x - acc[mt][nt][0] - c.x * x.x;
         o.y = r.y - w.y - acc[mt][nt][1] - c.y * x.y;
@@ -196,7 +205,7 @@ HPS_DEV bool solve_block(const double* Rb, double* Xb, double* Wb, const FdmSmem
     mma_block<false>(vi, Wb, acc, g, t4);
     store_t<false>(Wb, acc, nullptr, g, t4);
     mma_block<false>(vi, Wb, acc, g, t4);
-    store_t<true>(Wb, acc, s.den, g, t4);
+    store_t<true>(Wb, acc, den, g, t4);
     mma_block<false>(vv, Wb, acc, g, t4);
     store_t<false>(Wb, acc, nullptr, g, t4);
     mma_block<false>(vv, Wb, acc, g, t4);
@@ -254,83 +263,104 @@ __global__ void __launch_bounds__(kT, HPS_FDM_MINB) leaf_fdm_kernel(const LeafFd
   }
   __syncthreads();
 
-  for (long long leaf = blockIdx.x; leaf < f.n_leaves; leaf += gridDim.x) {
+  // several leaves per iteration only when every CTA still gets many iterations (small trees: one leaf each)
+  const int lpb = f.n_leaves >= (long long)gridDim.x * kLPB * 8 ? kLPB : 1;
+  for (long long leaf0 = (long long)blockIdx.x * lpb; leaf0 < f.n_leaves; leaf0 += (long long)gridDim.x * lpb) {
+    const int nl = (int)min((long long)lpb, f.n_leaves - leaf0);
     // ---- coefficients and source at the leaf points (leaf_cheb_points, discretize_operator's sampling)
-    if (tid == 0) s.bad = INT_MAX, s.ndmma = 0;
-    for (int e = tid; e < kBlk; e += kT) s.cz[e] = 0.0;
+    if (tid < kLPB) s.bad[tid] = INT_MAX, s.ndmma[tid] = 0, s.failed[tid] = 0;
+    for (int e = tid; e < kLPB * kBlk; e += kT) s.cz[e / kBlk][e % kBlk] = 0.0;
     __syncthreads();
-    const double* box = a.leaf_box + leaf * 6;
-    double cmin = DBL_MAX, cmax = -DBL_MAX;
-    for (int i = tid; i < NPT; i += kT) {
-      const int i1 = i / P, i2 = i % P;
-      double x[3] = {0.0, 0.0, 0.0};
-      x[0] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(box[0], box[3])), __dmul_rn(__dmul_rn(0.5, __dsub_rn(box[3], box[0])), a.cheb[i1]));
-      x[1] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(box[1], box[4])), __dmul_rn(__dmul_rn(0.5, __dsub_rn(box[4], box[1])), a.cheb[i2]));
-      double cz = 0.0;
-      for (int t = 0; t < a.nterms; ++t) {
-        const double v = eval_field_t<2>(a.terms[t].f, x, leaf, i, NPT);
-        if (!isfinite(v)) atomicMin(&s.bad, i);
-        if (a.terms[t].role == 2) cz = __dadd_rn(cz, v);
+#pragma unroll
+    for (int lf = 0; lf < kLPB; ++lf) {
+      if (lf >= nl) break;
+      const long long leaf = leaf0 + lf;
+      const double* box = a.leaf_box + leaf * 6;
+      double cmin = DBL_MAX, cmax = -DBL_MAX;
+      for (int i = tid; i < NPT; i += kT) {
+        const int i1 = i / P, i2 = i % P;
+        double x[3] = {0.0, 0.0, 0.0};
+        x[0] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(box[0], box[3])), __dmul_rn(__dmul_rn(0.5, __dsub_rn(box[3], box[0])), a.cheb[i1]));
+        x[1] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(box[1], box[4])), __dmul_rn(__dmul_rn(0.5, __dsub_rn(box[4], box[1])), a.cheb[i2]));
+        double cz = 0.0;
+        for (int t = 0; t < a.nterms; ++t) {
+          const double v = eval_field_t<2>(a.terms[t].f, x, leaf, i, NPT);
+          if (!isfinite(v)) atomicMin(&s.bad[lf], i);
+          if (a.terms[t].role == 2) cz = __dadd_rn(cz, v);
+        }
+        s.fsrc[lf][0][i] = (a.has_source && !srcmode) ? eval_field_t<2>(a.source, x, leaf, i, NPT) : 0.0;
+        if (f.iti) s.fsrc[lf][1][i] = f.has_source_im ? eval_field_t<2>(f.source_im, x, leaf, i, NPT) : 0.0;
+        const int r = s.pos[i];
+        if (r >= 0) {
+          s.cz[lf][swz(r % N1, r / N1)] = cz;
+          cmin = fmin(cmin, cz);
+          cmax = fmax(cmax, cz);
+        }
       }
-      s.fsrc[0][i] = (a.has_source && !srcmode) ? eval_field_t<2>(a.source, x, leaf, i, NPT) : 0.0;
-      if (f.iti) s.fsrc[1][i] = f.has_source_im ? eval_field_t<2>(f.source_im, x, leaf, i, NPT) : 0.0;
-      const int r = s.pos[i];
-      if (r >= 0) {
-        s.cz[swz(r % N1, r / N1)] = cz;
-        cmin = fmin(cmin, cz);
-        cmax = fmax(cmax, cz);
-      }
+      cmin = -warp_max(-cmin);
+      cmax = warp_max(cmax);
+      if (lane == 0) s.wmin[lf][warp] = cmin, s.wmax[lf][warp] = cmax;
     }
-    cmin = -warp_max(-cmin);
-    cmax = warp_max(cmax);
-    if (lane == 0) s.wmin[warp] = cmin, s.wmax[warp] = cmax;
     __syncthreads();
-    cmin = s.wmin[0], cmax = s.wmax[0];
-    for (int w = 1; w < kW; ++w) cmin = fmin(cmin, s.wmin[w]), cmax = fmax(cmax, s.wmax[w]);
-    const double cbar = 0.5 * (cmin + cmax);
-    double dmin = DBL_MAX, dmax = 0.0;
-    for (int e = tid; e < kBlk; e += kT) {
-      const int col = e >> 4, row = (e & 15) ^ swx(col);
-      double d = 0.0;
-      if (row < N1 && col < N1) {
-        const double ev = f.lam[row] + f.lam[col] + cbar;
-        d = 1.0 / ev;
-        dmin = fmin(dmin, fabs(ev));
-        dmax = fmax(dmax, fabs(ev));
+    double dmin[kLPB], dmax[kLPB];
+#pragma unroll
+    for (int lf = 0; lf < kLPB; ++lf) {
+      dmin[lf] = DBL_MAX, dmax[lf] = 0.0;
+      if (lf >= nl) continue;
+      double cmin = s.wmin[lf][0], cmax = s.wmax[lf][0];
+      for (int w = 1; w < kW; ++w) cmin = fmin(cmin, s.wmin[lf][w]), cmax = fmax(cmax, s.wmax[lf][w]);
+      const double cbar = 0.5 * (cmin + cmax);
+      if (!isfinite(cbar)) dmin[lf] = -1.0;  // not ok
+      for (int e = tid; e < kBlk; e += kT) {
+        const int col = e >> 4, row = (e & 15) ^ swx(col);
+        double d = 0.0;
+        if (row < N1 && col < N1) {
+          const double ev = f.lam[row] + f.lam[col] + cbar;
+          d = 1.0 / ev;
+          dmin[lf] = fmin(dmin[lf], fabs(ev));
+          dmax[lf] = fmax(dmax[lf], fabs(ev));
+        }
+        s.den[lf][e] = d;
       }
-      s.den[e] = d;
+      dmin[lf] = -warp_max(-dmin[lf]);
+      dmax[lf] = warp_max(dmax[lf]);
     }
-    dmin = -warp_max(-dmin);
-    dmax = warp_max(dmax);
     __syncthreads();  // everyone read s.wmin/wmax
-    if (lane == 0) s.wmin[warp] = dmin, s.wmax[warp] = dmax;
+#pragma unroll
+    for (int lf = 0; lf < kLPB; ++lf)
+      if (lane == 0 && lf < nl) s.wmin[lf][warp] = dmin[lf], s.wmax[lf][warp] = dmax[lf];
     __syncthreads();
-    dmin = s.wmin[0], dmax = s.wmax[0];
-    for (int w = 1; w < kW; ++w) dmin = fmin(dmin, s.wmin[w]), dmax = fmax(dmax, s.wmax[w]);
-    bool ok = s.bad == INT_MAX && dmin > 1e-12 * dmax && isfinite(cbar);
-    if (tid == 0 && !srcmode) {
-      a.bad_point[leaf] = s.bad;
-      f.stats[3 * leaf + 0] = dmin;  // spectral analogue of the pivot statistics: min / max |lam_i + lam_j + cbar|
-      f.stats[3 * leaf + 1] = dmax;
-      f.stats[3 * leaf + 2] = -1.0;
+    if (tid < nl) {
+      const int lf = tid;
+      const long long leaf = leaf0 + lf;
+      double dn = s.wmin[lf][0], dx = s.wmax[lf][0];
+      for (int w = 1; w < kW; ++w) dn = fmin(dn, s.wmin[lf][w]), dx = fmax(dx, s.wmax[lf][w]);
+      // a negative dn marks a non-finite cbar (fmin keeps it negative)
+      const bool ok = s.bad[lf] == INT_MAX && dn > 1e-12 * dx && dn >= 0.0;
+      if (!srcmode) {
+        a.bad_point[leaf] = s.bad[lf];
+        f.stats[3 * leaf + 0] = dn;  // spectral analogue of the pivot statistics: min / max |lam_i + lam_j + cbar|
+        f.stats[3 * leaf + 1] = dx;
+        f.stats[3 * leaf + 2] = -1.0;
+      }
+      // non-finite samples (reported by the host) or a resonant leaf: the LU path takes over
+      if (!ok && s.bad[lf] == INT_MAX) f.fail_list[atomicAdd(f.fail_count, 1)] = int(leaf);
+      s.ok[lf] = ok;
     }
-    if (!ok) {  // non-finite samples (reported by the host) or a resonant leaf: the LU path takes over
-      if (tid == 0 && s.bad == INT_MAX) f.fail_list[atomicAdd(f.fail_count, 1)] = int(leaf);
-      __syncthreads();
-      continue;
-    }
-    if (tid == 0) s.failed = 0;
+    __syncthreads();
 
-    // ---- per warp: its columns c = warp + 1, warp + 1 + kW, ... (mod ncol; column 0, the source, goes to the last
-    // warp), each solved, written and contracted to [h | T] without CTA barriers
+    // ---- per warp: the iteration's columns t = warp + 1, warp + 1 + kW, ... over the leaves in turn (within a
+    // leaf, column 0, the source, comes last), each solved, written and contracted to [h | T] without CTA barriers
     {
       double* Rb = s.R + warp * kBlk;
       double* Xb = s.X + warp * kBlk;
       double* Wb = s.W + warp * kBlk;
-      bool conv = true;
-      int npass = 0, nout = 0;
-      for (int c = warp + 1; c < ncol + 1; c += kW) {
+      for (int t = warp + 1; t <= nl * ncol; t += kW) {
+        const int lf = (t - 1) / ncol, c = (t - 1) - lf * ncol + 1;
+        if (!s.ok[lf]) continue;
+        const long long leaf = leaf0 + lf;
         const int col = c == ncol ? 0 : c;
+        int npass = 0, nout = 0;
         // right-hand side: the source column(s) (formed here); then -L_ie P (-L_ie in the ItI mode), the same for
         // every leaf (constant Laplacian): R and R^ = V^-1 R V^-T from the prep tables (L2-resident)
         if (col >= nsrc) {
@@ -350,24 +380,21 @@ __global__ void __launch_bounds__(kT, HPS_FDM_MINB) leaf_fdm_kernel(const LeafFd
         } else {
           for (int e = lane; e < kBlk; e += 32) {
             const int cc = e >> 4, row = (e & 15) ^ swx(cc);
-            Rb[e] = (row < N1 && cc < N1) ? a.fsign * s.fsrc[col][(cc + 1) * P + row + 1] : 0.0;
+            Rb[e] = (row < N1 && cc < N1) ? a.fsign * s.fsrc[lf][col][(cc + 1) * P + row + 1] : 0.0;
           }
         }
         __syncwarp();
-        conv = solve_block(Rb, Xb, Wb, s, vi, vv, aa, g, t4, npass, !srcmode && col >= nsrc) && conv;
+        const bool conv = solve_block(Rb, Xb, Wb, s.cz[lf], s.den[lf], vi, vv, aa, g, t4, npass, !srcmode && col >= nsrc);
+        if (!conv && lane == 0) s.failed[lf] = 1;
         // [v_i | Y_i] column (interior index r = (i1-1) N1 + (i2-1)); ItI mode: the column of Z
         double* Yv = f.Yv + leaf * f.strideYv + (long long)col * NI;
 #pragma unroll
         for (int r = lane; r < NI; r += 32) __stcs(&Yv[r], Xb[swz(r % N1, r / N1)]);
-        if (f.iti || srcmode) {
-          __syncwarp();
-          continue;
-        }
-        // [h | T] = Q_i X + [0 | Q_e P] through the separable Q_i (geometry.cpp q_interior_factors), on DMMA:
-        // U = Dm X (rows S, N: u_s(m) = sum_k d_s(k) X(k, m)) and Dm X^T (rows E, W), then H = G U^T, h = ds H.
-        // Block element (row, col) = X(i1 = col + 1, i2 = row + 1).  U goes to Rb (free after the solve) as a
-        // B operand: element (m, side) at swz(m, side); rows 4..7 of Dm are zero, so are those sides.
-        {
+        if (!(f.iti || srcmode)) {
+          // [h | T] = Q_i X + [0 | Q_e P] through the separable Q_i (geometry.cpp q_interior_factors), on DMMA:
+          // U = Dm X (rows S, N: u_s(m) = sum_k d_s(k) X(k, m)) and Dm X^T (rows E, W), then H = G U^T, h = ds H.
+          // Block element (row, col) = X(i1 = col + 1, i2 = row + 1).  U goes to Rb (free after the solve) as a
+          // B operand: element (m, side) at swz(m, side); rows 4..7 of Dm are zero, so are those sides.
           double ad[4];
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) ad[ks] = s.qDm[(ks * 4 + t4) * 16 + g];
@@ -407,16 +434,16 @@ __global__ void __launch_bounds__(kT, HPS_FDM_MINB) leaf_fdm_kernel(const LeafFd
                 if (i < N1) __stcs(&HT[row], f.qds * hh[mt][h] + __ldg(zq + row));
               }
           nout += 24;  // DMMA: two 8-row passes and one 8-column pass
-          __syncwarp();
         }
+        __syncwarp();
+        if (lane == 0 && npass) atomicAdd(&s.ndmma[lf], 16 * npass + nout);
       }
-      if (!conv && lane == 0) s.failed = 1;
-      if (lane == 0 && npass) atomicAdd(&s.ndmma, 16 * npass + nout);
     }
     __syncthreads();
-    if (tid == 0) {
-      if (s.failed) f.fail_list[atomicAdd(f.fail_count, 1)] = int(leaf);
-      if (!srcmode) f.stats[3 * leaf + 2] = -1.0 - double(s.ndmma);  // < 0: no zero pivot; the LU fallback rewrites it
+    if (tid < nl && s.ok[tid]) {
+      const long long leaf = leaf0 + tid;
+      if (s.failed[tid]) f.fail_list[atomicAdd(f.fail_count, 1)] = int(leaf);
+      if (!srcmode) f.stats[3 * leaf + 2] = -1.0 - double(s.ndmma[tid]);  // < 0: no zero pivot; the LU fallback rewrites it
     }
   }
 }
