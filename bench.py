@@ -46,7 +46,7 @@ PAPER_H100_DOFS = 16777216 / 4.02
 FP64_PEAK_TFLOPS = 37.155     # DMMA microbench: profiles/r01_fp64_peak.json 37.155, re-measured with SM clocks at 1965 MHz in profiles/r02_fp64_peak.json 37.148 (MEASURED_PEAKS.json has no FP64 entry)
 # dram__bytes_read.sum + dram__bytes_write.sum of one leaf-stage launch at p=16 L=8, per leaf kernel
 # (ncu --set full of the current kernels, profiles/r02_ncu_summary.md)
-LEAF_KERNEL_DRAM_BYTES = {"leaf_fused_kernel": 18.89e9 + 69.29e9, "leaf_fdm_kernel": 4.663e9 + 7.480e9}
+LEAF_KERNEL_DRAM_BYTES = {"leaf_fused_kernel": 18.89e9 + 69.29e9, "leaf_fdm_kernel": 5.675e9 + 7.492e9}
 
 
 def leaf_roofline(kernel, n_leaves, ref_flops, t_leaf_ms, exec_flops, traffic):
