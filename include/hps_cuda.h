@@ -277,7 +277,9 @@ int hpsg_get_leaf(hpsg_ctx* ctx, int ord, double* Y, double* v, double* T, doubl
 /* MergeArtifact sizes of an internal node (merge.hpp:58-64) */
 int hpsg_node_sizes(hpsg_ctx* ctx, int node_id, int* n_ext, int* n_int);
 /* MergeArtifact S_mat (n_int x n_ext), gtilde (n_int) and node_T/node_h (n_ext^2, n_ext) of a
- * non-root internal node (solver.hpp:83-85).  Any pointer may be NULL. */
+ * non-root internal node (solver.hpp:83-85).  Any pointer may be NULL.  The build leaves the rows of T/h on the
+ * domain boundary unformed where nothing downstream reads them (a root that forms no T); the first request for
+ * T or h forms them (GPU work on the context's stream), with the values an unskipped build stores. */
 int hpsg_get_node(hpsg_ctx* ctx, int node_id, double* S, double* gtilde, double* T, double* h);
 int hpsg_get_stats(hpsg_ctx* ctx, hpsg_stats* out);
 /* run all later work of ctx on a caller-owned cudaStream_t (passed as void*; NULL = legacy
