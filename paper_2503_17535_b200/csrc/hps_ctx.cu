@@ -62,8 +62,12 @@ void gemm(hpsg_ctx* c, const GemmArgs& g) {
 
 int lu_launches(int n, int m, bool factor) { return hpsk::lu_launch_count(n, m, factor); }
 
-// block-sparse Schur products from this face size up (below it one dense GEMM launch is cheaper)
-constexpr int kSparseSchurMinS = 32;
+// block-sparse Schur products from this face size up (below it one dense GEMM launch is cheaper; with the
+// boundary-row skip, 16 and 8 measured 175.9 -> 176.6 / 178.6 ms at L=8)
+#ifndef HPS_SPARSE_SCHUR_MIN_S
+#define HPS_SPARSE_SCHUR_MIN_S 32
+#endif
+constexpr int kSparseSchurMinS = HPS_SPARSE_SCHUR_MIN_S;
 void plan_boundary_rows(hpsg_ctx* c, Level& L, cudaStream_t st);
 
 // Solve-time products: a streaming GEMV for up to 4 right-hand sides (HBM-bound), the DMMA
