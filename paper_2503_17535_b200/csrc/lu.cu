@@ -1178,7 +1178,10 @@ cudaError_t lu_stats_init(double* stats, int batch, cudaStream_t st) {
 
 // look-ahead (panels of the next outer block on a high-priority side stream) from this n up; measured at
 // L=8: d0 -1.7 ms, d1 -3 ms, d2 -1 ms (256 and 512 measured equal as the threshold)
-constexpr int kLookaheadMinN = 2 * kOuterNB;
+#ifndef HPS_LOOKAHEAD_MIN_N
+#define HPS_LOOKAHEAD_MIN_N (2 * kOuterNB)
+#endif
+constexpr int kLookaheadMinN = HPS_LOOKAHEAD_MIN_N;
 
 cudaError_t bgetrf_aug(int batch, int n, int m, BatchedMat M, int* ipiv, double* stats, LuWorkspace& ws,
                        cudaStream_t st, bool keep_L) {
