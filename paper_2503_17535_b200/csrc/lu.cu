@@ -364,7 +364,10 @@ struct SwapTrsmArgs {
   Seg seg[3];
 };
 
-constexpr int kColThreads = 128;
+#ifndef HPS_COL_THREADS
+#define HPS_COL_THREADS 128
+#endif
+constexpr int kColThreads = HPS_COL_THREADS;
 
 // Row swaps of one panel applied to column segments, then U12 = L11^-1 A12
 // (proj/src/local_solve.cpp:128 / merge.cpp:291: the forward half of the solve).
